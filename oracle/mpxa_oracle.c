@@ -1,0 +1,569 @@
+/*
+ * mpxa CPU oracle -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+ * leg may load or call this file.  The product path (paper_2309_07337_b200/) never
+ * links, imports or executes it, and it shares no code with the product: no headers,
+ * helpers, tables or generators.  Inputs come from the seeded generator module synth/.
+ *
+ * What it is: a plain, slow, single-threaded simulation of p MPI ranks exchanging
+ * messages through an in-process transport with one FIFO per (src, dst) link and
+ * message/byte counters ("transport").  Sends are
+ * eager (buffered), so "every rank sends, then every rank receives" is a legal
+ * execution of each round.  Every payload byte is moved with memcpy; nothing is
+ * blocked, fused or reordered beyond what the algorithm states.
+ *
+ * Paper passages followed (PAPER.md = arXiv 2309.07337 LaTeX):
+ *   - MPI_Alltoallv / MPIX_Alltoallv semantics, Listings 1-2, PAPER.md:104-118 (§2.1).
+ *   - "minimize message count for small data sizes and bytes transported for larger
+ *     messages" (Bruck vs pairwise) and "distinguishing between inter- and intra- node
+ *     communication, reducing message count" (hierarchical), PAPER.md:98 (§2.1).
+ *   - The paper gives no algorithm steps; the step lists are the ones BASELINE.json's
+ *     north_star names ("local rotation, bit-indexed block send/recv, final inverse
+ *     rotation"; "gather blocks within a group, exchange once between groups,
+ *     redistribute") as read in SURVEY.md §8(c) C.4, items 1-7, and DESIGN.md §3.
+ *
+ * Pinning: tests/test_oracle_pins.py checks every function against numpy transposes /
+ * concatenations, brute force with unique byte labels, closed-form message counts and
+ * the Bruck per-round invariants.  No function here is "parity unpinned".
+ *
+ * Layout conventions (all buffers host memory, caller-owned):
+ *   alltoall : send is p rows of p*blk bytes (row r = rank r, block j -> rank j),
+ *              recv likewise (block j of row r came from rank j).
+ *   allgather: send is p rows of blk bytes; recv is p rows of p*blk bytes.
+ *   alltoallv: send rows of sstride bytes, recv rows of rstride bytes; counts and
+ *              displacements are p*p int64 arrays in ELEMENTS of w bytes,
+ *              sc[r*p+j] = sendcounts of rank r for destination j, rc[r*p+j] =
+ *              recvcounts of rank r from source j (MPI semantics).
+ * Return value: 0 on success, -1 on bad arguments, -2 on internal inconsistency
+ * (a receive that found no matching message, which would be a deadlock in MPI).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------------------ */
+/* Statistics (SPEC.md:37-42 TransportStats; loopback messages are counted) */
+typedef struct {
+    int64_t ppn;          /* input: ranks per node for the intra/inter split (0 -> p)   */
+    int64_t msgs;         /* total messages, including loopback                          */
+    int64_t bytes;        /* total payload bytes                                          */
+    int64_t intra_msgs, inter_msgs;
+    int64_t intra_bytes, inter_bytes;
+    int64_t max_msgs_per_rank;  /* max over ranks of messages sent                       */
+    int64_t rounds;       /* communication rounds of the schedule                         */
+} orc_stats;
+
+/* ------------------------------------------------------------------------------------ */
+/* Transport: one FIFO per (src, dst) link; matching on (src, dst, tag) in FIFO order.   */
+typedef struct msg_s {
+    int tag;
+    size_t len;
+    unsigned char *data;
+    struct msg_s *next;
+} msg_t;
+
+typedef struct {
+    int p;
+    msg_t **head;   /* p*p FIFOs, index src*p+dst */
+    msg_t **tail;
+    int64_t *sent;  /* per-rank messages sent */
+    orc_stats *st;
+    int ppn;
+} transport_t;
+
+static int tp_init(transport_t *t, int p, orc_stats *st) {
+    t->p = p;
+    t->head = (msg_t **)calloc((size_t)p * p, sizeof(msg_t *));
+    t->tail = (msg_t **)calloc((size_t)p * p, sizeof(msg_t *));
+    t->sent = (int64_t *)calloc((size_t)p, sizeof(int64_t));
+    t->st = st;
+    t->ppn = (st && st->ppn > 0) ? (int)st->ppn : p;
+    if (st) {
+        int64_t keep = st->ppn;
+        memset(st, 0, sizeof(*st));
+        st->ppn = keep;
+    }
+    return (t->head && t->tail && t->sent) ? 0 : -1;
+}
+
+static int tp_pending(const transport_t *t) {
+    for (int i = 0; i < t->p * t->p; i++)
+        if (t->head[i]) return 1;
+    return 0;
+}
+
+static void tp_free(transport_t *t) {
+    for (int i = 0; i < t->p * t->p; i++) {
+        msg_t *m = t->head[i];
+        while (m) { msg_t *n = m->next; free(m->data); free(m); m = n; }
+    }
+    if (t->st) {
+        int64_t mx = 0;
+        for (int r = 0; r < t->p; r++) if (t->sent[r] > mx) mx = t->sent[r];
+        t->st->max_msgs_per_rank = mx;
+    }
+    free(t->head); free(t->tail); free(t->sent);
+}
+
+/* eager send: the payload is copied into the envelope */
+static int tp_send(transport_t *t, int src, int dst, int tag, const void *buf, size_t len) {
+    msg_t *m = (msg_t *)malloc(sizeof(msg_t));
+    if (!m) return -1;
+    m->tag = tag; m->len = len; m->next = NULL;
+    m->data = (unsigned char *)malloc(len ? len : 1);
+    if (!m->data) { free(m); return -1; }
+    if (len) memcpy(m->data, buf, len);
+    int link = src * t->p + dst;
+    if (t->tail[link]) t->tail[link]->next = m; else t->head[link] = m;
+    t->tail[link] = m;
+    t->sent[src]++;
+    if (t->st) {
+        int same = (src / t->ppn) == (dst / t->ppn);
+        t->st->msgs++; t->st->bytes += (int64_t)len;
+        if (same) { t->st->intra_msgs++; t->st->intra_bytes += (int64_t)len; }
+        else      { t->st->inter_msgs++; t->st->inter_bytes += (int64_t)len; }
+    }
+    return 0;
+}
+
+/* blocking receive of the first message on link (src -> dst) with this tag.
+ * Returns the payload length, or -1 if no such message exists (deadlock in MPI terms). */
+static int64_t tp_recv(transport_t *t, int dst, int src, int tag, void *buf, size_t cap) {
+    int link = src * t->p + dst;
+    msg_t *prev = NULL, *m = t->head[link];
+    while (m && m->tag != tag) { prev = m; m = m->next; }
+    if (!m || m->len > cap) return -1;
+    if (m->len) memcpy(buf, m->data, m->len);
+    if (prev) prev->next = m->next; else t->head[link] = m->next;
+    if (t->tail[link] == m) t->tail[link] = prev;
+    int64_t n = (int64_t)m->len;
+    free(m->data); free(m);
+    return n;
+}
+
+static int imod(int64_t a, int p) { int64_t r = a % p; return (int)(r < 0 ? r + p : r); }
+static int ceil_log2(int p) { int k = 0; while ((1 << k) < p) k++; return k; }
+
+/* ==================================================================================== */
+/* C.3 Definitions -- the result every variant must reach.                              */
+/* ==================================================================================== */
+
+/* alltoall identity recv_r[j] = send_j[r] (BASELINE.json north_star; MPI_Alltoall). */
+int orc_alltoall_definition(int p, size_t blk, const unsigned char *send, unsigned char *recv) {
+    if (p < 1) return -1;
+    for (int r = 0; r < p; r++)
+        for (int j = 0; j < p; j++)
+            if (blk) memcpy(recv + ((size_t)r * p + j) * blk, send + ((size_t)j * p + r) * blk, blk);
+    return 0;
+}
+
+/* allgather: recv_r[j] = send_j for all r (concatenation in rank order). */
+int orc_allgather_definition(int p, size_t blk, const unsigned char *send, unsigned char *recv) {
+    if (p < 1) return -1;
+    for (int r = 0; r < p; r++)
+        for (int j = 0; j < p; j++)
+            if (blk) memcpy(recv + ((size_t)r * p + j) * blk, send + (size_t)j * blk, blk);
+    return 0;
+}
+
+/* Checks of the MPI alltoallv argument contract: non-negative counts,
+ * in-bounds regions, sendcounts_j[r] == recvcounts_r[j]. */
+static int v_args_ok(int p, size_t w, size_t sstride, const int64_t *sc, const int64_t *sd,
+                     size_t rstride, const int64_t *rc, const int64_t *rd) {
+    if (p < 1 || w < 1) return 0;
+    for (int r = 0; r < p; r++)
+        for (int j = 0; j < p; j++) {
+            int64_t a = sc[r * p + j], b = sd[r * p + j], c = rc[r * p + j], d = rd[r * p + j];
+            if (a < 0 || b < 0 || c < 0 || d < 0) return 0;
+            if ((uint64_t)(b + a) * w > sstride) return 0;
+            if ((uint64_t)(d + c) * w > rstride) return 0;
+            if (sc[r * p + j] != rc[j * p + r]) return 0;
+        }
+    return 1;
+}
+
+/* alltoallv: recv_r[rd_r[j]*w, +rc_r[j]*w) = send_j[sd_j[r]*w, +sc_j[r]*w); all other bytes
+ * of recv_r unchanged. */
+int orc_alltoallv_definition(int p, size_t w, const unsigned char *send, size_t sstride,
+                             const int64_t *sc, const int64_t *sd, unsigned char *recv,
+                             size_t rstride, const int64_t *rc, const int64_t *rd) {
+    if (!v_args_ok(p, w, sstride, sc, sd, rstride, rc, rd)) return -1;
+    for (int r = 0; r < p; r++)
+        for (int j = 0; j < p; j++) {
+            size_t n = (size_t)rc[r * p + j] * w;
+            if (n) memcpy(recv + (size_t)r * rstride + (size_t)rd[r * p + j] * w,
+                          send + (size_t)j * sstride + (size_t)sd[j * p + r] * w, n);
+        }
+    return 0;
+}
+
+/* ==================================================================================== */
+/* C.4 Variant simulations through the transport                                        */
+/* ==================================================================================== */
+
+/* C.4 item 1 -- pairwise alltoallv: for s = 0..p-1 every rank r sends its
+ * segment for dst = (r+s) mod p and receives from src = (r-s) mod p; s = 0 is the
+ * self-exchange (a loopback message).  p messages per rank, p^2 in total. */
+int orc_alltoallv_pairwise(int p, size_t w, const unsigned char *send, size_t sstride,
+                           const int64_t *sc, const int64_t *sd, unsigned char *recv,
+                           size_t rstride, const int64_t *rc, const int64_t *rd, orc_stats *st) {
+    if (!v_args_ok(p, w, sstride, sc, sd, rstride, rc, rd)) return -1;
+    transport_t t;
+    if (tp_init(&t, p, st)) return -1;
+    int err = 0;
+    for (int s = 0; s < p && !err; s++) {
+        for (int r = 0; r < p && !err; r++) {
+            int dst = imod(r + s, p);
+            err = tp_send(&t, r, dst, s, send + (size_t)r * sstride + (size_t)sd[r * p + dst] * w,
+                          (size_t)sc[r * p + dst] * w);
+        }
+        for (int r = 0; r < p && !err; r++) {
+            int src = imod(r - s, p);
+            int64_t n = tp_recv(&t, r, src, s, recv + (size_t)r * rstride + (size_t)rd[r * p + src] * w,
+                                (size_t)rc[r * p + src] * w);
+            if (n != rc[r * p + src] * (int64_t)w) err = -2;
+        }
+        if (st) st->rounds++;
+    }
+    if (!err && tp_pending(&t)) err = -2;
+    tp_free(&t);
+    return err;
+}
+
+/* pairwise alltoall = pairwise alltoallv with every count = blk bytes, packed displs. */
+int orc_alltoall_pairwise(int p, size_t blk, const unsigned char *send, unsigned char *recv,
+                          orc_stats *st) {
+    if (p < 1) return -1;
+    int64_t *c = (int64_t *)malloc(sizeof(int64_t) * p * p);
+    int64_t *d = (int64_t *)malloc(sizeof(int64_t) * p * p);
+    for (int r = 0; r < p; r++)
+        for (int j = 0; j < p; j++) { c[r * p + j] = (int64_t)blk; d[r * p + j] = (int64_t)blk * j; }
+    int rc = orc_alltoallv_pairwise(p, 1, send, (size_t)p * blk, c, d, recv, (size_t)p * blk, c, d, st);
+    free(c); free(d);
+    return rc;
+}
+
+/* C.4 item 2 -- Bruck alltoall (BASELINE.json north_star: "local rotation, bit-indexed
+ * block send/recv, final inverse rotation"; SURVEY.md Q1-Q3 conventions):
+ *   R1  T_r[i] = send_r[(r+i) mod p]                                   (local rotation)
+ *   R2  for k = 0..K-1, d = 2^k: rank r sends {T_r[i] : bit k of i is 1}, in increasing i,
+ *       as ONE message to (r+d) mod p; the receiver stores the j-th received block at
+ *       T[i_j] (same index set), i.e. it keeps the sender's pre-round values.
+ *   R3  recv_r[j] = T_r[(r-j) mod p]                                   (inverse rotation)
+ * stop_stage: -1 runs everything; 0 stops after R1; k+1 stops after round k.  When
+ * T_out != NULL, T (p rows of p*blk) is copied there at the stop point (or at the end,
+ * before R3, for stop_stage = -1). */
+int orc_alltoall_bruck(int p, size_t blk, const unsigned char *send, unsigned char *recv,
+                       int stop_stage, unsigned char *T_out, orc_stats *st) {
+    if (p < 1) return -1;
+    size_t row = (size_t)p * blk;
+    unsigned char *T = (unsigned char *)malloc(row * p + 1);
+    unsigned char *pack = (unsigned char *)malloc(row + 1);
+    if (!T || !pack) { free(T); free(pack); return -1; }
+    transport_t t;
+    if (tp_init(&t, p, st)) { free(T); free(pack); return -1; }
+    int err = 0;
+    /* R1 */
+    for (int r = 0; r < p; r++)
+        for (int i = 0; i < p; i++)
+            if (blk) memcpy(T + r * row + (size_t)i * blk, send + r * row + (size_t)imod(r + i, p) * blk, blk);
+    int K = ceil_log2(p);
+    int done = (stop_stage == 0);
+    for (int k = 0; k < K && !done && !err; k++) {
+        int d = 1 << k;
+        for (int r = 0; r < p && !err; r++) {      /* every rank packs and sends */
+            size_t n = 0;
+            for (int i = 0; i < p; i++)
+                if ((i >> k) & 1) { if (blk) memcpy(pack + n, T + r * row + (size_t)i * blk, blk); n += blk; }
+            err = tp_send(&t, r, imod(r + d, p), k, pack, n);
+        }
+        for (int r = 0; r < p && !err; r++) {      /* every rank receives and unpacks */
+            int src = imod(r - d, p);
+            int64_t n = tp_recv(&t, r, src, k, pack, row);
+            size_t o = 0;
+            for (int i = 0; i < p; i++)
+                if ((i >> k) & 1) { if (blk) memcpy(T + r * row + (size_t)i * blk, pack + o, blk); o += blk; }
+            if (n != (int64_t)o) err = -2;
+        }
+        if (st) st->rounds++;
+        if (stop_stage == k + 1) done = 1;
+    }
+    if (!err && T_out) memcpy(T_out, T, row * p);
+    if (!err && !done)                               /* R3 */
+        for (int r = 0; r < p; r++)
+            for (int j = 0; j < p; j++)
+                if (blk) memcpy(recv + r * row + (size_t)j * blk, T + r * row + (size_t)imod(r - j, p) * blk, blk);
+    if (!err && tp_pending(&t)) err = -2;
+    tp_free(&t);
+    free(T); free(pack);
+    return err;
+}
+
+/* C.4 item 3 -- Bruck allgather: T_r[0] = send_r; for k = 0..K-1,
+ * d = 2^k, n_k = min(d, p-d): rank r sends T_r[0..n_k) to (r-d) mod p, which stores them
+ * at T[d..d+n_k); finally recv_r[j] = T_r[(j-r) mod p].  stop_stage as for alltoall
+ * (0 = after T_r[0] = send_r). */
+int orc_allgather_bruck(int p, size_t blk, const unsigned char *send, unsigned char *recv,
+                        int stop_stage, unsigned char *T_out, orc_stats *st) {
+    if (p < 1) return -1;
+    size_t row = (size_t)p * blk;
+    unsigned char *T = (unsigned char *)calloc(row * p + 1, 1);
+    if (!T) return -1;
+    transport_t t;
+    if (tp_init(&t, p, st)) { free(T); return -1; }
+    int err = 0;
+    for (int r = 0; r < p; r++) if (blk) memcpy(T + r * row, send + (size_t)r * blk, blk);
+    int K = ceil_log2(p);
+    int done = (stop_stage == 0);
+    for (int k = 0; k < K && !done && !err; k++) {
+        int d = 1 << k, nk = d < p - d ? d : p - d;
+        for (int r = 0; r < p && !err; r++)
+            err = tp_send(&t, r, imod(r - d, p), k, T + r * row, (size_t)nk * blk);
+        for (int r = 0; r < p && !err; r++) {
+            int64_t n = tp_recv(&t, r, imod(r + d, p), k, T + r * row + (size_t)d * blk, (size_t)nk * blk);
+            if (n != (int64_t)((size_t)nk * blk)) err = -2;
+        }
+        if (st) st->rounds++;
+        if (stop_stage == k + 1) done = 1;
+    }
+    if (!err && T_out) memcpy(T_out, T, row * p);
+    if (!err && !done)
+        for (int r = 0; r < p; r++)
+            for (int j = 0; j < p; j++)
+                if (blk) memcpy(recv + r * row + (size_t)j * blk, T + r * row + (size_t)imod(j - r, p) * blk, blk);
+    if (!err && tp_pending(&t)) err = -2;
+    tp_free(&t);
+    free(T);
+    return err;
+}
+
+/* C.4 item 4 -- ring allgather: recv_r[r] = send_r; for s = 0..p-2, rank r
+ * sends block (r-s) mod p to (r+1) mod p, which stores it at index (r-s) mod p. */
+int orc_allgather_ring(int p, size_t blk, const unsigned char *send, unsigned char *recv,
+                       orc_stats *st) {
+    if (p < 1) return -1;
+    size_t row = (size_t)p * blk;
+    transport_t t;
+    if (tp_init(&t, p, st)) return -1;
+    int err = 0;
+    for (int r = 0; r < p; r++) if (blk) memcpy(recv + r * row + (size_t)r * blk, send + (size_t)r * blk, blk);
+    for (int s = 0; s < p - 1 && !err; s++) {
+        for (int r = 0; r < p && !err; r++) {
+            int b = imod(r - s, p);
+            err = tp_send(&t, r, imod(r + 1, p), s, recv + r * row + (size_t)b * blk, blk);
+        }
+        for (int r = 0; r < p && !err; r++) {
+            int src = imod(r - 1, p), b = imod(src - s, p);
+            int64_t n = tp_recv(&t, r, src, s, recv + r * row + (size_t)b * blk, blk);
+            if (n != (int64_t)blk) err = -2;
+        }
+        if (st) st->rounds++;
+    }
+    if (!err && tp_pending(&t)) err = -2;
+    tp_free(&t);
+    return err;
+}
+
+/* C.4 item 5 -- direct ("pairwise") allgather: r sends send_r to every j != r, and
+ * copies it locally into recv_r[r]. */
+int orc_allgather_direct(int p, size_t blk, const unsigned char *send, unsigned char *recv,
+                         orc_stats *st) {
+    if (p < 1) return -1;
+    size_t row = (size_t)p * blk;
+    transport_t t;
+    if (tp_init(&t, p, st)) return -1;
+    int err = 0;
+    for (int r = 0; r < p; r++) if (blk) memcpy(recv + r * row + (size_t)r * blk, send + (size_t)r * blk, blk);
+    for (int s = 1; s < p && !err; s++)
+        for (int r = 0; r < p && !err; r++)
+            err = tp_send(&t, r, imod(r + s, p), 0, send + (size_t)r * blk, blk);
+    for (int s = 1; s < p && !err; s++)
+        for (int r = 0; r < p && !err; r++) {
+            int src = imod(r - s, p);
+            int64_t n = tp_recv(&t, r, src, 0, recv + r * row + (size_t)src * blk, blk);
+            if (n != (int64_t)blk) err = -2;
+        }
+    if (st) st->rounds = p > 1 ? 1 : 0;
+    if (!err && tp_pending(&t)) err = -2;
+    tp_free(&t);
+    return err;
+}
+
+/* C.4 item 6 -- locality-aware hierarchical alltoallv ("distinguishing between
+ * inter- and intra- node communication, reducing message count"; SPEC.md:158-166, 220;
+ * BASELINE.json north_star "gather blocks within a group, exchange once between groups,
+ * redistribute").  Groups are contiguous of size g; group of r is A = r/g;
+ * leader L(A,B) = A*g + (B mod g).
+ *   Step 1: every rank r in A, for every remote group B, sends ONE message to L(A,B) with
+ *           its g segments (r -> B*g+t), t = 0..g-1, concatenated in t order.
+ *   Step 2: L(A,B) sends L(B,A) ONE aggregated message with segments ordered (s,t)
+ *           row-major (s = source local index in A, t = destination local index in B);
+ *           empty group pairs send no message.
+ *   Step 3: L(B,A) sends each rank B*g+t ONE message with its g segments (s = 0..g-1);
+ *           the rank stores segment s at rdispls[A*g+s].
+ *   Intra-group pairs (B = A) are exchanged directly.
+ * The aggregated layout is fixed by the count matrix (no in-band headers).
+ * st->ppn should be set to g by the caller to count inter-group messages. */
+int orc_alltoallv_hier(int p, int g, size_t w, const unsigned char *send, size_t sstride,
+                       const int64_t *sc, const int64_t *sd, unsigned char *recv, size_t rstride,
+                       const int64_t *rc, const int64_t *rd, orc_stats *st) {
+    if (g < 1 || p % g) return -1;
+    if (!v_args_ok(p, w, sstride, sc, sd, rstride, rc, rd)) return -1;
+    int G = p / g;
+    transport_t t;
+    if (tp_init(&t, p, st)) return -1;
+    int err = 0;
+    size_t cap = 0;   /* largest message any step can carry */
+    for (int a = 0; a < p; a++)
+        for (int b = 0; b < p; b++) cap += (size_t)sc[a * p + b] * w;
+    unsigned char *buf = (unsigned char *)malloc(cap + 1);
+    unsigned char *agg = (unsigned char *)malloc(cap + 1);
+    if (!buf || !agg) { free(buf); free(agg); tp_free(&t); return -1; }
+    enum { TAG_DIRECT = 1, TAG_GATHER = 2, TAG_EXCH = 3, TAG_SCATTER = 4 };
+
+    /* intra-group direct exchange */
+    for (int r = 0; r < p && !err; r++) {
+        int A = r / g;
+        for (int u = 0; u < g && !err; u++) {
+            int j = A * g + u;
+            err = tp_send(&t, r, j, TAG_DIRECT, send + (size_t)r * sstride + (size_t)sd[r * p + j] * w,
+                          (size_t)sc[r * p + j] * w);
+        }
+    }
+    for (int r = 0; r < p && !err; r++) {
+        int A = r / g;
+        for (int u = 0; u < g && !err; u++) {
+            int j = A * g + u;
+            int64_t n = tp_recv(&t, r, j, TAG_DIRECT, recv + (size_t)r * rstride + (size_t)rd[r * p + j] * w,
+                                (size_t)rc[r * p + j] * w);
+            if (n != rc[r * p + j] * (int64_t)w) err = -2;
+        }
+    }
+    /* Step 1: gather to L(A,B) */
+    for (int r = 0; r < p && !err; r++) {
+        int A = r / g;
+        for (int B = 0; B < G && !err; B++) {
+            if (B == A) continue;
+            size_t n = 0;
+            for (int u = 0; u < g; u++) {
+                int j = B * g + u;
+                size_t len = (size_t)sc[r * p + j] * w;
+                if (len) memcpy(buf + n, send + (size_t)r * sstride + (size_t)sd[r * p + j] * w, len);
+                n += len;
+            }
+            err = tp_send(&t, r, A * g + (B % g), TAG_GATHER + 8 * B, buf, n);
+        }
+    }
+    if (st && G > 1) st->rounds++;
+    /* Step 2: each leader L(A,B) receives the g gathered messages, lays them out (s,t)
+     * row-major, and sends one aggregated message to L(B,A) */
+    for (int A = 0; A < G && !err; A++)
+        for (int B = 0; B < G && !err; B++) {
+            if (B == A) continue;
+            int lead = A * g + (B % g), peer = B * g + (A % g);
+            size_t n = 0;
+            for (int s = 0; s < g && !err; s++) {
+                int src = A * g + s;
+                size_t want = 0;
+                for (int u = 0; u < g; u++) want += (size_t)sc[src * p + B * g + u] * w;
+                int64_t got = tp_recv(&t, lead, src, TAG_GATHER + 8 * B, agg + n, cap - n);
+                if (got != (int64_t)want) err = -2;
+                n += want;
+            }
+            if (!err && n) err = tp_send(&t, lead, peer, TAG_EXCH + 8 * A, agg, n);
+        }
+    if (st && G > 1) st->rounds++;
+    /* Step 3: L(B,A) receives from L(A,B) and redistributes segment (s,t) to B*g+t */
+    for (int B = 0; B < G && !err; B++)
+        for (int A = 0; A < G && !err; A++) {
+            if (A == B) continue;
+            int lead = B * g + (A % g), peer = A * g + (B % g);
+            size_t total = 0;
+            for (int s = 0; s < g; s++)
+                for (int u = 0; u < g; u++) total += (size_t)sc[(A * g + s) * p + B * g + u] * w;
+            if (total) {
+                int64_t got = tp_recv(&t, lead, peer, TAG_EXCH + 8 * A, agg, cap);
+                if (got != (int64_t)total) { err = -2; break; }
+            }
+            for (int u = 0; u < g && !err; u++) {
+                size_t n = 0;
+                for (int s = 0; s < g; s++) {      /* segment (s,u) offset in (s,t) row-major */
+                    size_t off = 0;
+                    for (int s2 = 0; s2 < g; s2++)
+                        for (int u2 = 0; u2 < g; u2++) {
+                            if (s2 == s && u2 == u) goto found;
+                            off += (size_t)sc[(A * g + s2) * p + B * g + u2] * w;
+                        }
+                found:;
+                    size_t len = (size_t)sc[(A * g + s) * p + B * g + u] * w;
+                    if (len) memcpy(buf + n, agg + off, len);
+                    n += len;
+                }
+                err = tp_send(&t, lead, B * g + u, TAG_SCATTER + 8 * A, buf, n);
+            }
+        }
+    if (st && G > 1) st->rounds++;
+    for (int r = 0; r < p && !err; r++) {
+        int B = r / g, u = r % g;
+        for (int A = 0; A < G && !err; A++) {
+            if (A == B) continue;
+            int lead = B * g + (A % g);
+            size_t want = 0;
+            for (int s = 0; s < g; s++) want += (size_t)rc[r * p + A * g + s] * w;
+            int64_t got = tp_recv(&t, r, lead, TAG_SCATTER + 8 * A, buf, cap);
+            if (got != (int64_t)want) { err = -2; break; }
+            size_t o = 0;
+            for (int s = 0; s < g; s++) {
+                size_t len = (size_t)rc[r * p + A * g + s] * w;
+                if (len) memcpy(recv + (size_t)r * rstride + (size_t)rd[r * p + A * g + s] * w, buf + o, len);
+                o += len;
+            }
+        }
+        (void)u;
+    }
+    if (!err && tp_pending(&t)) err = -2;
+    free(buf); free(agg);
+    tp_free(&t);
+    return err;
+}
+
+/* hierarchical alltoall = hierarchical alltoallv with uniform counts. */
+int orc_alltoall_hier(int p, int g, size_t blk, const unsigned char *send, unsigned char *recv,
+                      orc_stats *st) {
+    if (p < 1) return -1;
+    int64_t *c = (int64_t *)malloc(sizeof(int64_t) * p * p);
+    int64_t *d = (int64_t *)malloc(sizeof(int64_t) * p * p);
+    for (int r = 0; r < p; r++)
+        for (int j = 0; j < p; j++) { c[r * p + j] = (int64_t)blk; d[r * p + j] = (int64_t)blk * j; }
+    int rc = orc_alltoallv_hier(p, g, 1, send, (size_t)p * blk, c, d, recv, (size_t)p * blk, c, d, st);
+    free(c); free(d);
+    return rc;
+}
+
+/* C.4 item 7 -- counts exchange + displacement scan (BASELINE.json cfg4 "counts/displs
+ * exchanged then data"): recvcounts = alltoall of sendcounts (one int64 per pair, sent as
+ * messages through the transport); rdispls_r[j] = sum_{i<j} recvcounts_r[i]. */
+int orc_counts_exchange(int p, const int64_t *sendcounts, int64_t *recvcounts, int64_t *rdispls,
+                        orc_stats *st) {
+    if (p < 1) return -1;
+    transport_t t;
+    if (tp_init(&t, p, st)) return -1;
+    int err = 0;
+    for (int s = 0; s < p && !err; s++) {
+        for (int r = 0; r < p && !err; r++) {
+            int dst = imod(r + s, p);
+            err = tp_send(&t, r, dst, 0, &sendcounts[r * p + dst], sizeof(int64_t));
+        }
+        for (int r = 0; r < p && !err; r++) {
+            int src = imod(r - s, p);
+            if (tp_recv(&t, r, src, 0, &recvcounts[r * p + src], sizeof(int64_t)) != (int64_t)sizeof(int64_t)) err = -2;
+        }
+    }
+    for (int r = 0; r < p && !err; r++) {
+        int64_t acc = 0;
+        for (int j = 0; j < p; j++) { rdispls[r * p + j] = acc; acc += recvcounts[r * p + j]; }
+    }
+    tp_free(&t);
+    return err;
+}
