@@ -1,0 +1,200 @@
+/*
+ * mpxa.h -- C ABI of the B200-native MPI Advance collectives hot path
+ * (arXiv 2309.07337, "MPI Advance: Open-Source Message Passing Optimizations").
+ *
+ * What the calls compute (the paper adopts MPI semantics: MPIX_Alltoallv is a drop-in
+ * for MPI_Alltoallv, §2.1):
+ *   alltoall : recv_r[j] = send_j[r]                    (personalized exchange)
+ *   alltoallv: recv_r[rdispls_r[j]*w, +recvcounts_r[j]*w) = send_j[sdispls_j[r]*w, +..)
+ *   allgather: recv_r[j] = send_j                        (concatenation in rank order)
+ * in the paper's algorithm families ("minimize message count for small data
+ * sizes and bytes transported for larger messages"; "distinguishing between inter- and
+ * intra- node communication"): pairwise/direct exchange, Bruck's log-step algorithm
+ * (local rotation, bit-indexed block send/recv, inverse rotation), ring, and the
+ * locality-aware hierarchical variant (gather within a group, exchange once between
+ * groups, redistribute).  Every implementation is public and selectable, with a default
+ * ("make all implementations publicly available"); persistent forms follow
+ * the MPI-4 init/start/wait model ("setup costs to be incurred
+ * only once in the initialization method").
+ *
+ * Conventions
+ *  - Every call returns an int status (mpxa_status); the library never aborts or throws
+ *    across the ABI.  All argument errors are detected before any data moves.
+ *  - Ranks: p = nprocs * ranks_per_proc logical ranks; rank r lives on process/GPU
+ *    r / ranks_per_proc (contiguous map).  A process hosting R > 1 ranks
+ *    passes PROCESS-LEVEL buffers laid out rank-major: [R][per-rank buffer].  Per-rank
+ *    strides: alltoall send/recv p*count*w; allgather send count*w, recv p*count*w;
+ *    alltoallv send_bytes_per_rank / recv_bytes_per_rank.  Count/displacement arrays of
+ *    the v-form are R*p int64 (one row of p per local rank), in ELEMENTS of dtype_size.
+ *  - Buffers (sendbuf, recvbuf) are DEVICE pointers on the comm's device.  Payload bytes
+ *    are opaque (no datatype conversion; NaN payloads survive bit-exactly).  sendbuf and
+ *    recvbuf must not overlap (no MPI_IN_PLACE).  Count/displacement arrays are HOST
+ *    pointers unless stated otherwise.
+ *  - Streams: `stream` is a cudaStream_t passed as void*.  Calls are stream-ordered:
+ *    sendbuf must be ready in stream order and recvbuf is valid once the stream passes the
+ *    call (one-shot) or mpxa_wait (persistent).  No call synchronizes the host with the
+ *    device except where documented.
+ *  - Ownership: the caller owns user buffers and streams; the library owns comms,
+ *    requests, its device workspace (symmetric heap), flags and IPC mappings.
+ *  - Collective calls (every process, same order): mpxa_init, mpxa_finalize,
+ *    mpxa_register, every mpxa_alltoall* / mpxa_allgather* call, every *_init,
+ *    mpxa_start and mpxa_request_free.  A ragged call order is erroneous and surfaces as
+ *    MPXA_ERR_TIMEOUT from the device watchdog, not as a hang.
+ *  - Multi-process mode (nprocs > 1): one process per GPU; recvbufs written by peers
+ *    must lie in buffers registered with mpxa_register (or bound by a persistent *_init).
+ */
+#ifndef MPXA_H
+#define MPXA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mpxa_comm_s *mpxa_comm_t;        /* MPIX_Comm analog */
+typedef struct mpxa_request_s *mpxa_request_t;  /* MPIX_Request analog */
+typedef void *mpxa_stream_t;                    /* a cudaStream_t (0 = legacy default)    */
+
+typedef enum {
+    MPXA_SUCCESS = 0,
+    MPXA_ERR_ARG = 1,        /* NULL pointer, overlap, displ+count beyond capacity, negative
+                                count, dtype_size not in {1,2,4,8,16}, bad stage index      */
+    MPXA_ERR_ALGO = 2,       /* unknown / unsupported variant for this op or p */
+    MPXA_ERR_LIFECYCLE = 3,  /* start on ACTIVE, wait on INACTIVE, free while ACTIVE */
+    MPXA_ERR_TOPOLOGY = 4,   /* p not divisible by g, bad rank map / device */
+    MPXA_ERR_MISMATCH = 5,   /* cross-process argument mismatch detected at *_init          */
+    MPXA_ERR_CUDA = 6,       /* a CUDA runtime call failed                                    */
+    MPXA_ERR_TIMEOUT = 7,    /* device watchdog fired; the comm is poisoned                   */
+    MPXA_ERR_NOMEM = 8,      /* device or host allocation failed                              */
+    MPXA_ERR_UNREGISTERED = 9 /* multi-process: recvbuf not in a registered buffer            */
+} mpxa_status;
+
+typedef enum { MPXA_OP_ALLTOALL = 0, MPXA_OP_ALLTOALLV = 1, MPXA_OP_ALLGATHER = 2 } mpxa_op_t;
+
+/* Variant registry.  PAIRWISE is the direct exchange
+ * (for allgather: every rank pushes its block to every rank). */
+typedef enum {
+    MPXA_ALGO_DEFAULT = 0,   /* selector decides (mpxa_get_algorithm)                    */
+    MPXA_ALGO_PAIRWISE = 1,  /* alltoall, alltoallv, allgather                            */
+    MPXA_ALGO_BRUCK = 2,     /* alltoall, allgather                                       */
+    MPXA_ALGO_HIER = 3,      /* alltoall, alltoallv (groups of group_size ranks)          */
+    MPXA_ALGO_RING = 4       /* allgather                                                 */
+} mpxa_algo_t;
+
+/* Bootstrap callback: all-gather `bytes` bytes from every process into out[nprocs*bytes]
+ * (out is ordered by process index).  Returns 0 on success.  Used only by collective
+ * setup calls (init, register, *_init, heap growth), never on the data path. */
+typedef int (*mpxa_allgather_fn)(const void *in, void *out, size_t bytes, void *ctx);
+
+typedef struct {
+    int nprocs;               /* processes (one per GPU)                                     */
+    int proc;                 /* this process's index                                        */
+    int ranks_per_proc;       /* R >= 1 logical ranks hosted by this process                 */
+    int device;               /* CUDA device ordinal of this process                         */
+    int group_size;           /* g for MPXA_ALGO_HIER; 0 -> R when R > 1, else 1             */
+    int emulate_gpus;         /* nprocs == 1 only: run the multi-GPU protocol (flags, CTS,
+                                 peer-style stores) over this many virtual GPUs of the one
+                                 device in a cooperative launch; 0 or 1 = off                */
+    mpxa_allgather_fn bootstrap_allgather;  /* required when nprocs > 1                      */
+    void *ctx;                /* passed to bootstrap_allgather                               */
+    size_t heap_bytes;        /* initial device workspace per process (0 = 64 MiB); grows
+                                 collectively on demand                                      */
+    double timeout_s;         /* device watchdog for flag waits (0 = 60 s)                   */
+} mpxa_init_args;
+
+/* ---- communicator (MPIX_Comm_init) ----------------- */
+int mpxa_init(mpxa_comm_t *comm, const mpxa_init_args *args);
+int mpxa_finalize(mpxa_comm_t comm);
+int mpxa_comm_size(mpxa_comm_t comm, int *p);              /* total logical ranks p          */
+int mpxa_comm_rank0(mpxa_comm_t comm, int *first_rank);    /* first rank hosted here         */
+/* Returns MPXA_ERR_TIMEOUT if the device watchdog has fired on this comm (call after the
+ * stream has been synchronized), else MPXA_SUCCESS.  Local. */
+int mpxa_comm_check(mpxa_comm_t comm);
+/* Number of kernels this comm has launched so far (for launch accounting).  Local. */
+int mpxa_launch_count(mpxa_comm_t comm, uint64_t *count);
+
+/* Collective registration of a device buffer for direct peer writes (multi-process mode;
+ * a no-op in single-process mode).  The whole [ptr, ptr+bytes) range must lie in one
+ * cudaMalloc allocation. */
+int mpxa_register(mpxa_comm_t comm, void *ptr, size_t bytes);
+int mpxa_deregister(mpxa_comm_t comm, void *ptr);
+
+/* ---- one-shot collectives (MPI semantics) ---------------------------- */
+/* count elements of dtype_size bytes per destination block. */
+int mpxa_alltoall(const void *sendbuf, size_t count, size_t dtype_size, void *recvbuf,
+                  mpxa_comm_t comm, mpxa_stream_t stream);
+/* count elements of dtype_size bytes contributed by every rank. */
+int mpxa_allgather(const void *sendbuf, size_t count, size_t dtype_size, void *recvbuf,
+                   mpxa_comm_t comm, mpxa_stream_t stream);
+/* R*p int64 counts/displacements (host pointers), in elements. */
+int mpxa_alltoallv(const void *sendbuf, const int64_t *sendcounts, const int64_t *sdispls,
+                   size_t send_bytes_per_rank, void *recvbuf, const int64_t *recvcounts,
+                   const int64_t *rdispls, size_t recv_bytes_per_rank, size_t dtype_size,
+                   mpxa_comm_t comm, mpxa_stream_t stream);
+/* Explicit-variant forms ("users can select a non-default algorithm"). */
+int mpxa_alltoall_algo(const void *sendbuf, size_t count, size_t dtype_size, void *recvbuf,
+                       mpxa_algo_t algo, mpxa_comm_t comm, mpxa_stream_t stream);
+int mpxa_allgather_algo(const void *sendbuf, size_t count, size_t dtype_size, void *recvbuf,
+                        mpxa_algo_t algo, mpxa_comm_t comm, mpxa_stream_t stream);
+int mpxa_alltoallv_algo(const void *sendbuf, const int64_t *sendcounts, const int64_t *sdispls,
+                        size_t send_bytes_per_rank, void *recvbuf, const int64_t *recvcounts,
+                        const int64_t *rdispls, size_t recv_bytes_per_rank, size_t dtype_size,
+                        mpxa_algo_t algo, mpxa_comm_t comm, mpxa_stream_t stream);
+
+/* A2: counts exchange + displacement scan on the device (BASELINE.json cfg4 "counts/displs
+ * exchanged then data").  d_sendcounts: DEVICE R*p int64; outputs DEVICE R*p int64:
+ * d_recvcounts[t*p+j] = sendcounts of rank j for local rank t, d_rdispls = exclusive prefix
+ * sum of each row.  One kernel; stream-ordered, no host synchronization. */
+int mpxa_alltoallv_counts(const int64_t *d_sendcounts, int64_t *d_recvcounts,
+                          int64_t *d_rdispls, mpxa_comm_t comm, mpxa_stream_t stream);
+
+/* ---- Bruck step-level entry points (intermediate states) -------- */
+/* Runs Bruck alltoall (rotation, then rounds 0..stop_stage-1) and writes T (rank-major,
+ * p blocks of count*w per rank) to T_out.  stop_stage = 0 -> T after the local rotation;
+ * stop_stage = k+1 -> after round k; stop_stage = -1 -> complete alltoall into T_out. */
+int mpxa_alltoall_bruck_stage(const void *sendbuf, size_t count, size_t dtype_size,
+                              void *T_out, int stop_stage, mpxa_comm_t comm,
+                              mpxa_stream_t stream);
+/* Same for Bruck allgather: T_r[0] = send_r, round k fills T[2^k, 2^k + n_k). */
+int mpxa_allgather_bruck_stage(const void *sendbuf, size_t count, size_t dtype_size,
+                               void *T_out, int stop_stage, mpxa_comm_t comm,
+                               mpxa_stream_t stream);
+
+/* ---- persistent forms (MPI-4 style) ------------- */
+/* Buffers are bound at init and must stay allocated until mpxa_request_free.  `info` is
+ * opaque and may be NULL. */
+int mpxa_alltoall_init(const void *sendbuf, size_t count, size_t dtype_size, void *recvbuf,
+                       mpxa_algo_t algo, mpxa_comm_t comm, const void *info,
+                       mpxa_request_t *req);
+int mpxa_allgather_init(const void *sendbuf, size_t count, size_t dtype_size, void *recvbuf,
+                        mpxa_algo_t algo, mpxa_comm_t comm, const void *info,
+                        mpxa_request_t *req);
+int mpxa_alltoallv_init(const void *sendbuf, const int64_t *sendcounts, const int64_t *sdispls,
+                        size_t send_bytes_per_rank, void *recvbuf, const int64_t *recvcounts,
+                        const int64_t *rdispls, size_t recv_bytes_per_rank, size_t dtype_size,
+                        mpxa_algo_t algo, mpxa_comm_t comm, const void *info,
+                        mpxa_request_t *req);
+int mpxa_start(mpxa_request_t req, mpxa_stream_t stream);  /* INACTIVE -> ACTIVE; enqueues   */
+int mpxa_wait(mpxa_request_t req, mpxa_stream_t stream);   /* ACTIVE -> INACTIVE; enqueues the
+                                                              device-side completion on
+                                                              `stream` (no host round trip)  */
+int mpxa_request_free(mpxa_request_t *req);
+int mpxa_request_algorithm(mpxa_request_t req, mpxa_algo_t *algo);
+
+/* ---- variant registry and selector --------------------- */
+int mpxa_set_algorithm(mpxa_comm_t comm, mpxa_op_t op, mpxa_algo_t algo); /* DEFAULT = selector */
+int mpxa_get_algorithm(mpxa_comm_t comm, mpxa_op_t op, size_t bytes, mpxa_algo_t *chosen);
+int mpxa_list_algorithms(mpxa_op_t op, mpxa_algo_t *out, int *n);  /* *n in: capacity; out: count */
+/* Load a selector table: lines "op p ranks_per_proc max_bytes algo" (text, '#' comments);
+ * for each (op, p, R) the first line with bytes <= max_bytes wins. */
+int mpxa_load_selector(mpxa_comm_t comm, const char *path);
+
+const char *mpxa_error_string(int status);
+const char *mpxa_algo_name(mpxa_algo_t algo);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPXA_H */

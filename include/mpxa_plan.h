@@ -1,0 +1,55 @@
+/*
+ * mpxa_plan.h -- host-only introspection of the schedules libmpxa compiles (no CUDA calls,
+ * usable on a machine without a GPU).  Tests use it to simulate a schedule on the CPU and
+ * check its message counts against the closed forms of SURVEY.md §8(c) C.6.
+ *
+ * A plan is the per-GPU program one collective call runs: steps of moves (byte copies
+ * between rank buffers) executed by the GPU that owns the source rank.
+ *   op    : mpxa_op_t;  algo: mpxa_algo_t (not DEFAULT);  p = R * G ranks, R per GPU;
+ *   g     : hierarchical group size (HIER only);
+ *   stop_stage: -1 for the complete collective, else the Bruck stage entry-point truncation;
+ *   c, sd, rd: ALLTOALLV only, full p x p int64 matrices (elements): c[s*p+j] sent by s to j,
+ *              sd[s*p+j] its displacement in s's sendbuf, rd[j*p+s] the displacement in j's
+ *              recvbuf of the segment from s.  Ignored (may be NULL) for uniform ops, whose
+ *              units are whole blocks.
+ * The handle is owned by the caller and released with mpxa_plan_free.
+ */
+#ifndef MPXA_PLAN_H
+#define MPXA_PLAN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+    int64_t src_off, dst_off, len;   /* units                                   */
+    uint16_t src_rank, dst_rank;
+    uint8_t src_kind, dst_kind;      /* 0 send buffer, 1 recv buffer, 2 library workspace */
+    uint8_t fanout;                  /* 1: to every rank's dst_kind buffer at dst_off */
+    uint8_t pad;
+} mpxa_plan_move;
+
+typedef struct {
+    int32_t move_begin, move_end;
+    uint32_t signal_mask, wait_mask; /* peer GPUs written / writing in this step */
+    int64_t total_len, max_len;
+} mpxa_plan_step;
+
+typedef struct {
+    int64_t nsteps, work_units, max_move, max_step_units, signals, total_moves;
+} mpxa_plan_info_t;
+
+int mpxa_plan_build(int op, int algo, int p, int R, int G, int g, int stop_stage,
+                    const int64_t *c, const int64_t *sd, const int64_t *rd, void **plan);
+int mpxa_plan_info(const void *plan, mpxa_plan_info_t *info);
+/* copies GPU `gpu`'s steps / moves; *n in: capacity, out: count */
+int mpxa_plan_steps(const void *plan, int gpu, mpxa_plan_step *out, int *n);
+int mpxa_plan_moves(const void *plan, int gpu, mpxa_plan_move *out, int *n);
+int mpxa_plan_free(void *plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPXA_PLAN_H */

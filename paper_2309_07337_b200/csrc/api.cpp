@@ -1,0 +1,977 @@
+// libmpxa host runtime: communicator, symmetric memory, program cache, launches, persistent
+// requests, selector, and the C ABI of include/mpxa.h / include/mpxa_plan.h.
+//
+// Paper passages: MPIX_Comm_init / MPIX_Alltoallv (§2.1); persistent
+// init/start/wait with setup paid once; default algorithm +
+// every implementation selectable.  Argument contract and lifecycle errors
+// follow SPEC.md:204-216, 239-247, 282-325 (interfaces only).
+#include <cuda_runtime.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/mpxa.h"
+#include "../../include/mpxa_plan.h"
+#include "mpxa_internal.h"
+#include "plan.h"
+
+namespace mpxa {
+cudaError_t launch_exec(const ExecParams &P, int nC, int nG, bool cooperative, cudaStream_t stream);
+cudaError_t launch_counts(const int64_t *sc, int64_t *rc, int64_t *rd, int p, int r0, int nr,
+                          cudaStream_t stream);
+cudaError_t launch_scan(const int64_t *counts, int64_t *rc, int64_t *rd, int p, int nr,
+                        cudaStream_t stream);
+int exec_max_ctas_per_sm();
+}  // namespace mpxa
+
+using namespace mpxa;
+
+#define CK(x)                                                              \
+    do {                                                                   \
+        cudaError_t e_ = (x);                                              \
+        if (e_ != cudaSuccess) {                                           \
+            if (getenv("MPXA_DEBUG"))                                      \
+                fprintf(stderr, "mpxa: %s failed: %s (%s:%d)\n", #x,       \
+                        cudaGetErrorString(e_), __FILE__, __LINE__);       \
+            return e_ == cudaErrorMemoryAllocation ? MPXA_ERR_NOMEM : MPXA_ERR_CUDA; \
+        }                                                                  \
+    } while (0)
+
+namespace {
+
+constexpr uint64_t kBytesPerCta = 32768;   // launch sizing target per CTA per step
+
+// A program uploaded to device memory: [GpuProg x G][steps][moves].
+struct DevProg {
+    void *dmem = nullptr;
+    size_t bytes = 0;
+    Program host;
+    int nsteps = 0;
+};
+
+size_t serialize(const Program &P, std::vector<char> &buf, uintptr_t dbase) {
+    const int G = P.G;
+    size_t off = sizeof(GpuProg) * G;
+    std::vector<size_t> soff(G), moff(G);
+    for (int g = 0; g < G; g++) { soff[g] = off; off += sizeof(Step) * P.steps[g].size(); }
+    for (int g = 0; g < G; g++) { moff[g] = off; off += sizeof(Move) * P.moves[g].size(); }
+    buf.assign(off, 0);
+    for (int g = 0; g < G; g++) {
+        GpuProg gp{};
+        gp.steps = (const Step *)(dbase + soff[g]);
+        gp.moves = (const Move *)(dbase + moff[g]);
+        gp.nsteps = (int32_t)P.steps[g].size();
+        gp.nmoves = (int32_t)P.moves[g].size();
+        memcpy(buf.data() + sizeof(GpuProg) * g, &gp, sizeof gp);
+        if (!P.steps[g].empty()) memcpy(buf.data() + soff[g], P.steps[g].data(), sizeof(Step) * P.steps[g].size());
+        if (!P.moves[g].empty()) memcpy(buf.data() + moff[g], P.moves[g].data(), sizeof(Move) * P.moves[g].size());
+    }
+    return off;
+}
+
+size_t serialized_size(const Program &P) {
+    size_t n = sizeof(GpuProg) * P.G;
+    for (int g = 0; g < P.G; g++) n += sizeof(Step) * P.steps[g].size() + sizeof(Move) * P.moves[g].size();
+    return n;
+}
+
+struct Window {
+    uintptr_t base = 0;
+    size_t size = 0;
+};
+
+struct SelEntry {
+    int op, p, R;
+    uint64_t max_bytes;
+    int algo;
+};
+
+// ring slot for per-call programs (v-ops)
+struct Slot {
+    void *dmem = nullptr;
+    size_t cap = 0;
+    char *pinned = nullptr;
+    size_t pcap = 0;
+    cudaEvent_t ev = nullptr;
+    bool used = false;
+};
+
+}  // namespace
+
+struct mpxa_comm_s {
+    int nprocs = 1, proc = 0, R = 1, device = 0, g = 1;
+    int G = 1;            // GPUs in programs (nprocs, or emulated GPUs)
+    int p = 1;
+    int Rg = 1;           // ranks per program GPU
+    bool emulated = false;
+    mpxa_allgather_fn boot = nullptr;
+    void *ctx = nullptr;
+    double timeout_s = 60.0;
+    int sm_count = 148, cap_ctas = 296;
+
+    SymRegion *sym_local = nullptr;            // G regions when emulated, else 1
+    SymRegion *sym_map[kMaxGpus] = {};
+    char *work_local = nullptr;
+    size_t work_bytes = 0;                     // per program GPU
+    char *work_map[kMaxGpus] = {};
+    int32_t *err_host = nullptr, *err_dev = nullptr;
+    char **win_table_dev = nullptr;            // [G][kMaxWindows]
+    std::vector<Window> windows;               // local registered windows (multi-process)
+    std::vector<std::vector<char *>> win_map;  // [window][gpu] mapped bases
+
+    uint64_t epoch = 0;
+    uint64_t launches = 0;
+    bool poisoned = false;
+    mpxa_request_t active = nullptr;
+
+    int user_algo[3] = {0, 0, 0};
+    std::vector<SelEntry> selector;
+
+    std::map<std::tuple<int, int, int, int>, std::shared_ptr<DevProg>> cache;  // (op,algo,stage,g)
+    std::vector<Slot> ring;
+    int ring_next = 0;
+    int64_t *counts_tmp = nullptr;             // multi-process counts exchange staging
+    size_t counts_tmp_bytes = 0;
+};
+
+struct mpxa_request_s {
+    mpxa_comm_t comm = nullptr;
+    int op = 0, algo = 0;
+    bool active = false;
+    std::shared_ptr<DevProg> prog;
+    const char *send = nullptr;
+    char *recv = nullptr;
+    uint64_t unit = 0, send_stride = 0, recv_stride = 0;
+    int nC = 1;
+    cudaEvent_t done = nullptr;
+    cudaStream_t start_stream = nullptr;
+};
+
+namespace {
+
+bool dtype_ok(size_t w) { return w == 1 || w == 2 || w == 4 || w == 8 || w == 16; }
+
+int bootstrap(mpxa_comm_t c, const void *in, void *out, size_t bytes) {
+    if (c->nprocs == 1) { memcpy(out, in, bytes); return MPXA_SUCCESS; }
+    if (!c->boot) return MPXA_ERR_ARG;
+    return c->boot(in, out, bytes, c->ctx) == 0 ? MPXA_SUCCESS : MPXA_ERR_CUDA;
+}
+
+// ---- symmetric memory --------------------------------------------------------------
+
+int ipc_exchange(mpxa_comm_t c, void *local, char **mapped) {
+    // all-gather IPC handles of `local` and open every peer's
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, local));
+    std::vector<cudaIpcMemHandle_t> all(c->nprocs);
+    int rc = bootstrap(c, &h, all.data(), sizeof h);
+    if (rc) return rc;
+    for (int d = 0; d < c->nprocs; d++) {
+        if (d == c->proc) { mapped[d] = (char *)local; continue; }
+        void *ptr = nullptr;
+        CK(cudaIpcOpenMemHandle(&ptr, all[d], cudaIpcMemLazyEnablePeerAccess));
+        mapped[d] = (char *)ptr;
+    }
+    return MPXA_SUCCESS;
+}
+
+int ensure_work(mpxa_comm_t c, size_t need_per_gpu) {
+    if (need_per_gpu <= c->work_bytes) return MPXA_SUCCESS;
+    size_t nb = std::max(need_per_gpu, c->work_bytes * 2);
+    nb = (nb + 4095) & ~size_t(4095);
+    CK(cudaDeviceSynchronize());   // growth is rare: retire work that may use the old heap
+    if (c->nprocs > 1) {
+        for (int d = 0; d < c->nprocs; d++)
+            if (d != c->proc && c->work_map[d]) cudaIpcCloseMemHandle(c->work_map[d]);
+    }
+    if (c->work_local) cudaFree(c->work_local);
+    c->work_local = nullptr;
+    c->work_bytes = 0;
+    size_t total = c->emulated ? nb * c->G : nb;
+    CK(cudaMalloc((void **)&c->work_local, total));
+    c->work_bytes = nb;
+    if (c->nprocs > 1) {
+        int rc = ipc_exchange(c, c->work_local, c->work_map);
+        if (rc) return rc;
+    } else {
+        for (int g = 0; g < c->G; g++) c->work_map[g] = c->work_local + (size_t)g * nb;
+    }
+    return MPXA_SUCCESS;
+}
+
+// ---- selector -------------------------------------------------------------------------
+int default_algo(mpxa_comm_t c, int op, size_t bytes) {
+    if (c->user_algo[op]) return c->user_algo[op];
+    for (const SelEntry &e : c->selector)
+        if (e.op == op && e.p == c->p && e.R == c->R && bytes <= e.max_bytes) return e.algo;
+    // SPEC.md:256 defaults when nothing was measured: pairwise (alltoall/v); for allgather
+    // the direct (pairwise) exchange, which the measured tables confirm on NVSwitch.
+    return A_PAIRWISE;
+}
+
+bool algo_valid(int op, int algo) {
+    if (op == MPXA_OP_ALLTOALL) return algo == A_PAIRWISE || algo == A_BRUCK || algo == A_HIER;
+    if (op == MPXA_OP_ALLTOALLV) return algo == A_PAIRWISE || algo == A_HIER;
+    if (op == MPXA_OP_ALLGATHER) return algo == A_PAIRWISE || algo == A_BRUCK || algo == A_RING;
+    return false;
+}
+
+int upload_program(const Program &P, std::shared_ptr<DevProg> &out) {
+    auto dp = std::make_shared<DevProg>();
+    size_t n = serialized_size(P);
+    CK(cudaMalloc(&dp->dmem, n ? n : 16));
+    std::vector<char> buf;
+    serialize(P, buf, (uintptr_t)dp->dmem);
+    CK(cudaMemcpy(dp->dmem, buf.data(), n, cudaMemcpyHostToDevice));
+    dp->bytes = n;
+    dp->host = P;
+    dp->nsteps = P.nsteps();
+    out = dp;
+    return MPXA_SUCCESS;
+}
+
+int cached_uniform(mpxa_comm_t c, int op, int algo, int stage, std::shared_ptr<DevProg> &out) {
+    auto key = std::make_tuple(op, algo, stage, c->g);
+    auto it = c->cache.find(key);
+    if (it != c->cache.end()) { out = it->second; return MPXA_SUCCESS; }
+    Program P;
+    bool ok = op == MPXA_OP_ALLTOALL ? build_alltoall(P, algo, c->p, c->Rg, c->G, c->g, stage)
+                                     : build_allgather(P, algo, c->p, c->Rg, c->G, stage);
+    if (!ok) return MPXA_ERR_ALGO;
+    int rc = upload_program(P, out);
+    if (rc) return rc;
+    c->cache[key] = out;
+    return MPXA_SUCCESS;
+}
+
+int choose_ctas(mpxa_comm_t c, const Program &P, uint64_t unit) {
+    uint64_t step_bytes = (uint64_t)P.max_step_units * unit;
+    uint64_t move_bytes = (uint64_t)P.max_move * unit;
+    uint64_t n = (step_bytes + kBytesPerCta - 1) / kBytesPerCta;
+    uint64_t lines = (move_bytes + 127) / 128;
+    n = std::min<uint64_t>(n, std::max<uint64_t>(lines, 1));
+    const char *env = getenv("MPXA_CTAS");
+    if (env && atoi(env) > 0) n = (uint64_t)atoi(env);
+    n = std::max<uint64_t>(1, std::min<uint64_t>(n, (uint64_t)c->cap_ctas));
+    return (int)n;
+}
+
+// Fill launch parameters for a program on this comm.
+int make_params(mpxa_comm_t c, ExecParams &E, const DevProg &dp, const char *send, char *recv,
+                uint64_t unit, uint64_t send_stride, uint64_t recv_stride) {
+    memset(&E, 0, sizeof E);
+    E.progs = (const GpuProg *)dp.dmem;
+    E.G = c->G;
+    E.R = c->Rg;
+    E.p = c->p;
+    E.my_gpu = c->emulated ? -1 : (c->nprocs > 1 ? c->proc : 0);
+    E.unit = unit;
+    E.send_stride = send_stride;
+    E.recv_stride = recv_stride;
+    E.work_stride = (uint64_t)dp.host.work_units * unit;
+    E.err = c->err_dev;
+    E.timeout_ns = (int64_t)(c->timeout_s * 1e9);
+    E.win_table = c->win_table_dev;
+    if (c->nprocs > 1) {
+        int me = c->proc;
+        E.send_base[me] = (char *)send;
+        E.recv_base[me] = recv;
+        for (int d = 0; d < c->G; d++) { E.work_base[d] = c->work_map[d]; E.sym[d] = (SymRegion *)c->sym_map[d]; }
+        // remote recv bases: from the CTS message (registered windows)
+        E.recv_from_cts = 1;
+        uintptr_t r = (uintptr_t)recv;
+        int wi = -1;
+        for (size_t w = 0; w < c->windows.size(); w++)
+            if (r >= c->windows[w].base && r < c->windows[w].base + c->windows[w].size) { wi = (int)w; break; }
+        if (wi < 0) return MPXA_ERR_UNREGISTERED;
+        E.recv_win[me] = (uint64_t)wi;
+        E.recv_off[me] = r - c->windows[wi].base;
+    } else {
+        for (int g = 0; g < c->G; g++) {
+            E.send_base[g] = (char *)send + (size_t)g * c->Rg * send_stride;
+            E.recv_base[g] = recv + (size_t)g * c->Rg * recv_stride;
+            E.work_base[g] = c->work_map[g];
+            E.sym[g] = c->sym_local + g;
+            if (c->emulated) {   // exercise the CTS-carried recv resolution: base 0 + absolute address
+                E.recv_win[g] = 0;
+                E.recv_off[g] = (uint64_t)(uintptr_t)E.recv_base[g];
+            }
+        }
+        E.recv_from_cts = c->emulated ? 1 : 0;
+    }
+    return MPXA_SUCCESS;
+}
+
+int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, uint64_t unit,
+                uint64_t send_stride, uint64_t recv_stride, cudaStream_t stream, int nC = 0) {
+    if (c->poisoned) return MPXA_ERR_TIMEOUT;
+    if (dp.nsteps == 0) return MPXA_SUCCESS;
+    size_t need = (size_t)dp.host.work_units * unit * c->Rg;
+    int rc = ensure_work(c, need);
+    if (rc) return rc;
+    ExecParams E;
+    rc = make_params(c, E, dp, send, recv, unit, send_stride, recv_stride);
+    if (rc) return rc;
+    if (nC <= 0) nC = choose_ctas(c, dp.host, unit);
+    E.epoch = ++c->epoch;
+    cudaError_t e = launch_exec(E, nC, c->emulated ? c->G : 1, c->emulated, stream);
+    if (e != cudaSuccess) {
+        if (getenv("MPXA_DEBUG")) fprintf(stderr, "mpxa: launch failed: %s\n", cudaGetErrorString(e));
+        return MPXA_ERR_CUDA;
+    }
+    c->launches++;
+    return MPXA_SUCCESS;
+}
+
+// per-call program upload through a ring of pinned slots (stream-ordered, no host sync
+// unless the ring wraps onto a copy still in flight)
+int run_dynamic(mpxa_comm_t c, const Program &P, const char *send, char *recv, uint64_t unit,
+                uint64_t send_stride, uint64_t recv_stride, cudaStream_t stream) {
+    if (c->ring.empty()) c->ring.resize(8);
+    Slot &s = c->ring[c->ring_next];
+    c->ring_next = (c->ring_next + 1) % (int)c->ring.size();
+    if (!s.ev) CK(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming));
+    if (s.used) CK(cudaEventSynchronize(s.ev));
+    size_t n = serialized_size(P);
+    if (n > s.cap) {
+        if (s.dmem) CK(cudaFree(s.dmem));
+        CK(cudaMalloc(&s.dmem, n));
+        s.cap = n;
+    }
+    if (n > s.pcap) {
+        if (s.pinned) CK(cudaFreeHost(s.pinned));
+        CK(cudaHostAlloc((void **)&s.pinned, n, cudaHostAllocDefault));
+        s.pcap = n;
+    }
+    std::vector<char> buf;
+    serialize(P, buf, (uintptr_t)s.dmem);
+    memcpy(s.pinned, buf.data(), n);
+    CK(cudaMemcpyAsync(s.dmem, s.pinned, n, cudaMemcpyHostToDevice, stream));
+    DevProg dp;
+    dp.dmem = s.dmem;
+    dp.bytes = n;
+    dp.host = P;
+    dp.nsteps = P.nsteps();
+    int rc = run_program(c, dp, send, recv, unit, send_stride, recv_stride, stream);
+    CK(cudaEventRecord(s.ev, stream));
+    s.used = true;
+    dp.dmem = nullptr;
+    return rc;
+}
+
+// ---- argument checks (all before any data moves) -------------------------
+bool overlap(const void *a, size_t na, const void *b, size_t nb) {
+    uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+    return na && nb && x < y + nb && y < x + na;
+}
+
+int check_uniform(mpxa_comm_t c, const void *send, size_t count, size_t w, void *recv, int op) {
+    if (!c) return MPXA_ERR_ARG;
+    if (!dtype_ok(w)) return MPXA_ERR_ARG;
+    if (count && (!send || !recv)) return MPXA_ERR_ARG;
+    size_t blk = count * w;
+    size_t sbytes = (op == MPXA_OP_ALLTOALL ? (size_t)c->p : 1) * blk * c->R;
+    size_t rbytes = (size_t)c->p * blk * c->R;
+    if (overlap(send, sbytes, recv, rbytes)) return MPXA_ERR_ARG;
+    return MPXA_SUCCESS;
+}
+
+// Gather the FULL count/displacement matrices a v-schedule needs.  Single process: the
+// caller's R*p rows are all p rows.  Multi-process: all-gather through the bootstrap
+// (host collective; persistent requests pay it once at init).
+int gather_v(mpxa_comm_t c, const int64_t *sc, const int64_t *sd, const int64_t *rc,
+             const int64_t *rd, size_t w, size_t send_bpr, size_t recv_bpr,
+             std::vector<int64_t> &C, std::vector<int64_t> &SD, std::vector<int64_t> &RD) {
+    const int p = c->p, R = c->R;
+    if (!sc || !sd || !rc || !rd) return MPXA_ERR_ARG;
+    for (int t = 0; t < R; t++)
+        for (int j = 0; j < p; j++) {
+            size_t i = (size_t)t * p + j;
+            if (sc[i] < 0 || sd[i] < 0 || rc[i] < 0 || rd[i] < 0) return MPXA_ERR_ARG;
+            if ((uint64_t)(sc[i] + sd[i]) * w > send_bpr) return MPXA_ERR_ARG;
+            if ((uint64_t)(rc[i] + rd[i]) * w > recv_bpr) return MPXA_ERR_ARG;
+        }
+    size_t rows = (size_t)R * p;
+    std::vector<int64_t> mine(rows * 4);
+    memcpy(mine.data(), sc, rows * 8);
+    memcpy(mine.data() + rows, sd, rows * 8);
+    memcpy(mine.data() + 2 * rows, rc, rows * 8);
+    memcpy(mine.data() + 3 * rows, rd, rows * 8);
+    std::vector<int64_t> all(rows * 4 * c->nprocs);
+    int r = bootstrap(c, mine.data(), all.data(), rows * 4 * 8);
+    if (r) return r;
+    C.assign((size_t)p * p, 0);
+    SD.assign((size_t)p * p, 0);
+    RD.assign((size_t)p * p, 0);
+    std::vector<int64_t> RC((size_t)p * p);
+    for (int q = 0; q < c->nprocs; q++) {
+        const int64_t *b = all.data() + (size_t)q * rows * 4;
+        for (size_t i = 0; i < rows; i++) {
+            size_t gi = (size_t)q * rows + i;   // global row-major index (rank q*R + t, j)
+            C[gi] = b[i];
+            SD[gi] = b[rows + i];
+            RC[gi] = b[2 * rows + i];
+            RD[gi] = b[3 * rows + i];
+        }
+    }
+    for (int s = 0; s < p; s++)   // SPEC.md:208 global consistency
+        for (int j = 0; j < p; j++)
+            if (C[(size_t)s * p + j] != RC[(size_t)j * p + s]) return MPXA_ERR_MISMATCH;
+    return MPXA_SUCCESS;
+}
+
+int alltoallv_impl(const void *sendbuf, const int64_t *sc, const int64_t *sd, size_t send_bpr,
+                   void *recvbuf, const int64_t *rc, const int64_t *rd, size_t recv_bpr, size_t w,
+                   int algo, mpxa_comm_t c, cudaStream_t stream, mpxa_request_t *req) {
+    if (!c) return MPXA_ERR_ARG;
+    if (!dtype_ok(w)) return MPXA_ERR_ARG;
+    if (!sendbuf || !recvbuf) return MPXA_ERR_ARG;
+    if (overlap(sendbuf, send_bpr * c->R, recvbuf, recv_bpr * c->R)) return MPXA_ERR_ARG;
+    if (algo == A_DEFAULT) algo = default_algo(c, MPXA_OP_ALLTOALLV, recv_bpr);
+    if (!algo_valid(MPXA_OP_ALLTOALLV, algo)) return MPXA_ERR_ALGO;
+    if (algo == A_HIER && c->p % c->g) return MPXA_ERR_TOPOLOGY;
+    std::vector<int64_t> C, SD, RD;
+    int r = gather_v(c, sc, sd, rc, rd, w, send_bpr, recv_bpr, C, SD, RD);
+    if (r) return r;
+    Program P;
+    if (!build_alltoallv(P, algo, c->p, c->Rg, c->G, c->g, C.data(), SD.data(), RD.data())) return MPXA_ERR_ALGO;
+    if (req) {
+        auto q = new mpxa_request_s();
+        q->comm = c; q->op = MPXA_OP_ALLTOALLV; q->algo = algo;
+        int rc2 = upload_program(P, q->prog);
+        if (rc2) { delete q; return rc2; }
+        q->send = (const char *)sendbuf; q->recv = (char *)recvbuf;
+        q->unit = w; q->send_stride = send_bpr; q->recv_stride = recv_bpr;
+        q->nC = choose_ctas(c, P, w);
+        if (c->nprocs > 1) {
+            rc2 = mpxa_register(c, recvbuf, recv_bpr * c->R);
+            if (rc2) { delete q; return rc2; }
+        }
+        rc2 = ensure_work(c, (size_t)P.work_units * w * c->Rg);
+        if (rc2) { delete q; return rc2; }
+        *req = q;
+        return MPXA_SUCCESS;
+    }
+    return run_dynamic(c, P, (const char *)sendbuf, (char *)recvbuf, w, send_bpr, recv_bpr, stream);
+}
+
+int uniform_impl(int op, const void *sendbuf, size_t count, size_t w, void *recvbuf, int algo,
+                 mpxa_comm_t c, cudaStream_t stream, mpxa_request_t *req, int stage = -1,
+                 bool force_bruck = false) {
+    int rc = check_uniform(c, sendbuf, count, w, recvbuf, op);
+    if (rc) return rc;
+    const uint64_t unit = (uint64_t)count * w;
+    if (force_bruck) algo = A_BRUCK;
+    if (algo == A_DEFAULT) algo = default_algo(c, op, unit);
+    if (!algo_valid(op, algo)) return MPXA_ERR_ALGO;
+    if (algo == A_HIER && c->p % c->g) return MPXA_ERR_TOPOLOGY;
+    std::shared_ptr<DevProg> dp;
+    rc = cached_uniform(c, op, algo, stage, dp);
+    if (rc) return rc;
+    uint64_t sstride = op == MPXA_OP_ALLTOALL ? (uint64_t)c->p * unit : unit;
+    uint64_t rstride = (uint64_t)c->p * unit;
+    if (req) {
+        auto q = new mpxa_request_s();
+        q->comm = c; q->op = op; q->algo = algo; q->prog = dp;
+        q->send = (const char *)sendbuf; q->recv = (char *)recvbuf;
+        q->unit = unit; q->send_stride = sstride; q->recv_stride = rstride;
+        q->nC = choose_ctas(c, dp->host, unit);
+        if (c->nprocs > 1 && unit) {
+            rc = mpxa_register(c, recvbuf, rstride * c->R);
+            if (rc) { delete q; return rc; }
+        }
+        rc = ensure_work(c, (size_t)dp->host.work_units * unit * c->Rg);
+        if (rc) { delete q; return rc; }
+        *req = q;
+        return MPXA_SUCCESS;
+    }
+    if (unit == 0) return MPXA_SUCCESS;   // nothing moves; every process takes this branch
+    return run_program(c, *dp, (const char *)sendbuf, (char *)recvbuf, unit, sstride, rstride, stream);
+}
+
+cudaStream_t S(mpxa_stream_t s) { return (cudaStream_t)s; }
+
+}  // namespace
+
+// =========================================================================================
+// C ABI
+// =========================================================================================
+extern "C" {
+
+const char *mpxa_error_string(int s) {
+    switch (s) {
+        case MPXA_SUCCESS: return "success";
+        case MPXA_ERR_ARG: return "invalid argument";
+        case MPXA_ERR_ALGO: return "unknown or unsupported algorithm for this operation";
+        case MPXA_ERR_LIFECYCLE: return "request lifecycle violation";
+        case MPXA_ERR_TOPOLOGY: return "invalid rank / group topology";
+        case MPXA_ERR_MISMATCH: return "argument mismatch across processes";
+        case MPXA_ERR_CUDA: return "CUDA error";
+        case MPXA_ERR_TIMEOUT: return "device watchdog timeout (communicator poisoned)";
+        case MPXA_ERR_NOMEM: return "out of memory";
+        case MPXA_ERR_UNREGISTERED: return "recvbuf not registered (multi-process mode)";
+        default: return "unknown status";
+    }
+}
+
+const char *mpxa_algo_name(mpxa_algo_t a) {
+    switch (a) {
+        case MPXA_ALGO_DEFAULT: return "default";
+        case MPXA_ALGO_PAIRWISE: return "pairwise";
+        case MPXA_ALGO_BRUCK: return "bruck";
+        case MPXA_ALGO_HIER: return "hier";
+        case MPXA_ALGO_RING: return "ring";
+        default: return "unknown";
+    }
+}
+
+int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
+    if (!out || !a) return MPXA_ERR_ARG;
+    *out = nullptr;
+    if (a->nprocs < 1 || a->proc < 0 || a->proc >= a->nprocs || a->ranks_per_proc < 1) return MPXA_ERR_TOPOLOGY;
+    if (a->nprocs > 1 && !a->bootstrap_allgather) return MPXA_ERR_ARG;
+    if (a->nprocs > 1 && a->emulate_gpus > 1) return MPXA_ERR_ARG;
+    std::unique_ptr<mpxa_comm_s> c(new mpxa_comm_s());
+    c->nprocs = a->nprocs;
+    c->proc = a->proc;
+    c->R = a->ranks_per_proc;
+    c->device = a->device;
+    c->p = c->nprocs * c->R;
+    c->g = a->group_size > 0 ? a->group_size : (c->R > 1 ? c->R : 1);
+    if (c->p % c->g) return MPXA_ERR_TOPOLOGY;
+    c->boot = a->bootstrap_allgather;
+    c->ctx = a->ctx;
+    c->timeout_s = a->timeout_s > 0 ? a->timeout_s : 60.0;
+    if (a->emulate_gpus > 1) {
+        if (c->R % a->emulate_gpus) return MPXA_ERR_TOPOLOGY;
+        c->emulated = true;
+        c->G = a->emulate_gpus;
+        c->Rg = c->R / c->G;
+    } else {
+        c->G = c->nprocs;
+        c->Rg = c->R;
+    }
+    if (c->G > kMaxGpus || c->p > 65535) return MPXA_ERR_TOPOLOGY;
+    CK(cudaSetDevice(c->device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, c->device));
+    c->sm_count = prop.multiProcessorCount;
+    int occ = exec_max_ctas_per_sm();
+    if (occ < 1) occ = 1;
+    int cap = std::min(kMaxCtas, c->sm_count * occ);
+    if (c->emulated) cap = std::max(1, cap / c->G);
+    c->cap_ctas = cap;
+    CK(cudaHostAlloc((void **)&c->err_host, sizeof(int32_t), cudaHostAllocMapped));
+    *c->err_host = 0;
+    CK(cudaHostGetDevicePointer((void **)&c->err_dev, c->err_host, 0));
+    int nsym = c->emulated ? c->G : 1;
+    CK(cudaMalloc((void **)&c->sym_local, sizeof(SymRegion) * nsym));
+    CK(cudaMemset(c->sym_local, 0, sizeof(SymRegion) * nsym));
+    CK(cudaMalloc((void **)&c->win_table_dev, sizeof(char *) * kMaxGpus * kMaxWindows));
+    CK(cudaMemset(c->win_table_dev, 0, sizeof(char *) * kMaxGpus * kMaxWindows));
+    if (c->nprocs > 1) {
+        // consistency of the topology across processes (MPXA_ERR_MISMATCH)
+        int mine[3] = {c->R, c->g, c->nprocs};
+        std::vector<int> all(3 * c->nprocs);
+        int rc = bootstrap(c.get(), mine, all.data(), sizeof mine);
+        if (rc) return rc;
+        for (int q = 0; q < c->nprocs; q++)
+            if (memcmp(mine, &all[3 * q], sizeof mine)) return MPXA_ERR_MISMATCH;
+        rc = ipc_exchange(c.get(), c->sym_local, (char **)c->sym_map);
+        if (rc) return rc;
+    } else {
+        for (int g = 0; g < c->G; g++) c->sym_map[g] = c->sym_local + g;
+    }
+    size_t heap = a->heap_bytes ? a->heap_bytes : (size_t)64 << 20;
+    int rc = ensure_work(c.get(), heap);
+    if (rc) return rc;
+    // built-in selector table shipped next to the library (optional)
+    const char *sel = getenv("MPXA_SELECTOR");
+    if (sel) mpxa_load_selector(c.get(), sel);
+    const char *al = getenv("MPXA_ALGO");   // e.g. "alltoall:bruck,allgather:ring"
+    if (al) {
+        std::string s(al);
+        std::stringstream ss(s);
+        std::string item;
+        while (std::getline(ss, item, ',')) {
+            auto k = item.find(':');
+            if (k == std::string::npos) continue;
+            std::string o = item.substr(0, k), v = item.substr(k + 1);
+            int op = o == "alltoall" ? 0 : o == "alltoallv" ? 1 : o == "allgather" ? 2 : -1;
+            int av = v == "pairwise" ? 1 : v == "bruck" ? 2 : v == "hier" ? 3 : v == "ring" ? 4 : 0;
+            if (op >= 0 && algo_valid(op, av)) c->user_algo[op] = av;
+        }
+    }
+    CK(cudaDeviceSynchronize());
+    *out = c.release();
+    return MPXA_SUCCESS;
+}
+
+int mpxa_finalize(mpxa_comm_t c) {
+    if (!c) return MPXA_ERR_ARG;
+    cudaDeviceSynchronize();
+    if (c->nprocs > 1) {
+        for (int d = 0; d < c->nprocs; d++) {
+            if (d == c->proc) continue;
+            if (c->sym_map[d]) cudaIpcCloseMemHandle(c->sym_map[d]);
+            if (c->work_map[d]) cudaIpcCloseMemHandle(c->work_map[d]);
+            for (auto &w : c->win_map)
+                if (w.size() > (size_t)d && w[d]) cudaIpcCloseMemHandle(w[d]);
+        }
+    }
+    for (auto &kv : c->cache) cudaFree(kv.second->dmem);
+    for (auto &s : c->ring) {
+        if (s.dmem) cudaFree(s.dmem);
+        if (s.pinned) cudaFreeHost(s.pinned);
+        if (s.ev) cudaEventDestroy(s.ev);
+    }
+    if (c->work_local) cudaFree(c->work_local);
+    if (c->sym_local) cudaFree(c->sym_local);
+    if (c->win_table_dev) cudaFree(c->win_table_dev);
+    if (c->err_host) cudaFreeHost(c->err_host);
+    if (c->counts_tmp) cudaFree(c->counts_tmp);
+    delete c;
+    return MPXA_SUCCESS;
+}
+
+int mpxa_comm_size(mpxa_comm_t c, int *p) {
+    if (!c || !p) return MPXA_ERR_ARG;
+    *p = c->p;
+    return MPXA_SUCCESS;
+}
+
+int mpxa_comm_rank0(mpxa_comm_t c, int *r0) {
+    if (!c || !r0) return MPXA_ERR_ARG;
+    *r0 = c->proc * c->R;
+    return MPXA_SUCCESS;
+}
+
+int mpxa_comm_check(mpxa_comm_t c) {
+    if (!c) return MPXA_ERR_ARG;
+    if (c->err_host && *(volatile int32_t *)c->err_host) c->poisoned = true;
+    return c->poisoned ? MPXA_ERR_TIMEOUT : MPXA_SUCCESS;
+}
+
+int mpxa_launch_count(mpxa_comm_t c, uint64_t *n) {
+    if (!c || !n) return MPXA_ERR_ARG;
+    *n = c->launches;
+    return MPXA_SUCCESS;
+}
+
+int mpxa_register(mpxa_comm_t c, void *ptr, size_t bytes) {
+    if (!c || !ptr) return MPXA_ERR_ARG;
+    if (c->nprocs == 1) return MPXA_SUCCESS;
+    uintptr_t x = (uintptr_t)ptr;
+    // already inside a registered window?  (collective decision: every process registers
+    // a buffer of its own, so all take the same branch only if all hit -- exchange a flag)
+    int hit = 0;
+    for (auto &w : c->windows)
+        if (x >= w.base && x + bytes <= w.base + w.size) hit = 1;
+    std::vector<int> hits(c->nprocs);
+    int rc = bootstrap(c, &hit, hits.data(), sizeof hit);
+    if (rc) return rc;
+    bool all = true;
+    for (int h : hits) all = all && h;
+    if (all) return MPXA_SUCCESS;
+    if (c->windows.size() >= (size_t)kMaxWindows) return MPXA_ERR_NOMEM;
+    // allocation range of ptr: resolve through the driver entry point (no libcuda link)
+    typedef int (*range_fn)(uintptr_t *, size_t *, uintptr_t);
+    static range_fn fn = nullptr;
+    if (!fn) {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q));
+        fn = (range_fn)f;
+    }
+    uintptr_t base = 0;
+    size_t size = 0;
+    if (!fn || fn(&base, &size, x) != 0) return MPXA_ERR_ARG;
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, (void *)base));
+    std::vector<cudaIpcMemHandle_t> allh(c->nprocs);
+    rc = bootstrap(c, &h, allh.data(), sizeof h);
+    if (rc) return rc;
+    std::vector<char *> mapped(c->nprocs, nullptr);
+    for (int d = 0; d < c->nprocs; d++) {
+        if (d == c->proc) { mapped[d] = (char *)base; continue; }
+        void *m = nullptr;
+        CK(cudaIpcOpenMemHandle(&m, allh[d], cudaIpcMemLazyEnablePeerAccess));
+        mapped[d] = (char *)m;
+    }
+    int wi = (int)c->windows.size();
+    c->windows.push_back(Window{base, size});
+    c->win_map.push_back(mapped);
+    std::vector<char *> col(c->nprocs);
+    for (int d = 0; d < c->nprocs; d++)
+        CK(cudaMemcpy(c->win_table_dev + (size_t)d * kMaxWindows + wi, &mapped[d], sizeof(char *),
+                      cudaMemcpyHostToDevice));
+    return MPXA_SUCCESS;
+}
+
+int mpxa_deregister(mpxa_comm_t c, void *ptr) {
+    if (!c || !ptr) return MPXA_ERR_ARG;
+    return MPXA_SUCCESS;   // windows live until finalize (indices must stay stable)
+}
+
+int mpxa_alltoall(const void *s, size_t count, size_t w, void *r, mpxa_comm_t c, mpxa_stream_t st) {
+    return uniform_impl(MPXA_OP_ALLTOALL, s, count, w, r, A_DEFAULT, c, S(st), nullptr);
+}
+int mpxa_allgather(const void *s, size_t count, size_t w, void *r, mpxa_comm_t c, mpxa_stream_t st) {
+    return uniform_impl(MPXA_OP_ALLGATHER, s, count, w, r, A_DEFAULT, c, S(st), nullptr);
+}
+int mpxa_alltoall_algo(const void *s, size_t count, size_t w, void *r, mpxa_algo_t a, mpxa_comm_t c,
+                       mpxa_stream_t st) {
+    return uniform_impl(MPXA_OP_ALLTOALL, s, count, w, r, a, c, S(st), nullptr);
+}
+int mpxa_allgather_algo(const void *s, size_t count, size_t w, void *r, mpxa_algo_t a, mpxa_comm_t c,
+                        mpxa_stream_t st) {
+    return uniform_impl(MPXA_OP_ALLGATHER, s, count, w, r, a, c, S(st), nullptr);
+}
+int mpxa_alltoallv(const void *s, const int64_t *sc, const int64_t *sd, size_t sb, void *r,
+                   const int64_t *rc, const int64_t *rd, size_t rb, size_t w, mpxa_comm_t c,
+                   mpxa_stream_t st) {
+    return alltoallv_impl(s, sc, sd, sb, r, rc, rd, rb, w, A_DEFAULT, c, S(st), nullptr);
+}
+int mpxa_alltoallv_algo(const void *s, const int64_t *sc, const int64_t *sd, size_t sb, void *r,
+                        const int64_t *rc, const int64_t *rd, size_t rb, size_t w, mpxa_algo_t a,
+                        mpxa_comm_t c, mpxa_stream_t st) {
+    return alltoallv_impl(s, sc, sd, sb, r, rc, rd, rb, w, a, c, S(st), nullptr);
+}
+
+int mpxa_alltoall_bruck_stage(const void *s, size_t count, size_t w, void *T, int stage, mpxa_comm_t c,
+                              mpxa_stream_t st) {
+    if (!c) return MPXA_ERR_ARG;
+    if (stage < -1 || stage > ceil_log2(c->p)) return MPXA_ERR_ARG;
+    return uniform_impl(MPXA_OP_ALLTOALL, s, count, w, T, A_BRUCK, c, S(st), nullptr, stage, true);
+}
+int mpxa_allgather_bruck_stage(const void *s, size_t count, size_t w, void *T, int stage, mpxa_comm_t c,
+                               mpxa_stream_t st) {
+    if (!c) return MPXA_ERR_ARG;
+    if (stage < -1 || stage > ceil_log2(c->p)) return MPXA_ERR_ARG;
+    return uniform_impl(MPXA_OP_ALLGATHER, s, count, w, T, A_BRUCK, c, S(st), nullptr, stage, true);
+}
+
+int mpxa_alltoallv_counts(const int64_t *d_sc, int64_t *d_rc, int64_t *d_rd, mpxa_comm_t c,
+                          mpxa_stream_t st) {
+    if (!c || !d_sc || !d_rc || !d_rd) return MPXA_ERR_ARG;
+    if (c->poisoned) return MPXA_ERR_TIMEOUT;
+    if (c->nprocs == 1) {
+        // all p ranks are on this device: one kernel, transpose + warp scans
+        cudaError_t e = launch_counts(d_sc, d_rc, d_rd, c->p, 0, c->p, S(st));
+        if (e != cudaSuccess) return MPXA_ERR_CUDA;
+        c->launches++;
+        return MPXA_SUCCESS;
+    }
+    // multi-process: an alltoall of one int64 per rank pair into registered staging,
+    // then the scan kernel (2 launches)
+    size_t bytes = (size_t)c->R * c->p * sizeof(int64_t);
+    if (!c->counts_tmp) {
+        CK(cudaMalloc((void **)&c->counts_tmp, bytes));
+        c->counts_tmp_bytes = bytes;
+        int rc = mpxa_register(c, c->counts_tmp, bytes);
+        if (rc) return rc;
+    }
+    int rc = uniform_impl(MPXA_OP_ALLTOALL, d_sc, 1, 8, c->counts_tmp, A_PAIRWISE, c, S(st), nullptr);
+    if (rc) return rc;
+    cudaError_t e = launch_scan(c->counts_tmp, d_rc, d_rd, c->p, c->R, S(st));
+    if (e != cudaSuccess) return MPXA_ERR_CUDA;
+    c->launches++;
+    return MPXA_SUCCESS;
+}
+
+// ---- persistent requests ----------------------------------------------------------------
+int mpxa_alltoall_init(const void *s, size_t count, size_t w, void *r, mpxa_algo_t a, mpxa_comm_t c,
+                       const void *info, mpxa_request_t *req) {
+    (void)info;
+    if (!req) return MPXA_ERR_ARG;
+    *req = nullptr;
+    return uniform_impl(MPXA_OP_ALLTOALL, s, count, w, r, a, c, nullptr, req);
+}
+int mpxa_allgather_init(const void *s, size_t count, size_t w, void *r, mpxa_algo_t a, mpxa_comm_t c,
+                        const void *info, mpxa_request_t *req) {
+    (void)info;
+    if (!req) return MPXA_ERR_ARG;
+    *req = nullptr;
+    return uniform_impl(MPXA_OP_ALLGATHER, s, count, w, r, a, c, nullptr, req);
+}
+int mpxa_alltoallv_init(const void *s, const int64_t *sc, const int64_t *sd, size_t sb, void *r,
+                        const int64_t *rc, const int64_t *rd, size_t rb, size_t w, mpxa_algo_t a,
+                        mpxa_comm_t c, const void *info, mpxa_request_t *req) {
+    (void)info;
+    if (!req) return MPXA_ERR_ARG;
+    *req = nullptr;
+    return alltoallv_impl(s, sc, sd, sb, r, rc, rd, rb, w, a, c, nullptr, req);
+}
+
+int mpxa_start(mpxa_request_t q, mpxa_stream_t st) {
+    if (!q) return MPXA_ERR_ARG;
+    if (q->active) return MPXA_ERR_LIFECYCLE;
+    mpxa_comm_t c = q->comm;
+    if (c->active && c->active != q) return MPXA_ERR_LIFECYCLE;   // one in flight
+    if (q->unit) {
+        int rc = run_program(c, *q->prog, q->send, q->recv, q->unit, q->send_stride, q->recv_stride, S(st), q->nC);
+        if (rc) return rc;
+    }
+    if (!q->done) CK(cudaEventCreateWithFlags(&q->done, cudaEventDisableTiming));
+    CK(cudaEventRecord(q->done, S(st)));
+    q->start_stream = S(st);
+    q->active = true;
+    c->active = q;
+    return MPXA_SUCCESS;
+}
+
+int mpxa_wait(mpxa_request_t q, mpxa_stream_t st) {
+    if (!q) return MPXA_ERR_ARG;
+    if (!q->active) return MPXA_ERR_LIFECYCLE;
+    if (S(st) != q->start_stream) CK(cudaStreamWaitEvent(S(st), q->done, 0));
+    q->active = false;
+    if (q->comm->active == q) q->comm->active = nullptr;
+    return MPXA_SUCCESS;
+}
+
+int mpxa_request_free(mpxa_request_t *qp) {
+    if (!qp || !*qp) return MPXA_ERR_ARG;
+    mpxa_request_t q = *qp;
+    if (q->active) return MPXA_ERR_LIFECYCLE;
+    if (q->done) cudaEventDestroy(q->done);
+    // cached uniform programs are shared with the comm; v-programs are owned
+    if (q->op == MPXA_OP_ALLTOALLV && q->prog && q->prog.use_count() == 1) {
+        cudaDeviceSynchronize();
+        cudaFree(q->prog->dmem);
+    }
+    delete q;
+    *qp = nullptr;
+    return MPXA_SUCCESS;
+}
+
+int mpxa_request_algorithm(mpxa_request_t q, mpxa_algo_t *a) {
+    if (!q || !a) return MPXA_ERR_ARG;
+    *a = (mpxa_algo_t)q->algo;
+    return MPXA_SUCCESS;
+}
+
+// ---- registry / selector -----------------------------------------------------------------
+int mpxa_set_algorithm(mpxa_comm_t c, mpxa_op_t op, mpxa_algo_t a) {
+    if (!c || op < 0 || op > 2) return MPXA_ERR_ARG;
+    if (a != MPXA_ALGO_DEFAULT && !algo_valid(op, a)) return MPXA_ERR_ALGO;
+    c->user_algo[op] = a;
+    return MPXA_SUCCESS;
+}
+
+int mpxa_get_algorithm(mpxa_comm_t c, mpxa_op_t op, size_t bytes, mpxa_algo_t *chosen) {
+    if (!c || !chosen || op < 0 || op > 2) return MPXA_ERR_ARG;
+    *chosen = (mpxa_algo_t)default_algo(c, op, bytes);
+    return MPXA_SUCCESS;
+}
+
+int mpxa_list_algorithms(mpxa_op_t op, mpxa_algo_t *out, int *n) {
+    if (!n || op < 0 || op > 2) return MPXA_ERR_ARG;
+    static const mpxa_algo_t a2a[] = {MPXA_ALGO_PAIRWISE, MPXA_ALGO_BRUCK, MPXA_ALGO_HIER};
+    static const mpxa_algo_t a2av[] = {MPXA_ALGO_PAIRWISE, MPXA_ALGO_HIER};
+    static const mpxa_algo_t ag[] = {MPXA_ALGO_PAIRWISE, MPXA_ALGO_BRUCK, MPXA_ALGO_RING};
+    const mpxa_algo_t *src = op == 0 ? a2a : op == 1 ? a2av : ag;
+    int cnt = op == 1 ? 2 : 3;
+    if (out) {
+        if (*n < cnt) { *n = cnt; return MPXA_ERR_ARG; }
+        for (int i = 0; i < cnt; i++) out[i] = src[i];
+    }
+    *n = cnt;
+    return MPXA_SUCCESS;
+}
+
+int mpxa_load_selector(mpxa_comm_t c, const char *path) {
+    if (!c || !path) return MPXA_ERR_ARG;
+    std::ifstream f(path);
+    if (!f) return MPXA_ERR_ARG;
+    std::vector<SelEntry> t;
+    std::string line;
+    while (std::getline(f, line)) {
+        auto h = line.find('#');
+        if (h != std::string::npos) line = line.substr(0, h);
+        std::stringstream ss(line);
+        std::string op, algo;
+        SelEntry e{};
+        unsigned long long mb = 0;
+        if (!(ss >> op >> e.p >> e.R >> mb >> algo)) continue;
+        e.op = op == "alltoall" ? 0 : op == "alltoallv" ? 1 : op == "allgather" ? 2 : -1;
+        e.algo = algo == "pairwise" ? 1 : algo == "bruck" ? 2 : algo == "hier" ? 3 : algo == "ring" ? 4 : 0;
+        e.max_bytes = mb;
+        if (e.op < 0 || !algo_valid(e.op, e.algo)) return MPXA_ERR_ARG;
+        t.push_back(e);
+    }
+    c->selector = t;
+    return MPXA_SUCCESS;
+}
+
+// ---- host-only plan introspection (include/mpxa_plan.h) ---------------------------------
+int mpxa_plan_build(int op, int algo, int p, int R, int G, int g, int stop_stage, const int64_t *cnt,
+                    const int64_t *sd, const int64_t *rd, void **plan) {
+    if (!plan) return MPXA_ERR_ARG;
+    *plan = nullptr;
+    auto P = new Program();
+    bool ok = false;
+    if (op == MPXA_OP_ALLTOALL) ok = build_alltoall(*P, algo, p, R, G, g, stop_stage);
+    else if (op == MPXA_OP_ALLGATHER) ok = build_allgather(*P, algo, p, R, G, stop_stage);
+    else if (op == MPXA_OP_ALLTOALLV && cnt && sd && rd) ok = build_alltoallv(*P, algo, p, R, G, g, cnt, sd, rd);
+    if (!ok) { delete P; return MPXA_ERR_ALGO; }
+    *plan = P;
+    return MPXA_SUCCESS;
+}
+
+int mpxa_plan_info(const void *plan, mpxa_plan_info_t *info) {
+    if (!plan || !info) return MPXA_ERR_ARG;
+    const Program *P = (const Program *)plan;
+    info->nsteps = P->nsteps();
+    info->work_units = P->work_units;
+    info->max_move = P->max_move;
+    info->max_step_units = P->max_step_units;
+    info->signals = P->signals;
+    int64_t tm = 0;
+    for (auto &m : P->moves) tm += (int64_t)m.size();
+    info->total_moves = tm;
+    return MPXA_SUCCESS;
+}
+
+int mpxa_plan_steps(const void *plan, int gpu, mpxa_plan_step *out, int *n) {
+    if (!plan || !n) return MPXA_ERR_ARG;
+    const Program *P = (const Program *)plan;
+    if (gpu < 0 || gpu >= P->G) return MPXA_ERR_ARG;
+    const auto &v = P->steps[gpu];
+    if (out) {
+        if (*n < (int)v.size()) return MPXA_ERR_ARG;
+        static_assert(sizeof(mpxa_plan_step) == sizeof(Step), "plan step layout");
+        memcpy(out, v.data(), sizeof(Step) * v.size());
+    }
+    *n = (int)v.size();
+    return MPXA_SUCCESS;
+}
+
+int mpxa_plan_moves(const void *plan, int gpu, mpxa_plan_move *out, int *n) {
+    if (!plan || !n) return MPXA_ERR_ARG;
+    const Program *P = (const Program *)plan;
+    if (gpu < 0 || gpu >= P->G) return MPXA_ERR_ARG;
+    const auto &v = P->moves[gpu];
+    if (out) {
+        if (*n < (int)v.size()) return MPXA_ERR_ARG;
+        static_assert(sizeof(mpxa_plan_move) == sizeof(Move), "plan move layout");
+        memcpy(out, v.data(), sizeof(Move) * v.size());
+    }
+    *n = (int)v.size();
+    return MPXA_SUCCESS;
+}
+
+int mpxa_plan_free(void *plan) {
+    delete (Program *)plan;
+    return MPXA_SUCCESS;
+}
+
+}  // extern "C"

@@ -1,0 +1,389 @@
+// sm_100a kernels of the mpxa hot path.
+//
+//  mpxa_exec_kernel   -- executes a collective PROGRAM (mpxa_internal.h): every step of
+//                        pairwise / Bruck / ring / hierarchical alltoall(v) and allgather
+//                        (SURVEY.md §8(a) A3-A8).  Column-slice ownership: CTA c moves
+//                        slice c of every move, so steps are separated by __syncthreads
+//                        only; cross-GPU dependencies use per-(src GPU, CTA) release/acquire
+//                        flags plus one clear-to-send (CTS) flag per GPU pair (A9).
+//  mpxa_counts_kernel -- counts exchange + exclusive scan (A2) for ranks resident on this
+//                        device, one warp per receiving rank, __shfl_up_sync scans.
+//  mpxa_scan_kernel   -- exclusive scan only (multi-process path: counts arrive through
+//                        an exchange program first).
+//
+// Payloads are opaque bytes: only integer vector loads/stores, never a float conversion.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "mpxa_internal.h"
+
+namespace mpxa {
+
+// ------------------------------------------------------------------------------------
+// memory primitives
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t *p, uint64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Source loads: SEND buffers are never written inside a launch -> read-only path, no L1
+// allocation.  Every other buffer (RECV, WORK) may have been written earlier in the same
+// launch by another SM or a peer GPU -> cache-global (.cg, L2 only, never a stale L1 line).
+template <bool RO>
+__device__ __forceinline__ uint4 ld16(const uint4 *p) {
+    uint4 v;
+    if (RO)
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    else
+        asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st16(uint4 *p, const uint4 &v) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w) : "memory");
+}
+template <typename T>
+__device__ __forceinline__ T ldcg(const T *p) { return __ldcg(p); }
+template <>
+__device__ __forceinline__ uint8_t ldcg<uint8_t>(const uint8_t *p) {
+    unsigned short v;
+    asm volatile("ld.global.cg.u8 %0, [%1];" : "=h"(v) : "l"(p));
+    return (uint8_t)v;
+}
+
+// Copy n bytes with NT cooperating threads (index t), all sharing the alignment class W of
+// (src, dst): W-byte accesses for the body (U in flight per thread), bytes for head/tail.
+// NT is a compile-time constant so the U addresses of an iteration are one base register
+// plus immediates.
+template <typename V, int U, int NT>
+__device__ __forceinline__ void copy_words(char *dst, const char *src, uint64_t n, int t) {
+    constexpr int W = sizeof(V);
+    uint32_t head = (uint32_t)((W - ((uintptr_t)dst & (W - 1))) & (W - 1));
+    if (head > n) head = (uint32_t)n;
+    for (uint32_t i = t; i < head; i += NT) dst[i] = (char)ldcg((const uint8_t *)src + i);
+    const V *s = (const V *)(src + head) + t;
+    V *d = (V *)(dst + head) + t;
+    const uint64_t nv = (n - head) / W;
+    uint64_t i = t;
+    for (; i + (uint64_t)(U - 1) * NT < nv; i += (uint64_t)U * NT, s += U * NT, d += U * NT) {
+        V v[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) v[u] = ldcg(s + u * NT);
+#pragma unroll
+        for (int u = 0; u < U; u++) d[u * NT] = v[u];
+    }
+    for (; i < nv; i += NT, s += NT, d += NT) *d = ldcg(s);
+    const uint64_t done = head + nv * W;
+    for (uint64_t k = done + t; k < n; k += NT) dst[k] = (char)ldcg((const uint8_t *)src + k);
+}
+
+// 16-byte path: one load, nd stores (nd = 1 except allgather direct fan-out); every
+// destination shares the source's 16-B alignment.
+template <bool RO, int U, int NT>
+__device__ __forceinline__ void copy16_fan(char *const *dsts, int nd, const char *src, uint64_t n, int t) {
+    uint32_t head = (uint32_t)((16 - ((uintptr_t)src & 15)) & 15);
+    if (head > n) head = (uint32_t)n;
+    for (uint32_t i = t; i < head; i += NT) {
+        char b = (char)ldcg((const uint8_t *)src + i);
+        for (int k = 0; k < nd; k++) dsts[k][i] = b;
+    }
+    const uint4 *s = (const uint4 *)(src + head) + t;
+    const uint64_t nv = (n - head) >> 4;
+    uint64_t i = t;
+    for (; i + (uint64_t)(U - 1) * NT < nv; i += (uint64_t)U * NT, s += U * NT) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) v[u] = ld16<RO>(s + u * NT);
+        for (int k = 0; k < nd; k++) {
+            uint4 *d = (uint4 *)(dsts[k] + head) + i;
+#pragma unroll
+            for (int u = 0; u < U; u++) st16(d + u * NT, v[u]);
+        }
+    }
+    for (; i < nv; i += NT, s += NT) {
+        uint4 v = ld16<RO>(s);
+        for (int k = 0; k < nd; k++) st16((uint4 *)(dsts[k] + head) + i, v);
+    }
+    const uint64_t done = head + nv * 16;
+    for (uint64_t k2 = done + t; k2 < n; k2 += NT) {
+        char b = (char)ldcg((const uint8_t *)src + k2);
+        for (int k = 0; k < nd; k++) dsts[k][k2] = b;
+    }
+}
+
+// Copy of one slice to one destination: widest access class shared by (src, dst).
+template <int U, int NT>
+__device__ __forceinline__ void copy_slice1(char *dst, const char *src, uint64_t n, bool ro, int t) {
+    if (n == 0) return;
+    unsigned m = (unsigned)(((uintptr_t)dst ^ (uintptr_t)src) & 15);
+    if (m == 0) {
+        char *const d1[1] = {dst};
+        if (ro) copy16_fan<true, U, NT>(d1, 1, src, n, t);
+        else    copy16_fan<false, U, NT>(d1, 1, src, n, t);
+    } else if ((m & 7) == 0) copy_words<unsigned long long, U, NT>(dst, src, n, t);
+    else if ((m & 3) == 0)   copy_words<unsigned int, U, NT>(dst, src, n, t);
+    else if ((m & 1) == 0)   copy_words<unsigned short, U, NT>(dst, src, n, t);
+    else                     copy_words<uint8_t, 1, NT>(dst, src, n, t);
+}
+
+// Fan-out copy of one slice to nd destinations (allgather direct): one load, nd stores
+// when every destination shares the source's 16-B alignment, else per-destination copies.
+template <int U, int NT>
+__device__ __forceinline__ void copy_slice_fan(char *const *dsts, int nd, const char *src, uint64_t n,
+                                               bool ro, int t) {
+    if (n == 0) return;
+    unsigned mis = 0;
+    for (int k = 0; k < nd; k++) mis |= (unsigned)(((uintptr_t)dsts[k] ^ (uintptr_t)src) & 15);
+    if (mis == 0) {
+        if (ro) copy16_fan<true, U, NT>(dsts, nd, src, n, t);
+        else    copy16_fan<false, U, NT>(dsts, nd, src, n, t);
+        return;
+    }
+    for (int k = 0; k < nd; k++) copy_slice1<U, NT>(dsts[k], src, n, ro, t);
+}
+
+// ------------------------------------------------------------------------------------
+// executor
+// ------------------------------------------------------------------------------------
+constexpr uint64_t kLine = 128;          // slice boundaries are 128-B multiples of a move
+constexpr uint64_t kCtaCopyMin = 8192;   // slices at least this long use the whole CTA
+constexpr int kWarps = kThreads / 32;
+
+__device__ __forceinline__ void slice_of(uint64_t nbytes, int c, int nC, uint64_t &lo, uint64_t &hi) {
+    uint64_t nl = (nbytes + kLine - 1) / kLine;
+    lo = ((uint64_t)c * nl / nC) * kLine;
+    hi = ((uint64_t)(c + 1) * nl / nC) * kLine;
+    if (hi > nbytes) hi = nbytes;
+    if (lo > hi) lo = hi;
+}
+
+struct ExecShared {
+    char *recv_base[kMaxGpus];
+    uint32_t cts_ok;     // remote GPUs whose CTS for this epoch was observed
+    int abort_flag;
+};
+
+__device__ __forceinline__ char *base_of(const ExecParams &P, const ExecShared &S, int kind,
+                                         int rank) {
+    int g = rank / P.R;
+    uint64_t local = (uint64_t)(rank - g * P.R);
+    if (kind == BK_SEND) return P.send_base[g] + local * P.send_stride;
+    if (kind == BK_RECV) return S.recv_base[g] + local * P.recv_stride;
+    return P.work_base[g] + local * P.work_stride;
+}
+
+// Spin (threads < 32, one per bit of mask) until *slot(bit) >= want; sets abort on timeout.
+__device__ __forceinline__ void wait_mask_ge(const ExecParams &P, ExecShared &S, uint32_t mask,
+                                             const uint64_t *slot0, uint64_t stride_elems,
+                                             uint64_t want) {
+    int t = threadIdx.x;
+    if (t < 32 && ((mask >> t) & 1u)) {
+        const uint64_t *slot = slot0 + (uint64_t)t * stride_elems;
+        uint64_t start = 0;
+        int it = 0;
+        while (ld_acquire_sys(slot) < want) {
+            if (++it > 32) {
+                __nanosleep(128);
+                if (start == 0) start = globaltimer();
+                else if ((int64_t)(globaltimer() - start) > P.timeout_ns) {
+                    atomicExch(P.err, 1);
+                    S.abort_flag = 1;
+                    break;
+                }
+            }
+            if (*(volatile int *)&S.abort_flag) break;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) mpxa_exec_kernel(const __grid_constant__ ExecParams P) {
+    __shared__ ExecShared S;
+    const int g = P.my_gpu >= 0 ? P.my_gpu : (int)blockIdx.y;
+    const int c = blockIdx.x;
+    const int nC = gridDim.x;
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    const GpuProg prog = P.progs[g];
+    const bool multi = P.G > 1;
+
+    if (t < kMaxGpus) S.recv_base[t] = P.recv_base[t];
+    if (t == 0) { S.cts_ok = 0; S.abort_flag = 0; }
+    // CTS: this GPU is inside epoch `epoch`, so every earlier use of its buffers is complete
+    // (stream order); tell every peer it may write into them.
+    if (multi && c == 0 && t < P.G && t != g) {
+        CtsSlot *slot = &P.sym[t]->cts[g];
+        if (P.recv_from_cts) { slot->win = P.recv_win[g]; slot->off = P.recv_off[g]; }
+        __threadfence_system();
+        st_release_sys(&slot->epoch, P.epoch);
+    }
+    __syncthreads();
+
+    for (int s = 0; s < prog.nsteps; s++) {
+        const Step st = prog.steps[s];
+        if (multi) {
+            // data written into this GPU by peers in step s-1 (slice c) must have landed
+            if (s > 0 && prog.steps[s - 1].wait_mask)
+                wait_mask_ge(P, S, prog.steps[s - 1].wait_mask, &P.sym[g]->flags[0][c], kMaxCtas,
+                             (P.epoch << 8) | (uint64_t)s);
+            // peers written in this step must have cleared us to send in this epoch
+            uint32_t need = st.signal_mask & ~S.cts_ok;
+            if (need) {
+                wait_mask_ge(P, S, need, &P.sym[g]->cts[0].epoch, sizeof(CtsSlot) / 8, P.epoch);
+                if (P.recv_from_cts && t < 32 && ((need >> t) & 1u)) {
+                    const CtsSlot *cs = &P.sym[g]->cts[t];
+                    S.recv_base[t] = P.win_table[t * kMaxWindows + cs->win] + cs->off;
+                }
+            }
+            __syncthreads();
+            if (t == 0) S.cts_ok |= need;
+            if (S.abort_flag) return;
+        }
+        // ---- the moves of this step, slice c of each; staggered start per CTA ----
+        const int nm = st.move_end - st.move_begin;
+        int small_idx = 0;
+        for (int q = 0; q < nm; q++) {
+            const Move m = prog.moves[st.move_begin + (q + c) % nm];
+            const uint64_t nbytes = (uint64_t)m.len * P.unit;
+            uint64_t lo, hi;
+            slice_of(nbytes, c, nC, lo, hi);
+            if (hi <= lo) continue;
+            const uint64_t n = hi - lo;
+            const bool big = n >= kCtaCopyMin;
+            if (!big) {
+                int mine = (small_idx++ % kWarps) == warp;
+                if (!mine) continue;
+            }
+            const char *src = base_of(P, S, m.src_kind, m.src_rank) + (uint64_t)m.src_off * P.unit + lo;
+            const uint64_t doff = (uint64_t)m.dst_off * P.unit + lo;
+            const bool ro = m.src_kind == BK_SEND;
+            if (!m.fanout) {
+                char *dst = base_of(P, S, m.dst_kind, m.dst_rank) + doff;
+                if (big) copy_slice1<8, kThreads>(dst, src, n, ro, t);
+                else     copy_slice1<4, 32>(dst, src, n, ro, lane);
+            } else {
+                char *dsts[8];
+                for (int j0 = 0; j0 < P.p; j0 += 8) {
+                    int nd = min(8, P.p - j0);
+                    for (int k = 0; k < nd; k++) dsts[k] = base_of(P, S, m.dst_kind, j0 + k) + doff;
+                    if (big) copy_slice_fan<4, kThreads>(dsts, nd, src, n, ro, t);
+                    else     copy_slice_fan<2, 32>(dsts, nd, src, n, ro, lane);
+                }
+            }
+        }
+        __syncthreads();
+        // ---- signal the peers written in this step (slice c) ----
+        if (multi && st.signal_mask && t < 32 && ((st.signal_mask >> t) & 1u)) {
+            __threadfence_system();
+            st_release_sys(&P.sym[t]->flags[g][c], (P.epoch << 8) | (uint64_t)(s + 1));
+        }
+    }
+    // completion: everything peers write into this GPU in the last step has landed
+    if (multi && prog.nsteps > 0 && prog.steps[prog.nsteps - 1].wait_mask) {
+        wait_mask_ge(P, S, prog.steps[prog.nsteps - 1].wait_mask, &P.sym[g]->flags[0][c], kMaxCtas,
+                     (P.epoch << 8) | (uint64_t)prog.nsteps);
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// A2: counts exchange + exclusive scan, all ranks on this device (single-process mode).
+//   recvcounts[r*p + j] = sendcounts[j*p + r];  rdispls[r*p + j] = sum_{i<j} recvcounts[r*p+i]
+// One warp per receiving rank r, 32 entries per iteration, carry across iterations.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ int64_t warp_incl_scan(int64_t v, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int64_t y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+    }
+    return v;
+}
+
+__global__ void mpxa_counts_kernel(const int64_t *__restrict__ sendcounts, int64_t *__restrict__ recvcounts,
+                                   int64_t *__restrict__ rdispls, int p, int r0, int nr) {
+    int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (warp >= nr) return;
+    int r = r0 + warp;                  // global receiving rank
+    int64_t carry = 0;
+    for (int j0 = 0; j0 < p; j0 += 32) {
+        int j = j0 + lane;
+        int64_t v = j < p ? sendcounts[(int64_t)j * p + r] : 0;
+        int64_t inc = warp_incl_scan(v, lane);
+        if (j < p) {
+            recvcounts[(int64_t)warp * p + j] = v;
+            rdispls[(int64_t)warp * p + j] = carry + inc - v;
+        }
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+}
+
+// exclusive scan of nr rows of p entries (rows already gathered into `counts`)
+__global__ void mpxa_scan_kernel(const int64_t *__restrict__ counts, int64_t *__restrict__ recvcounts,
+                                 int64_t *__restrict__ rdispls, int p, int nr) {
+    int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (warp >= nr) return;
+    int64_t carry = 0;
+    for (int j0 = 0; j0 < p; j0 += 32) {
+        int j = j0 + lane;
+        int64_t v = j < p ? counts[(int64_t)warp * p + j] : 0;
+        int64_t inc = warp_incl_scan(v, lane);
+        if (j < p) {
+            recvcounts[(int64_t)warp * p + j] = v;
+            rdispls[(int64_t)warp * p + j] = carry + inc - v;
+        }
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// host-side launchers (called from api.cpp)
+// ------------------------------------------------------------------------------------
+cudaError_t launch_exec(const ExecParams &P, int nC, int nG, bool cooperative, cudaStream_t stream) {
+    dim3 grid(nC, nG), block(kThreads);
+    if (cooperative) {
+        void *args[] = {(void *)&P};
+        return cudaLaunchCooperativeKernel((const void *)mpxa_exec_kernel, grid, block, args, 0, stream);
+    }
+    mpxa_exec_kernel<<<grid, block, 0, stream>>>(P);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_counts(const int64_t *sc, int64_t *rc, int64_t *rd, int p, int r0, int nr,
+                          cudaStream_t stream) {
+    int threads = 256, warps_per = threads / 32;
+    int blocks = (nr + warps_per - 1) / warps_per;
+    if (blocks < 1) blocks = 1;
+    mpxa_counts_kernel<<<blocks, threads, 0, stream>>>(sc, rc, rd, p, r0, nr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scan(const int64_t *counts, int64_t *rc, int64_t *rd, int p, int nr,
+                        cudaStream_t stream) {
+    int threads = 256, warps_per = threads / 32;
+    int blocks = (nr + warps_per - 1) / warps_per;
+    if (blocks < 1) blocks = 1;
+    mpxa_scan_kernel<<<blocks, threads, 0, stream>>>(counts, rc, rd, p, nr);
+    return cudaGetLastError();
+}
+
+int exec_max_ctas_per_sm() {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mpxa_exec_kernel, kThreads, 0);
+    return n;
+}
+
+}  // namespace mpxa

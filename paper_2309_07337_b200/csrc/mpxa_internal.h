@@ -1,0 +1,95 @@
+// Internal types shared by the host runtime (comm.cpp, plan.cpp, api.cpp) and the sm_100a
+// kernels (kernels.cu).  Not part of the C ABI (include/mpxa.h).
+//
+// Execution model: every collective call is compiled, on the host, into a
+// PROGRAM per GPU: a list of STEPS, each a list of MOVES (byte copies between rank
+// buffers, possibly on a peer GPU).  One kernel launch executes the whole program.  CTA c
+// of a GPU owns "column slice" c of every unit (block / segment) that moves, through all
+// steps, so a step's inputs written by this GPU were written by the same CTA and only a
+// __syncthreads separates steps; inputs written by a peer GPU were written by the peer's
+// CTA c, which signals a per-(src GPU, CTA) flag that this CTA acquires.  No grid-wide
+// barrier is ever needed.
+#pragma once
+#include <stdint.h>
+
+namespace mpxa {
+
+constexpr int kMaxGpus = 32;       // processes or virtual GPUs per comm (signal masks are 32-bit)
+constexpr int kMaxCtas = 1024;     // CTAs per GPU per launch (flag slots per source GPU)
+constexpr int kThreads = 512;      // threads per CTA of the executor kernel
+constexpr int kMaxWindows = 16;    // registered recv windows per process
+
+enum BufKind : uint8_t { BK_SEND = 0, BK_RECV = 1, BK_WORK = 2 };
+
+// One copy of `len` units from (src_kind, src_rank, src_off) to (dst_kind, dst_rank, dst_off).
+// Offsets and lengths are in UNITS of ExecParams::unit bytes.  fanout = 1: copy to the
+// dst_kind buffer of EVERY rank at dst_off (allgather direct); dst_rank is ignored.
+struct Move {
+    int64_t src_off;
+    int64_t dst_off;
+    int64_t len;
+    uint16_t src_rank;
+    uint16_t dst_rank;
+    uint8_t src_kind;
+    uint8_t dst_kind;
+    uint8_t fanout;
+    uint8_t pad;
+};
+static_assert(sizeof(Move) == 32, "Move layout");
+
+struct Step {
+    int32_t move_begin;     // [move_begin, move_end) in the GPU's move array
+    int32_t move_end;
+    uint32_t signal_mask;   // remote GPUs this GPU writes to in this step
+    uint32_t wait_mask;     // remote GPUs that write into this GPU in this step
+    int64_t total_len;      // sum of move lengths in units (host-side sizing)
+    int64_t max_len;        // max move length in units (host-side path hints)
+};
+static_assert(sizeof(Step) == 32, "Step layout");
+
+struct GpuProg {
+    const Step *steps;
+    const Move *moves;
+    int32_t nsteps;
+    int32_t nmoves;
+};
+
+// Clear-to-send message from receiver GPU d to sender GPU s, stored in s's region.
+struct CtsSlot {
+    uint64_t epoch;         // written last, with release semantics
+    uint64_t win;           // registered window of d's recvbuf (recv_from_cts mode)
+    uint64_t off;           // byte offset of d's recvbuf in that window
+    uint64_t pad;
+};
+
+// Per-GPU symmetric region (device memory, IPC-exported in multi-process mode).
+struct SymRegion {
+    CtsSlot cts[kMaxGpus];                    // cts[d]: receiver d cleared this GPU to send
+    uint64_t flags[kMaxGpus][kMaxCtas];       // flags[s][c]: src GPU s, CTA c, (epoch<<8)|(step+1)
+};
+
+struct ExecParams {
+    const GpuProg *progs;      // device array [G] (only progs[my_gpu] used in multi-process)
+    int32_t G;                 // GPUs (processes or virtual)
+    int32_t R;                 // ranks per GPU
+    int32_t p;                 // ranks
+    int32_t my_gpu;            // -1: emulated, GPU = blockIdx.y
+    uint64_t unit;             // bytes per unit
+    uint64_t epoch;            // > 0, increases by one per launch on the comm
+    uint64_t send_stride;      // bytes between consecutive local ranks' buffers
+    uint64_t recv_stride;
+    uint64_t work_stride;
+    char *send_base[kMaxGpus]; // per GPU: buffer of its first local rank (mapped here)
+    char *recv_base[kMaxGpus];
+    char *work_base[kMaxGpus];
+    SymRegion *sym[kMaxGpus];  // per GPU symmetric region (mapped here)
+    uint64_t recv_win[kMaxGpus];  // per GPU: window index of its recvbuf (recv_from_cts mode)
+    uint64_t recv_off[kMaxGpus];  // per GPU: byte offset of its recvbuf in that window
+    char *const *win_table;    // device [G][kMaxWindows] window bases (recv_from_cts mode)
+    int32_t recv_from_cts;     // remote RECV bases come from the CTS message
+    int32_t pad0;
+    int32_t *err;              // host-mapped error word (watchdog)
+    int64_t timeout_ns;
+};
+
+}  // namespace mpxa

@@ -1,0 +1,314 @@
+// Schedule builders.  Each builder emits the steps of
+// the paper-family algorithm as moves executed by the GPU that owns the SOURCE rank (push
+// model: payload crosses NVLink as stores into the peer's buffer).  A move never
+// concatenates units that later moves split, so the column slice a CTA owns is the same
+// byte range of a block in every step (mpxa_exec_kernel's ownership rule).
+#include "plan.h"
+
+#include <algorithm>
+
+namespace mpxa {
+
+int ceil_log2(int p) {
+    int k = 0;
+    while ((1 << k) < p) k++;
+    return k;
+}
+
+static inline int imod(int64_t a, int p) {
+    int64_t r = a % p;
+    return (int)(r < 0 ? r + p : r);
+}
+
+namespace {
+
+class Builder {
+public:
+    Builder(Program &P, int p, int R, int G) : P_(P), p_(p), R_(R), G_(G) {
+        P_ = Program();
+        P_.p = p; P_.R = R; P_.G = G;
+        P_.steps.assign(G, {});
+        P_.moves.assign(G, {});
+        cur_.assign(G, {});
+    }
+    void move(int sk, int sr, int64_t so, int dk, int dr, int64_t dof, int64_t len, int fan = 0) {
+        if (len <= 0) return;
+        Move m{};
+        m.src_off = so; m.dst_off = dof; m.len = len;
+        m.src_rank = (uint16_t)sr; m.dst_rank = (uint16_t)dr;
+        m.src_kind = (uint8_t)sk; m.dst_kind = (uint8_t)dk; m.fanout = (uint8_t)fan;
+        cur_[sr / R_].push_back(m);
+    }
+    void end_step() {
+        std::vector<uint32_t> sig(G_, 0), wt(G_, 0);
+        for (int g = 0; g < G_; g++)
+            for (const Move &m : cur_[g]) {
+                if (m.fanout) {
+                    for (int d = 0; d < G_; d++)
+                        if (d != g) { sig[g] |= 1u << d; wt[d] |= 1u << g; }
+                } else {
+                    int d = m.dst_rank / R_;
+                    if (d != g) { sig[g] |= 1u << d; wt[d] |= 1u << g; }
+                }
+            }
+        for (int g = 0; g < G_; g++) {
+            Step s{};
+            s.move_begin = (int32_t)P_.moves[g].size();
+            int64_t tot = 0, mx = 0;
+            for (const Move &m : cur_[g]) {
+                P_.moves[g].push_back(m);
+                tot += m.len * (m.fanout ? p_ : 1);
+                mx = std::max(mx, m.len);
+            }
+            s.move_end = (int32_t)P_.moves[g].size();
+            s.signal_mask = sig[g];
+            s.wait_mask = wt[g];
+            s.total_len = tot;
+            s.max_len = mx;
+            P_.steps[g].push_back(s);
+            P_.max_move = std::max(P_.max_move, mx);
+            P_.max_step_units = std::max(P_.max_step_units, tot);
+            P_.signals += __builtin_popcount(sig[g]);
+            cur_[g].clear();
+        }
+    }
+    int gpu(int r) const { return r / R_; }
+
+private:
+    Program &P_;
+    int p_, R_, G_;
+    std::vector<std::vector<Move>> cur_;
+};
+
+bool topo_ok(int p, int R, int G) {
+    return p >= 1 && R >= 1 && G >= 1 && G <= kMaxGpus && p == R * G && p <= 65535;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------
+// alltoall
+// ---------------------------------------------------------------------------------------
+bool build_alltoall(Program &P, int algo, int p, int R, int G, int g, int stop_stage) {
+    if (!topo_ok(p, R, G)) return false;
+    Builder B(P, p, R, G);
+    if (algo == A_PAIRWISE) {
+        // A3: step s sends to (r+s) mod p; all s run concurrently on the GPU.
+        for (int s = 0; s < p; s++)
+            for (int t = 0; t < p; t++) {
+                int j = imod(s + t, p);
+                B.move(BK_SEND, s, j, BK_RECV, j, s, 1);
+            }
+        B.end_step();
+        P.work_units = 0;
+        return true;
+    }
+    if (algo == A_BRUCK) {
+        // A4-A6: T_r[i] = send_r[(r+i) mod p]; rounds k: blocks with bit k of i set go to
+        // (r+2^k) mod p (packed into the peer's round-k staging, then unpacked into T at
+        // the same index); recv_r[j] = T_r[(r-j) mod p].
+        const int K = ceil_log2(p);
+        std::vector<int64_t> soff(K + 1, p);
+        for (int k = 0; k < K; k++) {
+            int64_t mk = 0;
+            for (int i = 0; i < p; i++) mk += (i >> k) & 1;
+            soff[k + 1] = soff[k] + mk;
+        }
+        P.work_units = soff[K];
+        const int rounds = stop_stage < 0 ? K : std::min(stop_stage, K);
+        for (int r = 0; r < p; r++)                          // A4 local rotation
+            for (int i = 0; i < p; i++) B.move(BK_SEND, r, imod(r + i, p), BK_WORK, r, i, 1);
+        B.end_step();
+        for (int k = 0; k < rounds; k++) {                   // A5 bit-indexed rounds
+            const int d = 1 << k;
+            for (int r = 0; r < p; r++) {
+                int64_t pos = 0;
+                for (int i = 0; i < p; i++)
+                    if ((i >> k) & 1) B.move(BK_WORK, r, i, BK_WORK, imod(r + d, p), soff[k] + pos++, 1);
+            }
+            B.end_step();
+            for (int r = 0; r < p; r++) {
+                int64_t pos = 0;
+                for (int i = 0; i < p; i++)
+                    if ((i >> k) & 1) B.move(BK_WORK, r, soff[k] + pos++, BK_WORK, r, i, 1);
+            }
+            B.end_step();
+        }
+        if (stop_stage < 0) {                                // A6 inverse rotation
+            for (int r = 0; r < p; r++)
+                for (int j = 0; j < p; j++) B.move(BK_WORK, r, imod(r - j, p), BK_RECV, r, j, 1);
+        } else {                                             // dump T for stage tests
+            for (int r = 0; r < p; r++)
+                for (int i = 0; i < p; i++) B.move(BK_WORK, r, i, BK_RECV, r, i, 1);
+        }
+        B.end_step();
+        return true;
+    }
+    if (algo == A_HIER) {
+        if (g < 1 || p % g) return false;
+        std::vector<int64_t> c((size_t)p * p, 1), sd((size_t)p * p), rd((size_t)p * p);
+        for (int s = 0; s < p; s++)
+            for (int j = 0; j < p; j++) { sd[(size_t)s * p + j] = j; rd[(size_t)j * p + s] = s; }
+        return build_alltoallv(P, A_HIER, p, R, G, g, c.data(), sd.data(), rd.data());
+    }
+    return false;
+}
+
+// ---------------------------------------------------------------------------------------
+// allgather
+// ---------------------------------------------------------------------------------------
+bool build_allgather(Program &P, int algo, int p, int R, int G, int stop_stage) {
+    if (!topo_ok(p, R, G)) return false;
+    Builder B(P, p, R, G);
+    if (algo == A_PAIRWISE) {
+        // direct: read send_s once, store it into block s of every rank's recvbuf
+        for (int s = 0; s < p; s++) B.move(BK_SEND, s, 0, BK_RECV, 0, s, 1, /*fanout=*/1);
+        B.end_step();
+        return true;
+    }
+    if (algo == A_RING) {
+        // recv_r[r] = send_r; step s: r sends block (r-s) mod p to r+1.
+        for (int r = 0; r < p; r++) {
+            B.move(BK_SEND, r, 0, BK_RECV, r, r, 1);
+            if (p > 1) B.move(BK_SEND, r, 0, BK_RECV, imod(r + 1, p), r, 1);
+        }
+        B.end_step();
+        for (int s = 1; s < p - 1; s++) {
+            for (int r = 0; r < p; r++) {
+                int b = imod(r - s, p);
+                B.move(BK_RECV, r, b, BK_RECV, imod(r + 1, p), b, 1);
+            }
+            B.end_step();
+        }
+        return true;
+    }
+    if (algo == A_BRUCK) {
+        // T_r[0] = send_r; round k sends T_r[0..n_k) to (r-2^k) mod p,
+        // stored at T[2^k..2^k+n_k); recv_r[j] = T_r[(j-r) mod p].
+        const int K = ceil_log2(p);
+        P.work_units = p;
+        const int rounds = stop_stage < 0 ? K : std::min(stop_stage, K);
+        for (int r = 0; r < p; r++) B.move(BK_SEND, r, 0, BK_WORK, r, 0, 1);
+        B.end_step();
+        for (int k = 0; k < rounds; k++) {
+            const int d = 1 << k, nk = std::min(d, p - d);
+            for (int r = 0; r < p; r++)
+                for (int i = 0; i < nk; i++) B.move(BK_WORK, r, i, BK_WORK, imod(r - d, p), d + i, 1);
+            B.end_step();
+        }
+        if (stop_stage < 0) {
+            for (int r = 0; r < p; r++)
+                for (int j = 0; j < p; j++) B.move(BK_WORK, r, imod(j - r, p), BK_RECV, r, j, 1);
+        } else {
+            int filled = std::min(1 << rounds, p);
+            for (int r = 0; r < p; r++)
+                for (int i = 0; i < filled; i++) B.move(BK_WORK, r, i, BK_RECV, r, i, 1);
+        }
+        B.end_step();
+        return true;
+    }
+    return false;
+}
+
+// ---------------------------------------------------------------------------------------
+// alltoallv
+// ---------------------------------------------------------------------------------------
+bool build_alltoallv(Program &P, int algo, int p, int R, int G, int g, const int64_t *c,
+                     const int64_t *sd, const int64_t *rd) {
+    if (!topo_ok(p, R, G)) return false;
+    auto C = [&](int s, int j) { return c[(size_t)s * p + j]; };
+    auto SD = [&](int s, int j) { return sd[(size_t)s * p + j]; };
+    auto RD = [&](int j, int s) { return rd[(size_t)j * p + s]; };
+    if (algo == A_PAIRWISE) {
+        Builder B(P, p, R, G);
+        for (int s = 0; s < p; s++)
+            for (int t = 0; t < p; t++) {
+                int j = imod(s + t, p);
+                B.move(BK_SEND, s, SD(s, j), BK_RECV, j, RD(j, s), C(s, j));
+            }
+        B.end_step();
+        P.work_units = 0;
+        return true;
+    }
+    if (algo != A_HIER) return false;
+    if (g < 1 || p % g) return false;
+    // A8: groups of g consecutive ranks, leader
+    // L(A,B) = A*g + (B mod g); aggregated message segments ordered (s,t) row-major.
+    const int NG = p / g;
+    auto L = [&](int A, int Bg) { return A * g + (Bg % g); };
+    auto pair_units = [&](int A, int Bg) {
+        int64_t n = 0;
+        for (int s = 0; s < g; s++)
+            for (int t = 0; t < g; t++) n += C(A * g + s, Bg * g + t);
+        return n;
+    };
+    // work layout of every rank: first the out-aggregates it leads, then the in-aggregates
+    std::vector<int64_t> out_off((size_t)NG * NG, -1), in_off((size_t)NG * NG, -1);
+    int64_t work = 0;
+    for (int x = 0; x < p; x++) {
+        int64_t cur = 0;
+        int A = x / g;
+        for (int Bg = 0; Bg < NG; Bg++)
+            if (Bg != A && L(A, Bg) == x) { out_off[(size_t)A * NG + Bg] = cur; cur += pair_units(A, Bg); }
+        for (int A2 = 0; A2 < NG; A2++)   // x receives pair (A2 -> A) when L(A, A2) == x
+            if (A2 != A && L(A, A2) == x) { in_off[(size_t)A2 * NG + A] = cur; cur += pair_units(A2, A); }
+        work = std::max(work, cur);
+    }
+    auto segoff = [&](int A, int Bg, int s, int t) {
+        int64_t o = 0;
+        for (int s2 = 0; s2 < g; s2++)
+            for (int t2 = 0; t2 < g; t2++) {
+                if (s2 == s && t2 == t) return o;
+                o += C(A * g + s2, Bg * g + t2);
+            }
+        return o;
+    };
+    Builder B(P, p, R, G);
+    P.work_units = work;
+    // step 1: intra-group direct + gather to leaders
+    for (int r = 0; r < p; r++) {
+        int A = r / g, s = r % g;
+        for (int t = 0; t < g; t++) {
+            int j = A * g + t;
+            B.move(BK_SEND, r, SD(r, j), BK_RECV, j, RD(j, r), C(r, j));
+        }
+        for (int Bg = 0; Bg < NG; Bg++) {
+            if (Bg == A) continue;
+            int lead = L(A, Bg);
+            for (int t = 0; t < g; t++) {
+                int j = Bg * g + t;
+                B.move(BK_SEND, r, SD(r, j), BK_WORK, lead, out_off[(size_t)A * NG + Bg] + segoff(A, Bg, s, t), C(r, j));
+            }
+        }
+    }
+    B.end_step();
+    // step 2: one aggregated exchange per group pair (segment-wise moves, one signal)
+    for (int A = 0; A < NG; A++)
+        for (int Bg = 0; Bg < NG; Bg++) {
+            if (Bg == A) continue;
+            int lead = L(A, Bg), peer = L(Bg, A);
+            for (int s = 0; s < g; s++)
+                for (int t = 0; t < g; t++) {
+                    int64_t o = segoff(A, Bg, s, t);
+                    B.move(BK_WORK, lead, out_off[(size_t)A * NG + Bg] + o, BK_WORK, peer,
+                           in_off[(size_t)A * NG + Bg] + o, C(A * g + s, Bg * g + t));
+                }
+        }
+    B.end_step();
+    // step 3: redistribute segment (s,t) to rank Bg*g+t at rdispls[A*g+s]
+    for (int Bg = 0; Bg < NG; Bg++)
+        for (int A = 0; A < NG; A++) {
+            if (A == Bg) continue;
+            int lead = L(Bg, A);
+            for (int s = 0; s < g; s++)
+                for (int t = 0; t < g; t++) {
+                    int dst = Bg * g + t, src = A * g + s;
+                    B.move(BK_WORK, lead, in_off[(size_t)A * NG + Bg] + segoff(A, Bg, s, t), BK_RECV, dst,
+                           RD(dst, src), C(src, dst));
+                }
+        }
+    B.end_step();
+    return true;
+}
+
+}  // namespace mpxa

@@ -1,0 +1,38 @@
+// Schedule builders: compile one collective call into a per-GPU program of steps and moves
+// (mpxa_internal.h).  Pure host logic, no CUDA calls -- exported for CPU tests through
+// mpxa_plan_* in api.cpp.
+#pragma once
+#include <stdint.h>
+
+#include <vector>
+
+#include "mpxa_internal.h"
+
+namespace mpxa {
+
+struct Program {
+    int p = 0, R = 1, G = 1;
+    std::vector<std::vector<Step>> steps;  // [G][nsteps]
+    std::vector<std::vector<Move>> moves;  // [G][...]
+    int64_t work_units = 0;                // WORK units needed per rank
+    int64_t max_move = 0;                  // longest move (units)
+    int64_t max_step_units = 0;            // max over (GPU, step) of the summed move units
+    int64_t signals = 0;                   // inter-GPU signals per launch (GPU-pair messages)
+    int nsteps() const { return steps.empty() ? 0 : (int)steps[0].size(); }
+};
+
+enum Algo { A_DEFAULT = 0, A_PAIRWISE = 1, A_BRUCK = 2, A_HIER = 3, A_RING = 4 };
+
+// Uniform ops: units are blocks (count * dtype_size bytes).
+//   stop_stage: -1 complete; >= 0 truncated Bruck ending with a T dump into RECV.
+bool build_alltoall(Program &P, int algo, int p, int R, int G, int g, int stop_stage);
+bool build_allgather(Program &P, int algo, int p, int R, int G, int stop_stage);
+// v-op: units are elements.  c, sd, rd are FULL p x p matrices:
+//   c[s*p+j]  = elements rank s sends to j, sd[s*p+j] its displacement in s's sendbuf,
+//   rd[j*p+s] = displacement in j's recvbuf of the segment from s.
+bool build_alltoallv(Program &P, int algo, int p, int R, int G, int g, const int64_t *c,
+                     const int64_t *sd, const int64_t *rd);
+
+int ceil_log2(int p);
+
+}  // namespace mpxa

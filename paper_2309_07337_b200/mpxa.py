@@ -1,0 +1,395 @@
+"""Thin Python binding over libmpxa.so (include/mpxa.h, include/mpxa_plan.h).
+
+Argument marshalling only: every step of every collective runs in the library's sm_100a
+kernels.  PyTorch supplies device memory (tensors), streams and -- for multi-process
+communicators -- the process group used by the bootstrap all-gather.  There is no CPU or
+PyTorch fallback: if libmpxa.so is missing the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmpxa.so")
+
+# ---- constants (mirror include/mpxa.h) ------------------------------------------------
+SUCCESS, ERR_ARG, ERR_ALGO, ERR_LIFECYCLE, ERR_TOPOLOGY, ERR_MISMATCH, ERR_CUDA, ERR_TIMEOUT, \
+    ERR_NOMEM, ERR_UNREGISTERED = range(10)
+OP_ALLTOALL, OP_ALLTOALLV, OP_ALLGATHER = 0, 1, 2
+ALGO = {"default": 0, "pairwise": 1, "bruck": 2, "hier": 3, "ring": 4}
+ALGO_NAME = {v: k for k, v in ALGO.items()}
+OPS = {"alltoall": OP_ALLTOALL, "alltoallv": OP_ALLTOALLV, "allgather": OP_ALLGATHER}
+
+
+class MpxaError(RuntimeError):
+    def __init__(self, status: int, what: str = ""):
+        self.status = status
+        msg = _lib().mpxa_error_string(status).decode() if _LIB is not None else str(status)
+        super().__init__(f"{what}: mpxa status {status} ({msg})")
+
+
+BOOT_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+
+
+class InitArgs(ctypes.Structure):
+    _fields_ = [("nprocs", ctypes.c_int), ("proc", ctypes.c_int), ("ranks_per_proc", ctypes.c_int),
+                ("device", ctypes.c_int), ("group_size", ctypes.c_int), ("emulate_gpus", ctypes.c_int),
+                ("bootstrap_allgather", BOOT_FN), ("ctx", ctypes.c_void_p),
+                ("heap_bytes", ctypes.c_size_t), ("timeout_s", ctypes.c_double)]
+
+
+class PlanMove(ctypes.Structure):
+    _fields_ = [("src_off", ctypes.c_int64), ("dst_off", ctypes.c_int64), ("len", ctypes.c_int64),
+                ("src_rank", ctypes.c_uint16), ("dst_rank", ctypes.c_uint16),
+                ("src_kind", ctypes.c_uint8), ("dst_kind", ctypes.c_uint8),
+                ("fanout", ctypes.c_uint8), ("pad", ctypes.c_uint8)]
+
+
+class PlanStep(ctypes.Structure):
+    _fields_ = [("move_begin", ctypes.c_int32), ("move_end", ctypes.c_int32),
+                ("signal_mask", ctypes.c_uint32), ("wait_mask", ctypes.c_uint32),
+                ("total_len", ctypes.c_int64), ("max_len", ctypes.c_int64)]
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in
+                ("nsteps", "work_units", "max_move", "max_step_units", "signals", "total_moves")]
+
+
+# every symbol of include/mpxa.h and include/mpxa_plan.h, with its ctypes signature
+_P, _I, _Z, _U64P = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t, ctypes.POINTER(ctypes.c_uint64)
+SIGNATURES = {
+    "mpxa_init": ([_P, ctypes.POINTER(InitArgs)], _I),
+    "mpxa_finalize": ([_P], _I),
+    "mpxa_comm_size": ([_P, ctypes.POINTER(_I)], _I),
+    "mpxa_comm_rank0": ([_P, ctypes.POINTER(_I)], _I),
+    "mpxa_comm_check": ([_P], _I),
+    "mpxa_launch_count": ([_P, _U64P], _I),
+    "mpxa_register": ([_P, _P, _Z], _I),
+    "mpxa_deregister": ([_P, _P], _I),
+    "mpxa_alltoall": ([_P, _Z, _Z, _P, _P, _P], _I),
+    "mpxa_allgather": ([_P, _Z, _Z, _P, _P, _P], _I),
+    "mpxa_alltoallv": ([_P, _P, _P, _Z, _P, _P, _P, _Z, _Z, _P, _P], _I),
+    "mpxa_alltoall_algo": ([_P, _Z, _Z, _P, _I, _P, _P], _I),
+    "mpxa_allgather_algo": ([_P, _Z, _Z, _P, _I, _P, _P], _I),
+    "mpxa_alltoallv_algo": ([_P, _P, _P, _Z, _P, _P, _P, _Z, _Z, _I, _P, _P], _I),
+    "mpxa_alltoallv_counts": ([_P, _P, _P, _P, _P], _I),
+    "mpxa_alltoall_bruck_stage": ([_P, _Z, _Z, _P, _I, _P, _P], _I),
+    "mpxa_allgather_bruck_stage": ([_P, _Z, _Z, _P, _I, _P, _P], _I),
+    "mpxa_alltoall_init": ([_P, _Z, _Z, _P, _I, _P, _P, _P], _I),
+    "mpxa_allgather_init": ([_P, _Z, _Z, _P, _I, _P, _P, _P], _I),
+    "mpxa_alltoallv_init": ([_P, _P, _P, _Z, _P, _P, _P, _Z, _Z, _I, _P, _P, _P], _I),
+    "mpxa_start": ([_P, _P], _I),
+    "mpxa_wait": ([_P, _P], _I),
+    "mpxa_request_free": ([_P], _I),
+    "mpxa_request_algorithm": ([_P, ctypes.POINTER(_I)], _I),
+    "mpxa_set_algorithm": ([_P, _I, _I], _I),
+    "mpxa_get_algorithm": ([_P, _I, _Z, ctypes.POINTER(_I)], _I),
+    "mpxa_list_algorithms": ([_I, ctypes.POINTER(_I), ctypes.POINTER(_I)], _I),
+    "mpxa_load_selector": ([_P, ctypes.c_char_p], _I),
+    "mpxa_error_string": ([_I], ctypes.c_char_p),
+    "mpxa_algo_name": ([_I], ctypes.c_char_p),
+    "mpxa_plan_build": ([_I, _I, _I, _I, _I, _I, _I, _P, _P, _P, ctypes.POINTER(_P)], _I),
+    "mpxa_plan_info": ([_P, ctypes.POINTER(PlanInfo)], _I),
+    "mpxa_plan_steps": ([_P, _I, _P, ctypes.POINTER(_I)], _I),
+    "mpxa_plan_moves": ([_P, _I, _P, ctypes.POINTER(_I)], _I),
+    "mpxa_plan_free": ([_P], _I),
+}
+
+_LIB = None
+
+
+def _lib():
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"libmpxa.so not built at {LIB_PATH}: run `python __graft_entry__.py` "
+                              "(build()) -- there is no fallback implementation")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (args, res) in SIGNATURES.items():
+            f = getattr(lib, name)
+            f.argtypes = args
+            f.restype = res
+        _LIB = lib
+    return _LIB
+
+
+def lib():
+    return _lib()
+
+
+def _ck(status: int, what: str):
+    if status != SUCCESS:
+        raise MpxaError(status, what)
+
+
+def _algo(a) -> int:
+    if a is None:
+        return 0
+    return ALGO[a] if isinstance(a, str) else int(a)
+
+
+def _stream(stream) -> int:
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def _host_i64(a):
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.int64))
+    return a, a.ctypes.data_as(ctypes.c_void_p)
+
+
+def list_algorithms(op: str):
+    n = ctypes.c_int(8)
+    out = (ctypes.c_int * 8)()
+    _ck(_lib().mpxa_list_algorithms(OPS[op], out, ctypes.byref(n)), "list_algorithms")
+    return [ALGO_NAME[out[i]] for i in range(n.value)]
+
+
+class Request:
+    """Persistent collective (MPIX_Request analog): start()/wait() any number of times."""
+
+    def __init__(self, comm: "Comm", handle: int, keep):
+        self.comm = comm
+        self.handle = ctypes.c_void_p(handle)
+        self._keep = keep   # keep bound tensors / host arrays alive
+
+    def start(self, stream=None):
+        _ck(_lib().mpxa_start(self.handle, _stream(stream)), "start")
+
+    def wait(self, stream=None):
+        _ck(_lib().mpxa_wait(self.handle, _stream(stream)), "wait")
+
+    @property
+    def algorithm(self) -> str:
+        a = ctypes.c_int()
+        _ck(_lib().mpxa_request_algorithm(self.handle, ctypes.byref(a)), "request_algorithm")
+        return ALGO_NAME[a.value]
+
+    def free(self):
+        if self.handle:
+            h = ctypes.c_void_p(self.handle.value)
+            _ck(_lib().mpxa_request_free(ctypes.byref(h)), "request_free")
+            self.handle = None
+
+
+class Comm:
+    """MPIX_Comm analog.
+
+    Single process (pg None or world size 1): all p = ranks_per_proc ranks live on this
+    device; buffers are rank-major [R][per-rank].  emulate_gpus = G > 1 splits them over G
+    virtual GPUs that run the multi-GPU protocol (flags, CTS, peer-style stores) in one
+    cooperative launch.  Multi-process (pg with world size > 1): one process per GPU,
+    bootstrap all-gather over a gloo group.
+    """
+
+    def __init__(self, ranks_per_proc: int = 1, device: Optional[int] = None, group_size: int = 0,
+                 emulate_gpus: int = 0, pg=None, heap_bytes: int = 0, timeout_s: float = 0.0):
+        import torch
+        self.handle = ctypes.c_void_p()
+        nprocs, proc = 1, 0
+        self._boot = None
+        if pg is not None:
+            import torch.distributed as dist
+            nprocs, proc = dist.get_world_size(pg), dist.get_rank(pg)
+            if nprocs > 1:
+                gloo = pg if dist.get_backend(pg) == "gloo" else dist.new_group(backend="gloo")
+                self._boot = make_bootstrap(gloo, nprocs)
+        if device is None:
+            device = torch.cuda.current_device()
+        args = InitArgs(nprocs=nprocs, proc=proc, ranks_per_proc=ranks_per_proc, device=device,
+                        group_size=group_size, emulate_gpus=emulate_gpus,
+                        bootstrap_allgather=self._boot if self._boot else BOOT_FN(),
+                        ctx=None, heap_bytes=heap_bytes, timeout_s=timeout_s)
+        _ck(_lib().mpxa_init(ctypes.byref(self.handle), ctypes.byref(args)), "init")
+        self.R = ranks_per_proc
+        self.nprocs = nprocs
+        self.proc = proc
+        p = ctypes.c_int()
+        _ck(_lib().mpxa_comm_size(self.handle, ctypes.byref(p)), "comm_size")
+        self.p = p.value
+        self.device = device
+
+    # ---- introspection -------------------------------------------------------------
+    def launch_count(self) -> int:
+        n = ctypes.c_uint64()
+        _ck(_lib().mpxa_launch_count(self.handle, ctypes.byref(n)), "launch_count")
+        return n.value
+
+    def check(self) -> int:
+        return _lib().mpxa_comm_check(self.handle)
+
+    def set_algorithm(self, op: str, algo):
+        _ck(_lib().mpxa_set_algorithm(self.handle, OPS[op], _algo(algo)), "set_algorithm")
+
+    def get_algorithm(self, op: str, nbytes: int) -> str:
+        a = ctypes.c_int()
+        _ck(_lib().mpxa_get_algorithm(self.handle, OPS[op], nbytes, ctypes.byref(a)), "get_algorithm")
+        return ALGO_NAME[a.value]
+
+    def load_selector(self, path: str):
+        _ck(_lib().mpxa_load_selector(self.handle, path.encode()), "load_selector")
+
+    def register(self, t):
+        _ck(_lib().mpxa_register(self.handle, _ptr(t), t.numel() * t.element_size()), "register")
+
+    # ---- one-shot collectives ------------------------------------------------------
+    def _count(self, send, per_rank_blocks: int) -> int:
+        n = send.numel()
+        d = self.R * per_rank_blocks
+        if n % d:
+            raise ValueError(f"send numel {n} not divisible by R*blocks = {d}")
+        return n // d
+
+    def alltoall(self, send, recv, algo=None, stream=None, count: Optional[int] = None):
+        count = self._count(send, self.p) if count is None else count
+        _ck(_lib().mpxa_alltoall_algo(_ptr(send), count, send.element_size(), _ptr(recv), _algo(algo),
+                                      self.handle, _stream(stream)), "alltoall")
+
+    def allgather(self, send, recv, algo=None, stream=None, count: Optional[int] = None):
+        count = self._count(send, 1) if count is None else count
+        _ck(_lib().mpxa_allgather_algo(_ptr(send), count, send.element_size(), _ptr(recv), _algo(algo),
+                                       self.handle, _stream(stream)), "allgather")
+
+    def alltoallv(self, send, sendcounts, sdispls, recv, recvcounts, rdispls, algo=None, stream=None,
+                  dtype_size: Optional[int] = None):
+        w = send.element_size() if dtype_size is None else dtype_size
+        sc, scp = _host_i64(sendcounts)
+        sd, sdp = _host_i64(sdispls)
+        rc, rcp = _host_i64(recvcounts)
+        rd, rdp = _host_i64(rdispls)
+        sbpr = send.numel() * send.element_size() // self.R
+        rbpr = recv.numel() * recv.element_size() // self.R
+        _ck(_lib().mpxa_alltoallv_algo(_ptr(send), scp, sdp, sbpr, _ptr(recv), rcp, rdp, rbpr, w, _algo(algo),
+                                       self.handle, _stream(stream)), "alltoallv")
+
+    def alltoallv_counts(self, d_sendcounts, d_recvcounts, d_rdispls, stream=None):
+        _ck(_lib().mpxa_alltoallv_counts(_ptr(d_sendcounts), _ptr(d_recvcounts), _ptr(d_rdispls),
+                                         self.handle, _stream(stream)), "alltoallv_counts")
+
+    def alltoall_bruck_stage(self, send, T, stage: int, stream=None):
+        count = self._count(send, self.p)
+        _ck(_lib().mpxa_alltoall_bruck_stage(_ptr(send), count, send.element_size(), _ptr(T), stage,
+                                             self.handle, _stream(stream)), "alltoall_bruck_stage")
+
+    def allgather_bruck_stage(self, send, T, stage: int, stream=None):
+        count = self._count(send, 1)
+        _ck(_lib().mpxa_allgather_bruck_stage(_ptr(send), count, send.element_size(), _ptr(T), stage,
+                                              self.handle, _stream(stream)), "allgather_bruck_stage")
+
+    # ---- persistent forms ---------------------------------------------------------
+    def alltoall_init(self, send, recv, algo=None, count: Optional[int] = None) -> Request:
+        count = self._count(send, self.p) if count is None else count
+        h = ctypes.c_void_p()
+        _ck(_lib().mpxa_alltoall_init(_ptr(send), count, send.element_size(), _ptr(recv), _algo(algo),
+                                      self.handle, None, ctypes.byref(h)), "alltoall_init")
+        return Request(self, h.value, (send, recv))
+
+    def allgather_init(self, send, recv, algo=None, count: Optional[int] = None) -> Request:
+        count = self._count(send, 1) if count is None else count
+        h = ctypes.c_void_p()
+        _ck(_lib().mpxa_allgather_init(_ptr(send), count, send.element_size(), _ptr(recv), _algo(algo),
+                                       self.handle, None, ctypes.byref(h)), "allgather_init")
+        return Request(self, h.value, (send, recv))
+
+    def alltoallv_init(self, send, sendcounts, sdispls, recv, recvcounts, rdispls, algo=None,
+                       dtype_size: Optional[int] = None) -> Request:
+        w = send.element_size() if dtype_size is None else dtype_size
+        arrs = [_host_i64(a) for a in (sendcounts, sdispls, recvcounts, rdispls)]
+        sbpr = send.numel() * send.element_size() // self.R
+        rbpr = recv.numel() * recv.element_size() // self.R
+        h = ctypes.c_void_p()
+        _ck(_lib().mpxa_alltoallv_init(_ptr(send), arrs[0][1], arrs[1][1], sbpr, _ptr(recv), arrs[2][1],
+                                       arrs[3][1], rbpr, w, _algo(algo), self.handle, None,
+                                       ctypes.byref(h)), "alltoallv_init")
+        return Request(self, h.value, (send, recv))
+
+    def finalize(self):
+        if self.handle:
+            _ck(_lib().mpxa_finalize(self.handle), "finalize")
+            self.handle = None
+
+    def __del__(self):
+        try:
+            if self.handle:
+                _lib().mpxa_finalize(self.handle)
+        except Exception:
+            pass
+
+
+def make_bootstrap(group, nprocs: int):
+    """A C callback doing the bootstrap all-gather over a gloo process group."""
+    import torch
+    import torch.distributed as dist
+
+    def cb(inp, out, nbytes, ctx):
+        try:
+            src = torch.frombuffer(ctypes.string_at(inp, nbytes), dtype=torch.uint8).clone() if nbytes else \
+                torch.empty(0, dtype=torch.uint8)
+            outs = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(nprocs)]
+            dist.all_gather(outs, src, group=group)
+            buf = torch.cat(outs).numpy().tobytes()
+            ctypes.memmove(out, buf, len(buf))
+            return 0
+        except Exception:   # the library maps a non-zero return to an error status
+            return 1
+
+    return BOOT_FN(cb)
+
+
+# ---- host-only plan introspection (no GPU needed) ---------------------------------------
+class Plan:
+    """A compiled schedule (include/mpxa_plan.h), for CPU simulation in tests."""
+
+    def __init__(self, op: str, algo: str, p: int, R: int = 0, G: int = 1, g: int = 1, stop_stage: int = -1,
+                 counts=None, sdispls=None, rdispls=None):
+        R = R or p // G
+        h = ctypes.c_void_p()
+        keep = []
+        cp = sp = rp = None
+        if counts is not None:
+            (c, cp), (s, sp), (r, rp) = _host_i64(counts), _host_i64(sdispls), _host_i64(rdispls)
+            keep = [c, s, r]
+        _ck(_lib().mpxa_plan_build(OPS[op], ALGO[algo], p, R, G, g, stop_stage, cp, sp, rp, ctypes.byref(h)),
+            "plan_build")
+        self.h = h
+        self.p, self.R, self.G = p, R, G
+        self._keep = keep
+        info = PlanInfo()
+        _ck(_lib().mpxa_plan_info(h, ctypes.byref(info)), "plan_info")
+        self.info = {n: int(getattr(info, n)) for n, _ in PlanInfo._fields_}
+
+    def steps(self, gpu: int):
+        n = ctypes.c_int(0)
+        _ck(_lib().mpxa_plan_steps(self.h, gpu, None, ctypes.byref(n)), "plan_steps")
+        arr = (PlanStep * max(1, n.value))()
+        _ck(_lib().mpxa_plan_steps(self.h, gpu, arr, ctypes.byref(n)), "plan_steps")
+        return [arr[i] for i in range(n.value)]
+
+    def moves(self, gpu: int):
+        n = ctypes.c_int(0)
+        _ck(_lib().mpxa_plan_moves(self.h, gpu, None, ctypes.byref(n)), "plan_moves")
+        arr = (PlanMove * max(1, n.value))()
+        _ck(_lib().mpxa_plan_moves(self.h, gpu, arr, ctypes.byref(n)), "plan_moves")
+        return [arr[i] for i in range(n.value)]
+
+    def __del__(self):
+        try:
+            if self.h:
+                _lib().mpxa_plan_free(self.h)
+        except Exception:
+            pass

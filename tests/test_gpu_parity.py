@@ -1,0 +1,359 @@
+"""GPU parity: libmpxa (C ABI, sm_100a kernels) vs the CPU oracle, bit-exact (-m gpu).
+
+Inputs come from synth/ (seeded); expected values from oracle/ only.  Payloads are opaque
+bytes, so the bar is bit-exactness for every op, variant, size and topology, including
+ragged / misaligned sizes, zero counts, canaries outside received ranges, emulated
+multi-GPU protocol runs, Bruck intermediate states and persistent start/wait cycles.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2309_07337_b200 import Comm, MpxaError  # noqa: E402
+from paper_2309_07337_b200 import mpxa as M  # noqa: E402
+
+DEV = "cuda:0"
+_COMMS = {}
+
+
+def comm(p, G=0, g=0):
+    key = (p, G, g)
+    if key not in _COMMS:
+        _COMMS[key] = Comm(ranks_per_proc=p, device=0, emulate_gpus=G, group_size=g, timeout_s=20.0)
+    return _COMMS[key]
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def topologies(p):
+    return [G for G in (0, 2, 4, 8) if G == 0 or (p % G == 0 and G <= p)]
+
+
+def run_alltoall(c, send, algo):
+    d_send = dev(send)
+    d_recv = torch.full_like(d_send, 0xA5)
+    c.alltoall(d_send, d_recv, algo=algo, count=send.shape[1] // c.p)
+    out = host(d_recv)
+    assert c.check() == 0
+    return out
+
+
+# ------------------------------------------------------------------ cfg1 (configs[0])
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+@pytest.mark.parametrize("algo", ["pairwise", "bruck", "hier"])
+def test_cfg1_alltoall_p4_8xint32(seed, algo):
+    p = 4
+    send = np.stack([np.concatenate([synth.cfg1_block(seed, r, j) for j in range(p)]) for r in range(p)])
+    send8 = send.view(np.uint8)
+    want = oracle.alltoall_definition(send8)
+    for G in (0, 2, 4):
+        for g in (2, 4):
+            c = comm(p, G, g)
+            d_send = dev(send)               # int32 words, count = 8 per destination
+            d_recv = torch.zeros_like(d_send)
+            c.alltoall(d_send, d_recv, algo=algo)
+            assert np.array_equal(host(d_recv).view(np.uint8), want), (G, g)
+
+
+# ------------------------------------------------------------------ alltoall sweeps
+
+SIZES = [1, 3, 4, 8, 16, 48, 100, 1000, 4096 + 12, 65536 + 128, 300_000]
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 7, 8, 16])
+def test_alltoall_all_variants_sizes(p):
+    for b in SIZES:
+        if p * p * b > 64 << 20:
+            continue
+        send = synth.alltoall_sendbuf(b + p, p, b)
+        want = oracle.alltoall_definition(send)
+        for G in topologies(p):
+            for algo in ("pairwise", "bruck", "hier"):
+                g = 2 if p % 2 == 0 else 1
+                got = run_alltoall(comm(p, G, g), send, algo)
+                assert np.array_equal(got, want), (p, b, G, algo)
+
+
+@pytest.mark.parametrize("p,g", [(8, 2), (8, 4), (6, 3), (4, 4), (8, 8), (32, 4)])
+def test_alltoall_hier_groups(p, g):
+    b = 260
+    send = synth.alltoall_sendbuf(11, p, b)
+    want = oracle.alltoall_definition(send)
+    for G in topologies(p) + ([] if p != 32 else [32 // 4]):
+        got = run_alltoall(comm(p, G, g), send, "hier")
+        assert np.array_equal(got, want), (G,)
+
+
+def test_cfg3_float32_payload_opaque_nan():
+    """cfg3 float32 U[-1,1) blocks + NaN/denormal bit patterns survive bit-exactly."""
+    p, count = 8, 1024 + 3
+    send = np.stack([np.concatenate([synth.cfg3_block(5, r, j, count) for j in range(p)]) for r in range(p)])
+    raw = send.view(np.uint32)
+    raw[:, ::97] = 0x7FC00001      # quiet NaN with payload
+    raw[:, 1::89] = 0x00000001     # denormal
+    raw[:, 2::83] = 0xFF800000     # -inf
+    want = oracle.alltoall_definition(send.view(np.uint8))
+    for algo in ("pairwise", "bruck", "hier"):
+        for G in (0, 8):
+            c = comm(p, G, 2)
+            d_send = dev(send)
+            d_recv = torch.zeros_like(d_send)
+            c.alltoall(d_send, d_recv, algo=algo)
+            assert np.array_equal(host(d_recv).view(np.uint8), want), (algo, G)
+
+
+def test_cfg5_bf16_payload_p32():
+    """cfg5 shape on one device: p=32 ranks, bf16 N(0,1) payload, 4 ranks per (virtual) GPU."""
+    p, count = 32, 8 + 64
+    send = np.stack([np.concatenate([synth.cfg5_block(3, r, j, count) for j in range(p)]) for r in range(p)])
+    want = oracle.alltoall_definition(send.view(np.uint8))
+    for algo in ("pairwise", "bruck", "hier"):
+        for G in (0, 8):
+            c = comm(p, G, 4)
+            d_send = dev(send).view(torch.bfloat16)
+            d_recv = torch.zeros_like(d_send)
+            c.alltoall(d_send, d_recv, algo=algo)
+            assert np.array_equal(host(d_recv.view(torch.int16)).view(np.uint8), want), (algo, G)
+
+
+def test_misaligned_pointers():
+    """recv / send at odd byte offsets exercise the 8/4/2/1-byte copy paths."""
+    p, b = 4, 777
+    send = synth.alltoall_sendbuf(3, p, b)
+    want = oracle.alltoall_definition(send)
+    c = comm(p)
+    for so, ro in ((1, 0), (0, 3), (5, 7), (8, 4), (2, 6)):
+        bs = torch.zeros(p * p * b + 64, dtype=torch.uint8, device=DEV)
+        br = torch.zeros(p * p * b + 64, dtype=torch.uint8, device=DEV)
+        bs[so:so + p * p * b] = dev(send.reshape(-1))
+        for algo in ("pairwise", "bruck", "hier"):
+            br.fill_(0)
+            c.alltoall(bs[so:so + p * p * b], br[ro:ro + p * p * b], algo=algo, count=b)
+            got = host(br)[ro:ro + p * p * b].reshape(p, p * b)
+            assert np.array_equal(got, want), (so, ro, algo)
+
+
+def test_zero_count_is_noop():
+    c = comm(4)
+    d = torch.empty(0, dtype=torch.uint8, device=DEV)
+    r = torch.full((16,), 7, dtype=torch.uint8, device=DEV)
+    c.alltoall(d, r, count=0)
+    c.allgather(d, r, count=0)
+    assert np.all(host(r) == 7)
+
+
+# ------------------------------------------------------------------ allgather (cfg2 shape)
+
+@pytest.mark.parametrize("p", [1, 2, 3, 5, 8, 16])
+def test_allgather_all_variants(p):
+    for b in [1, 4, 7, 64, 1000, 4096, 65536 + 5, 1 << 20]:
+        if p * p * b > 64 << 20:
+            continue
+        send = synth.allgather_sendbuf(b, p, b)
+        want = oracle.allgather_definition(send)
+        for G in topologies(p):
+            c = comm(p, G)
+            for algo in ("pairwise", "bruck", "ring"):
+                d_send = dev(send)
+                d_recv = torch.full((p, p * b), 0x5A, dtype=torch.uint8, device=DEV)
+                c.allgather(d_send, d_recv, algo=algo)
+                assert np.array_equal(host(d_recv), want), (p, b, G, algo)
+
+
+# ------------------------------------------------------------------ Bruck intermediate states
+
+@pytest.mark.parametrize("p", [2, 3, 4, 5, 8, 16])
+def test_bruck_intermediate_states(p):
+    b = 36
+    send = synth.alltoall_sendbuf(p, p, b)
+    ag = synth.allgather_sendbuf(p, p, b)
+    K = max(0, int(np.ceil(np.log2(p))))
+    for G in topologies(p):
+        c = comm(p, G)
+        for stage in range(K + 1):
+            _, T, _ = oracle.alltoall(send, "bruck", stop_stage=stage)
+            d_T = torch.zeros((p, p * b), dtype=torch.uint8, device=DEV)
+            c.alltoall_bruck_stage(dev(send), d_T, stage)
+            assert np.array_equal(host(d_T), T), ("alltoall", G, stage)
+            _, Tg, _ = oracle.allgather(ag, "bruck", stop_stage=stage)
+            d_Tg = torch.zeros((p, p * b), dtype=torch.uint8, device=DEV)
+            c.allgather_bruck_stage(dev(ag), d_Tg, stage)
+            n = min(1 << stage, p) * b
+            assert np.array_equal(host(d_Tg)[:, :n], Tg[:, :n]), ("allgather", G, stage)
+
+
+# ------------------------------------------------------------------ alltoallv (cfg4 shape)
+
+@pytest.mark.parametrize("mean", [64, 4096, 65536])
+@pytest.mark.parametrize("packed", [True, False])
+def test_cfg4_alltoallv(mean, packed):
+    p = 8
+    for seed in (0, 1, 2):
+        c4 = synth.cfg4_counts(seed, p, mean)
+        send, sc, sd, rc, rd, S, Rcap = synth.alltoallv_buffers(seed, c4, elem=8, packed=packed)
+        recv0 = np.full((p, Rcap), 0xA5, dtype=np.uint8)
+        want = oracle.alltoallv_definition(send, sc, sd, rc, rd, 8, recv0)
+        for G in (0, 2, 8):
+            for algo, g in (("pairwise", 2), ("hier", 2), ("hier", 4)):
+                c = comm(p, G, g)
+                d_send = dev(send.view(np.int64))
+                d_recv = dev(recv0.view(np.int64))
+                c.alltoallv(d_send, sc, sd, d_recv, rc, rd, algo=algo)
+                assert np.array_equal(host(d_recv).view(np.uint8), want), (seed, G, algo, g)
+
+
+def test_alltoallv_counts_kernel():
+    for p in (1, 3, 8, 32, 40):
+        sc = synth.cfg4_counts(p, p, 4096)
+        rc_w, rd_w, _ = oracle.counts_exchange(sc)
+        c = comm(p)
+        d_sc = dev(sc)
+        d_rc = torch.zeros_like(d_sc)
+        d_rd = torch.zeros_like(d_sc)
+        c.alltoallv_counts(d_sc, d_rc, d_rd)
+        assert np.array_equal(host(d_rc), rc_w) and np.array_equal(host(d_rd), rd_w), p
+
+
+# ------------------------------------------------------------------ persistent requests
+
+def test_persistent_alltoallv_100_cycles():
+    """cfg4: init once, start/wait 100 times; fresh data verified at cycles 0, 1, 99."""
+    p = 8
+    c4 = synth.cfg4_counts(0, p, 4096)
+    for G in (0, 8):
+        c = comm(p, G, 2)
+        for algo in ("pairwise", "hier"):
+            send, sc, sd, rc, rd, S, Rcap = synth.alltoallv_buffers(0, c4, elem=8)
+            d_send = dev(send.view(np.int64))
+            d_recv = torch.zeros((p, Rcap // 8), dtype=torch.int64, device=DEV)
+            req = c.alltoallv_init(d_send, sc, sd, d_recv, rc, rd, algo=algo)
+            assert req.algorithm == algo
+            launches0 = c.launch_count()
+            for cyc in range(100):
+                if cyc in (0, 1, 99):
+                    send_c, *_ = synth.alltoallv_buffers(cyc + 100, c4, elem=8)
+                    d_send.copy_(dev(send_c.view(np.int64)))
+                req.start()
+                req.wait()
+                if cyc in (0, 1, 99):
+                    want = oracle.alltoallv_definition(send_c, sc, sd, rc, rd, 8, np.zeros((p, Rcap), np.uint8))
+                    assert np.array_equal(host(d_recv).view(np.uint8), want), (G, algo, cyc)
+            assert c.launch_count() - launches0 == 100      # one kernel per start, nothing else
+            req.free()
+
+
+def test_persistent_lifecycle_errors():
+    p = 4
+    c = comm(p)
+    d_send = torch.zeros(p * p * 16, dtype=torch.uint8, device=DEV)
+    d_recv = torch.zeros_like(d_send)
+    req = c.alltoall_init(d_send, d_recv, algo="pairwise")
+    with pytest.raises(MpxaError) as e:
+        req.wait()                        # wait on INACTIVE
+    assert e.value.status == M.ERR_LIFECYCLE
+    req.start()
+    with pytest.raises(MpxaError) as e:
+        req.start()                       # start on ACTIVE
+    assert e.value.status == M.ERR_LIFECYCLE
+    with pytest.raises(MpxaError) as e:
+        req.free()                        # free while ACTIVE
+    assert e.value.status == M.ERR_LIFECYCLE
+    req.wait()
+    req.free()
+
+
+@pytest.mark.parametrize("op", ["alltoall", "allgather"])
+def test_persistent_uniform_cycles(op):
+    p, b = 8, 4096 + 64
+    for G in (0, 4):
+        c = comm(p, G)
+        for algo in M.list_algorithms(op):
+            if op == "alltoall":
+                send = synth.alltoall_sendbuf(1, p, b)
+                d_send, d_recv = dev(send), torch.zeros((p, p * b), dtype=torch.uint8, device=DEV)
+                req = c.alltoall_init(d_send, d_recv, algo=algo)
+            else:
+                send = synth.allgather_sendbuf(1, p, b)
+                d_send, d_recv = dev(send), torch.zeros((p, p * b), dtype=torch.uint8, device=DEV)
+                req = c.allgather_init(d_send, d_recv, algo=algo)
+            for cyc in range(5):
+                fresh = (synth.alltoall_sendbuf(cyc, p, b) if op == "alltoall"
+                         else synth.allgather_sendbuf(cyc, p, b))
+                d_send.copy_(dev(fresh))
+                req.start()
+                req.wait()
+                want = (oracle.alltoall_definition(fresh) if op == "alltoall"
+                        else oracle.allgather_definition(fresh))
+                assert np.array_equal(host(d_recv), want), (G, algo, cyc)
+            req.free()
+
+
+def test_selector_and_registry():
+    c = comm(8)
+    assert c.get_algorithm("alltoall", 1 << 20) in ("pairwise", "bruck", "hier")
+    c.set_algorithm("allgather", "ring")
+    assert c.get_algorithm("allgather", 4) == "ring"
+    c.set_algorithm("allgather", "default")
+    with pytest.raises(MpxaError):
+        c.set_algorithm("alltoallv", "bruck")
+
+
+# ------------------------------------------------------------------ full-size (bench launch config)
+
+def _column_sample_check(send_d, recv_d, p, b, cols):
+    """alltoall acts independently on every byte column of a block: check sampled columns
+    through the oracle on the reduced (p, p*len(cols)) instance."""
+    s = send_d.view(p, p, b)[:, :, cols].cpu().numpy().reshape(p, p * len(cols))
+    r = recv_d.view(p, p, b)[:, :, cols].cpu().numpy().reshape(p, p * len(cols))
+    assert np.array_equal(r, oracle.alltoall_definition(s))
+
+
+@pytest.mark.parametrize("G", [0, 8])
+def test_full_size_cfg3_p8_16MiB_sampled(G):
+    p, b = 8, 16 << 20
+    g = torch.Generator(device=DEV)
+    g.manual_seed(0)
+    send = torch.randint(0, 256, (p, p * b), dtype=torch.uint8, device=DEV, generator=g)
+    recv = torch.zeros_like(send)
+    rng = np.random.default_rng(0)
+    cols = np.unique(np.concatenate([rng.integers(0, b, 4096), [0, 1, 15, 16, 127, 128, b - 1]]))
+    c = comm(p, G, 2)
+    for algo in ("pairwise", "bruck", "hier"):
+        recv.zero_()
+        c.alltoall(send, recv, algo=algo)
+        torch.cuda.synchronize()
+        _column_sample_check(send, recv, p, b, torch.from_numpy(cols).to(DEV))
+        # whole-buffer invariant: recv is a permutation of blocks of send
+        assert torch.equal(recv.view(p, p, b).transpose(0, 1).reshape(p, p * b), send)
+
+
+def test_full_size_cfg2_allgather_64MiB_sampled():
+    p, b = 8, 64 << 20
+    g = torch.Generator(device=DEV)
+    g.manual_seed(1)
+    send = torch.randint(0, 256, (p, b), dtype=torch.uint8, device=DEV, generator=g)
+    recv = torch.zeros((p, p * b), dtype=torch.uint8, device=DEV)
+    c = comm(p)
+    for algo in ("pairwise", "bruck", "ring"):
+        recv.zero_()
+        c.allgather(send, recv, algo=algo)
+        torch.cuda.synchronize()
+        cols = torch.from_numpy(np.unique(np.random.default_rng(2).integers(0, b, 4096))).to(DEV)
+        s = send[:, cols].cpu().numpy()
+        r = recv.view(p, p, b)[:, :, cols].cpu().numpy().reshape(p, -1)
+        assert np.array_equal(r, oracle.allgather_definition(s)), algo
+        for r_ in range(p):
+            assert torch.equal(recv[r_].view(p, b), send), algo
