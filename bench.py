@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""bench.py -- measures the mpxa hot path on B200 (contract: see DESIGN.md §7).
+
+Default (N=1): BASELINE.json configs[1] -- allgather over p=8 ranks, per-rank contribution
+64 MiB (the sweep's largest point), uint8 payload uniform random from a seed -- with all
+8 ranks hosted on the one B200 (the paper's multi-process-per-GPU setting).  A "step" is
+one mpxa_allgather call (selector-chosen variant): one kernel launch.
+
+With --gpus N > 1 (torchrun, one process per GPU): the same p=8 ranks spread over N GPUs
+(R = 8/N ranks per process; strong scaling), IPC peer stores over NVLink + device flags.
+
+Prints ONE JSON line (rank 0).  value = aggregate payload bytes received by all ranks per
+second (sum over ranks of p*b, over the max-over-ranks device time).  Also reported:
+roofline of the dominant kernel, the CPU oracle timed on host cores (cpu_baseline), the
+end-to-end number through host buffers (e2e), clocks sampled during the timed region,
+and a per-size / per-variant sweep (us and GB/s) for allgather (cfg2 sizes) and alltoall
+(cfg3 sizes) -- the BASELINE metric is "GB/s & us vs block size".
+
+--impl reference: the reference arm is the CPU oracle (oracle/), timed on the host cores
+on bounded samples of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASELINE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
+METRIC = BASELINE["metric"]
+P_RANKS = 8
+DEFAULT_BYTES = 64 << 20
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---------------------------------------------------------------------------------------
+# clocks sampler (NVML, every 10 ms, during the timed region)
+# ---------------------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons = [], 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nvml = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM))
+                self.reasons |= self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.nvml:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def report(self):
+        if not self.nvml:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        names = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------------------
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def max_over_ranks(x: float, ws: int) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------------------
+def time_loop(fn, steps, warmup, stream, ws):
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    barrier(ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    ms = e0.elapsed_time(e1)
+    return max_over_ranks(ms, ws) / steps
+
+
+def sweep(comm, torch, stream, reps=20):
+    """Per-size / per-variant us and GB/s on this device (BASELINE metric: vs block size)."""
+    p = comm.p
+    R = comm.R
+    out = {"allgather": {}, "alltoall": {}}
+    dev = "cuda"
+    big = torch.empty(2 << 30, dtype=torch.uint8, device=dev)
+    # allgather, cfg2 sizes 4 B .. 64 MiB (x2)
+    for algo in ("pairwise", "bruck", "ring"):
+        rows = []
+        b = 4
+        while b <= (64 << 20):
+            send = big[: R * b].view(R, b)
+            recv = torch.empty((R, p * b), dtype=torch.uint8, device=dev)
+            it = max(3, min(reps, int(2e9 // max(1, p * p * b))))
+            us = 1e3 * time_loop(lambda: comm.allgather(send, recv, algo=algo, stream=stream), it, 3, stream, 1)
+            rows.append([b, round(us, 3), round(p * p * b / us / 1e3, 2)])
+            del recv
+            b *= 2
+        out["allgather"][algo] = rows
+    # alltoall, cfg3 sizes 4 B .. 16 MiB (x4)
+    for algo in ("pairwise", "bruck", "hier"):
+        rows = []
+        b = 4
+        while b <= (16 << 20):
+            send = big[: R * p * b].view(R, p * b)
+            recv = torch.empty((R, p * b), dtype=torch.uint8, device=dev)
+            it = max(3, min(reps, int(2e9 // max(1, p * p * b))))
+            us = 1e3 * time_loop(lambda: comm.alltoall(send, recv, algo=algo, stream=stream), it, 3, stream, 1)
+            rows.append([b, round(us, 3), round(p * p * b / us / 1e3, 2)])
+            del recv
+            b *= 4
+        out["alltoall"][algo] = rows
+    del big
+    return out
+
+
+def write_selector(sw, path, p, R):
+    """Measured selector table: for each op and size, the fastest variant (ties -> SPEC default)."""
+    lines = ["# op p ranks_per_proc max_bytes algo  (generated by bench.py --write-selector)"]
+    for op, variants in sw.items():
+        sizes = [row[0] for row in next(iter(variants.values()))]
+        best_prev = None
+        for i, b in enumerate(sizes):
+            best = min(variants, key=lambda a: (variants[a][i][1], a != "pairwise"))
+            if best_prev is not None and best != best_prev[0]:
+                lines.append(f"{op} {p} {R} {best_prev[1]} {best_prev[0]}")
+            best_prev = (best, b)
+        lines.append(f"{op} {p} {R} 18446744073709551615 {best_prev[0]}")
+    open(path, "w").write("\n".join(lines) + "\n")
+
+
+def cpu_oracle_sample(send_host: np.ndarray, budget_s: float):
+    """Time the oracle's allgather (direct variant, as the GPU's selector chose) on host cores."""
+    import oracle
+    p, b = send_host.shape
+    t0 = time.perf_counter()
+    oracle.allgather(send_host, "direct")
+    dt = time.perf_counter() - t0
+    reps = 1
+    while time.perf_counter() - t0 + dt < budget_s and reps < 50:
+        oracle.allgather(send_host, "direct")
+        reps += 1
+    total = time.perf_counter() - t0
+    return {"value": round(p * p * b * reps / total / 1e9, 3), "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"{reps} full step(s) of the workload (allgather p={p}, {b} B per rank, direct variant, "
+                      f"single-threaded C simulation incl. transport envelopes), {total:.1f} s"}
+
+
+def gpu_arm(args):
+    import torch
+    from paper_2309_07337_b200 import Comm
+
+    ws, rank, local = dist_env()
+    N = args.gpus
+    assert ws == N or (ws == 1 and N == 1), f"--gpus {N} but WORLD_SIZE={ws}"
+    torch.cuda.set_device(local)
+    pg = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        pg = dist.group.WORLD
+    p = P_RANKS
+    if p % N:
+        raise SystemExit(f"--gpus {N} must divide p={p}")
+    R = p // N
+    b = args.bytes
+    comm = Comm(ranks_per_proc=R, device=local, pg=pg)
+    stream = torch.cuda.current_stream()
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(1000 + rank)
+    send = torch.randint(0, 256, (R, b), dtype=torch.uint8, device="cuda", generator=gen)
+    recv = torch.empty((R, p * b), dtype=torch.uint8, device="cuda")
+    if ws > 1:
+        comm.register(recv)
+    algo = comm.get_algorithm("allgather", b)
+
+    def step():
+        comm.allgather(send, recv, stream=stream)
+
+    peak, peak_src = load_peaks()
+    l0 = comm.launch_count()
+    with ClockSampler(local) as clk:
+        ms = time_loop(step, args.steps, args.warmup, stream, ws)
+    launches = comm.launch_count() - l0 - args.warmup
+    # ---- parity spot check of the timed configuration (sampled columns, oracle) ----
+    verified = None
+    if rank == 0 and ws == 1:
+        import oracle
+        cols = torch.from_numpy(np.unique(np.random.default_rng(0).integers(0, b, 2048))).cuda()
+        s = send[:, cols].cpu().numpy()
+        r = recv.view(R, p, b)[:, :, cols].cpu().numpy().reshape(R, -1)
+        verified = bool(np.array_equal(r, oracle.allgather_definition(s)))
+    # ---- metric ----
+    total_recv = p * p * b                      # all ranks, bytes received (incl. own block)
+    value = total_recv / (ms * 1e-3) / 1e9
+    # algorithmic HBM bytes of the kernel on this GPU: read R*b, write R*p*b (+ peer-in)
+    hbm_bytes = R * b + R * p * b
+    achieved = hbm_bytes / (ms * 1e-3) / 1e9
+    # ---- e2e through host buffers (pinned), same metric ----
+    e2e = None
+    if not args.no_e2e:
+        h_send = torch.empty((R, b), dtype=torch.uint8, pin_memory=True)
+        h_send.copy_(send.cpu())
+        h_recv = torch.empty((R, p * b), dtype=torch.uint8, pin_memory=True)
+
+        def e2e_step():
+            send.copy_(h_send, non_blocking=True)
+            comm.allgather(send, recv, stream=stream)
+            h_recv.copy_(recv, non_blocking=True)
+
+        e_ms = time_loop(e2e_step, max(3, min(args.steps, 10)), 2, stream, ws)
+        e2e = {"value": round(total_recv / (e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": R * b, "d2h_bytes_per_step": R * p * b, "ms_per_step": round(e_ms, 4)}
+    sw = None
+    if args.sweep and ws == 1:
+        sw = sweep(comm, torch, stream)
+        if args.write_selector:
+            write_selector(sw, args.write_selector, p, R)
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_oracle_sample(send.cpu().numpy(), args.cpu_budget) if ws == 1 else None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
+            "metric_definition": "aggregate payload bytes received by all p ranks (p*p*b) per second "
+                                 "of device time (max over ranks), one mpxa_allgather per step",
+            "n_gpus": N, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 5),
+            "us_per_call": round(ms * 1e3, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u8", "data": "synthetic (seeded torch uniform bytes)",
+            "config": {"workload": "BASELINE configs[1]: allgather p=8 ranks, 64 MiB per-rank contribution "
+                                   f"(all 8 ranks on {N} B200)", "op": "allgather", "p": p,
+                       "ranks_per_gpu": R, "bytes_per_rank": b, "variant": algo,
+                       "l2": "inputs larger than L2 (send 512 MiB, recv 4 GiB)"},
+            "verified_sampled_vs_oracle": verified,
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": hbm_bytes,
+                         "kernel": "mpxa_exec_kernel (one launch per step; CUDA events on its stream)"},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.report(), "sweep": sw,
+        }
+        if args.traffic is not None:
+            line["roofline"]["traffic"] = args.traffic
+        print(json.dumps(line))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------------------
+# reference arm: the CPU oracle on bounded samples
+# ---------------------------------------------------------------------------------------
+def reference_arm(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    import synth
+    oracle.build()
+    p = P_RANKS
+    # bounded sample per step: calibrate so that (steps + warmup) fit in ~90 s
+    b = args.bytes
+    probe = 1 << 20
+    send = synth.allgather_sendbuf(0, p, probe)
+    t0 = time.perf_counter()
+    oracle.allgather(send, "direct")
+    per_byte = (time.perf_counter() - t0) / probe
+    budget = 90.0 / max(1, args.steps + args.warmup)
+    sb = int(min(b, max(4096, budget / max(per_byte, 1e-12))))
+    sb = 1 << (sb.bit_length() - 1)
+    send = synth.allgather_sendbuf(0, p, sb)
+    for _ in range(args.warmup):
+        oracle.allgather(send, "direct")
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.allgather(send, "direct")
+    dt = (time.perf_counter() - t0) / args.steps
+    value = p * p * sb / dt / 1e9
+    sample = f"allgather p={p}, {sb} B per rank (bounded sample of the {b} B workload), direct variant"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (synth.cfg2 payload)",
+        "config": {"workload": "BASELINE configs[1]: allgather p=8 ranks (CPU oracle sample)", "op": "allgather",
+                   "p": p, "bytes_per_rank": sb},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="mpxa", choices=["mpxa", "reference"])
+    ap.add_argument("--bytes", type=int, default=DEFAULT_BYTES, help="per-rank contribution")
+    ap.add_argument("--no-sweep", dest="sweep", action="store_false")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--write-selector", default=None)
+    ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per launch, if captured")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

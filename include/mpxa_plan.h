@@ -25,20 +25,22 @@ extern "C" {
 
 typedef struct {
     int64_t src_off, dst_off, len;   /* units                                   */
+    uint32_t flow;                   /* identity of the data moved (origin block / segment) */
     uint16_t src_rank, dst_rank;
     uint8_t src_kind, dst_kind;      /* 0 send buffer, 1 recv buffer, 2 library workspace */
     uint8_t fanout;                  /* 1: to every rank's dst_kind buffer at dst_off */
-    uint8_t pad;
+    uint8_t pad[5];
 } mpxa_plan_move;
 
 typedef struct {
-    int32_t move_begin, move_end;
+    int32_t move_begin, move_end;    /* moves sorted by flow within the step     */
     uint32_t signal_mask, wait_mask; /* peer GPUs written / writing in this step */
     int64_t total_len, max_len;
+    int64_t flow_index;              /* internal                                 */
 } mpxa_plan_step;
 
 typedef struct {
-    int64_t nsteps, work_units, max_move, max_step_units, signals, total_moves;
+    int64_t nsteps, work_units, max_move, max_step_units, signals, total_moves, nflows, max_step_moves;
 } mpxa_plan_info_t;
 
 int mpxa_plan_build(int op, int algo, int p, int R, int G, int g, int stop_stage,

@@ -48,7 +48,9 @@ using namespace mpxa;
 
 namespace {
 
-constexpr uint64_t kBytesPerCta = 32768;   // launch sizing target per CTA per step
+constexpr uint64_t kBytesPerCta = 65536;   // launch sizing target per CTA per step
+constexpr uint64_t kSliceBytes = 16384;    // target column-slice length of the longest move
+constexpr uint64_t kMovesPerCta = 8;       // small moves per CTA (latency-bound regime)
 
 // A program uploaded to device memory: [GpuProg x G][steps][moves].
 struct DevProg {
@@ -61,26 +63,32 @@ struct DevProg {
 size_t serialize(const Program &P, std::vector<char> &buf, uintptr_t dbase) {
     const int G = P.G;
     size_t off = sizeof(GpuProg) * G;
-    std::vector<size_t> soff(G), moff(G);
+    std::vector<size_t> soff(G), moff(G), foff(G);
     for (int g = 0; g < G; g++) { soff[g] = off; off += sizeof(Step) * P.steps[g].size(); }
     for (int g = 0; g < G; g++) { moff[g] = off; off += sizeof(Move) * P.moves[g].size(); }
+    for (int g = 0; g < G; g++) { foff[g] = off; off += sizeof(int32_t) * P.findex[g].size(); }
     buf.assign(off, 0);
     for (int g = 0; g < G; g++) {
         GpuProg gp{};
         gp.steps = (const Step *)(dbase + soff[g]);
         gp.moves = (const Move *)(dbase + moff[g]);
+        gp.findex = (const int32_t *)(dbase + foff[g]);
         gp.nsteps = (int32_t)P.steps[g].size();
         gp.nmoves = (int32_t)P.moves[g].size();
         memcpy(buf.data() + sizeof(GpuProg) * g, &gp, sizeof gp);
         if (!P.steps[g].empty()) memcpy(buf.data() + soff[g], P.steps[g].data(), sizeof(Step) * P.steps[g].size());
         if (!P.moves[g].empty()) memcpy(buf.data() + moff[g], P.moves[g].data(), sizeof(Move) * P.moves[g].size());
+        if (!P.findex[g].empty())
+            memcpy(buf.data() + foff[g], P.findex[g].data(), sizeof(int32_t) * P.findex[g].size());
     }
     return off;
 }
 
 size_t serialized_size(const Program &P) {
     size_t n = sizeof(GpuProg) * P.G;
-    for (int g = 0; g < P.G; g++) n += sizeof(Step) * P.steps[g].size() + sizeof(Move) * P.moves[g].size();
+    for (int g = 0; g < P.G; g++)
+        n += sizeof(Step) * P.steps[g].size() + sizeof(Move) * P.moves[g].size() +
+             sizeof(int32_t) * P.findex[g].size();
     return n;
 }
 
@@ -93,6 +101,13 @@ struct SelEntry {
     int op, p, R;
     uint64_t max_bytes;
     int algo;
+};
+
+// CTA decomposition: nS column slices per move x nF flow groups.  Depends
+// only on the (global) program and the unit, so every process computes the same grid.
+struct Grid {
+    int nS = 1, nF = 1;
+    int n() const { return nS * nF; }
 };
 
 // ring slot for per-call programs (v-ops)
@@ -117,6 +132,7 @@ struct mpxa_comm_s {
     void *ctx = nullptr;
     double timeout_s = 60.0;
     int sm_count = 148, cap_ctas = 296;
+    int force_ns = 0, force_nf = 0;           // MPXA_NS / MPXA_NF overrides (tuning)
 
     SymRegion *sym_local = nullptr;            // G regions when emulated, else 1
     SymRegion *sym_map[kMaxGpus] = {};
@@ -151,7 +167,7 @@ struct mpxa_request_s {
     const char *send = nullptr;
     char *recv = nullptr;
     uint64_t unit = 0, send_stride = 0, recv_stride = 0;
-    int nC = 1;
+    Grid grid;
     cudaEvent_t done = nullptr;
     cudaStream_t start_stream = nullptr;
 };
@@ -253,16 +269,29 @@ int cached_uniform(mpxa_comm_t c, int op, int algo, int stage, std::shared_ptr<D
     return MPXA_SUCCESS;
 }
 
-int choose_ctas(mpxa_comm_t c, const Program &P, uint64_t unit) {
-    uint64_t step_bytes = (uint64_t)P.max_step_units * unit;
-    uint64_t move_bytes = (uint64_t)P.max_move * unit;
-    uint64_t n = (step_bytes + kBytesPerCta - 1) / kBytesPerCta;
-    uint64_t lines = (move_bytes + 127) / 128;
-    n = std::min<uint64_t>(n, std::max<uint64_t>(lines, 1));
-    const char *env = getenv("MPXA_CTAS");
-    if (env && atoi(env) > 0) n = (uint64_t)atoi(env);
-    n = std::max<uint64_t>(1, std::min<uint64_t>(n, (uint64_t)c->cap_ctas));
-    return (int)n;
+
+uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+Grid choose_grid(mpxa_comm_t c, const Program &P, uint64_t unit) {
+    const uint64_t cap = (uint64_t)c->cap_ctas;
+    const uint64_t L = (uint64_t)P.max_move * unit;          // longest move
+    const uint64_t T = (uint64_t)P.max_step_units * unit;    // busiest step of one GPU
+    Grid gr;
+    uint64_t nS = std::min<uint64_t>(cap, std::max<uint64_t>(1, cdiv(L, kSliceBytes)));
+    uint64_t nF_bw = cdiv(T, nS * kBytesPerCta);              // enough CTAs for bandwidth
+    uint64_t nF_lat = cdiv((uint64_t)P.max_step_moves, kMovesPerCta);  // ~1 move per LSU warp
+    uint64_t nF = std::max<uint64_t>(1, std::max(nF_bw, nF_lat));
+    nF = std::min<uint64_t>(nF, std::max<uint64_t>(1, cap / nS));
+    nF = std::min<uint64_t>(nF, (uint64_t)P.nflows);
+    if (c->force_ns > 0) nS = (uint64_t)c->force_ns;
+    if (c->force_nf > 0) nF = std::min<uint64_t>((uint64_t)c->force_nf, (uint64_t)P.nflows);
+    while (nS * nF > (uint64_t)kMaxCtas || nS * nF > cap) {
+        if (nF > 1) nF--;
+        else nS--;
+    }
+    gr.nS = (int)std::max<uint64_t>(1, nS);
+    gr.nF = (int)std::max<uint64_t>(1, nF);
+    return gr;
 }
 
 // Fill launch parameters for a program on this comm.
@@ -273,6 +302,7 @@ int make_params(mpxa_comm_t c, ExecParams &E, const DevProg &dp, const char *sen
     E.G = c->G;
     E.R = c->Rg;
     E.p = c->p;
+    E.nflows = dp.host.nflows;
     E.my_gpu = c->emulated ? -1 : (c->nprocs > 1 ? c->proc : 0);
     E.unit = unit;
     E.send_stride = send_stride;
@@ -312,7 +342,7 @@ int make_params(mpxa_comm_t c, ExecParams &E, const DevProg &dp, const char *sen
 }
 
 int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, uint64_t unit,
-                uint64_t send_stride, uint64_t recv_stride, cudaStream_t stream, int nC = 0) {
+                uint64_t send_stride, uint64_t recv_stride, cudaStream_t stream, const Grid *grid = nullptr) {
     if (c->poisoned) return MPXA_ERR_TIMEOUT;
     if (dp.nsteps == 0) return MPXA_SUCCESS;
     size_t need = (size_t)dp.host.work_units * unit * c->Rg;
@@ -321,9 +351,11 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
     ExecParams E;
     rc = make_params(c, E, dp, send, recv, unit, send_stride, recv_stride);
     if (rc) return rc;
-    if (nC <= 0) nC = choose_ctas(c, dp.host, unit);
+    const Grid gr = grid ? *grid : choose_grid(c, dp.host, unit);
+    E.nS = gr.nS;
+    E.nF = gr.nF;
     E.epoch = ++c->epoch;
-    cudaError_t e = launch_exec(E, nC, c->emulated ? c->G : 1, c->emulated, stream);
+    cudaError_t e = launch_exec(E, gr.n(), c->emulated ? c->G : 1, c->emulated, stream);
     if (e != cudaSuccess) {
         if (getenv("MPXA_DEBUG")) fprintf(stderr, "mpxa: launch failed: %s\n", cudaGetErrorString(e));
         return MPXA_ERR_CUDA;
@@ -451,7 +483,7 @@ int alltoallv_impl(const void *sendbuf, const int64_t *sc, const int64_t *sd, si
         if (rc2) { delete q; return rc2; }
         q->send = (const char *)sendbuf; q->recv = (char *)recvbuf;
         q->unit = w; q->send_stride = send_bpr; q->recv_stride = recv_bpr;
-        q->nC = choose_ctas(c, P, w);
+        q->grid = choose_grid(c, P, w);
         if (c->nprocs > 1) {
             rc2 = mpxa_register(c, recvbuf, recv_bpr * c->R);
             if (rc2) { delete q; return rc2; }
@@ -484,7 +516,7 @@ int uniform_impl(int op, const void *sendbuf, size_t count, size_t w, void *recv
         q->comm = c; q->op = op; q->algo = algo; q->prog = dp;
         q->send = (const char *)sendbuf; q->recv = (char *)recvbuf;
         q->unit = unit; q->send_stride = sstride; q->recv_stride = rstride;
-        q->nC = choose_ctas(c, dp->host, unit);
+        q->grid = choose_grid(c, dp->host, unit);
         if (c->nprocs > 1 && unit) {
             rc = mpxa_register(c, recvbuf, rstride * c->R);
             if (rc) { delete q; return rc; }
@@ -570,6 +602,8 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     int cap = std::min(kMaxCtas, c->sm_count * occ);
     if (c->emulated) cap = std::max(1, cap / c->G);
     c->cap_ctas = cap;
+    if (const char *e = getenv("MPXA_NS")) c->force_ns = atoi(e);
+    if (const char *e = getenv("MPXA_NF")) c->force_nf = atoi(e);
     CK(cudaHostAlloc((void **)&c->err_host, sizeof(int32_t), cudaHostAllocMapped));
     *c->err_host = 0;
     CK(cudaHostGetDevicePointer((void **)&c->err_dev, c->err_host, 0));
@@ -818,7 +852,7 @@ int mpxa_start(mpxa_request_t q, mpxa_stream_t st) {
     mpxa_comm_t c = q->comm;
     if (c->active && c->active != q) return MPXA_ERR_LIFECYCLE;   // one in flight
     if (q->unit) {
-        int rc = run_program(c, *q->prog, q->send, q->recv, q->unit, q->send_stride, q->recv_stride, S(st), q->nC);
+        int rc = run_program(c, *q->prog, q->send, q->recv, q->unit, q->send_stride, q->recv_stride, S(st), &q->grid);
         if (rc) return rc;
     }
     if (!q->done) CK(cudaEventCreateWithFlags(&q->done, cudaEventDisableTiming));
@@ -938,6 +972,8 @@ int mpxa_plan_info(const void *plan, mpxa_plan_info_t *info) {
     int64_t tm = 0;
     for (auto &m : P->moves) tm += (int64_t)m.size();
     info->total_moves = tm;
+    info->nflows = P->nflows;
+    info->max_step_moves = P->max_step_moves;
     return MPXA_SUCCESS;
 }
 

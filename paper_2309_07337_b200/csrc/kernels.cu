@@ -158,8 +158,45 @@ __device__ __forceinline__ void copy_slice_fan(char *const *dsts, int nd, const 
 // executor
 // ------------------------------------------------------------------------------------
 constexpr uint64_t kLine = 128;          // slice boundaries are 128-B multiples of a move
-constexpr uint64_t kCtaCopyMin = 8192;   // slices at least this long use the whole CTA
+constexpr uint64_t kTmaMin = 2048;       // aligned slices at least this long go through TMA
+constexpr uint64_t kLsuBig = 8192;       // misaligned slices at least this long use all LSU warps
 constexpr int kWarps = kThreads / 32;
+constexpr int kLsuWarps = kWarps - 1;    // warp 0 is the TMA producer
+constexpr int kLsuThreads = kThreads - 32;
+constexpr int kAhead = kStages - 2;      // TMA loads in flight ahead of the oldest store
+
+// ---- TMA bulk copies (cp.async.bulk: SASS UBLKCP) --------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(uint32_t dst_smem, const void *src, uint32_t bytes, uint32_t mbar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst_smem), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
+    asm volatile("{\n\t.reg .pred P1;\n"
+                 "WAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+                 "@!P1 bra WAIT_%=;\n}" ::"r"(mbar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_store_1d(void *dst, uint32_t src_smem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src_smem), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read(int n) {
+    switch (n) {
+        case 0: asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); break;
+        case 1: asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); break;
+        case 2: asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory"); break;
+        case 3: asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory"); break;
+        default: asm volatile("cp.async.bulk.wait_group.read 4;" ::: "memory"); break;
+    }
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
 
 __device__ __forceinline__ void slice_of(uint64_t nbytes, int c, int nC, uint64_t &lo, uint64_t &hi) {
     uint64_t nl = (nbytes + kLine - 1) / kLine;
@@ -169,14 +206,23 @@ __device__ __forceinline__ void slice_of(uint64_t nbytes, int c, int nC, uint64_
     if (lo > hi) lo = hi;
 }
 
+struct RingEntry {
+    char *dst;          // non-fanout destination of the chunk
+    uint64_t doff;      // fanout: byte offset inside every rank's dst_kind buffer
+    uint32_t len;
+    uint8_t fanout, dst_kind;
+};
+
 struct ExecShared {
     char *recv_base[kMaxGpus];
+    Move moves[kMoveTile];
+    uint64_t mbar[kStages];
+    RingEntry ring[kStages];
     uint32_t cts_ok;     // remote GPUs whose CTS for this epoch was observed
     int abort_flag;
 };
 
-__device__ __forceinline__ char *base_of(const ExecParams &P, const ExecShared &S, int kind,
-                                         int rank) {
+__device__ __forceinline__ char *base_of(const ExecParams &P, const ExecShared &S, int kind, int rank) {
     int g = rank / P.R;
     uint64_t local = (uint64_t)(rank - g * P.R);
     if (kind == BK_SEND) return P.send_base[g] + local * P.send_stride;
@@ -208,18 +254,112 @@ __device__ __forceinline__ void wait_mask_ge(const ExecParams &P, ExecShared &S,
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) mpxa_exec_kernel(const __grid_constant__ ExecParams P) {
+// The single-thread TMA producer: a ring of kStages smem stages; loads run kAhead chunks
+// ahead of the oldest pending store; each chunk's stores form one bulk group.
+struct Producer {
+    uint32_t issued = 0, stored = 0;
+    char *stages;
+
+    __device__ __forceinline__ void store_one(const ExecParams &P, ExecShared &S) {
+        const uint32_t s = stored % kStages;
+        mbar_wait(smem_u32(&S.mbar[s]), (stored / kStages) & 1u);
+        const RingEntry e = S.ring[s];
+        const uint32_t src = smem_u32(stages + (size_t)s * kChunk);
+        if (!e.fanout) {
+            tma_store_1d(e.dst, src, e.len);
+        } else {
+            for (int j = 0; j < P.p; j++) tma_store_1d(base_of(P, S, e.dst_kind, j) + e.doff, src, e.len);
+        }
+        bulk_commit();
+        stored++;
+    }
+    __device__ __forceinline__ void push(const ExecParams &P, ExecShared &S, const char *src, const RingEntry &e) {
+        if (issued - stored == (uint32_t)kAhead) store_one(P, S);
+        const uint32_t s = issued % kStages;
+        if (issued >= (uint32_t)kStages) bulk_wait_read((int)(stored - 1 - (issued - kStages)));
+        S.ring[s] = e;
+        tma_load_1d(smem_u32(stages + (size_t)s * kChunk), src, e.len, smem_u32(&S.mbar[s]));
+        issued++;
+    }
+    __device__ __forceinline__ void drain(const ExecParams &P, ExecShared &S) {
+        while (stored < issued) store_one(P, S);
+        bulk_wait_all();
+        fence_proxy_async();
+    }
+};
+
+// How CTA (flow group f, slice sl) handles one move: byte range of its slice, source and
+// destination addresses, and the path (TMA body + LSU head/tail, or LSU only).
+struct MovePlan {
+    const char *src;
+    char *dst;          // non-fanout
+    uint64_t doff;      // offset inside each rank's dst buffer (fanout)
+    uint64_t n;         // slice bytes
+    bool tma;
+    uint32_t head;      // TMA: bytes before the 16-B aligned body
+    uint64_t body;      // TMA: aligned body bytes (multiple of 16)
+};
+
+__device__ __forceinline__ MovePlan plan_move(const ExecParams &P, const ExecShared &S, const Move &m, int sl) {
+    MovePlan mp;
+    const uint64_t nbytes = (uint64_t)m.len * P.unit;
+    uint64_t lo, hi;
+    slice_of(nbytes, sl, P.nS, lo, hi);
+    mp.n = hi - lo;
+    mp.src = base_of(P, S, m.src_kind, m.src_rank) + (uint64_t)m.src_off * P.unit + lo;
+    mp.doff = (uint64_t)m.dst_off * P.unit + lo;
+    mp.dst = m.fanout ? nullptr : base_of(P, S, m.dst_kind, m.dst_rank) + mp.doff;
+    unsigned mis;
+    if (!m.fanout) {
+        mis = (unsigned)(((uintptr_t)mp.dst ^ (uintptr_t)mp.src) & 15);
+    } else {
+        mis = 0;
+        for (int j = 0; j < P.p; j++) mis |= (unsigned)(((uintptr_t)(base_of(P, S, m.dst_kind, j) + mp.doff) ^ (uintptr_t)mp.src) & 15);
+    }
+    mp.tma = mis == 0 && mp.n >= kTmaMin;
+    mp.head = (uint32_t)((16 - ((uintptr_t)mp.src & 15)) & 15);
+    if (mp.head > mp.n) mp.head = (uint32_t)mp.n;
+    mp.body = (mp.n - mp.head) & ~(uint64_t)15;
+    return mp;
+}
+
+template <int U, int NT>
+__device__ __forceinline__ void lsu_copy(const ExecParams &P, const ExecShared &S, const Move &m, const MovePlan &mp,
+                                         uint64_t off, uint64_t n, int t) {
+    const bool ro = m.src_kind == BK_SEND;
+    if (!m.fanout) {
+        copy_slice1<U, NT>(mp.dst + off, mp.src + off, n, ro, t);
+    } else {
+        char *dsts[8];
+        for (int j0 = 0; j0 < P.p; j0 += 8) {
+            const int nd = min(8, P.p - j0);
+            for (int k = 0; k < nd; k++) dsts[k] = base_of(P, S, m.dst_kind, j0 + k) + mp.doff + off;
+            copy_slice_fan<U, NT>(dsts, nd, mp.src + off, n, ro, t);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_constant__ ExecParams P) {
+    extern __shared__ __align__(128) char dyn_smem[];
     __shared__ ExecShared S;
     const int g = P.my_gpu >= 0 ? P.my_gpu : (int)blockIdx.y;
     const int c = blockIdx.x;
-    const int nC = gridDim.x;
+    const int sl = c % P.nS;                  // column slice
+    const int f = c / P.nS;                   // flow group
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
     const GpuProg prog = P.progs[g];
     const bool multi = P.G > 1;
+    Producer prod;
+    prod.stages = dyn_smem;
 
     if (t < kMaxGpus) S.recv_base[t] = P.recv_base[t];
-    if (t == 0) { S.cts_ok = 0; S.abort_flag = 0; }
+    if (t == 0) {
+        S.cts_ok = 0;
+        S.abort_flag = 0;
+        for (int s = 0; s < kStages; s++) mbar_init(smem_u32(&S.mbar[s]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     // CTS: this GPU is inside epoch `epoch`, so every earlier use of its buffers is complete
     // (stream order); tell every peer it may write into them.
     if (multi && c == 0 && t < P.G && t != g) {
@@ -230,10 +370,11 @@ __global__ void __launch_bounds__(kThreads, 1) mpxa_exec_kernel(const __grid_con
     }
     __syncthreads();
 
+    const int64_t x0 = (int64_t)f * P.nflows / P.nF, x1 = (int64_t)(f + 1) * P.nflows / P.nF;
     for (int s = 0; s < prog.nsteps; s++) {
         const Step st = prog.steps[s];
         if (multi) {
-            // data written into this GPU by peers in step s-1 (slice c) must have landed
+            // data written into this GPU by peers in step s-1 (this CTA's share) must have landed
             if (s > 0 && prog.steps[s - 1].wait_mask)
                 wait_mask_ge(P, S, prog.steps[s - 1].wait_mask, &P.sym[g]->flags[0][c], kMaxCtas,
                              (P.epoch << 8) | (uint64_t)s);
@@ -250,40 +391,63 @@ __global__ void __launch_bounds__(kThreads, 1) mpxa_exec_kernel(const __grid_con
             if (t == 0) S.cts_ok |= need;
             if (S.abort_flag) return;
         }
-        // ---- the moves of this step, slice c of each; staggered start per CTA ----
-        const int nm = st.move_end - st.move_begin;
-        int small_idx = 0;
-        for (int q = 0; q < nm; q++) {
-            const Move m = prog.moves[st.move_begin + (q + c) % nm];
-            const uint64_t nbytes = (uint64_t)m.len * P.unit;
-            uint64_t lo, hi;
-            slice_of(nbytes, c, nC, lo, hi);
-            if (hi <= lo) continue;
-            const uint64_t n = hi - lo;
-            const bool big = n >= kCtaCopyMin;
-            if (!big) {
-                int mine = (small_idx++ % kWarps) == warp;
-                if (!mine) continue;
+        if (t == 0) fence_proxy_async();   // acquired peer writes before this CTA's TMA reads
+        const int32_t *fx = prog.findex + st.flow_index;
+        const int m0 = fx[x0], m1 = fx[x1];
+        const int nm = m1 - m0;
+        const int rot = nm ? (int)(((int64_t)sl + (int64_t)g * nm / P.G) % nm) : 0;
+        for (int tile = 0; tile < nm; tile += kMoveTile) {
+            const int cnt = min(kMoveTile, nm - tile);
+            __syncthreads();   // the previous tile's moves are no longer read
+            for (int i = t; i < cnt; i += kThreads) {
+                int q = tile + i + rot;
+                if (q >= nm) q -= nm;
+                S.moves[i] = prog.moves[st.move_begin + m0 + q];
             }
-            const char *src = base_of(P, S, m.src_kind, m.src_rank) + (uint64_t)m.src_off * P.unit + lo;
-            const uint64_t doff = (uint64_t)m.dst_off * P.unit + lo;
-            const bool ro = m.src_kind == BK_SEND;
-            if (!m.fanout) {
-                char *dst = base_of(P, S, m.dst_kind, m.dst_rank) + doff;
-                if (big) copy_slice1<8, kThreads>(dst, src, n, ro, t);
-                else     copy_slice1<4, 32>(dst, src, n, ro, lane);
+            __syncthreads();
+            if (warp == 0) {
+                if (lane == 0) {
+                    for (int i = 0; i < cnt; i++) {
+                        const Move &m = S.moves[i];
+                        const MovePlan mp = plan_move(P, S, m, sl);
+                        if (!mp.tma) continue;
+                        for (uint64_t o = 0; o < mp.body; o += kChunk) {
+                            RingEntry e;
+                            e.len = (uint32_t)min((uint64_t)kChunk, mp.body - o);
+                            e.fanout = m.fanout;
+                            e.dst_kind = m.dst_kind;
+                            e.doff = mp.doff + mp.head + o;
+                            e.dst = m.fanout ? nullptr : mp.dst + mp.head + o;
+                            prod.push(P, S, mp.src + mp.head + o, e);
+                        }
+                    }
+                }
             } else {
-                char *dsts[8];
-                for (int j0 = 0; j0 < P.p; j0 += 8) {
-                    int nd = min(8, P.p - j0);
-                    for (int k = 0; k < nd; k++) dsts[k] = base_of(P, S, m.dst_kind, j0 + k) + doff;
-                    if (big) copy_slice_fan<4, kThreads>(dsts, nd, src, n, ro, t);
-                    else     copy_slice_fan<2, 32>(dsts, nd, src, n, ro, lane);
+                const int lw = warp - 1, lt = t - 32;
+                for (int i = 0; i < cnt; i++) {
+                    const Move &m = S.moves[i];
+                    const MovePlan mp = plan_move(P, S, m, sl);
+                    if (mp.n == 0) continue;
+                    if (mp.tma) {
+                        if (i % kLsuWarps == lw) {   // head / tail bytes around the TMA body
+                            const uint64_t tail = mp.n - mp.head - mp.body;
+                            if (lane < 16) lsu_copy<1, 16>(P, S, m, mp, 0, mp.head, lane);
+                            else lsu_copy<1, 16>(P, S, m, mp, mp.head + mp.body, tail, lane - 16);
+                        }
+                    } else if (mp.n >= kLsuBig) {
+                        lsu_copy<4, kLsuThreads>(P, S, m, mp, 0, mp.n, lt);
+                    } else if (i % kLsuWarps == lw) {
+                        lsu_copy<4, 32>(P, S, m, mp, 0, mp.n, lane);
+                    }
                 }
             }
         }
+        // every writer makes its generic stores visible to the async proxy (TMA reads of the
+        // next step); the producer waits its bulk stores and fences them for generic readers
+        fence_proxy_async();
+        if (t == 0) prod.drain(P, S);
         __syncthreads();
-        // ---- signal the peers written in this step (slice c) ----
+        // ---- signal the peers written in this step (this CTA's share) ----
         if (multi && st.signal_mask && t < 32 && ((st.signal_mask >> t) & 1u)) {
             __threadfence_system();
             st_release_sys(&P.sym[t]->flags[g][c], (P.epoch << 8) | (uint64_t)(s + 1));
@@ -352,13 +516,23 @@ __global__ void mpxa_scan_kernel(const int64_t *__restrict__ counts, int64_t *__
 // ------------------------------------------------------------------------------------
 // host-side launchers (called from api.cpp)
 // ------------------------------------------------------------------------------------
+constexpr size_t kDynSmem = (size_t)kStages * kChunk;
+
+static cudaError_t exec_attr_once() {
+    static cudaError_t e = cudaFuncSetAttribute(mpxa_exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)kDynSmem);
+    return e;
+}
+
 cudaError_t launch_exec(const ExecParams &P, int nC, int nG, bool cooperative, cudaStream_t stream) {
+    cudaError_t e = exec_attr_once();
+    if (e != cudaSuccess) return e;
     dim3 grid(nC, nG), block(kThreads);
     if (cooperative) {
         void *args[] = {(void *)&P};
-        return cudaLaunchCooperativeKernel((const void *)mpxa_exec_kernel, grid, block, args, 0, stream);
+        return cudaLaunchCooperativeKernel((const void *)mpxa_exec_kernel, grid, block, args, kDynSmem, stream);
     }
-    mpxa_exec_kernel<<<grid, block, 0, stream>>>(P);
+    mpxa_exec_kernel<<<grid, block, kDynSmem, stream>>>(P);
     return cudaGetLastError();
 }
 
@@ -381,8 +555,9 @@ cudaError_t launch_scan(const int64_t *counts, int64_t *rc, int64_t *rd, int p, 
 }
 
 int exec_max_ctas_per_sm() {
+    if (exec_attr_once() != cudaSuccess) return 1;
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mpxa_exec_kernel, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mpxa_exec_kernel, kThreads, kDynSmem);
     return n;
 }
 

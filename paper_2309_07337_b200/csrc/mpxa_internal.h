@@ -16,7 +16,10 @@ namespace mpxa {
 
 constexpr int kMaxGpus = 32;       // processes or virtual GPUs per comm (signal masks are 32-bit)
 constexpr int kMaxCtas = 1024;     // CTAs per GPU per launch (flag slots per source GPU)
-constexpr int kThreads = 512;      // threads per CTA of the executor kernel
+constexpr int kThreads = 256;      // threads per CTA of the executor kernel (warp 0: TMA producer)
+constexpr int kStages = 6;         // TMA ring stages per CTA
+constexpr int kChunk = 16384;      // bytes per TMA stage
+constexpr int kMoveTile = 256;     // moves staged in shared memory at a time
 constexpr int kMaxWindows = 16;    // registered recv windows per process
 
 enum BufKind : uint8_t { BK_SEND = 0, BK_RECV = 1, BK_WORK = 2 };
@@ -24,19 +27,24 @@ enum BufKind : uint8_t { BK_SEND = 0, BK_RECV = 1, BK_WORK = 2 };
 // One copy of `len` units from (src_kind, src_rank, src_off) to (dst_kind, dst_rank, dst_off).
 // Offsets and lengths are in UNITS of ExecParams::unit bytes.  fanout = 1: copy to the
 // dst_kind buffer of EVERY rank at dst_off (allgather direct); dst_rank is ignored.
+// flow: identity of the data the move carries (its origin block / segment), preserved
+// along the data's path through the steps; CTAs own (flow group, column slice) pairs.
 struct Move {
     int64_t src_off;
     int64_t dst_off;
     int64_t len;
+    uint32_t flow;
     uint16_t src_rank;
     uint16_t dst_rank;
     uint8_t src_kind;
     uint8_t dst_kind;
     uint8_t fanout;
-    uint8_t pad;
+    uint8_t pad[5];
 };
-static_assert(sizeof(Move) == 32, "Move layout");
+static_assert(sizeof(Move) == 40, "Move layout");
 
+// Moves of a step are sorted by flow; findex[flow_index + x] = number of the step's moves
+// with flow < x (x = 0..nflows), so flow group [x0, x1) owns moves [findex[x0], findex[x1]).
 struct Step {
     int32_t move_begin;     // [move_begin, move_end) in the GPU's move array
     int32_t move_end;
@@ -44,12 +52,14 @@ struct Step {
     uint32_t wait_mask;     // remote GPUs that write into this GPU in this step
     int64_t total_len;      // sum of move lengths in units (host-side sizing)
     int64_t max_len;        // max move length in units (host-side path hints)
+    int64_t flow_index;     // offset of this step's flow index in GpuProg::findex
 };
-static_assert(sizeof(Step) == 32, "Step layout");
+static_assert(sizeof(Step) == 40, "Step layout");
 
 struct GpuProg {
     const Step *steps;
     const Move *moves;
+    const int32_t *findex;
     int32_t nsteps;
     int32_t nmoves;
 };
@@ -74,6 +84,10 @@ struct ExecParams {
     int32_t R;                 // ranks per GPU
     int32_t p;                 // ranks
     int32_t my_gpu;            // -1: emulated, GPU = blockIdx.y
+    int32_t nflows;            // flows of the program (same on every GPU)
+    int32_t nS;                // column slices per move; CTA c owns slice c % nS
+    int32_t nF;                // flow groups; CTA c owns flow group c / nS
+    int32_t pad1;
     uint64_t unit;             // bytes per unit
     uint64_t epoch;            // > 0, increases by one per launch on the comm
     uint64_t send_stride;      // bytes between consecutive local ranks' buffers

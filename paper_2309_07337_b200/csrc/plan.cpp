@@ -24,22 +24,35 @@ namespace {
 
 class Builder {
 public:
-    Builder(Program &P, int p, int R, int G) : P_(P), p_(p), R_(R), G_(G) {
+    Builder(Program &P, int p, int R, int G, int nflows) : P_(P), p_(p), R_(R), G_(G) {
         P_ = Program();
         P_.p = p; P_.R = R; P_.G = G;
+        P_.nflows = nflows;
         P_.steps.assign(G, {});
         P_.moves.assign(G, {});
+        P_.findex.assign(G, {});
         cur_.assign(G, {});
     }
-    void move(int sk, int sr, int64_t so, int dk, int dr, int64_t dof, int64_t len, int fan = 0) {
+    // flow < 0: the flow of the data currently at the source location (set by the move
+    // that wrote it); SEND-sourced moves pass their origin flow explicitly.
+    void move(int sk, int sr, int64_t so, int dk, int dr, int64_t dof, int64_t len, int64_t flow = -1,
+              int fan = 0) {
         if (len <= 0) return;
+        if (flow < 0) {
+            auto it = loc_.find(key(sk, sr, so));
+            flow = it == loc_.end() ? 0 : it->second;
+        }
         Move m{};
         m.src_off = so; m.dst_off = dof; m.len = len;
+        m.flow = (uint32_t)flow;
         m.src_rank = (uint16_t)sr; m.dst_rank = (uint16_t)dr;
         m.src_kind = (uint8_t)sk; m.dst_kind = (uint8_t)dk; m.fanout = (uint8_t)fan;
         cur_[sr / R_].push_back(m);
+        if (!fan) pending_.push_back({key(dk, dr, dof), (uint32_t)flow});
     }
     void end_step() {
+        for (auto &kv : pending_) loc_[kv.first] = kv.second;
+        pending_.clear();
         std::vector<uint32_t> sig(G_, 0), wt(G_, 0);
         for (int g = 0; g < G_; g++)
             for (const Move &m : cur_[g]) {
@@ -52,6 +65,8 @@ public:
                 }
             }
         for (int g = 0; g < G_; g++) {
+            std::stable_sort(cur_[g].begin(), cur_[g].end(),
+                             [](const Move &a, const Move &b) { return a.flow < b.flow; });
             Step s{};
             s.move_begin = (int32_t)P_.moves[g].size();
             int64_t tot = 0, mx = 0;
@@ -65,19 +80,30 @@ public:
             s.wait_mask = wt[g];
             s.total_len = tot;
             s.max_len = mx;
+            s.flow_index = (int64_t)P_.findex[g].size();
+            size_t q = 0;
+            for (int x = 0; x <= P_.nflows; x++) {       // findex[x] = #moves with flow < x
+                while (q < cur_[g].size() && cur_[g][q].flow < (uint32_t)x) q++;
+                P_.findex[g].push_back((int32_t)q);
+            }
             P_.steps[g].push_back(s);
             P_.max_move = std::max(P_.max_move, mx);
             P_.max_step_units = std::max(P_.max_step_units, tot);
+            P_.max_step_moves = std::max<int64_t>(P_.max_step_moves, (int64_t)cur_[g].size());
             P_.signals += __builtin_popcount(sig[g]);
             cur_[g].clear();
         }
     }
-    int gpu(int r) const { return r / R_; }
 
 private:
+    static uint64_t key(int k, int r, int64_t off) {
+        return ((uint64_t)k << 62) ^ ((uint64_t)r << 44) ^ (uint64_t)off;
+    }
     Program &P_;
     int p_, R_, G_;
     std::vector<std::vector<Move>> cur_;
+    std::unordered_map<uint64_t, uint32_t> loc_;
+    std::vector<std::pair<uint64_t, uint32_t>> pending_;
 };
 
 bool topo_ok(int p, int R, int G) {
@@ -91,22 +117,25 @@ bool topo_ok(int p, int R, int G) {
 // ---------------------------------------------------------------------------------------
 bool build_alltoall(Program &P, int algo, int p, int R, int G, int g, int stop_stage) {
     if (!topo_ok(p, R, G)) return false;
-    Builder B(P, p, R, G);
+    Builder B(P, p, R, G, p * p);
     if (algo == A_PAIRWISE) {
         // A3: step s sends to (r+s) mod p; all s run concurrently on the GPU.
         for (int s = 0; s < p; s++)
             for (int t = 0; t < p; t++) {
                 int j = imod(s + t, p);
-                B.move(BK_SEND, s, j, BK_RECV, j, s, 1);
+                B.move(BK_SEND, s, j, BK_RECV, j, s, 1, (int64_t)s * p + j);
             }
         B.end_step();
         P.work_units = 0;
         return true;
     }
     if (algo == A_BRUCK) {
-        // A4-A6: T_r[i] = send_r[(r+i) mod p]; rounds k: blocks with bit k of i set go to
-        // (r+2^k) mod p (packed into the peer's round-k staging, then unpacked into T at
-        // the same index); recv_r[j] = T_r[(r-j) mod p].
+        // A4-A6: T_r[i] = send_r[(r+i) mod p]; round k: the blocks with bit k of i set go, in
+        // increasing i, to (r+2^k) mod p, which keeps them as its new T[i]; finally
+        // recv_r[j] = T_r[(r-j) mod p].  Zero-copy receive: round k lands in the receiver's
+        // round-k area S_k and T[i] is thereafter READ from there (loc[i]) instead of being
+        // unpacked over the old T[i].  Every workspace byte is written once per launch, so no
+        // CTA ever overwrites data another CTA has still to read.
         const int K = ceil_log2(p);
         std::vector<int64_t> soff(K + 1, p);
         for (int k = 0; k < K; k++) {
@@ -115,31 +144,30 @@ bool build_alltoall(Program &P, int algo, int p, int R, int G, int g, int stop_s
             soff[k + 1] = soff[k] + mk;
         }
         P.work_units = soff[K];
+        std::vector<int64_t> loc(p);                         // current WORK offset of T[i]
+        for (int i = 0; i < p; i++) loc[i] = i;
         const int rounds = stop_stage < 0 ? K : std::min(stop_stage, K);
         for (int r = 0; r < p; r++)                          // A4 local rotation
-            for (int i = 0; i < p; i++) B.move(BK_SEND, r, imod(r + i, p), BK_WORK, r, i, 1);
+            for (int i = 0; i < p; i++) B.move(BK_SEND, r, imod(r + i, p), BK_WORK, r, i, 1, (int64_t)r * p + imod(r + i, p));
         B.end_step();
         for (int k = 0; k < rounds; k++) {                   // A5 bit-indexed rounds
             const int d = 1 << k;
             for (int r = 0; r < p; r++) {
                 int64_t pos = 0;
                 for (int i = 0; i < p; i++)
-                    if ((i >> k) & 1) B.move(BK_WORK, r, i, BK_WORK, imod(r + d, p), soff[k] + pos++, 1);
+                    if ((i >> k) & 1) B.move(BK_WORK, r, loc[i], BK_WORK, imod(r + d, p), soff[k] + pos++, 1);
             }
             B.end_step();
-            for (int r = 0; r < p; r++) {
-                int64_t pos = 0;
-                for (int i = 0; i < p; i++)
-                    if ((i >> k) & 1) B.move(BK_WORK, r, soff[k] + pos++, BK_WORK, r, i, 1);
-            }
-            B.end_step();
+            int64_t pos = 0;
+            for (int i = 0; i < p; i++)
+                if ((i >> k) & 1) loc[i] = soff[k] + pos++;
         }
         if (stop_stage < 0) {                                // A6 inverse rotation
             for (int r = 0; r < p; r++)
-                for (int j = 0; j < p; j++) B.move(BK_WORK, r, imod(r - j, p), BK_RECV, r, j, 1);
+                for (int j = 0; j < p; j++) B.move(BK_WORK, r, loc[imod(r - j, p)], BK_RECV, r, j, 1);
         } else {                                             // dump T for stage tests
             for (int r = 0; r < p; r++)
-                for (int i = 0; i < p; i++) B.move(BK_WORK, r, i, BK_RECV, r, i, 1);
+                for (int i = 0; i < p; i++) B.move(BK_WORK, r, loc[i], BK_RECV, r, i, 1);
         }
         B.end_step();
         return true;
@@ -159,18 +187,18 @@ bool build_alltoall(Program &P, int algo, int p, int R, int G, int g, int stop_s
 // ---------------------------------------------------------------------------------------
 bool build_allgather(Program &P, int algo, int p, int R, int G, int stop_stage) {
     if (!topo_ok(p, R, G)) return false;
-    Builder B(P, p, R, G);
+    Builder B(P, p, R, G, p);
     if (algo == A_PAIRWISE) {
         // direct: read send_s once, store it into block s of every rank's recvbuf
-        for (int s = 0; s < p; s++) B.move(BK_SEND, s, 0, BK_RECV, 0, s, 1, /*fanout=*/1);
+        for (int s = 0; s < p; s++) B.move(BK_SEND, s, 0, BK_RECV, 0, s, 1, s, /*fanout=*/1);
         B.end_step();
         return true;
     }
     if (algo == A_RING) {
         // recv_r[r] = send_r; step s: r sends block (r-s) mod p to r+1.
         for (int r = 0; r < p; r++) {
-            B.move(BK_SEND, r, 0, BK_RECV, r, r, 1);
-            if (p > 1) B.move(BK_SEND, r, 0, BK_RECV, imod(r + 1, p), r, 1);
+            B.move(BK_SEND, r, 0, BK_RECV, r, r, 1, r);
+            if (p > 1) B.move(BK_SEND, r, 0, BK_RECV, imod(r + 1, p), r, 1, r);
         }
         B.end_step();
         for (int s = 1; s < p - 1; s++) {
@@ -188,7 +216,7 @@ bool build_allgather(Program &P, int algo, int p, int R, int G, int stop_stage) 
         const int K = ceil_log2(p);
         P.work_units = p;
         const int rounds = stop_stage < 0 ? K : std::min(stop_stage, K);
-        for (int r = 0; r < p; r++) B.move(BK_SEND, r, 0, BK_WORK, r, 0, 1);
+        for (int r = 0; r < p; r++) B.move(BK_SEND, r, 0, BK_WORK, r, 0, 1, r);
         B.end_step();
         for (int k = 0; k < rounds; k++) {
             const int d = 1 << k, nk = std::min(d, p - d);
@@ -220,11 +248,11 @@ bool build_alltoallv(Program &P, int algo, int p, int R, int G, int g, const int
     auto SD = [&](int s, int j) { return sd[(size_t)s * p + j]; };
     auto RD = [&](int j, int s) { return rd[(size_t)j * p + s]; };
     if (algo == A_PAIRWISE) {
-        Builder B(P, p, R, G);
+        Builder B(P, p, R, G, p * p);
         for (int s = 0; s < p; s++)
             for (int t = 0; t < p; t++) {
                 int j = imod(s + t, p);
-                B.move(BK_SEND, s, SD(s, j), BK_RECV, j, RD(j, s), C(s, j));
+                B.move(BK_SEND, s, SD(s, j), BK_RECV, j, RD(j, s), C(s, j), (int64_t)s * p + j);
             }
         B.end_step();
         P.work_units = 0;
@@ -263,21 +291,22 @@ bool build_alltoallv(Program &P, int algo, int p, int R, int G, int g, const int
             }
         return o;
     };
-    Builder B(P, p, R, G);
+    Builder B(P, p, R, G, p * p);
     P.work_units = work;
     // step 1: intra-group direct + gather to leaders
     for (int r = 0; r < p; r++) {
         int A = r / g, s = r % g;
         for (int t = 0; t < g; t++) {
             int j = A * g + t;
-            B.move(BK_SEND, r, SD(r, j), BK_RECV, j, RD(j, r), C(r, j));
+            B.move(BK_SEND, r, SD(r, j), BK_RECV, j, RD(j, r), C(r, j), (int64_t)r * p + j);
         }
         for (int Bg = 0; Bg < NG; Bg++) {
             if (Bg == A) continue;
             int lead = L(A, Bg);
             for (int t = 0; t < g; t++) {
                 int j = Bg * g + t;
-                B.move(BK_SEND, r, SD(r, j), BK_WORK, lead, out_off[(size_t)A * NG + Bg] + segoff(A, Bg, s, t), C(r, j));
+                B.move(BK_SEND, r, SD(r, j), BK_WORK, lead, out_off[(size_t)A * NG + Bg] + segoff(A, Bg, s, t), C(r, j),
+                       (int64_t)r * p + j);
             }
         }
     }

@@ -4,6 +4,7 @@
 #pragma once
 #include <stdint.h>
 
+#include <unordered_map>
 #include <vector>
 
 #include "mpxa_internal.h"
@@ -14,9 +15,12 @@ struct Program {
     int p = 0, R = 1, G = 1;
     std::vector<std::vector<Step>> steps;  // [G][nsteps]
     std::vector<std::vector<Move>> moves;  // [G][...]
+    std::vector<std::vector<int32_t>> findex;  // [G][...] per-step flow indexes
+    int nflows = 1;
     int64_t work_units = 0;                // WORK units needed per rank
     int64_t max_move = 0;                  // longest move (units)
     int64_t max_step_units = 0;            // max over (GPU, step) of the summed move units
+    int64_t max_step_moves = 0;            // max over (GPU, step) of the move count
     int64_t signals = 0;                   // inter-GPU signals per launch (GPU-pair messages)
     int nsteps() const { return steps.empty() ? 0 : (int)steps[0].size(); }
 };

@@ -44,20 +44,21 @@ class InitArgs(ctypes.Structure):
 
 class PlanMove(ctypes.Structure):
     _fields_ = [("src_off", ctypes.c_int64), ("dst_off", ctypes.c_int64), ("len", ctypes.c_int64),
-                ("src_rank", ctypes.c_uint16), ("dst_rank", ctypes.c_uint16),
+                ("flow", ctypes.c_uint32), ("src_rank", ctypes.c_uint16), ("dst_rank", ctypes.c_uint16),
                 ("src_kind", ctypes.c_uint8), ("dst_kind", ctypes.c_uint8),
-                ("fanout", ctypes.c_uint8), ("pad", ctypes.c_uint8)]
+                ("fanout", ctypes.c_uint8), ("pad", ctypes.c_uint8 * 5)]
 
 
 class PlanStep(ctypes.Structure):
     _fields_ = [("move_begin", ctypes.c_int32), ("move_end", ctypes.c_int32),
                 ("signal_mask", ctypes.c_uint32), ("wait_mask", ctypes.c_uint32),
-                ("total_len", ctypes.c_int64), ("max_len", ctypes.c_int64)]
+                ("total_len", ctypes.c_int64), ("max_len", ctypes.c_int64), ("flow_index", ctypes.c_int64)]
 
 
 class PlanInfo(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in
-                ("nsteps", "work_units", "max_move", "max_step_units", "signals", "total_moves")]
+                ("nsteps", "work_units", "max_move", "max_step_units", "signals", "total_moves", "nflows",
+                 "max_step_moves")]
 
 
 # every symbol of include/mpxa.h and include/mpxa_plan.h, with its ctypes signature
