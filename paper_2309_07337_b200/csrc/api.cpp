@@ -9,6 +9,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <fstream>
@@ -140,7 +141,8 @@ struct mpxa_comm_s {
     size_t work_bytes = 0;                     // per program GPU
     char *work_map[kMaxGpus] = {};
     int32_t *err_host = nullptr, *err_dev = nullptr;
-    char **win_table_dev = nullptr;            // [G][kMaxWindows]
+    DevComm *dc = nullptr;                     // device-resident comm state (tables, epoch)
+    DevComm dc_host;                           // host mirror of the tables
     std::vector<Window> windows;               // local registered windows (multi-process)
     std::vector<std::vector<char *>> win_map;  // [window][gpu] mapped bases
 
@@ -200,6 +202,17 @@ int ipc_exchange(mpxa_comm_t c, void *local, char **mapped) {
     return MPXA_SUCCESS;
 }
 
+// copy the host mirror of the device tables (work bases, symmetric regions, windows)
+int upload_tables(mpxa_comm_t c) {
+    if (!c->dc) return MPXA_SUCCESS;
+    for (int g = 0; g < c->G; g++) {
+        c->dc_host.work_base[g] = c->work_map[g];
+        c->dc_host.sym[g] = c->sym_map[g];
+    }
+    CK(cudaMemcpy(c->dc, &c->dc_host, offsetof(DevComm, epoch), cudaMemcpyHostToDevice));
+    return MPXA_SUCCESS;
+}
+
 int ensure_work(mpxa_comm_t c, size_t need_per_gpu) {
     if (need_per_gpu <= c->work_bytes) return MPXA_SUCCESS;
     size_t nb = std::max(need_per_gpu, c->work_bytes * 2);
@@ -221,7 +234,7 @@ int ensure_work(mpxa_comm_t c, size_t need_per_gpu) {
     } else {
         for (int g = 0; g < c->G; g++) c->work_map[g] = c->work_local + (size_t)g * nb;
     }
-    return MPXA_SUCCESS;
+    return upload_tables(c);
 }
 
 // ---- selector -------------------------------------------------------------------------
@@ -299,44 +312,30 @@ int make_params(mpxa_comm_t c, ExecParams &E, const DevProg &dp, const char *sen
                 uint64_t unit, uint64_t send_stride, uint64_t recv_stride) {
     memset(&E, 0, sizeof E);
     E.progs = (const GpuProg *)dp.dmem;
-    E.G = c->G;
-    E.R = c->Rg;
-    E.p = c->p;
-    E.nflows = dp.host.nflows;
-    E.my_gpu = c->emulated ? -1 : (c->nprocs > 1 ? c->proc : 0);
+    E.dc = c->dc;
+    E.send = send;
+    E.recv = recv;
     E.unit = unit;
     E.send_stride = send_stride;
     E.recv_stride = recv_stride;
     E.work_stride = (uint64_t)dp.host.work_units * unit;
     E.err = c->err_dev;
     E.timeout_ns = (int64_t)(c->timeout_s * 1e9);
-    E.win_table = c->win_table_dev;
+    E.G = c->G;
+    E.R = c->Rg;
+    E.p = c->p;
+    E.nflows = dp.host.nflows;
+    E.my_gpu = c->emulated ? -1 : (c->nprocs > 1 ? c->proc : 0);
+    E.mode = c->emulated ? 1 : (c->nprocs > 1 ? 2 : 0);
     if (c->nprocs > 1) {
-        int me = c->proc;
-        E.send_base[me] = (char *)send;
-        E.recv_base[me] = recv;
-        for (int d = 0; d < c->G; d++) { E.work_base[d] = c->work_map[d]; E.sym[d] = (SymRegion *)c->sym_map[d]; }
-        // remote recv bases: from the CTS message (registered windows)
-        E.recv_from_cts = 1;
+        // remote recv bases are resolved on the device from the CTS message (window + offset)
         uintptr_t r = (uintptr_t)recv;
         int wi = -1;
         for (size_t w = 0; w < c->windows.size(); w++)
             if (r >= c->windows[w].base && r < c->windows[w].base + c->windows[w].size) { wi = (int)w; break; }
         if (wi < 0) return MPXA_ERR_UNREGISTERED;
-        E.recv_win[me] = (uint64_t)wi;
-        E.recv_off[me] = r - c->windows[wi].base;
-    } else {
-        for (int g = 0; g < c->G; g++) {
-            E.send_base[g] = (char *)send + (size_t)g * c->Rg * send_stride;
-            E.recv_base[g] = recv + (size_t)g * c->Rg * recv_stride;
-            E.work_base[g] = c->work_map[g];
-            E.sym[g] = c->sym_local + g;
-            if (c->emulated) {   // exercise the CTS-carried recv resolution: base 0 + absolute address
-                E.recv_win[g] = 0;
-                E.recv_off[g] = (uint64_t)(uintptr_t)E.recv_base[g];
-            }
-        }
-        E.recv_from_cts = c->emulated ? 1 : 0;
+        E.recv_win = (uint64_t)wi;
+        E.recv_off = r - c->windows[wi].base;
     }
     return MPXA_SUCCESS;
 }
@@ -354,7 +353,7 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
     const Grid gr = grid ? *grid : choose_grid(c, dp.host, unit);
     E.nS = gr.nS;
     E.nF = gr.nF;
-    E.epoch = ++c->epoch;
+    ++c->epoch;   // host mirror only; the kernels keep the authoritative epoch in DevComm
     cudaError_t e = launch_exec(E, gr.n(), c->emulated ? c->G : 1, c->emulated, stream);
     if (e != cudaSuccess) {
         if (getenv("MPXA_DEBUG")) fprintf(stderr, "mpxa: launch failed: %s\n", cudaGetErrorString(e));
@@ -610,8 +609,9 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     int nsym = c->emulated ? c->G : 1;
     CK(cudaMalloc((void **)&c->sym_local, sizeof(SymRegion) * nsym));
     CK(cudaMemset(c->sym_local, 0, sizeof(SymRegion) * nsym));
-    CK(cudaMalloc((void **)&c->win_table_dev, sizeof(char *) * kMaxGpus * kMaxWindows));
-    CK(cudaMemset(c->win_table_dev, 0, sizeof(char *) * kMaxGpus * kMaxWindows));
+    CK(cudaMalloc((void **)&c->dc, sizeof(DevComm)));
+    CK(cudaMemset(c->dc, 0, sizeof(DevComm)));
+    memset(&c->dc_host, 0, sizeof(DevComm));
     if (c->nprocs > 1) {
         // consistency of the topology across processes (MPXA_ERR_MISMATCH)
         int mine[3] = {c->R, c->g, c->nprocs};
@@ -670,7 +670,7 @@ int mpxa_finalize(mpxa_comm_t c) {
     }
     if (c->work_local) cudaFree(c->work_local);
     if (c->sym_local) cudaFree(c->sym_local);
-    if (c->win_table_dev) cudaFree(c->win_table_dev);
+    if (c->dc) cudaFree(c->dc);
     if (c->err_host) cudaFreeHost(c->err_host);
     if (c->counts_tmp) cudaFree(c->counts_tmp);
     delete c;
@@ -744,11 +744,9 @@ int mpxa_register(mpxa_comm_t c, void *ptr, size_t bytes) {
     int wi = (int)c->windows.size();
     c->windows.push_back(Window{base, size});
     c->win_map.push_back(mapped);
-    std::vector<char *> col(c->nprocs);
-    for (int d = 0; d < c->nprocs; d++)
-        CK(cudaMemcpy(c->win_table_dev + (size_t)d * kMaxWindows + wi, &mapped[d], sizeof(char *),
-                      cudaMemcpyHostToDevice));
-    return MPXA_SUCCESS;
+    for (int d = 0; d < c->nprocs; d++) c->dc_host.win_table[(size_t)d * kMaxWindows + wi] = mapped[d];
+    CK(cudaDeviceSynchronize());
+    return upload_tables(c);
 }
 
 int mpxa_deregister(mpxa_comm_t c, void *ptr) {

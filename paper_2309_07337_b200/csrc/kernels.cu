@@ -163,7 +163,7 @@ constexpr uint64_t kLsuBig = 8192;       // misaligned slices at least this long
 constexpr int kWarps = kThreads / 32;
 constexpr int kLsuWarps = kWarps - 1;    // warp 0 is the TMA producer
 constexpr int kLsuThreads = kThreads - 32;
-constexpr int kAhead = kStages - 2;      // TMA loads in flight ahead of the oldest store
+constexpr int kAhead = MPXA_AHEAD;       // TMA loads in flight ahead of the oldest store
 
 // ---- TMA bulk copies (cp.async.bulk: SASS UBLKCP) --------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -193,7 +193,11 @@ __device__ __forceinline__ void bulk_wait_read(int n) {
         case 1: asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); break;
         case 2: asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory"); break;
         case 3: asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory"); break;
-        default: asm volatile("cp.async.bulk.wait_group.read 4;" ::: "memory"); break;
+        case 4: asm volatile("cp.async.bulk.wait_group.read 4;" ::: "memory"); break;
+        case 5: asm volatile("cp.async.bulk.wait_group.read 5;" ::: "memory"); break;
+        case 6: asm volatile("cp.async.bulk.wait_group.read 6;" ::: "memory"); break;
+        case 7: asm volatile("cp.async.bulk.wait_group.read 7;" ::: "memory"); break;
+        default: asm volatile("cp.async.bulk.wait_group.read 8;" ::: "memory"); break;
     }
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
@@ -215,9 +219,12 @@ struct RingEntry {
 
 struct ExecShared {
     char *recv_base[kMaxGpus];
+    char *work_base[kMaxGpus];
+    SymRegion *sym[kMaxGpus];
     Move moves[kMoveTile];
     uint64_t mbar[kStages];
     RingEntry ring[kStages];
+    uint64_t epoch;      // this launch's epoch (device-side sequence number)
     uint32_t cts_ok;     // remote GPUs whose CTS for this epoch was observed
     int abort_flag;
 };
@@ -225,9 +232,10 @@ struct ExecShared {
 __device__ __forceinline__ char *base_of(const ExecParams &P, const ExecShared &S, int kind, int rank) {
     int g = rank / P.R;
     uint64_t local = (uint64_t)(rank - g * P.R);
-    if (kind == BK_SEND) return P.send_base[g] + local * P.send_stride;
+    if (kind == BK_SEND)   // sources are always local: only this process's (or virtual GPU's) ranks
+        return (char *)P.send + (P.mode == 2 ? 0 : (uint64_t)g * P.R * P.send_stride) + local * P.send_stride;
     if (kind == BK_RECV) return S.recv_base[g] + local * P.recv_stride;
-    return P.work_base[g] + local * P.work_stride;
+    return S.work_base[g] + local * P.work_stride;
 }
 
 // Spin (threads < 32, one per bit of mask) until *slot(bit) >= want; sets abort on timeout.
@@ -349,26 +357,37 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
     const GpuProg prog = P.progs[g];
-    const bool multi = P.G > 1;
+    const bool multi = P.G > 1;   // emulated or multi-process: flags + CTS
     Producer prod;
     prod.stages = dyn_smem;
 
-    if (t < kMaxGpus) S.recv_base[t] = P.recv_base[t];
+    if (t < P.G) {
+        S.work_base[t] = P.dc->work_base[t];
+        S.sym[t] = P.dc->sym[t];
+        // own / local recv bases; remote ones (emulated, multi-process) arrive with the CTS
+        S.recv_base[t] = P.mode == 0 ? P.recv
+                         : P.mode == 1 ? (t == g ? P.recv + (uint64_t)t * P.R * P.recv_stride : nullptr)
+                                       : (t == g ? P.recv : nullptr);
+    }
     if (t == 0) {
         S.cts_ok = 0;
         S.abort_flag = 0;
+        S.epoch = *(volatile uint64_t *)&P.dc->epoch + 1;
         for (int s = 0; s < kStages; s++) mbar_init(smem_u32(&S.mbar[s]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // CTS: this GPU is inside epoch `epoch`, so every earlier use of its buffers is complete
-    // (stream order); tell every peer it may write into them.
-    if (multi && c == 0 && t < P.G && t != g) {
-        CtsSlot *slot = &P.sym[t]->cts[g];
-        if (P.recv_from_cts) { slot->win = P.recv_win[g]; slot->off = P.recv_off[g]; }
-        __threadfence_system();
-        st_release_sys(&slot->epoch, P.epoch);
-    }
     __syncthreads();
+    const uint64_t epoch = S.epoch;
+    // CTS: this GPU is inside `epoch`, so every earlier use of its buffers is complete
+    // (stream order); tell every peer it may write into them, and where its recvbuf is
+    // (registered window + offset; emulated GPUs: window 0 has base 0, offset = address).
+    if (multi && c == 0 && t < P.G && t != g) {
+        CtsSlot *slot = &S.sym[t]->cts[g];
+        if (P.mode == 2) { slot->win = P.recv_win; slot->off = P.recv_off; }
+        else { slot->win = 0; slot->off = (uint64_t)(uintptr_t)(P.recv + (uint64_t)g * P.R * P.recv_stride); }
+        __threadfence_system();
+        st_release_sys(&slot->epoch, epoch);
+    }
 
     const int64_t x0 = (int64_t)f * P.nflows / P.nF, x1 = (int64_t)(f + 1) * P.nflows / P.nF;
     for (int s = 0; s < prog.nsteps; s++) {
@@ -376,15 +395,15 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
         if (multi) {
             // data written into this GPU by peers in step s-1 (this CTA's share) must have landed
             if (s > 0 && prog.steps[s - 1].wait_mask)
-                wait_mask_ge(P, S, prog.steps[s - 1].wait_mask, &P.sym[g]->flags[0][c], kMaxCtas,
-                             (P.epoch << 8) | (uint64_t)s);
+                wait_mask_ge(P, S, prog.steps[s - 1].wait_mask, &S.sym[g]->flags[0][c], kMaxCtas,
+                             (epoch << 8) | (uint64_t)s);
             // peers written in this step must have cleared us to send in this epoch
             uint32_t need = st.signal_mask & ~S.cts_ok;
             if (need) {
-                wait_mask_ge(P, S, need, &P.sym[g]->cts[0].epoch, sizeof(CtsSlot) / 8, P.epoch);
-                if (P.recv_from_cts && t < 32 && ((need >> t) & 1u)) {
-                    const CtsSlot *cs = &P.sym[g]->cts[t];
-                    S.recv_base[t] = P.win_table[t * kMaxWindows + cs->win] + cs->off;
+                wait_mask_ge(P, S, need, &S.sym[g]->cts[0].epoch, sizeof(CtsSlot) / 8, epoch);
+                if (t < 32 && ((need >> t) & 1u)) {
+                    const CtsSlot *cs = &S.sym[g]->cts[t];
+                    S.recv_base[t] = P.dc->win_table[t * kMaxWindows + cs->win] + cs->off;
                 }
             }
             __syncthreads();
@@ -450,14 +469,24 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
         // ---- signal the peers written in this step (this CTA's share) ----
         if (multi && st.signal_mask && t < 32 && ((st.signal_mask >> t) & 1u)) {
             __threadfence_system();
-            st_release_sys(&P.sym[t]->flags[g][c], (P.epoch << 8) | (uint64_t)(s + 1));
+            st_release_sys(&S.sym[t]->flags[g][c], (epoch << 8) | (uint64_t)(s + 1));
         }
     }
     // completion: everything peers write into this GPU in the last step has landed
     if (multi && prog.nsteps > 0 && prog.steps[prog.nsteps - 1].wait_mask) {
-        wait_mask_ge(P, S, prog.steps[prog.nsteps - 1].wait_mask, &P.sym[g]->flags[0][c], kMaxCtas,
-                     (P.epoch << 8) | (uint64_t)prog.nsteps);
+        wait_mask_ge(P, S, prog.steps[prog.nsteps - 1].wait_mask, &S.sym[g]->flags[0][c], kMaxCtas,
+                     (epoch << 8) | (uint64_t)prog.nsteps);
         __syncthreads();
+    }
+    // the last CTA of the launch publishes the epoch (the next launch is stream-ordered after)
+    if (multi && t == 0) {
+        __threadfence();
+        const uint32_t total = gridDim.x * gridDim.y;
+        if (atomicAdd(&P.dc->done_ctas, 1u) == total - 1) {
+            P.dc->done_ctas = 0;
+            P.dc->epoch = epoch;
+            __threadfence();
+        }
     }
 }
 

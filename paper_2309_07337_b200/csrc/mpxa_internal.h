@@ -17,8 +17,17 @@ namespace mpxa {
 constexpr int kMaxGpus = 32;       // processes or virtual GPUs per comm (signal masks are 32-bit)
 constexpr int kMaxCtas = 1024;     // CTAs per GPU per launch (flag slots per source GPU)
 constexpr int kThreads = 256;      // threads per CTA of the executor kernel (warp 0: TMA producer)
-constexpr int kStages = 6;         // TMA ring stages per CTA
-constexpr int kChunk = 16384;      // bytes per TMA stage
+#ifndef MPXA_STAGES
+#define MPXA_STAGES 6
+#endif
+#ifndef MPXA_CHUNK
+#define MPXA_CHUNK 16384
+#endif
+#ifndef MPXA_AHEAD
+#define MPXA_AHEAD (MPXA_STAGES - 2)
+#endif
+constexpr int kStages = MPXA_STAGES;   // TMA ring stages per CTA
+constexpr int kChunk = MPXA_CHUNK;     // bytes per TMA stage
 constexpr int kMoveTile = 256;     // moves staged in shared memory at a time
 constexpr int kMaxWindows = 16;    // registered recv windows per process
 
@@ -78,8 +87,32 @@ struct SymRegion {
     uint64_t flags[kMaxGpus][kMaxCtas];       // flags[s][c]: src GPU s, CTA c, (epoch<<8)|(step+1)
 };
 
+// Per-communicator device-resident state (rewritten by the host only between launches:
+// heap growth, buffer registration).  epoch/done make the launch sequence number
+// device-side, so a captured CUDA graph replays with fresh epochs.
+struct DevComm {
+    char *work_base[kMaxGpus];              // per GPU: workspace heap (mapped here)
+    SymRegion *sym[kMaxGpus];               // per GPU: symmetric region (mapped here)
+    char *win_table[kMaxGpus * kMaxWindows];  // per GPU: registered recv windows (mapped here)
+    uint64_t epoch;                         // epochs completed on this GPU (or emulated set)
+    uint32_t done_ctas;                     // CTAs of the current launch that finished
+    uint32_t pad;
+};
+
+// Launch parameters (~130 B).  Buffers are the caller's process-level rank-major buffers.
 struct ExecParams {
     const GpuProg *progs;      // device array [G] (only progs[my_gpu] used in multi-process)
+    DevComm *dc;
+    const char *send;          // this process's sendbuf (first local rank)
+    char *recv;                // this process's recvbuf
+    uint64_t unit;             // bytes per unit
+    uint64_t send_stride;      // bytes between consecutive local ranks' buffers
+    uint64_t recv_stride;
+    uint64_t work_stride;
+    uint64_t recv_win;         // multi-process: registered window of recv, and its offset
+    uint64_t recv_off;
+    int32_t *err;              // host-mapped error word (watchdog)
+    int64_t timeout_ns;
     int32_t G;                 // GPUs (processes or virtual)
     int32_t R;                 // ranks per GPU
     int32_t p;                 // ranks
@@ -87,23 +120,7 @@ struct ExecParams {
     int32_t nflows;            // flows of the program (same on every GPU)
     int32_t nS;                // column slices per move; CTA c owns slice c % nS
     int32_t nF;                // flow groups; CTA c owns flow group c / nS
-    int32_t pad1;
-    uint64_t unit;             // bytes per unit
-    uint64_t epoch;            // > 0, increases by one per launch on the comm
-    uint64_t send_stride;      // bytes between consecutive local ranks' buffers
-    uint64_t recv_stride;
-    uint64_t work_stride;
-    char *send_base[kMaxGpus]; // per GPU: buffer of its first local rank (mapped here)
-    char *recv_base[kMaxGpus];
-    char *work_base[kMaxGpus];
-    SymRegion *sym[kMaxGpus];  // per GPU symmetric region (mapped here)
-    uint64_t recv_win[kMaxGpus];  // per GPU: window index of its recvbuf (recv_from_cts mode)
-    uint64_t recv_off[kMaxGpus];  // per GPU: byte offset of its recvbuf in that window
-    char *const *win_table;    // device [G][kMaxWindows] window bases (recv_from_cts mode)
-    int32_t recv_from_cts;     // remote RECV bases come from the CTS message
-    int32_t pad0;
-    int32_t *err;              // host-mapped error word (watchdog)
-    int64_t timeout_ns;
+    int32_t mode;              // 0 single GPU, 1 emulated GPUs, 2 multi-process
 };
 
 }  // namespace mpxa

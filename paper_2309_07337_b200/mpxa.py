@@ -14,7 +14,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmpxa.so")
+LIB_PATH = os.environ.get("MPXA_LIB") or os.path.join(_HERE, "libmpxa.so")   # MPXA_LIB: tuning builds
 
 # ---- constants (mirror include/mpxa.h) ------------------------------------------------
 SUCCESS, ERR_ARG, ERR_ALGO, ERR_LIFECYCLE, ERR_TOPOLOGY, ERR_MISMATCH, ERR_CUDA, ERR_TIMEOUT, \

@@ -357,3 +357,32 @@ def test_full_size_cfg2_allgather_64MiB_sampled():
         assert np.array_equal(r, oracle.allgather_definition(s)), algo
         for r_ in range(p):
             assert torch.equal(recv[r_].view(p, b), send), algo
+
+
+def test_graph_replay_device_epochs():
+    """CUDA-graph capture of several collectives, replayed repeatedly: epochs live on the
+    device, so the emulated multi-GPU flag protocol stays consistent across replays."""
+    p, b = 8, 4096 + 16
+    for G in (0, 4, 8):
+        c = comm(p, G, 2)
+        for algo in ("pairwise", "bruck", "hier"):
+            send = synth.alltoall_sendbuf(G, p, b)
+            d_send = dev(send)
+            d_recv = torch.zeros_like(d_send)
+            s = torch.cuda.Stream()
+            c.alltoall(d_send, d_recv, algo=algo, stream=s)      # compile + warm outside capture
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(3):
+                    c.alltoall(d_send, d_recv, algo=algo, stream=s)
+            for rep in range(4):
+                fresh = synth.alltoall_sendbuf(100 + rep, p, b)
+                d_send.copy_(dev(fresh))
+                d_recv.zero_()
+                torch.cuda.synchronize()
+                g.replay()
+                torch.cuda.synchronize()
+                assert np.array_equal(host(d_recv), oracle.alltoall_definition(fresh)), (G, algo, rep)
+            assert c.check() == 0
+            del g
