@@ -158,16 +158,17 @@ def time_graph(fn, calls, stream):
     with torch.cuda.graph(g, stream=stream):
         for _ in range(calls):
             fn()
-    g.replay()
-    torch.cuda.synchronize()
     times = []
-    for _ in range(5):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+    with torch.cuda.stream(stream):          # replay() launches on the current stream
         g.replay()
-        e1.record(stream)
         torch.cuda.synchronize()
-        times.append(e0.elapsed_time(e1) / calls)
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            g.replay()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / calls)
     del g
     return statistics.median(times)
 
@@ -293,9 +294,16 @@ def gpu_arm(args):
     # ---- metric ----
     total_recv = p * p * b                      # all ranks, bytes received (incl. own block)
     value = total_recv / (ms * 1e-3) / 1e9
-    # algorithmic HBM bytes of the kernel on this GPU: read R*b, write R*p*b (+ peer-in)
+    # algorithmic bytes of the kernel on this GPU.  1 GPU: HBM read R*b + write R*p*b.
+    # N GPUs: NVLink ingress per GPU (p-R)*b*R (every hosted rank receives p-R remote blocks)
     hbm_bytes = R * b + R * p * b
-    achieved = hbm_bytes / (ms * 1e-3) / 1e9
+    nvl_bytes = R * (p - R) * b
+    if ws == 1:
+        bound, alg_bytes, peak_use, peak_note = "hbm", hbm_bytes, peak, peak_src
+    else:
+        bound, alg_bytes, peak_use, peak_note = ("nvlink", nvl_bytes, 770.0,
+                                                 "measured peer copy 770 GB/s/direction (B200_PROFILING.md); 900 nominal")
+    achieved = alg_bytes / (ms * 1e-3) / 1e9
     # ---- e2e through host buffers (pinned), same metric ----
     e2e = None
     if not args.no_e2e:
@@ -311,6 +319,23 @@ def gpu_arm(args):
         e_ms = time_loop(e2e_step, max(3, min(args.steps, 10)), 2, stream, ws)
         e2e = {"value": round(total_recv / (e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": R * b, "d2h_bytes_per_step": R * p * b, "ms_per_step": round(e_ms, 4)}
+    # ---- NCCL baseline on the same buffers (N > 1 only; NCCL needs one rank per GPU) ----
+    nccl = None
+    if ws > 1:
+        import torch.distributed as dist
+        gathered = torch.empty((N, R * b), dtype=torch.uint8, device="cuda")
+
+        def nccl_step():
+            dist.all_gather_into_tensor(gathered, send.view(-1))
+            if R > 1:   # every hosted rank needs the full concatenation (rank-major layout)
+                recv.view(R, p * b).copy_(gathered.view(1, p * b).expand(R, p * b))
+            else:
+                recv.view(-1).copy_(gathered.view(-1))
+
+        n_ms = time_loop(nccl_step, max(3, min(args.steps, 20)), 3, stream, ws)
+        nccl = {"impl": "torch.distributed all_gather_into_tensor (NCCL %s) + local replication" %
+                        ".".join(map(str, torch.cuda.nccl.version())),
+                "ms_per_step": round(n_ms, 5), "value": round(total_recv / (n_ms * 1e-3) / 1e9, 3), "unit": "GB/s"}
     sw = None
     if args.sweep and ws == 1:
         sw = sweep(comm, torch, stream)
@@ -333,16 +358,24 @@ def gpu_arm(args):
                        "ranks_per_gpu": R, "bytes_per_rank": b, "variant": algo,
                        "l2": "inputs larger than L2 (send 512 MiB, recv 4 GiB)"},
             "verified_sampled_vs_oracle": verified,
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": None,
-                         "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": hbm_bytes,
+            "roofline": {"bound": bound, "achieved": round(achieved, 1), "peak": peak_use, "unit": "GB/s",
+                         "frac": round(achieved / peak_use, 4), "traffic": None,
+                         "peak_source": peak_note,
+                         "algorithmic_bytes_per_launch": alg_bytes,
                          "kernel": "mpxa_exec_kernel (one launch per step; CUDA events on its stream)"},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "nccl": nccl,
             "clocks": clk.report(), "sweep": sw,
         }
         if args.traffic is not None:
             line["roofline"]["traffic"] = args.traffic
+        else:
+            tpath = os.path.join(ROOT, "profiles", "traffic.json")
+            key = f"allgather_p{p}_R{R}_{b}_{algo}"
+            if os.path.exists(tpath):
+                t = json.load(open(tpath)).get(key)
+                if t:
+                    line["roofline"]["traffic"] = t["bytes"]
+                    line["roofline"]["traffic_source"] = t["source"]
         print(json.dumps(line))
     if ws > 1:
         import torch.distributed as dist

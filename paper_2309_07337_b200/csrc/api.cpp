@@ -6,6 +6,7 @@
 // every implementation selectable.  Argument contract and lifecycle errors
 // follow SPEC.md:204-216, 239-247, 282-325 (interfaces only).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <string.h>
 
 #include <algorithm>
@@ -52,6 +53,7 @@ namespace {
 constexpr uint64_t kBytesPerCta = 65536;   // launch sizing target per CTA per step
 constexpr uint64_t kSliceBytes = 16384;    // target column-slice length of the longest move
 constexpr uint64_t kMovesPerCta = 8;       // small moves per CTA (latency-bound regime)
+constexpr uint64_t kMinSlice = 4096;       // smallest slice worth a CTA when filling the GPU
 
 // A program uploaded to device memory: [GpuProg x G][steps][moves].
 struct DevProg {
@@ -59,6 +61,7 @@ struct DevProg {
     size_t bytes = 0;
     Program host;
     int nsteps = 0;
+    std::vector<GpuProg> gp;   // the [G] GpuProg table as uploaded (device pointers)
 };
 
 size_t serialize(const Program &P, std::vector<char> &buf, uintptr_t dbase) {
@@ -261,6 +264,7 @@ int upload_program(const Program &P, std::shared_ptr<DevProg> &out) {
     std::vector<char> buf;
     serialize(P, buf, (uintptr_t)dp->dmem);
     CK(cudaMemcpy(dp->dmem, buf.data(), n, cudaMemcpyHostToDevice));
+    dp->gp.assign((const GpuProg *)buf.data(), (const GpuProg *)buf.data() + P.G);
     dp->bytes = n;
     dp->host = P;
     dp->nsteps = P.nsteps();
@@ -302,6 +306,13 @@ Grid choose_grid(mpxa_comm_t c, const Program &P, uint64_t unit) {
         if (nF > 1) nF--;
         else nS--;
     }
+    // fill the machine: widen the slices' count to use every resident CTA slot when the
+    // slices stay >= kMinSlice bytes
+    if (c->force_ns <= 0 && nF >= 1) {
+        uint64_t wide = cap / nF;
+        if (wide > nS && L / wide >= kMinSlice) nS = wide;
+        else if (wide > nS && L / kMinSlice > nS) nS = std::min<uint64_t>(wide, L / kMinSlice);
+    }
     gr.nS = (int)std::max<uint64_t>(1, nS);
     gr.nF = (int)std::max<uint64_t>(1, nF);
     return gr;
@@ -312,6 +323,7 @@ int make_params(mpxa_comm_t c, ExecParams &E, const DevProg &dp, const char *sen
                 uint64_t unit, uint64_t send_stride, uint64_t recv_stride) {
     memset(&E, 0, sizeof E);
     E.progs = (const GpuProg *)dp.dmem;
+    if (!c->emulated) E.prog = dp.gp[c->nprocs > 1 ? c->proc : 0];
     E.dc = c->dc;
     E.send = send;
     E.recv = recv;
@@ -389,6 +401,7 @@ int run_dynamic(mpxa_comm_t c, const Program &P, const char *send, char *recv, u
     CK(cudaMemcpyAsync(s.dmem, s.pinned, n, cudaMemcpyHostToDevice, stream));
     DevProg dp;
     dp.dmem = s.dmem;
+    dp.gp.assign((const GpuProg *)buf.data(), (const GpuProg *)buf.data() + P.G);
     dp.bytes = n;
     dp.host = P;
     dp.nsteps = P.nsteps();
@@ -629,8 +642,19 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     int rc = ensure_work(c.get(), heap);
     if (rc) return rc;
     // built-in selector table shipped next to the library (optional)
+    // measured selector table: $MPXA_SELECTOR, else selector_b200.txt next to libmpxa.so
     const char *sel = getenv("MPXA_SELECTOR");
-    if (sel) mpxa_load_selector(c.get(), sel);
+    if (sel) {
+        mpxa_load_selector(c.get(), sel);
+    } else {
+        Dl_info info;
+        if (dladdr((void *)&mpxa_init, &info) && info.dli_fname) {
+            std::string path(info.dli_fname);
+            auto slash = path.rfind('/');
+            path = (slash == std::string::npos ? std::string(".") : path.substr(0, slash)) + "/selector_b200.txt";
+            mpxa_load_selector(c.get(), path.c_str());   // absent file: built-in defaults
+        }
+    }
     const char *al = getenv("MPXA_ALGO");   // e.g. "alltoall:bruck,allgather:ring"
     if (al) {
         std::string s(al);

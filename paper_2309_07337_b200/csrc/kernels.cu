@@ -63,95 +63,85 @@ __device__ __forceinline__ uint8_t ldcg<uint8_t>(const uint8_t *p) {
     return (uint8_t)v;
 }
 
-// Copy n bytes with NT cooperating threads (index t), all sharing the alignment class W of
-// (src, dst): W-byte accesses for the body (U in flight per thread), bytes for head/tail.
-// NT is a compile-time constant so the U addresses of an iteration are one base register
-// plus immediates.
-template <typename V, int U, int NT>
-__device__ __forceinline__ void copy_words(char *dst, const char *src, uint64_t n, int t) {
-    constexpr int W = sizeof(V);
-    uint32_t head = (uint32_t)((W - ((uintptr_t)dst & (W - 1))) & (W - 1));
-    if (head > n) head = (uint32_t)n;
-    for (uint32_t i = t; i < head; i += NT) dst[i] = (char)ldcg((const uint8_t *)src + i);
-    const V *s = (const V *)(src + head) + t;
-    V *d = (V *)(dst + head) + t;
-    const uint64_t nv = (n - head) / W;
+// LSU copies.  Deliberately NOT templated on width / thread count / unroll: the executor
+// must stay small enough for the instruction cache (a template-expanded version was 87 K
+// SASS instructions and spent small launches stalled on instruction fetch).
+//
+// Copy n bytes with nt cooperating threads (index t): the widest access class W shared by
+// (src, dst) for the body, bytes for head / tail.  ro: the source is never written in the
+// launch (SEND), so the 16-B path may use the read-only, no-L1-allocate load.
+template <typename V>
+__device__ __forceinline__ void body_loop(char *dst, const char *src, uint64_t nv, int t, int nt) {
+    const V *s = (const V *)src;
+    V *d = (V *)dst;
     uint64_t i = t;
-    for (; i + (uint64_t)(U - 1) * NT < nv; i += (uint64_t)U * NT, s += U * NT, d += U * NT) {
-        V v[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) v[u] = ldcg(s + u * NT);
-#pragma unroll
-        for (int u = 0; u < U; u++) d[u * NT] = v[u];
+    for (; i + 3 * (uint64_t)nt < nv; i += 4 * (uint64_t)nt) {
+        V a = ldcg(s + i), b = ldcg(s + i + nt), c = ldcg(s + i + 2 * nt), e = ldcg(s + i + 3 * nt);
+        d[i] = a; d[i + nt] = b; d[i + 2 * nt] = c; d[i + 3 * nt] = e;
     }
-    for (; i < nv; i += NT, s += NT, d += NT) *d = ldcg(s);
-    const uint64_t done = head + nv * W;
-    for (uint64_t k = done + t; k < n; k += NT) dst[k] = (char)ldcg((const uint8_t *)src + k);
+    for (; i < nv; i += nt) d[i] = ldcg(s + i);
 }
 
-// 16-byte path: one load, nd stores (nd = 1 except allgather direct fan-out); every
-// destination shares the source's 16-B alignment.
-template <bool RO, int U, int NT>
-__device__ __forceinline__ void copy16_fan(char *const *dsts, int nd, const char *src, uint64_t n, int t) {
-    uint32_t head = (uint32_t)((16 - ((uintptr_t)src & 15)) & 15);
-    if (head > n) head = (uint32_t)n;
-    for (uint32_t i = t; i < head; i += NT) {
-        char b = (char)ldcg((const uint8_t *)src + i);
-        for (int k = 0; k < nd; k++) dsts[k][i] = b;
-    }
-    const uint4 *s = (const uint4 *)(src + head) + t;
-    const uint64_t nv = (n - head) >> 4;
-    uint64_t i = t;
-    for (; i + (uint64_t)(U - 1) * NT < nv; i += (uint64_t)U * NT, s += U * NT) {
-        uint4 v[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) v[u] = ld16<RO>(s + u * NT);
-        for (int k = 0; k < nd; k++) {
-            uint4 *d = (uint4 *)(dsts[k] + head) + i;
-#pragma unroll
-            for (int u = 0; u < U; u++) st16(d + u * NT, v[u]);
-        }
-    }
-    for (; i < nv; i += NT, s += NT) {
-        uint4 v = ld16<RO>(s);
-        for (int k = 0; k < nd; k++) st16((uint4 *)(dsts[k] + head) + i, v);
-    }
-    const uint64_t done = head + nv * 16;
-    for (uint64_t k2 = done + t; k2 < n; k2 += NT) {
-        char b = (char)ldcg((const uint8_t *)src + k2);
-        for (int k = 0; k < nd; k++) dsts[k][k2] = b;
-    }
-}
-
-// Copy of one slice to one destination: widest access class shared by (src, dst).
-template <int U, int NT>
-__device__ __forceinline__ void copy_slice1(char *dst, const char *src, uint64_t n, bool ro, int t) {
+__device__ __noinline__ void lsu_copy_range(char *dst, const char *src, uint64_t n, int t, int nt, bool ro) {
     if (n == 0) return;
-    unsigned m = (unsigned)(((uintptr_t)dst ^ (uintptr_t)src) & 15);
-    if (m == 0) {
-        char *const d1[1] = {dst};
-        if (ro) copy16_fan<true, U, NT>(d1, 1, src, n, t);
-        else    copy16_fan<false, U, NT>(d1, 1, src, n, t);
-    } else if ((m & 7) == 0) copy_words<unsigned long long, U, NT>(dst, src, n, t);
-    else if ((m & 3) == 0)   copy_words<unsigned int, U, NT>(dst, src, n, t);
-    else if ((m & 1) == 0)   copy_words<unsigned short, U, NT>(dst, src, n, t);
-    else                     copy_words<uint8_t, 1, NT>(dst, src, n, t);
+    const unsigned m = (unsigned)(((uintptr_t)dst ^ (uintptr_t)src) & 15);
+    const unsigned W = m == 0 ? 16 : (m & 7) == 0 ? 8 : (m & 3) == 0 ? 4 : (m & 1) == 0 ? 2 : 1;
+    uint64_t head = (W - ((uintptr_t)dst & (W - 1))) & (W - 1);
+    if (head > n) head = n;
+    for (uint64_t i = t; i < head; i += nt) dst[i] = (char)ldcg((const uint8_t *)src + i);
+    const uint64_t nv = (n - head) / W;
+    char *d = dst + head;
+    const char *s = src + head;
+    switch (W) {
+        case 16:
+            if (ro) {
+                const uint4 *s4 = (const uint4 *)s;
+                uint4 *d4 = (uint4 *)d;
+                uint64_t i = t;
+                for (; i + 3 * (uint64_t)nt < nv; i += 4 * (uint64_t)nt) {
+                    uint4 a = ld16<true>(s4 + i), b = ld16<true>(s4 + i + nt), c = ld16<true>(s4 + i + 2 * nt),
+                          e = ld16<true>(s4 + i + 3 * nt);
+                    st16(d4 + i, a); st16(d4 + i + nt, b); st16(d4 + i + 2 * nt, c); st16(d4 + i + 3 * nt, e);
+                }
+                for (; i < nv; i += nt) st16(d4 + i, ld16<true>(s4 + i));
+            } else {
+                body_loop<uint4>(d, s, nv, t, nt);
+            }
+            break;
+        case 8: body_loop<unsigned long long>(d, s, nv, t, nt); break;
+        case 4: body_loop<unsigned int>(d, s, nv, t, nt); break;
+        case 2: body_loop<unsigned short>(d, s, nv, t, nt); break;
+        default: body_loop<uint8_t>(d, s, nv, t, nt); break;
+    }
+    for (uint64_t k = head + nv * W + t; k < n; k += nt) dst[k] = (char)ldcg((const uint8_t *)src + k);
 }
 
-// Fan-out copy of one slice to nd destinations (allgather direct): one load, nd stores
-// when every destination shares the source's 16-B alignment, else per-destination copies.
-template <int U, int NT>
-__device__ __forceinline__ void copy_slice_fan(char *const *dsts, int nd, const char *src, uint64_t n,
-                                               bool ro, int t) {
+// Fan-out: one read, nd stores, when every destination shares the source's 16-B alignment.
+__device__ __noinline__ void lsu_copy_fan(char *const *dsts, int nd, const char *src, uint64_t n, int t, int nt,
+                                          bool ro) {
     if (n == 0) return;
     unsigned mis = 0;
     for (int k = 0; k < nd; k++) mis |= (unsigned)(((uintptr_t)dsts[k] ^ (uintptr_t)src) & 15);
-    if (mis == 0) {
-        if (ro) copy16_fan<true, U, NT>(dsts, nd, src, n, t);
-        else    copy16_fan<false, U, NT>(dsts, nd, src, n, t);
+    if (mis) {
+        for (int k = 0; k < nd; k++) lsu_copy_range(dsts[k], src, n, t, nt, ro);
         return;
     }
-    for (int k = 0; k < nd; k++) copy_slice1<U, NT>(dsts[k], src, n, ro, t);
+    uint64_t head = (16 - ((uintptr_t)src & 15)) & 15;
+    if (head > n) head = n;
+    for (uint64_t i = t; i < head; i += nt) {
+        const char b = (char)ldcg((const uint8_t *)src + i);
+        for (int k = 0; k < nd; k++) dsts[k][i] = b;
+    }
+    const uint4 *s4 = (const uint4 *)(src + head);
+    const uint64_t nv = (n - head) >> 4;
+    for (uint64_t i = t; i < nv; i += nt) {
+        const uint4 v = ro ? ld16<true>(s4 + i) : ld16<false>(s4 + i);
+        for (int k = 0; k < nd; k++) st16((uint4 *)(dsts[k] + head) + i, v);
+    }
+    for (uint64_t k2 = head + nv * 16 + t; k2 < n; k2 += nt) {
+        const char b = (char)ldcg((const uint8_t *)src + k2);
+        for (int k = 0; k < nd; k++) dsts[k][k2] = b;
+    }
 }
 
 // ------------------------------------------------------------------------------------
@@ -217,6 +207,13 @@ struct RingEntry {
     uint8_t fanout, dst_kind;
 };
 
+constexpr int kMaxStepsSmem = 64;
+struct StepInfo {
+    int32_t first;          // index of this CTA's first move (flow group range start)
+    int32_t nm;             // number of moves in this CTA's flow group range
+    uint32_t signal_mask, wait_mask;
+};
+
 struct ExecShared {
     char *recv_base[kMaxGpus];
     char *work_base[kMaxGpus];
@@ -224,6 +221,7 @@ struct ExecShared {
     Move moves[kMoveTile];
     uint64_t mbar[kStages];
     RingEntry ring[kStages];
+    StepInfo steps[kMaxStepsSmem];   // this CTA's view of every step, loaded once
     uint64_t epoch;      // this launch's epoch (device-side sequence number)
     uint32_t cts_ok;     // remote GPUs whose CTS for this epoch was observed
     int abort_flag;
@@ -239,7 +237,7 @@ __device__ __forceinline__ char *base_of(const ExecParams &P, const ExecShared &
 }
 
 // Spin (threads < 32, one per bit of mask) until *slot(bit) >= want; sets abort on timeout.
-__device__ __forceinline__ void wait_mask_ge(const ExecParams &P, ExecShared &S, uint32_t mask,
+__device__ __noinline__ void wait_mask_ge(const ExecParams &P, ExecShared &S, uint32_t mask,
                                              const uint64_t *slot0, uint64_t stride_elems,
                                              uint64_t want) {
     int t = threadIdx.x;
@@ -289,10 +287,10 @@ struct Producer {
         tma_load_1d(smem_u32(stages + (size_t)s * kChunk), src, e.len, smem_u32(&S.mbar[s]));
         issued++;
     }
-    __device__ __forceinline__ void drain(const ExecParams &P, ExecShared &S) {
+    __device__ __forceinline__ void drain(const ExecParams &P, ExecShared &S, bool consumed) {
         while (stored < issued) store_one(P, S);
         bulk_wait_all();
-        fence_proxy_async();
+        if (consumed) fence_proxy_async();   // bulk writes before generic readers / flag release
     }
 };
 
@@ -308,22 +306,45 @@ struct MovePlan {
     uint64_t body;      // TMA: aligned body bytes (multiple of 16)
 };
 
-__device__ __forceinline__ MovePlan plan_move(const ExecParams &P, const ExecShared &S, const Move &m, int sl) {
+// Slice bounds of a move length, cached per thread: uniform ops have one length for every
+// move, so the 64-bit divisions run once per launch instead of once per move.
+struct SliceCache {
+    uint64_t len = ~0ull, lo = 0, hi = 0;
+    __device__ __forceinline__ void get(uint64_t nbytes, int sl, int nS, uint64_t &l, uint64_t &h) {
+        if (nbytes != len) {
+            len = nbytes;
+            slice_of(nbytes, sl, nS, lo, hi);
+        }
+        l = lo;
+        h = hi;
+    }
+};
+
+__device__ __noinline__ unsigned fan_misalign(const ExecParams &P, const ExecShared &S, int kind, uint64_t doff,
+                                              const char *src) {
+    unsigned mis = 0;
+    for (int j = 0; j < P.p; j++) mis |= (unsigned)(((uintptr_t)(base_of(P, S, kind, j) + doff) ^ (uintptr_t)src) & 15);
+    return mis;
+}
+
+// slice length only (cheap classification shared by every thread)
+__device__ __forceinline__ uint64_t slice_len(const ExecParams &P, const Move &m, int sl, SliceCache &sc,
+                                              uint64_t &lo) {
+    uint64_t hi;
+    sc.get((uint64_t)m.len * P.unit, sl, P.nS, lo, hi);
+    return hi - lo;
+}
+
+__device__ __forceinline__ MovePlan plan_move(const ExecParams &P, const ExecShared &S, const Move &m, int sl,
+                                              SliceCache &sc) {
     MovePlan mp;
-    const uint64_t nbytes = (uint64_t)m.len * P.unit;
-    uint64_t lo, hi;
-    slice_of(nbytes, sl, P.nS, lo, hi);
-    mp.n = hi - lo;
+    uint64_t lo;
+    mp.n = slice_len(P, m, sl, sc, lo);
     mp.src = base_of(P, S, m.src_kind, m.src_rank) + (uint64_t)m.src_off * P.unit + lo;
     mp.doff = (uint64_t)m.dst_off * P.unit + lo;
     mp.dst = m.fanout ? nullptr : base_of(P, S, m.dst_kind, m.dst_rank) + mp.doff;
-    unsigned mis;
-    if (!m.fanout) {
-        mis = (unsigned)(((uintptr_t)mp.dst ^ (uintptr_t)mp.src) & 15);
-    } else {
-        mis = 0;
-        for (int j = 0; j < P.p; j++) mis |= (unsigned)(((uintptr_t)(base_of(P, S, m.dst_kind, j) + mp.doff) ^ (uintptr_t)mp.src) & 15);
-    }
+    const unsigned mis = !m.fanout ? (unsigned)(((uintptr_t)mp.dst ^ (uintptr_t)mp.src) & 15)
+                                   : fan_misalign(P, S, m.dst_kind, mp.doff, mp.src);
     mp.tma = mis == 0 && mp.n >= kTmaMin;
     mp.head = (uint32_t)((16 - ((uintptr_t)mp.src & 15)) & 15);
     if (mp.head > mp.n) mp.head = (uint32_t)mp.n;
@@ -331,18 +352,79 @@ __device__ __forceinline__ MovePlan plan_move(const ExecParams &P, const ExecSha
     return mp;
 }
 
-template <int U, int NT>
-__device__ __forceinline__ void lsu_copy(const ExecParams &P, const ExecShared &S, const Move &m, const MovePlan &mp,
-                                         uint64_t off, uint64_t n, int t) {
+__device__ __noinline__ void lsu_copy(const ExecParams &P, const ExecShared &S, const Move &m, const MovePlan &mp,
+                                         uint64_t off, uint64_t n, int t, int nt) {
     const bool ro = m.src_kind == BK_SEND;
     if (!m.fanout) {
-        copy_slice1<U, NT>(mp.dst + off, mp.src + off, n, ro, t);
+        lsu_copy_range(mp.dst + off, mp.src + off, n, t, nt, ro);
     } else {
         char *dsts[8];
         for (int j0 = 0; j0 < P.p; j0 += 8) {
             const int nd = min(8, P.p - j0);
             for (int k = 0; k < nd; k++) dsts[k] = base_of(P, S, m.dst_kind, j0 + k) + mp.doff + off;
-            copy_slice_fan<U, NT>(dsts, nd, mp.src + off, n, ro, t);
+            lsu_copy_fan(dsts, nd, mp.src + off, n, t, nt, ro);
+        }
+    }
+}
+
+// Batched copy of up to kBatch SMALL moves by one warp (n <= 512 B each): every lane loads
+// its 16-byte piece of every move first (kBatch loads in flight), then stores them -- one
+// memory round trip per batch instead of one per move.  Byte-granular when a piece is not
+// 16-B aligned on both sides.
+constexpr int kBatch = 4;
+constexpr uint64_t kSmallMax = 512;
+
+struct SmallJob {
+    const char *src;
+    char *dst;          // non-fanout destination (or first fan-out destination offset base)
+    uint64_t doff;
+    uint32_t n;
+    uint8_t fanout, dst_kind, ro;
+};
+
+__device__ __noinline__ void small_batch(const ExecParams &P, const ExecShared &S, const SmallJob *jobs, int nj,
+                                            int lane) {
+    uint4 v[kBatch];
+    bool vec[kBatch];
+#pragma unroll
+    for (int k = 0; k < kBatch; k++) {
+        v[k] = make_uint4(0, 0, 0, 0);
+        vec[k] = false;
+        if (k >= nj) continue;
+        const SmallJob &j = jobs[k];
+        const uint32_t o = (uint32_t)lane * 16;
+        if (o >= j.n) continue;
+        const uint32_t len = min(16u, j.n - o);
+        const char *sp = j.src + o;
+        bool dal = true;
+        if (!j.fanout) dal = (((uintptr_t)(j.dst + o)) & 15) == 0;
+        else
+            for (int r = 0; r < P.p; r++) dal &= (((uintptr_t)(base_of(P, S, j.dst_kind, r) + j.doff + o)) & 15) == 0;
+        if (len == 16 && (((uintptr_t)sp) & 15) == 0 && dal) {
+            vec[k] = true;
+            v[k] = j.ro ? ld16<true>((const uint4 *)sp) : ld16<false>((const uint4 *)sp);
+        } else {
+            uint32_t w[4] = {0, 0, 0, 0};
+            for (uint32_t b = 0; b < len; b++) w[b >> 2] |= (uint32_t)ldcg((const uint8_t *)sp + b) << (8 * (b & 3));
+            v[k] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kBatch; k++) {
+        if (k >= nj) continue;
+        const SmallJob &j = jobs[k];
+        const uint32_t o = (uint32_t)lane * 16;
+        if (o >= j.n) continue;
+        const uint32_t len = min(16u, j.n - o);
+        const int nd = j.fanout ? P.p : 1;
+        for (int r = 0; r < nd; r++) {
+            char *dp = (j.fanout ? base_of(P, S, j.dst_kind, r) + j.doff : j.dst) + o;
+            if (vec[k]) {
+                st16((uint4 *)dp, v[k]);
+            } else {
+                const uint32_t w[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+                for (uint32_t b = 0; b < len; b++) dp[b] = (char)(w[b >> 2] >> (8 * (b & 3)));
+            }
         }
     }
 }
@@ -356,11 +438,25 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
     const int f = c / P.nS;                   // flow group
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
-    const GpuProg prog = P.progs[g];
+    const GpuProg prog = P.mode == 1 ? P.progs[g] : P.prog;
     const bool multi = P.G > 1;   // emulated or multi-process: flags + CTS
     Producer prod;
     prod.stages = dyn_smem;
 
+    const int64_t x0 = (int64_t)f * P.nflows / P.nF, x1 = (int64_t)(f + 1) * P.nflows / P.nF;
+    const int nsteps = prog.nsteps;
+    const bool steps_in_smem = nsteps <= kMaxStepsSmem;
+    // the whole step table (with this CTA's flow-group move range) in one parallel round trip
+    if (steps_in_smem && t < nsteps) {
+        const Step st = prog.steps[t];
+        if (P.nF == 1) {            // one flow group: the whole step, no flow-index lookup
+            S.steps[t] = StepInfo{st.move_begin, st.move_end - st.move_begin, st.signal_mask, st.wait_mask};
+        } else {
+            const int32_t *fx = prog.findex + st.flow_index;
+            const int m0 = fx[x0];
+            S.steps[t] = StepInfo{st.move_begin + m0, fx[x1] - m0, st.signal_mask, st.wait_mask};
+        }
+    }
     if (t < P.G) {
         S.work_base[t] = P.dc->work_base[t];
         S.sym[t] = P.dc->sym[t];
@@ -389,14 +485,23 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
         st_release_sys(&slot->epoch, epoch);
     }
 
-    const int64_t x0 = (int64_t)f * P.nflows / P.nF, x1 = (int64_t)(f + 1) * P.nflows / P.nF;
-    for (int s = 0; s < prog.nsteps; s++) {
-        const Step st = prog.steps[s];
+    SliceCache sc;
+    for (int s = 0; s < nsteps; s++) {
+        StepInfo st;
+        if (steps_in_smem) {
+            st = S.steps[s];
+        } else {
+            const Step g_st = prog.steps[s];
+            const int32_t *fx = prog.findex + g_st.flow_index;
+            const int m0 = fx[x0];
+            st = StepInfo{g_st.move_begin + m0, fx[x1] - m0, g_st.signal_mask, g_st.wait_mask};
+        }
+        const uint32_t prev_wait = s == 0 ? 0u : (steps_in_smem ? S.steps[s - 1].wait_mask : prog.steps[s - 1].wait_mask);
+        bool wrote = false;   // this thread issued generic global stores in this step
         if (multi) {
             // data written into this GPU by peers in step s-1 (this CTA's share) must have landed
-            if (s > 0 && prog.steps[s - 1].wait_mask)
-                wait_mask_ge(P, S, prog.steps[s - 1].wait_mask, &S.sym[g]->flags[0][c], kMaxCtas,
-                             (epoch << 8) | (uint64_t)s);
+            if (prev_wait)
+                wait_mask_ge(P, S, prev_wait, &S.sym[g]->flags[0][c], kMaxCtas, (epoch << 8) | (uint64_t)s);
             // peers written in this step must have cleared us to send in this epoch
             uint32_t need = st.signal_mask & ~S.cts_ok;
             if (need) {
@@ -410,10 +515,8 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
             if (t == 0) S.cts_ok |= need;
             if (S.abort_flag) return;
         }
-        if (t == 0) fence_proxy_async();   // acquired peer writes before this CTA's TMA reads
-        const int32_t *fx = prog.findex + st.flow_index;
-        const int m0 = fx[x0], m1 = fx[x1];
-        const int nm = m1 - m0;
+        if (multi && t == 0) fence_proxy_async();   // acquired peer writes before TMA reads
+        const int nm = st.nm;
         const int rot = nm ? (int)(((int64_t)sl + (int64_t)g * nm / P.G) % nm) : 0;
         for (int tile = 0; tile < nm; tile += kMoveTile) {
             const int cnt = min(kMoveTile, nm - tile);
@@ -421,14 +524,16 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
             for (int i = t; i < cnt; i += kThreads) {
                 int q = tile + i + rot;
                 if (q >= nm) q -= nm;
-                S.moves[i] = prog.moves[st.move_begin + m0 + q];
+                S.moves[i] = prog.moves[st.first + q];
             }
             __syncthreads();
             if (warp == 0) {
                 if (lane == 0) {
                     for (int i = 0; i < cnt; i++) {
                         const Move &m = S.moves[i];
-                        const MovePlan mp = plan_move(P, S, m, sl);
+                        uint64_t lo;
+                        if (slice_len(P, m, sl, sc, lo) < kTmaMin) continue;   // cheap reject
+                        const MovePlan mp = plan_move(P, S, m, sl, sc);
                         if (!mp.tma) continue;
                         for (uint64_t o = 0; o < mp.body; o += kChunk) {
                             RingEntry e;
@@ -443,28 +548,50 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
                 }
             } else {
                 const int lw = warp - 1, lt = t - 32;
+                SmallJob jobs[kBatch];
+                int nj = 0;
                 for (int i = 0; i < cnt; i++) {
                     const Move &m = S.moves[i];
-                    const MovePlan mp = plan_move(P, S, m, sl);
-                    if (mp.n == 0) continue;
+                    uint64_t lo;
+                    const uint64_t n = slice_len(P, m, sl, sc, lo);
+                    // only the owning warp plans small moves; big ones involve every LSU thread
+                    if (n == 0 || (n < kLsuBig && i % kLsuWarps != lw)) continue;
+                    const MovePlan mp = plan_move(P, S, m, sl, sc);
                     if (mp.tma) {
                         if (i % kLsuWarps == lw) {   // head / tail bytes around the TMA body
                             const uint64_t tail = mp.n - mp.head - mp.body;
-                            if (lane < 16) lsu_copy<1, 16>(P, S, m, mp, 0, mp.head, lane);
-                            else lsu_copy<1, 16>(P, S, m, mp, mp.head + mp.body, tail, lane - 16);
+                            if (lane < 16) lsu_copy(P, S, m, mp, 0, mp.head, lane, 16);
+                            else lsu_copy(P, S, m, mp, mp.head + mp.body, tail, lane - 16, 16);
+                            wrote = true;
                         }
                     } else if (mp.n >= kLsuBig) {
-                        lsu_copy<4, kLsuThreads>(P, S, m, mp, 0, mp.n, lt);
+                        lsu_copy(P, S, m, mp, 0, mp.n, lt, kLsuThreads);
+                        wrote = true;
                     } else if (i % kLsuWarps == lw) {
-                        lsu_copy<4, 32>(P, S, m, mp, 0, mp.n, lane);
+                        if (mp.n <= kSmallMax) {     // batch small moves: one round trip per batch
+                            jobs[nj].src = mp.src;
+                            jobs[nj].dst = mp.dst;
+                            jobs[nj].doff = mp.doff;
+                            jobs[nj].n = (uint32_t)mp.n;
+                            jobs[nj].fanout = m.fanout;
+                            jobs[nj].dst_kind = m.dst_kind;
+                            jobs[nj].ro = m.src_kind == BK_SEND;
+                            if (++nj == kBatch) { small_batch(P, S, jobs, nj, lane); nj = 0; }
+                        } else {
+                            lsu_copy(P, S, m, mp, 0, mp.n, lane, 32);
+                        }
+                        wrote = true;
                     }
                 }
+                if (nj) small_batch(P, S, jobs, nj, lane);
             }
         }
-        // every writer makes its generic stores visible to the async proxy (TMA reads of the
-        // next step); the producer waits its bulk stores and fences them for generic readers
-        fence_proxy_async();
-        if (t == 0) prod.drain(P, S);
+        // writers make their generic stores visible to the async proxy when anything will
+        // consume them (a later step of this launch, or a peer signalled now); the producer
+        // waits its bulk stores and fences them for generic readers
+        const bool consumed = (s + 1 < nsteps) || (multi && st.signal_mask);
+        if (consumed && wrote) fence_proxy_async();
+        if (t == 0) prod.drain(P, S, consumed);
         __syncthreads();
         // ---- signal the peers written in this step (this CTA's share) ----
         if (multi && st.signal_mask && t < 32 && ((st.signal_mask >> t) & 1u)) {
@@ -473,9 +600,10 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
         }
     }
     // completion: everything peers write into this GPU in the last step has landed
-    if (multi && prog.nsteps > 0 && prog.steps[prog.nsteps - 1].wait_mask) {
-        wait_mask_ge(P, S, prog.steps[prog.nsteps - 1].wait_mask, &S.sym[g]->flags[0][c], kMaxCtas,
-                     (epoch << 8) | (uint64_t)prog.nsteps);
+    const uint32_t last_wait = nsteps == 0 ? 0u : (steps_in_smem ? S.steps[nsteps - 1].wait_mask
+                                                                  : prog.steps[nsteps - 1].wait_mask);
+    if (multi && last_wait) {
+        wait_mask_ge(P, S, last_wait, &S.sym[g]->flags[0][c], kMaxCtas, (epoch << 8) | (uint64_t)nsteps);
         __syncthreads();
     }
     // the last CTA of the launch publishes the epoch (the next launch is stream-ordered after)

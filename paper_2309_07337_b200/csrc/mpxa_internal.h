@@ -102,6 +102,7 @@ struct DevComm {
 // Launch parameters (~130 B).  Buffers are the caller's process-level rank-major buffers.
 struct ExecParams {
     const GpuProg *progs;      // device array [G] (only progs[my_gpu] used in multi-process)
+    GpuProg prog;              // modes 0 and 2: this GPU's program by value (saves a round trip)
     DevComm *dc;
     const char *send;          // this process's sendbuf (first local rank)
     char *recv;                // this process's recvbuf
