@@ -32,7 +32,7 @@ cudaError_t launch_counts(const int64_t *sc, int64_t *rc, int64_t *rd, int p, in
                           cudaStream_t stream);
 cudaError_t launch_scan(const int64_t *counts, int64_t *rc, int64_t *rd, int p, int nr,
                         cudaStream_t stream);
-int exec_max_ctas_per_sm();
+int exec_max_ctas_per_sm(size_t dyn_smem);
 }  // namespace mpxa
 
 using namespace mpxa;
@@ -54,6 +54,7 @@ constexpr uint64_t kBytesPerCta = 65536;   // launch sizing target per CTA per s
 constexpr uint64_t kSliceBytes = 16384;    // target column-slice length of the longest move
 constexpr uint64_t kMovesPerCta = 8;       // small moves per CTA (latency-bound regime)
 constexpr uint64_t kMinSlice = 4096;       // smallest slice worth a CTA when filling the GPU
+constexpr uint64_t kBigPerCta = 2u << 20;  // bytes per CTA per step above which the big TMA config wins
 
 // A program uploaded to device memory: [GpuProg x G][steps][moves].
 struct DevProg {
@@ -111,6 +112,7 @@ struct SelEntry {
 // only on the (global) program and the unit, so every process computes the same grid.
 struct Grid {
     int nS = 1, nF = 1;
+    bool big = false;   // TMA config: big (1 CTA / SM, 32 KiB stages) or mid
     int n() const { return nS * nF; }
 };
 
@@ -135,8 +137,10 @@ struct mpxa_comm_s {
     mpxa_allgather_fn boot = nullptr;
     void *ctx = nullptr;
     double timeout_s = 60.0;
-    int sm_count = 148, cap_ctas = 296;
+    int sm_count = 148, cap_ctas = 296;   // cap_ctas: mid TMA config (2 CTAs / SM)
+    int cap_big = 148;                     // big TMA config (1 CTA / SM)
     int force_ns = 0, force_nf = 0;           // MPXA_NS / MPXA_NF overrides (tuning)
+    int force_big = -1;                       // MPXA_TMA_BIG=0/1 override (tuning)
 
     SymRegion *sym_local = nullptr;            // G regions when emulated, else 1
     SymRegion *sym_map[kMaxGpus] = {};
@@ -290,10 +294,12 @@ int cached_uniform(mpxa_comm_t c, int op, int algo, int stage, std::shared_ptr<D
 uint64_t cdiv(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
 Grid choose_grid(mpxa_comm_t c, const Program &P, uint64_t unit) {
-    const uint64_t cap = (uint64_t)c->cap_ctas;
     const uint64_t L = (uint64_t)P.max_move * unit;          // longest move
     const uint64_t T = (uint64_t)P.max_step_units * unit;    // busiest step of one GPU
     Grid gr;
+    // large steps stream through fewer, fatter pipelines; the rest through more CTAs
+    gr.big = c->force_big >= 0 ? c->force_big > 0 : T / (uint64_t)c->cap_big >= kBigPerCta;
+    const uint64_t cap = (uint64_t)(gr.big ? c->cap_big : c->cap_ctas);
     uint64_t nS = std::min<uint64_t>(cap, std::max<uint64_t>(1, cdiv(L, kSliceBytes)));
     uint64_t nF_bw = cdiv(T, nS * kBytesPerCta);              // enough CTAs for bandwidth
     uint64_t nF_lat = cdiv((uint64_t)P.max_step_moves, kMovesPerCta);  // ~1 move per LSU warp
@@ -365,6 +371,10 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
     const Grid gr = grid ? *grid : choose_grid(c, dp.host, unit);
     E.nS = gr.nS;
     E.nF = gr.nF;
+    const TmaConfig tc = gr.big ? kTmaBig : kTmaMid;
+    E.stages = tc.stages;
+    E.chunk = tc.chunk;
+    E.ahead = tc.ahead;
     ++c->epoch;   // host mirror only; the kernels keep the authoritative epoch in DevComm
     cudaError_t e = launch_exec(E, gr.n(), c->emulated ? c->G : 1, c->emulated, stream);
     if (e != cudaSuccess) {
@@ -609,13 +619,16 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, c->device));
     c->sm_count = prop.multiProcessorCount;
-    int occ = exec_max_ctas_per_sm();
-    if (occ < 1) occ = 1;
+    int occ = std::max(1, exec_max_ctas_per_sm((size_t)kTmaMid.stages * kTmaMid.chunk));
+    int occ_big = std::max(1, exec_max_ctas_per_sm((size_t)kTmaBig.stages * kTmaBig.chunk));
     int cap = std::min(kMaxCtas, c->sm_count * occ);
-    if (c->emulated) cap = std::max(1, cap / c->G);
+    int capb = std::min(kMaxCtas, c->sm_count * occ_big);
+    if (c->emulated) { cap = std::max(1, cap / c->G); capb = std::max(1, capb / c->G); }
     c->cap_ctas = cap;
+    c->cap_big = capb;
     if (const char *e = getenv("MPXA_NS")) c->force_ns = atoi(e);
     if (const char *e = getenv("MPXA_NF")) c->force_nf = atoi(e);
+    if (const char *e = getenv("MPXA_TMA_BIG")) c->force_big = atoi(e);
     CK(cudaHostAlloc((void **)&c->err_host, sizeof(int32_t), cudaHostAllocMapped));
     *c->err_host = 0;
     CK(cudaHostGetDevicePointer((void **)&c->err_dev, c->err_host, 0));

@@ -153,7 +153,6 @@ constexpr uint64_t kLsuBig = 8192;       // misaligned slices at least this long
 constexpr int kWarps = kThreads / 32;
 constexpr int kLsuWarps = kWarps - 1;    // warp 0 is the TMA producer
 constexpr int kLsuThreads = kThreads - 32;
-constexpr int kAhead = MPXA_AHEAD;       // TMA loads in flight ahead of the oldest store
 
 // ---- TMA bulk copies (cp.async.bulk: SASS UBLKCP) --------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -219,8 +218,8 @@ struct ExecShared {
     char *work_base[kMaxGpus];
     SymRegion *sym[kMaxGpus];
     Move moves[kMoveTile];
-    uint64_t mbar[kStages];
-    RingEntry ring[kStages];
+    uint64_t mbar[kMaxStages];
+    RingEntry ring[kMaxStages];
     StepInfo steps[kMaxStepsSmem];   // this CTA's view of every step, loaded once
     uint64_t epoch;      // this launch's epoch (device-side sequence number)
     uint32_t cts_ok;     // remote GPUs whose CTS for this epoch was observed
@@ -260,17 +259,17 @@ __device__ __noinline__ void wait_mask_ge(const ExecParams &P, ExecShared &S, ui
     }
 }
 
-// The single-thread TMA producer: a ring of kStages smem stages; loads run kAhead chunks
+// The single-thread TMA producer: a ring of P.stages smem stages; loads run P.ahead chunks
 // ahead of the oldest pending store; each chunk's stores form one bulk group.
 struct Producer {
     uint32_t issued = 0, stored = 0;
     char *stages;
 
     __device__ __forceinline__ void store_one(const ExecParams &P, ExecShared &S) {
-        const uint32_t s = stored % kStages;
-        mbar_wait(smem_u32(&S.mbar[s]), (stored / kStages) & 1u);
+        const uint32_t s = stored % (uint32_t)P.stages;
+        mbar_wait(smem_u32(&S.mbar[s]), (stored / (uint32_t)P.stages) & 1u);
         const RingEntry e = S.ring[s];
-        const uint32_t src = smem_u32(stages + (size_t)s * kChunk);
+        const uint32_t src = smem_u32(stages + (size_t)s * P.chunk);
         if (!e.fanout) {
             tma_store_1d(e.dst, src, e.len);
         } else {
@@ -280,11 +279,12 @@ struct Producer {
         stored++;
     }
     __device__ __forceinline__ void push(const ExecParams &P, ExecShared &S, const char *src, const RingEntry &e) {
-        if (issued - stored == (uint32_t)kAhead) store_one(P, S);
-        const uint32_t s = issued % kStages;
-        if (issued >= (uint32_t)kStages) bulk_wait_read((int)(stored - 1 - (issued - kStages)));
+        if (issued - stored == (uint32_t)P.ahead) store_one(P, S);
+        const uint32_t ns = (uint32_t)P.stages;
+        const uint32_t s = issued % ns;
+        if (issued >= ns) bulk_wait_read((int)(stored - 1 - (issued - ns)));
         S.ring[s] = e;
-        tma_load_1d(smem_u32(stages + (size_t)s * kChunk), src, e.len, smem_u32(&S.mbar[s]));
+        tma_load_1d(smem_u32(stages + (size_t)s * P.chunk), src, e.len, smem_u32(&S.mbar[s]));
         issued++;
     }
     __device__ __forceinline__ void drain(const ExecParams &P, ExecShared &S, bool consumed) {
@@ -335,8 +335,12 @@ __device__ __forceinline__ uint64_t slice_len(const ExecParams &P, const Move &m
     return hi - lo;
 }
 
-__device__ __forceinline__ MovePlan plan_move(const ExecParams &P, const ExecShared &S, const Move &m, int sl,
-                                              SliceCache &sc) {
+#ifdef MPXA_PLAN_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+MovePlan plan_move(const ExecParams &P, const ExecShared &S, const Move &m, int sl, SliceCache &sc) {
     MovePlan mp;
     uint64_t lo;
     mp.n = slice_len(P, m, sl, sc, lo);
@@ -469,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
         S.cts_ok = 0;
         S.abort_flag = 0;
         S.epoch = *(volatile uint64_t *)&P.dc->epoch + 1;
-        for (int s = 0; s < kStages; s++) mbar_init(smem_u32(&S.mbar[s]), 1);
+        for (int s = 0; s < P.stages; s++) mbar_init(smem_u32(&S.mbar[s]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -515,7 +519,11 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
             if (t == 0) S.cts_ok |= need;
             if (S.abort_flag) return;
         }
+#ifdef MPXA_STEP_FENCE
+        if (t == 0) fence_proxy_async();
+#else
         if (multi && t == 0) fence_proxy_async();   // acquired peer writes before TMA reads
+#endif
         const int nm = st.nm;
         const int rot = nm ? (int)(((int64_t)sl + (int64_t)g * nm / P.G) % nm) : 0;
         for (int tile = 0; tile < nm; tile += kMoveTile) {
@@ -535,9 +543,10 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
                         if (slice_len(P, m, sl, sc, lo) < kTmaMin) continue;   // cheap reject
                         const MovePlan mp = plan_move(P, S, m, sl, sc);
                         if (!mp.tma) continue;
-                        for (uint64_t o = 0; o < mp.body; o += kChunk) {
+                        const uint64_t chunk = (uint64_t)P.chunk;
+                        for (uint64_t o = 0; o < mp.body; o += chunk) {
                             RingEntry e;
-                            e.len = (uint32_t)min((uint64_t)kChunk, mp.body - o);
+                            e.len = (uint32_t)min(chunk, mp.body - o);
                             e.fanout = m.fanout;
                             e.dst_kind = m.dst_kind;
                             e.doff = mp.doff + mp.head + o;
@@ -673,23 +682,22 @@ __global__ void mpxa_scan_kernel(const int64_t *__restrict__ counts, int64_t *__
 // ------------------------------------------------------------------------------------
 // host-side launchers (called from api.cpp)
 // ------------------------------------------------------------------------------------
-constexpr size_t kDynSmem = (size_t)kStages * kChunk;
-
 static cudaError_t exec_attr_once() {
     static cudaError_t e = cudaFuncSetAttribute(mpxa_exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)kDynSmem);
+                                                kMaxDynSmem);
     return e;
 }
 
 cudaError_t launch_exec(const ExecParams &P, int nC, int nG, bool cooperative, cudaStream_t stream) {
     cudaError_t e = exec_attr_once();
     if (e != cudaSuccess) return e;
+    const size_t smem = (size_t)P.stages * P.chunk;
     dim3 grid(nC, nG), block(kThreads);
     if (cooperative) {
         void *args[] = {(void *)&P};
-        return cudaLaunchCooperativeKernel((const void *)mpxa_exec_kernel, grid, block, args, kDynSmem, stream);
+        return cudaLaunchCooperativeKernel((const void *)mpxa_exec_kernel, grid, block, args, smem, stream);
     }
-    mpxa_exec_kernel<<<grid, block, kDynSmem, stream>>>(P);
+    mpxa_exec_kernel<<<grid, block, smem, stream>>>(P);
     return cudaGetLastError();
 }
 
@@ -711,10 +719,10 @@ cudaError_t launch_scan(const int64_t *counts, int64_t *rc, int64_t *rd, int p, 
     return cudaGetLastError();
 }
 
-int exec_max_ctas_per_sm() {
+int exec_max_ctas_per_sm(size_t dyn_smem) {
     if (exec_attr_once() != cudaSuccess) return 1;
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mpxa_exec_kernel, kThreads, kDynSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mpxa_exec_kernel, kThreads, dyn_smem);
     return n;
 }
 

@@ -17,17 +17,16 @@ namespace mpxa {
 constexpr int kMaxGpus = 32;       // processes or virtual GPUs per comm (signal masks are 32-bit)
 constexpr int kMaxCtas = 1024;     // CTAs per GPU per launch (flag slots per source GPU)
 constexpr int kThreads = 256;      // threads per CTA of the executor kernel (warp 0: TMA producer)
-#ifndef MPXA_STAGES
-#define MPXA_STAGES 6
-#endif
-#ifndef MPXA_CHUNK
-#define MPXA_CHUNK 16384
-#endif
-#ifndef MPXA_AHEAD
-#define MPXA_AHEAD (MPXA_STAGES - 2)
-#endif
-constexpr int kStages = MPXA_STAGES;   // TMA ring stages per CTA
-constexpr int kChunk = MPXA_CHUNK;     // bytes per TMA stage
+// TMA ring configurations (runtime-selected per launch):
+//   mid : 6 x 16 KiB stages, 2 CTAs / SM  (many CTAs: mid-size messages, latency)
+//   big : 6 x 32 KiB stages, 1 CTA / SM   (more bytes in flight per SM: large messages)
+constexpr int kMaxStages = 8;
+struct TmaConfig {
+    int stages, chunk, ahead;
+};
+constexpr TmaConfig kTmaMid = {6, 16384, 4};
+constexpr TmaConfig kTmaBig = {6, 32768, 4};
+constexpr int kMaxDynSmem = 6 * 32768;
 constexpr int kMoveTile = 256;     // moves staged in shared memory at a time
 constexpr int kMaxWindows = 16;    // registered recv windows per process
 
@@ -122,6 +121,10 @@ struct ExecParams {
     int32_t nS;                // column slices per move; CTA c owns slice c % nS
     int32_t nF;                // flow groups; CTA c owns flow group c / nS
     int32_t mode;              // 0 single GPU, 1 emulated GPUs, 2 multi-process
+    int32_t stages;            // TMA ring: stages x chunk bytes of dynamic shared memory
+    int32_t chunk;
+    int32_t ahead;             // loads in flight ahead of the oldest store (<= stages - 2)
+    int32_t pad2;
 };
 
 }  // namespace mpxa
