@@ -28,6 +28,7 @@
 
 namespace mpxa {
 cudaError_t launch_exec(const ExecParams &P, int nC, int nG, bool cooperative, cudaStream_t stream);
+cudaError_t launch_small(const ExecParams &P, int nC, int nG, bool cooperative, cudaStream_t stream);
 cudaError_t launch_counts(const int64_t *sc, int64_t *rc, int64_t *rd, int p, int r0, int nr,
                           cudaStream_t stream);
 cudaError_t launch_scan(const int64_t *counts, int64_t *rc, int64_t *rd, int p, int nr,
@@ -55,6 +56,8 @@ constexpr uint64_t kSliceBytes = 16384;    // target column-slice length of the 
 constexpr uint64_t kMovesPerCta = 8;       // small moves per CTA (latency-bound regime)
 constexpr uint64_t kMinSlice = 4096;       // smallest slice worth a CTA when filling the GPU
 constexpr uint64_t kBigPerCta = 2u << 20;  // bytes per CTA per step above which the big TMA config wins
+constexpr uint64_t kSmallItemsPerCta = 2048;   // small kernel: 16-B pieces per CTA per step (one batch)
+constexpr uint64_t kSmallItemsOneCta = 2048;   // multi-step programs: largest step one CTA handles
 
 // A program uploaded to device memory: [GpuProg x G][steps][moves].
 struct DevProg {
@@ -139,8 +142,10 @@ struct mpxa_comm_s {
     double timeout_s = 60.0;
     int sm_count = 148, cap_ctas = 296;   // cap_ctas: mid TMA config (2 CTAs / SM)
     int cap_big = 148;                     // big TMA config (1 CTA / SM)
+    int cap_small = 148;                   // small-message kernel (1 CTA / SM)
     int force_ns = 0, force_nf = 0;           // MPXA_NS / MPXA_NF overrides (tuning)
     int force_big = -1;                       // MPXA_TMA_BIG=0/1 override (tuning)
+    bool force_exec = false;                  // MPXA_NO_SMALL=1: never use the small-message kernel
 
     SymRegion *sym_local = nullptr;            // G regions when emulated, else 1
     SymRegion *sym_map[kMaxGpus] = {};
@@ -376,7 +381,28 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
     E.chunk = tc.chunk;
     E.ahead = tc.ahead;
     ++c->epoch;   // host mirror only; the kernels keep the authoritative epoch in DevComm
-    cudaError_t e = launch_exec(E, gr.n(), c->emulated ? c->G : 1, c->emulated, stream);
+    cudaError_t e;
+    const uint64_t maxmove = (uint64_t)dp.host.max_move * unit;
+    const uint64_t ppm = std::max<uint64_t>(1, cdiv(maxmove, 16));
+    // pieces per step, fan-out stores counted per destination (max_step_units counts them)
+    const uint64_t items = std::max<uint64_t>((uint64_t)dp.host.max_step_moves,
+                                              (uint64_t)dp.host.max_step_units / std::max<int64_t>(1, dp.host.max_move)) * ppm;
+    const bool one_step = dp.nsteps == 1;
+    // latency regime: short moves, and a step small enough for one CTA unless the program
+    // has a single step (then several CTAs may share it)
+    const bool small = !c->force_exec && maxmove <= kSmallKernelMax &&
+                       (one_step || items <= kSmallItemsOneCta);
+    if (small) {
+        E.nS = E.nF = 1;
+        E.small_ppm = (int32_t)ppm;
+        size_t nmoves_g = 0;
+        for (const auto &mv : dp.host.moves) nmoves_g = std::max(nmoves_g, mv.size());
+        E.small_cache = nmoves_g <= (size_t)kSmallMovesSmem ? (int32_t)nmoves_g : 0;
+        int nC = one_step ? (int)std::min<uint64_t>(cdiv(items, kSmallItemsPerCta), (uint64_t)c->cap_small) : 1;
+        e = launch_small(E, std::max(1, nC), c->emulated ? c->G : 1, c->emulated, stream);
+    } else {
+        e = launch_exec(E, gr.n(), c->emulated ? c->G : 1, c->emulated, stream);
+    }
     if (e != cudaSuccess) {
         if (getenv("MPXA_DEBUG")) fprintf(stderr, "mpxa: launch failed: %s\n", cudaGetErrorString(e));
         return MPXA_ERR_CUDA;
@@ -626,9 +652,11 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     if (c->emulated) { cap = std::max(1, cap / c->G); capb = std::max(1, capb / c->G); }
     c->cap_ctas = cap;
     c->cap_big = capb;
+    c->cap_small = std::max(1, (c->emulated ? c->sm_count / c->G : c->sm_count));
     if (const char *e = getenv("MPXA_NS")) c->force_ns = atoi(e);
     if (const char *e = getenv("MPXA_NF")) c->force_nf = atoi(e);
     if (const char *e = getenv("MPXA_TMA_BIG")) c->force_big = atoi(e);
+    if (const char *e = getenv("MPXA_NO_SMALL")) c->force_exec = atoi(e) != 0;
     CK(cudaHostAlloc((void **)&c->err_host, sizeof(int32_t), cudaHostAllocMapped));
     *c->err_host = 0;
     CK(cudaHostGetDevicePointer((void **)&c->err_dev, c->err_host, 0));
@@ -833,15 +861,15 @@ int mpxa_alltoallv_counts(const int64_t *d_sc, int64_t *d_rc, int64_t *d_rd, mpx
                           mpxa_stream_t st) {
     if (!c || !d_sc || !d_rc || !d_rd) return MPXA_ERR_ARG;
     if (c->poisoned) return MPXA_ERR_TIMEOUT;
-    if (c->nprocs == 1) {
+    if (c->nprocs == 1 && !c->emulated) {
         // all p ranks are on this device: one kernel, transpose + warp scans
         cudaError_t e = launch_counts(d_sc, d_rc, d_rd, c->p, 0, c->p, S(st));
         if (e != cudaSuccess) return MPXA_ERR_CUDA;
         c->launches++;
         return MPXA_SUCCESS;
     }
-    // multi-process: an alltoall of one int64 per rank pair into registered staging,
-    // then the scan kernel (2 launches)
+    // multi-process (and emulated GPUs, which run the same protocol): an alltoall of one
+    // int64 per rank pair into registered staging, then the scan kernel (2 launches)
     size_t bytes = (size_t)c->R * c->p * sizeof(int64_t);
     if (!c->counts_tmp) {
         CK(cudaMalloc((void **)&c->counts_tmp, bytes));
@@ -1037,6 +1065,13 @@ int mpxa_plan_moves(const void *plan, int gpu, mpxa_plan_move *out, int *n) {
         memcpy(out, v.data(), sizeof(Move) * v.size());
     }
     *n = (int)v.size();
+    return MPXA_SUCCESS;
+}
+
+// undocumented debug hook (MPXA_TRACE builds): copy the device phase stamps
+int mpxa__trace(mpxa_comm_t c, uint64_t *out16) {
+    if (!c || !out16) return MPXA_ERR_ARG;
+    CK(cudaMemcpy(out16, (char *)c->dc + offsetof(DevComm, trace), 32 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     return MPXA_SUCCESS;
 }
 

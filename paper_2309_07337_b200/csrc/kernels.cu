@@ -206,6 +206,11 @@ struct RingEntry {
     uint8_t fanout, dst_kind;
 };
 
+#ifdef MPXA_TRACE
+#define TRACE(k) do { if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x == 0 || threadIdx.x == 32)) P.dc->trace[(k) + (threadIdx.x ? 16 : 0)] = globaltimer(); } while (0)
+#else
+#define TRACE(k) do { } while (0)
+#endif
 constexpr int kMaxStepsSmem = 64;
 struct StepInfo {
     int32_t first;          // index of this CTA's first move (flow group range start)
@@ -386,33 +391,56 @@ struct SmallJob {
     uint8_t fanout, dst_kind, ro;
 };
 
+// Up to 16 bytes at any alignment, in registers: the (at most five) aligned words that
+// overlap [sp, sp+len) are loaded independently (one round trip), then funnel-shifted.
+// Only words holding wanted bytes are touched, so nothing outside the 4-byte granules of
+// the piece is read.
+__device__ __forceinline__ uint4 load_piece(const char *sp, uint32_t len) {
+    const uintptr_t a = (uintptr_t)sp & ~(uintptr_t)3;
+    const uint32_t sh = 8u * (uint32_t)((uintptr_t)sp & 3);
+    const uint32_t *wp = (const uint32_t *)a;
+    const uintptr_t end = (uintptr_t)sp + len;
+    uint32_t w[5];
+#pragma unroll
+    for (int i = 0; i < 5; i++) w[i] = (a + 4 * i < end) ? __ldcg(wp + i) : 0u;
+    return make_uint4(__funnelshift_r(w[0], w[1], sh), __funnelshift_r(w[1], w[2], sh),
+                      __funnelshift_r(w[2], w[3], sh), __funnelshift_r(w[3], w[4], sh));
+}
+
+__device__ __forceinline__ void store_piece(char *dp, uint4 v, uint32_t len) {
+    if (len == 16 && (((uintptr_t)dp) & 15) == 0) { st16((uint4 *)dp, v); return; }
+    if (len == 16 && (((uintptr_t)dp) & 3) == 0) {
+        uint32_t *d = (uint32_t *)dp;
+        d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+        return;
+    }
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int b = 0; b < 16; b++)
+        if ((uint32_t)b < len) dp[b] = (char)(w[b >> 2] >> (8 * (b & 3)));
+}
+
+// Batched copy of up to kBatch SMALL moves by one warp (n <= 512 B each): lane l moves bytes
+// [16l, 16l+16) of every move; all loads of the batch are issued before any store.
 __device__ __noinline__ void small_batch(const ExecParams &P, const ExecShared &S, const SmallJob *jobs, int nj,
                                             int lane) {
+    TRACE(6);
     uint4 v[kBatch];
-    bool vec[kBatch];
 #pragma unroll
     for (int k = 0; k < kBatch; k++) {
         v[k] = make_uint4(0, 0, 0, 0);
-        vec[k] = false;
         if (k >= nj) continue;
         const SmallJob &j = jobs[k];
         const uint32_t o = (uint32_t)lane * 16;
         if (o >= j.n) continue;
         const uint32_t len = min(16u, j.n - o);
         const char *sp = j.src + o;
-        bool dal = true;
-        if (!j.fanout) dal = (((uintptr_t)(j.dst + o)) & 15) == 0;
-        else
-            for (int r = 0; r < P.p; r++) dal &= (((uintptr_t)(base_of(P, S, j.dst_kind, r) + j.doff + o)) & 15) == 0;
-        if (len == 16 && (((uintptr_t)sp) & 15) == 0 && dal) {
-            vec[k] = true;
+        if (len == 16 && (((uintptr_t)sp) & 15) == 0)
             v[k] = j.ro ? ld16<true>((const uint4 *)sp) : ld16<false>((const uint4 *)sp);
-        } else {
-            uint32_t w[4] = {0, 0, 0, 0};
-            for (uint32_t b = 0; b < len; b++) w[b >> 2] |= (uint32_t)ldcg((const uint8_t *)sp + b) << (8 * (b & 3));
-            v[k] = make_uint4(w[0], w[1], w[2], w[3]);
-        }
+        else
+            v[k] = load_piece(sp, len);
     }
+    TRACE(7);
 #pragma unroll
     for (int k = 0; k < kBatch; k++) {
         if (k >= nj) continue;
@@ -420,22 +448,26 @@ __device__ __noinline__ void small_batch(const ExecParams &P, const ExecShared &
         const uint32_t o = (uint32_t)lane * 16;
         if (o >= j.n) continue;
         const uint32_t len = min(16u, j.n - o);
-        const int nd = j.fanout ? P.p : 1;
-        for (int r = 0; r < nd; r++) {
-            char *dp = (j.fanout ? base_of(P, S, j.dst_kind, r) + j.doff : j.dst) + o;
-            if (vec[k]) {
-                st16((uint4 *)dp, v[k]);
-            } else {
-                const uint32_t w[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
-                for (uint32_t b = 0; b < len; b++) dp[b] = (char)(w[b >> 2] >> (8 * (b & 3)));
-            }
+        if (!j.fanout) {
+            store_piece(j.dst + o, v[k], len);
+        } else {
+            for (int r = 0; r < P.p; r++) store_piece(base_of(P, S, j.dst_kind, r) + j.doff + o, v[k], len);
         }
     }
+    TRACE(8);
 }
 
-__global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_constant__ ExecParams P) {
+__global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_constant__ ExecParams Pk) {
     extern __shared__ __align__(128) char dyn_smem[];
     __shared__ ExecShared S;
+    // the helpers take the parameters by reference; a shared-memory copy keeps those
+    // references out of the (slow, generic-addressed) kernel-parameter window
+    __shared__ ExecParams P;
+    static_assert(sizeof(ExecParams) % 8 == 0, "ExecParams copy");
+    for (int i = threadIdx.x; i < (int)(sizeof(ExecParams) / 8); i += kThreads)
+        reinterpret_cast<uint64_t *>(&P)[i] = reinterpret_cast<const uint64_t *>(&Pk)[i];
+    __syncthreads();
+    TRACE(0);
     const int g = P.my_gpu >= 0 ? P.my_gpu : (int)blockIdx.y;
     const int c = blockIdx.x;
     const int sl = c % P.nS;                  // column slice
@@ -490,6 +522,7 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
     }
 
     SliceCache sc;
+    TRACE(1);
     for (int s = 0; s < nsteps; s++) {
         StepInfo st;
         if (steps_in_smem) {
@@ -535,6 +568,7 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
                 S.moves[i] = prog.moves[st.first + q];
             }
             __syncthreads();
+            TRACE(2);
             if (warp == 0) {
                 if (lane == 0) {
                     for (int i = 0; i < cnt; i++) {
@@ -594,6 +628,7 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
                 }
                 if (nj) small_batch(P, S, jobs, nj, lane);
             }
+            TRACE(3);
         }
         // writers make their generic stores visible to the async proxy when anything will
         // consume them (a later step of this launch, or a peer signalled now); the producer
@@ -601,7 +636,9 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
         const bool consumed = (s + 1 < nsteps) || (multi && st.signal_mask);
         if (consumed && wrote) fence_proxy_async();
         if (t == 0) prod.drain(P, S, consumed);
+        TRACE(4);
         __syncthreads();
+        TRACE(5);
         // ---- signal the peers written in this step (this CTA's share) ----
         if (multi && st.signal_mask && t < 32 && ((st.signal_mask >> t) & 1u)) {
             __threadfence_system();
@@ -682,6 +719,176 @@ __global__ void mpxa_scan_kernel(const int64_t *__restrict__ counts, int64_t *__
 // ------------------------------------------------------------------------------------
 // host-side launchers (called from api.cpp)
 // ------------------------------------------------------------------------------------
+// ------------------------------------------------------------------------------------
+// Small-message executor (short moves): items are (move, 16-byte piece) pairs spread over
+// all threads, four in flight per thread, moves cached in shared memory, no TMA and little
+// code -- these launches are latency-bound, so the kernel touches as few instruction lines
+// and memory round trips as possible.  Multi-step programs run in ONE CTA per GPU (steps
+// are separated by __syncthreads); single-step programs may use several CTAs (no step
+// reads another CTA's output).  Same program format and flag/CTS protocol as
+// mpxa_exec_kernel (CTA c signals / waits slot c).
+// ------------------------------------------------------------------------------------
+constexpr int kSmallThreads = 512;
+
+struct SmallShared {
+    char *recv_base[kMaxGpus];
+    char *work_base[kMaxGpus];
+    SymRegion *sym[kMaxGpus];
+    uint64_t epoch;
+    uint32_t cts_ok;
+    int abort_flag;
+};
+
+__device__ __forceinline__ char *sbase(const ExecParams &P, const SmallShared &S, int kind, int rank) {
+    const int g = rank / P.R;
+    const uint64_t local = (uint64_t)(rank - g * P.R);
+    if (kind == BK_SEND)
+        return (char *)P.send + (P.mode == 2 ? 0 : (uint64_t)g * P.R * P.send_stride) + local * P.send_stride;
+    if (kind == BK_RECV) return S.recv_base[g] + local * P.recv_stride;
+    return S.work_base[g] + local * P.work_stride;
+}
+
+// threads < 32, one per set bit of mask: spin until slot >= want (watchdog as in the main kernel)
+__device__ __forceinline__ void small_wait(const ExecParams &P, SmallShared &S, uint32_t mask, const uint64_t *slot0,
+                                           uint64_t stride, uint64_t want) {
+    const int t = threadIdx.x;
+    if (t < 32 && ((mask >> t) & 1u)) {
+        const uint64_t *slot = slot0 + (uint64_t)t * stride;
+        uint64_t start = 0;
+        int it = 0;
+        while (ld_acquire_sys(slot) < want) {
+            if (++it > 32) {
+                __nanosleep(64);
+                if (start == 0) start = globaltimer();
+                else if ((int64_t)(globaltimer() - start) > P.timeout_ns) {
+                    atomicExch(P.err, 1);
+                    S.abort_flag = 1;
+                    break;
+                }
+            }
+            if (*(volatile int *)&S.abort_flag) break;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __grid_constant__ ExecParams P) {
+    __shared__ SmallShared S;
+    extern __shared__ __align__(16) char small_dyn[];   // the program's moves, when they fit
+    const int g = P.mode == 1 ? (int)blockIdx.y : P.my_gpu;
+    const int t = threadIdx.x;
+    const GpuProg prog = P.mode == 1 ? P.progs[g] : P.prog;
+    const bool multi = P.G > 1;
+    const bool cached = P.small_cache != 0;
+    Move *smoves = reinterpret_cast<Move *>(small_dyn);
+    if (cached)   // every move of the program, once: no descriptor round trip in any step
+        for (int i = t; i < prog.nmoves; i += kSmallThreads) smoves[i] = prog.moves[i];
+    if (t < P.G) {
+        S.work_base[t] = P.dc->work_base[t];
+        S.sym[t] = P.dc->sym[t];
+        S.recv_base[t] = P.mode == 0 ? P.recv
+                         : P.mode == 1 ? (t == g ? P.recv + (uint64_t)t * P.R * P.recv_stride : nullptr)
+                                       : (t == g ? P.recv : nullptr);
+    }
+    if (t == 0) {
+        S.cts_ok = 0;
+        S.abort_flag = 0;
+        S.epoch = multi ? *(volatile uint64_t *)&P.dc->epoch + 1 : 0;
+    }
+    __syncthreads();
+    const uint64_t epoch = S.epoch;
+    if (multi && t < P.G && t != g) {
+        CtsSlot *slot = &S.sym[t]->cts[g];
+        if (P.mode == 2) { slot->win = P.recv_win; slot->off = P.recv_off; }
+        else { slot->win = 0; slot->off = (uint64_t)(uintptr_t)(P.recv + (uint64_t)g * P.R * P.recv_stride); }
+        __threadfence_system();
+        st_release_sys(&slot->epoch, epoch);
+    }
+    const Move *mvs = cached ? smoves : prog.moves;
+    const uint32_t ppm = (uint32_t)P.small_ppm;        // 16-byte pieces per move (uniform bound)
+    uint32_t prev_wait = 0;
+    for (int s = 0; s < prog.nsteps; s++) {
+        const Step st = prog.steps[s];
+        if (multi) {
+            if (prev_wait) small_wait(P, S, prev_wait, &S.sym[g]->flags[0][blockIdx.x], kMaxCtas, (epoch << 8) | (uint64_t)s);
+            const uint32_t need = st.signal_mask & ~S.cts_ok;
+            if (need) {
+                small_wait(P, S, need, &S.sym[g]->cts[0].epoch, sizeof(CtsSlot) / 8, epoch);
+                if (t < 32 && ((need >> t) & 1u)) {
+                    const CtsSlot *cs = &S.sym[g]->cts[t];
+                    S.recv_base[t] = P.dc->win_table[t * kMaxWindows + cs->win] + cs->off;
+                }
+            }
+            __syncthreads();
+            if (t == 0) S.cts_ok |= need;
+            if (S.abort_flag) return;
+        }
+        // items = (move, 16-byte piece); thread t takes items t, t+T, ... four at a time:
+        // all four loads in flight before the stores
+        const uint32_t items = (uint32_t)(st.move_end - st.move_begin) * ppm;
+        const uint32_t TT = gridDim.x * kSmallThreads;   // several CTAs only for 1-step programs
+        for (uint32_t base = blockIdx.x * kSmallThreads + t; base < items; base += TT * kBatch) {
+            uint4 v[kBatch];
+#pragma unroll
+            for (int k = 0; k < kBatch; k++) {
+                v[k] = make_uint4(0, 0, 0, 0);
+                const uint32_t it = base + (uint32_t)k * TT;
+                if (it >= items) continue;
+                const Move &m = mvs[st.move_begin + it / ppm];
+                const uint32_t n = (uint32_t)((uint64_t)m.len * P.unit), o = (it % ppm) * 16;
+                if (o >= n) continue;
+                v[k] = load_piece(sbase(P, S, m.src_kind, m.src_rank) + (uint64_t)m.src_off * P.unit + o, min(16u, n - o));
+            }
+#pragma unroll
+            for (int k = 0; k < kBatch; k++) {
+                const uint32_t it = base + (uint32_t)k * TT;
+                if (it >= items) continue;
+                const Move &m = mvs[st.move_begin + it / ppm];
+                const uint32_t n = (uint32_t)((uint64_t)m.len * P.unit), o = (it % ppm) * 16;
+                if (o >= n) continue;
+                const uint32_t len = min(16u, n - o);
+                const uint64_t doff = (uint64_t)m.dst_off * P.unit + o;
+                if (!m.fanout) {
+                    store_piece(sbase(P, S, m.dst_kind, m.dst_rank) + doff, v[k], len);
+                } else {
+                    for (int r = 0; r < P.p; r++) store_piece(sbase(P, S, m.dst_kind, r) + doff, v[k], len);
+                }
+            }
+        }
+        __syncthreads();
+        if (multi && st.signal_mask && t < 32 && ((st.signal_mask >> t) & 1u)) {
+            __threadfence_system();
+            st_release_sys(&S.sym[t]->flags[g][blockIdx.x], (epoch << 8) | (uint64_t)(s + 1));
+        }
+        prev_wait = st.wait_mask;
+    }
+    if (multi && prev_wait) {
+        small_wait(P, S, prev_wait, &S.sym[g]->flags[0][blockIdx.x], kMaxCtas, (epoch << 8) | (uint64_t)prog.nsteps);
+        __syncthreads();
+    }
+    if (multi && t == 0) {
+        __threadfence();
+        if (atomicAdd(&P.dc->done_ctas, 1u) == gridDim.x * gridDim.y - 1) {
+            P.dc->done_ctas = 0;
+            P.dc->epoch = epoch;
+            __threadfence();
+        }
+    }
+}
+
+cudaError_t launch_small(const ExecParams &P, int nC, int nG, bool cooperative, cudaStream_t stream) {
+    static cudaError_t attr = cudaFuncSetAttribute(mpxa_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)(kSmallMovesSmem * sizeof(Move)));
+    if (attr != cudaSuccess) return attr;
+    const size_t smem = P.small_cache ? (size_t)P.small_cache * sizeof(Move) : 0;
+    dim3 grid(nC, nG), block(kSmallThreads);
+    if (cooperative) {
+        void *args[] = {(void *)&P};
+        return cudaLaunchCooperativeKernel((const void *)mpxa_small_kernel, grid, block, args, smem, stream);
+    }
+    mpxa_small_kernel<<<grid, block, smem, stream>>>(P);
+    return cudaGetLastError();
+}
+
 static cudaError_t exec_attr_once() {
     static cudaError_t e = cudaFuncSetAttribute(mpxa_exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 kMaxDynSmem);

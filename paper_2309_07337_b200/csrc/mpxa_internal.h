@@ -28,6 +28,8 @@ constexpr TmaConfig kTmaMid = {6, 16384, 4};
 constexpr TmaConfig kTmaBig = {6, 32768, 4};
 constexpr int kMaxDynSmem = 6 * 32768;
 constexpr int kMoveTile = 256;     // moves staged in shared memory at a time
+constexpr uint64_t kSmallKernelMax = 8192;  // longest move (bytes) the small-message kernel takes
+constexpr int kSmallMovesSmem = 2048;       // program moves cached in shared memory by the small kernel
 constexpr int kMaxWindows = 16;    // registered recv windows per process
 
 enum BufKind : uint8_t { BK_SEND = 0, BK_RECV = 1, BK_WORK = 2 };
@@ -96,6 +98,7 @@ struct DevComm {
     uint64_t epoch;                         // epochs completed on this GPU (or emulated set)
     uint32_t done_ctas;                     // CTAs of the current launch that finished
     uint32_t pad;
+    uint64_t trace[32];                     // MPXA_TRACE builds: %globaltimer phase stamps
 };
 
 // Launch parameters (~130 B).  Buffers are the caller's process-level rank-major buffers.
@@ -124,7 +127,9 @@ struct ExecParams {
     int32_t stages;            // TMA ring: stages x chunk bytes of dynamic shared memory
     int32_t chunk;
     int32_t ahead;             // loads in flight ahead of the oldest store (<= stages - 2)
-    int32_t pad2;
+    int32_t small_ppm;         // small kernel: 16-byte pieces per move (ceil(max move / 16))
+    int32_t small_cache;       // small kernel: moves cached in shared memory (0 = read global)
+    int32_t pad3;
 };
 
 }  // namespace mpxa

@@ -216,15 +216,18 @@ def test_cfg4_alltoallv(mean, packed):
 
 
 def test_alltoallv_counts_kernel():
+    """A2: single GPU -> fused transpose+scan kernel; emulated GPUs -> the multi-process
+    path (alltoall of one int64 per pair through the flag protocol, then the scan kernel)."""
     for p in (1, 3, 8, 32, 40):
         sc = synth.cfg4_counts(p, p, 4096)
         rc_w, rd_w, _ = oracle.counts_exchange(sc)
-        c = comm(p)
-        d_sc = dev(sc)
-        d_rc = torch.zeros_like(d_sc)
-        d_rd = torch.zeros_like(d_sc)
-        c.alltoallv_counts(d_sc, d_rc, d_rd)
-        assert np.array_equal(host(d_rc), rc_w) and np.array_equal(host(d_rd), rd_w), p
+        for G in [0] + [G for G in (2, 4, 8) if p % G == 0]:
+            c = comm(p, G)
+            d_sc = dev(sc)
+            d_rc = torch.zeros_like(d_sc)
+            d_rd = torch.zeros_like(d_sc)
+            c.alltoallv_counts(d_sc, d_rc, d_rd)
+            assert np.array_equal(host(d_rc), rc_w) and np.array_equal(host(d_rd), rd_w), (p, G)
 
 
 # ------------------------------------------------------------------ persistent requests

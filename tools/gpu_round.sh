@@ -6,7 +6,7 @@ mkdir -p gpurun_out
 TAG=${TAG:-r01}
 SHORT="python bench.py --no-sweep --no-e2e --no-cpu --steps 5 --warmup 3"
 nvidia-smi --query-gpu=index,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/clocks_start_${TAG}.csv 2>&1
-timeout 900 python bench.py ${BENCH_ARGS:-} > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err; echo "bench rc=$?"
+timeout 900 python bench.py ${BENCH_ARGS:-} --write-selector gpurun_out/selector_${TAG}.txt > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err; echo "bench rc=$?"
 tail -c 3000 gpurun_out/bench_${TAG}.json
 if [ "${NCU:-1}" = "1" ]; then
   timeout 300 $SHORT > gpurun_out/short_${TAG}.log 2>&1 && \

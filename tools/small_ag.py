@@ -1,0 +1,13 @@
+"""Tiny allgather launches for latency profiling (ncu)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2309_07337_b200 import Comm
+p = 8
+c = Comm(ranks_per_proc=p, device=0)
+b = int(os.environ.get("B", "4"))
+s = torch.zeros((p, b), dtype=torch.uint8, device="cuda"); r = torch.empty((p, p * b), dtype=torch.uint8, device="cuda")
+for _ in range(8):
+    c.allgather(s, r, algo=os.environ.get("ALGO", "pairwise"))
+torch.cuda.synchronize()
+print("ok")
