@@ -36,7 +36,8 @@ typedef struct {
     int32_t move_begin, move_end;    /* moves sorted by flow within the step     */
     uint32_t signal_mask, wait_mask; /* peer GPUs written / writing in this step */
     int64_t total_len, max_len;
-    int64_t flow_index;              /* internal                                 */
+    int32_t flow_index;              /* internal                                 */
+    int32_t dense_base;              /* >= 0: move k carries flow dense_base + k */
 } mpxa_plan_step;
 
 typedef struct {

@@ -27,8 +27,8 @@
 #include "plan.h"
 
 namespace mpxa {
-cudaError_t launch_exec(const ExecParams &P, int nC, int nG, bool cooperative, cudaStream_t stream);
-cudaError_t launch_small(const ExecParams &P, int nC, int nG, bool cooperative, cudaStream_t stream);
+cudaError_t launch_exec(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream);
+cudaError_t launch_small(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream);
 cudaError_t launch_counts(const int64_t *sc, int64_t *rc, int64_t *rd, int p, int r0, int nr,
                           cudaStream_t stream);
 cudaError_t launch_scan(const int64_t *counts, int64_t *rc, int64_t *rd, int p, int nr,
@@ -53,9 +53,9 @@ namespace {
 
 constexpr uint64_t kBytesPerCta = 65536;   // launch sizing target per CTA per step
 constexpr uint64_t kSliceBytes = 16384;    // target column-slice length of the longest move
-constexpr uint64_t kMovesPerCta = 8;       // small moves per CTA (latency-bound regime)
-constexpr uint64_t kMinSlice = 4096;       // smallest slice worth a CTA when filling the GPU
-constexpr uint64_t kBigPerCta = 2u << 20;  // bytes per CTA per step above which the big TMA config wins
+constexpr uint64_t kMovesPerCta = 1;       // moves per CTA (latency-bound regime: one each)
+constexpr uint64_t kMinSlice = 2048;       // smallest slice worth a CTA when filling the GPU (= TMA min)
+constexpr uint64_t kBigPerCta = 1u << 20;  // bytes per CTA per step above which the big TMA config wins
 constexpr uint64_t kSmallItemsPerCta = 2048;   // small kernel: 16-B pieces per CTA per step (one batch)
 constexpr uint64_t kSmallItemsOneCta = 2048;   // multi-step programs: largest step one CTA handles
 
@@ -146,6 +146,7 @@ struct mpxa_comm_s {
     int force_ns = 0, force_nf = 0;           // MPXA_NS / MPXA_NF overrides (tuning)
     int force_big = -1;                       // MPXA_TMA_BIG=0/1 override (tuning)
     bool force_exec = false;                  // MPXA_NO_SMALL=1: never use the small-message kernel
+    bool pdl = true;                          // MPXA_NO_PDL=1: launches without programmatic serialization
 
     SymRegion *sym_local = nullptr;            // G regions when emulated, else 1
     SymRegion *sym_map[kMaxGpus] = {};
@@ -350,6 +351,20 @@ int make_params(mpxa_comm_t c, ExecParams &E, const DevProg &dp, const char *sen
     E.nflows = dp.host.nflows;
     E.my_gpu = c->emulated ? -1 : (c->nprocs > 1 ? c->proc : 0);
     E.mode = c->emulated ? 1 : (c->nprocs > 1 ? 2 : 0);
+    // step 0 dense on EVERY GPU with one base flow and count (single program per launch
+    // in modes 0 / 2; emulated launches need them equal across the virtual GPUs)
+    E.d0_base = -1;
+    if (dp.nsteps > 0) {
+        const int g0 = c->emulated ? 0 : (c->nprocs > 1 ? c->proc : 0);
+        const Step &s0 = dp.host.steps[g0][0];
+        bool ok = s0.dense_base >= 0;
+        if (c->emulated)
+            for (int g = 1; g < c->G && ok; g++) {
+                const Step &o = dp.host.steps[g][0];
+                ok = o.dense_base == s0.dense_base && o.move_end == s0.move_end;
+            }
+        if (ok) { E.d0_base = s0.dense_base; E.d0_n = s0.move_end - s0.move_begin; }
+    }
     if (c->nprocs > 1) {
         // remote recv bases are resolved on the device from the CTS message (window + offset)
         uintptr_t r = (uintptr_t)recv;
@@ -363,8 +378,12 @@ int make_params(mpxa_comm_t c, ExecParams &E, const DevProg &dp, const char *sen
     return MPXA_SUCCESS;
 }
 
+// pdl: the launch may overlap the previous kernel's tail (the kernel waits on
+// griddepcontrol before touching anything that kernel wrote).  Off for per-call programs,
+// whose tables arrive by a cudaMemcpyAsync right before the launch.
 int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, uint64_t unit,
-                uint64_t send_stride, uint64_t recv_stride, cudaStream_t stream, const Grid *grid = nullptr) {
+                uint64_t send_stride, uint64_t recv_stride, cudaStream_t stream, const Grid *grid = nullptr,
+                bool pdl = true) {
     if (c->poisoned) return MPXA_ERR_TIMEOUT;
     if (dp.nsteps == 0) return MPXA_SUCCESS;
     size_t need = (size_t)dp.host.work_units * unit * c->Rg;
@@ -399,9 +418,9 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
         for (const auto &mv : dp.host.moves) nmoves_g = std::max(nmoves_g, mv.size());
         E.small_cache = nmoves_g <= (size_t)kSmallMovesSmem ? (int32_t)nmoves_g : 0;
         int nC = one_step ? (int)std::min<uint64_t>(cdiv(items, kSmallItemsPerCta), (uint64_t)c->cap_small) : 1;
-        e = launch_small(E, std::max(1, nC), c->emulated ? c->G : 1, c->emulated, stream);
+        e = launch_small(E, std::max(1, nC), c->emulated ? c->G : 1, c->emulated, pdl && c->pdl, stream);
     } else {
-        e = launch_exec(E, gr.n(), c->emulated ? c->G : 1, c->emulated, stream);
+        e = launch_exec(E, gr.n(), c->emulated ? c->G : 1, c->emulated, pdl && c->pdl, stream);
     }
     if (e != cudaSuccess) {
         if (getenv("MPXA_DEBUG")) fprintf(stderr, "mpxa: launch failed: %s\n", cudaGetErrorString(e));
@@ -441,7 +460,7 @@ int run_dynamic(mpxa_comm_t c, const Program &P, const char *send, char *recv, u
     dp.bytes = n;
     dp.host = P;
     dp.nsteps = P.nsteps();
-    int rc = run_program(c, dp, send, recv, unit, send_stride, recv_stride, stream);
+    int rc = run_program(c, dp, send, recv, unit, send_stride, recv_stride, stream, nullptr, /*pdl=*/false);
     CK(cudaEventRecord(s.ev, stream));
     s.used = true;
     dp.dmem = nullptr;
@@ -657,6 +676,7 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     if (const char *e = getenv("MPXA_NF")) c->force_nf = atoi(e);
     if (const char *e = getenv("MPXA_TMA_BIG")) c->force_big = atoi(e);
     if (const char *e = getenv("MPXA_NO_SMALL")) c->force_exec = atoi(e) != 0;
+    if (const char *e = getenv("MPXA_NO_PDL")) c->pdl = atoi(e) == 0;
     CK(cudaHostAlloc((void **)&c->err_host, sizeof(int32_t), cudaHostAllocMapped));
     *c->err_host = 0;
     CK(cudaHostGetDevicePointer((void **)&c->err_dev, c->err_host, 0));

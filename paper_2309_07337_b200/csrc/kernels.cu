@@ -30,6 +30,15 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p) {
 __device__ __forceinline__ void st_release_sys(uint64_t *p, uint64_t v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// Programmatic dependent launch (launches carry programmaticStreamSerialization): the
+// prologue (program tables: library-owned, immutable while launches are in flight) overlaps
+// the previous kernel's tail; everything that kernel may have written or still reads (user
+// buffers, workspace, epoch, flags) is touched only after griddepcontrol.wait, which returns
+// once the preceding grid has completed and its memory is visible.  No-op without PDL.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 __device__ __forceinline__ uint64_t globaltimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -191,6 +200,8 @@ __device__ __forceinline__ void bulk_wait_read(int n) {
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
 
+__device__ __forceinline__ int clampi(int64_t v, int n) { return v < 0 ? 0 : v > n ? n : (int)v; }
+
 __device__ __forceinline__ void slice_of(uint64_t nbytes, int c, int nC, uint64_t &lo, uint64_t &hi) {
     uint64_t nl = (nbytes + kLine - 1) / kLine;
     lo = ((uint64_t)c * nl / nC) * kLine;
@@ -207,11 +218,15 @@ struct RingEntry {
 };
 
 #ifdef MPXA_TRACE
+__device__ uint64_t g_cta_trace[2][kMaxCtas];   // per-CTA entry / exit %globaltimer (GPU 0)
+#define CTA_STAMP(w) do { if (threadIdx.x == 0 && blockIdx.y == 0) g_cta_trace[w][blockIdx.x] = globaltimer(); } while (0)
 #define TRACE(k) do { if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x == 0 || threadIdx.x == 32)) P.dc->trace[(k) + (threadIdx.x ? 16 : 0)] = globaltimer(); } while (0)
 #else
 #define TRACE(k) do { } while (0)
+#define CTA_STAMP(w) do { } while (0)
 #endif
 constexpr int kMaxStepsSmem = 64;
+static_assert(kMoveTile <= kThreads, "prologue prefetch: one move per thread");
 struct StepInfo {
     int32_t first;          // index of this CTA's first move (flow group range start)
     int32_t nm;             // number of moves in this CTA's flow group range
@@ -294,8 +309,14 @@ struct Producer {
     }
     __device__ __forceinline__ void drain(const ExecParams &P, ExecShared &S, bool consumed) {
         while (stored < issued) store_one(P, S);
-        bulk_wait_all();
-        if (consumed) fence_proxy_async();   // bulk writes before generic readers / flag release
+        if (consumed) {
+            bulk_wait_all();
+            fence_proxy_async();   // bulk writes before generic readers / flag release
+        } else {
+            // nothing in this launch reads the data again: only the shared-memory source
+            // must outlive the CTA (kernel completion publishes the global writes)
+            bulk_wait_read(0);
+        }
     }
 };
 
@@ -463,6 +484,7 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
     // the helpers take the parameters by reference; a shared-memory copy keeps those
     // references out of the (slow, generic-addressed) kernel-parameter window
     __shared__ ExecParams P;
+    CTA_STAMP(0);
     static_assert(sizeof(ExecParams) % 8 == 0, "ExecParams copy");
     for (int i = threadIdx.x; i < (int)(sizeof(ExecParams) / 8); i += kThreads)
         reinterpret_cast<uint64_t *>(&P)[i] = reinterpret_cast<const uint64_t *>(&Pk)[i];
@@ -482,20 +504,57 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
     const int64_t x0 = (int64_t)f * P.nflows / P.nF, x1 = (int64_t)(f + 1) * P.nflows / P.nF;
     const int nsteps = prog.nsteps;
     const bool steps_in_smem = nsteps <= kMaxStepsSmem;
-    // the whole step table (with this CTA's flow-group move range) in one parallel round trip
-    if (steps_in_smem && t < nsteps) {
-        const Step st = prog.steps[t];
-        if (P.nF == 1) {            // one flow group: the whole step, no flow-index lookup
-            S.steps[t] = StepInfo{st.move_begin, st.move_end - st.move_begin, st.signal_mask, st.wait_mask};
-        } else {
-            const int32_t *fx = prog.findex + st.flow_index;
-            const int m0 = fx[x0];
-            S.steps[t] = StepInfo{st.move_begin + m0, fx[x1] - m0, st.signal_mask, st.wait_mask};
+    // Prologue: every bookkeeping load of the launch (step table, step 0's first move tile,
+    // workspace / symmetric-region bases, epoch) is ISSUED before any is consumed -- one
+    // memory round trip instead of a chain of them (these launches are latency-bound).
+    const bool ld_step = steps_in_smem && t < nsteps;
+    Step st_r;
+    if (ld_step) st_r = prog.steps[t];
+    // step 0 dense: its moves start at index 0 of every GPU's move array, so this CTA's
+    // first move tile is known without the step table
+    const bool pre = steps_in_smem && nsteps > 0 && P.d0_base >= 0;
+    int pre_cnt = 0;
+    Move mv_r;
+    if (pre) {
+        const int a = clampi(x0 - P.d0_base, P.d0_n);
+        const int nm = clampi(x1 - P.d0_base, P.d0_n) - a;
+        const int rot = nm ? (int)(((int64_t)sl + (int64_t)g * nm / P.G) % nm) : 0;
+        pre_cnt = min(kMoveTile, nm);            // <= kThreads: one move per thread
+        if (t < pre_cnt) {
+            int q = t + rot;
+            if (q >= nm) q -= nm;
+            mv_r = prog.moves[a + q];
         }
     }
+    char *wb_r = nullptr;
+    SymRegion *sym_r = nullptr;
     if (t < P.G) {
-        S.work_base[t] = P.dc->work_base[t];
-        S.sym[t] = P.dc->sym[t];
+        wb_r = P.dc->work_base[t];
+        sym_r = P.dc->sym[t];
+    }
+    if (t == kThreads - 1) {    // a thread with no load outstanding (the fence is a release)
+        for (int s = 0; s < P.stages; s++) mbar_init(smem_u32(&S.mbar[s]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    TRACE(9);
+    if (ld_step) {
+        if (P.nF == 1) {            // one flow group: the whole step, no flow-index lookup
+            S.steps[t] = StepInfo{st_r.move_begin, st_r.move_end - st_r.move_begin, st_r.signal_mask, st_r.wait_mask};
+        } else if (st_r.dense_base >= 0) {   // move k carries flow dense_base + k: arithmetic range
+            const int n = st_r.move_end - st_r.move_begin;
+            const int a = clampi(x0 - st_r.dense_base, n);
+            const int b = clampi(x1 - st_r.dense_base, n);
+            S.steps[t] = StepInfo{st_r.move_begin + a, b - a, st_r.signal_mask, st_r.wait_mask};
+        } else {
+            const int32_t *fx = prog.findex + st_r.flow_index;
+            const int m0 = fx[x0];
+            S.steps[t] = StepInfo{st_r.move_begin + m0, fx[x1] - m0, st_r.signal_mask, st_r.wait_mask};
+        }
+    }
+    if (t < pre_cnt) S.moves[t] = mv_r;
+    if (t < P.G) {
+        S.work_base[t] = wb_r;
+        S.sym[t] = sym_r;
         // own / local recv bases; remote ones (emulated, multi-process) arrive with the CTS
         S.recv_base[t] = P.mode == 0 ? P.recv
                          : P.mode == 1 ? (t == g ? P.recv + (uint64_t)t * P.R * P.recv_stride : nullptr)
@@ -504,11 +563,16 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
     if (t == 0) {
         S.cts_ok = 0;
         S.abort_flag = 0;
-        S.epoch = *(volatile uint64_t *)&P.dc->epoch + 1;
-        for (int s = 0; s < P.stages; s++) mbar_init(smem_u32(&S.mbar[s]), 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    TRACE(10);
     __syncthreads();
+    griddep_wait();
+    griddep_launch_dependents();
+    if (multi) {
+        if (t == 0) S.epoch = *(volatile uint64_t *)&P.dc->epoch + 1;
+        __syncthreads();
+    }
+    TRACE(14);
     const uint64_t epoch = S.epoch;
     // CTS: this GPU is inside `epoch`, so every earlier use of its buffers is complete
     // (stream order); tell every peer it may write into them, and where its recvbuf is
@@ -561,13 +625,15 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
         const int rot = nm ? (int)(((int64_t)sl + (int64_t)g * nm / P.G) % nm) : 0;
         for (int tile = 0; tile < nm; tile += kMoveTile) {
             const int cnt = min(kMoveTile, nm - tile);
-            __syncthreads();   // the previous tile's moves are no longer read
-            for (int i = t; i < cnt; i += kThreads) {
-                int q = tile + i + rot;
-                if (q >= nm) q -= nm;
-                S.moves[i] = prog.moves[st.first + q];
+            if (!(pre && s == 0 && tile == 0)) {   // (prefetched in the prologue)
+                __syncthreads();   // the previous tile's moves are no longer read
+                for (int i = t; i < cnt; i += kThreads) {
+                    int q = tile + i + rot;
+                    if (q >= nm) q -= nm;
+                    S.moves[i] = prog.moves[st.first + q];
+                }
+                __syncthreads();
             }
-            __syncthreads();
             TRACE(2);
             if (warp == 0) {
                 if (lane == 0) {
@@ -662,6 +728,7 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
             __threadfence();
         }
     }
+    CTA_STAMP(1);
 }
 
 // ------------------------------------------------------------------------------------
@@ -789,6 +856,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
                          : P.mode == 1 ? (t == g ? P.recv + (uint64_t)t * P.R * P.recv_stride : nullptr)
                                        : (t == g ? P.recv : nullptr);
     }
+    __syncthreads();
+    griddep_wait();
+    griddep_launch_dependents();
     if (t == 0) {
         S.cts_ok = 0;
         S.abort_flag = 0;
@@ -875,18 +945,34 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
     }
 }
 
-cudaError_t launch_small(const ExecParams &P, int nC, int nG, bool cooperative, cudaStream_t stream) {
+// Launch with the PDL attribute (pdl) or cooperatively (emulated GPUs: co-residency of the
+// virtual GPUs' CTA rows is required by the flag protocol).
+static cudaError_t launch_kernel(void (*kern)(ExecParams), const ExecParams &P, dim3 grid, dim3 block, size_t smem,
+                                 bool cooperative, bool pdl, cudaStream_t stream) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    if (cooperative) {
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+    } else {
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, P);
+}
+
+cudaError_t launch_small(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream) {
     static cudaError_t attr = cudaFuncSetAttribute(mpxa_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)(kSmallMovesSmem * sizeof(Move)));
     if (attr != cudaSuccess) return attr;
     const size_t smem = P.small_cache ? (size_t)P.small_cache * sizeof(Move) : 0;
-    dim3 grid(nC, nG), block(kSmallThreads);
-    if (cooperative) {
-        void *args[] = {(void *)&P};
-        return cudaLaunchCooperativeKernel((const void *)mpxa_small_kernel, grid, block, args, smem, stream);
-    }
-    mpxa_small_kernel<<<grid, block, smem, stream>>>(P);
-    return cudaGetLastError();
+    return launch_kernel(mpxa_small_kernel, P, dim3(nC, nG), dim3(kSmallThreads), smem, cooperative, pdl, stream);
 }
 
 static cudaError_t exec_attr_once() {
@@ -895,17 +981,11 @@ static cudaError_t exec_attr_once() {
     return e;
 }
 
-cudaError_t launch_exec(const ExecParams &P, int nC, int nG, bool cooperative, cudaStream_t stream) {
+cudaError_t launch_exec(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream) {
     cudaError_t e = exec_attr_once();
     if (e != cudaSuccess) return e;
     const size_t smem = (size_t)P.stages * P.chunk;
-    dim3 grid(nC, nG), block(kThreads);
-    if (cooperative) {
-        void *args[] = {(void *)&P};
-        return cudaLaunchCooperativeKernel((const void *)mpxa_exec_kernel, grid, block, args, smem, stream);
-    }
-    mpxa_exec_kernel<<<grid, block, smem, stream>>>(P);
-    return cudaGetLastError();
+    return launch_kernel(mpxa_exec_kernel, P, dim3(nC, nG), dim3(kThreads), smem, cooperative, pdl, stream);
 }
 
 cudaError_t launch_counts(const int64_t *sc, int64_t *rc, int64_t *rd, int p, int r0, int nr,
@@ -934,3 +1014,9 @@ int exec_max_ctas_per_sm(size_t dyn_smem) {
 }
 
 }  // namespace mpxa
+
+#ifdef MPXA_TRACE
+extern "C" int mpxa__cta_trace(uint64_t *out) {   // debug hook: [2][kMaxCtas] stamps
+    return cudaMemcpyFromSymbol(out, mpxa::g_cta_trace, sizeof(mpxa::g_cta_trace)) == cudaSuccess ? 0 : 6;
+}
+#endif

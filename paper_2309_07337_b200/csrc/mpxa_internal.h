@@ -62,7 +62,9 @@ struct Step {
     uint32_t wait_mask;     // remote GPUs that write into this GPU in this step
     int64_t total_len;      // sum of move lengths in units (host-side sizing)
     int64_t max_len;        // max move length in units (host-side path hints)
-    int64_t flow_index;     // offset of this step's flow index in GpuProg::findex
+    int32_t flow_index;     // offset of this step's flow index in GpuProg::findex
+    int32_t dense_base;     // >= 0: move k of the step carries flow dense_base + k (the flow
+                            // index is then arithmetic: no findex lookup); -1 otherwise
 };
 static_assert(sizeof(Step) == 40, "Step layout");
 
@@ -129,6 +131,8 @@ struct ExecParams {
     int32_t ahead;             // loads in flight ahead of the oldest store (<= stages - 2)
     int32_t small_ppm;         // small kernel: 16-byte pieces per move (ceil(max move / 16))
     int32_t small_cache;       // small kernel: moves cached in shared memory (0 = read global)
+    int32_t d0_base;           // step 0 dense (Step::dense_base >= 0): its base flow, and
+    int32_t d0_n;              // its move count -> step 0's moves are fetched in the prologue
     int32_t pad3;
 };
 

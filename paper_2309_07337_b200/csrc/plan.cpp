@@ -81,7 +81,14 @@ public:
             s.wait_mask = wt[g];
             s.total_len = tot;
             s.max_len = mx;
-            s.flow_index = (int64_t)P_.findex[g].size();
+            s.flow_index = (int32_t)P_.findex[g].size();
+            s.dense_base = -1;
+            if (!cur_[g].empty()) {
+                bool dense = true;
+                const uint32_t fb = cur_[g][0].flow;
+                for (size_t k = 0; k < cur_[g].size() && dense; k++) dense = cur_[g][k].flow == fb + (uint32_t)k;
+                if (dense) s.dense_base = (int32_t)fb;
+            }
             size_t q = 0;
             for (int x = 0; x <= P_.nflows; x++) {       // findex[x] = #moves with flow < x
                 while (q < cur_[g].size() && cur_[g][q].flow < (uint32_t)x) q++;

@@ -52,7 +52,8 @@ class PlanMove(ctypes.Structure):
 class PlanStep(ctypes.Structure):
     _fields_ = [("move_begin", ctypes.c_int32), ("move_end", ctypes.c_int32),
                 ("signal_mask", ctypes.c_uint32), ("wait_mask", ctypes.c_uint32),
-                ("total_len", ctypes.c_int64), ("max_len", ctypes.c_int64), ("flow_index", ctypes.c_int64)]
+                ("total_len", ctypes.c_int64), ("max_len", ctypes.c_int64), ("flow_index", ctypes.c_int32),
+                ("dense_base", ctypes.c_int32)]
 
 
 class PlanInfo(ctypes.Structure):
