@@ -58,6 +58,10 @@ constexpr uint64_t kMinSlice = 2048;       // smallest slice worth a CTA when fi
 constexpr uint64_t kBigPerCta = 1u << 20;  // bytes per CTA per step above which the big TMA config wins
 constexpr uint64_t kSmallItemsPerCta = 2048;   // small kernel: 16-B pieces per CTA per step (one batch)
 constexpr uint64_t kSmallItemsOneCta = 2048;   // multi-step programs: largest step one CTA handles
+constexpr uint64_t kDynMinMove = 64u << 10;    // dynamic mode: smallest move (bytes) ...
+constexpr uint64_t kDynMinTotal = 8u << 20;    // ... and smallest per-GPU step volume
+constexpr uint64_t kDynPiecesPerCta = 64;      // target queue pieces per CTA (measured: 16 -> 64 closes the tail)
+constexpr uint64_t kDynMaxPiece = 512u << 10;  // largest piece (bytes)
 
 // A program uploaded to device memory: [GpuProg x G][steps][moves].
 struct DevProg {
@@ -66,7 +70,25 @@ struct DevProg {
     Program host;
     int nsteps = 0;
     std::vector<GpuProg> gp;   // the [G] GpuProg table as uploaded (device pointers)
+    int64_t eq_len = -1;       // single-step program whose moves all have this length (units)
+    int64_t max_gpu_moves = 0; // most moves any GPU runs
 };
+
+// dynamic-mode eligibility facts of a program (DevProg::eq_len, max_gpu_moves)
+void prog_facts(DevProg &dp) {
+    const Program &P = dp.host;
+    dp.eq_len = -1;
+    dp.max_gpu_moves = 0;
+    for (const auto &mv : P.moves) dp.max_gpu_moves = std::max<int64_t>(dp.max_gpu_moves, (int64_t)mv.size());
+    if (P.nsteps() != 1) return;
+    int64_t L = -1;
+    for (const auto &mv : P.moves)
+        for (const Move &m : mv) {
+            if (L < 0) L = m.len;
+            else if (m.len != L) return;
+        }
+    dp.eq_len = L;
+}
 
 size_t serialize(const Program &P, std::vector<char> &buf, uintptr_t dbase) {
     const int G = P.G;
@@ -147,6 +169,8 @@ struct mpxa_comm_s {
     int force_big = -1;                       // MPXA_TMA_BIG=0/1 override (tuning)
     bool force_exec = false;                  // MPXA_NO_SMALL=1: never use the small-message kernel
     bool pdl = true;                          // MPXA_NO_PDL=1: launches without programmatic serialization
+    bool dyn = true;                          // MPXA_NO_DYN=1: static slices only (no work queue)
+    int dyn_pieces = (int)kDynPiecesPerCta;   // MPXA_DYN_PIECES: queue pieces per CTA (tuning)
 
     SymRegion *sym_local = nullptr;            // G regions when emulated, else 1
     SymRegion *sym_map[kMaxGpus] = {};
@@ -278,6 +302,7 @@ int upload_program(const Program &P, std::shared_ptr<DevProg> &out) {
     dp->bytes = n;
     dp->host = P;
     dp->nsteps = P.nsteps();
+    prog_facts(*dp);
     out = dp;
     return MPXA_SUCCESS;
 }
@@ -420,7 +445,36 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
         int nC = one_step ? (int)std::min<uint64_t>(cdiv(items, kSmallItemsPerCta), (uint64_t)c->cap_small) : 1;
         e = launch_small(E, std::max(1, nC), c->emulated ? c->G : 1, c->emulated, pdl && c->pdl, stream);
     } else {
-        e = launch_exec(E, gr.n(), c->emulated ? c->G : 1, c->emulated, pdl && c->pdl, stream);
+        int nC = gr.n();
+        // dynamic mode: large equal-length moves of one step, 16-B congruent addresses
+        // (every move's src and dst differ by a multiple of 16 when all bases, strides and
+        // the unit are); the whole move list fits the prologue's shared-memory tile
+        const uint64_t L = dp.eq_len > 0 ? (uint64_t)dp.eq_len * unit : 0;
+        const uint64_t total = L * (uint64_t)dp.max_gpu_moves;
+        const bool congruent = unit % 16 == 0 && send_stride % 16 == 0 && recv_stride % 16 == 0 &&
+                               ((uintptr_t)send - (uintptr_t)recv) % 16 == 0;
+        if (c->dyn && E.d0_base >= 0 && L >= kDynMinMove && total >= kDynMinTotal && congruent &&
+            dp.max_gpu_moves <= kMoveTile) {
+            // same grid as the static decomposition: it depends on the program only, so
+            // processes that decide differently (local buffer alignment) still pair CTA
+            // flag slots one to one
+            uint64_t U = total / ((uint64_t)nC * (uint64_t)c->dyn_pieces);
+            U = std::max<uint64_t>((uint64_t)E.chunk, std::min<uint64_t>(U, kDynMaxPiece));
+            U = U / (uint64_t)E.chunk * (uint64_t)E.chunk;
+            const uint64_t k = cdiv(L, U);
+            E.nS = nC;
+            E.nF = 1;
+            E.dyn_len = L;
+            E.dyn_u = (int32_t)U;
+            E.dyn_k = (int32_t)k;
+            E.dyn_units = (int32_t)(k * (uint64_t)dp.max_gpu_moves);
+            // every GPU must run the same number of pieces (moves per GPU are equal in the
+            // uniform single-step programs; otherwise stay static)
+            for (const auto &mv : dp.host.moves)
+                if ((int64_t)mv.size() != dp.max_gpu_moves) { E.dyn_units = 0; break; }
+            if (!E.dyn_units) { E.nS = gr.nS; E.nF = gr.nF; nC = gr.n(); }
+        }
+        e = launch_exec(E, nC, c->emulated ? c->G : 1, c->emulated, pdl && c->pdl, stream);
     }
     if (e != cudaSuccess) {
         if (getenv("MPXA_DEBUG")) fprintf(stderr, "mpxa: launch failed: %s\n", cudaGetErrorString(e));
@@ -460,6 +514,7 @@ int run_dynamic(mpxa_comm_t c, const Program &P, const char *send, char *recv, u
     dp.bytes = n;
     dp.host = P;
     dp.nsteps = P.nsteps();
+    prog_facts(dp);
     int rc = run_program(c, dp, send, recv, unit, send_stride, recv_stride, stream, nullptr, /*pdl=*/false);
     CK(cudaEventRecord(s.ev, stream));
     s.used = true;
@@ -677,6 +732,8 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     if (const char *e = getenv("MPXA_TMA_BIG")) c->force_big = atoi(e);
     if (const char *e = getenv("MPXA_NO_SMALL")) c->force_exec = atoi(e) != 0;
     if (const char *e = getenv("MPXA_NO_PDL")) c->pdl = atoi(e) == 0;
+    if (const char *e = getenv("MPXA_NO_DYN")) c->dyn = atoi(e) == 0;
+    if (const char *e = getenv("MPXA_DYN_PIECES")) c->dyn_pieces = std::max(1, atoi(e));
     CK(cudaHostAlloc((void **)&c->err_host, sizeof(int32_t), cudaHostAllocMapped));
     *c->err_host = 0;
     CK(cudaHostGetDevicePointer((void **)&c->err_dev, c->err_host, 0));

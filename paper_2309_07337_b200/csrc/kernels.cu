@@ -478,6 +478,50 @@ __device__ __noinline__ void small_batch(const ExecParams &P, const ExecShared &
     TRACE(8);
 }
 
+// Dynamic mode (ExecParams::dyn_units): the producer thread takes pieces u (dyn_u bytes of
+// move u / dyn_k, whose descriptors the prologue put in S.moves) from the GPU's work queue
+// until it runs dry; the next piece is requested before the current one is streamed, so the
+// atomic's round trip is hidden.  Bytes outside the 16-B aligned body of a piece (only when
+// the move's start or length is not 16-B aligned) are copied by this thread directly.
+__device__ __noinline__ void dyn_produce(const ExecParams &P, ExecShared &S, Producer &prod, int g) {
+    uint32_t *q = &P.dc->dyn_next[g];
+    const uint32_t n = (uint32_t)P.dyn_units, k = (uint32_t)P.dyn_k;
+    const uint64_t U = (uint64_t)P.dyn_u, chunk = (uint64_t)P.chunk;
+    uint32_t u = atomicAdd(q, 1u);
+    while (u < n) {
+        const uint32_t un = atomicAdd(q, 1u);
+        const uint32_t mi = u / k;
+        const Move &m = S.moves[mi];
+        const uint64_t lo = (uint64_t)(u - mi * k) * U;
+        const uint64_t hi = min(P.dyn_len, lo + U);
+        const char *src = base_of(P, S, m.src_kind, m.src_rank) + (uint64_t)m.src_off * P.unit + lo;
+        const uint64_t doff = (uint64_t)m.dst_off * P.unit + lo;
+        char *dst = m.fanout ? nullptr : base_of(P, S, m.dst_kind, m.dst_rank) + doff;
+        const uint64_t nb = hi - lo;
+        uint64_t head = (16 - ((uintptr_t)src & 15)) & 15;
+        if (head > nb) head = nb;
+        const uint64_t body = (nb - head) & ~(uint64_t)15;
+        for (uint64_t i = 0; i < nb; i++) {          // head and tail bytes (plain stores)
+            if (i == head) i = head + body;
+            if (i >= nb) break;
+            const char b = (char)ldcg((const uint8_t *)src + i);
+            if (!m.fanout) dst[i] = b;
+            else
+                for (int j = 0; j < P.p; j++) base_of(P, S, m.dst_kind, j)[doff + i] = b;
+        }
+        for (uint64_t o = 0; o < body; o += chunk) {
+            RingEntry e;
+            e.len = (uint32_t)min(chunk, body - o);
+            e.fanout = m.fanout;
+            e.dst_kind = m.dst_kind;
+            e.doff = doff + head + o;
+            e.dst = m.fanout ? nullptr : dst + head + o;
+            prod.push(P, S, src + head + o, e);
+        }
+        u = un;
+    }
+}
+
 __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_constant__ ExecParams Pk) {
     extern __shared__ __align__(128) char dyn_smem[];
     __shared__ ExecShared S;
@@ -518,7 +562,7 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
     if (pre) {
         const int a = clampi(x0 - P.d0_base, P.d0_n);
         const int nm = clampi(x1 - P.d0_base, P.d0_n) - a;
-        const int rot = nm ? (int)(((int64_t)sl + (int64_t)g * nm / P.G) % nm) : 0;
+        const int rot = (nm && !P.dyn_units) ? (int)(((int64_t)sl + (int64_t)g * nm / P.G) % nm) : 0;
         pre_cnt = min(kMoveTile, nm);            // <= kThreads: one move per thread
         if (t < pre_cnt) {
             int q = t + rot;
@@ -621,8 +665,9 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
 #else
         if (multi && t == 0) fence_proxy_async();   // acquired peer writes before TMA reads
 #endif
-        const int nm = st.nm;
+        const int nm = P.dyn_units ? 0 : st.nm;   // dynamic mode: the work queue below
         const int rot = nm ? (int)(((int64_t)sl + (int64_t)g * nm / P.G) % nm) : 0;
+        if (P.dyn_units && t == 0) dyn_produce(P, S, prod, g);
         for (int tile = 0; tile < nm; tile += kMoveTile) {
             const int cnt = min(kMoveTile, nm - tile);
             if (!(pre && s == 0 && tile == 0)) {   // (prefetched in the prologue)
@@ -718,13 +763,16 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
         wait_mask_ge(P, S, last_wait, &S.sym[g]->flags[0][c], kMaxCtas, (epoch << 8) | (uint64_t)nsteps);
         __syncthreads();
     }
-    // the last CTA of the launch publishes the epoch (the next launch is stream-ordered after)
-    if (multi && t == 0) {
+    // the last CTA of the launch publishes the epoch and resets the work queues (the next
+    // launch is stream-ordered after, and waits on griddepcontrol before reading either)
+    if ((multi || P.dyn_units) && t == 0) {
         __threadfence();
         const uint32_t total = gridDim.x * gridDim.y;
         if (atomicAdd(&P.dc->done_ctas, 1u) == total - 1) {
             P.dc->done_ctas = 0;
-            P.dc->epoch = epoch;
+            if (multi) P.dc->epoch = epoch;
+            if (P.dyn_units)
+                for (int r = 0; r < (int)gridDim.y; r++) P.dc->dyn_next[P.my_gpu >= 0 ? P.my_gpu : r] = 0;
             __threadfence();
         }
     }
@@ -1016,7 +1064,11 @@ int exec_max_ctas_per_sm(size_t dyn_smem) {
 }  // namespace mpxa
 
 #ifdef MPXA_TRACE
-extern "C" int mpxa__cta_trace(uint64_t *out) {   // debug hook: [2][kMaxCtas] stamps
+extern "C" int mpxa__cta_trace(uint64_t *out) {   // debug hook: [2][kMaxCtas] stamps; NULL resets
+    if (!out) {
+        static uint64_t zero[2][mpxa::kMaxCtas];
+        return cudaMemcpyToSymbol(mpxa::g_cta_trace, zero, sizeof zero) == cudaSuccess ? 0 : 6;
+    }
     return cudaMemcpyFromSymbol(out, mpxa::g_cta_trace, sizeof(mpxa::g_cta_trace)) == cudaSuccess ? 0 : 6;
 }
 #endif

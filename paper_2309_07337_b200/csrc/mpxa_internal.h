@@ -100,6 +100,8 @@ struct DevComm {
     uint64_t epoch;                         // epochs completed on this GPU (or emulated set)
     uint32_t done_ctas;                     // CTAs of the current launch that finished
     uint32_t pad;
+    uint32_t dyn_next[kMaxGpus];            // work-queue heads of dynamic launches (per GPU row),
+                                            // reset to 0 by the launch's last CTA
     uint64_t trace[32];                     // MPXA_TRACE builds: %globaltimer phase stamps
 };
 
@@ -133,7 +135,14 @@ struct ExecParams {
     int32_t small_cache;       // small kernel: moves cached in shared memory (0 = read global)
     int32_t d0_base;           // step 0 dense (Step::dense_base >= 0): its base flow, and
     int32_t d0_n;              // its move count -> step 0's moves are fetched in the prologue
-    int32_t pad3;
+    // dynamic mode (dyn_units > 0): single-step program whose moves all have dyn_len bytes and
+    // 16-B congruent source / destination; the moves are cut into dyn_u-byte pieces (dyn_k
+    // per move) that CTAs take from a device work queue (DevComm::dyn_next) -- per-SM
+    // bandwidth differs across the chip, so static slices leave a long tail of slow CTAs
+    int32_t dyn_units;
+    int32_t dyn_k;
+    int32_t dyn_u;
+    uint64_t dyn_len;
 };
 
 }  // namespace mpxa

@@ -49,7 +49,7 @@ if hasattr(L, "mpxa__cta_trace"):
         torch.cuda.synchronize()
         ctypes.memset(buf, 0, 2048 * 8)
         L.mpxa__cta_trace.argtypes = [ctypes.c_void_p]
-        # clear, run one launch, read
+        torch.cuda.synchronize(); L.mpxa__cta_trace(None)   # clear, run one launch, read
         fn(); torch.cuda.synchronize()
         L.mpxa__cta_trace(buf)
         a = np.frombuffer(buf, dtype=np.uint64).reshape(2, 1024).astype(np.int64)
@@ -57,4 +57,5 @@ if hasattr(L, "mpxa__cta_trace"):
         st, en = a[0, :n], a[1, :n]
         t0 = st.min()
         q = lambda x: [int(np.percentile(x - t0, v)) for v in (0, 50, 90, 100)]
-        print(op, b, "ctas", n, "start p0/50/90/100", q(st), "end", q(en), "dur p50", int(np.median(en - st)), flush=True)
+        d = en - st
+        print(op, b, "ctas", n, "dur min/p50/max", int(d.min()), int(np.median(d)), int(d.max()), "start p0/50/90/100", q(st), "end", q(en), "dur p50", int(np.median(en - st)), flush=True)
