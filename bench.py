@@ -210,15 +210,175 @@ def sweep(comm, torch, stream, reps=20):
             del recv
             b *= 4
         out["alltoall"][algo] = rows
+    # library baseline on ONE GPU: NCCL cannot host several ranks of one communicator on a
+    # device, so the reference point is PyTorch's own copy kernels doing the same data
+    # movement (broadcast copy for allgather, transpose copy for alltoall)
+    rows_ag, rows_a2a = [], []
+    b = 4
+    while b <= (64 << 20):
+        send = big[: R * b].view(R, 1, b)
+        recv = torch.empty((R, p, b), dtype=torch.uint8, device=dev)
+        it = max(3, min(reps, int(2e9 // max(1, p * p * b))))
+        us = 1e3 * time_graph(lambda: recv.copy_(send.view(1, p, b).expand(R, p, b)), it, gstream)
+        rows_ag.append([b, round(us, 3), round(p * p * b / us / 1e3, 2)])
+        del recv
+        b *= 2
+    b = 4
+    while b <= (16 << 20):
+        send = big[: R * p * b].view(p, p, b)
+        recv = torch.empty((p, p, b), dtype=torch.uint8, device=dev)
+        it = max(3, min(reps, int(2e9 // max(1, p * p * b))))
+        us = 1e3 * time_graph(lambda: recv.copy_(send.transpose(0, 1)), it, gstream)
+        rows_a2a.append([b, round(us, 3), round(p * p * b / us / 1e3, 2)])
+        del recv
+        b *= 4
+    out["allgather"]["torch_copy_baseline"] = rows_ag
+    out["alltoall"]["torch_copy_baseline"] = rows_a2a
     del big
     return out
+
+
+def configs_on_one_gpu(torch, reps=20):
+    """The other BASELINE.json configs, reduced to what one B200 can host (ranks on one
+    device; cfg5's 8 GPUs also as 8 emulated GPUs running the multi-GPU flag protocol).
+    Every timed point is verified bit-exactly against the oracle first."""
+    import oracle
+    import synth
+    from paper_2309_07337_b200 import Comm
+    dev = "cuda"
+    gstream = torch.cuda.Stream()
+    res = {}
+
+    def dt(x):
+        return torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+
+    # ---- cfg1: p=4 ranks, 8 int32 per destination (latency + exactness) ----
+    c = Comm(ranks_per_proc=4, device=torch.cuda.current_device())
+    send = synth.alltoall_sendbuf(0, 4, 32)
+    want = oracle.alltoall_definition(send)
+    row = {}
+    for algo in ("pairwise", "bruck", "hier"):
+        d_s = dt(send.view(np.int32))
+        d_r = torch.zeros_like(d_s)
+        c.alltoall(d_s, d_r, algo=algo, stream=gstream)
+        torch.cuda.synchronize()
+        ok = bool(np.array_equal(d_r.cpu().numpy().view(np.uint8), want))
+        us = 1e3 * time_graph(lambda: c.alltoall(d_s, d_r, algo=algo, stream=gstream), 100, gstream)
+        row[algo] = {"us": round(us, 3), "verified": ok}
+    res["cfg1_alltoall_p4_8xint32"] = row
+    c.finalize()
+
+    # ---- cfg3 at p=2, 4 (p=8 is the main sweep): alltoall block 4 B .. 16 MiB x4 ----
+    for p in (2, 4):
+        c = Comm(ranks_per_proc=p, device=torch.cuda.current_device(), group_size=2)
+        big = torch.randint(0, 256, (p * p * (16 << 20),), dtype=torch.uint8, device=dev)
+        out = {}
+        for algo in ("pairwise", "bruck", "hier"):
+            rows = []
+            b = 4
+            while b <= (16 << 20):
+                s_ = big[: p * p * b].view(p, p * b)
+                r_ = torch.empty_like(s_)
+                it = max(3, min(reps, int(2e9 // max(1, p * p * b))))
+                us = 1e3 * time_graph(lambda: c.alltoall(s_, r_, algo=algo, stream=gstream), it, gstream)
+                rows.append([b, round(us, 3), round(p * p * b / us / 1e3, 2)])
+                b *= 4
+            # exactness at the largest point (whole buffer, oracle definition)
+            want = oracle.alltoall_definition(s_.cpu().numpy())
+            rows.append({"verified_16MiB": bool(np.array_equal(r_.cpu().numpy(), want))})
+            out[algo] = rows
+        res[f"cfg3_alltoall_p{p}"] = out
+        del big
+        c.finalize()
+
+    # ---- cfg4: alltoallv p=8, int64, counts U{0..2 mean} with 10% zeros; persistent
+    #      init once, then 100 x (start, wait); vs the one-shot call (plan built per call) ----
+    p = 8
+    c = Comm(ranks_per_proc=p, device=torch.cuda.current_device())
+    out = {}
+    for mean in (64, 64 << 10, 4 << 20):
+        counts = synth.cfg4_counts(0, p, mean)
+        sc = counts.astype(np.int64)
+        rc = counts.T.copy()
+        sd = np.zeros_like(sc); sd[:, 1:] = np.cumsum(sc, 1)[:, :-1]
+        rd = np.zeros_like(rc); rd[:, 1:] = np.cumsum(rc, 1)[:, :-1]
+        S = int(max(1, (sd + sc).max())) * 8
+        Rc = int(max(1, (rd + rc).max())) * 8
+        d_s = torch.randint(0, 256, (p, S), dtype=torch.uint8, device=dev)
+        d_r = torch.full((p, Rc), 0xA5, dtype=torch.uint8, device=dev)
+        req = c.alltoallv_init(d_s, sc, sd, d_r, rc, rd, dtype_size=8)
+        req.start(gstream); req.wait(gstream)
+        torch.cuda.synchronize()
+        want = oracle.alltoallv_definition(d_s.cpu().numpy(), sc, sd, rc, rd, 8,
+                                           np.full((p, Rc), 0xA5, dtype=np.uint8))
+        ok = bool(np.array_equal(d_r.cpu().numpy(), want))
+        moved = int(counts.sum()) * 8
+
+        def cycles(n=100):
+            for _ in range(n):
+                req.start(gstream)
+                req.wait(gstream)
+
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        cycles(5)
+        e0.record(gstream); cycles(100); e1.record(gstream)
+        torch.cuda.synchronize()
+        us_p = e0.elapsed_time(e1) * 1e3 / 100
+        us_g = 1e3 * time_graph(lambda: (req.start(gstream), req.wait(gstream)), 100, gstream)
+
+        def one_shot():
+            c.alltoallv(d_s, sc, sd, d_r, rc, rd, dtype_size=8, stream=gstream)
+        one_shot()
+        torch.cuda.synchronize()
+        e0.record(gstream)
+        for _ in range(20):
+            one_shot()
+        e1.record(gstream)
+        torch.cuda.synchronize()
+        us_o = e0.elapsed_time(e1) * 1e3 / 20
+        req.free()
+        out[f"mean_{mean}B"] = {"bytes_moved": moved, "verified": ok,
+                                "persistent_start_wait_us": round(us_p, 3),
+                                "persistent_graph_us": round(us_g, 3),
+                                "one_shot_us": round(us_o, 3),
+                                "GBps_persistent": round(moved / us_p / 1e3, 2),
+                                "hbm_TBps_persistent_graph": round(2 * moved / us_g / 1e6, 3)}
+        del d_s, d_r
+    res["cfg4_alltoallv_p8_persistent_100x"] = out
+    c.finalize()
+
+    # ---- cfg5: p=32 ranks, bf16, block 16 B .. 1 MiB x4: all 32 ranks on this GPU, and the
+    #      same ranks as 8 emulated GPUs x 4 ranks (multi-GPU flag/CTS protocol) ----
+    p = 32
+    for G in (0, 8):
+        c = Comm(ranks_per_proc=p, device=torch.cuda.current_device(), group_size=4, emulate_gpus=G)
+        big = torch.randint(0, 256, (p * p * (1 << 20),), dtype=torch.uint8, device=dev)
+        out = {}
+        for algo in ("hier", "bruck", "pairwise"):
+            rows = []
+            b = 16
+            while b <= (1 << 20):
+                s_ = big[: p * p * b].view(p, p * b).view(torch.bfloat16)
+                r_ = torch.empty_like(s_)
+                it = max(3, min(reps, int(2e9 // max(1, p * p * b))))
+                us = 1e3 * time_graph(lambda: c.alltoall(s_, r_, algo=algo, stream=gstream), it, gstream)
+                rows.append([b, round(us, 3), round(p * p * b / us / 1e3, 2)])
+                b *= 4
+            want = oracle.alltoall_definition(s_.view(torch.uint8).cpu().numpy())
+            rows.append({"verified_1MiB": bool(np.array_equal(r_.view(torch.uint8).cpu().numpy(), want))})
+            out[algo] = rows
+        res["cfg5_alltoall_p32_" + ("1gpu" if G == 0 else "8_emulated_gpus")] = out
+        del big
+        c.finalize()
+    return res
 
 
 def write_selector(sw, path, p, R):
     """Measured selector table: for each op and size, the fastest variant (ties -> SPEC default)."""
     lines = ["# op p ranks_per_proc max_bytes algo  (generated by bench.py --write-selector)"]
     for op in ("allgather", "alltoall"):
-        variants = sw[op]
+        variants = {k: v for k, v in sw[op].items() if not k.startswith("torch")}
         sizes = [row[0] for row in next(iter(variants.values()))]
         best_prev = None
         for i, b in enumerate(sizes):
@@ -341,10 +501,12 @@ def gpu_arm(args):
                         ".".join(map(str, torch.cuda.nccl.version())),
                 "ms_per_step": round(n_ms, 5), "value": round(total_recv / (n_ms * 1e-3) / 1e9, 3), "unit": "GB/s"}
     sw = None
+    cfgs = None
     if args.sweep and ws == 1:
         sw = sweep(comm, torch, stream)
         if args.write_selector:
             write_selector(sw, args.write_selector, p, R)
+        cfgs = configs_on_one_gpu(torch)
     cpu = None
     if rank == 0 and not args.no_cpu:
         cpu = cpu_oracle_sample(send.cpu().numpy(), args.cpu_budget) if ws == 1 else None
@@ -368,7 +530,7 @@ def gpu_arm(args):
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "kernel": "mpxa_exec_kernel (one launch per step; CUDA events on its stream)"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "nccl": nccl,
-            "clocks": clk.report(), "sweep": sw,
+            "clocks": clk.report(), "sweep": sw, "configs": cfgs,
         }
         if args.traffic is not None:
             line["roofline"]["traffic"] = args.traffic

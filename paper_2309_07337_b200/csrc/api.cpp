@@ -427,7 +427,8 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
     ++c->epoch;   // host mirror only; the kernels keep the authoritative epoch in DevComm
     cudaError_t e;
     const uint64_t maxmove = (uint64_t)dp.host.max_move * unit;
-    const uint64_t ppm = std::max<uint64_t>(1, cdiv(maxmove, 16));
+    uint64_t ppm = 1;   // 16-B pieces per move, rounded up to a power of two (shift decode)
+    while (ppm * 16 < maxmove) ppm <<= 1;
     // pieces per step, fan-out stores counted per destination (max_step_units counts them)
     const uint64_t items = std::max<uint64_t>((uint64_t)dp.host.max_step_moves,
                                               (uint64_t)dp.host.max_step_units / std::max<int64_t>(1, dp.host.max_move)) * ppm;
@@ -438,6 +439,8 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
                        (one_step || items <= kSmallItemsOneCta);
     if (small) {
         E.nS = E.nF = 1;
+        E.small_a16 = unit % 16 == 0 && (uintptr_t)send % 16 == 0 && (uintptr_t)recv % 16 == 0 &&
+                      send_stride % 16 == 0 && recv_stride % 16 == 0 && E.work_stride % 16 == 0;
         E.small_ppm = (int32_t)ppm;
         size_t nmoves_g = 0;
         for (const auto &mv : dp.host.moves) nmoves_g = std::max(nmoves_g, mv.size());

@@ -45,18 +45,16 @@ __device__ __forceinline__ uint64_t globaltimer() {
     return t;
 }
 
-// Source loads: SEND buffers are never written inside a launch -> read-only path, no L1
-// allocation.  Every other buffer (RECV, WORK) may have been written earlier in the same
-// launch by another SM or a peer GPU -> cache-global (.cg, L2 only, never a stale L1 line).
+// Source loads are cache-global (.cg: L2 only, never an L1 line).  RECV / WORK may have been
+// written earlier in the same launch by another SM or a peer GPU; SEND is read-only inside
+// the launch, but under PDL the launch began before its producer finished, so no source is
+// read through the non-coherent path either.  (RO is kept as the call sites' statement of
+// which buffers are read-only.)
 template <bool RO>
 __device__ __forceinline__ uint4 ld16(const uint4 *p) {
     uint4 v;
-    if (RO)
-        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-    else
-        asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
     return v;
 }
 __device__ __forceinline__ void st16(uint4 *p, const uint4 &v) {
@@ -416,17 +414,40 @@ struct SmallJob {
 // overlap [sp, sp+len) are loaded independently (one round trip), then funnel-shifted.
 // Only words holding wanted bytes are touched, so nothing outside the 4-byte granules of
 // the piece is read.
-__device__ __forceinline__ uint4 load_piece(const char *sp, uint32_t len) {
-    const uintptr_t a = (uintptr_t)sp & ~(uintptr_t)3;
-    const uint32_t sh = 8u * (uint32_t)((uintptr_t)sp & 3);
-    const uint32_t *wp = (const uint32_t *)a;
-    const uintptr_t end = (uintptr_t)sp + len;
-    uint32_t w[5];
-#pragma unroll
-    for (int i = 0; i < 5; i++) w[i] = (a + 4 * i < end) ? __ldcg(wp + i) : 0u;
-    return make_uint4(__funnelshift_r(w[0], w[1], sh), __funnelshift_r(w[1], w[2], sh),
-                      __funnelshift_r(w[2], w[3], sh), __funnelshift_r(w[3], w[4], sh));
-}
+// A batch of up to kBatch 16-byte pieces: every load of the batch is issued before any
+// loaded register is touched (a use right after a load -- even a register move where two
+// code paths merge -- would expose one memory latency per piece).  A16: every piece is a
+// whole, 16-B aligned 16-byte vector on both sides (one LDG.128 / STG.128 each); otherwise
+// the aligned words overlapping each piece are loaded and funnel-shifted at store time.
+struct PieceRef {
+    const char *src;
+    uint32_t len;     // 0: no piece
+};
+template <bool A16>
+struct PieceRegs {
+    uint4 v[kBatch];
+    uint32_t w4[kBatch];
+    __device__ __forceinline__ void issue(int k, const char *sp, uint32_t len) {
+        if (A16) {
+            v[k] = ld16<false>((const uint4 *)sp);
+        } else {
+            const uintptr_t a = (uintptr_t)sp & ~(uintptr_t)3;
+            const uint32_t *wp = (const uint32_t *)a;
+            const uintptr_t end = (uintptr_t)sp + len;
+            v[k].x = __ldcg(wp);                        // a < end always (len >= 1)
+            v[k].y = (a + 4 < end) ? __ldcg(wp + 1) : 0u;
+            v[k].z = (a + 8 < end) ? __ldcg(wp + 2) : 0u;
+            v[k].w = (a + 12 < end) ? __ldcg(wp + 3) : 0u;
+            w4[k] = (a + 16 < end) ? __ldcg(wp + 4) : 0u;
+        }
+    }
+    __device__ __forceinline__ uint4 value(int k, const char *sp) const {
+        if (A16) return v[k];
+        const uint32_t sh = 8u * (uint32_t)((uintptr_t)sp & 3);
+        return make_uint4(__funnelshift_r(v[k].x, v[k].y, sh), __funnelshift_r(v[k].y, v[k].z, sh),
+                          __funnelshift_r(v[k].z, v[k].w, sh), __funnelshift_r(v[k].w, w4[k], sh));
+    }
+};
 
 __device__ __forceinline__ void store_piece(char *dp, uint4 v, uint32_t len) {
     if (len == 16 && (((uintptr_t)dp) & 15) == 0) { st16((uint4 *)dp, v); return; }
@@ -443,38 +464,44 @@ __device__ __forceinline__ void store_piece(char *dp, uint4 v, uint32_t len) {
 
 // Batched copy of up to kBatch SMALL moves by one warp (n <= 512 B each): lane l moves bytes
 // [16l, 16l+16) of every move; all loads of the batch are issued before any store.
-__device__ __noinline__ void small_batch(const ExecParams &P, const ExecShared &S, const SmallJob *jobs, int nj,
-                                            int lane) {
-    TRACE(6);
-    uint4 v[kBatch];
+template <bool A16>
+__device__ __forceinline__ void small_batch_t(const ExecParams &P, const ExecShared &S, const SmallJob *jobs, int nj,
+                                              int lane) {
+    PieceRegs<A16> R;
+    const uint32_t o = (uint32_t)lane * 16;
 #pragma unroll
-    for (int k = 0; k < kBatch; k++) {
-        v[k] = make_uint4(0, 0, 0, 0);
-        if (k >= nj) continue;
-        const SmallJob &j = jobs[k];
-        const uint32_t o = (uint32_t)lane * 16;
-        if (o >= j.n) continue;
-        const uint32_t len = min(16u, j.n - o);
-        const char *sp = j.src + o;
-        if (len == 16 && (((uintptr_t)sp) & 15) == 0)
-            v[k] = j.ro ? ld16<true>((const uint4 *)sp) : ld16<false>((const uint4 *)sp);
-        else
-            v[k] = load_piece(sp, len);
-    }
+    for (int k = 0; k < kBatch; k++)
+        if (k < nj && o < jobs[k].n) R.issue(k, jobs[k].src + o, min(16u, jobs[k].n - o));
     TRACE(7);
 #pragma unroll
     for (int k = 0; k < kBatch; k++) {
-        if (k >= nj) continue;
+        if (k >= nj || o >= jobs[k].n) continue;
         const SmallJob &j = jobs[k];
-        const uint32_t o = (uint32_t)lane * 16;
-        if (o >= j.n) continue;
         const uint32_t len = min(16u, j.n - o);
+        const uint4 val = R.value(k, j.src + o);
         if (!j.fanout) {
-            store_piece(j.dst + o, v[k], len);
+            store_piece(j.dst + o, val, len);
         } else {
-            for (int r = 0; r < P.p; r++) store_piece(base_of(P, S, j.dst_kind, r) + j.doff + o, v[k], len);
+            for (int r = 0; r < P.p; r++) store_piece(base_of(P, S, j.dst_kind, r) + j.doff + o, val, len);
         }
     }
+}
+
+__device__ __noinline__ void small_batch(const ExecParams &P, const ExecShared &S, const SmallJob *jobs, int nj,
+                                            int lane) {
+    TRACE(6);
+    // every piece whole and 16-B aligned on both sides (uniform across the warp)?
+    bool a16 = true;
+    for (int k = 0; k < nj; k++) {
+        const SmallJob &j = jobs[k];
+        uintptr_t bits = (uintptr_t)j.src | (uintptr_t)j.n;
+        if (!j.fanout) bits |= (uintptr_t)j.dst;
+        else
+            for (int r = 0; r < P.p; r++) bits |= (uintptr_t)(base_of(P, S, j.dst_kind, r) + j.doff);
+        a16 = a16 && (bits & 15) == 0;
+    }
+    if (a16) small_batch_t<true>(P, S, jobs, nj, lane);
+    else small_batch_t<false>(P, S, jobs, nj, lane);
     TRACE(8);
 }
 
@@ -845,7 +872,11 @@ __global__ void mpxa_scan_kernel(const int64_t *__restrict__ counts, int64_t *__
 // ------------------------------------------------------------------------------------
 constexpr int kSmallThreads = 512;
 
+constexpr int kRankTable = 256;   // small kernel: per-rank buffer bases kept in shared memory
+
 struct SmallShared {
+    StepInfo steps[kMaxStepsSmem];   // step table, loaded in the prologue (before griddep wait)
+    char *rb[3][kRankTable];         // [kind][rank] buffer base (p <= kRankTable): no divisions
     char *recv_base[kMaxGpus];
     char *work_base[kMaxGpus];
     SymRegion *sym[kMaxGpus];
@@ -861,6 +892,22 @@ __device__ __forceinline__ char *sbase(const ExecParams &P, const SmallShared &S
         return (char *)P.send + (P.mode == 2 ? 0 : (uint64_t)g * P.R * P.send_stride) + local * P.send_stride;
     if (kind == BK_RECV) return S.recv_base[g] + local * P.recv_stride;
     return S.work_base[g] + local * P.work_stride;
+}
+
+__device__ __forceinline__ char *sb(const ExecParams &P, const SmallShared &S, int kind, int rank) {
+    return P.p <= kRankTable ? S.rb[kind][rank] : sbase(P, S, kind, rank);
+}
+// (re)fill the rank-base rows of the ranks on GPUs in gmask (threads t < p)
+__device__ __forceinline__ void fill_rank_bases(const ExecParams &P, SmallShared &S, uint32_t gmask, bool all_kinds) {
+    const int t = threadIdx.x;
+    if (P.p > kRankTable || t >= P.p) return;
+    const int gg = t / P.R;
+    if (!((gmask >> gg) & 1u)) return;
+    if (all_kinds) {
+        S.rb[BK_SEND][t] = sbase(P, S, BK_SEND, t);
+        S.rb[BK_WORK][t] = sbase(P, S, BK_WORK, t);
+    }
+    S.rb[BK_RECV][t] = S.recv_base[gg] ? sbase(P, S, BK_RECV, t) : nullptr;
 }
 
 // threads < 32, one per set bit of mask: spin until slot >= want (watchdog as in the main kernel)
@@ -886,17 +933,63 @@ __device__ __forceinline__ void small_wait(const ExecParams &P, SmallShared &S, 
     }
 }
 
+// items = (move, 16-byte piece); thread takes items base0, base0 + TT, ... kBatch at a time
+template <bool A16>
+__device__ __forceinline__ void small_items(const ExecParams &P, const SmallShared &S, const Move *mv, uint32_t items,
+                                            uint32_t lg, uint32_t TT, uint32_t base0) {
+    const uint32_t mask = (1u << lg) - 1u;   // pieces per move: a power of two (host-rounded)
+    for (uint32_t base = base0; base < items; base += TT * kBatch) {
+        PieceRegs<A16> R;
+        const char *sp[kBatch];
+#pragma unroll
+        for (int k = 0; k < kBatch; k++) {
+            sp[k] = nullptr;
+            const uint32_t it = base + (uint32_t)k * TT;
+            if (it >= items) continue;
+            const Move &m = mv[it >> lg];
+            const uint32_t n = (uint32_t)((uint64_t)m.len * P.unit), o = (it & mask) * 16;
+            if (o >= n) continue;
+            sp[k] = sb(P, S, m.src_kind, m.src_rank) + (uint64_t)m.src_off * P.unit + o;
+            R.issue(k, sp[k], min(16u, n - o));
+        }
+        TRACE(1);
+#pragma unroll
+        for (int k = 0; k < kBatch; k++) {
+            if (!sp[k]) continue;
+            const uint32_t it = base + (uint32_t)k * TT;
+            const Move &m = mv[it >> lg];
+            const uint32_t n = (uint32_t)((uint64_t)m.len * P.unit), o = (it & mask) * 16;
+            const uint32_t len = min(16u, n - o);
+            const uint64_t doff = (uint64_t)m.dst_off * P.unit + o;
+            const uint4 val = R.value(k, sp[k]);
+            if (!m.fanout) {
+                store_piece(sb(P, S, m.dst_kind, m.dst_rank) + doff, val, len);
+            } else {
+                for (int r = 0; r < P.p; r++) store_piece(sb(P, S, m.dst_kind, r) + doff, val, len);
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __grid_constant__ ExecParams P) {
     __shared__ SmallShared S;
-    extern __shared__ __align__(16) char small_dyn[];   // the program's moves, when they fit
+    extern __shared__ __align__(16) char small_dyn[];
+    CTA_STAMP(0);   // the program's moves, when they fit
     const int g = P.mode == 1 ? (int)blockIdx.y : P.my_gpu;
     const int t = threadIdx.x;
     const GpuProg prog = P.mode == 1 ? P.progs[g] : P.prog;
     const bool multi = P.G > 1;
     const bool cached = P.small_cache != 0;
     Move *smoves = reinterpret_cast<Move *>(small_dyn);
-    if (cached)   // every move of the program, once: no descriptor round trip in any step
+    // prologue (overlaps the previous kernel under PDL): step table and every move, once --
+    // no descriptor round trip after the dependency wait
+    const bool steps_smem = prog.nsteps <= kMaxStepsSmem;
+    const bool ld_step = steps_smem && t < prog.nsteps;
+    Step st_r;
+    if (ld_step) st_r = prog.steps[t];
+    if (cached)
         for (int i = t; i < prog.nmoves; i += kSmallThreads) smoves[i] = prog.moves[i];
+    if (ld_step) S.steps[t] = StepInfo{st_r.move_begin, st_r.move_end - st_r.move_begin, st_r.signal_mask, st_r.wait_mask};
     if (t < P.G) {
         S.work_base[t] = P.dc->work_base[t];
         S.sym[t] = P.dc->sym[t];
@@ -912,7 +1005,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
         S.abort_flag = 0;
         S.epoch = multi ? *(volatile uint64_t *)&P.dc->epoch + 1 : 0;
     }
+    // rank bases known now: every rank's SEND / WORK row and the RECV rows of resolved GPUs
+    fill_rank_bases(P, S, 0xffffffffu, true);
     __syncthreads();
+    TRACE(0);
     const uint64_t epoch = S.epoch;
     if (multi && t < P.G && t != g) {
         CtsSlot *slot = &S.sym[t]->cts[g];
@@ -922,10 +1018,17 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
         st_release_sys(&slot->epoch, epoch);
     }
     const Move *mvs = cached ? smoves : prog.moves;
-    const uint32_t ppm = (uint32_t)P.small_ppm;        // 16-byte pieces per move (uniform bound)
+    const uint32_t ppm = (uint32_t)P.small_ppm;        // 16-byte pieces per move: power-of-two bound
+    const uint32_t lg = 31u - (uint32_t)__clz((int)ppm);
     uint32_t prev_wait = 0;
     for (int s = 0; s < prog.nsteps; s++) {
-        const Step st = prog.steps[s];
+        StepInfo st;
+        if (steps_smem) {
+            st = S.steps[s];
+        } else {
+            const Step g_st = prog.steps[s];
+            st = StepInfo{g_st.move_begin, g_st.move_end - g_st.move_begin, g_st.signal_mask, g_st.wait_mask};
+        }
         if (multi) {
             if (prev_wait) small_wait(P, S, prev_wait, &S.sym[g]->flags[0][blockIdx.x], kMaxCtas, (epoch << 8) | (uint64_t)s);
             const uint32_t need = st.signal_mask & ~S.cts_ok;
@@ -935,6 +1038,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
                     const CtsSlot *cs = &S.sym[g]->cts[t];
                     S.recv_base[t] = P.dc->win_table[t * kMaxWindows + cs->win] + cs->off;
                 }
+                __syncthreads();
+                fill_rank_bases(P, S, need, false);
             }
             __syncthreads();
             if (t == 0) S.cts_ok |= need;
@@ -942,37 +1047,19 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
         }
         // items = (move, 16-byte piece); thread t takes items t, t+T, ... four at a time:
         // all four loads in flight before the stores
-        const uint32_t items = (uint32_t)(st.move_end - st.move_begin) * ppm;
+        const uint32_t items = (uint32_t)st.nm * ppm;
         const uint32_t TT = gridDim.x * kSmallThreads;   // several CTAs only for 1-step programs
-        for (uint32_t base = blockIdx.x * kSmallThreads + t; base < items; base += TT * kBatch) {
-            uint4 v[kBatch];
-#pragma unroll
-            for (int k = 0; k < kBatch; k++) {
-                v[k] = make_uint4(0, 0, 0, 0);
-                const uint32_t it = base + (uint32_t)k * TT;
-                if (it >= items) continue;
-                const Move &m = mvs[st.move_begin + it / ppm];
-                const uint32_t n = (uint32_t)((uint64_t)m.len * P.unit), o = (it % ppm) * 16;
-                if (o >= n) continue;
-                v[k] = load_piece(sbase(P, S, m.src_kind, m.src_rank) + (uint64_t)m.src_off * P.unit + o, min(16u, n - o));
-            }
-#pragma unroll
-            for (int k = 0; k < kBatch; k++) {
-                const uint32_t it = base + (uint32_t)k * TT;
-                if (it >= items) continue;
-                const Move &m = mvs[st.move_begin + it / ppm];
-                const uint32_t n = (uint32_t)((uint64_t)m.len * P.unit), o = (it % ppm) * 16;
-                if (o >= n) continue;
-                const uint32_t len = min(16u, n - o);
-                const uint64_t doff = (uint64_t)m.dst_off * P.unit + o;
-                if (!m.fanout) {
-                    store_piece(sbase(P, S, m.dst_kind, m.dst_rank) + doff, v[k], len);
-                } else {
-                    for (int r = 0; r < P.p; r++) store_piece(sbase(P, S, m.dst_kind, r) + doff, v[k], len);
-                }
-            }
-        }
+        // 16-B fast path: the host vouched for every local offset / length / base, and the
+        // recv bases of the peers written in this step arrived with their CTS
+        bool a16 = P.small_a16 != 0;
+        for (int q = 0; q < P.G; q++)
+            if (((st.signal_mask >> q) & 1u) && ((uintptr_t)S.recv_base[q] & 15)) a16 = false;
+        const uint32_t base0 = blockIdx.x * kSmallThreads + t;
+        if (a16) small_items<true>(P, S, mvs + st.first, items, lg, TT, base0);
+        else small_items<false>(P, S, mvs + st.first, items, lg, TT, base0);
+        TRACE(2);
         __syncthreads();
+        TRACE(3);
         if (multi && st.signal_mask && t < 32 && ((st.signal_mask >> t) & 1u)) {
             __threadfence_system();
             st_release_sys(&S.sym[t]->flags[g][blockIdx.x], (epoch << 8) | (uint64_t)(s + 1));
@@ -991,6 +1078,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
             __threadfence();
         }
     }
+    CTA_STAMP(1);
 }
 
 // Launch with the PDL attribute (pdl) or cooperatively (emulated GPUs: co-residency of the

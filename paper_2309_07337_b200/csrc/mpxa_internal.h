@@ -142,6 +142,7 @@ struct ExecParams {
     int32_t dyn_units;
     int32_t dyn_k;
     int32_t dyn_u;
+    int32_t small_a16;         // every local offset, length, base and stride is a 16-B multiple
     uint64_t dyn_len;
 };
 
