@@ -70,24 +70,21 @@ struct DevProg {
     Program host;
     int nsteps = 0;
     std::vector<GpuProg> gp;   // the [G] GpuProg table as uploaded (device pointers)
-    int64_t eq_len = -1;       // single-step program whose moves all have this length (units)
-    int64_t max_gpu_moves = 0; // most moves any GPU runs
+    int64_t max_gpu_moves = 0;      // most moves any GPU runs
+    int64_t max_gpu_bytes_units = 0;  // single-step programs: most units any GPU moves (source side)
 };
 
-// dynamic-mode eligibility facts of a program (DevProg::eq_len, max_gpu_moves)
+// dynamic-mode eligibility facts of a program (DevProg::max_gpu_moves, max_gpu_bytes_units)
 void prog_facts(DevProg &dp) {
     const Program &P = dp.host;
-    dp.eq_len = -1;
     dp.max_gpu_moves = 0;
-    for (const auto &mv : P.moves) dp.max_gpu_moves = std::max<int64_t>(dp.max_gpu_moves, (int64_t)mv.size());
-    if (P.nsteps() != 1) return;
-    int64_t L = -1;
-    for (const auto &mv : P.moves)
-        for (const Move &m : mv) {
-            if (L < 0) L = m.len;
-            else if (m.len != L) return;
-        }
-    dp.eq_len = L;
+    dp.max_gpu_bytes_units = 0;
+    for (const auto &mv : P.moves) {
+        dp.max_gpu_moves = std::max<int64_t>(dp.max_gpu_moves, (int64_t)mv.size());
+        int64_t u = 0;
+        for (const Move &m : mv) u += m.len;
+        dp.max_gpu_bytes_units = std::max(dp.max_gpu_bytes_units, u);
+    }
 }
 
 size_t serialize(const Program &P, std::vector<char> &buf, uintptr_t dbase) {
@@ -449,33 +446,22 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
         e = launch_small(E, std::max(1, nC), c->emulated ? c->G : 1, c->emulated, pdl && c->pdl, stream);
     } else {
         int nC = gr.n();
-        // dynamic mode: large equal-length moves of one step, 16-B congruent addresses
-        // (every move's src and dst differ by a multiple of 16 when all bases, strides and
-        // the unit are); the whole move list fits the prologue's shared-memory tile
-        const uint64_t L = dp.eq_len > 0 ? (uint64_t)dp.eq_len * unit : 0;
-        const uint64_t total = L * (uint64_t)dp.max_gpu_moves;
-        const bool congruent = unit % 16 == 0 && send_stride % 16 == 0 && recv_stride % 16 == 0 &&
-                               ((uintptr_t)send - (uintptr_t)recv) % 16 == 0;
-        if (c->dyn && E.d0_base >= 0 && L >= kDynMinMove && total >= kDynMinTotal && congruent &&
-            dp.max_gpu_moves <= kMoveTile) {
-            // same grid as the static decomposition: it depends on the program only, so
-            // processes that decide differently (local buffer alignment) still pair CTA
-            // flag slots one to one
-            uint64_t U = total / ((uint64_t)nC * (uint64_t)c->dyn_pieces);
-            U = std::max<uint64_t>((uint64_t)E.chunk, std::min<uint64_t>(U, kDynMaxPiece));
-            U = U / (uint64_t)E.chunk * (uint64_t)E.chunk;
-            const uint64_t k = cdiv(L, U);
-            E.nS = nC;
-            E.nF = 1;
-            E.dyn_len = L;
-            E.dyn_u = (int32_t)U;
-            E.dyn_k = (int32_t)k;
-            E.dyn_units = (int32_t)(k * (uint64_t)dp.max_gpu_moves);
-            // every GPU must run the same number of pieces (moves per GPU are equal in the
-            // uniform single-step programs; otherwise stay static)
-            for (const auto &mv : dp.host.moves)
-                if ((int64_t)mv.size() != dp.max_gpu_moves) { E.dyn_units = 0; break; }
-            if (!E.dyn_units) { E.nS = gr.nS; E.nF = gr.nF; nC = gr.n(); }
+        // dynamic mode: one step whose moves all fit the CTA's shared-memory move tile and
+        // whose busiest GPU moves enough bytes for the tail of static slices to matter
+        if (c->dyn && dp.nsteps == 1 && dp.max_gpu_moves <= kMoveTile && dp.max_gpu_bytes_units > 0) {
+            const uint64_t total = (uint64_t)dp.max_gpu_bytes_units * unit;
+            const uint64_t L = (uint64_t)dp.host.max_move * unit;
+            if (total >= kDynMinTotal && L >= kDynMinMove) {
+                // same grid as the static decomposition: it depends on the program only, so
+                // processes still pair CTA flag slots one to one
+                uint64_t U = total / ((uint64_t)nC * (uint64_t)c->dyn_pieces);
+                U = std::max<uint64_t>((uint64_t)E.chunk, std::min<uint64_t>(U, kDynMaxPiece));
+                U = U / (uint64_t)E.chunk * (uint64_t)E.chunk;
+                E.nS = nC;
+                E.nF = 1;
+                E.dyn_units = 1;
+                E.dyn_u = (int32_t)U;
+            }
         }
         e = launch_exec(E, nC, c->emulated ? c->G : 1, c->emulated, pdl && c->pdl, stream);
     }

@@ -74,53 +74,66 @@ __device__ __forceinline__ uint8_t ldcg<uint8_t>(const uint8_t *p) {
 // must stay small enough for the instruction cache (a template-expanded version was 87 K
 // SASS instructions and spent small launches stalled on instruction fetch).
 //
-// Copy n bytes with nt cooperating threads (index t): the widest access class W shared by
-// (src, dst) for the body, bytes for head / tail.  ro: the source is never written in the
-// launch (SEND), so the 16-B path may use the read-only, no-L1-allocate load.
-template <typename V>
-__device__ __forceinline__ void body_loop(char *dst, const char *src, uint64_t nv, int t, int nt) {
-    const V *s = (const V *)src;
-    V *d = (V *)dst;
-    uint64_t i = t;
-    for (; i + 3 * (uint64_t)nt < nv; i += 4 * (uint64_t)nt) {
-        V a = ldcg(s + i), b = ldcg(s + i + nt), c = ldcg(s + i + 2 * nt), e = ldcg(s + i + 3 * nt);
-        d[i] = a; d[i + nt] = b; d[i + 2 * nt] = c; d[i + 3 * nt] = e;
+// Copy n bytes with nt cooperating threads (index t).  The SOURCE side is always read in
+// 16-byte aligned vectors, kLsuUnroll of them in flight per thread (loads are what bound an
+// LSU copy's bandwidth: stores are fire-and-forget); each vector is stored in pieces of the
+// widest access class W the destination allows at that offset ((dst - src) mod 16).  Bytes
+// before the first aligned source vector and after the last are copied singly.
+#ifndef MPXA_LSU_UNROLL
+#define MPXA_LSU_UNROLL 8
+#endif
+constexpr int kLsuUnroll = MPXA_LSU_UNROLL;
+
+__device__ __forceinline__ void store_w(char *d, const uint4 &v, unsigned W) {
+    switch (W) {
+        case 16: st16((uint4 *)d, v); break;
+        case 8:
+            ((uint2 *)d)[0] = make_uint2(v.x, v.y);
+            ((uint2 *)d)[1] = make_uint2(v.z, v.w);
+            break;
+        case 4: {
+            uint32_t *q = (uint32_t *)d;
+            q[0] = v.x; q[1] = v.y; q[2] = v.z; q[3] = v.w;
+            break;
+        }
+        default: {
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+            if (W == 2) {
+#pragma unroll
+                for (int i = 0; i < 8; i++) ((uint16_t *)d)[i] = (uint16_t)(w[i >> 1] >> (16 * (i & 1)));
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; i++) d[i] = (char)(w[i >> 2] >> (8 * (i & 3)));
+            }
+        }
     }
-    for (; i < nv; i += nt) d[i] = ldcg(s + i);
 }
 
 __device__ __noinline__ void lsu_copy_range(char *dst, const char *src, uint64_t n, int t, int nt, bool ro) {
+    (void)ro;
     if (n == 0) return;
-    const unsigned m = (unsigned)(((uintptr_t)dst ^ (uintptr_t)src) & 15);
-    const unsigned W = m == 0 ? 16 : (m & 7) == 0 ? 8 : (m & 3) == 0 ? 4 : (m & 1) == 0 ? 2 : 1;
-    uint64_t head = (W - ((uintptr_t)dst & (W - 1))) & (W - 1);
+    uint64_t head = (16 - ((uintptr_t)src & 15)) & 15;
     if (head > n) head = n;
     for (uint64_t i = t; i < head; i += nt) dst[i] = (char)ldcg((const uint8_t *)src + i);
-    const uint64_t nv = (n - head) / W;
+    const uint64_t nv = (n - head) >> 4;
+    const uint4 *s4 = (const uint4 *)(src + head);
     char *d = dst + head;
-    const char *s = src + head;
-    switch (W) {
-        case 16:
-            if (ro) {
-                const uint4 *s4 = (const uint4 *)s;
-                uint4 *d4 = (uint4 *)d;
-                uint64_t i = t;
-                for (; i + 3 * (uint64_t)nt < nv; i += 4 * (uint64_t)nt) {
-                    uint4 a = ld16<true>(s4 + i), b = ld16<true>(s4 + i + nt), c = ld16<true>(s4 + i + 2 * nt),
-                          e = ld16<true>(s4 + i + 3 * nt);
-                    st16(d4 + i, a); st16(d4 + i + nt, b); st16(d4 + i + 2 * nt, c); st16(d4 + i + 3 * nt, e);
-                }
-                for (; i < nv; i += nt) st16(d4 + i, ld16<true>(s4 + i));
-            } else {
-                body_loop<uint4>(d, s, nv, t, nt);
-            }
-            break;
-        case 8: body_loop<unsigned long long>(d, s, nv, t, nt); break;
-        case 4: body_loop<unsigned int>(d, s, nv, t, nt); break;
-        case 2: body_loop<unsigned short>(d, s, nv, t, nt); break;
-        default: body_loop<uint8_t>(d, s, nv, t, nt); break;
+    const unsigned m = (unsigned)((uintptr_t)d & 15);
+    const unsigned W = m == 0 ? 16u : (m & -m);
+    for (uint64_t i0 = t; i0 < nv; i0 += (uint64_t)kLsuUnroll * nt) {
+        uint4 v[kLsuUnroll];
+#pragma unroll
+        for (int k = 0; k < kLsuUnroll; k++) {
+            const uint64_t i = i0 + (uint64_t)k * nt;
+            if (i < nv) v[k] = ld16<false>(s4 + i);
+        }
+#pragma unroll
+        for (int k = 0; k < kLsuUnroll; k++) {
+            const uint64_t i = i0 + (uint64_t)k * nt;
+            if (i < nv) store_w(d + 16 * i, v[k], W);
+        }
     }
-    for (uint64_t k = head + nv * W + t; k < n; k += nt) dst[k] = (char)ldcg((const uint8_t *)src + k);
+    for (uint64_t k = head + nv * 16 + t; k < n; k += nt) dst[k] = (char)ldcg((const uint8_t *)src + k);
 }
 
 // Fan-out: one read, nd stores, when every destination shares the source's 16-B alignment.
@@ -242,6 +255,11 @@ struct ExecShared {
     uint64_t epoch;      // this launch's epoch (device-side sequence number)
     uint32_t cts_ok;     // remote GPUs whose CTS for this epoch was observed
     int abort_flag;
+    uint32_t pcA[kMoveTile + 1];  // dynamic mode: exclusive prefix of TMA pieces per move
+    uint32_t pcB[kMoveTile + 1];  //               and of LSU pieces per move
+    const char *msrc[kMoveTile];  //               resolved source of each move
+    uint64_t mdst[kMoveTile];     //               destination address (fan-out: offset)
+    uint64_t wsum[kThreads / 32];
 };
 
 __device__ __forceinline__ char *base_of(const ExecParams &P, const ExecShared &S, int kind, int rank) {
@@ -505,51 +523,136 @@ __device__ __noinline__ void small_batch(const ExecParams &P, const ExecShared &
     TRACE(8);
 }
 
-// Dynamic mode (ExecParams::dyn_units): the producer thread takes pieces u (dyn_u bytes of
-// move u / dyn_k, whose descriptors the prologue put in S.moves) from the GPU's work queue
-// until it runs dry; the next piece is requested before the current one is streamed, so the
-// atomic's round trip is hidden.  Bytes outside the 16-B aligned body of a piece (only when
-// the move's start or length is not 16-B aligned) are copied by this thread directly.
-__device__ __noinline__ void dyn_produce(const ExecParams &P, ExecShared &S, Producer &prod, int g) {
-    uint32_t *q = &P.dc->dyn_next[g];
-    const uint32_t n = (uint32_t)P.dyn_units, k = (uint32_t)P.dyn_k;
-    const uint64_t U = (uint64_t)P.dyn_u, chunk = (uint64_t)P.chunk;
-    uint32_t u = atomicAdd(q, 1u);
-    while (u < n) {
-        const uint32_t un = atomicAdd(q, 1u);
-        const uint32_t mi = u / k;
-        const Move &m = S.moves[mi];
-        const uint64_t lo = (uint64_t)(u - mi * k) * U;
-        const uint64_t hi = min(P.dyn_len, lo + U);
-        const char *src = base_of(P, S, m.src_kind, m.src_rank) + (uint64_t)m.src_off * P.unit + lo;
-        const uint64_t doff = (uint64_t)m.dst_off * P.unit + lo;
-        char *dst = m.fanout ? nullptr : base_of(P, S, m.dst_kind, m.dst_rank) + doff;
-        const uint64_t nb = hi - lo;
-        uint64_t head = (16 - ((uintptr_t)src & 15)) & 15;
-        if (head > nb) head = nb;
-        const uint64_t body = (nb - head) & ~(uint64_t)15;
-        for (uint64_t i = 0; i < nb; i++) {          // head and tail bytes (plain stores)
-            if (i == head) i = head + body;
-            if (i >= nb) break;
-            const char b = (char)ldcg((const uint8_t *)src + i);
-            if (!m.fanout) dst[i] = b;
-            else
-                for (int j = 0; j < P.p; j++) base_of(P, S, m.dst_kind, j)[doff + i] = b;
-        }
-        for (uint64_t o = 0; o < body; o += chunk) {
-            RingEntry e;
-            e.len = (uint32_t)min(chunk, body - o);
-            e.fanout = m.fanout;
-            e.dst_kind = m.dst_kind;
-            e.doff = doff + head + o;
-            e.dst = m.fanout ? nullptr : dst + head + o;
-            prod.push(P, S, src + head + o, e);
-        }
-        u = un;
+// Dynamic mode (ExecParams::dyn_units != 0; single-step programs): the step's moves (all in
+// S.moves) are cut into pieces of at most dyn_u bytes, taken from device work queues until
+// they run dry (per-SM bandwidth differs across the chip, so static slices leave a tail of
+// slow CTAs).  Moves whose source and destination(s) are 16-B congruent feed queue A: the
+// producer thread streams those pieces through the TMA ring (bytes outside the aligned
+// body copied by that thread).  All other moves feed queue B: each LSU warp takes pieces on
+// its own and copies them with 16-B source vectors and destination-width stores.  The
+// queues are independent, so neither role waits for the other.  Returns whether this
+// thread issued generic stores.
+__device__ __forceinline__ int find_move(const uint32_t *pc, int nm, uint32_t u) {
+    int lo = 0, hi = nm - 1;      // last move with pc[m] <= u (moves with no piece are skipped)
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (pc[mid] <= u) lo = mid;
+        else hi = mid - 1;
     }
+    return lo;
 }
 
-__global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_constant__ ExecParams Pk) {
+__device__ __forceinline__ MovePlan piece_plan(const ExecParams &P, const ExecShared &S, int mi, uint64_t lo,
+                                               uint64_t U) {
+    const Move &m = S.moves[mi];
+    MovePlan mp;
+    const uint64_t L = (uint64_t)m.len * P.unit;
+    mp.src = S.msrc[mi] + lo;
+    mp.doff = (m.fanout ? S.mdst[mi] : 0) + lo;
+    mp.dst = m.fanout ? nullptr : (char *)(uintptr_t)S.mdst[mi] + lo;
+    mp.n = min(L, lo + U) - lo;
+    return mp;
+}
+
+__device__ __noinline__ bool dyn_step(const ExecParams &P, ExecShared &S, Producer &prod, int g, int first, int nm,
+                                      bool loaded) {
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint64_t U = (uint64_t)P.dyn_u, chunk = (uint64_t)P.chunk;
+    if (!loaded) {   // moves not prefetched by the prologue (step 0 not dense)
+        __syncthreads();
+        if (t < nm) S.moves[t] = P.mode == 1 ? P.progs[g].moves[first + t] : P.prog.moves[first + t];
+        __syncthreads();
+    }
+    // classify each move (one per thread: nm <= kMoveTile = kThreads) and count its pieces;
+    // one 64-bit block scan gives both prefixes (A in the low, B in the high half)
+    uint64_t kt = 0;
+    if (t < nm) {
+        const Move &m = S.moves[t];
+        const uint64_t L = (uint64_t)m.len * P.unit;
+        const char *src = base_of(P, S, m.src_kind, m.src_rank) + (uint64_t)m.src_off * P.unit;
+        const uint64_t doff = (uint64_t)m.dst_off * P.unit;
+        char *dst = m.fanout ? nullptr : base_of(P, S, m.dst_kind, m.dst_rank) + doff;
+        S.msrc[t] = src;
+        S.mdst[t] = m.fanout ? doff : (uint64_t)(uintptr_t)dst;
+        const unsigned mis = !m.fanout ? (unsigned)(((uintptr_t)dst ^ (uintptr_t)src) & 15)
+                                       : fan_misalign(P, S, m.dst_kind, doff, src);
+        const uint64_t k = (L + U - 1) / U;
+        kt = (mis == 0 && L >= kTmaMin) ? k : (k << 32);
+    }
+    uint64_t inc = kt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) S.wsum[warp] = inc;
+    __syncthreads();
+    uint64_t wo = 0;
+    for (int w = 0; w < warp; w++) wo += S.wsum[w];
+    const uint64_t ex = wo + inc - kt;
+    S.pcA[t] = (uint32_t)ex;
+    S.pcB[t] = (uint32_t)(ex >> 32);
+    if (t == kThreads - 1) {
+        S.pcA[kThreads] = (uint32_t)(wo + inc);
+        S.pcB[kThreads] = (uint32_t)((wo + inc) >> 32);
+    }
+    __syncthreads();
+    const uint32_t totA = S.pcA[nm], totB = S.pcB[nm];
+    bool wrote = false;
+    if (t == 0) {
+        if (totA == 0) return false;
+        uint32_t *q = &P.dc->dyn_next[g];
+        uint32_t u = atomicAdd(q, 1u);
+        while (u < totA) {
+            const uint32_t un = atomicAdd(q, 1u);   // next piece requested while this one streams
+            const int mi = find_move(S.pcA, nm, u);
+            const Move &m = S.moves[mi];
+            const MovePlan mp = piece_plan(P, S, mi, (uint64_t)(u - S.pcA[mi]) * U, U);
+            const uint64_t nb = mp.n;
+            uint64_t head = (16 - ((uintptr_t)mp.src & 15)) & 15;
+            if (head > nb) head = nb;
+            const uint64_t body = (nb - head) & ~(uint64_t)15;
+            for (uint64_t i = 0; i < nb; i++) {            // head and tail bytes
+                if (i == head) i = head + body;
+                if (i >= nb) break;
+                const char bt = (char)ldcg((const uint8_t *)mp.src + i);
+                if (!m.fanout) mp.dst[i] = bt;
+                else
+                    for (int j = 0; j < P.p; j++) base_of(P, S, m.dst_kind, j)[mp.doff + i] = bt;
+                wrote = true;
+            }
+            for (uint64_t o = 0; o < body; o += chunk) {
+                RingEntry e;
+                e.len = (uint32_t)min(chunk, body - o);
+                e.fanout = m.fanout;
+                e.dst_kind = m.dst_kind;
+                e.doff = mp.doff + head + o;
+                e.dst = m.fanout ? nullptr : mp.dst + head + o;
+                prod.push(P, S, mp.src + head + o, e);
+            }
+            u = un;
+        }
+    } else if (warp >= 1 && totB) {
+        uint32_t *q = &P.dc->dyn_next2[g];
+        for (;;) {
+            uint32_t u = 0;
+            if (lane == 0) u = atomicAdd(q, 1u);
+            u = __shfl_sync(0xffffffffu, u, 0);
+            if (u >= totB) break;
+            const int mi = find_move(S.pcB, nm, u);
+            const Move &m = S.moves[mi];
+            const MovePlan mp = piece_plan(P, S, mi, (uint64_t)(u - S.pcB[mi]) * U, U);
+            lsu_copy(P, S, m, mp, 0, mp.n, lane, 32);
+            wrote = true;
+        }
+    }
+    return wrote;
+}
+
+#ifndef MPXA_EXEC_MINB
+#define MPXA_EXEC_MINB 2
+#endif
+__global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(const __grid_constant__ ExecParams Pk) {
     extern __shared__ __align__(128) char dyn_smem[];
     __shared__ ExecShared S;
     // the helpers take the parameters by reference; a shared-memory copy keeps those
@@ -694,7 +797,7 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
 #endif
         const int nm = P.dyn_units ? 0 : st.nm;   // dynamic mode: the work queue below
         const int rot = nm ? (int)(((int64_t)sl + (int64_t)g * nm / P.G) % nm) : 0;
-        if (P.dyn_units && t == 0) dyn_produce(P, S, prod, g);
+        if (P.dyn_units) wrote = dyn_step(P, S, prod, g, st.first, st.nm, pre);
         for (int tile = 0; tile < nm; tile += kMoveTile) {
             const int cnt = min(kMoveTile, nm - tile);
             if (!(pre && s == 0 && tile == 0)) {   // (prefetched in the prologue)
@@ -799,7 +902,10 @@ __global__ void __launch_bounds__(kThreads, 2) mpxa_exec_kernel(const __grid_con
             P.dc->done_ctas = 0;
             if (multi) P.dc->epoch = epoch;
             if (P.dyn_units)
-                for (int r = 0; r < (int)gridDim.y; r++) P.dc->dyn_next[P.my_gpu >= 0 ? P.my_gpu : r] = 0;
+                for (int r = 0; r < (int)gridDim.y; r++) {
+                    P.dc->dyn_next[P.my_gpu >= 0 ? P.my_gpu : r] = 0;
+                    P.dc->dyn_next2[P.my_gpu >= 0 ? P.my_gpu : r] = 0;
+                }
             __threadfence();
         }
     }

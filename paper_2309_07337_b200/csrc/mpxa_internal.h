@@ -16,7 +16,11 @@ namespace mpxa {
 
 constexpr int kMaxGpus = 32;       // processes or virtual GPUs per comm (signal masks are 32-bit)
 constexpr int kMaxCtas = 1024;     // CTAs per GPU per launch (flag slots per source GPU)
-constexpr int kThreads = 256;      // threads per CTA of the executor kernel (warp 0: TMA producer)
+#ifndef MPXA_THREADS
+#define MPXA_THREADS 128
+#endif
+constexpr int kThreads = MPXA_THREADS;   // threads per CTA of the executor kernel (warp 0: TMA producer;
+                                         // 128: no register spills at 2 CTAs / SM, measured fastest)
 // TMA ring configurations (runtime-selected per launch):
 //   mid : 6 x 16 KiB stages, 2 CTAs / SM  (many CTAs: mid-size messages, latency)
 //   big : 6 x 32 KiB stages, 1 CTA / SM   (more bytes in flight per SM: large messages)
@@ -27,7 +31,7 @@ struct TmaConfig {
 constexpr TmaConfig kTmaMid = {6, 16384, 4};
 constexpr TmaConfig kTmaBig = {6, 32768, 4};
 constexpr int kMaxDynSmem = 6 * 32768;
-constexpr int kMoveTile = 256;     // moves staged in shared memory at a time
+constexpr int kMoveTile = kThreads;   // moves staged in shared memory at a time (one per thread)
 constexpr uint64_t kSmallKernelMax = 8192;  // longest move (bytes) the small-message kernel takes
 constexpr int kSmallMovesSmem = 2048;       // program moves cached in shared memory by the small kernel
 constexpr int kMaxWindows = 16;    // registered recv windows per process
@@ -100,8 +104,8 @@ struct DevComm {
     uint64_t epoch;                         // epochs completed on this GPU (or emulated set)
     uint32_t done_ctas;                     // CTAs of the current launch that finished
     uint32_t pad;
-    uint32_t dyn_next[kMaxGpus];            // work-queue heads of dynamic launches (per GPU row),
-                                            // reset to 0 by the launch's last CTA
+    uint32_t dyn_next[kMaxGpus];            // work-queue heads of dynamic launches (per GPU row):
+    uint32_t dyn_next2[kMaxGpus];           // TMA pieces / LSU pieces; reset by the last CTA
     uint64_t trace[32];                     // MPXA_TRACE builds: %globaltimer phase stamps
 };
 
@@ -135,15 +139,13 @@ struct ExecParams {
     int32_t small_cache;       // small kernel: moves cached in shared memory (0 = read global)
     int32_t d0_base;           // step 0 dense (Step::dense_base >= 0): its base flow, and
     int32_t d0_n;              // its move count -> step 0's moves are fetched in the prologue
-    // dynamic mode (dyn_units > 0): single-step program whose moves all have dyn_len bytes and
-    // 16-B congruent source / destination; the moves are cut into dyn_u-byte pieces (dyn_k
-    // per move) that CTAs take from a device work queue (DevComm::dyn_next) -- per-SM
-    // bandwidth differs across the chip, so static slices leave a long tail of slow CTAs
+    // dynamic mode (dyn_units != 0): single-step program whose moves are cut into pieces of
+    // at most dyn_u bytes that CTAs take from a device work queue (DevComm::dyn_next) --
+    // per-SM bandwidth differs across the chip, so static slices leave a tail of slow CTAs
     int32_t dyn_units;
-    int32_t dyn_k;
     int32_t dyn_u;
     int32_t small_a16;         // every local offset, length, base and stride is a 16-B multiple
-    uint64_t dyn_len;
+    int32_t pad4;
 };
 
 }  // namespace mpxa
