@@ -452,8 +452,14 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
             const uint64_t total = (uint64_t)dp.max_gpu_bytes_units * unit;
             const uint64_t L = (uint64_t)dp.host.max_move * unit;
             if (total >= kDynMinTotal && L >= kDynMinMove) {
-                // same grid as the static decomposition: it depends on the program only, so
-                // processes still pair CTA flag slots one to one
+                // the mid TMA ring at 2 CTAs / SM: twice the producers and LSU warps of the
+                // big ring (the LSU queue needs the warps; the TMA queue is indifferent).  The
+                // grid depends on the program only, so processes pair CTA flag slots 1:1.
+                const TmaConfig tm = c->force_big > 0 ? kTmaBig : kTmaMid;
+                E.stages = tm.stages;
+                E.chunk = tm.chunk;
+                E.ahead = tm.ahead;
+                nC = c->force_big > 0 ? c->cap_big : c->cap_ctas;
                 uint64_t U = total / ((uint64_t)nC * (uint64_t)c->dyn_pieces);
                 U = std::max<uint64_t>((uint64_t)E.chunk, std::min<uint64_t>(U, kDynMaxPiece));
                 U = U / (uint64_t)E.chunk * (uint64_t)E.chunk;
@@ -716,6 +722,9 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     c->cap_ctas = cap;
     c->cap_big = capb;
     c->cap_small = std::max(1, (c->emulated ? c->sm_count / c->G : c->sm_count));
+    if (getenv("MPXA_DEBUG"))
+        fprintf(stderr, "mpxa: %d SMs, executor CTAs/SM mid %d big %d -> caps %d / %d\n", c->sm_count, occ, occ_big,
+                c->cap_ctas, c->cap_big);
     if (const char *e = getenv("MPXA_NS")) c->force_ns = atoi(e);
     if (const char *e = getenv("MPXA_NF")) c->force_nf = atoi(e);
     if (const char *e = getenv("MPXA_TMA_BIG")) c->force_big = atoi(e);

@@ -120,6 +120,7 @@ __device__ __noinline__ void lsu_copy_range(char *dst, const char *src, uint64_t
     char *d = dst + head;
     const unsigned m = (unsigned)((uintptr_t)d & 15);
     const unsigned W = m == 0 ? 16u : (m & -m);
+    // shifted full-vector stores pay off once every warp has a whole block of spans
     for (uint64_t i0 = t; i0 < nv; i0 += (uint64_t)kLsuUnroll * nt) {
         uint4 v[kLsuUnroll];
 #pragma unroll
@@ -532,6 +533,42 @@ __device__ __noinline__ void small_batch(const ExecParams &P, const ExecShared &
 // its own and copies them with 16-B source vectors and destination-width stores.  The
 // queues are independent, so neither role waits for the other.  Returns whether this
 // thread issued generic stores.
+// Up to 15 bytes [o, o+n) of a piece whose source and destination(s) are 16-B congruent:
+// split into naturally aligned 1/2/4/8-byte accesses, every load issued before any store.
+__device__ __noinline__ void copy_edge(const ExecParams &P, const ExecShared &S, const Move &m, const MovePlan &mp,
+                                       uint64_t o, uint32_t n) {
+    uint64_t v[7];
+    uint8_t sz[7];
+    int k = 0;
+    const char *a = mp.src + o;
+    for (uint32_t done = 0; done < n && k < 7; k++) {
+        const uintptr_t x = (uintptr_t)(a + done);
+        uint32_t w = 8;
+        while (w > 1 && ((x & (w - 1)) || w > n - done)) w >>= 1;
+        sz[k] = (uint8_t)w;
+        const char *q = a + done;
+        v[k] = w == 8 ? __ldcg((const unsigned long long *)q)
+             : w == 4 ? __ldcg((const unsigned int *)q)
+             : w == 2 ? __ldcg((const unsigned short *)q) : (uint64_t)ldcg((const uint8_t *)q);
+        done += w;
+    }
+    const int nd = m.fanout ? P.p : 1;
+    for (int j = 0; j < nd; j++) {
+        char *d = (m.fanout ? base_of(P, S, m.dst_kind, j) + mp.doff : mp.dst) + o;
+        uint32_t done = 0;
+        for (int i = 0; i < k; i++) {
+            char *q = d + done;
+            switch (sz[i]) {
+                case 8: *(unsigned long long *)q = v[i]; break;
+                case 4: *(unsigned int *)q = (unsigned int)v[i]; break;
+                case 2: *(unsigned short *)q = (unsigned short)v[i]; break;
+                default: *q = (char)v[i];
+            }
+            done += sz[i];
+        }
+    }
+}
+
 __device__ __forceinline__ int find_move(const uint32_t *pc, int nm, uint32_t u) {
     int lo = 0, hi = nm - 1;      // last move with pc[m] <= u (moves with no piece are skipped)
     while (lo < hi) {
@@ -612,15 +649,9 @@ __device__ __noinline__ bool dyn_step(const ExecParams &P, ExecShared &S, Produc
             uint64_t head = (16 - ((uintptr_t)mp.src & 15)) & 15;
             if (head > nb) head = nb;
             const uint64_t body = (nb - head) & ~(uint64_t)15;
-            for (uint64_t i = 0; i < nb; i++) {            // head and tail bytes
-                if (i == head) i = head + body;
-                if (i >= nb) break;
-                const char bt = (char)ldcg((const uint8_t *)mp.src + i);
-                if (!m.fanout) mp.dst[i] = bt;
-                else
-                    for (int j = 0; j < P.p; j++) base_of(P, S, m.dst_kind, j)[mp.doff + i] = bt;
-                wrote = true;
-            }
+            // head and tail bytes (< 16 each; congruent piece: widest aligned accesses)
+            if (head) { copy_edge(P, S, m, mp, 0, (uint32_t)head); wrote = true; }
+            if (nb > head + body) { copy_edge(P, S, m, mp, head + body, (uint32_t)(nb - head - body)); wrote = true; }
             for (uint64_t o = 0; o < body; o += chunk) {
                 RingEntry e;
                 e.len = (uint32_t)min(chunk, body - o);
@@ -634,11 +665,12 @@ __device__ __noinline__ bool dyn_step(const ExecParams &P, ExecShared &S, Produc
         }
     } else if (warp >= 1 && totB) {
         uint32_t *q = &P.dc->dyn_next2[g];
+        uint32_t un = 0;
+        if (lane == 0) un = atomicAdd(q, 1u);
         for (;;) {
-            uint32_t u = 0;
-            if (lane == 0) u = atomicAdd(q, 1u);
-            u = __shfl_sync(0xffffffffu, u, 0);
+            const uint32_t u = __shfl_sync(0xffffffffu, un, 0);
             if (u >= totB) break;
+            if (lane == 0) un = atomicAdd(q, 1u);   // next piece requested while this one copies
             const int mi = find_move(S.pcB, nm, u);
             const Move &m = S.moves[mi];
             const MovePlan mp = piece_plan(P, S, mi, (uint64_t)(u - S.pcB[mi]) * U, U);

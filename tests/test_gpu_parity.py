@@ -215,6 +215,39 @@ def test_cfg4_alltoallv(mean, packed):
                 assert np.array_equal(host(d_recv).view(np.uint8), want), (seed, G, algo, g)
 
 
+@pytest.mark.parametrize("dyn", [True, False])
+def test_alltoallv_large_misaligned(dyn, monkeypatch):
+    """Large byte-granular alltoallv (dtype 1, 0.5-1.5 MiB per pair, 0-15 byte gaps between
+    segments): every source/destination misalignment class, through the dynamic work-queue
+    executor (TMA queue for 16-B congruent segments, LSU queue with shifted 16-B stores
+    otherwise) and the static slices; canary bytes outside the segments must survive."""
+    p = 8
+    rng = np.random.default_rng(7)
+    counts = rng.integers(512 << 10, 3 << 19, size=(p, p)).astype(np.int64)
+    counts[0, 3] = 0
+    sc, rc = counts, counts.T.copy()
+    gs = rng.integers(0, 16, size=(p, p))
+    gr = rng.integers(0, 16, size=(p, p))
+    sd = np.zeros_like(sc); sd[:, 1:] = np.cumsum(sc + gs, 1)[:, :-1]; sd += gs[:, :1]
+    rd = np.zeros_like(rc); rd[:, 1:] = np.cumsum(rc + gr, 1)[:, :-1]; rd += gr[:, :1]
+    S = int((sd + sc).max()) + 16
+    R = int((rd + rc).max()) + 16
+    send = rng.integers(0, 256, size=(p, S), dtype=np.uint8)
+    recv0 = np.full((p, R), 0xA5, dtype=np.uint8)
+    want = oracle.alltoallv_definition(send, sc, sd, rc, rd, 1, recv0)
+    if not dyn:
+        monkeypatch.setenv("MPXA_NO_DYN", "1")
+    for G in (0, 8):
+        c = Comm(ranks_per_proc=p, device=0, emulate_gpus=G, timeout_s=20.0)
+        for off in (0, 1, 8):           # shift the whole send buffer: more alignment classes
+            d_send = torch.zeros(p * S + 16, dtype=torch.uint8, device=DEV)
+            d_send[off:off + p * S] = dev(send.reshape(-1))
+            d_recv = dev(recv0)
+            c.alltoallv(d_send[off:off + p * S].view(p, S), sc, sd, d_recv, rc, rd)
+            assert np.array_equal(host(d_recv), want), (G, off, dyn)
+        c.finalize()
+
+
 def test_alltoallv_counts_kernel():
     """A2: single GPU -> fused transpose+scan kernel; emulated GPUs -> the multi-process
     path (alltoall of one int64 per pair through the flag protocol, then the scan kernel)."""
