@@ -59,6 +59,9 @@ def lib():
             "orc_alltoallv_hier": [I, I, Z, P, Z, P, P, P, Z, P, P, S],
             "orc_alltoall_hier": [I, I, Z, P, P, S],
             "orc_counts_exchange": [I, P, P, P, S],
+            "orc_neighbor_definition": [I, Z, P, P, P, P, P, Z, P, P, P, P, P, Z],
+            "orc_neighbor_standard": [I, Z, P, P, P, P, P, Z, P, P, P, P, P, Z, S],
+            "orc_neighbor_locality": [I, I, Z, P, P, P, P, P, P, Z, P, P, P, P, P, P, Z, S, P],
         }
         for name, args in sig.items():
             f = getattr(_lib, name)
@@ -193,3 +196,61 @@ def counts_exchange(sendcounts: np.ndarray):
     st = Stats()
     _check(lib().orc_counts_exchange(p, _ptr(sc), _ptr(rc), _ptr(rd), ctypes.byref(st)), "counts_exchange")
     return rc, rd, st.as_dict()
+
+
+# ---- f1: neighborhood alltoallv --------------------
+# A graph is a dict of numpy arrays (global view, rank-major edge lists):
+#   indeg (p,) int32, src/rc/rd (sum indeg,) int32/int64/int64 -- in-edges in order
+#   outdeg (p,) int32, dst/sc/sd (sum outdeg,) int32/int64/int64 -- out-edges in order
+# Locality variant: send_idx / recv_idx, one int64 global index per element, edge by edge.
+
+def _graph_args(gr):
+    i32 = lambda a: np.ascontiguousarray(a, dtype=np.int32)
+    i64 = lambda a: np.ascontiguousarray(a, dtype=np.int64)
+    return (i32(gr["indeg"]), i32(gr["src"]), i64(gr["rc"]), i64(gr["rd"]),
+            i32(gr["outdeg"]), i32(gr["dst"]), i64(gr["sc"]), i64(gr["sd"]))
+
+
+def neighbor_definition(send, recv_init, w, gr):
+    """MPI_Neighbor_alltoallv result: recv_init copy with every in-edge's range written."""
+    send = _u8(send)
+    recv = np.array(_u8(recv_init), copy=True)
+    indeg, src, rc, rd, outdeg, dst, sc, sd = a = _graph_args(gr)
+    p = send.shape[0]
+    _check(lib().orc_neighbor_definition(p, w, _ptr(indeg), _ptr(src), _ptr(rc), _ptr(rd), _ptr(recv),
+                                         recv.shape[1], _ptr(outdeg), _ptr(dst), _ptr(sc), _ptr(sd),
+                                         _ptr(send), send.shape[1]), "neighbor_definition")
+    del a
+    return recv
+
+
+def neighbor(send, recv_init, w, gr, variant="standard", g=0, send_idx=None, recv_idx=None, ppn=0):
+    """Simulate the standard or the locality-aware (variant='locality', groups of g ranks)
+    persistent neighbor alltoallv.  Returns (recv, stats dict); stats gains 'inter_values'
+    (index/value records crossing group boundaries) for the locality variant."""
+    send = _u8(send)
+    recv = np.array(_u8(recv_init), copy=True)
+    indeg, src, rc, rd, outdeg, dst, sc, sd = _graph_args(gr)
+    p = send.shape[0]
+    st = Stats(ppn=ppn or g or p)
+    L = lib()
+    if variant == "standard":
+        r = L.orc_neighbor_standard(p, w, _ptr(indeg), _ptr(src), _ptr(rc), _ptr(rd), _ptr(recv), recv.shape[1],
+                                    _ptr(outdeg), _ptr(dst), _ptr(sc), _ptr(sd), _ptr(send), send.shape[1],
+                                    ctypes.byref(st))
+        _check(r, "neighbor/standard")
+        return recv, st.as_dict()
+    if variant != "locality":
+        raise ValueError(variant)
+    si = np.ascontiguousarray(send_idx, dtype=np.int64)
+    ri = np.ascontiguousarray(recv_idx, dtype=np.int64)
+    iv = ctypes.c_int64(0)
+    r = L.orc_neighbor_locality(p, g, w, _ptr(indeg), _ptr(src), _ptr(rc), _ptr(rd), _ptr(ri), _ptr(recv),
+                                recv.shape[1], _ptr(outdeg), _ptr(dst), _ptr(sc), _ptr(sd), _ptr(si), _ptr(send),
+                                send.shape[1], ctypes.byref(st), ctypes.byref(iv))
+    if r == -3:
+        raise ValueError("inconsistent recv_indices (locality handshake)")
+    _check(r, "neighbor/locality")
+    d = st.as_dict()
+    d["inter_values"] = int(iv.value)
+    return recv, d

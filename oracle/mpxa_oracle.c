@@ -567,3 +567,325 @@ int orc_counts_exchange(int p, const int64_t *sendcounts, int64_t *recvcounts, i
     tp_free(&t);
     return err;
 }
+
+/* ==================================================================================== */
+/* f1: persistent neighborhood alltoallv (§2.2).      */
+/*                                                                                      */
+/* Graph layout (global view, one entry list per rank, rank-major):                     */
+/*   indeg[r], and for r's in-edges k (in order): src, rc (count, elements), rd (displ)  */
+/*   outdeg[r], and for r's out-edges k: dst, sc, sd.                                    */
+/* Edges are matched like MPI matches messages: the j-th out-edge of r towards q pairs   */
+/* with the j-th in-edge of q from r (multigraphs allowed); counts must agree.           */
+/* Locality variant: send_idx / recv_idx hold one global index per element, laid out     */
+/* edge by edge in edge order (r's out-edges: sc[k] ids each; q's in-edges likewise).     */
+/* ==================================================================================== */
+
+/* position of the out-edge of r that pairs with in-edge kin of q (-1 if none) */
+static int64_t nb_match(const int *outdeg, const int64_t *ooff, const int *dst,
+                        const int *indeg, const int64_t *ioff, const int *src, int q, int kin) {
+    int r = src[ioff[q] + kin];
+    int occ = 0;
+    for (int k = 0; k < kin; k++) if (src[ioff[q] + k] == r) occ++;
+    for (int k = 0; k < outdeg[r]; k++)
+        if (dst[ooff[r] + k] == q) {
+            if (occ == 0) return ooff[r] + k;
+            occ--;
+        }
+    (void)indeg;
+    return -1;
+}
+
+static void nb_offsets(int p, const int *deg, int64_t *off) {
+    off[0] = 0;
+    for (int r = 0; r < p; r++) off[r + 1] = off[r] + deg[r];
+}
+
+/* Checks of the Dist_graph / Neighbor_alltoallv contract:
+ * valid ranks, non-negative counts, in-bounds regions, every in-edge matched by an
+ * out-edge of the same count and every out-edge matched. */
+static int nb_args_ok(int p, size_t w, const int *indeg, const int *src, const int64_t *rc,
+                      const int64_t *rd, size_t rstride, const int *outdeg, const int *dst,
+                      const int64_t *sc, const int64_t *sd, size_t sstride, int64_t *ioff,
+                      int64_t *ooff) {
+    if (p < 1 || w < 1) return 0;
+    nb_offsets(p, indeg, ioff);
+    nb_offsets(p, outdeg, ooff);
+    for (int r = 0; r < p; r++) {
+        if (indeg[r] < 0 || outdeg[r] < 0) return 0;
+        for (int64_t e = ioff[r]; e < ioff[r + 1]; e++) {
+            if (src[e] < 0 || src[e] >= p || rc[e] < 0 || rd[e] < 0) return 0;
+            if ((uint64_t)(rc[e] + rd[e]) * w > rstride) return 0;
+        }
+        for (int64_t e = ooff[r]; e < ooff[r + 1]; e++) {
+            if (dst[e] < 0 || dst[e] >= p || sc[e] < 0 || sd[e] < 0) return 0;
+            if ((uint64_t)(sc[e] + sd[e]) * w > sstride) return 0;
+        }
+    }
+    int64_t nin = ioff[p], matched = 0;
+    for (int q = 0; q < p; q++)
+        for (int k = 0; k < indeg[q]; k++) {
+            int64_t o = nb_match(outdeg, ooff, dst, indeg, ioff, src, q, k);
+            if (o < 0 || sc[o] != rc[ioff[q] + k]) return 0;
+            matched++;
+        }
+    return matched == nin && nin == ooff[p];
+}
+
+/* Definition (MPI_Neighbor_alltoallv, Listing 3): for every in-edge k of q
+ * from r, recv_q[rd*w, +rc*w) = the bytes r's matching out-edge names in send_r; every other
+ * byte of recv_q unchanged. */
+int orc_neighbor_definition(int p, size_t w, const int *indeg, const int *src, const int64_t *rc,
+                            const int64_t *rd, unsigned char *recv, size_t rstride, const int *outdeg,
+                            const int *dst, const int64_t *sc, const int64_t *sd,
+                            const unsigned char *send, size_t sstride) {
+    int64_t *ioff = (int64_t *)malloc(sizeof(int64_t) * (p + 1));
+    int64_t *ooff = (int64_t *)malloc(sizeof(int64_t) * (p + 1));
+    int ok = nb_args_ok(p, w, indeg, src, rc, rd, rstride, outdeg, dst, sc, sd, sstride, ioff, ooff);
+    if (ok)
+        for (int q = 0; q < p; q++)
+            for (int k = 0; k < indeg[q]; k++) {
+                int64_t e = ioff[q] + k, o = nb_match(outdeg, ooff, dst, indeg, ioff, src, q, k);
+                if (rc[e])
+                    memcpy(recv + (size_t)q * rstride + (size_t)rd[e] * w,
+                           send + (size_t)src[e] * sstride + (size_t)sd[o] * w, (size_t)rc[e] * w);
+            }
+    free(ioff); free(ooff);
+    return ok ? 0 : -1;
+}
+
+/* Standard persistent neighbor alltoallv: one message per out-edge with
+ * count > 0 (tag = occurrence of that destination among the rank's out-edges), then every
+ * rank receives its in-edges in order.  Counters: msgs = edges with count > 0. */
+int orc_neighbor_standard(int p, size_t w, const int *indeg, const int *src, const int64_t *rc,
+                          const int64_t *rd, unsigned char *recv, size_t rstride, const int *outdeg,
+                          const int *dst, const int64_t *sc, const int64_t *sd,
+                          const unsigned char *send, size_t sstride, orc_stats *st) {
+    int64_t *ioff = (int64_t *)malloc(sizeof(int64_t) * (p + 1));
+    int64_t *ooff = (int64_t *)malloc(sizeof(int64_t) * (p + 1));
+    int err = nb_args_ok(p, w, indeg, src, rc, rd, rstride, outdeg, dst, sc, sd, sstride, ioff, ooff) ? 0 : -1;
+    transport_t t;
+    if (!err && tp_init(&t, p, st)) err = -1;
+    if (!err) {
+        for (int r = 0; r < p && !err; r++)
+            for (int k = 0; k < outdeg[r] && !err; k++) {
+                int64_t e = ooff[r] + k;
+                int occ = 0;
+                for (int k2 = 0; k2 < k; k2++) if (dst[ooff[r] + k2] == dst[e]) occ++;
+                if (sc[e]) err = tp_send(&t, r, dst[e], occ, send + (size_t)r * sstride + (size_t)sd[e] * w,
+                                         (size_t)sc[e] * w);
+            }
+        if (st) st->rounds = 1;
+        for (int q = 0; q < p && !err; q++)
+            for (int k = 0; k < indeg[q] && !err; k++) {
+                int64_t e = ioff[q] + k;
+                int occ = 0;
+                for (int k2 = 0; k2 < k; k2++) if (src[ioff[q] + k2] == src[e]) occ++;
+                if (rc[e] && tp_recv(&t, q, src[e], occ, recv + (size_t)q * rstride + (size_t)rd[e] * w,
+                                     (size_t)rc[e] * w) != rc[e] * (int64_t)w) err = -2;
+            }
+        if (!err && tp_pending(&t)) err = -2;
+        tp_free(&t);
+    }
+    free(ioff); free(ooff);
+    return err;
+}
+
+static int cmp_i64(const void *a, const void *b) {
+    int64_t x = *(const int64_t *)a, y = *(const int64_t *)b;
+    return x < y ? -1 : x > y;
+}
+
+/* sorted unique copy of v[0..n) into out; returns the count */
+static int64_t uniq_sorted(const int64_t *v, int64_t n, int64_t *out) {
+    if (n <= 0) return 0;
+    memcpy(out, v, sizeof(int64_t) * (size_t)n);
+    qsort(out, (size_t)n, sizeof(int64_t), cmp_i64);
+    int64_t m = 1;
+    for (int64_t i = 1; i < n; i++) if (out[i] != out[m - 1]) out[m++] = out[i];
+    return m;
+}
+
+static int64_t find_sorted(const int64_t *v, int64_t n, int64_t x) {
+    int64_t lo = 0, hi = n - 1;
+    while (lo <= hi) {
+        int64_t mid = (lo + hi) / 2;
+        if (v[mid] == x) return mid;
+        if (v[mid] < x) lo = mid + 1; else hi = mid - 1;
+    }
+    return -1;
+}
+
+#define NB_TAG_FWD 100000
+#define NB_TAG_EXCH 200000
+#define NB_TAG_FAN 300000
+
+/* Locality-aware persistent neighbor alltoallv with unique value indices (PAPER.md:157:
+ * "unique indices for all values ... eliminate a single value from being sent between a set
+ * of nodes multiple times"; three-phase plan of SPEC.md:307-315).  Nodes are groups of g
+ * consecutive ranks; the aggregator for (node A, remote node B) is leader_for(B) on A =
+ * A*g + (B mod g).  Messages carry (index, value) records, index sorted:
+ *   (1) every rank r of A sends, per remote node B, the set of unique indices among its
+ *       elements bound for ranks of B (per-sender dedup), with their values, to L(A,B);
+ *   (2) L(A,B) merges the sets of its node's senders (one record per index) and sends ONE
+ *       message with each unique index once to L(B,A);
+ *   (3) L(B,A) sends every rank q of B the values of its in-edge elements from node A, in
+ *       q's element order; q stores them at its receive displacements.
+ * Intra-node edges are sent directly (standard).  *inter_values counts the (index,value)
+ * records crossing node boundaries (phase 2).  Returns -3 when a received element's index
+ * differs from the index of the element its edge matches (inconsistent recv_indices). */
+int orc_neighbor_locality(int p, int g, size_t w, const int *indeg, const int *src, const int64_t *rc,
+                          const int64_t *rd, const int64_t *recv_idx, unsigned char *recv, size_t rstride,
+                          const int *outdeg, const int *dst, const int64_t *sc, const int64_t *sd,
+                          const int64_t *send_idx, const unsigned char *send, size_t sstride, orc_stats *st,
+                          int64_t *inter_values) {
+    if (g < 1 || p % g) return -1;
+    int64_t *ioff = (int64_t *)malloc(sizeof(int64_t) * (p + 1));
+    int64_t *ooff = (int64_t *)malloc(sizeof(int64_t) * (p + 1));
+    int err = nb_args_ok(p, w, indeg, src, rc, rd, rstride, outdeg, dst, sc, sd, sstride, ioff, ooff) ? 0 : -1;
+    if (err) { free(ioff); free(ooff); return err; }
+    const int G = p / g;
+    /* element offsets of every edge in the index arrays */
+    int64_t *oe = (int64_t *)malloc(sizeof(int64_t) * (ooff[p] + 1));
+    int64_t *ie = (int64_t *)malloc(sizeof(int64_t) * (ioff[p] + 1));
+    oe[0] = 0; for (int64_t e = 0; e < ooff[p]; e++) oe[e + 1] = oe[e] + sc[e];
+    ie[0] = 0; for (int64_t e = 0; e < ioff[p]; e++) ie[e + 1] = ie[e] + rc[e];
+    /* consistency handshake: each received element's index equals its matched sent index */
+    for (int q = 0; q < p && !err; q++)
+        for (int k = 0; k < indeg[q] && !err; k++) {
+            int64_t e = ioff[q] + k, o = nb_match(outdeg, ooff, dst, indeg, ioff, src, q, k);
+            for (int64_t x = 0; x < rc[e]; x++)
+                if (recv_idx[ie[e] + x] != send_idx[oe[o] + x]) { err = -3; break; }
+        }
+    int64_t nel = oe[ooff[p]] + ie[ioff[p]] + 1;
+    size_t rec = sizeof(int64_t) + w;                     /* (index, value) record */
+    int64_t *ids = (int64_t *)malloc(sizeof(int64_t) * (size_t)nel);
+    int64_t *uq = (int64_t *)malloc(sizeof(int64_t) * (size_t)nel);
+    unsigned char *buf = (unsigned char *)malloc(rec * (size_t)nel);
+    unsigned char *agg = (unsigned char *)malloc(rec * (size_t)nel);
+    transport_t t;
+    if (!err && tp_init(&t, p, st)) err = -1;
+    if (err) goto out_noT;
+    if (inter_values) *inter_values = 0;
+    /* intra-node edges: direct (standard) messages */
+    for (int r = 0; r < p && !err; r++)
+        for (int k = 0; k < outdeg[r] && !err; k++) {
+            int64_t e = ooff[r] + k;
+            if (dst[e] / g != r / g || !sc[e]) continue;
+            int occ = 0;
+            for (int k2 = 0; k2 < k; k2++) if (dst[ooff[r] + k2] == dst[e]) occ++;
+            err = tp_send(&t, r, dst[e], occ, send + (size_t)r * sstride + (size_t)sd[e] * w, (size_t)sc[e] * w);
+        }
+    /* phase 1: per-sender dedup, forward (index, value) records to L(A,B) */
+    for (int r = 0; r < p && !err; r++) {
+        int A = r / g;
+        for (int B = 0; B < G && !err; B++) {
+            if (B == A) continue;
+            int64_t n = 0;
+            for (int k = 0; k < outdeg[r]; k++) {
+                int64_t e = ooff[r] + k;
+                if (dst[e] / g == B) for (int64_t x = 0; x < sc[e]; x++) ids[n++] = send_idx[oe[e] + x];
+            }
+            int64_t m = uniq_sorted(ids, n, uq);
+            for (int64_t u = 0; u < m; u++) {           /* value: first element with that index */
+                const unsigned char *v = NULL;
+                for (int k = 0; k < outdeg[r] && !v; k++) {
+                    int64_t e = ooff[r] + k;
+                    if (dst[e] / g != B) continue;
+                    for (int64_t x = 0; x < sc[e]; x++)
+                        if (send_idx[oe[e] + x] == uq[u]) {
+                            v = send + (size_t)r * sstride + (size_t)(sd[e] + x) * w;
+                            break;
+                        }
+                }
+                memcpy(buf + rec * u, &uq[u], sizeof(int64_t));
+                memcpy(buf + rec * u + sizeof(int64_t), v, w);
+            }
+            if (m) err = tp_send(&t, r, A * g + (B % g), NB_TAG_FWD + B, buf, rec * (size_t)m);
+        }
+    }
+    if (st) st->rounds++;
+    /* phase 2: L(A,B) merges its node's records (one per index) and sends one message */
+    for (int A = 0; A < G && !err; A++)
+        for (int B = 0; B < G && !err; B++) {
+            if (B == A) continue;
+            int lead = A * g + (B % g), peer = B * g + (A % g);
+            int64_t n = 0;
+            for (int s = 0; s < g && !err; s++) {
+                int64_t got = tp_recv(&t, lead, A * g + s, NB_TAG_FWD + B, agg + rec * n, rec * (size_t)(nel - n));
+                if (got == -1) continue;                       /* that sender had nothing for B */
+                n += got / (int64_t)rec;
+            }
+            /* merge: records sorted by index, first occurrence kept */
+            for (int64_t i = 0; i < n; i++) memcpy(&ids[i], agg + rec * i, sizeof(int64_t));
+            int64_t m = uniq_sorted(ids, n, uq);
+            for (int64_t u = 0; u < m; u++) {
+                int64_t i = 0;
+                while (memcmp(agg + rec * i, &uq[u], sizeof(int64_t))) i++;
+                memcpy(buf + rec * u, agg + rec * i, rec);
+            }
+            if (m) {
+                err = tp_send(&t, lead, peer, NB_TAG_EXCH + A, buf, rec * (size_t)m);
+                if (inter_values) *inter_values += m;
+            }
+        }
+    if (st) st->rounds++;
+    /* phase 3: L(B,A) fans the values out to every rank q of B, in q's element order */
+    for (int B = 0; B < G && !err; B++)
+        for (int A = 0; A < G && !err; A++) {
+            if (A == B) continue;
+            int lead = B * g + (A % g), peer = A * g + (B % g);
+            int64_t got = tp_recv(&t, lead, peer, NB_TAG_EXCH + A, agg, rec * (size_t)nel);
+            int64_t m = got < 0 ? 0 : got / (int64_t)rec;
+            for (int64_t u = 0; u < m; u++) memcpy(&uq[u], agg + rec * u, sizeof(int64_t));
+            for (int qq = 0; qq < g && !err; qq++) {
+                int q = B * g + qq;
+                int64_t n = 0;
+                for (int k = 0; k < indeg[q] && !err; k++) {
+                    int64_t e = ioff[q] + k;
+                    if (src[e] / g != A) continue;
+                    for (int64_t x = 0; x < rc[e]; x++) {
+                        int64_t u = find_sorted(uq, m, recv_idx[ie[e] + x]);
+                        if (u < 0) { err = -2; break; }
+                        memcpy(buf + w * n, agg + rec * u + sizeof(int64_t), w);
+                        n++;
+                    }
+                }
+                if (!err && n) err = tp_send(&t, lead, q, NB_TAG_FAN + A, buf, w * (size_t)n);
+            }
+        }
+    if (st) st->rounds++;
+    /* receivers: direct intra-node edges, then one fan-out message per remote node */
+    for (int q = 0; q < p && !err; q++) {
+        int B = q / g;
+        for (int k = 0; k < indeg[q] && !err; k++) {
+            int64_t e = ioff[q] + k;
+            if (src[e] / g != B || !rc[e]) continue;
+            int occ = 0;
+            for (int k2 = 0; k2 < k; k2++) if (src[ioff[q] + k2] == src[e]) occ++;
+            if (tp_recv(&t, q, src[e], occ, recv + (size_t)q * rstride + (size_t)rd[e] * w, (size_t)rc[e] * w) !=
+                rc[e] * (int64_t)w) err = -2;
+        }
+        for (int A = 0; A < G && !err; A++) {
+            if (A == B) continue;
+            int64_t need = 0;
+            for (int k = 0; k < indeg[q]; k++) if (src[ioff[q] + k] / g == A) need += rc[ioff[q] + k];
+            if (!need) continue;
+            if (tp_recv(&t, q, B * g + (A % g), NB_TAG_FAN + A, buf, w * (size_t)nel) != need * (int64_t)w) {
+                err = -2;
+                break;
+            }
+            int64_t n = 0;
+            for (int k = 0; k < indeg[q]; k++) {
+                int64_t e = ioff[q] + k;
+                if (src[e] / g != A) continue;
+                if (rc[e]) memcpy(recv + (size_t)q * rstride + (size_t)rd[e] * w, buf + w * n, (size_t)rc[e] * w);
+                n += rc[e];
+            }
+        }
+    }
+    if (!err && tp_pending(&t)) err = -2;
+    tp_free(&t);
+out_noT:
+    free(ids); free(uq); free(buf); free(agg); free(oe); free(ie); free(ioff); free(ooff);
+    return err;
+}

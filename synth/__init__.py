@@ -199,3 +199,119 @@ def alltoallv_buffers(seed: int, counts: np.ndarray, elem: int = 8, packed: bool
                 o = int(sd[r, j]) * elem
                 send[r, o:o + n * elem] = seg
     return send, sc, sd, rc, rd, S, Rcap
+
+
+# ---- f1: neighborhood topologies -------------------------------------
+# Graph dicts as in oracle.neighbor_*: global, rank-major edge lists with packed
+# displacements (exclusive prefix sums in edge order).  Element payloads are a pure
+# function of the element's global index (h32 of the index), so equal indices carry equal
+# values everywhere -- the precondition of the locality-aware variant.
+
+def _pack(counts_per_rank):
+    """Exclusive prefix sums of each rank's edge counts (packed displacements)."""
+    out = []
+    for cs in counts_per_rank:
+        d, acc = [], 0
+        for c in cs:
+            d.append(acc)
+            acc += c
+        out.append(d)
+    return out
+
+
+def graph_from_edges(p, edges):
+    """edges: list of (src, dst, ids) with ids a list of global indices (count = len).
+    Out-edges of a rank are in list order; in-edges of a rank are in list order too.
+    Returns (graph, send_idx, recv_idx)."""
+    outs = [[] for _ in range(p)]
+    ins = [[] for _ in range(p)]
+    for s, d, ids in edges:
+        outs[s].append((d, list(ids)))
+        ins[d].append((s, list(ids)))
+    sd = _pack([[len(i) for _, i in o] for o in outs])
+    rd = _pack([[len(i) for _, i in o] for o in ins])
+    g = {"indeg": np.array([len(i) for i in ins], np.int32),
+         "src": np.array([s for i in ins for s, _ in i], np.int32),
+         "rc": np.array([len(ids) for i in ins for _, ids in i], np.int64),
+         "rd": np.array([x for r in rd for x in r], np.int64),
+         "outdeg": np.array([len(o) for o in outs], np.int32),
+         "dst": np.array([d for o in outs for d, _ in o], np.int32),
+         "sc": np.array([len(ids) for o in outs for _, ids in o], np.int64),
+         "sd": np.array([x for r in sd for x in r], np.int64)}
+    send_idx = np.array([x for o in outs for _, ids in o for x in ids], np.int64)
+    recv_idx = np.array([x for i in ins for _, ids in i for x in ids], np.int64)
+    return g, send_idx, recv_idx
+
+
+def neighbor_buffers(seed, p, gr, send_idx, w=8, canary=0xA5):
+    """Send rows (packed per out-edge; element value = h32-based function of its global
+    index, w bytes) and a canary-filled recv buffer sized for the in-edges."""
+    sc, sd, rc, rd = gr["sc"], gr["sd"], gr["rc"], gr["rd"]
+    ooff = np.concatenate([[0], np.cumsum(gr["outdeg"])])
+    ioff = np.concatenate([[0], np.cumsum(gr["indeg"])])
+    S = max(1, max((int((sd[ooff[r]:ooff[r + 1]] + sc[ooff[r]:ooff[r + 1]]).max()) if ooff[r + 1] > ooff[r] else 0)
+                   for r in range(p))) * w
+    R = max(1, max((int((rd[ioff[r]:ioff[r + 1]] + rc[ioff[r]:ioff[r + 1]]).max()) if ioff[r + 1] > ioff[r] else 0)
+                   for r in range(p))) * w
+    send = np.zeros((p, S), np.uint8)
+    e0 = 0
+    for r in range(p):
+        for e in range(ooff[r], ooff[r + 1]):
+            n = int(sc[e])
+            ids = send_idx[e0:e0 + n].astype(np.uint64)
+            e0 += n
+            if n:
+                words = (w + 3) // 4
+                vals = np.stack([h32(seed, 0, 0, ids * np.uint64(words) + np.uint64(k)) for k in range(words)], 1)
+                send[r, int(sd[e]) * w:(int(sd[e]) + n) * w] = vals.astype(np.uint32).view(np.uint8).reshape(n, -1)[:, :w].reshape(-1)
+    return send, np.full((p, R), canary, np.uint8)
+
+
+def ring_edges(p, count):
+    """SPEC.md:300-303 ring: rank r sends `count` elements to r-1 and r+1 (ids unique per edge)."""
+    edges = []
+    for r in range(p):
+        for d in ((r - 1) % p, (r + 1) % p):
+            edges.append((r, d, [(r * p + d) * count + k for k in range(count)]))
+    return edges
+
+
+def stencil_edges(px, py, nx, ny, corners=True):
+    """2-D halo exchange: an nx x ny grid of points (global index y*nx + x) split into
+    px x py rank blocks (rank = by*px + bx).  Each rank sends the boundary points a
+    neighbouring block needs: one row/column to each edge neighbour (5-point) and, with
+    corners, its corner point to each diagonal neighbour (9-point).  A corner point thus goes
+    to three ranks -- duplicate indices across a node boundary when those ranks share a node."""
+    bw, bh = nx // px, ny // py
+    edges = []
+    for by in range(py):
+        for bx in range(px):
+            r = by * px + bx
+            x0, y0 = bx * bw, by * bh
+            x1, y1 = x0 + bw - 1, y0 + bh - 1
+            nbrs = []
+            if bx > 0: nbrs.append(((by, bx - 1), [y * nx + x0 for y in range(y0, y1 + 1)]))
+            if bx < px - 1: nbrs.append(((by, bx + 1), [y * nx + x1 for y in range(y0, y1 + 1)]))
+            if by > 0: nbrs.append(((by - 1, bx), [y0 * nx + x for x in range(x0, x1 + 1)]))
+            if by < py - 1: nbrs.append(((by + 1, bx), [y1 * nx + x for x in range(x0, x1 + 1)]))
+            if corners:
+                for dy, dx, cx, cy in ((-1, -1, x0, y0), (-1, 1, x1, y0), (1, -1, x0, y1), (1, 1, x1, y1)):
+                    if 0 <= by + dy < py and 0 <= bx + dx < px:
+                        nbrs.append(((by + dy, bx + dx), [cy * nx + cx]))
+            for (ny_, nx_), ids in nbrs:
+                edges.append((r, ny_ * px + nx_, ids))
+    return edges
+
+
+def random_edges(seed, p, max_deg, max_count, idx_space):
+    """Random multigraph: each rank gets up to max_deg out-edges (repeats and self-edges
+    allowed), counts 0..max_count, element ids drawn from [0, idx_space) (duplicates
+    across and within edges)."""
+    rng = np.random.default_rng(seed)
+    edges = []
+    for r in range(p):
+        for _ in range(int(rng.integers(0, max_deg + 1))):
+            d = int(rng.integers(0, p))
+            n = int(rng.integers(0, max_count + 1))
+            edges.append((r, d, [int(x) for x in rng.integers(0, idx_space, n)]))
+    return edges
