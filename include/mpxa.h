@@ -71,7 +71,8 @@ typedef enum {
     MPXA_ERR_UNREGISTERED = 9 /* multi-process: recvbuf not in a registered buffer            */
 } mpxa_status;
 
-typedef enum { MPXA_OP_ALLTOALL = 0, MPXA_OP_ALLTOALLV = 1, MPXA_OP_ALLGATHER = 2 } mpxa_op_t;
+typedef enum { MPXA_OP_ALLTOALL = 0, MPXA_OP_ALLTOALLV = 1, MPXA_OP_ALLGATHER = 2,
+               MPXA_OP_NEIGHBOR_ALLTOALLV = 3 } mpxa_op_t;
 
 /* Variant registry.  PAIRWISE is the direct exchange
  * (for allgather: every rank pushes its block to every rank). */
@@ -80,8 +81,12 @@ typedef enum {
     MPXA_ALGO_PAIRWISE = 1,  /* alltoall, alltoallv, allgather                            */
     MPXA_ALGO_BRUCK = 2,     /* alltoall, allgather                                       */
     MPXA_ALGO_HIER = 3,      /* alltoall, alltoallv (groups of group_size ranks)          */
-    MPXA_ALGO_RING = 4       /* allgather                                                 */
+    MPXA_ALGO_RING = 4,      /* allgather                                                 */
+    MPXA_ALGO_LOCALITY = 5   /* neighbor alltoallv with global-index dedup    */
 } mpxa_algo_t;
+
+/* Adjacency topology (MPIX_Dist_graph_create_adjacent). */
+typedef struct mpxa_topo_s *mpxa_topo_t;
 
 /* Bootstrap callback: all-gather `bytes` bytes from every process into out[nprocs*bytes]
  * (out is ordered by process index).  Returns 0 on success.  Used only by collective
@@ -182,6 +187,59 @@ int mpxa_wait(mpxa_request_t req, mpxa_stream_t stream);   /* ACTIVE -> INACTIVE
                                                               `stream` (no host round trip)  */
 int mpxa_request_free(mpxa_request_t *req);
 int mpxa_request_algorithm(mpxa_request_t req, mpxa_algo_t *algo);
+
+/* ---- persistent neighborhood collectives (§2.2) ------ */
+/* MPIX_Dist_graph_create_adjacent (Listing 4).  Collective over the comm's
+ * processes.  Per local rank t (R of them, rank-major): indegree[t] in-neighbours listed in
+ * `sources` (sum(indegree) entries, local rank 0's first), outdegree[t] out-neighbours in
+ * `destinations`.  Repeated neighbours are separate edges, paired in order like MPI
+ * messages (the j-th edge r->q with the j-th edge q<-r).  Weights may be NULL; they are stored
+ * and, as the paper gives them no meaning, unused (SPEC.md decision).  `info` opaque, `reorder`
+ * accepted and ignored.  The caller owns *topo (mpxa_topo_free); it references `comm`.
+ * Errors: MPXA_ERR_ARG (NULL, negative degree, rank out of range).  Cross-process pairing is
+ * checked at *_init. */
+int mpxa_dist_graph_create_adjacent(mpxa_comm_t comm, const int *indegree, const int *sources,
+                                    const int *sourceweights, const int *outdegree,
+                                    const int *destinations, const int *destweights,
+                                    const void *info, int reorder, mpxa_topo_t *topo);
+int mpxa_topo_free(mpxa_topo_t *topo);
+
+/* MPIX_Neighbor_alltoallv_init (Listing 4): out-edge k of local rank t sends
+ * sendcounts[k] elements of dtype_size bytes from sendbuf + t*send_bytes_per_rank +
+ * sdispls[k]*w; in-edge k receives recvcounts[k] elements at recvbuf + t*recv_bytes_per_rank
+ * + rdispls[k]*w.  counts/displacements: host int64 arrays, one entry per edge, in the
+ * topology's edge order (rank-major).  The whole schedule (one move per edge) is compiled and
+ * uploaded here, once ("all setup costs ... incurred only once"); start/wait
+ * then launch one kernel each.  Collective.  Errors: MPXA_ERR_ARG (bounds, overlap, dtype),
+ * MPXA_ERR_MISMATCH (an edge without its partner, or partner counts differ). */
+int mpxa_neighbor_alltoallv_init(const void *sendbuf, const int64_t *sendcounts,
+                                 const int64_t *sdispls, size_t send_bytes_per_rank,
+                                 void *recvbuf, const int64_t *recvcounts,
+                                 const int64_t *rdispls, size_t recv_bytes_per_rank,
+                                 size_t dtype_size, mpxa_topo_t topo, const void *info,
+                                 mpxa_request_t *req);
+/* Locality-aware variant ("unique indices for all values to be sent and
+ * received ... eliminate a single value from being sent between a set of nodes multiple
+ * times").  send_indices: one global index per sent element (edge by edge, in the order of
+ * sendcounts); recv_indices: one per received element.  Equal indices must carry equal
+ * values.  Ranks form groups of the comm's group_size (default: the ranks of one GPU); the
+ * schedule forwards each group's unique (index) values for a remote group to the aggregator
+ * leader_for, sends every unique index ONCE between the two groups, and fans
+ * the values out to every (rank, offset) that needs them.  Extra error:
+ * MPXA_ERR_TOPOLOGY when a received element's index differs from the one its edge sends. */
+int mpxa_neighbor_alltoallv_locality_init(const void *sendbuf, const int64_t *sendcounts,
+                                          const int64_t *sdispls, size_t send_bytes_per_rank,
+                                          void *recvbuf, const int64_t *recvcounts,
+                                          const int64_t *rdispls, size_t recv_bytes_per_rank,
+                                          size_t dtype_size, const int64_t *send_indices,
+                                          const int64_t *recv_indices, mpxa_topo_t topo,
+                                          const void *info, mpxa_request_t *req);
+/* One-shot MPI_Neighbor_alltoallv (Listing 3): the standard schedule,
+ * compiled per call (the persistent form is the fast path). */
+int mpxa_neighbor_alltoallv(const void *sendbuf, const int64_t *sendcounts, const int64_t *sdispls,
+                            size_t send_bytes_per_rank, void *recvbuf, const int64_t *recvcounts,
+                            const int64_t *rdispls, size_t recv_bytes_per_rank, size_t dtype_size,
+                            mpxa_topo_t topo, mpxa_stream_t stream);
 
 /* ---- variant registry and selector --------------------- */
 int mpxa_set_algorithm(mpxa_comm_t comm, mpxa_op_t op, mpxa_algo_t algo); /* DEFAULT = selector */

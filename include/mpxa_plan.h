@@ -46,6 +46,14 @@ typedef struct {
 
 int mpxa_plan_build(int op, int algo, int p, int R, int G, int g, int stop_stage,
                     const int64_t *c, const int64_t *sd, const int64_t *rd, void **plan);
+/* f1 neighbor alltoallv schedule from a GLOBAL graph (all p ranks, rank-major edge lists as
+ * in mpxa_dist_graph_create_adjacent; counts/displacements per edge): locality = 0 standard,
+ * 1 locality-aware with groups of g ranks and per-element global indices (else NULL).
+ * Returns the mpxa status of the validation (MPXA_ERR_MISMATCH / _TOPOLOGY / _ARG). */
+int mpxa_plan_build_neighbor(int p, int R, int G, int g, int locality, const int *indeg, const int *src,
+                             const int64_t *rc, const int64_t *rd, const int *outdeg, const int *dst,
+                             const int64_t *sc, const int64_t *sd, const int64_t *send_idx,
+                             const int64_t *recv_idx, void **plan);
 int mpxa_plan_info(const void *plan, mpxa_plan_info_t *info);
 /* copies GPU `gpu`'s steps / moves; *n in: capacity, out: count */
 int mpxa_plan_steps(const void *plan, int gpu, mpxa_plan_step *out, int *n);

@@ -208,6 +208,15 @@ struct mpxa_request_s {
     cudaStream_t start_stream = nullptr;
 };
 
+struct mpxa_topo_s {
+    mpxa_comm_t comm = nullptr;
+    int p = 0;
+    std::vector<int> indeg, src, outdeg, dst;   // global graph, rank-major edge lists
+    std::vector<int> srcw, dstw;                // weights: stored, unused (SPEC.md decision)
+    int64_t in0 = 0, out0 = 0;                  // this process's first in / out edge
+    int64_t nin = 0, nout = 0;                  // this process's edge counts
+};
+
 namespace {
 
 bool dtype_ok(size_t w) { return w == 1 || w == 2 || w == 4 || w == 8 || w == 16; }
@@ -216,6 +225,34 @@ int bootstrap(mpxa_comm_t c, const void *in, void *out, size_t bytes) {
     if (c->nprocs == 1) { memcpy(out, in, bytes); return MPXA_SUCCESS; }
     if (!c->boot) return MPXA_ERR_ARG;
     return c->boot(in, out, bytes, c->ctx) == 0 ? MPXA_SUCCESS : MPXA_ERR_CUDA;
+}
+
+// all-gather variable-length byte strings (collective; two bootstrap rounds)
+int allgather_var(mpxa_comm_t c, const void *mine, size_t n, std::vector<std::vector<char>> &out) {
+    std::vector<uint64_t> sizes(c->nprocs);
+    uint64_t n64 = n;
+    int rc = bootstrap(c, &n64, sizes.data(), sizeof n64);
+    if (rc) return rc;
+    uint64_t mx = 0;
+    for (uint64_t z : sizes) mx = std::max(mx, z);
+    std::vector<char> pad(std::max<uint64_t>(mx, 1), 0), all((size_t)std::max<uint64_t>(mx, 1) * c->nprocs);
+    if (n) memcpy(pad.data(), mine, n);
+    rc = bootstrap(c, pad.data(), all.data(), pad.size());
+    if (rc) return rc;
+    out.assign(c->nprocs, {});
+    for (int q = 0; q < c->nprocs; q++)
+        out[q].assign(all.data() + (size_t)q * pad.size(), all.data() + (size_t)q * pad.size() + sizes[q]);
+    return MPXA_SUCCESS;
+}
+
+template <typename T>
+int allgather_concat(mpxa_comm_t c, const T *mine, size_t n, std::vector<T> &out) {
+    std::vector<std::vector<char>> parts;
+    int rc = allgather_var(c, mine, n * sizeof(T), parts);
+    if (rc) return rc;
+    out.clear();
+    for (auto &b : parts) out.insert(out.end(), (const T *)b.data(), (const T *)(b.data() + b.size()));
+    return MPXA_SUCCESS;
 }
 
 // ---- symmetric memory --------------------------------------------------------------
@@ -647,6 +684,63 @@ int uniform_impl(int op, const void *sendbuf, size_t count, size_t w, void *recv
     return run_program(c, *dp, (const char *)sendbuf, (char *)recvbuf, unit, sstride, rstride, stream);
 }
 
+// f1: persistent / one-shot neighbor alltoallv.  Local per-edge arrays of
+// this process's ranks are all-gathered into the global graph, validated and compiled.
+int neighbor_impl(bool locality, const void *sendbuf, const int64_t *sc, const int64_t *sd, size_t send_bpr,
+                  void *recvbuf, const int64_t *rc, const int64_t *rd, size_t recv_bpr, size_t w,
+                  const int64_t *sidx, const int64_t *ridx, mpxa_topo_t topo, cudaStream_t stream,
+                  mpxa_request_t *req) {
+    if (!topo || !topo->comm) return MPXA_ERR_ARG;
+    mpxa_comm_t c = topo->comm;
+    if (!dtype_ok(w)) return MPXA_ERR_ARG;
+    if ((topo->nout && (!sc || !sd)) || (topo->nin && (!rc || !rd))) return MPXA_ERR_ARG;
+    if (!sendbuf || !recvbuf) return MPXA_ERR_ARG;
+    if (overlap(sendbuf, send_bpr * c->R, recvbuf, recv_bpr * c->R)) return MPXA_ERR_ARG;
+    // local bounds ("counts/displs address in-bounds disjoint regions")
+    int64_t nsel = 0, nrel = 0;
+    for (int64_t e = 0; e < topo->nout; e++) {
+        if (sc[e] < 0 || sd[e] < 0 || (uint64_t)(sc[e] + sd[e]) * w > send_bpr) return MPXA_ERR_ARG;
+        nsel += sc[e];
+    }
+    for (int64_t e = 0; e < topo->nin; e++) {
+        if (rc[e] < 0 || rd[e] < 0 || (uint64_t)(rc[e] + rd[e]) * w > recv_bpr) return MPXA_ERR_ARG;
+        nrel += rc[e];
+    }
+    if (locality && ((nsel && !sidx) || (nrel && !ridx))) return MPXA_ERR_ARG;
+    std::vector<int64_t> SC, SD, RC, RD, SI, RI;
+    int r = allgather_concat(c, sc, (size_t)topo->nout, SC);
+    if (!r) r = allgather_concat(c, sd, (size_t)topo->nout, SD);
+    if (!r) r = allgather_concat(c, rc, (size_t)topo->nin, RC);
+    if (!r) r = allgather_concat(c, rd, (size_t)topo->nin, RD);
+    if (!r && locality) r = allgather_concat(c, sidx, (size_t)nsel, SI);
+    if (!r && locality) r = allgather_concat(c, ridx, (size_t)nrel, RI);
+    if (r) return r;
+    if (SC.size() != topo->dst.size() || RC.size() != topo->src.size()) return MPXA_ERR_MISMATCH;
+    Program P;
+    r = build_neighbor(P, locality, c->p, c->Rg, c->G, c->g, topo->indeg.data(), topo->src.data(), RC.data(),
+                       RD.data(), topo->outdeg.data(), topo->dst.data(), SC.data(), SD.data(),
+                       locality ? SI.data() : nullptr, locality ? RI.data() : nullptr);
+    if (r) return r;
+    if (req) {
+        auto q = new mpxa_request_s();
+        q->comm = c; q->op = MPXA_OP_NEIGHBOR_ALLTOALLV; q->algo = locality ? A_LOCALITY : A_PAIRWISE;
+        int rc2 = upload_program(P, q->prog);
+        if (rc2) { delete q; return rc2; }
+        q->send = (const char *)sendbuf; q->recv = (char *)recvbuf;
+        q->unit = w; q->send_stride = send_bpr; q->recv_stride = recv_bpr;
+        q->grid = choose_grid(c, P, w);
+        if (c->nprocs > 1) {
+            rc2 = mpxa_register(c, recvbuf, recv_bpr * c->R);
+            if (rc2) { delete q; return rc2; }
+        }
+        rc2 = ensure_work(c, (size_t)P.work_units * w * c->Rg);
+        if (rc2) { delete q; return rc2; }
+        *req = q;
+        return MPXA_SUCCESS;
+    }
+    return run_dynamic(c, P, (const char *)sendbuf, (char *)recvbuf, w, send_bpr, recv_bpr, stream);
+}
+
 cudaStream_t S(mpxa_stream_t s) { return (cudaStream_t)s; }
 
 }  // namespace
@@ -679,6 +773,7 @@ const char *mpxa_algo_name(mpxa_algo_t a) {
         case MPXA_ALGO_BRUCK: return "bruck";
         case MPXA_ALGO_HIER: return "hier";
         case MPXA_ALGO_RING: return "ring";
+        case MPXA_ALGO_LOCALITY: return "locality";
         default: return "unknown";
     }
 }
@@ -1016,7 +1111,7 @@ int mpxa_request_free(mpxa_request_t *qp) {
     if (q->active) return MPXA_ERR_LIFECYCLE;
     if (q->done) cudaEventDestroy(q->done);
     // cached uniform programs are shared with the comm; v-programs are owned
-    if (q->op == MPXA_OP_ALLTOALLV && q->prog && q->prog.use_count() == 1) {
+    if ((q->op == MPXA_OP_ALLTOALLV || q->op == MPXA_OP_NEIGHBOR_ALLTOALLV) && q->prog && q->prog.use_count() == 1) {
         cudaDeviceSynchronize();
         cudaFree(q->prog->dmem);
     }
@@ -1029,6 +1124,72 @@ int mpxa_request_algorithm(mpxa_request_t q, mpxa_algo_t *a) {
     if (!q || !a) return MPXA_ERR_ARG;
     *a = (mpxa_algo_t)q->algo;
     return MPXA_SUCCESS;
+}
+
+// ---- neighborhood collectives ------------------------------------------
+int mpxa_dist_graph_create_adjacent(mpxa_comm_t c, const int *indegree, const int *sources, const int *sourceweights,
+                                    const int *outdegree, const int *destinations, const int *destweights,
+                                    const void *info, int reorder, mpxa_topo_t *topo) {
+    (void)info; (void)reorder;
+    if (!c || !topo || !indegree || !outdegree) return MPXA_ERR_ARG;
+    *topo = nullptr;
+    int64_t nin = 0, nout = 0;
+    for (int t = 0; t < c->R; t++) {
+        if (indegree[t] < 0 || outdegree[t] < 0) return MPXA_ERR_ARG;
+        nin += indegree[t];
+        nout += outdegree[t];
+    }
+    if ((nin && !sources) || (nout && !destinations)) return MPXA_ERR_ARG;
+    for (int64_t e = 0; e < nin; e++) if (sources[e] < 0 || sources[e] >= c->p) return MPXA_ERR_ARG;
+    for (int64_t e = 0; e < nout; e++) if (destinations[e] < 0 || destinations[e] >= c->p) return MPXA_ERR_ARG;
+    std::unique_ptr<mpxa_topo_s> T(new mpxa_topo_s());
+    T->comm = c;
+    T->p = c->p;
+    T->nin = nin;
+    T->nout = nout;
+    std::vector<int> zin((size_t)nin, 1), zout((size_t)nout, 1);
+    int r = allgather_concat(c, indegree, (size_t)c->R, T->indeg);
+    if (!r) r = allgather_concat(c, outdegree, (size_t)c->R, T->outdeg);
+    if (!r) r = allgather_concat(c, sources, (size_t)nin, T->src);
+    if (!r) r = allgather_concat(c, destinations, (size_t)nout, T->dst);
+    if (!r) r = allgather_concat(c, sourceweights ? sourceweights : zin.data(), (size_t)nin, T->srcw);
+    if (!r) r = allgather_concat(c, destweights ? destweights : zout.data(), (size_t)nout, T->dstw);
+    if (r) return r;
+    for (int q = 0; q < c->proc * c->R; q++) { T->in0 += T->indeg[q]; T->out0 += T->outdeg[q]; }
+    *topo = T.release();
+    return MPXA_SUCCESS;
+}
+
+int mpxa_topo_free(mpxa_topo_t *topo) {
+    if (!topo || !*topo) return MPXA_ERR_ARG;
+    delete *topo;
+    *topo = nullptr;
+    return MPXA_SUCCESS;
+}
+
+int mpxa_neighbor_alltoallv_init(const void *s, const int64_t *sc, const int64_t *sd, size_t sb, void *r,
+                                 const int64_t *rc, const int64_t *rd, size_t rb, size_t w, mpxa_topo_t topo,
+                                 const void *info, mpxa_request_t *req) {
+    (void)info;
+    if (!req) return MPXA_ERR_ARG;
+    *req = nullptr;
+    return neighbor_impl(false, s, sc, sd, sb, r, rc, rd, rb, w, nullptr, nullptr, topo, nullptr, req);
+}
+
+int mpxa_neighbor_alltoallv_locality_init(const void *s, const int64_t *sc, const int64_t *sd, size_t sb, void *r,
+                                          const int64_t *rc, const int64_t *rd, size_t rb, size_t w,
+                                          const int64_t *sidx, const int64_t *ridx, mpxa_topo_t topo,
+                                          const void *info, mpxa_request_t *req) {
+    (void)info;
+    if (!req) return MPXA_ERR_ARG;
+    *req = nullptr;
+    return neighbor_impl(true, s, sc, sd, sb, r, rc, rd, rb, w, sidx, ridx, topo, nullptr, req);
+}
+
+int mpxa_neighbor_alltoallv(const void *s, const int64_t *sc, const int64_t *sd, size_t sb, void *r,
+                            const int64_t *rc, const int64_t *rd, size_t rb, size_t w, mpxa_topo_t topo,
+                            mpxa_stream_t st) {
+    return neighbor_impl(false, s, sc, sd, sb, r, rc, rd, rb, w, nullptr, nullptr, topo, S(st), nullptr);
 }
 
 // ---- registry / selector -----------------------------------------------------------------
@@ -1046,12 +1207,13 @@ int mpxa_get_algorithm(mpxa_comm_t c, mpxa_op_t op, size_t bytes, mpxa_algo_t *c
 }
 
 int mpxa_list_algorithms(mpxa_op_t op, mpxa_algo_t *out, int *n) {
-    if (!n || op < 0 || op > 2) return MPXA_ERR_ARG;
+    if (!n || op < 0 || op > 3) return MPXA_ERR_ARG;
     static const mpxa_algo_t a2a[] = {MPXA_ALGO_PAIRWISE, MPXA_ALGO_BRUCK, MPXA_ALGO_HIER};
     static const mpxa_algo_t a2av[] = {MPXA_ALGO_PAIRWISE, MPXA_ALGO_HIER};
     static const mpxa_algo_t ag[] = {MPXA_ALGO_PAIRWISE, MPXA_ALGO_BRUCK, MPXA_ALGO_RING};
-    const mpxa_algo_t *src = op == 0 ? a2a : op == 1 ? a2av : ag;
-    int cnt = op == 1 ? 2 : 3;
+    static const mpxa_algo_t nb[] = {MPXA_ALGO_PAIRWISE, MPXA_ALGO_LOCALITY};
+    const mpxa_algo_t *src = op == 0 ? a2a : op == 1 ? a2av : op == 2 ? ag : nb;
+    int cnt = (op == 1 || op == 3) ? 2 : 3;
     if (out) {
         if (*n < cnt) { *n = cnt; return MPXA_ERR_ARG; }
         for (int i = 0; i < cnt; i++) out[i] = src[i];
@@ -1095,6 +1257,19 @@ int mpxa_plan_build(int op, int algo, int p, int R, int G, int g, int stop_stage
     else if (op == MPXA_OP_ALLGATHER) ok = build_allgather(*P, algo, p, R, G, stop_stage);
     else if (op == MPXA_OP_ALLTOALLV && cnt && sd && rd) ok = build_alltoallv(*P, algo, p, R, G, g, cnt, sd, rd);
     if (!ok) { delete P; return MPXA_ERR_ALGO; }
+    *plan = P;
+    return MPXA_SUCCESS;
+}
+
+int mpxa_plan_build_neighbor(int p, int R, int G, int g, int locality, const int *indeg, const int *src,
+                             const int64_t *rc, const int64_t *rd, const int *outdeg, const int *dst,
+                             const int64_t *sc, const int64_t *sd, const int64_t *send_idx,
+                             const int64_t *recv_idx, void **plan) {
+    if (!plan || !indeg || !outdeg) return MPXA_ERR_ARG;
+    *plan = nullptr;
+    auto P = new Program();
+    int r = build_neighbor(*P, locality != 0, p, R, G, g, indeg, src, rc, rd, outdeg, dst, sc, sd, send_idx, recv_idx);
+    if (r) { delete P; return r; }
     *plan = P;
     return MPXA_SUCCESS;
 }

@@ -7,6 +7,9 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <map>
+
+#include "../../include/mpxa.h"
 
 namespace mpxa {
 
@@ -351,6 +354,185 @@ bool build_alltoallv(Program &P, int algo, int p, int R, int G, int g, const int
         }
     B.end_step();
     return true;
+}
+
+// ---------------------------------------------------------------------------------------
+// f1: persistent neighborhood alltoallv (§2.2)
+// ---------------------------------------------------------------------------------------
+namespace {
+
+struct NbGraph {
+    int p;
+    std::vector<int64_t> ioff, ooff, ie, oe;   // edge offsets per rank; element offsets per edge
+    std::vector<int64_t> match;                // in-edge -> matched global out-edge
+};
+
+// Validates the graph (valid ranks, non-negative counts / displacements, MPI pairing with equal
+// counts, every out-edge paired) and pairs the edges.
+int nb_prepare(NbGraph &N, int p, const int *indeg, const int *src, const int64_t *rc, const int64_t *rd,
+               const int *outdeg, const int *dst, const int64_t *sc, const int64_t *sd) {
+    N.p = p;
+    N.ioff.assign(p + 1, 0);
+    N.ooff.assign(p + 1, 0);
+    for (int r = 0; r < p; r++) {
+        if (indeg[r] < 0 || outdeg[r] < 0) return MPXA_ERR_ARG;
+        N.ioff[r + 1] = N.ioff[r] + indeg[r];
+        N.ooff[r + 1] = N.ooff[r] + outdeg[r];
+    }
+    const int64_t ni = N.ioff[p], no = N.ooff[p];
+    if (ni != no) return MPXA_ERR_MISMATCH;
+    for (int64_t e = 0; e < ni; e++)
+        if (src[e] < 0 || src[e] >= p || rc[e] < 0 || rd[e] < 0) return MPXA_ERR_ARG;
+    for (int64_t e = 0; e < no; e++)
+        if (dst[e] < 0 || dst[e] >= p || sc[e] < 0 || sd[e] < 0) return MPXA_ERR_ARG;
+    N.ie.assign(ni + 1, 0);
+    N.oe.assign(no + 1, 0);
+    for (int64_t e = 0; e < ni; e++) N.ie[e + 1] = N.ie[e] + rc[e];
+    for (int64_t e = 0; e < no; e++) N.oe[e + 1] = N.oe[e] + sc[e];
+    // pair: per (r, q), the k-th out-edge r->q with the k-th in-edge q<-r
+    std::map<std::pair<int, int>, std::vector<int64_t>> outs;
+    for (int r = 0; r < p; r++)
+        for (int64_t e = N.ooff[r]; e < N.ooff[r + 1]; e++) outs[{r, dst[e]}].push_back(e);
+    std::map<std::pair<int, int>, size_t> used;
+    N.match.assign(ni, -1);
+    for (int q = 0; q < p; q++)
+        for (int64_t e = N.ioff[q]; e < N.ioff[q + 1]; e++) {
+            auto key = std::make_pair(src[e], q);
+            size_t k = used[key]++;
+            auto it = outs.find(key);
+            if (it == outs.end() || k >= it->second.size()) return MPXA_ERR_MISMATCH;
+            const int64_t o = it->second[k];
+            if (sc[o] != rc[e]) return MPXA_ERR_MISMATCH;
+            N.match[e] = o;
+        }
+    for (auto &kv : outs)
+        if (used[kv.first] != kv.second.size()) return MPXA_ERR_MISMATCH;
+    return MPXA_SUCCESS;
+}
+
+}  // namespace
+
+int build_neighbor(Program &P, bool locality, int p, int R, int G, int g, const int *indeg, const int *src,
+                   const int64_t *rc, const int64_t *rd, const int *outdeg, const int *dst, const int64_t *sc,
+                   const int64_t *sd, const int64_t *send_idx, const int64_t *recv_idx) {
+    if (!topo_ok(p, R, G)) return MPXA_ERR_TOPOLOGY;
+    NbGraph N;
+    int rcode = nb_prepare(N, p, indeg, src, rc, rd, outdeg, dst, sc, sd);
+    if (rcode) return rcode;
+    const int64_t no = N.ooff[p];
+    if (!locality) {
+        // standard: one move per out-edge with a count, sender side
+        Builder B(P, p, R, G, (int)std::max<int64_t>(1, no));
+        for (int q = 0; q < p; q++)
+            for (int64_t e = N.ioff[q]; e < N.ioff[q + 1]; e++) {
+                const int64_t o = N.match[e];
+                B.move(BK_SEND, src[e], sd[o], BK_RECV, q, rd[e], rc[e], o);
+            }
+        B.end_step();
+        P.work_units = 0;
+        return MPXA_SUCCESS;
+    }
+    // locality-aware three-phase plan over groups of g ranks
+    if (g < 1 || p % g) return MPXA_ERR_TOPOLOGY;
+    if ((N.oe[no] && !send_idx) || (N.ie[N.ioff[p]] && !recv_idx)) return MPXA_ERR_ARG;
+    for (int q = 0; q < p; q++)              // index handshake: received ids = matched sent ids
+        for (int64_t e = N.ioff[q]; e < N.ioff[q + 1]; e++) {
+            const int64_t o = N.match[e];
+            for (int64_t x = 0; x < rc[e]; x++)
+                if (recv_idx[N.ie[e] + x] != send_idx[N.oe[o] + x]) return MPXA_ERR_TOPOLOGY;
+        }
+    auto L = [&](int A, int Bg) { return A * g + (Bg % g); };
+    // per group pair (A,B): unique ids (sorted), the first holder (rank, element offset in its
+    // sendbuf) of each, and every final destination (rank, element offset in its recvbuf)
+    struct Slot { int64_t id; int holder; int64_t hoff; std::vector<std::pair<int, int64_t>> dests; };
+    std::map<std::pair<int, int>, std::vector<Slot>> pairs;
+    std::map<std::pair<int, int>, std::map<int64_t, size_t>> slot_of;
+    for (int r = 0; r < p; r++)
+        for (int64_t o = N.ooff[r]; o < N.ooff[r + 1]; o++) {
+            const int A = r / g, Bg = dst[o] / g;
+            if (A == Bg) continue;
+            auto &ids = slot_of[{A, Bg}];
+            for (int64_t x = 0; x < sc[o]; x++) ids.emplace(send_idx[N.oe[o] + x], 0);
+        }
+    for (auto &kv : slot_of) {               // sorted unique ids -> slot numbers
+        size_t s = 0;
+        auto &vec = pairs[kv.first];
+        for (auto &id : kv.second) { id.second = s++; vec.push_back(Slot{id.first, -1, 0, {}}); }
+    }
+    for (int r = 0; r < p; r++)              // holders: first sender in (rank, edge, element) order
+        for (int64_t o = N.ooff[r]; o < N.ooff[r + 1]; o++) {
+            const int A = r / g, Bg = dst[o] / g;
+            if (A == Bg) continue;
+            auto &vec = pairs[{A, Bg}];
+            auto &ids = slot_of[{A, Bg}];
+            for (int64_t x = 0; x < sc[o]; x++) {
+                Slot &sl = vec[ids[send_idx[N.oe[o] + x]]];
+                if (sl.holder < 0) { sl.holder = r; sl.hoff = sd[o] + x; }
+            }
+        }
+    for (int q = 0; q < p; q++)              // final destinations, receiver element order
+        for (int64_t e = N.ioff[q]; e < N.ioff[q + 1]; e++) {
+            const int A = src[e] / g, Bg = q / g;
+            if (A == Bg) continue;
+            auto &vec = pairs[{A, Bg}];
+            auto &ids = slot_of[{A, Bg}];
+            for (int64_t x = 0; x < rc[e]; x++) vec[ids[recv_idx[N.ie[e] + x]]].dests.push_back({q, rd[e] + x});
+        }
+    // runs: consecutive slots moved as one unit through all three steps -- same holder with
+    // consecutive offsets and the same destination pattern shifted by one element
+    struct Run { int A, Bg; size_t s0, n; };
+    std::vector<Run> runs;
+    for (auto &kv : pairs) {
+        auto &vec = kv.second;
+        size_t s0 = 0;
+        for (size_t s = 1; s <= vec.size(); s++) {
+            bool cont = s < vec.size() && vec[s].holder == vec[s - 1].holder && vec[s].hoff == vec[s - 1].hoff + 1 &&
+                        vec[s].dests.size() == vec[s - 1].dests.size();
+            for (size_t d = 0; cont && d < vec[s].dests.size(); d++)
+                cont = vec[s].dests[d].first == vec[s - 1].dests[d].first &&
+                       vec[s].dests[d].second == vec[s - 1].dests[d].second + 1;
+            if (!cont) { runs.push_back(Run{kv.first.first, kv.first.second, s0, s - s0}); s0 = s; }
+        }
+    }
+    // workspace of each rank: out-aggregates it leads, then in-aggregates it receives
+    std::map<std::pair<int, int>, int64_t> out_base, in_base;
+    std::vector<int64_t> cur(p, 0);
+    for (auto &kv : pairs) { const int x = L(kv.first.first, kv.first.second); out_base[kv.first] = cur[x]; cur[x] += (int64_t)kv.second.size(); }
+    for (auto &kv : pairs) { const int x = L(kv.first.second, kv.first.first); in_base[kv.first] = cur[x]; cur[x] += (int64_t)kv.second.size(); }
+    int64_t work = 0;
+    for (int x = 0; x < p; x++) work = std::max(work, cur[x]);
+    // flows: intra-group edges first, then runs
+    int64_t nintra = 0;
+    for (int r = 0; r < p; r++)
+        for (int64_t o = N.ooff[r]; o < N.ooff[r + 1]; o++) nintra += (r / g == dst[o] / g);
+    Builder B(P, p, R, G, (int)std::max<int64_t>(1, nintra + (int64_t)runs.size()));
+    P.work_units = work;
+    // step 1: intra-group edges directly; one representative of each run to L(A,B)
+    int64_t f = 0;
+    for (int q = 0; q < p; q++)
+        for (int64_t e = N.ioff[q]; e < N.ioff[q + 1]; e++)
+            if (src[e] / g == q / g) B.move(BK_SEND, src[e], sd[N.match[e]], BK_RECV, q, rd[e], rc[e], f++);
+    for (size_t k = 0; k < runs.size(); k++) {
+        const Run &u = runs[k];
+        const Slot &sl = pairs[{u.A, u.Bg}][u.s0];
+        B.move(BK_SEND, sl.holder, sl.hoff, BK_WORK, L(u.A, u.Bg), out_base[{u.A, u.Bg}] + (int64_t)u.s0, (int64_t)u.n,
+               nintra + (int64_t)k);
+    }
+    B.end_step();
+    // step 2: L(A,B) -> L(B,A), each unique id once (one signal per GPU pair per CTA)
+    for (const Run &u : runs)
+        B.move(BK_WORK, L(u.A, u.Bg), out_base[{u.A, u.Bg}] + (int64_t)u.s0, BK_WORK, L(u.Bg, u.A),
+               in_base[{u.A, u.Bg}] + (int64_t)u.s0, (int64_t)u.n);
+    B.end_step();
+    // step 3: fan out to every final (rank, offset)
+    for (const Run &u : runs) {
+        const Slot &sl = pairs[{u.A, u.Bg}][u.s0];
+        for (const auto &d : sl.dests)
+            B.move(BK_WORK, L(u.Bg, u.A), in_base[{u.A, u.Bg}] + (int64_t)u.s0, BK_RECV, d.first, d.second, (int64_t)u.n);
+    }
+    B.end_step();
+    (void)f;
+    return MPXA_SUCCESS;
 }
 
 }  // namespace mpxa

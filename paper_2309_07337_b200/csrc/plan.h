@@ -25,7 +25,7 @@ struct Program {
     int nsteps() const { return steps.empty() ? 0 : (int)steps[0].size(); }
 };
 
-enum Algo { A_DEFAULT = 0, A_PAIRWISE = 1, A_BRUCK = 2, A_HIER = 3, A_RING = 4 };
+enum Algo { A_DEFAULT = 0, A_PAIRWISE = 1, A_BRUCK = 2, A_HIER = 3, A_RING = 4, A_LOCALITY = 5 };
 
 // Uniform ops: units are blocks (count * dtype_size bytes).
 //   stop_stage: -1 complete; >= 0 truncated Bruck ending with a T dump into RECV.
@@ -36,6 +36,15 @@ bool build_allgather(Program &P, int algo, int p, int R, int G, int stop_stage);
 //   rd[j*p+s] = displacement in j's recvbuf of the segment from s.
 bool build_alltoallv(Program &P, int algo, int p, int R, int G, int g, const int64_t *c,
                      const int64_t *sd, const int64_t *rd);
+
+// f1 neighbor alltoallv.  Global graph, rank-major edge lists: indeg[p],
+// src/rc/rd per in-edge; outdeg[p], dst/sc/sd per out-edge (elements).  Edges pair like MPI
+// messages (j-th out-edge r->q with the j-th in-edge q<-r).  locality: groups of g
+// consecutive ranks, send_idx / recv_idx = one global index per element, edge by edge.
+// Returns 0, or an mpxa status (MPXA_ERR_ARG / _MISMATCH / _TOPOLOGY) without building.
+int build_neighbor(Program &P, bool locality, int p, int R, int G, int g, const int *indeg, const int *src,
+                   const int64_t *rc, const int64_t *rd, const int *outdeg, const int *dst, const int64_t *sc,
+                   const int64_t *sd, const int64_t *send_idx, const int64_t *recv_idx);
 
 int ceil_log2(int p);
 

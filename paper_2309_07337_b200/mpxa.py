@@ -19,10 +19,11 @@ LIB_PATH = os.environ.get("MPXA_LIB") or os.path.join(_HERE, "libmpxa.so")   # M
 # ---- constants (mirror include/mpxa.h) ------------------------------------------------
 SUCCESS, ERR_ARG, ERR_ALGO, ERR_LIFECYCLE, ERR_TOPOLOGY, ERR_MISMATCH, ERR_CUDA, ERR_TIMEOUT, \
     ERR_NOMEM, ERR_UNREGISTERED = range(10)
-OP_ALLTOALL, OP_ALLTOALLV, OP_ALLGATHER = 0, 1, 2
-ALGO = {"default": 0, "pairwise": 1, "bruck": 2, "hier": 3, "ring": 4}
+OP_ALLTOALL, OP_ALLTOALLV, OP_ALLGATHER, OP_NEIGHBOR_ALLTOALLV = 0, 1, 2, 3
+ALGO = {"default": 0, "pairwise": 1, "bruck": 2, "hier": 3, "ring": 4, "locality": 5}
 ALGO_NAME = {v: k for k, v in ALGO.items()}
-OPS = {"alltoall": OP_ALLTOALL, "alltoallv": OP_ALLTOALLV, "allgather": OP_ALLGATHER}
+OPS = {"alltoall": OP_ALLTOALL, "alltoallv": OP_ALLTOALLV, "allgather": OP_ALLGATHER,
+       "neighbor_alltoallv": OP_NEIGHBOR_ALLTOALLV}
 
 
 class MpxaError(RuntimeError):
@@ -96,6 +97,13 @@ SIGNATURES = {
     "mpxa_error_string": ([_I], ctypes.c_char_p),
     "mpxa_algo_name": ([_I], ctypes.c_char_p),
     "mpxa_plan_build": ([_I, _I, _I, _I, _I, _I, _I, _P, _P, _P, ctypes.POINTER(_P)], _I),
+    "mpxa_dist_graph_create_adjacent": ([_P, _P, _P, _P, _P, _P, _P, _P, _I, ctypes.POINTER(_P)], _I),
+    "mpxa_topo_free": ([ctypes.POINTER(_P)], _I),
+    "mpxa_neighbor_alltoallv_init": ([_P, _P, _P, _Z, _P, _P, _P, _Z, _Z, _P, _P, ctypes.POINTER(_P)], _I),
+    "mpxa_neighbor_alltoallv_locality_init": ([_P, _P, _P, _Z, _P, _P, _P, _Z, _Z, _P, _P, _P, _P,
+                                               ctypes.POINTER(_P)], _I),
+    "mpxa_neighbor_alltoallv": ([_P, _P, _P, _Z, _P, _P, _P, _Z, _Z, _P, _P], _I),
+    "mpxa_plan_build_neighbor": ([_I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.POINTER(_P)], _I),
     "mpxa_plan_info": ([_P, ctypes.POINTER(PlanInfo)], _I),
     "mpxa_plan_steps": ([_P, _I, _P, ctypes.POINTER(_I)], _I),
     "mpxa_plan_moves": ([_P, _I, _P, ctypes.POINTER(_I)], _I),
@@ -320,6 +328,59 @@ class Comm:
                                        ctypes.byref(h)), "alltoallv_init")
         return Request(self, h.value, (send, recv))
 
+    # ---- neighborhood collectives --------------------------------
+    def dist_graph_create_adjacent(self, sources, destinations, sourceweights=None, destweights=None,
+                                   reorder: int = 0) -> "Topology":
+        """sources / destinations: per local rank, the list of in / out neighbour ranks
+        (MPIX_Dist_graph_create_adjacent).  Collective over the comm's processes."""
+        indeg = np.array([len(x) for x in sources], np.int32)
+        outdeg = np.array([len(x) for x in destinations], np.int32)
+        if len(indeg) != self.R or len(outdeg) != self.R:
+            raise ValueError(f"one neighbour list per local rank expected ({self.R})")
+        src = np.array([v for x in sources for v in x], np.int32)
+        dst = np.array([v for x in destinations for v in x], np.int32)
+        sw = None if sourceweights is None else np.array([v for x in sourceweights for v in x], np.int32)
+        dw = None if destweights is None else np.array([v for x in destweights for v in x], np.int32)
+        h = ctypes.c_void_p()
+        _ck(_lib().mpxa_dist_graph_create_adjacent(
+            self.handle, indeg.ctypes.data, src.ctypes.data if len(src) else None,
+            sw.ctypes.data if sw is not None and len(sw) else None, outdeg.ctypes.data,
+            dst.ctypes.data if len(dst) else None, dw.ctypes.data if dw is not None and len(dw) else None,
+            None, reorder, ctypes.byref(h)), "dist_graph_create_adjacent")
+        return Topology(self, h.value)
+
+    def _nb_args(self, send, sendcounts, sdispls, recv, recvcounts, rdispls, dtype_size):
+        w = send.element_size() if dtype_size is None else dtype_size
+        arrs = [_host_i64(a) for a in (sendcounts, sdispls, recvcounts, rdispls)]
+        sbpr = send.numel() * send.element_size() // self.R
+        rbpr = recv.numel() * recv.element_size() // self.R
+        return w, arrs, sbpr, rbpr
+
+    def neighbor_alltoallv_init(self, topo, send, sendcounts, sdispls, recv, recvcounts, rdispls,
+                                dtype_size: Optional[int] = None, send_indices=None, recv_indices=None) -> Request:
+        """Persistent neighbor alltoallv (counts / displacements: one entry per edge of the
+        local ranks, rank-major); with send_indices / recv_indices (one global index per
+        element) the locality-aware variant."""
+        w, arrs, sbpr, rbpr = self._nb_args(send, sendcounts, sdispls, recv, recvcounts, rdispls, dtype_size)
+        h = ctypes.c_void_p()
+        if send_indices is None:
+            _ck(_lib().mpxa_neighbor_alltoallv_init(
+                _ptr(send), arrs[0][1], arrs[1][1], sbpr, _ptr(recv), arrs[2][1], arrs[3][1], rbpr, w,
+                topo.handle, None, ctypes.byref(h)), "neighbor_alltoallv_init")
+        else:
+            si, sip = _host_i64(send_indices)
+            ri, rip = _host_i64(recv_indices)
+            _ck(_lib().mpxa_neighbor_alltoallv_locality_init(
+                _ptr(send), arrs[0][1], arrs[1][1], sbpr, _ptr(recv), arrs[2][1], arrs[3][1], rbpr, w,
+                sip, rip, topo.handle, None, ctypes.byref(h)), "neighbor_alltoallv_locality_init")
+        return Request(self, h.value, (send, recv, topo))
+
+    def neighbor_alltoallv(self, topo, send, sendcounts, sdispls, recv, recvcounts, rdispls, stream=None,
+                           dtype_size: Optional[int] = None):
+        w, arrs, sbpr, rbpr = self._nb_args(send, sendcounts, sdispls, recv, recvcounts, rdispls, dtype_size)
+        _ck(_lib().mpxa_neighbor_alltoallv(_ptr(send), arrs[0][1], arrs[1][1], sbpr, _ptr(recv), arrs[2][1],
+                                           arrs[3][1], rbpr, w, topo.handle, _stream(stream)), "neighbor_alltoallv")
+
     def finalize(self):
         if self.handle:
             _ck(_lib().mpxa_finalize(self.handle), "finalize")
@@ -329,6 +390,26 @@ class Comm:
         try:
             if self.handle:
                 _lib().mpxa_finalize(self.handle)
+        except Exception:
+            pass
+
+
+class Topology:
+    """MPIX_Dist_graph_create_adjacent result."""
+
+    def __init__(self, comm: Comm, handle: int):
+        self.comm = comm
+        self.handle = ctypes.c_void_p(handle)
+
+    def free(self):
+        if self.handle:
+            h = ctypes.c_void_p(self.handle.value)
+            _ck(_lib().mpxa_topo_free(ctypes.byref(h)), "topo_free")
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.free()
         except Exception:
             pass
 
@@ -374,6 +455,29 @@ class Plan:
         info = PlanInfo()
         _ck(_lib().mpxa_plan_info(h, ctypes.byref(info)), "plan_info")
         self.info = {n: int(getattr(info, n)) for n, _ in PlanInfo._fields_}
+
+    @classmethod
+    def neighbor(cls, gr, R: int, G: int, g: int = 1, locality: bool = False, send_idx=None, recv_idx=None):
+        """Schedule of a neighbor alltoallv over a GLOBAL graph dict (oracle/synth layout)."""
+        self = cls.__new__(cls)
+        p = len(gr["indeg"])
+        i32 = lambda a: np.ascontiguousarray(a, dtype=np.int32)
+        arrs = [i32(gr["indeg"]), i32(gr["src"]), np.ascontiguousarray(gr["rc"], np.int64),
+                np.ascontiguousarray(gr["rd"], np.int64), i32(gr["outdeg"]), i32(gr["dst"]),
+                np.ascontiguousarray(gr["sc"], np.int64), np.ascontiguousarray(gr["sd"], np.int64)]
+        si = np.ascontiguousarray(send_idx, np.int64) if send_idx is not None else None
+        ri = np.ascontiguousarray(recv_idx, np.int64) if recv_idx is not None else None
+        h = ctypes.c_void_p()
+        ptr = lambda a: a.ctypes.data if a is not None and a.size else None
+        _ck(_lib().mpxa_plan_build_neighbor(p, R, G, g, int(locality), *[ptr(a) for a in arrs], ptr(si), ptr(ri),
+                                            ctypes.byref(h)), "plan_build_neighbor")
+        self.h = h
+        self.p, self.R, self.G = p, R, G
+        self._keep = arrs + [si, ri]
+        info = PlanInfo()
+        _ck(_lib().mpxa_plan_info(h, ctypes.byref(info)), "plan_info")
+        self.info = {n: int(getattr(info, n)) for n, _ in PlanInfo._fields_}
+        return self
 
     def steps(self, gpu: int):
         n = ctypes.c_int(0)

@@ -315,3 +315,17 @@ def random_edges(seed, p, max_deg, max_count, idx_space):
             n = int(rng.integers(0, max_count + 1))
             edges.append((r, d, [int(x) for x in rng.integers(0, idx_space, n)]))
     return edges
+
+
+def spmv_edges(seed, p, m, k, deg):
+    """Sparse-matrix halo (the neighbourhood collectives' use case): rank r owns m boundary
+    values (global ids r*m .. r*m+m-1); every rank q needs k of them (sorted, drawn without
+    replacement) from each of `deg` distinct other ranks.  Ranks of one group needing the
+    same value create the duplicates the locality-aware variant removes."""
+    rng = np.random.default_rng(seed)
+    need = {}
+    for q in range(p):
+        owners = rng.choice([r for r in range(p) if r != q], size=min(deg, p - 1), replace=False)
+        for r in owners:
+            need[(int(r), q)] = sorted(int(r) * m + int(x) for x in rng.choice(m, size=min(k, m), replace=False))
+    return [(r, q, need[(r, q)]) for (r, q) in sorted(need)]
