@@ -442,63 +442,92 @@ int build_neighbor(Program &P, bool locality, int p, int R, int G, int g, const 
                 if (recv_idx[N.ie[e] + x] != send_idx[N.oe[o] + x]) return MPXA_ERR_TOPOLOGY;
         }
     auto L = [&](int A, int Bg) { return A * g + (Bg % g); };
+    const int NG = p / g;
     // per group pair (A,B): unique ids (sorted), the first holder (rank, element offset in its
-    // sendbuf) of each, and every final destination (rank, element offset in its recvbuf)
-    struct Slot { int64_t id; int holder; int64_t hoff; std::vector<std::pair<int, int64_t>> dests; };
-    std::map<std::pair<int, int>, std::vector<Slot>> pairs;
-    std::map<std::pair<int, int>, std::map<int64_t, size_t>> slot_of;
-    for (int r = 0; r < p; r++)
-        for (int64_t o = N.ooff[r]; o < N.ooff[r + 1]; o++) {
-            const int A = r / g, Bg = dst[o] / g;
-            if (A == Bg) continue;
-            auto &ids = slot_of[{A, Bg}];
-            for (int64_t x = 0; x < sc[o]; x++) ids.emplace(send_idx[N.oe[o] + x], 0);
-        }
-    for (auto &kv : slot_of) {               // sorted unique ids -> slot numbers
-        size_t s = 0;
-        auto &vec = pairs[kv.first];
-        for (auto &id : kv.second) { id.second = s++; vec.push_back(Slot{id.first, -1, 0, {}}); }
-    }
-    for (int r = 0; r < p; r++)              // holders: first sender in (rank, edge, element) order
-        for (int64_t o = N.ooff[r]; o < N.ooff[r + 1]; o++) {
-            const int A = r / g, Bg = dst[o] / g;
-            if (A == Bg) continue;
-            auto &vec = pairs[{A, Bg}];
-            auto &ids = slot_of[{A, Bg}];
-            for (int64_t x = 0; x < sc[o]; x++) {
-                Slot &sl = vec[ids[send_idx[N.oe[o] + x]]];
-                if (sl.holder < 0) { sl.holder = r; sl.hoff = sd[o] + x; }
+    // sendbuf) of each in (rank, edge, element) order, and every final destination (rank,
+    // element offset in its recvbuf) in receiver element order
+    struct SrcEl { int64_t id, off; int r; };
+    struct DstEl { int64_t slot, off; int q; };
+    struct PairSched {
+        std::vector<int64_t> ids, hoff;
+        std::vector<int> holder;
+        std::vector<DstEl> dests;          // sorted by slot (stable: receiver order inside)
+        std::vector<int64_t> dstart;       // dests of slot s: [dstart[s], dstart[s+1])
+    };
+    std::vector<PairSched> ps((size_t)NG * NG);
+    {
+        std::vector<std::vector<SrcEl>> sends((size_t)NG * NG);
+        for (int r = 0; r < p; r++)
+            for (int64_t o = N.ooff[r]; o < N.ooff[r + 1]; o++) {
+                const int A = r / g, Bg = dst[o] / g;
+                if (A == Bg) continue;
+                auto &v = sends[(size_t)A * NG + Bg];
+                for (int64_t x = 0; x < sc[o]; x++) v.push_back(SrcEl{send_idx[N.oe[o] + x], sd[o] + x, r});
             }
+        for (size_t k = 0; k < sends.size(); k++) {
+            auto &v = sends[k];
+            std::stable_sort(v.begin(), v.end(), [](const SrcEl &x, const SrcEl &y) { return x.id < y.id; });
+            PairSched &P2 = ps[k];
+            for (size_t i = 0; i < v.size(); i++)
+                if (i == 0 || v[i].id != v[i - 1].id) {   // first holder of each id
+                    P2.ids.push_back(v[i].id);
+                    P2.hoff.push_back(v[i].off);
+                    P2.holder.push_back(v[i].r);
+                }
         }
-    for (int q = 0; q < p; q++)              // final destinations, receiver element order
+    }
+    for (int q = 0; q < p; q++)
         for (int64_t e = N.ioff[q]; e < N.ioff[q + 1]; e++) {
             const int A = src[e] / g, Bg = q / g;
             if (A == Bg) continue;
-            auto &vec = pairs[{A, Bg}];
-            auto &ids = slot_of[{A, Bg}];
-            for (int64_t x = 0; x < rc[e]; x++) vec[ids[recv_idx[N.ie[e] + x]]].dests.push_back({q, rd[e] + x});
+            PairSched &P2 = ps[(size_t)A * NG + Bg];
+            for (int64_t x = 0; x < rc[e]; x++) {
+                const int64_t id = recv_idx[N.ie[e] + x];
+                const int64_t slot = std::lower_bound(P2.ids.begin(), P2.ids.end(), id) - P2.ids.begin();
+                P2.dests.push_back(DstEl{slot, rd[e] + x, q});
+            }
         }
+    for (PairSched &P2 : ps) {
+        std::stable_sort(P2.dests.begin(), P2.dests.end(), [](const DstEl &x, const DstEl &y) { return x.slot < y.slot; });
+        P2.dstart.assign(P2.ids.size() + 1, 0);
+        for (const DstEl &d : P2.dests) P2.dstart[(size_t)d.slot + 1]++;
+        for (size_t s2 = 0; s2 < P2.ids.size(); s2++) P2.dstart[s2 + 1] += P2.dstart[s2];
+    }
     // runs: consecutive slots moved as one unit through all three steps -- same holder with
     // consecutive offsets and the same destination pattern shifted by one element
     struct Run { int A, Bg; size_t s0, n; };
     std::vector<Run> runs;
-    for (auto &kv : pairs) {
-        auto &vec = kv.second;
-        size_t s0 = 0;
-        for (size_t s = 1; s <= vec.size(); s++) {
-            bool cont = s < vec.size() && vec[s].holder == vec[s - 1].holder && vec[s].hoff == vec[s - 1].hoff + 1 &&
-                        vec[s].dests.size() == vec[s - 1].dests.size();
-            for (size_t d = 0; cont && d < vec[s].dests.size(); d++)
-                cont = vec[s].dests[d].first == vec[s - 1].dests[d].first &&
-                       vec[s].dests[d].second == vec[s - 1].dests[d].second + 1;
-            if (!cont) { runs.push_back(Run{kv.first.first, kv.first.second, s0, s - s0}); s0 = s; }
+    for (int A = 0; A < NG; A++)
+        for (int Bg = 0; Bg < NG; Bg++) {
+            const PairSched &P2 = ps[(size_t)A * NG + Bg];
+            const size_t n = P2.ids.size();
+            size_t s0 = 0;
+            for (size_t s2 = 1; s2 <= n; s2++) {
+                bool cont = s2 < n && P2.holder[s2] == P2.holder[s2 - 1] && P2.hoff[s2] == P2.hoff[s2 - 1] + 1 &&
+                            P2.dstart[s2 + 1] - P2.dstart[s2] == P2.dstart[s2] - P2.dstart[s2 - 1];
+                for (int64_t d = 0; cont && d < P2.dstart[s2 + 1] - P2.dstart[s2]; d++) {
+                    const DstEl &x = P2.dests[(size_t)(P2.dstart[s2] + d)], &y = P2.dests[(size_t)(P2.dstart[s2 - 1] + d)];
+                    cont = x.q == y.q && x.off == y.off + 1;
+                }
+                if (!cont) { runs.push_back(Run{A, Bg, s0, s2 - s0}); s0 = s2; }
+            }
         }
-    }
     // workspace of each rank: out-aggregates it leads, then in-aggregates it receives
-    std::map<std::pair<int, int>, int64_t> out_base, in_base;
-    std::vector<int64_t> cur(p, 0);
-    for (auto &kv : pairs) { const int x = L(kv.first.first, kv.first.second); out_base[kv.first] = cur[x]; cur[x] += (int64_t)kv.second.size(); }
-    for (auto &kv : pairs) { const int x = L(kv.first.second, kv.first.first); in_base[kv.first] = cur[x]; cur[x] += (int64_t)kv.second.size(); }
+    std::vector<int64_t> out_base((size_t)NG * NG, 0), in_base((size_t)NG * NG, 0), cur(p, 0);
+    for (int A = 0; A < NG; A++)
+        for (int Bg = 0; Bg < NG; Bg++) {
+            const size_t k = (size_t)A * NG + Bg;
+            if (ps[k].ids.empty()) continue;
+            out_base[k] = cur[L(A, Bg)];
+            cur[L(A, Bg)] += (int64_t)ps[k].ids.size();
+        }
+    for (int A = 0; A < NG; A++)
+        for (int Bg = 0; Bg < NG; Bg++) {
+            const size_t k = (size_t)A * NG + Bg;
+            if (ps[k].ids.empty()) continue;
+            in_base[k] = cur[L(Bg, A)];
+            cur[L(Bg, A)] += (int64_t)ps[k].ids.size();
+        }
     int64_t work = 0;
     for (int x = 0; x < p; x++) work = std::max(work, cur[x]);
     // flows: intra-group edges first, then runs
@@ -514,21 +543,25 @@ int build_neighbor(Program &P, bool locality, int p, int R, int G, int g, const 
             if (src[e] / g == q / g) B.move(BK_SEND, src[e], sd[N.match[e]], BK_RECV, q, rd[e], rc[e], f++);
     for (size_t k = 0; k < runs.size(); k++) {
         const Run &u = runs[k];
-        const Slot &sl = pairs[{u.A, u.Bg}][u.s0];
-        B.move(BK_SEND, sl.holder, sl.hoff, BK_WORK, L(u.A, u.Bg), out_base[{u.A, u.Bg}] + (int64_t)u.s0, (int64_t)u.n,
-               nintra + (int64_t)k);
+        const size_t pk = (size_t)u.A * NG + u.Bg;
+        B.move(BK_SEND, ps[pk].holder[u.s0], ps[pk].hoff[u.s0], BK_WORK, L(u.A, u.Bg), out_base[pk] + (int64_t)u.s0,
+               (int64_t)u.n, nintra + (int64_t)k);
     }
     B.end_step();
     // step 2: L(A,B) -> L(B,A), each unique id once (one signal per GPU pair per CTA)
-    for (const Run &u : runs)
-        B.move(BK_WORK, L(u.A, u.Bg), out_base[{u.A, u.Bg}] + (int64_t)u.s0, BK_WORK, L(u.Bg, u.A),
-               in_base[{u.A, u.Bg}] + (int64_t)u.s0, (int64_t)u.n);
+    for (const Run &u : runs) {
+        const size_t pk = (size_t)u.A * NG + u.Bg;
+        B.move(BK_WORK, L(u.A, u.Bg), out_base[pk] + (int64_t)u.s0, BK_WORK, L(u.Bg, u.A), in_base[pk] + (int64_t)u.s0,
+               (int64_t)u.n);
+    }
     B.end_step();
     // step 3: fan out to every final (rank, offset)
     for (const Run &u : runs) {
-        const Slot &sl = pairs[{u.A, u.Bg}][u.s0];
-        for (const auto &d : sl.dests)
-            B.move(BK_WORK, L(u.Bg, u.A), in_base[{u.A, u.Bg}] + (int64_t)u.s0, BK_RECV, d.first, d.second, (int64_t)u.n);
+        const size_t pk = (size_t)u.A * NG + u.Bg;
+        const PairSched &P2 = ps[pk];
+        for (int64_t d = P2.dstart[u.s0]; d < P2.dstart[u.s0 + 1]; d++)
+            B.move(BK_WORK, L(u.Bg, u.A), in_base[pk] + (int64_t)u.s0, BK_RECV, P2.dests[(size_t)d].q,
+                   P2.dests[(size_t)d].off, (int64_t)u.n);
     }
     B.end_step();
     (void)f;

@@ -317,15 +317,21 @@ def random_edges(seed, p, max_deg, max_count, idx_space):
     return edges
 
 
-def spmv_edges(seed, p, m, k, deg):
+def spmv_edges(seed, p, m, k, deg, contiguous=False):
     """Sparse-matrix halo (the neighbourhood collectives' use case): rank r owns m boundary
-    values (global ids r*m .. r*m+m-1); every rank q needs k of them (sorted, drawn without
-    replacement) from each of `deg` distinct other ranks.  Ranks of one group needing the
-    same value create the duplicates the locality-aware variant removes."""
+    values (global ids r*m .. r*m+m-1); every rank q needs k of them from each of `deg`
+    distinct other ranks -- a random subset (sorted, without replacement), or with
+    contiguous=True a random window of k consecutive ids (banded / reordered matrices).
+    Ranks of one group needing the same value create the duplicates the locality-aware
+    variant removes."""
     rng = np.random.default_rng(seed)
     need = {}
     for q in range(p):
         owners = rng.choice([r for r in range(p) if r != q], size=min(deg, p - 1), replace=False)
         for r in owners:
-            need[(int(r), q)] = sorted(int(r) * m + int(x) for x in rng.choice(m, size=min(k, m), replace=False))
+            if contiguous:
+                s0 = int(rng.integers(0, m - min(k, m) + 1))
+                need[(int(r), q)] = list(range(int(r) * m + s0, int(r) * m + s0 + min(k, m)))
+            else:
+                need[(int(r), q)] = sorted(int(r) * m + int(x) for x in rng.choice(m, size=min(k, m), replace=False))
     return [(r, q, need[(r, q)]) for (r, q) in sorted(need)]
