@@ -786,20 +786,22 @@ int orc_neighbor_locality(int p, int g, size_t w, const int *indeg, const int *s
                 if (dst[e] / g == B) for (int64_t x = 0; x < sc[e]; x++) ids[n++] = send_idx[oe[e] + x];
             }
             int64_t m = uniq_sorted(ids, n, uq);
-            for (int64_t u = 0; u < m; u++) {           /* value: first element with that index */
-                const unsigned char *v = NULL;
-                for (int k = 0; k < outdeg[r] && !v; k++) {
-                    int64_t e = ooff[r] + k;
-                    if (dst[e] / g != B) continue;
-                    for (int64_t x = 0; x < sc[e]; x++)
-                        if (send_idx[oe[e] + x] == uq[u]) {
-                            v = send + (size_t)r * sstride + (size_t)(sd[e] + x) * w;
-                            break;
-                        }
+            /* value of each unique index: its first element in (edge, element) order */
+            int64_t *first = (int64_t *)malloc(sizeof(int64_t) * (size_t)(m ? m : 1));
+            for (int64_t u = 0; u < m; u++) first[u] = -1;
+            for (int k = 0; k < outdeg[r]; k++) {
+                int64_t e = ooff[r] + k;
+                if (dst[e] / g != B) continue;
+                for (int64_t x = 0; x < sc[e]; x++) {
+                    int64_t u = find_sorted(uq, m, send_idx[oe[e] + x]);
+                    if (first[u] < 0) first[u] = sd[e] + x;        /* element offset in send_r */
                 }
-                memcpy(buf + rec * u, &uq[u], sizeof(int64_t));
-                memcpy(buf + rec * u + sizeof(int64_t), v, w);
             }
+            for (int64_t u = 0; u < m; u++) {
+                memcpy(buf + rec * u, &uq[u], sizeof(int64_t));
+                memcpy(buf + rec * u + sizeof(int64_t), send + (size_t)r * sstride + (size_t)first[u] * w, w);
+            }
+            free(first);
             if (m) err = tp_send(&t, r, A * g + (B % g), NB_TAG_FWD + B, buf, rec * (size_t)m);
         }
     }
@@ -815,14 +817,17 @@ int orc_neighbor_locality(int p, int g, size_t w, const int *indeg, const int *s
                 if (got == -1) continue;                       /* that sender had nothing for B */
                 n += got / (int64_t)rec;
             }
-            /* merge: records sorted by index, first occurrence kept */
+            /* merge: one record per index (the first received), index ascending */
             for (int64_t i = 0; i < n; i++) memcpy(&ids[i], agg + rec * i, sizeof(int64_t));
             int64_t m = uniq_sorted(ids, n, uq);
-            for (int64_t u = 0; u < m; u++) {
-                int64_t i = 0;
-                while (memcmp(agg + rec * i, &uq[u], sizeof(int64_t))) i++;
-                memcpy(buf + rec * u, agg + rec * i, rec);
+            int64_t *first = (int64_t *)malloc(sizeof(int64_t) * (size_t)(m ? m : 1));
+            for (int64_t u = 0; u < m; u++) first[u] = -1;
+            for (int64_t i = 0; i < n; i++) {
+                int64_t u = find_sorted(uq, m, ids[i]);
+                if (first[u] < 0) first[u] = i;
             }
+            for (int64_t u = 0; u < m; u++) memcpy(buf + rec * u, agg + rec * first[u], rec);
+            free(first);
             if (m) {
                 err = tp_send(&t, lead, peer, NB_TAG_EXCH + A, buf, rec * (size_t)m);
                 if (inter_values) *inter_values += m;
