@@ -62,6 +62,8 @@ def lib():
             "orc_neighbor_definition": [I, Z, P, P, P, P, P, Z, P, P, P, P, P, Z],
             "orc_neighbor_standard": [I, Z, P, P, P, P, P, Z, P, P, P, P, P, Z, S],
             "orc_neighbor_locality": [I, I, Z, P, P, P, P, P, P, Z, P, P, P, P, P, P, Z, S, P],
+            "orc_part_arrived": [I, Z, I, Z, P, P],
+            "orc_part_cycle": [I, Z, I, Z, P, P, P, P, S],
         }
         for name, args in sig.items():
             f = getattr(_lib, name)
@@ -254,3 +256,28 @@ def neighbor(send, recv_init, w, gr, variant="standard", g=0, send_idx=None, rec
     d = st.as_dict()
     d["inter_values"] = int(iv.value)
     return recv, d
+
+
+# ---- f3: partitioned point-to-point ----------------
+
+def part_arrived(n_s, bs, n_r, br, delivered):
+    """Parrived of every receiver partition, given which sender partitions were delivered."""
+    d = np.ascontiguousarray(np.asarray(delivered, dtype=np.uint8))
+    out = np.zeros(n_r, np.uint8)
+    _check(lib().orc_part_arrived(n_s, bs, n_r, br, _ptr(d), _ptr(out)), "part_arrived")
+    return out.astype(bool)
+
+
+def part_cycle(send, n_s, n_r, order):
+    """One partitioned cycle with Pready in `order`: returns (recv bytes, trace (n_s, n_r) of
+    Parrived after each delivery, stats)."""
+    send = np.ascontiguousarray(send, dtype=np.uint8)
+    total = send.size
+    bs, br = total // n_s, total // n_r
+    recv = np.zeros_like(send)
+    order = np.ascontiguousarray(order, dtype=np.int32)
+    trace = np.zeros((n_s, n_r), np.uint8)
+    st = Stats()
+    _check(lib().orc_part_cycle(n_s, bs, n_r, br, _ptr(send), _ptr(recv), _ptr(order), _ptr(trace),
+                                ctypes.byref(st)), "part_cycle")
+    return recv, trace.astype(bool), st.as_dict()

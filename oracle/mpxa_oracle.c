@@ -894,3 +894,52 @@ out_noT:
     free(ids); free(uq); free(buf); free(agg); free(oe); free(ie); free(ioff); free(ooff);
     return err;
 }
+
+/* ==================================================================================== */
+/* f3: partitioned point-to-point (§2.3).              */
+/* A channel moves one message of n_s * bs bytes; the sender marks n_s equal partitions   */
+/* ready (Pready), the receiver sees n_r equal partitions of br bytes (same total) and   */
+/* asks whether each has arrived (Parrived): "partitions of the same or different sizes  */
+/* can be accessed as complete, prior to completion of the whole message". */
+/* ==================================================================================== */
+
+/* Parrived by byte coverage ("arrived(i) iff the byte interval of receiver
+ * partition i is fully covered by delivered fragments"): brute force over bytes. */
+int orc_part_arrived(int n_s, size_t bs, int n_r, size_t br, const unsigned char *delivered,
+                     unsigned char *arrived) {
+    if (n_s < 1 || n_r < 1 || (size_t)n_s * bs != (size_t)n_r * br) return -1;
+    for (int j = 0; j < n_r; j++) {
+        int ok = 1;
+        for (size_t b = (size_t)j * br; b < (size_t)(j + 1) * br && ok; b++)
+            if (!delivered[b / (bs ? bs : 1)]) ok = 0;
+        arrived[j] = (unsigned char)ok;
+    }
+    return 0;
+}
+
+/* One cycle through the transport: the sender readies partitions in `order` (a permutation
+ * of 0..n_s-1); each Pready sends one fragment (partition bytes; tag = partition index)
+ * that the receiver integrates on arrival (one fragment per READY
+ * partition).  After the k-th delivery, arrived_trace[k*n_r + j] = Parrived(j).  Returns
+ * the receiver buffer in recv; stats count fragments (messages). */
+int orc_part_cycle(int n_s, size_t bs, int n_r, size_t br, const unsigned char *send, unsigned char *recv,
+                   const int *order, unsigned char *arrived_trace, orc_stats *st) {
+    if (n_s < 1 || n_r < 1 || (size_t)n_s * bs != (size_t)n_r * br) return -1;
+    transport_t t;
+    if (tp_init(&t, 2, st)) return -1;
+    unsigned char *delivered = (unsigned char *)calloc((size_t)n_s, 1);
+    int err = 0;
+    for (int k = 0; k < n_s && !err; k++) {
+        int i = order[k];
+        if (i < 0 || i >= n_s || delivered[i]) { err = -1; break; }
+        err = tp_send(&t, 0, 1, i, send + (size_t)i * bs, bs);            /* Pready(i) */
+        if (!err && tp_recv(&t, 1, 0, i, recv + (size_t)i * bs, bs) != (int64_t)bs) err = -2;
+        delivered[i] = 1;
+        if (!err) err = orc_part_arrived(n_s, bs, n_r, br, delivered, arrived_trace + (size_t)k * n_r);
+    }
+    if (st) st->rounds = n_s;
+    if (!err && tp_pending(&t)) err = -2;
+    tp_free(&t);
+    free(delivered);
+    return err;
+}
