@@ -241,6 +241,48 @@ int mpxa_neighbor_alltoallv(const void *sendbuf, const int64_t *sendcounts, cons
                             const int64_t *rdispls, size_t recv_bytes_per_rank, size_t dtype_size,
                             mpxa_topo_t topo, mpxa_stream_t stream);
 
+/* ---- partitioned point-to-point (§2.3) -------------- */
+/* MPI-4 partitioned communication on the device: one match at initialization, per-partition
+ * Pready from the host (stream-ordered) or from a producer kernel (include/mpxa_device.cuh),
+ * Parrived as a host query or as a stream-ordered device wait.  No progress thread: each
+ * readied partition is copied straight into the matched receiver's buffer by the GPU (peer
+ * stores over NVLink when the receiver is on another GPU) and published with a per-partition
+ * release flag tagged with the cycle number.
+ *
+ * psend_init: local rank `rank` (hosted by this process) will send `partitions` equal
+ * partitions of `count` elements of dtype_size bytes from buf to rank `dest` with `tag`.
+ * precv_init: local rank `rank` receives from `source` into buf, split into `partitions`
+ * equal partitions (may differ from the sender's: "partitions of the same or different
+ * sizes"; the total bytes must match).  Both return an unmatched request. */
+int mpxa_psend_init(const void *buf, int partitions, size_t count, size_t dtype_size, int rank, int dest,
+                    int tag, mpxa_comm_t comm, const void *info, mpxa_request_t *req);
+int mpxa_precv_init(void *buf, int partitions, size_t count, size_t dtype_size, int rank, int source,
+                    int tag, mpxa_comm_t comm, const void *info, mpxa_request_t *req);
+/* The single match ("establishes a single match between a sender and receiver at
+ * initialization"): collective over the comm's processes; pairs every unmatched send with the
+ * first unmatched receive of the same (source, destination, tag), in creation order, maps the
+ * receiver's buffer and flags for the sender, and readies both ends for mpxa_start.  Errors:
+ * MPXA_ERR_MISMATCH (an unmatched end, or total bytes differ) -- no request is matched then. */
+int mpxa_pmatch(mpxa_comm_t comm);
+/* Mark sender partition(s) ready (Pready / Pready_range): enqueued on `stream` after the work
+ * that produced them; the copy to the receiver starts when the stream reaches it ("early-bird
+ * communication").  Request must be ACTIVE (after mpxa_start); each partition at
+ * most once per cycle (else MPXA_ERR_ARG). */
+int mpxa_pready(mpxa_request_t req, int partition, mpxa_stream_t stream);
+int mpxa_pready_range(mpxa_request_t req, int partition_lo, int partition_hi, mpxa_stream_t stream);
+/* Host query (Parrived): *flag = 1 iff receiver partition `partition` of the current cycle has
+ * fully arrived (byte coverage by delivered sender partitions).  Non-blocking with respect to
+ * the channel; reads the flags with a private stream. */
+int mpxa_parrived(mpxa_request_t req, int partition, int *flag);
+/* Device-side Parrived: work enqueued on `stream` after this call starts only once receiver
+ * partitions [partition_lo, partition_hi) have arrived (consumers overlap the transfer). */
+int mpxa_parrived_wait(mpxa_request_t req, int partition_lo, int partition_hi, mpxa_stream_t stream);
+/* Device handle of an ACTIVE matched send request for mpxa_dev_pready (include/mpxa_device.cuh). */
+int mpxa_psend_device(mpxa_request_t req, void *handle_out, size_t handle_bytes);
+/* mpxa_start / mpxa_wait / mpxa_request_free apply: start begins a cycle on that end (the
+ * receiver's start also clears the sender to write); wait enqueues, on `stream`, the wait for
+ * every partition of the cycle (sender: delivered; receiver: arrived). */
+
 /* ---- variant registry and selector --------------------- */
 int mpxa_set_algorithm(mpxa_comm_t comm, mpxa_op_t op, mpxa_algo_t algo); /* DEFAULT = selector */
 int mpxa_get_algorithm(mpxa_comm_t comm, mpxa_op_t op, size_t bytes, mpxa_algo_t *chosen);

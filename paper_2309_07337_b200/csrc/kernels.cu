@@ -16,6 +16,7 @@
 #include <stdint.h>
 
 #include "mpxa_internal.h"
+#include "../../include/mpxa_device.cuh"
 
 namespace mpxa {
 
@@ -1260,6 +1261,81 @@ cudaError_t launch_exec(const ExecParams &P, int nC, int nG, bool cooperative, b
     if (e != cudaSuccess) return e;
     const size_t smem = (size_t)P.stages * P.chunk;
     return launch_kernel(mpxa_exec_kernel, P, dim3(nC, nG), dim3(kThreads), smem, cooperative, pdl, stream);
+}
+
+// ------------------------------------------------------------------------------------
+// f3: partitioned point-to-point.  Cycle counters and flags live in the
+// comm's partition heap; the sender's partitions go straight into the receiver's buffer.
+// ------------------------------------------------------------------------------------
+__global__ void part_start_send(unsigned long long *scycle) {
+    if (threadIdx.x == 0) *scycle += 1ull;
+}
+
+// receiver enters the next cycle: everything stream-ordered before it (its consumers of the
+// previous cycle) is done, so the sender may overwrite the buffer -> clear-to-send
+__global__ void part_start_recv(unsigned long long *rcycle, unsigned long long *cts_remote) {
+    if (threadIdx.x == 0) {
+        const unsigned long long c = *rcycle + 1ull;
+        *rcycle = c;
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(cts_remote), "l"(c) : "memory");
+    }
+}
+
+// host-enqueued Pready of sender partitions [p0, p0 + gridDim.x / nct): nct CTAs per partition
+__global__ void __launch_bounds__(256) part_pready(mpxa_psend_dev_t ch, int p0, unsigned long long chunk,
+                                                   unsigned int nct) {
+    const int i = p0 + (int)(blockIdx.x / nct);
+    const unsigned long long k = blockIdx.x % nct;
+    const unsigned long long lo = k * chunk;
+    const unsigned long long hi = lo + chunk < ch.part_bytes ? lo + chunk : ch.part_bytes;
+    mpxa_dev_pready_part(&ch, i, lo, hi, nct);
+}
+
+// stream-ordered Parrived / completion: block until flags[lo, hi) >= *cycle (one CTA)
+__global__ void part_wait_flags(const unsigned long long *flags, int lo, int hi, const unsigned long long *cycle,
+                                int *err, long long timeout_ns) {
+    __shared__ unsigned long long want;
+    if (threadIdx.x == 0) want = *(volatile const unsigned long long *)cycle;
+    __syncthreads();
+    for (int i = lo + (int)threadIdx.x; i < hi; i += blockDim.x) {
+        unsigned long long t0 = 0;
+        int it = 0;
+        while (mpxa_dev_ld_acquire(flags + i) < want) {
+            if (++it > 32) {
+                __nanosleep(256);
+                if (!t0) t0 = mpxa_dev_now();
+                else if ((long long)(mpxa_dev_now() - t0) > timeout_ns) { atomicExch(err, 1); break; }
+            }
+        }
+    }
+}
+
+cudaError_t launch_part_start(bool sender, unsigned long long *cycle, unsigned long long *cts_remote,
+                              cudaStream_t stream) {
+    if (sender) part_start_send<<<1, 32, 0, stream>>>(cycle);
+    else part_start_recv<<<1, 32, 0, stream>>>(cycle, cts_remote);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_part_pready(const mpxa_psend_dev_t &ch, int p0, int np, cudaStream_t stream) {
+    // enough CTAs per partition to stream it (256 KiB each), at most one wave per partition
+    const unsigned long long chunk = 256ull << 10;
+    unsigned long long nct = (ch.part_bytes + chunk - 1) / chunk;
+    if (nct < 1) nct = 1;
+    if (nct > 148) nct = 148;
+    const unsigned long long per = (ch.part_bytes + nct - 1) / nct;
+    const unsigned long long ch16 = (per + 15) & ~15ull;
+    nct = ch16 ? (ch.part_bytes + ch16 - 1) / ch16 : 1;
+    if (nct < 1) nct = 1;
+    part_pready<<<(unsigned)(np * nct), 256, 0, stream>>>(ch, p0, ch16 ? ch16 : 1, (unsigned)nct);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_part_wait(const unsigned long long *flags, int lo, int hi, const unsigned long long *cycle,
+                             int *err, long long timeout_ns, cudaStream_t stream) {
+    part_wait_flags<<<1, 256, 0, stream>>>(flags, lo, hi, cycle, err, timeout_ns);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_counts(const int64_t *sc, int64_t *rc, int64_t *rd, int p, int r0, int nr,

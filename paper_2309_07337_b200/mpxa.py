@@ -103,6 +103,14 @@ SIGNATURES = {
     "mpxa_neighbor_alltoallv_locality_init": ([_P, _P, _P, _Z, _P, _P, _P, _Z, _Z, _P, _P, _P, _P,
                                                ctypes.POINTER(_P)], _I),
     "mpxa_neighbor_alltoallv": ([_P, _P, _P, _Z, _P, _P, _P, _Z, _Z, _P, _P], _I),
+    "mpxa_psend_init": ([_P, _I, _Z, _Z, _I, _I, _I, _P, _P, ctypes.POINTER(_P)], _I),
+    "mpxa_precv_init": ([_P, _I, _Z, _Z, _I, _I, _I, _P, _P, ctypes.POINTER(_P)], _I),
+    "mpxa_pmatch": ([_P], _I),
+    "mpxa_pready": ([_P, _I, _P], _I),
+    "mpxa_pready_range": ([_P, _I, _I, _P], _I),
+    "mpxa_parrived": ([_P, _I, ctypes.POINTER(_I)], _I),
+    "mpxa_parrived_wait": ([_P, _I, _I, _P], _I),
+    "mpxa_psend_device": ([_P, _P, _Z], _I),
     "mpxa_plan_build_neighbor": ([_I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.POINTER(_P)], _I),
     "mpxa_plan_info": ([_P, ctypes.POINTER(PlanInfo)], _I),
     "mpxa_plan_steps": ([_P, _I, _P, ctypes.POINTER(_I)], _I),
@@ -381,6 +389,29 @@ class Comm:
         _ck(_lib().mpxa_neighbor_alltoallv(_ptr(send), arrs[0][1], arrs[1][1], sbpr, _ptr(recv), arrs[2][1],
                                            arrs[3][1], rbpr, w, topo.handle, _stream(stream)), "neighbor_alltoallv")
 
+    # ---- partitioned point-to-point ----------------------------------
+    def psend_init(self, buf, partitions: int, rank: int, dest: int, tag: int = 0,
+                   count: Optional[int] = None) -> "PRequest":
+        """Partitioned send of `buf` (all of it, or `count` elements per partition) from local
+        rank `rank` to `dest`; matched later by pmatch()."""
+        count = buf.numel() // partitions if count is None else count
+        h = ctypes.c_void_p()
+        _ck(_lib().mpxa_psend_init(_ptr(buf), partitions, count, buf.element_size(), rank, dest, tag, self.handle,
+                                   None, ctypes.byref(h)), "psend_init")
+        return PRequest(self, h.value, buf, partitions, True)
+
+    def precv_init(self, buf, partitions: int, rank: int, source: int, tag: int = 0,
+                   count: Optional[int] = None) -> "PRequest":
+        count = buf.numel() // partitions if count is None else count
+        h = ctypes.c_void_p()
+        _ck(_lib().mpxa_precv_init(_ptr(buf), partitions, count, buf.element_size(), rank, source, tag, self.handle,
+                                   None, ctypes.byref(h)), "precv_init")
+        return PRequest(self, h.value, buf, partitions, False)
+
+    def pmatch(self):
+        """The single match of every pending partitioned end (collective)."""
+        _ck(_lib().mpxa_pmatch(self.handle), "pmatch")
+
     def finalize(self):
         if self.handle:
             _ck(_lib().mpxa_finalize(self.handle), "finalize")
@@ -392,6 +423,34 @@ class Comm:
                 _lib().mpxa_finalize(self.handle)
         except Exception:
             pass
+
+
+class PRequest(Request):
+    """One end of a partitioned channel (MPI-4 Psend_init / Precv_init)."""
+
+    def __init__(self, comm, handle, buf, partitions, sender):
+        super().__init__(comm, handle, buf)
+        self.partitions = partitions
+        self.sender = sender
+
+    def pready(self, lo: int, hi: Optional[int] = None, stream=None):
+        hi = lo + 1 if hi is None else hi
+        _ck(_lib().mpxa_pready_range(self.handle, lo, hi, _stream(stream)), "pready")
+
+    def parrived(self, j: int) -> bool:
+        f = ctypes.c_int()
+        _ck(_lib().mpxa_parrived(self.handle, j, ctypes.byref(f)), "parrived")
+        return bool(f.value)
+
+    def parrived_wait(self, lo: int, hi: Optional[int] = None, stream=None):
+        hi = lo + 1 if hi is None else hi
+        _ck(_lib().mpxa_parrived_wait(self.handle, lo, hi, _stream(stream)), "parrived_wait")
+
+    def device_handle(self) -> bytes:
+        """Bytes of the mpxa_psend_dev_t for mpxa_dev_pready in a user kernel."""
+        buf = (ctypes.c_char * 128)()
+        _ck(_lib().mpxa_psend_device(self.handle, buf, 128), "psend_device")
+        return bytes(buf)
 
 
 class Topology:

@@ -18,6 +18,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def header_symbols():
     syms = set()
     for h in os.listdir(os.path.join(ROOT, "include")):
+        if not h.endswith(".h"):        # C-ABI headers only (mpxa_device.cuh is device code)
+            continue
         txt = open(os.path.join(ROOT, "include", h)).read()
         txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
         for m in re.finditer(r"\b(mpxa_\w+)\s*\(", txt):
