@@ -419,6 +419,32 @@ def configs_on_one_gpu(torch, reps=20):
     trip = np.stack([si[cross], e_src[cross], e_dst[cross]], 1)
     out["inter_group_values"] = {"standard": int(cross.sum()), "locality_g2": int(len(np.unique(trip, axis=0)))}
     res["f1_neighbor_alltoallv_spmv_halo_p8"] = out
+
+    # ---- f3: partitioned channel rank 0 -> rank 1 on this GPU: a whole
+    #      cycle (both starts, Pready of every partition, both waits), CUDA-graph timed ----
+    out = {}
+    c = Comm(ranks_per_proc=2, device=torch.cuda.current_device())
+    for nbytes, n_s, n_r in ((4096, 1, 1), (1 << 20, 4, 2), (256 << 20, 16, 4)):
+        sb = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device=dev)
+        rb = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+        ps = c.psend_init(sb, n_s, 0, 1)
+        pr = c.precv_init(rb, n_r, 1, 0)
+        c.pmatch()
+
+        def cycle():
+            pr.start(gstream); ps.start(gstream)
+            ps.pready(0, n_s, stream=gstream)
+            ps.wait(gstream); pr.wait(gstream)
+        cycle()
+        torch.cuda.synchronize()
+        ok = bool(torch.equal(rb, sb))
+        us = 1e3 * time_graph(cycle, 10 if nbytes > (64 << 20) else 50, gstream)
+        out[f"{nbytes}B_{n_s}to{n_r}"] = {"us_per_cycle": round(us, 2), "verified": ok,
+                                          "GBps": round(nbytes / us / 1e3, 1)}
+        ps.free(); pr.free()
+        del sb, rb
+    c.finalize()
+    res["f3_partitioned_p2p_1gpu"] = out
     return res
 
 

@@ -95,7 +95,14 @@ __device__ __forceinline__ void mpxa_dev_pready_part(const mpxa_psend_dev_t *ch,
     if ((((uintptr_t)(s + lo) | (uintptr_t)(d + lo) | n) & 15) == 0) {
         const uint4 *s4 = (const uint4 *)(s + lo);
         uint4 *d4 = (uint4 *)(d + lo);
-        for (unsigned long long k = threadIdx.x; k < n / 16; k += blockDim.x) d4[k] = __ldcg(s4 + k);
+        const unsigned long long nv = n / 16, bd = blockDim.x;
+        unsigned long long k = threadIdx.x;
+        for (; k + 3 * bd < nv; k += 4 * bd) {      /* four 16-B loads in flight per thread */
+            const uint4 a = __ldcg(s4 + k), b = __ldcg(s4 + k + bd), c = __ldcg(s4 + k + 2 * bd),
+                        e = __ldcg(s4 + k + 3 * bd);
+            d4[k] = a; d4[k + bd] = b; d4[k + 2 * bd] = c; d4[k + 3 * bd] = e;
+        }
+        for (; k < nv; k += bd) d4[k] = __ldcg(s4 + k);
     } else {
         for (unsigned long long k = lo + threadIdx.x; k < hi; k += blockDim.x) d[k] = (unsigned char)__ldcg(s + k);
     }

@@ -63,6 +63,7 @@ def lib():
             "orc_neighbor_standard": [I, Z, P, P, P, P, P, Z, P, P, P, P, P, Z, S],
             "orc_neighbor_locality": [I, I, Z, P, P, P, P, P, P, Z, P, P, P, P, P, P, Z, S, P],
             "orc_part_arrived": [I, Z, I, Z, P, P],
+            "orc_allgather_hier": [I, I, Z, P, P, S],
             "orc_part_cycle": [I, Z, I, Z, P, P, P, P, S],
         }
         for name, args in sig.items():
@@ -148,7 +149,7 @@ def alltoall(send: np.ndarray, variant: str = "pairwise", g: int = 0, stop_stage
     return recv, T, st.as_dict()
 
 
-def allgather(send: np.ndarray, variant: str = "bruck", stop_stage: int = -1, ppn: int = 0):
+def allgather(send: np.ndarray, variant: str = "bruck", stop_stage: int = -1, ppn: int = 0, g: int = 0):
     """send (p, blk) -> (recv (p, p*blk), T or None, stats)."""
     send = _u8(send)
     p, blk = send.shape
@@ -163,6 +164,9 @@ def allgather(send: np.ndarray, variant: str = "bruck", stop_stage: int = -1, pp
         rc = L.orc_allgather_ring(p, blk, _ptr(send), _ptr(recv), ctypes.byref(st))
     elif variant in ("direct", "pairwise"):
         rc = L.orc_allgather_direct(p, blk, _ptr(send), _ptr(recv), ctypes.byref(st))
+    elif variant == "hier":
+        st.ppn = g
+        rc = L.orc_allgather_hier(p, g, blk, _ptr(send), _ptr(recv), ctypes.byref(st))
     else:
         raise ValueError(variant)
     _check(rc, "allgather/" + variant)

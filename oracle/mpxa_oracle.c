@@ -943,3 +943,48 @@ int orc_part_cycle(int n_s, size_t bs, int n_r, size_t br, const unsigned char *
     free(delivered);
     return err;
 }
+
+/* f2(i): hierarchical allgather ("intra-node gather to leader, inter-node bruck
+ * among leaders, intra-node broadcast"; the locality-aware allgather family PAPER.md:173 cites).
+ * Nodes are groups of g consecutive ranks with leader A*g.  (1) every rank sends its block to
+ * its leader; (2) the G leaders run the Bruck allgather (C.4 item 3) on their node aggregates
+ * of g blocks; (3) every leader sends the full p-block result to each of its other ranks. */
+int orc_allgather_hier(int p, int g, size_t blk, const unsigned char *send, unsigned char *recv, orc_stats *st) {
+    if (p < 1 || g < 1 || p % g) return -1;
+    const int G = p / g, K = ceil_log2(G);
+    const size_t agg = (size_t)g * blk;
+    transport_t t;
+    if (tp_init(&t, p, st)) return -1;
+    unsigned char *T = (unsigned char *)calloc((size_t)G * (size_t)p * blk + 1, 1);   /* per leader: G aggregates */
+    unsigned char *buf = (unsigned char *)malloc((size_t)p * blk + 1);
+    int err = 0;
+    /* (1) gather to the node leader (self included, as a loopback message) */
+    for (int r = 0; r < p && !err; r++) err = tp_send(&t, r, (r / g) * g, 1, send + (size_t)r * blk, blk);
+    for (int A = 0; A < G && !err; A++)
+        for (int s = 0; s < g && !err; s++)
+            if (tp_recv(&t, A * g, A * g + s, 1, T + (size_t)A * p * blk + (size_t)s * blk, blk) != (int64_t)blk) err = -2;
+    if (st) st->rounds++;
+    /* (2) Bruck among leaders on aggregates: T_A[0] = own aggregate; round k sends T_A[0..n_k)
+     * to leader (A - 2^k) mod G, stored at T[2^k ..]; final aggregate j = T_A[(j - A) mod G] */
+    for (int k = 0; k < K && !err; k++) {
+        const int d = 1 << k, nk = (d < G - d) ? d : G - d;
+        for (int A = 0; A < G && !err; A++)
+            err = tp_send(&t, A * g, imod(A - d, G) * g, 2 + k, T + (size_t)A * p * blk, (size_t)nk * agg);
+        for (int A = 0; A < G && !err; A++)
+            if (tp_recv(&t, A * g, imod(A + d, G) * g, 2 + k, T + (size_t)A * p * blk + (size_t)d * agg,
+                        (size_t)nk * agg) != (int64_t)((size_t)nk * agg)) err = -2;
+        if (st) st->rounds++;
+    }
+    /* (3) leader unrotates into rank order and broadcasts to its node */
+    for (int A = 0; A < G && !err; A++) {
+        for (int j = 0; j < G; j++) memcpy(buf + (size_t)j * agg, T + (size_t)A * p * blk + (size_t)imod(j - A, G) * agg, agg);
+        for (int s = 0; s < g && !err; s++) err = tp_send(&t, A * g, A * g + s, 64, buf, (size_t)p * blk);
+    }
+    for (int r = 0; r < p && !err; r++)
+        if (tp_recv(&t, r, (r / g) * g, 64, recv + (size_t)r * p * blk, (size_t)p * blk) != (int64_t)((size_t)p * blk)) err = -2;
+    if (st) st->rounds++;
+    if (!err && tp_pending(&t)) err = -2;
+    tp_free(&t);
+    free(T); free(buf);
+    return err;
+}

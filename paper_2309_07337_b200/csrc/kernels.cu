@@ -1319,11 +1319,12 @@ cudaError_t launch_part_start(bool sender, unsigned long long *cycle, unsigned l
 }
 
 cudaError_t launch_part_pready(const mpxa_psend_dev_t &ch, int p0, int np, cudaStream_t stream) {
-    // enough CTAs per partition to stream it (256 KiB each), at most one wave per partition
-    const unsigned long long chunk = 256ull << 10;
+    // CTAs per partition: 32 KiB pieces, up to ~4 waves of the machine over the whole call
+    const unsigned long long chunk = 32ull << 10;
     unsigned long long nct = (ch.part_bytes + chunk - 1) / chunk;
+    const unsigned long long cap = np > 0 ? (4ull * 148 + np - 1) / np : 1;
+    if (nct > cap) nct = cap;
     if (nct < 1) nct = 1;
-    if (nct > 148) nct = 148;
     const unsigned long long per = (ch.part_bytes + nct - 1) / nct;
     const unsigned long long ch16 = (per + 15) & ~15ull;
     nct = ch16 ? (ch.part_bytes + ch16 - 1) / ch16 : 1;

@@ -336,3 +336,18 @@ def test_bad_arguments_rejected():
         oracle.alltoallv(send, bad, sd, rc, rd, 8, recv0)
     with pytest.raises(RuntimeError):
         oracle.alltoallv(send, sc, sd, rc, rd, 8, recv0, "hier", g=3)   # p % g != 0
+
+
+# ---- f2(i): hierarchical allgather ----------------------------------------
+
+@pytest.mark.parametrize("p,g", [(1, 1), (4, 2), (8, 2), (8, 4), (6, 3), (16, 4), (12, 4), (5, 5), (6, 1)])
+def test_allgather_hier_concatenation_and_counts(p, g):
+    """Equals numpy concatenation; inter-node messages = G * ceil(log2 G) (Bruck among the G
+    leaders, SPEC.md:236's count per rank) -- every other message stays inside a node."""
+    send = synth.allgather_sendbuf(p, p, 7)
+    recv, _, st = oracle.allgather(send, "hier", g=g)
+    assert np.array_equal(recv, np.tile(send.reshape(1, -1), (p, 1)))
+    G = p // g
+    K = 0 if G == 1 else int(np.ceil(np.log2(G)))
+    assert st["inter_msgs"] == G * K
+    assert st["intra_msgs"] == p + p                 # gather (incl. leader loopback) + broadcast
