@@ -445,6 +445,28 @@ def configs_on_one_gpu(torch, reps=20):
         del sb, rb
     c.finalize()
     res["f3_partitioned_p2p_1gpu"] = out
+
+    # ---- f2(i): locality-aware allgather, p=32 ranks as 8 emulated GPUs x 4 ranks: direct
+    #      fan-out (every block to all 28 remote ranks) vs hier (once per remote GPU, then
+    #      replicated on the GPU).  Cross-GPU bytes per GPU: R*(p-R)*b vs R*(G-1)*b ----
+    p, G = 32, 8
+    R = p // G
+    c = Comm(ranks_per_proc=p, device=torch.cuda.current_device(), emulate_gpus=G)
+    out = {"cross_gpu_bytes_per_gpu_per_block_byte": {"pairwise": R * (p - R), "hier": R * (G - 1)}}
+    for b in (1024, 65536, 1 << 20):
+        send_t = torch.randint(0, 256, (p, b), dtype=torch.uint8, device=dev)
+        recv_t = torch.empty((p, p * b), dtype=torch.uint8, device=dev)
+        want = oracle.allgather_definition(send_t.cpu().numpy())
+        row = {}
+        for algo in ("pairwise", "hier"):
+            c.allgather(send_t, recv_t, algo=algo, stream=gstream)
+            torch.cuda.synchronize()
+            ok = bool(np.array_equal(recv_t.cpu().numpy(), want))
+            us = 1e3 * time_graph(lambda: c.allgather(send_t, recv_t, algo=algo, stream=gstream), 10, gstream)
+            row[algo] = {"us": round(us, 2), "verified": ok}
+        out[f"{b}B"] = row
+    c.finalize()
+    res["f2_allgather_p32_8_emulated_gpus"] = out
     return res
 
 

@@ -80,7 +80,7 @@ typedef enum {
     MPXA_ALGO_DEFAULT = 0,   /* selector decides (mpxa_get_algorithm)                    */
     MPXA_ALGO_PAIRWISE = 1,  /* alltoall, alltoallv, allgather                            */
     MPXA_ALGO_BRUCK = 2,     /* alltoall, allgather                                       */
-    MPXA_ALGO_HIER = 3,      /* alltoall, alltoallv (groups of group_size ranks)          */
+    MPXA_ALGO_HIER = 3,      /* alltoall, alltoallv, allgather (groups of group_size ranks) */
     MPXA_ALGO_RING = 4,      /* allgather                                                 */
     MPXA_ALGO_LOCALITY = 5   /* neighbor alltoallv with global-index dedup    */
 } mpxa_algo_t;

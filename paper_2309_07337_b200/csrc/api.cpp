@@ -349,7 +349,7 @@ int default_algo(mpxa_comm_t c, int op, size_t bytes) {
 bool algo_valid(int op, int algo) {
     if (op == MPXA_OP_ALLTOALL) return algo == A_PAIRWISE || algo == A_BRUCK || algo == A_HIER;
     if (op == MPXA_OP_ALLTOALLV) return algo == A_PAIRWISE || algo == A_HIER;
-    if (op == MPXA_OP_ALLGATHER) return algo == A_PAIRWISE || algo == A_BRUCK || algo == A_RING;
+    if (op == MPXA_OP_ALLGATHER) return algo == A_PAIRWISE || algo == A_BRUCK || algo == A_RING || algo == A_HIER;
     return false;
 }
 
@@ -375,7 +375,7 @@ int cached_uniform(mpxa_comm_t c, int op, int algo, int stage, std::shared_ptr<D
     if (it != c->cache.end()) { out = it->second; return MPXA_SUCCESS; }
     Program P;
     bool ok = op == MPXA_OP_ALLTOALL ? build_alltoall(P, algo, c->p, c->Rg, c->G, c->g, stage)
-                                     : build_allgather(P, algo, c->p, c->Rg, c->G, stage);
+                                     : build_allgather(P, algo, c->p, c->Rg, c->G, stage, c->g);
     if (!ok) return MPXA_ERR_ALGO;
     int rc = upload_program(P, out);
     if (rc) return rc;
@@ -818,8 +818,7 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     c->R = a->ranks_per_proc;
     c->device = a->device;
     c->p = c->nprocs * c->R;
-    c->g = a->group_size > 0 ? a->group_size : (c->R > 1 ? c->R : 1);
-    if (c->p % c->g) return MPXA_ERR_TOPOLOGY;
+
     c->boot = a->bootstrap_allgather;
     c->ctx = a->ctx;
     c->timeout_s = a->timeout_s > 0 ? a->timeout_s : 60.0;
@@ -832,6 +831,9 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
         c->G = c->nprocs;
         c->Rg = c->R;
     }
+    // default group: the ranks of one (possibly emulated) GPU (Q6)
+    c->g = a->group_size > 0 ? a->group_size : c->Rg;
+    if (c->p % c->g) return MPXA_ERR_TOPOLOGY;
     if (c->G > kMaxGpus || c->p > 65535) return MPXA_ERR_TOPOLOGY;
     CK(cudaSetDevice(c->device));
     cudaDeviceProp prop;
@@ -1501,10 +1503,10 @@ int mpxa_list_algorithms(mpxa_op_t op, mpxa_algo_t *out, int *n) {
     if (!n || op < 0 || op > 3) return MPXA_ERR_ARG;
     static const mpxa_algo_t a2a[] = {MPXA_ALGO_PAIRWISE, MPXA_ALGO_BRUCK, MPXA_ALGO_HIER};
     static const mpxa_algo_t a2av[] = {MPXA_ALGO_PAIRWISE, MPXA_ALGO_HIER};
-    static const mpxa_algo_t ag[] = {MPXA_ALGO_PAIRWISE, MPXA_ALGO_BRUCK, MPXA_ALGO_RING};
+    static const mpxa_algo_t ag[] = {MPXA_ALGO_PAIRWISE, MPXA_ALGO_BRUCK, MPXA_ALGO_RING, MPXA_ALGO_HIER};
     static const mpxa_algo_t nb[] = {MPXA_ALGO_PAIRWISE, MPXA_ALGO_LOCALITY};
     const mpxa_algo_t *src = op == 0 ? a2a : op == 1 ? a2av : op == 2 ? ag : nb;
-    int cnt = (op == 1 || op == 3) ? 2 : 3;
+    int cnt = (op == 1 || op == 3) ? 2 : op == 2 ? 4 : 3;
     if (out) {
         if (*n < cnt) { *n = cnt; return MPXA_ERR_ARG; }
         for (int i = 0; i < cnt; i++) out[i] = src[i];
@@ -1545,7 +1547,7 @@ int mpxa_plan_build(int op, int algo, int p, int R, int G, int g, int stop_stage
     auto P = new Program();
     bool ok = false;
     if (op == MPXA_OP_ALLTOALL) ok = build_alltoall(*P, algo, p, R, G, g, stop_stage);
-    else if (op == MPXA_OP_ALLGATHER) ok = build_allgather(*P, algo, p, R, G, stop_stage);
+    else if (op == MPXA_OP_ALLGATHER) ok = build_allgather(*P, algo, p, R, G, stop_stage, g);
     else if (op == MPXA_OP_ALLTOALLV && cnt && sd && rd) ok = build_alltoallv(*P, algo, p, R, G, g, cnt, sd, rd);
     if (!ok) { delete P; return MPXA_ERR_ALGO; }
     *plan = P;

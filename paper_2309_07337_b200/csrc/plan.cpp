@@ -196,7 +196,7 @@ bool build_alltoall(Program &P, int algo, int p, int R, int G, int g, int stop_s
 // ---------------------------------------------------------------------------------------
 // allgather
 // ---------------------------------------------------------------------------------------
-bool build_allgather(Program &P, int algo, int p, int R, int G, int stop_stage) {
+bool build_allgather(Program &P, int algo, int p, int R, int G, int stop_stage, int gsize) {
     if (!topo_ok(p, R, G)) return false;
     Builder B(P, p, R, G, p);
     if (algo == A_PAIRWISE) {
@@ -224,6 +224,36 @@ bool build_allgather(Program &P, int algo, int p, int R, int G, int stop_stage) 
             }
             B.end_step();
         }
+        return true;
+    }
+    if (algo == A_HIER) {
+        // f2(i) locality-aware allgather over groups of g ranks (default: the ranks of one
+        // GPU): every block crosses each group boundary ONCE -- step 1 sends it to the ranks of
+        // its own group and to one receiver in each remote group B, rank B*g + (A mod g)
+        // (SPEC.md:161's leader rotation), straight into that rank's recvbuf; step 2 that
+        // receiver replicates it to the other ranks of B.  (SPEC.md:233 gathers to one leader
+        // and runs Bruck among leaders; on NVSwitch every group is one hop away, so the inter-
+        // group step is a direct exchange -- same result.)
+        const int g = gsize;
+        if (g < 1 || p % g) return false;
+        const int NG = p / g;
+        for (int r = 0; r < p; r++) {
+            const int A = r / g;
+            for (int t = 0; t < g; t++) B.move(BK_SEND, r, 0, BK_RECV, A * g + t, r, 1, r);
+            for (int Bg = 0; Bg < NG; Bg++)
+                if (Bg != A) B.move(BK_SEND, r, 0, BK_RECV, Bg * g + (A % g), r, 1, r);
+        }
+        B.end_step();
+        for (int r = 0; r < p; r++) {
+            const int A = r / g;
+            for (int Bg = 0; Bg < NG; Bg++) {
+                if (Bg == A) continue;
+                const int lead = Bg * g + (A % g);
+                for (int t = 0; t < g; t++)
+                    if (Bg * g + t != lead) B.move(BK_RECV, lead, r, BK_RECV, Bg * g + t, r, 1);
+            }
+        }
+        B.end_step();
         return true;
     }
     if (algo == A_BRUCK) {

@@ -30,7 +30,7 @@ enum Algo { A_DEFAULT = 0, A_PAIRWISE = 1, A_BRUCK = 2, A_HIER = 3, A_RING = 4, 
 // Uniform ops: units are blocks (count * dtype_size bytes).
 //   stop_stage: -1 complete; >= 0 truncated Bruck ending with a T dump into RECV.
 bool build_alltoall(Program &P, int algo, int p, int R, int G, int g, int stop_stage);
-bool build_allgather(Program &P, int algo, int p, int R, int G, int stop_stage);
+bool build_allgather(Program &P, int algo, int p, int R, int G, int stop_stage, int g = 1);
 // v-op: units are elements.  c, sd, rd are FULL p x p matrices:
 //   c[s*p+j]  = elements rank s sends to j, sd[s*p+j] its displacement in s's sendbuf,
 //   rd[j*p+s] = displacement in j's recvbuf of the segment from s.

@@ -166,11 +166,16 @@ def test_allgather_all_variants(p):
         want = oracle.allgather_definition(send)
         for G in topologies(p):
             c = comm(p, G)
-            for algo in ("pairwise", "bruck", "ring"):
+            for algo in ("pairwise", "bruck", "ring", "hier"):
                 d_send = dev(send)
                 d_recv = torch.full((p, p * b), 0x5A, dtype=torch.uint8, device=DEV)
                 c.allgather(d_send, d_recv, algo=algo)
                 assert np.array_equal(host(d_recv), want), (p, b, G, algo)
+            if p % 2 == 0 and b in (7, 4096, 1 << 20):          # locality-aware groups of 2 ranks
+                c2 = comm(p, G, 2)
+                d_recv = torch.full((p, p * b), 0x5A, dtype=torch.uint8, device=DEV)
+                c2.allgather(dev(send), d_recv, algo="hier")
+                assert np.array_equal(host(d_recv), want), (p, b, G, "hier g=2")
 
 
 # ------------------------------------------------------------------ Bruck intermediate states

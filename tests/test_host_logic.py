@@ -42,7 +42,7 @@ def test_error_strings_and_registry():
         assert lib.mpxa_error_string(s)
     assert list_algorithms("alltoall") == ["pairwise", "bruck", "hier"]
     assert list_algorithms("alltoallv") == ["pairwise", "hier"]
-    assert list_algorithms("allgather") == ["pairwise", "bruck", "ring"]
+    assert list_algorithms("allgather") == ["pairwise", "bruck", "ring", "hier"]
     assert lib.mpxa_algo_name(2) == b"bruck"
 
 
