@@ -64,6 +64,7 @@ def lib():
             "orc_neighbor_locality": [I, I, Z, P, P, P, P, P, P, Z, P, P, P, P, P, P, Z, S, P],
             "orc_part_arrived": [I, Z, I, Z, P, P],
             "orc_allgather_hier": [I, I, Z, P, P, S],
+            "orc_alltoallv_bruck": [I, Z, P, Z, P, P, P, Z, P, P, S],
             "orc_part_cycle": [I, Z, I, Z, P, P, P, P, S],
         }
         for name, args in sig.items():
@@ -187,6 +188,8 @@ def alltoallv(send, sc, sd, rc, rd, w, recv_init, variant: str = "pairwise", g: 
     elif variant == "hier":
         st.ppn = g
         r = L.orc_alltoallv_hier(p, g, w, *args, ctypes.byref(st))
+    elif variant == "bruck":
+        r = L.orc_alltoallv_bruck(p, w, *args, ctypes.byref(st))
     else:
         raise ValueError(variant)
     _check(r, "alltoallv/" + variant)

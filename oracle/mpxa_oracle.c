@@ -988,3 +988,75 @@ int orc_allgather_hier(int p, int g, size_t blk, const unsigned char *send, unsi
     free(T); free(buf);
     return err;
 }
+
+/* f2(iii) / north_star "Bruck ... pack/unpack for ... v-variants": Bruck alltoallv.  The
+ * paper is silent; this follows C.4 item 2 with variable blocks: R1 T_r[i] =
+ * the segment send_r sends to (r+i) mod p; round k packs the blocks with bit k of i set, in
+ * increasing i, each preceded by an 8-byte length header (SPEC.md:258's in-band headers), to
+ * (r+2^k) mod p, which unpacks them into the same indices; R3 recv_r[rd_r[j]] = T_r[(r-j)
+ * mod p].  Messages per rank = ceil(log2 p), as for the uniform Bruck. */
+int orc_alltoallv_bruck(int p, size_t w, const unsigned char *send, size_t sstride, const int64_t *sc,
+                        const int64_t *sd, unsigned char *recv, size_t rstride, const int64_t *rc,
+                        const int64_t *rd, orc_stats *st) {
+    if (!v_args_ok(p, w, sstride, sc, sd, rstride, rc, rd)) return -1;
+    unsigned char **T = (unsigned char **)calloc((size_t)p * p, sizeof(unsigned char *));
+    size_t *Tn = (size_t *)calloc((size_t)p * p, sizeof(size_t));
+    size_t cap = 8 * (size_t)p;
+    for (int r = 0; r < p; r++)
+        for (int j = 0; j < p; j++) cap += (size_t)sc[r * p + j] * w;
+    unsigned char *pack = (unsigned char *)malloc(cap + 1);
+    transport_t t;
+    if (!T || !Tn || !pack || tp_init(&t, p, st)) { free(T); free(Tn); free(pack); return -1; }
+    int err = 0;
+    for (int r = 0; r < p; r++)                     /* R1 */
+        for (int i = 0; i < p; i++) {
+            int j = imod(r + i, p);
+            size_t n = (size_t)sc[r * p + j] * w;
+            T[r * p + i] = (unsigned char *)malloc(n + 1);
+            Tn[r * p + i] = n;
+            if (n) memcpy(T[r * p + i], send + (size_t)r * sstride + (size_t)sd[r * p + j] * w, n);
+        }
+    const int K = ceil_log2(p);
+    for (int k = 0; k < K && !err; k++) {
+        const int d = 1 << k;
+        for (int r = 0; r < p && !err; r++) {      /* pack: [len][bytes] per block with bit k */
+            size_t n = 0;
+            for (int i = 0; i < p; i++)
+                if ((i >> k) & 1) {
+                    uint64_t len = Tn[r * p + i];
+                    memcpy(pack + n, &len, 8);
+                    if (len) memcpy(pack + n + 8, T[r * p + i], len);
+                    n += 8 + len;
+                }
+            err = tp_send(&t, r, imod(r + d, p), k, pack, n);
+        }
+        for (int r = 0; r < p && !err; r++) {      /* unpack into the same indices */
+            int64_t n = tp_recv(&t, r, imod(r - d, p), k, pack, cap);
+            if (n < 0) { err = -2; break; }
+            size_t o = 0;
+            for (int i = 0; i < p && !err; i++)
+                if ((i >> k) & 1) {
+                    uint64_t len;
+                    memcpy(&len, pack + o, 8);
+                    free(T[r * p + i]);
+                    T[r * p + i] = (unsigned char *)malloc(len + 1);
+                    Tn[r * p + i] = len;
+                    if (len) memcpy(T[r * p + i], pack + o + 8, len);
+                    o += 8 + len;
+                }
+            if (o != (size_t)n) err = -2;
+        }
+        if (st) st->rounds++;
+    }
+    for (int r = 0; r < p && !err; r++)            /* R3 */
+        for (int j = 0; j < p; j++) {
+            const size_t n = Tn[r * p + imod(r - j, p)];
+            if (n != (size_t)rc[r * p + j] * w) { err = -2; break; }
+            if (n) memcpy(recv + (size_t)r * rstride + (size_t)rd[r * p + j] * w, T[r * p + imod(r - j, p)], n);
+        }
+    if (!err && tp_pending(&t)) err = -2;
+    tp_free(&t);
+    for (int i = 0; i < p * p; i++) free(T[i]);
+    free(T); free(Tn); free(pack);
+    return err;
+}

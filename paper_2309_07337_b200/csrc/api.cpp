@@ -174,6 +174,7 @@ struct mpxa_comm_s {
     bool pdl = true;                          // MPXA_NO_PDL=1: launches without programmatic serialization
     bool dyn = true;                          // MPXA_NO_DYN=1: static slices only (no work queue)
     int dyn_pieces = (int)kDynPiecesPerCta;   // MPXA_DYN_PIECES: queue pieces per CTA (tuning)
+    uint64_t dyn_min_total = kDynMinTotal;    // MPXA_DYN_MIN: smallest busiest-GPU volume (tuning)
 
     SymRegion *sym_local = nullptr;            // G regions when emulated, else 1
     SymRegion *sym_map[kMaxGpus] = {};
@@ -516,7 +517,7 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
         if (c->dyn && dp.nsteps == 1 && dp.max_gpu_moves <= kMoveTile && dp.max_gpu_bytes_units > 0) {
             const uint64_t total = (uint64_t)dp.max_gpu_bytes_units * unit;
             const uint64_t L = (uint64_t)dp.host.max_move * unit;
-            if (total >= kDynMinTotal && L >= kDynMinMove) {
+            if (total >= c->dyn_min_total && L >= kDynMinMove) {
                 // the mid TMA ring at 2 CTAs / SM: twice the producers and LSU warps of the
                 // big ring (the LSU queue needs the warps; the TMA queue is indifferent).  The
                 // grid depends on the program only, so processes pair CTA flag slots 1:1.
@@ -857,6 +858,7 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     if (const char *e = getenv("MPXA_NO_PDL")) c->pdl = atoi(e) == 0;
     if (const char *e = getenv("MPXA_NO_DYN")) c->dyn = atoi(e) == 0;
     if (const char *e = getenv("MPXA_DYN_PIECES")) c->dyn_pieces = std::max(1, atoi(e));
+    if (const char *e = getenv("MPXA_DYN_MIN")) c->dyn_min_total = strtoull(e, nullptr, 10);
     CK(cudaHostAlloc((void **)&c->err_host, sizeof(int32_t), cudaHostAllocMapped));
     *c->err_host = 0;
     CK(cudaHostGetDevicePointer((void **)&c->err_dev, c->err_host, 0));

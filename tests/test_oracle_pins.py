@@ -116,7 +116,7 @@ def _check_v_labels(out, c, rd, w=1, canary=0xA5):
 @pytest.mark.parametrize("p", [1, 2, 3])
 def test_alltoallv_every_count_matrix_0_to_2(p):
     """Every count matrix with entries in {0,1,2} (p <= 3: 1, 16... 19683 instances)."""
-    variants = [("pairwise", 0)] + [("hier", g) for g in range(1, p + 1) if p % g == 0]
+    variants = [("pairwise", 0), ("bruck", 0)] + [("hier", g) for g in range(1, p + 1) if p % g == 0]
     for flat in itertools.product(range(3), repeat=p * p):
         c = np.array(flat, dtype=np.int64).reshape(p, p)
         send, sc, sd, rc, rd, recv0 = _v_instance_from_counts(c)
@@ -143,6 +143,7 @@ def test_alltoallv_seeded_instances_int64_labels(p):
         recv0 = np.full((p, Rcap), 0xA5, dtype=np.uint8)
         outs = [oracle.alltoallv_definition(send, sc, sd, rc, rd, 8, recv0)]
         outs.append(oracle.alltoallv(send, sc, sd, rc, rd, 8, recv0, "pairwise")[0])
+        outs.append(oracle.alltoallv(send, sc, sd, rc, rd, 8, recv0, "bruck")[0])
         for g in (2, 4):
             if p % g == 0:
                 outs.append(oracle.alltoallv(send, sc, sd, rc, rd, 8, recv0, "hier", g=g)[0])
@@ -351,3 +352,14 @@ def test_allgather_hier_concatenation_and_counts(p, g):
     K = 0 if G == 1 else int(np.ceil(np.log2(G)))
     assert st["inter_msgs"] == G * K
     assert st["intra_msgs"] == p + p                 # gather (incl. leader loopback) + broadcast
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 5, 8, 13])
+def test_alltoallv_bruck_message_counts(p):
+    """Bruck-v keeps Bruck's message count: ceil(log2 p) messages per rank."""
+    c = synth.cfg4_counts(p, p, 40)
+    send, sc, sd, rc, rd, S, Rcap = synth.alltoallv_buffers(p, c, elem=8)
+    out, st = oracle.alltoallv(send, sc, sd, rc, rd, 8, np.zeros((p, Rcap), np.uint8), "bruck")
+    K = 0 if p == 1 else int(np.ceil(np.log2(p)))
+    assert st["msgs"] == p * K and st["max_msgs_per_rank"] == K
+    assert np.array_equal(out, oracle.alltoallv_definition(send, sc, sd, rc, rd, 8, np.zeros((p, Rcap), np.uint8)))
