@@ -79,7 +79,7 @@ typedef enum { MPXA_OP_ALLTOALL = 0, MPXA_OP_ALLTOALLV = 1, MPXA_OP_ALLGATHER = 
 typedef enum {
     MPXA_ALGO_DEFAULT = 0,   /* selector decides (mpxa_get_algorithm)                    */
     MPXA_ALGO_PAIRWISE = 1,  /* alltoall, alltoallv, allgather                            */
-    MPXA_ALGO_BRUCK = 2,     /* alltoall, allgather                                       */
+    MPXA_ALGO_BRUCK = 2,     /* alltoall, allgather, alltoallv (variable blocks)          */
     MPXA_ALGO_HIER = 3,      /* alltoall, alltoallv, allgather (groups of group_size ranks) */
     MPXA_ALGO_RING = 4,      /* allgather                                                 */
     MPXA_ALGO_LOCALITY = 5   /* neighbor alltoallv with global-index dedup    */

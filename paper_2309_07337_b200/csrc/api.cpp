@@ -349,7 +349,7 @@ int default_algo(mpxa_comm_t c, int op, size_t bytes) {
 
 bool algo_valid(int op, int algo) {
     if (op == MPXA_OP_ALLTOALL) return algo == A_PAIRWISE || algo == A_BRUCK || algo == A_HIER;
-    if (op == MPXA_OP_ALLTOALLV) return algo == A_PAIRWISE || algo == A_HIER;
+    if (op == MPXA_OP_ALLTOALLV) return algo == A_PAIRWISE || algo == A_HIER || algo == A_BRUCK;
     if (op == MPXA_OP_ALLGATHER) return algo == A_PAIRWISE || algo == A_BRUCK || algo == A_RING || algo == A_HIER;
     return false;
 }
@@ -1504,11 +1504,11 @@ int mpxa_get_algorithm(mpxa_comm_t c, mpxa_op_t op, size_t bytes, mpxa_algo_t *c
 int mpxa_list_algorithms(mpxa_op_t op, mpxa_algo_t *out, int *n) {
     if (!n || op < 0 || op > 3) return MPXA_ERR_ARG;
     static const mpxa_algo_t a2a[] = {MPXA_ALGO_PAIRWISE, MPXA_ALGO_BRUCK, MPXA_ALGO_HIER};
-    static const mpxa_algo_t a2av[] = {MPXA_ALGO_PAIRWISE, MPXA_ALGO_HIER};
+    static const mpxa_algo_t a2av[] = {MPXA_ALGO_PAIRWISE, MPXA_ALGO_HIER, MPXA_ALGO_BRUCK};
     static const mpxa_algo_t ag[] = {MPXA_ALGO_PAIRWISE, MPXA_ALGO_BRUCK, MPXA_ALGO_RING, MPXA_ALGO_HIER};
     static const mpxa_algo_t nb[] = {MPXA_ALGO_PAIRWISE, MPXA_ALGO_LOCALITY};
     const mpxa_algo_t *src = op == 0 ? a2a : op == 1 ? a2av : op == 2 ? ag : nb;
-    int cnt = (op == 1 || op == 3) ? 2 : op == 2 ? 4 : 3;
+    int cnt = op == 3 ? 2 : op == 2 ? 4 : 3;
     if (out) {
         if (*n < cnt) { *n = cnt; return MPXA_ERR_ARG; }
         for (int i = 0; i < cnt; i++) out[i] = src[i];

@@ -304,6 +304,54 @@ bool build_alltoallv(Program &P, int algo, int p, int R, int G, int g, const int
         P.work_units = 0;
         return true;
     }
+    if (algo == A_BRUCK) {
+        // f2(iii) Bruck alltoallv (north_star "Bruck ... pack/unpack for ... v-variants"; paper
+        // silent): A4-A6 with per-rank variable blocks.  T_r[i] starts as the
+        // segment r sends to (r+i) mod p; round k moves the blocks with bit k of i to (r+2^k)
+        // mod p, landing in that rank's round-k area (zero-copy receive, as for alltoall);
+        // finally recv_r[rd_r[j]] = T_r[(r-j) mod p].  Areas are sized per rank.
+        Builder B(P, p, R, G, p * p);
+        const int K = ceil_log2(p);
+        std::vector<std::vector<int64_t>> loc(p, std::vector<int64_t>(p)), len(p, std::vector<int64_t>(p));
+        std::vector<int64_t> cur(p, 0);
+        for (int r = 0; r < p; r++)                          // A4 rotation into the rank's T area
+            for (int i = 0; i < p; i++) {
+                const int j = imod(r + i, p);
+                loc[r][i] = cur[r];
+                len[r][i] = C(r, j);
+                B.move(BK_SEND, r, SD(r, j), BK_WORK, r, cur[r], C(r, j), (int64_t)r * p + j);
+                cur[r] += C(r, j);
+            }
+        B.end_step();
+        for (int k = 0; k < K; k++) {                        // A5 rounds
+            const int d = 1 << k;
+            std::vector<std::vector<int64_t>> nloc = loc, nlen = len;
+            for (int r = 0; r < p; r++) {
+                const int to = imod(r + d, p);
+                for (int i = 0; i < p; i++)
+                    if ((i >> k) & 1) {
+                        B.move(BK_WORK, r, loc[r][i], BK_WORK, to, cur[to], len[r][i]);
+                        nloc[to][i] = cur[to];
+                        nlen[to][i] = len[r][i];
+                        cur[to] += len[r][i];
+                    }
+            }
+            B.end_step();
+            loc.swap(nloc);
+            len.swap(nlen);
+        }
+        for (int r = 0; r < p; r++)                          // A6 inverse rotation
+            for (int j = 0; j < p; j++) {
+                const int i = imod(r - j, p);
+                if (len[r][i] != C(j, r)) return false;      // (counts consistent by construction)
+                B.move(BK_WORK, r, loc[r][i], BK_RECV, r, RD(r, j), len[r][i]);
+            }
+        B.end_step();
+        int64_t work = 0;
+        for (int r = 0; r < p; r++) work = std::max(work, cur[r]);
+        P.work_units = work;
+        return true;
+    }
     if (algo != A_HIER) return false;
     if (g < 1 || p % g) return false;
     // A8: groups of g consecutive ranks, leader

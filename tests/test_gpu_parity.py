@@ -212,7 +212,7 @@ def test_cfg4_alltoallv(mean, packed):
         recv0 = np.full((p, Rcap), 0xA5, dtype=np.uint8)
         want = oracle.alltoallv_definition(send, sc, sd, rc, rd, 8, recv0)
         for G in (0, 2, 8):
-            for algo, g in (("pairwise", 2), ("hier", 2), ("hier", 4)):
+            for algo, g in (("pairwise", 2), ("hier", 2), ("hier", 4), ("bruck", 2)):
                 c = comm(p, G, g)
                 d_send = dev(send.view(np.int64))
                 d_recv = dev(recv0.view(np.int64))
@@ -247,9 +247,10 @@ def test_alltoallv_large_misaligned(dyn, monkeypatch):
         for off in (0, 1, 8):           # shift the whole send buffer: more alignment classes
             d_send = torch.zeros(p * S + 16, dtype=torch.uint8, device=DEV)
             d_send[off:off + p * S] = dev(send.reshape(-1))
-            d_recv = dev(recv0)
-            c.alltoallv(d_send[off:off + p * S].view(p, S), sc, sd, d_recv, rc, rd)
-            assert np.array_equal(host(d_recv), want), (G, off, dyn)
+            for algo in ("pairwise", "bruck"):
+                d_recv = dev(recv0)
+                c.alltoallv(d_send[off:off + p * S].view(p, S), sc, sd, d_recv, rc, rd, algo=algo)
+                assert np.array_equal(host(d_recv), want), (G, off, dyn, algo)
         c.finalize()
 
 
@@ -276,7 +277,7 @@ def test_persistent_alltoallv_100_cycles():
     c4 = synth.cfg4_counts(0, p, 4096)
     for G in (0, 8):
         c = comm(p, G, 2)
-        for algo in ("pairwise", "hier"):
+        for algo in ("pairwise", "hier", "bruck"):
             send, sc, sd, rc, rd, S, Rcap = synth.alltoallv_buffers(0, c4, elem=8)
             d_send = dev(send.view(np.int64))
             d_recv = torch.zeros((p, Rcap // 8), dtype=torch.int64, device=DEV)
@@ -348,8 +349,11 @@ def test_selector_and_registry():
     c.set_algorithm("allgather", "ring")
     assert c.get_algorithm("allgather", 4) == "ring"
     c.set_algorithm("allgather", "default")
+    c.set_algorithm("alltoallv", "bruck")             # Bruck-v (f2 iii) is selectable
+    assert c.get_algorithm("alltoallv", 64) == "bruck"
+    c.set_algorithm("alltoallv", "default")
     with pytest.raises(MpxaError):
-        c.set_algorithm("alltoallv", "bruck")
+        c.set_algorithm("alltoallv", "ring")          # ring is allgather-only
 
 
 # ------------------------------------------------------------------ full-size (bench launch config)

@@ -41,7 +41,7 @@ def test_error_strings_and_registry():
     for s in range(10):
         assert lib.mpxa_error_string(s)
     assert list_algorithms("alltoall") == ["pairwise", "bruck", "hier"]
-    assert list_algorithms("alltoallv") == ["pairwise", "hier"]
+    assert list_algorithms("alltoallv") == ["pairwise", "hier", "bruck"]
     assert list_algorithms("allgather") == ["pairwise", "bruck", "ring", "hier"]
     assert lib.mpxa_algo_name(2) == b"bruck"
 
@@ -97,7 +97,7 @@ def test_alltoallv_plans_simulate_to_oracle(p, g):
         recv0 = np.full((p, Rcap), 0xA5, dtype=np.uint8)
         want = oracle.alltoallv_definition(send, sc, sd, rc, rd, 8, recv0)
         for G in _topologies(p):
-            for algo, gg in (("pairwise", 1), ("hier", g)):
+            for algo, gg in (("pairwise", 1), ("hier", g), ("bruck", 1)):
                 pl = Plan("alltoallv", algo, p, G=G, g=gg, counts=sc, sdispls=sd, rdispls=rd)
                 got = simulate(pl, send, recv0, 8)
                 assert np.array_equal(got, want), (algo, G, seed)
