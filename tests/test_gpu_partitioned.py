@@ -185,3 +185,22 @@ def test_partitioned_errors():
     assert torch.equal(r, s)
     ps.free(); pr.free()
     c.finalize()
+
+
+def test_watchdog_poisons_comm_on_missing_partition():
+    """SURVEY.md §5 failure detection: a partition never readied makes the receiver's device
+    wait time out; the error word maps to MPXA_ERR_TIMEOUT and the comm is poisoned (no hang)."""
+    c = Comm(ranks_per_proc=2, device=0, timeout_s=0.3)
+    s, r, ps, pr = channel(c, 4, 4, 4096)
+    pr.start(); ps.start()
+    ps.pready(0, 3)                                 # partition 3 is never readied
+    pr.wait()
+    torch.cuda.synchronize()
+    assert c.check() == M.ERR_TIMEOUT
+    with pytest.raises(MpxaError) as e:
+        pr.start()
+    assert e.value.status == M.ERR_TIMEOUT
+    with pytest.raises(MpxaError) as e:             # collectives refuse to run on a poisoned comm
+        x = torch.zeros(2 * 2 * 64, dtype=torch.uint8, device=DEV)
+        c.alltoall(x, torch.empty_like(x))
+    assert e.value.status == M.ERR_TIMEOUT
