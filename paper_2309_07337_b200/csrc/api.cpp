@@ -64,8 +64,10 @@ constexpr uint64_t kMinSlice = 2048;       // smallest slice worth a CTA when fi
 constexpr uint64_t kBigPerCta = 1u << 20;  // bytes per CTA per step above which the big TMA config wins
 constexpr uint64_t kSmallItemsPerCta = 2048;   // small kernel: 16-B pieces per CTA per step (one batch)
 constexpr uint64_t kSmallItemsOneCta = 2048;   // multi-step programs: largest step one CTA handles
-constexpr uint64_t kDynMinMove = 64u << 10;    // dynamic mode: smallest move (bytes) ...
-constexpr uint64_t kDynMinTotal = 8u << 20;    // ... and smallest per-GPU step volume
+constexpr uint64_t kDynMinMove = 128u << 10;   // dynamic mode: smallest average move (bytes) when
+constexpr uint64_t kDynBigTotal = 128u << 20;  //   the busiest GPU moves this much, else ...
+constexpr uint64_t kDynMinAvg = 512u << 10;    //   this average move (and kDynMinTotal)
+constexpr uint64_t kDynMinTotal = 8u << 20;    // smallest per-GPU step volume
 constexpr uint64_t kDynPiecesPerCta = 64;      // target queue pieces per CTA (measured: 16 -> 64 closes the tail)
 constexpr uint64_t kDynMaxPiece = 512u << 10;  // largest piece (bytes)
 
@@ -514,10 +516,13 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
         int nC = gr.n();
         // dynamic mode: one step whose moves all fit the CTA's shared-memory move tile and
         // whose busiest GPU moves enough bytes for the tail of static slices to matter
-        if (c->dyn && dp.nsteps == 1 && dp.max_gpu_moves <= kMoveTile && dp.max_gpu_bytes_units > 0) {
+        const int64_t ntiles = (dp.max_gpu_moves + kMoveTile - 1) / kMoveTile;
+        if (c->dyn && dp.nsteps == 1 && ntiles <= kMaxDynTiles && dp.max_gpu_bytes_units > 0) {
             const uint64_t total = (uint64_t)dp.max_gpu_bytes_units * unit;
-            const uint64_t L = (uint64_t)dp.host.max_move * unit;
-            if (total >= c->dyn_min_total && L >= kDynMinMove) {
+            const uint64_t avg = total / (uint64_t)std::max<int64_t>(1, dp.max_gpu_moves);
+            // measured (p = 8..32 on one B200): the queues win once moves are large; with many
+            // mid-size moves the per-tile setup costs more than the tail it removes
+            if ((total >= c->dyn_min_total && avg >= kDynMinAvg) || (total >= kDynBigTotal && avg >= kDynMinMove)) {
                 // the mid TMA ring at 2 CTAs / SM: twice the producers and LSU warps of the
                 // big ring (the LSU queue needs the warps; the TMA queue is indifferent).  The
                 // grid depends on the program only, so processes pair CTA flag slots 1:1.
@@ -531,7 +536,7 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
                 U = U / (uint64_t)E.chunk * (uint64_t)E.chunk;
                 E.nS = nC;
                 E.nF = 1;
-                E.dyn_units = 1;
+                E.dyn_units = (int32_t)std::max<int64_t>(1, ntiles);
                 E.dyn_u = (int32_t)U;
             }
         }

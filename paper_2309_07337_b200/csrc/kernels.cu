@@ -592,12 +592,13 @@ __device__ __forceinline__ MovePlan piece_plan(const ExecParams &P, const ExecSh
     return mp;
 }
 
-__device__ __noinline__ bool dyn_step(const ExecParams &P, ExecShared &S, Producer &prod, int g, int first, int nm,
-                                      bool loaded) {
+// One tile of at most kMoveTile moves (queues of tile ti).
+__device__ __noinline__ bool dyn_tile(const ExecParams &P, ExecShared &S, Producer &prod, int g, int first, int nm,
+                                      bool loaded, int ti) {
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const uint64_t U = (uint64_t)P.dyn_u, chunk = (uint64_t)P.chunk;
-    if (!loaded) {   // moves not prefetched by the prologue (step 0 not dense)
-        __syncthreads();
+    if (!loaded) {   // moves not prefetched by the prologue (later tiles, or step 0 not dense)
+        __syncthreads();   // everyone is done with the previous tile's moves
         if (t < nm) S.moves[t] = P.mode == 1 ? P.progs[g].moves[first + t] : P.prog.moves[first + t];
         __syncthreads();
     }
@@ -639,7 +640,7 @@ __device__ __noinline__ bool dyn_step(const ExecParams &P, ExecShared &S, Produc
     bool wrote = false;
     if (t == 0) {
         if (totA == 0) return false;
-        uint32_t *q = &P.dc->dyn_next[g];
+        uint32_t *q = &P.dc->dyn_next[g * kMaxDynTiles + ti];
         uint32_t u = atomicAdd(q, 1u);
         while (u < totA) {
             const uint32_t un = atomicAdd(q, 1u);   // next piece requested while this one streams
@@ -665,7 +666,7 @@ __device__ __noinline__ bool dyn_step(const ExecParams &P, ExecShared &S, Produc
             u = un;
         }
     } else if (warp >= 1 && totB) {
-        uint32_t *q = &P.dc->dyn_next2[g];
+        uint32_t *q = &P.dc->dyn_next2[g * kMaxDynTiles + ti];
         uint32_t un = 0;
         if (lane == 0) un = atomicAdd(q, 1u);
         for (;;) {
@@ -679,6 +680,16 @@ __device__ __noinline__ bool dyn_step(const ExecParams &P, ExecShared &S, Produc
             wrote = true;
         }
     }
+    return wrote;
+}
+
+// Dynamic mode over the whole step: move tiles in order, each with its own pair of queues; a
+// CTA moves on to the next tile as soon as the current tile's queues are dry (no barrier).
+__device__ __noinline__ bool dyn_step(const ExecParams &P, ExecShared &S, Producer &prod, int g, int first, int nm,
+                                      bool loaded) {
+    bool wrote = false;
+    for (int tile = 0, ti = 0; tile < nm; tile += kMoveTile, ti++)
+        wrote |= dyn_tile(P, S, prod, g, first + tile, min(kMoveTile, nm - tile), loaded && tile == 0, ti);
     return wrote;
 }
 
@@ -935,10 +946,12 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
             P.dc->done_ctas = 0;
             if (multi) P.dc->epoch = epoch;
             if (P.dyn_units)
-                for (int r = 0; r < (int)gridDim.y; r++) {
-                    P.dc->dyn_next[P.my_gpu >= 0 ? P.my_gpu : r] = 0;
-                    P.dc->dyn_next2[P.my_gpu >= 0 ? P.my_gpu : r] = 0;
-                }
+                for (int r = 0; r < (int)gridDim.y; r++)
+                    for (int ti = 0; ti < P.dyn_units; ti++) {
+                        const int row = P.my_gpu >= 0 ? P.my_gpu : r;
+                        P.dc->dyn_next[row * kMaxDynTiles + ti] = 0;
+                        P.dc->dyn_next2[row * kMaxDynTiles + ti] = 0;
+                    }
             __threadfence();
         }
     }

@@ -32,6 +32,7 @@ constexpr TmaConfig kTmaMid = {6, 16384, 4};
 constexpr TmaConfig kTmaBig = {6, 32768, 4};
 constexpr int kMaxDynSmem = 6 * 32768;
 constexpr int kMoveTile = kThreads;   // moves staged in shared memory at a time (one per thread)
+constexpr int kMaxDynTiles = 64;      // dynamic mode: move tiles per step (queues per tile)
 constexpr uint64_t kSmallKernelMax = 8192;  // longest move (bytes) the small-message kernel takes
 constexpr int kSmallMovesSmem = 2048;       // program moves cached in shared memory by the small kernel
 constexpr int kMaxWindows = 16;    // registered recv windows per process
@@ -104,8 +105,9 @@ struct DevComm {
     uint64_t epoch;                         // epochs completed on this GPU (or emulated set)
     uint32_t done_ctas;                     // CTAs of the current launch that finished
     uint32_t pad;
-    uint32_t dyn_next[kMaxGpus];            // work-queue heads of dynamic launches (per GPU row):
-    uint32_t dyn_next2[kMaxGpus];           // TMA pieces / LSU pieces; reset by the last CTA
+    uint32_t dyn_next[kMaxGpus * kMaxDynTiles];   // work-queue heads of dynamic launches, per (GPU
+    uint32_t dyn_next2[kMaxGpus * kMaxDynTiles];  // row, move tile): TMA pieces / LSU pieces;
+                                                  // reset by the launch's last CTA
     uint64_t trace[32];                     // MPXA_TRACE builds: %globaltimer phase stamps
 };
 
@@ -139,9 +141,10 @@ struct ExecParams {
     int32_t small_cache;       // small kernel: moves cached in shared memory (0 = read global)
     int32_t d0_base;           // step 0 dense (Step::dense_base >= 0): its base flow, and
     int32_t d0_n;              // its move count -> step 0's moves are fetched in the prologue
-    // dynamic mode (dyn_units != 0): single-step program whose moves are cut into pieces of
-    // at most dyn_u bytes that CTAs take from a device work queue (DevComm::dyn_next) --
-    // per-SM bandwidth differs across the chip, so static slices leave a tail of slow CTAs
+    // dynamic mode (dyn_units = number of move tiles > 0): single-step program whose moves are
+    // cut into pieces of at most dyn_u bytes that CTAs take from device work queues
+    // (DevComm::dyn_next) -- per-SM bandwidth differs across the chip, so static slices
+    // leave a tail of slow CTAs
     int32_t dyn_units;
     int32_t dyn_u;
     int32_t small_a16;         // every local offset, length, base and stride is a 16-B multiple

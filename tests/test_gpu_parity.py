@@ -431,3 +431,22 @@ def test_graph_replay_device_epochs():
                 assert np.array_equal(host(d_recv), oracle.alltoall_definition(fresh)), (G, algo, rep)
             assert c.check() == 0
             del g
+
+
+@pytest.mark.parametrize("p,b,G", [(32, 262144, 0), (16, 1 << 20, 0), (32, 1 << 20, 4), (16, (1 << 20) + 40, 0),
+                                   (32, 65536, 0)])
+def test_dynamic_mode_many_move_tiles(p, b, G):
+    """Single-step launches with more moves than one shared-memory tile (p^2 > 128) run the
+    dynamic executor tile by tile (one pair of queues per tile): whole buffers vs the oracle,
+    alltoall and allgather, aligned and 8-byte-misaligned blocks."""
+    c = comm(p, G)
+    rng = np.random.default_rng(p + b)
+    send = rng.integers(0, 256, size=(p, p * b), dtype=np.uint8)
+    d_send = dev(send)
+    d_recv = torch.full_like(d_send, 0xA5)
+    c.alltoall(d_send, d_recv, algo="pairwise")
+    assert np.array_equal(host(d_recv), oracle.alltoall_definition(send)), (p, b, G)
+    ag = send[:, :b].copy()
+    d_ag = torch.full((p, p * b), 0x5A, dtype=torch.uint8, device=DEV)
+    c.allgather(dev(ag), d_ag, algo="pairwise")
+    assert np.array_equal(host(d_ag), oracle.allgather_definition(ag)), (p, b, G)

@@ -25,30 +25,31 @@ def t(fn, it=10):
     return sorted(ts)[1]
 
 
-p = 8
-sizes = [int(x) for x in os.environ.get("SIZES", str((256 << 10)) + "," + str(1 << 20) + "," + str(4 << 20) + "," + str(16 << 20)).split(",")]
-configs = [("auto", None, None, None)]
-for big in (0, 1):
-    for ns in (148, 296, 592):
-        if big and ns > 148 * 1: continue
-        configs.append((f"big{big}_ns{ns}", big, ns, None))
-    for nf in (2, 4, 8):
-        configs.append((f"big{big}_nf{nf}", big, None, nf))
-big_buf = torch.randint(0, 255, (p * p * (16 << 20),), dtype=torch.uint8, device="cuda")
-out_buf = torch.empty_like(big_buf)
-for name, big, ns, nf in configs:
-    for k, v in (("MPXA_TMA_BIG", big), ("MPXA_NS", ns), ("MPXA_NF", nf)):
-        if v is None: os.environ.pop(k, None)
-        else: os.environ[k] = str(v)
-    c = Comm(ranks_per_proc=p, device=0)
-    row = {"cfg": name}
-    for b in sizes:
-        s = big_buf[: p * p * b].view(p, p * b)
-        r = out_buf[: p * p * b].view(p, p * b)
-        us = t(lambda: c.alltoall(s, r, algo="pairwise", stream=GS))
-        row[f"a2a_{b >> 10}K"] = [round(us, 1), round(2 * p * p * b / us / 1e6, 2)]
-        s2 = big_buf[: p * b].view(p, b)
-        us = t(lambda: c.allgather(s2, r, algo="pairwise", stream=GS))
-        row[f"ag_{b >> 10}K"] = [round(us, 1), round((p * b + p * p * b) / us / 1e6, 2)]
-    c.finalize()
-    print(json.dumps(row), flush=True)
+if __name__ == "__main__":
+    p = 8
+    sizes = [int(x) for x in os.environ.get("SIZES", str((256 << 10)) + "," + str(1 << 20) + "," + str(4 << 20) + "," + str(16 << 20)).split(",")]
+    configs = [("auto", None, None, None)]
+    for big in (0, 1):
+        for ns in (148, 296, 592):
+            if big and ns > 148 * 1: continue
+            configs.append((f"big{big}_ns{ns}", big, ns, None))
+        for nf in (2, 4, 8):
+            configs.append((f"big{big}_nf{nf}", big, None, nf))
+    big_buf = torch.randint(0, 255, (p * p * (16 << 20),), dtype=torch.uint8, device="cuda")
+    out_buf = torch.empty_like(big_buf)
+    for name, big, ns, nf in configs:
+        for k, v in (("MPXA_TMA_BIG", big), ("MPXA_NS", ns), ("MPXA_NF", nf)):
+            if v is None: os.environ.pop(k, None)
+            else: os.environ[k] = str(v)
+        c = Comm(ranks_per_proc=p, device=0)
+        row = {"cfg": name}
+        for b in sizes:
+            s = big_buf[: p * p * b].view(p, p * b)
+            r = out_buf[: p * p * b].view(p, p * b)
+            us = t(lambda: c.alltoall(s, r, algo="pairwise", stream=GS))
+            row[f"a2a_{b >> 10}K"] = [round(us, 1), round(2 * p * p * b / us / 1e6, 2)]
+            s2 = big_buf[: p * b].view(p, b)
+            us = t(lambda: c.allgather(s2, r, algo="pairwise", stream=GS))
+            row[f"ag_{b >> 10}K"] = [round(us, 1), round((p * b + p * p * b) / us / 1e6, 2)]
+        c.finalize()
+        print(json.dumps(row), flush=True)
