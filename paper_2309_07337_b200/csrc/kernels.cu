@@ -379,12 +379,7 @@ __device__ __forceinline__ uint64_t slice_len(const ExecParams &P, const Move &m
     return hi - lo;
 }
 
-#ifdef MPXA_PLAN_NOINLINE
-__device__ __noinline__
-#else
-__device__ __forceinline__
-#endif
-MovePlan plan_move(const ExecParams &P, const ExecShared &S, const Move &m, int sl, SliceCache &sc) {
+__device__ __forceinline__ MovePlan plan_move(const ExecParams &P, const ExecShared &S, const Move &m, int sl, SliceCache &sc) {
     MovePlan mp;
     uint64_t lo;
     mp.n = slice_len(P, m, sl, sc, lo);
@@ -834,11 +829,7 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
             if (t == 0) S.cts_ok |= need;
             if (S.abort_flag) return;
         }
-#ifdef MPXA_STEP_FENCE
-        if (t == 0) fence_proxy_async();
-#else
         if (multi && t == 0) fence_proxy_async();   // acquired peer writes before TMA reads
-#endif
         const int nm = P.dyn_units ? 0 : st.nm;   // dynamic mode: the work queue below
         const int rot = nm ? (int)(((int64_t)sl + (int64_t)g * nm / P.G) % nm) : 0;
         if (P.dyn_units) wrote = dyn_step(P, S, prod, g, st.first, st.nm, pre);

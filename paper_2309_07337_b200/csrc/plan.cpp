@@ -201,12 +201,7 @@ bool build_allgather(Program &P, int algo, int p, int R, int G, int stop_stage, 
     Builder B(P, p, R, G, p);
     if (algo == A_PAIRWISE) {
         // direct: read send_s once, store it into block s of every rank's recvbuf
-        static const bool no_fan = getenv("MPXA_AG_NOFAN") != nullptr;   // tuning experiment
-        for (int s = 0; s < p; s++) {
-            if (!no_fan) B.move(BK_SEND, s, 0, BK_RECV, 0, s, 1, s, /*fanout=*/1);
-            else
-                for (int t = 0; t < p; t++) B.move(BK_SEND, s, 0, BK_RECV, imod(s + t, p), s, 1, s);
-        }
+        for (int s = 0; s < p; s++) B.move(BK_SEND, s, 0, BK_RECV, 0, s, 1, s, /*fanout=*/1);
         B.end_step();
         return true;
     }
