@@ -68,6 +68,11 @@ constexpr uint64_t kDynMinMove = 128u << 10;   // dynamic mode: smallest average
 constexpr uint64_t kDynBigTotal = 128u << 20;  //   the busiest GPU moves this much, else ...
 constexpr uint64_t kDynMinAvg = 512u << 10;    //   this average move (and kDynMinTotal)
 constexpr uint64_t kDynMinTotal = 8u << 20;    // smallest per-GPU step volume
+// multi-step dynamic mode: busiest step volume and move count (measured, p=8: Bruck / hier
+// alltoall and Bruck allgather gain 5-8 % from 4 MiB blocks; below, or with few moves per step
+// as in the ring, the per-step barrier costs more than the balance gains)
+constexpr uint64_t kDynSyncMin = 128u << 20;
+constexpr int64_t kDynSyncMoves = 32;
 constexpr uint64_t kDynPiecesPerCta = 64;      // target queue pieces per CTA (measured: 16 -> 64 closes the tail)
 constexpr uint64_t kDynMaxPiece = 512u << 10;  // largest piece (bytes)
 
@@ -80,6 +85,7 @@ struct DevProg {
     std::vector<GpuProg> gp;   // the [G] GpuProg table as uploaded (device pointers)
     int64_t max_gpu_moves = 0;      // most moves any GPU runs
     int64_t max_gpu_bytes_units = 0;  // single-step programs: most units any GPU moves (source side)
+    int64_t dyn_tiles = 0;          // sum over steps of the most move tiles any GPU has in the step
 };
 
 // dynamic-mode eligibility facts of a program (DevProg::max_gpu_moves, max_gpu_bytes_units)
@@ -87,6 +93,12 @@ void prog_facts(DevProg &dp) {
     const Program &P = dp.host;
     dp.max_gpu_moves = 0;
     dp.max_gpu_bytes_units = 0;
+    dp.dyn_tiles = 0;
+    for (int s = 0; s < P.nsteps(); s++) {
+        int64_t mx = 0;
+        for (int g = 0; g < P.G; g++) mx = std::max<int64_t>(mx, P.steps[g][s].move_end - P.steps[g][s].move_begin);
+        dp.dyn_tiles += std::max<int64_t>(1, (mx + kMoveTile - 1) / kMoveTile);
+    }
     for (const auto &mv : P.moves) {
         dp.max_gpu_moves = std::max<int64_t>(dp.max_gpu_moves, (int64_t)mv.size());
         int64_t u = 0;
@@ -539,6 +551,24 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
                 E.dyn_units = (int32_t)std::max<int64_t>(1, ntiles);
                 E.dyn_u = (int32_t)U;
             }
+        } else if (c->dyn && dp.nsteps > 1 && dp.dyn_tiles <= kMaxDynTiles && dp.host.max_step_moves >= kDynSyncMoves &&
+                   (uint64_t)dp.host.max_step_units * unit >= kDynSyncMin) {
+            // multi-step dynamic mode: queues per step, a CTA barrier per GPU row between steps,
+            // one flag per peer GPU (the flow-ownership rule no longer applies)
+            const TmaConfig tm = c->force_big > 0 ? kTmaBig : kTmaMid;
+            E.stages = tm.stages;
+            E.chunk = tm.chunk;
+            E.ahead = tm.ahead;
+            nC = c->force_big > 0 ? c->cap_big : c->cap_ctas;
+            const uint64_t total = (uint64_t)dp.host.max_step_units * unit;
+            uint64_t U = total / ((uint64_t)nC * (uint64_t)c->dyn_pieces);
+            U = std::max<uint64_t>((uint64_t)E.chunk, std::min<uint64_t>(U, kDynMaxPiece));
+            U = U / (uint64_t)E.chunk * (uint64_t)E.chunk;
+            E.nS = nC;
+            E.nF = 1;
+            E.dyn_units = (int32_t)dp.dyn_tiles;
+            E.dyn_u = (int32_t)U;
+            E.dyn_sync = 1;
         }
         e = launch_exec(E, nC, c->emulated ? c->G : 1, c->emulated, pdl && c->pdl, stream);
     }

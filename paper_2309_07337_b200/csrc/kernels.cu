@@ -681,11 +681,36 @@ __device__ __noinline__ bool dyn_tile(const ExecParams &P, ExecShared &S, Produc
 // Dynamic mode over the whole step: move tiles in order, each with its own pair of queues; a
 // CTA moves on to the next tile as soon as the current tile's queues are dry (no barrier).
 __device__ __noinline__ bool dyn_step(const ExecParams &P, ExecShared &S, Producer &prod, int g, int first, int nm,
-                                      bool loaded) {
+                                      bool loaded, int tile0) {
     bool wrote = false;
-    for (int tile = 0, ti = 0; tile < nm; tile += kMoveTile, ti++)
+    for (int tile = 0, ti = tile0; tile < nm; tile += kMoveTile, ti++)
         wrote |= dyn_tile(P, S, prod, g, first + tile, min(kMoveTile, nm - tile), loaded && tile == 0, ti);
     return wrote;
+}
+
+// Multi-step dynamic mode: every CTA of this GPU row has finished step s (its writes complete
+// and fenced) -- a counter barrier; the grid never exceeds the co-resident CTA count.
+__device__ __noinline__ void row_barrier(const ExecParams &P, ExecShared &S, int g, int s) {
+    if (threadIdx.x == 0) {
+        uint32_t *bar = &P.dc->dyn_bar[g];
+        __threadfence();
+        atomicAdd(bar, 1u);
+        const uint32_t want = (uint32_t)(s + 1) * gridDim.x;
+        uint64_t t0 = 0;
+        int it = 0;
+        for (;;) {
+            uint32_t v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+            if (v >= want) break;
+            if (++it > 16) {
+                __nanosleep(64);
+                if (!t0) t0 = globaltimer();
+                else if ((int64_t)(globaltimer() - t0) > P.timeout_ns) { atomicExch(P.err, 1); S.abort_flag = 1; break; }
+            }
+        }
+        fence_proxy_async();   // other CTAs' writes, acquired, before this CTA's TMA reads
+    }
+    __syncthreads();
 }
 
 #ifndef MPXA_EXEC_MINB
@@ -799,6 +824,7 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
     }
 
     SliceCache sc;
+    int tile_base = 0;   // dynamic mode: first queue tile of the current step
     TRACE(1);
     for (int s = 0; s < nsteps; s++) {
         StepInfo st;
@@ -812,10 +838,11 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
         }
         const uint32_t prev_wait = s == 0 ? 0u : (steps_in_smem ? S.steps[s - 1].wait_mask : prog.steps[s - 1].wait_mask);
         bool wrote = false;   // this thread issued generic global stores in this step
+        const int fslot = P.dyn_sync ? 0 : c;   // flag slot: this CTA's, or the row's (sync mode)
         if (multi) {
             // data written into this GPU by peers in step s-1 (this CTA's share) must have landed
             if (prev_wait)
-                wait_mask_ge(P, S, prev_wait, &S.sym[g]->flags[0][c], kMaxCtas, (epoch << 8) | (uint64_t)s);
+                wait_mask_ge(P, S, prev_wait, &S.sym[g]->flags[0][fslot], kMaxCtas, (epoch << 8) | (uint64_t)s);
             // peers written in this step must have cleared us to send in this epoch
             uint32_t need = st.signal_mask & ~S.cts_ok;
             if (need) {
@@ -832,7 +859,10 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
         if (multi && t == 0) fence_proxy_async();   // acquired peer writes before TMA reads
         const int nm = P.dyn_units ? 0 : st.nm;   // dynamic mode: the work queue below
         const int rot = nm ? (int)(((int64_t)sl + (int64_t)g * nm / P.G) % nm) : 0;
-        if (P.dyn_units) wrote = dyn_step(P, S, prod, g, st.first, st.nm, pre);
+        if (P.dyn_units) {
+            wrote = dyn_step(P, S, prod, g, st.first, st.nm, pre && s == 0, tile_base);
+            tile_base += (st.nm + kMoveTile - 1) / kMoveTile;
+        }
         for (int tile = 0; tile < nm; tile += kMoveTile) {
             const int cnt = min(kMoveTile, nm - tile);
             if (!(pre && s == 0 && tile == 0)) {   // (prefetched in the prologue)
@@ -915,6 +945,16 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
         TRACE(4);
         __syncthreads();
         TRACE(5);
+        if (P.dyn_sync) {
+            // every CTA of the row done with step s; then one signal per peer GPU
+            if (s + 1 < nsteps || (multi && st.signal_mask)) row_barrier(P, S, g, s);
+            if (S.abort_flag) return;
+            if (multi && c == 0 && st.signal_mask && t < 32 && ((st.signal_mask >> t) & 1u)) {
+                __threadfence_system();
+                st_release_sys(&S.sym[t]->flags[g][0], (epoch << 8) | (uint64_t)(s + 1));
+            }
+            continue;
+        }
         // ---- signal the peers written in this step (this CTA's share) ----
         if (multi && st.signal_mask && t < 32 && ((st.signal_mask >> t) & 1u)) {
             __threadfence_system();
@@ -925,7 +965,8 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
     const uint32_t last_wait = nsteps == 0 ? 0u : (steps_in_smem ? S.steps[nsteps - 1].wait_mask
                                                                   : prog.steps[nsteps - 1].wait_mask);
     if (multi && last_wait) {
-        wait_mask_ge(P, S, last_wait, &S.sym[g]->flags[0][c], kMaxCtas, (epoch << 8) | (uint64_t)nsteps);
+        wait_mask_ge(P, S, last_wait, &S.sym[g]->flags[0][P.dyn_sync ? 0 : c], kMaxCtas,
+                     (epoch << 8) | (uint64_t)nsteps);
         __syncthreads();
     }
     // the last CTA of the launch publishes the epoch and resets the work queues (the next
@@ -937,12 +978,14 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
             P.dc->done_ctas = 0;
             if (multi) P.dc->epoch = epoch;
             if (P.dyn_units)
-                for (int r = 0; r < (int)gridDim.y; r++)
+                for (int r = 0; r < (int)gridDim.y; r++) {
+                    const int row = P.my_gpu >= 0 ? P.my_gpu : r;
                     for (int ti = 0; ti < P.dyn_units; ti++) {
-                        const int row = P.my_gpu >= 0 ? P.my_gpu : r;
                         P.dc->dyn_next[row * kMaxDynTiles + ti] = 0;
                         P.dc->dyn_next2[row * kMaxDynTiles + ti] = 0;
                     }
+                    P.dc->dyn_bar[row] = 0;
+                }
             __threadfence();
         }
     }

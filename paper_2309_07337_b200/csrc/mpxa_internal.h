@@ -108,6 +108,7 @@ struct DevComm {
     uint32_t dyn_next[kMaxGpus * kMaxDynTiles];   // work-queue heads of dynamic launches, per (GPU
     uint32_t dyn_next2[kMaxGpus * kMaxDynTiles];  // row, move tile): TMA pieces / LSU pieces;
                                                   // reset by the launch's last CTA
+    uint32_t dyn_bar[kMaxGpus];                   // multi-step dynamic mode: per-row step barrier
     uint64_t trace[32];                     // MPXA_TRACE builds: %globaltimer phase stamps
 };
 
@@ -145,10 +146,12 @@ struct ExecParams {
     // cut into pieces of at most dyn_u bytes that CTAs take from device work queues
     // (DevComm::dyn_next) -- per-SM bandwidth differs across the chip, so static slices
     // leave a tail of slow CTAs
-    int32_t dyn_units;
+    int32_t dyn_units;         // queue tiles used by the launch (all steps)
     int32_t dyn_u;
     int32_t small_a16;         // every local offset, length, base and stride is a 16-B multiple
-    int32_t pad4;
+    int32_t dyn_sync;          // multi-step dynamic mode: steps separated by a per-GPU-row CTA
+                               // barrier and ONE flag per peer GPU (slot 0), so any CTA may move
+                               // any piece (no flow ownership needed)
 };
 
 }  // namespace mpxa
