@@ -444,8 +444,14 @@ def test_dynamic_mode_many_move_tiles(p, b, G):
     send = rng.integers(0, 256, size=(p, p * b), dtype=np.uint8)
     d_send = dev(send)
     d_recv = torch.full_like(d_send, 0xA5)
+    want = oracle.alltoall_definition(send)
     c.alltoall(d_send, d_recv, algo="pairwise")
-    assert np.array_equal(host(d_recv), oracle.alltoall_definition(send)), (p, b, G)
+    assert np.array_equal(host(d_recv), want), (p, b, G)
+    if b >= (1 << 20):    # multi-step dynamic mode (step barrier, per-GPU flags when G > 0)
+        for algo in ("bruck", "hier"):
+            d_recv.fill_(0xA5)
+            c.alltoall(d_send, d_recv, algo=algo)
+            assert np.array_equal(host(d_recv), want), (p, b, G, algo)
     ag = send[:, :b].copy()
     d_ag = torch.full((p, p * b), 0x5A, dtype=torch.uint8, device=DEV)
     c.allgather(dev(ag), d_ag, algo="pairwise")
