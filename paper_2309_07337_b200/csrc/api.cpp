@@ -68,11 +68,13 @@ constexpr uint64_t kDynMinMove = 128u << 10;   // dynamic mode: smallest average
 constexpr uint64_t kDynBigTotal = 128u << 20;  //   the busiest GPU moves this much, else ...
 constexpr uint64_t kDynMinAvg = 512u << 10;    //   this average move (and kDynMinTotal)
 constexpr uint64_t kDynMinTotal = 8u << 20;    // smallest per-GPU step volume
-// multi-step dynamic mode: busiest step volume and move count (measured, p=8: Bruck / hier
-// alltoall and Bruck allgather gain 5-8 % from 4 MiB blocks; below, or with few moves per step
-// as in the ring, the per-step barrier costs more than the balance gains)
+// multi-step dynamic mode (measured, p=8 on one B200): uniform blocks -- Bruck / hier alltoall,
+// Bruck allgather gain 5-8 % from 4 MiB blocks (busiest step >= 128 MiB, >= 32 moves); below,
+// or with few moves per step as in the ring, the per-step barrier costs more than the balance
+// gains.  Uneven moves (alltoallv hier / Bruck-v, locality neighbor) gain 1.8-2.2x from 16 MiB.
 constexpr uint64_t kDynSyncMin = 128u << 20;
 constexpr int64_t kDynSyncMoves = 32;
+constexpr uint64_t kDynSyncMinUneven = 16u << 20;
 constexpr uint64_t kDynPiecesPerCta = 64;      // target queue pieces per CTA (measured: 16 -> 64 closes the tail)
 constexpr uint64_t kDynMaxPiece = 512u << 10;  // largest piece (bytes)
 
@@ -86,6 +88,7 @@ struct DevProg {
     int64_t max_gpu_moves = 0;      // most moves any GPU runs
     int64_t max_gpu_bytes_units = 0;  // single-step programs: most units any GPU moves (source side)
     int64_t dyn_tiles = 0;          // sum over steps of the most move tiles any GPU has in the step
+    bool uniform_len = true;        // every move of the program has the same length
 };
 
 // dynamic-mode eligibility facts of a program (DevProg::max_gpu_moves, max_gpu_bytes_units)
@@ -99,6 +102,10 @@ void prog_facts(DevProg &dp) {
         for (int g = 0; g < P.G; g++) mx = std::max<int64_t>(mx, P.steps[g][s].move_end - P.steps[g][s].move_begin);
         dp.dyn_tiles += std::max<int64_t>(1, (mx + kMoveTile - 1) / kMoveTile);
     }
+    dp.uniform_len = true;
+    for (const auto &mv : P.moves)
+        for (const Move &m : mv)
+            if (m.len != P.max_move) { dp.uniform_len = false; break; }
     for (const auto &mv : P.moves) {
         dp.max_gpu_moves = std::max<int64_t>(dp.max_gpu_moves, (int64_t)mv.size());
         int64_t u = 0;
@@ -189,6 +196,7 @@ struct mpxa_comm_s {
     bool dyn = true;                          // MPXA_NO_DYN=1: static slices only (no work queue)
     int dyn_pieces = (int)kDynPiecesPerCta;   // MPXA_DYN_PIECES: queue pieces per CTA (tuning)
     uint64_t dyn_min_total = kDynMinTotal;    // MPXA_DYN_MIN: smallest busiest-GPU volume (tuning)
+    int force_sync = -1;                      // MPXA_DYN_SYNC=0/1: force multi-step dynamic mode (tuning)
 
     SymRegion *sym_local = nullptr;            // G regions when emulated, else 1
     SymRegion *sym_map[kMaxGpus] = {};
@@ -551,8 +559,11 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
                 E.dyn_units = (int32_t)std::max<int64_t>(1, ntiles);
                 E.dyn_u = (int32_t)U;
             }
-        } else if (c->dyn && dp.nsteps > 1 && dp.dyn_tiles <= kMaxDynTiles && dp.host.max_step_moves >= kDynSyncMoves &&
-                   (uint64_t)dp.host.max_step_units * unit >= kDynSyncMin) {
+        } else if (c->dyn && dp.nsteps > 1 && dp.dyn_tiles <= kMaxDynTiles &&
+                   (c->force_sync > 0 || (dp.host.max_step_moves >= kDynSyncMoves && (uint64_t)dp.host.max_step_units * unit >= kDynSyncMin) ||
+                    // moves of different lengths: static flow groups get unequal byte counts
+                    (!dp.uniform_len && (uint64_t)dp.host.max_step_units * unit >= kDynSyncMinUneven)) &&
+                   c->force_sync != 0) {
             // multi-step dynamic mode: queues per step, a CTA barrier per GPU row between steps,
             // one flag per peer GPU (the flow-ownership rule no longer applies)
             const TmaConfig tm = c->force_big > 0 ? kTmaBig : kTmaMid;
@@ -894,6 +905,7 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     if (const char *e = getenv("MPXA_NO_DYN")) c->dyn = atoi(e) == 0;
     if (const char *e = getenv("MPXA_DYN_PIECES")) c->dyn_pieces = std::max(1, atoi(e));
     if (const char *e = getenv("MPXA_DYN_MIN")) c->dyn_min_total = strtoull(e, nullptr, 10);
+    if (const char *e = getenv("MPXA_DYN_SYNC")) c->force_sync = atoi(e);
     CK(cudaHostAlloc((void **)&c->err_host, sizeof(int32_t), cudaHostAllocMapped));
     *c->err_host = 0;
     CK(cudaHostGetDevicePointer((void **)&c->err_dev, c->err_host, 0));
