@@ -576,6 +576,8 @@ def gpu_arm(args):
         streams = [stream, torch.cuda.Stream()]
         sends = [send, torch.empty_like(send)]
         recvs = [recv, torch.empty_like(recv)]
+        if ws > 1:
+            comm.register(recvs[1])      # peers write into it directly (multi-process mode)
         h_recvs = [torch.empty((R, p * b), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
         kev = [torch.cuda.Event(), torch.cuda.Event()]
         state = {"i": 0}
