@@ -229,7 +229,7 @@ struct mpxa_comm_s {
     std::vector<unsigned long long *> part_map;   // [nprocs]
     std::vector<uint64_t> part_cursor;            // [nprocs] next free slot (same on every process)
     std::vector<mpxa_request_t> ppending;         // created, not yet matched (creation order)
-    std::map<std::pair<int, uint64_t>, char *> ipc_opened;   // (proc, alloc key) -> mapped base
+    std::map<std::pair<int, std::string>, char *> ipc_opened;   // (proc, IPC handle bytes) -> mapped base
     cudaStream_t pquery = nullptr;                // private stream for Parrived host queries
 };
 
@@ -1362,8 +1362,7 @@ int mpxa_pmatch(mpxa_comm_t c) {
             if (rv.proc == c->proc || c->nprocs == 1) {
                 dst = c->ppending[rv.idx]->pbuf;
             } else if (rv.part_bytes) {
-                uint64_t key;
-                memcpy(&key, rv.h.reserved, sizeof key);
+                const std::string key(rv.h.reserved, sizeof rv.h.reserved);
                 auto it = c->ipc_opened.find({rv.proc, key});
                 if (it == c->ipc_opened.end()) {
                     void *m = nullptr;

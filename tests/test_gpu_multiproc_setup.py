@@ -49,6 +49,44 @@ def _body(rank, port, q):
             assert e.status == M.ERR_UNREGISTERED
         c.register(recv)
         c.register(recv)           # already registered everywhere: no new window
+        # f1: topology all-gather + persistent neighbor init (standard / locality-aware): the
+        # global graph is assembled from both processes' rank lists and compiled once
+        r0 = 2 * rank
+        srcs = [[(r0 + t - 1) % 4, (r0 + t + 1) % 4] for t in range(2)]
+        topo = c.dist_graph_create_adjacent(srcs, srcs)
+        nb_s = torch.zeros(2 * 2 * 8, dtype=torch.int64, device="cuda")
+        nb_r = torch.zeros(2 * 2 * 8, dtype=torch.int64, device="cuda")
+        sc = [8, 8, 8, 8]
+        sd = [0, 8, 0, 8]
+        ids = []
+        for t in range(2):
+            for d in ((r0 + t - 1) % 4, (r0 + t + 1) % 4):
+                ids += [(r0 + t) * 1000 + d * 10 + k for k in range(8)]
+        rids = []
+        for t in range(2):
+            for src in ((r0 + t - 1) % 4, (r0 + t + 1) % 4):
+                rids += [src * 1000 + (r0 + t) * 10 + k for k in range(8)]
+        for kw in ({}, dict(send_indices=ids, recv_indices=rids)):
+            req = c.neighbor_alltoallv_init(topo, nb_s, sc, sd, nb_r, sc, sd, **kw)
+            req.free()
+        topo.free()
+        # f3: partitioned channels across the two processes -- the single match maps the
+        # peer's receive buffer and flag heap (no kernels: they would wait on each other)
+        ps_buf = torch.zeros(4096, dtype=torch.uint8, device="cuda")
+        pr_buf = torch.zeros(4096, dtype=torch.uint8, device="cuda")
+        ps = c.psend_init(ps_buf, 4, r0, (r0 + 2) % 4, 7)
+        pr = c.precv_init(pr_buf, 2, r0, (r0 + 2) % 4, 7)
+        c.pmatch()
+        assert len(ps.device_handle()) == 128
+        ps.free(); pr.free()
+        lonely = c.psend_init(ps_buf, 4, r0, (r0 + 2) % 4, 99) if rank == 0 else None
+        try:
+            c.pmatch()
+            raise AssertionError("expected MPXA_ERR_MISMATCH")
+        except MpxaError as e:
+            assert e.status == M.ERR_MISMATCH
+        if lonely is not None:
+            lonely.free()
         assert c.launch_count() == 0
         c.finalize()
         # topology mismatch across processes
