@@ -63,6 +63,8 @@ constexpr uint64_t kMovesPerCta = 1;       // moves per CTA (latency-bound regim
 constexpr uint64_t kMinSlice = 2048;       // smallest slice worth a CTA when filling the GPU (= TMA min)
 constexpr uint64_t kBigPerCta = 1u << 20;  // bytes per CTA per step above which the big TMA config wins
 constexpr uint64_t kSmallItemsPerCta = 2048;   // small kernel: 16-B pieces per CTA per step (one batch)
+constexpr uint64_t kSmallOneStepMove = 1u << 20;   // single-step programs: longest move ...
+constexpr uint64_t kSmallOneStepVol = 16u << 20;   // ... and source bytes per GPU for the small kernel
 constexpr uint64_t kSmallItemsOneCta = 2048;   // multi-step programs: largest step one CTA handles
 constexpr uint64_t kDynMinMove = 128u << 10;   // dynamic mode: smallest average move (bytes) when
 constexpr uint64_t kDynBigTotal = 128u << 20;  //   the busiest GPU moves this much, else ...
@@ -197,6 +199,7 @@ struct mpxa_comm_s {
     int dyn_pieces = (int)kDynPiecesPerCta;   // MPXA_DYN_PIECES: queue pieces per CTA (tuning)
     uint64_t dyn_min_total = kDynMinTotal;    // MPXA_DYN_MIN: smallest busiest-GPU volume (tuning)
     int force_sync = -1;                      // MPXA_DYN_SYNC=0/1: force multi-step dynamic mode (tuning)
+    uint64_t small_max1 = kSmallOneStepMove;  // MPXA_SMALL_MAX: longest move of one-step small launches
 
     SymRegion *sym_local = nullptr;            // G regions when emulated, else 1
     SymRegion *sym_map[kMaxGpus] = {};
@@ -518,10 +521,15 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
     const uint64_t items = std::max<uint64_t>((uint64_t)dp.host.max_step_moves,
                                               (uint64_t)dp.host.max_step_units / std::max<int64_t>(1, dp.host.max_move)) * ppm;
     const bool one_step = dp.nsteps == 1;
-    // latency regime: short moves, and a step small enough for one CTA unless the program
-    // has a single step (then several CTAs may share it)
-    const bool small = !c->force_exec && maxmove <= kSmallKernelMax &&
-                       (one_step || items <= kSmallItemsOneCta);
+    // Small-message kernel: multi-step programs with short moves and a step small enough for
+    // one CTA; single-step programs (any number of CTAs) up to 1 MiB moves and 16 MiB of
+    // source data per GPU -- measured on one B200: its LSU pieces beat the TMA executor's
+    // fixed costs there (alltoall 64 KiB blocks 5.3 -> 3.8 us, allgather 1 MiB 17.9 -> 13.8 us,
+    // alltoallv cfg4 64 KiB mean 9.2 -> 5.2 us); beyond, the executor streams better.
+    const uint64_t src_vol = (uint64_t)dp.max_gpu_bytes_units * unit;
+    const bool small = !c->force_exec &&
+                       (one_step ? (maxmove <= c->small_max1 && src_vol <= kSmallOneStepVol)
+                                 : (maxmove <= kSmallKernelMax && items <= kSmallItemsOneCta));
     if (small) {
         E.nS = E.nF = 1;
         E.small_a16 = unit % 16 == 0 && (uintptr_t)send % 16 == 0 && (uintptr_t)recv % 16 == 0 &&
@@ -906,6 +914,7 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     if (const char *e = getenv("MPXA_DYN_PIECES")) c->dyn_pieces = std::max(1, atoi(e));
     if (const char *e = getenv("MPXA_DYN_MIN")) c->dyn_min_total = strtoull(e, nullptr, 10);
     if (const char *e = getenv("MPXA_DYN_SYNC")) c->force_sync = atoi(e);
+    if (const char *e = getenv("MPXA_SMALL_MAX")) c->small_max1 = strtoull(e, nullptr, 10);
     CK(cudaHostAlloc((void **)&c->err_host, sizeof(int32_t), cudaHostAllocMapped));
     *c->err_host = 0;
     CK(cudaHostGetDevicePointer((void **)&c->err_dev, c->err_host, 0));
