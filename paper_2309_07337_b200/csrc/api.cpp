@@ -19,6 +19,7 @@
 #include <sstream>
 #include <string>
 #include <tuple>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/mpxa.h"
@@ -221,6 +222,18 @@ struct mpxa_comm_s {
     std::vector<SelEntry> selector;
 
     std::map<std::tuple<int, int, int, int>, std::shared_ptr<DevProg>> cache;  // (op,algo,stage,g)
+    // one-shot alltoallv programs by (algo, global count / displacement matrices): repeated
+    // calls with the same layout skip the build and the upload
+    struct VEntry {
+        int algo;
+        std::vector<int64_t> C, SD, RD;
+        std::shared_ptr<DevProg> prog;
+        cudaEvent_t last = nullptr;      // recorded after the latest launch using prog
+        uint64_t used = 0;
+    };
+    std::unordered_map<uint64_t, std::vector<VEntry>> vcache;
+    uint64_t vcache_clock = 0;
+    size_t vcache_n = 0;
     std::vector<Slot> ring;
     int ring_next = 0;
     int64_t *counts_tmp = nullptr;             // multi-process counts exchange staging
@@ -698,6 +711,58 @@ int gather_v(mpxa_comm_t c, const int64_t *sc, const int64_t *sd, const int64_t 
     return MPXA_SUCCESS;
 }
 
+constexpr size_t kVCacheMax = 32;
+
+uint64_t fnv(uint64_t h, const void *p, size_t n) {
+    const unsigned char *b = (const unsigned char *)p;
+    for (size_t i = 0; i < n; i++) h = (h ^ b[i]) * 1099511628211ull;
+    return h;
+}
+
+// cached one-shot v-program (built and uploaded on a miss; LRU eviction waits for the
+// evicted program's last launch)
+int vprogram(mpxa_comm_t c, int algo, const std::vector<int64_t> &C, const std::vector<int64_t> &SD,
+             const std::vector<int64_t> &RD, mpxa_comm_s::VEntry *&out) {
+    uint64_t h = fnv(1469598103934665603ull, &algo, sizeof algo);
+    h = fnv(h, C.data(), C.size() * 8);
+    h = fnv(h, SD.data(), SD.size() * 8);
+    h = fnv(h, RD.data(), RD.size() * 8);
+    auto &bucket = c->vcache[h];
+    for (auto &e : bucket)
+        if (e.algo == algo && e.C == C && e.SD == SD && e.RD == RD) {
+            e.used = ++c->vcache_clock;
+            out = &e;
+            return MPXA_SUCCESS;
+        }
+    if (c->vcache_n >= kVCacheMax) {            // evict the least recently used entry
+        uint64_t best = ~0ull, bh = 0;
+        size_t bi = 0;
+        for (auto &kv : c->vcache)
+            for (size_t i = 0; i < kv.second.size(); i++)
+                if (kv.second[i].used < best) { best = kv.second[i].used; bh = kv.first; bi = i; }
+        auto &vb = c->vcache[bh];
+        if (vb[bi].last) { CK(cudaEventSynchronize(vb[bi].last)); cudaEventDestroy(vb[bi].last); }
+        if (vb[bi].prog) cudaFree(vb[bi].prog->dmem);
+        vb.erase(vb.begin() + (long)bi);
+        if (vb.empty()) c->vcache.erase(bh);
+        c->vcache_n--;
+    }
+    Program P;
+    if (!build_alltoallv(P, algo, c->p, c->Rg, c->G, c->g, C.data(), SD.data(), RD.data())) return MPXA_ERR_ALGO;
+    mpxa_comm_s::VEntry e;
+    e.algo = algo;
+    e.C = C; e.SD = SD; e.RD = RD;
+    int r = upload_program(P, e.prog);
+    if (r) return r;
+    CK(cudaEventCreateWithFlags(&e.last, cudaEventDisableTiming));
+    e.used = ++c->vcache_clock;
+    auto &b2 = c->vcache[h];
+    b2.push_back(std::move(e));
+    c->vcache_n++;
+    out = &b2.back();
+    return MPXA_SUCCESS;
+}
+
 int alltoallv_impl(const void *sendbuf, const int64_t *sc, const int64_t *sd, size_t send_bpr,
                    void *recvbuf, const int64_t *rc, const int64_t *rd, size_t recv_bpr, size_t w,
                    int algo, mpxa_comm_t c, cudaStream_t stream, mpxa_request_t *req) {
@@ -711,6 +776,15 @@ int alltoallv_impl(const void *sendbuf, const int64_t *sc, const int64_t *sd, si
     std::vector<int64_t> C, SD, RD;
     int r = gather_v(c, sc, sd, rc, rd, w, send_bpr, recv_bpr, C, SD, RD);
     if (r) return r;
+    if (!req) {                                  // one-shot: cached program, PDL launch
+        mpxa_comm_s::VEntry *e = nullptr;
+        r = vprogram(c, algo, C, SD, RD, e);
+        if (r) return r;
+        r = run_program(c, *e->prog, (const char *)sendbuf, (char *)recvbuf, w, send_bpr, recv_bpr, stream);
+        if (r) return r;
+        CK(cudaEventRecord(e->last, stream));
+        return MPXA_SUCCESS;
+    }
     Program P;
     if (!build_alltoallv(P, algo, c->p, c->Rg, c->G, c->g, C.data(), SD.data(), RD.data())) return MPXA_ERR_ALGO;
     if (req) {
@@ -730,7 +804,7 @@ int alltoallv_impl(const void *sendbuf, const int64_t *sc, const int64_t *sd, si
         *req = q;
         return MPXA_SUCCESS;
     }
-    return run_dynamic(c, P, (const char *)sendbuf, (char *)recvbuf, w, send_bpr, recv_bpr, stream);
+    return MPXA_SUCCESS;
 }
 
 int uniform_impl(int op, const void *sendbuf, size_t count, size_t w, void *recvbuf, int algo,
@@ -992,6 +1066,11 @@ int mpxa_finalize(mpxa_comm_t c) {
     if (c->part_local) cudaFree(c->part_local);
     if (c->pquery) cudaStreamDestroy(c->pquery);
     for (auto &kv : c->cache) cudaFree(kv.second->dmem);
+    for (auto &kv : c->vcache)
+        for (auto &e : kv.second) {
+            if (e.prog) cudaFree(e.prog->dmem);
+            if (e.last) cudaEventDestroy(e.last);
+        }
     for (auto &s : c->ring) {
         if (s.dmem) cudaFree(s.dmem);
         if (s.pinned) cudaFreeHost(s.pinned);

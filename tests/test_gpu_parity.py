@@ -456,3 +456,19 @@ def test_dynamic_mode_many_move_tiles(p, b, G):
     d_ag = torch.full((p, p * b), 0x5A, dtype=torch.uint8, device=DEV)
     c.allgather(dev(ag), d_ag, algo="pairwise")
     assert np.array_equal(host(d_ag), oracle.allgather_definition(ag)), (p, b, G)
+
+
+def test_one_shot_alltoallv_program_cache():
+    """One-shot alltoallv reuses the compiled program when the count/displacement matrices
+    repeat, and evicts (least recently used) past 32 layouts: every call stays exact."""
+    p = 8
+    c = comm(p)
+    layouts = [synth.cfg4_counts(seed, p, 512) for seed in range(40)]
+    for rep in range(2):
+        for seed, c4 in enumerate(layouts):
+            send, sc, sd, rc, rd, S, Rcap = synth.alltoallv_buffers(seed + 100 * rep, c4, elem=8, packed=bool(seed % 2))
+            recv0 = np.full((p, Rcap), 0xA5, dtype=np.uint8)
+            d_recv = dev(recv0)
+            c.alltoallv(dev(send.view(np.int64)), sc, sd, d_recv.view(torch.int64), rc, rd)
+            want = oracle.alltoallv_definition(send, sc, sd, rc, rd, 8, recv0)
+            assert np.array_equal(host(d_recv), want), (rep, seed)
