@@ -57,6 +57,9 @@ public:
     void end_step() {
         for (auto &kv : pending_) loc_[kv.first] = kv.second;
         pending_.clear();
+        bool any = false;                       // a step without moves on every GPU is dropped
+        for (int g = 0; g < G_ && !any; g++) any = !cur_[g].empty();
+        if (!any) return;
         std::vector<uint32_t> sig(G_, 0), wt(G_, 0);
         for (int g = 0; g < G_; g++)
             for (const Move &m : cur_[g]) {

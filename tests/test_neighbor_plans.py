@@ -41,7 +41,7 @@ def test_neighbor_plans_simulate_to_oracle(name, p, edges):
     for G in splits(p):
         pl = Plan.neighbor(gr, R=p // G, G=G)
         assert np.array_equal(simulate(pl, send, recv0, 8), want), ("standard", G)
-        assert pl.info["nsteps"] == 1
+        assert pl.info["nsteps"] == (1 if len(edges) and gr["sc"].sum() else 0)
         for g in [x for x in (1, 2, 4, p) if p % x == 0]:
             pl = Plan.neighbor(gr, R=p // G, G=G, g=g, locality=True, send_idx=si, recv_idx=ri)
             got = simulate(pl, send, recv0, 8)
@@ -58,8 +58,7 @@ def test_locality_crossing_values_match_oracle(name, p, edges):
     for g in [x for x in (1, 2, 4) if p % x == 0]:
         _, st = oracle.neighbor(send, recv0, 8, gr, "locality", g=g, send_idx=si, recv_idx=ri)
         pl = Plan.neighbor(gr, R=p, G=1, g=g, locality=True, send_idx=si, recv_idx=ri)
-        s2 = pl.steps(0)[1]
-        mv = pl.moves(0)[s2.move_begin:s2.move_end]
+        mv = pl.moves(0)                  # the only group-crossing moves are WORK -> WORK
         crossing = sum(m.len for m in mv if m.src_kind == WORK and m.dst_kind == WORK and m.src_rank // g != m.dst_rank // g)
         assert crossing == st["inter_values"], g
 
