@@ -630,6 +630,36 @@ def gpu_arm(args):
         nccl = {"impl": "torch.distributed all_gather_into_tensor (NCCL %s) + local replication" %
                         ".".join(map(str, torch.cuda.nccl.version())),
                 "ms_per_step": round(n_ms, 5), "value": round(total_recv / (n_ms * 1e-3) / 1e9, 3), "unit": "GB/s"}
+    # ---- multi-GPU sweep vs NCCL (N > 1): alltoall (one rank per GPU: NCCL all_to_all_single
+    #      has the same semantics) and allgather (process-level all_gather + replication) ----
+    nccl_sweep = None
+    if ws > 1 and args.sweep:
+        import torch.distributed as dist
+        nccl_sweep = {"timing": "eager loops, CUDA events, max over ranks; us per call",
+                      "columns": ["bytes_per_block", "mpxa_us", "nccl_us"], "alltoall": [], "allgather": []}
+        bmax = 16 << 20
+        a_send = torch.randint(0, 256, (R, p * bmax), dtype=torch.uint8, device="cuda")
+        a_recv = torch.empty_like(a_send)
+        comm.register(a_recv)
+        for bb in (4096, 65536, 1 << 20, 16 << 20):
+            it = 20 if bb < (1 << 20) else 5
+            if R == 1:
+                s_ = a_send.view(-1)[: p * bb].view(1, p * bb)
+                r_ = a_recv.view(-1)[: p * bb].view(1, p * bb)
+                m_ms = time_loop(lambda: comm.alltoall(s_, r_, algo="pairwise", stream=stream), it, 3, stream, ws)
+                n_ms = time_loop(lambda: dist.all_to_all_single(r_.view(-1), s_.view(-1)), it, 3, stream, ws)
+                nccl_sweep["alltoall"].append([bb, round(m_ms * 1e3, 2), round(n_ms * 1e3, 2)])
+            s2 = a_send.view(-1)[: R * bb].view(R, bb)
+            r2 = a_recv.view(-1)[: R * p * bb].view(R, p * bb)
+            g2 = torch.empty((N, R * bb), dtype=torch.uint8, device="cuda")
+
+            def ag_nccl():
+                dist.all_gather_into_tensor(g2, s2.view(-1))
+                r2.copy_(g2.view(1, p * bb).expand(R, p * bb))
+            m_ms = time_loop(lambda: comm.allgather(s2, r2, algo="pairwise", stream=stream), it, 3, stream, ws)
+            n_ms = time_loop(ag_nccl, it, 3, stream, ws)
+            nccl_sweep["allgather"].append([bb, round(m_ms * 1e3, 2), round(n_ms * 1e3, 2)])
+        del a_send, a_recv
     sw = None
     cfgs = None
     if args.sweep and ws == 1:
@@ -659,7 +689,7 @@ def gpu_arm(args):
                          "peak_source": peak_note,
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "kernel": "mpxa_exec_kernel (one launch per step; CUDA events on its stream)"},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "nccl": nccl,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "nccl": nccl, "nccl_sweep": nccl_sweep,
             "clocks": clk.report(), "sweep": sw, "configs": cfgs,
         }
         if args.traffic is not None:
