@@ -1314,13 +1314,22 @@ cudaError_t launch_exec(const ExecParams &P, int nC, int nG, bool cooperative, b
 // f3: partitioned point-to-point.  Cycle counters and flags live in the
 // comm's partition heap; the sender's partitions go straight into the receiver's buffer.
 // ------------------------------------------------------------------------------------
+// (all partitioned kernels are PDL launches: they wait for the preceding kernel's completion
+// before touching anything, then let the next launch start its own prologue)
+__device__ __forceinline__ void part_enter() {
+    griddep_wait();
+    griddep_launch_dependents();
+}
+
 __global__ void part_start_send(unsigned long long *scycle) {
+    part_enter();
     if (threadIdx.x == 0) *scycle += 1ull;
 }
 
 // receiver enters the next cycle: everything stream-ordered before it (its consumers of the
 // previous cycle) is done, so the sender may overwrite the buffer -> clear-to-send
 __global__ void part_start_recv(unsigned long long *rcycle, unsigned long long *cts_remote) {
+    part_enter();
     if (threadIdx.x == 0) {
         const unsigned long long c = *rcycle + 1ull;
         *rcycle = c;
@@ -1332,6 +1341,7 @@ __global__ void part_start_recv(unsigned long long *rcycle, unsigned long long *
 // host-enqueued Pready of sender partitions [p0, p0 + gridDim.x / nct): nct CTAs per partition
 __global__ void __launch_bounds__(256) part_pready(mpxa_psend_dev_t ch, int p0, unsigned long long chunk,
                                                    unsigned int nct) {
+    part_enter();
     const int i = p0 + (int)(blockIdx.x / nct);
     const unsigned long long k = blockIdx.x % nct;
     const unsigned long long lo = k * chunk;
@@ -1342,6 +1352,7 @@ __global__ void __launch_bounds__(256) part_pready(mpxa_psend_dev_t ch, int p0, 
 // stream-ordered Parrived / completion: block until flags[lo, hi) >= *cycle (one CTA)
 __global__ void part_wait_flags(const unsigned long long *flags, int lo, int hi, const unsigned long long *cycle,
                                 int *err, long long timeout_ns) {
+    part_enter();
     __shared__ unsigned long long want;
     if (threadIdx.x == 0) want = *(volatile const unsigned long long *)cycle;
     __syncthreads();
@@ -1358,11 +1369,24 @@ __global__ void part_wait_flags(const unsigned long long *flags, int lo, int hi,
     }
 }
 
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t stream, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 cudaError_t launch_part_start(bool sender, unsigned long long *cycle, unsigned long long *cts_remote,
                               cudaStream_t stream) {
-    if (sender) part_start_send<<<1, 32, 0, stream>>>(cycle);
-    else part_start_recv<<<1, 32, 0, stream>>>(cycle, cts_remote);
-    return cudaGetLastError();
+    if (sender) return launch_pdl(part_start_send, dim3(1), dim3(32), stream, cycle);
+    return launch_pdl(part_start_recv, dim3(1), dim3(32), stream, cycle, cts_remote);
 }
 
 cudaError_t launch_part_pready(const mpxa_psend_dev_t &ch, int p0, int np, cudaStream_t stream) {
@@ -1376,14 +1400,13 @@ cudaError_t launch_part_pready(const mpxa_psend_dev_t &ch, int p0, int np, cudaS
     const unsigned long long ch16 = (per + 15) & ~15ull;
     nct = ch16 ? (ch.part_bytes + ch16 - 1) / ch16 : 1;
     if (nct < 1) nct = 1;
-    part_pready<<<(unsigned)(np * nct), 256, 0, stream>>>(ch, p0, ch16 ? ch16 : 1, (unsigned)nct);
-    return cudaGetLastError();
+    return launch_pdl(part_pready, dim3((unsigned)(np * nct)), dim3(256), stream, ch, p0,
+                      (unsigned long long)(ch16 ? ch16 : 1), (unsigned)nct);
 }
 
 cudaError_t launch_part_wait(const unsigned long long *flags, int lo, int hi, const unsigned long long *cycle,
                              int *err, long long timeout_ns, cudaStream_t stream) {
-    part_wait_flags<<<1, 256, 0, stream>>>(flags, lo, hi, cycle, err, timeout_ns);
-    return cudaGetLastError();
+    return launch_pdl(part_wait_flags, dim3(1), dim3(256), stream, flags, lo, hi, cycle, err, timeout_ns);
 }
 
 cudaError_t launch_counts(const int64_t *sc, int64_t *rc, int64_t *rd, int p, int r0, int nr,
