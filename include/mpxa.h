@@ -133,7 +133,8 @@ int mpxa_alltoall(const void *sendbuf, size_t count, size_t dtype_size, void *re
 /* count elements of dtype_size bytes contributed by every rank. */
 int mpxa_allgather(const void *sendbuf, size_t count, size_t dtype_size, void *recvbuf,
                    mpxa_comm_t comm, mpxa_stream_t stream);
-/* R*p int64 counts/displacements (host pointers), in elements. */
+/* R*p int64 counts/displacements in elements (host or device pointers; device arrays are
+ * copied to the host synchronously). */
 int mpxa_alltoallv(const void *sendbuf, const int64_t *sendcounts, const int64_t *sdispls,
                    size_t send_bytes_per_rank, void *recvbuf, const int64_t *recvcounts,
                    const int64_t *rdispls, size_t recv_bytes_per_rank, size_t dtype_size,

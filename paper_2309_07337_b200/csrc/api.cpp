@@ -670,11 +670,34 @@ int check_uniform(mpxa_comm_t c, const void *send, size_t count, size_t w, void 
 // Gather the FULL count/displacement matrices a v-schedule needs.  Single process: the
 // caller's R*p rows are all p rows.  Multi-process: all-gather through the bootstrap
 // (host collective; persistent requests pay it once at init).
+// counts / displacements may live in device memory (SURVEY.md §8(b) ownership): such arrays
+// are copied to the host first (a synchronous copy -- the persistent forms pay it once)
+int host_view(const int64_t *&a, size_t n, std::vector<int64_t> &store) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, a) != cudaSuccess) {
+        cudaGetLastError();   // unregistered host memory on older drivers: treat as host
+        return MPXA_SUCCESS;
+    }
+    if (at.type == cudaMemoryTypeDevice) {
+        store.resize(n);
+        CK(cudaMemcpy(store.data(), a, n * sizeof(int64_t), cudaMemcpyDeviceToHost));
+        a = store.data();
+    }
+    return MPXA_SUCCESS;
+}
+
 int gather_v(mpxa_comm_t c, const int64_t *sc, const int64_t *sd, const int64_t *rc,
              const int64_t *rd, size_t w, size_t send_bpr, size_t recv_bpr,
              std::vector<int64_t> &C, std::vector<int64_t> &SD, std::vector<int64_t> &RD) {
     const int p = c->p, R = c->R;
     if (!sc || !sd || !rc || !rd) return MPXA_ERR_ARG;
+    std::vector<int64_t> hs[4];
+    const size_t nrows = (size_t)R * p;
+    int hr = host_view(sc, nrows, hs[0]);
+    if (!hr) hr = host_view(sd, nrows, hs[1]);
+    if (!hr) hr = host_view(rc, nrows, hs[2]);
+    if (!hr) hr = host_view(rd, nrows, hs[3]);
+    if (hr) return hr;
     for (int t = 0; t < R; t++)
         for (int j = 0; j < p; j++) {
             size_t i = (size_t)t * p + j;

@@ -171,6 +171,17 @@ def _host_i64(a):
     return a, a.ctypes.data_as(ctypes.c_void_p)
 
 
+def _i64_arg(a):
+    """(keep-alive, pointer) of an int64 array argument: a CUDA int64 tensor is passed as a
+    device pointer (the library copies it), anything else as a host array."""
+    if hasattr(a, "is_cuda") and a.is_cuda:
+        import torch
+        if a.dtype != torch.int64 or not a.is_contiguous():
+            raise ValueError("device counts / displacements must be contiguous int64 tensors")
+        return a, ctypes.c_void_p(a.data_ptr())
+    return _host_i64(a)
+
+
 def list_algorithms(op: str):
     n = ctypes.c_int(8)
     out = (ctypes.c_int * 8)()
@@ -286,10 +297,10 @@ class Comm:
     def alltoallv(self, send, sendcounts, sdispls, recv, recvcounts, rdispls, algo=None, stream=None,
                   dtype_size: Optional[int] = None):
         w = send.element_size() if dtype_size is None else dtype_size
-        sc, scp = _host_i64(sendcounts)
-        sd, sdp = _host_i64(sdispls)
-        rc, rcp = _host_i64(recvcounts)
-        rd, rdp = _host_i64(rdispls)
+        sc, scp = _i64_arg(sendcounts)
+        sd, sdp = _i64_arg(sdispls)
+        rc, rcp = _i64_arg(recvcounts)
+        rd, rdp = _i64_arg(rdispls)
         sbpr = send.numel() * send.element_size() // self.R
         rbpr = recv.numel() * recv.element_size() // self.R
         _ck(_lib().mpxa_alltoallv_algo(_ptr(send), scp, sdp, sbpr, _ptr(recv), rcp, rdp, rbpr, w, _algo(algo),
@@ -327,7 +338,7 @@ class Comm:
     def alltoallv_init(self, send, sendcounts, sdispls, recv, recvcounts, rdispls, algo=None,
                        dtype_size: Optional[int] = None) -> Request:
         w = send.element_size() if dtype_size is None else dtype_size
-        arrs = [_host_i64(a) for a in (sendcounts, sdispls, recvcounts, rdispls)]
+        arrs = [_i64_arg(a) for a in (sendcounts, sdispls, recvcounts, rdispls)]
         sbpr = send.numel() * send.element_size() // self.R
         rbpr = recv.numel() * recv.element_size() // self.R
         h = ctypes.c_void_p()

@@ -472,3 +472,27 @@ def test_one_shot_alltoallv_program_cache():
             c.alltoallv(dev(send.view(np.int64)), sc, sd, d_recv.view(torch.int64), rc, rd)
             want = oracle.alltoallv_definition(send, sc, sd, rc, rd, 8, recv0)
             assert np.array_equal(host(d_recv), want), (rep, seed)
+
+
+def test_alltoallv_device_counts_pipeline():
+    """cfg4's "counts/displs exchanged then data" entirely on the device: sendcounts on the
+    GPU -> mpxa_alltoallv_counts (A2) -> recvcounts / rdispls on the GPU -> alltoallv and the
+    persistent init taking the device arrays (copied by the library)."""
+    p = 8
+    c4 = synth.cfg4_counts(3, p, 4096)
+    send, sc, sd, rc, rd, S, Rcap = synth.alltoallv_buffers(3, c4, elem=8, packed=True)
+    want = oracle.alltoallv_definition(send, sc, sd, rc, rd, 8, np.zeros((p, Rcap), np.uint8))
+    for G in (0, 2):
+        c = comm(p, G)
+        d_sc = dev(sc)
+        d_rc, d_rd = torch.zeros_like(d_sc), torch.zeros_like(d_sc)
+        c.alltoallv_counts(d_sc, d_rc, d_rd)
+        d_sd = dev(sd)
+        d_recv = torch.zeros((p, Rcap // 8), dtype=torch.int64, device=DEV)
+        c.alltoallv(dev(send.view(np.int64)), d_sc, d_sd, d_recv, d_rc, d_rd)
+        assert np.array_equal(host(d_recv).view(np.uint8), want), G
+        d_recv.zero_()
+        req = c.alltoallv_init(dev(send.view(np.int64)), d_sc, d_sd, d_recv, d_rc, d_rd)
+        req.start(); req.wait()
+        assert np.array_equal(host(d_recv).view(np.uint8), want), G
+        req.free()
