@@ -201,6 +201,7 @@ struct mpxa_comm_s {
     uint64_t dyn_min_total = kDynMinTotal;    // MPXA_DYN_MIN: smallest busiest-GPU volume (tuning)
     int force_sync = -1;                      // MPXA_DYN_SYNC=0/1: force multi-step dynamic mode (tuning)
     uint64_t small_max1 = kSmallOneStepMove;  // MPXA_SMALL_MAX: longest move of one-step small launches
+    uint64_t small_vol1 = kSmallOneStepVol;   // MPXA_SMALL_VOL: their source bytes per GPU (tuning)
 
     SymRegion *sym_local = nullptr;            // G regions when emulated, else 1
     SymRegion *sym_map[kMaxGpus] = {};
@@ -541,7 +542,7 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
     // alltoallv cfg4 64 KiB mean 9.2 -> 5.2 us); beyond, the executor streams better.
     const uint64_t src_vol = (uint64_t)dp.max_gpu_bytes_units * unit;
     const bool small = !c->force_exec &&
-                       (one_step ? (maxmove <= c->small_max1 && src_vol <= kSmallOneStepVol)
+                       (one_step ? (maxmove <= c->small_max1 && src_vol <= c->small_vol1)
                                  : (maxmove <= kSmallKernelMax && items <= kSmallItemsOneCta));
     if (small) {
         E.nS = E.nF = 1;
@@ -1012,6 +1013,7 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     if (const char *e = getenv("MPXA_DYN_MIN")) c->dyn_min_total = strtoull(e, nullptr, 10);
     if (const char *e = getenv("MPXA_DYN_SYNC")) c->force_sync = atoi(e);
     if (const char *e = getenv("MPXA_SMALL_MAX")) c->small_max1 = strtoull(e, nullptr, 10);
+    if (const char *e = getenv("MPXA_SMALL_VOL")) c->small_vol1 = strtoull(e, nullptr, 10);
     CK(cudaHostAlloc((void **)&c->err_host, sizeof(int32_t), cudaHostAllocMapped));
     *c->err_host = 0;
     CK(cudaHostGetDevicePointer((void **)&c->err_dev, c->err_host, 0));
