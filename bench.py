@@ -338,12 +338,27 @@ def configs_on_one_gpu(torch, reps=20):
         torch.cuda.synchronize()
         us_o = e0.elapsed_time(e1) * 1e3 / 20
         req.free()
+        # the other alltoallv variants (persistent, graph-timed, verified): hierarchical with
+        # groups of 2 ranks and Bruck-v
+        others = {}
+        cg = Comm(ranks_per_proc=p, device=torch.cuda.current_device(), group_size=2)
+        for algo in ("hier", "bruck"):
+            d_r.fill_(0xA5)
+            rq = cg.alltoallv_init(d_s, sc, sd, d_r, rc, rd, dtype_size=8, algo=algo)
+            rq.start(gstream); rq.wait(gstream)
+            torch.cuda.synchronize()
+            ok_a = bool(np.array_equal(d_r.cpu().numpy(), want))
+            us_a = 1e3 * time_graph(lambda: (rq.start(gstream), rq.wait(gstream)), 20, gstream)
+            others[algo] = {"persistent_graph_us": round(us_a, 3), "verified": ok_a}
+            rq.free()
+        cg.finalize()
         out[f"mean_{mean}B"] = {"bytes_moved": moved, "verified": ok,
                                 "persistent_start_wait_us": round(us_p, 3),
                                 "persistent_graph_us": round(us_g, 3),
                                 "one_shot_us": round(us_o, 3),
                                 "GBps_persistent": round(moved / us_p / 1e3, 2),
-                                "hbm_TBps_persistent_graph": round(2 * moved / us_g / 1e6, 3)}
+                                "hbm_TBps_persistent_graph": round(2 * moved / us_g / 1e6, 3),
+                                "other_variants": others}
         del d_s, d_r
     res["cfg4_alltoallv_p8_persistent_100x"] = out
     c.finalize()
