@@ -66,6 +66,8 @@ constexpr uint64_t kBigPerCta = 1u << 20;  // bytes per CTA per step above which
 constexpr uint64_t kSmallItemsPerCta = 2048;   // small kernel: 16-B pieces per CTA per step (one batch)
 constexpr uint64_t kSmallOneStepMove = 1u << 20;   // single-step programs: longest move ...
 constexpr uint64_t kSmallOneStepVol = 16u << 20;   // ... and source bytes per GPU for the small kernel
+constexpr uint64_t kSmallSyncMove = 256u << 10;    // multi-step small launches on several CTAs:
+constexpr uint64_t kSmallSyncVol = 8u << 20;       //   longest move, busiest step
 constexpr uint64_t kSmallItemsOneCta = 2048;   // multi-step programs: largest step one CTA handles
 constexpr uint64_t kDynMinMove = 128u << 10;   // dynamic mode: smallest average move (bytes) when
 constexpr uint64_t kDynBigTotal = 128u << 20;  //   the busiest GPU moves this much, else ...
@@ -200,6 +202,7 @@ struct mpxa_comm_s {
     int dyn_pieces = (int)kDynPiecesPerCta;   // MPXA_DYN_PIECES: queue pieces per CTA (tuning)
     uint64_t dyn_min_total = kDynMinTotal;    // MPXA_DYN_MIN: smallest busiest-GPU volume (tuning)
     int force_sync = -1;                      // MPXA_DYN_SYNC=0/1: force multi-step dynamic mode (tuning)
+    bool small_sync = true;                   // MPXA_NO_SMALL_SYNC=1: multi-step small launches in one CTA
     uint64_t small_max1 = kSmallOneStepMove;  // MPXA_SMALL_MAX: longest move of one-step small launches
     uint64_t small_vol1 = kSmallOneStepVol;   // MPXA_SMALL_VOL: their source bytes per GPU (tuning)
 
@@ -541,9 +544,18 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
     // fixed costs there (alltoall 64 KiB blocks 5.3 -> 3.8 us, allgather 1 MiB 17.9 -> 13.8 us,
     // alltoallv cfg4 64 KiB mean 9.2 -> 5.2 us); beyond, the executor streams better.
     const uint64_t src_vol = (uint64_t)dp.max_gpu_bytes_units * unit;
+    // multi-step programs too large for one CTA but small in volume: several CTAs with a
+    // barrier between steps (sync mode)
+    const uint64_t step_vol = (uint64_t)dp.host.max_step_units * unit;
+    // (measured: it wins where the static executor is poorly balanced -- uneven moves, or few
+    // flows to spread over CTAs as in the allgathers; uniform alltoalls keep the barrier-free
+    // static executor)
+    const bool small_sync = !one_step && items > kSmallItemsOneCta && maxmove <= kSmallSyncMove &&
+                            step_vol <= kSmallSyncVol && c->small_sync &&
+                            (!dp.uniform_len || dp.host.nflows < 32);
     const bool small = !c->force_exec &&
                        (one_step ? (maxmove <= c->small_max1 && src_vol <= c->small_vol1)
-                                 : (maxmove <= kSmallKernelMax && items <= kSmallItemsOneCta));
+                                 : ((maxmove <= kSmallKernelMax && items <= kSmallItemsOneCta) || small_sync));
     if (small) {
         E.nS = E.nF = 1;
         E.small_a16 = unit % 16 == 0 && (uintptr_t)send % 16 == 0 && (uintptr_t)recv % 16 == 0 &&
@@ -552,7 +564,9 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
         size_t nmoves_g = 0;
         for (const auto &mv : dp.host.moves) nmoves_g = std::max(nmoves_g, mv.size());
         E.small_cache = nmoves_g <= (size_t)kSmallMovesSmem ? (int32_t)nmoves_g : 0;
-        int nC = one_step ? (int)std::min<uint64_t>(cdiv(items, kSmallItemsPerCta), (uint64_t)c->cap_small) : 1;
+        int nC = (one_step || small_sync) ? (int)std::min<uint64_t>(cdiv(items, kSmallItemsPerCta), (uint64_t)c->cap_small)
+                                          : 1;
+        E.dyn_sync = small_sync && nC > 1;
         e = launch_small(E, std::max(1, nC), c->emulated ? c->G : 1, c->emulated, pdl && c->pdl, stream);
     } else {
         int nC = gr.n();
@@ -1012,6 +1026,7 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     if (const char *e = getenv("MPXA_DYN_PIECES")) c->dyn_pieces = std::max(1, atoi(e));
     if (const char *e = getenv("MPXA_DYN_MIN")) c->dyn_min_total = strtoull(e, nullptr, 10);
     if (const char *e = getenv("MPXA_DYN_SYNC")) c->force_sync = atoi(e);
+    if (const char *e = getenv("MPXA_NO_SMALL_SYNC")) c->small_sync = atoi(e) == 0;
     if (const char *e = getenv("MPXA_SMALL_MAX")) c->small_max1 = strtoull(e, nullptr, 10);
     if (const char *e = getenv("MPXA_SMALL_VOL")) c->small_vol1 = strtoull(e, nullptr, 10);
     CK(cudaHostAlloc((void **)&c->err_host, sizeof(int32_t), cudaHostAllocMapped));

@@ -1119,6 +1119,30 @@ __device__ __forceinline__ void small_wait(const ExecParams &P, SmallShared &S, 
     }
 }
 
+// multi-step small launches over several CTAs (ExecParams::dyn_sync): the CTAs of a GPU row
+// meet at a counter barrier between steps (every CTA of the launch is co-resident)
+__device__ __noinline__ void small_row_barrier(const ExecParams &P, SmallShared &S, int g, int s) {
+    if (threadIdx.x == 0) {
+        uint32_t *bar = &P.dc->dyn_bar[g];
+        __threadfence();
+        atomicAdd(bar, 1u);
+        const uint32_t want = (uint32_t)(s + 1) * gridDim.x;
+        uint64_t t0 = 0;
+        int it = 0;
+        for (;;) {
+            uint32_t v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+            if (v >= want) break;
+            if (++it > 16) {
+                __nanosleep(32);
+                if (!t0) t0 = globaltimer();
+                else if ((int64_t)(globaltimer() - t0) > P.timeout_ns) { atomicExch(P.err, 1); S.abort_flag = 1; break; }
+            }
+        }
+    }
+    __syncthreads();
+}
+
 // items = (move, 16-byte piece); thread takes items base0, base0 + TT, ... kBatch at a time
 template <bool A16>
 __device__ __forceinline__ void small_items(const ExecParams &P, const SmallShared &S, const Move *mv, uint32_t items,
@@ -1215,8 +1239,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
             const Step g_st = prog.steps[s];
             st = StepInfo{g_st.move_begin, g_st.move_end - g_st.move_begin, g_st.signal_mask, g_st.wait_mask};
         }
+        const int fslot = P.dyn_sync ? 0 : (int)blockIdx.x;   // the row's flag in sync mode
         if (multi) {
-            if (prev_wait) small_wait(P, S, prev_wait, &S.sym[g]->flags[0][blockIdx.x], kMaxCtas, (epoch << 8) | (uint64_t)s);
+            if (prev_wait) small_wait(P, S, prev_wait, &S.sym[g]->flags[0][fslot], kMaxCtas, (epoch << 8) | (uint64_t)s);
             const uint32_t need = st.signal_mask & ~S.cts_ok;
             if (need) {
                 small_wait(P, S, need, &S.sym[g]->cts[0].epoch, sizeof(CtsSlot) / 8, epoch);
@@ -1246,21 +1271,28 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
         TRACE(2);
         __syncthreads();
         TRACE(3);
-        if (multi && st.signal_mask && t < 32 && ((st.signal_mask >> t) & 1u)) {
+        if (P.dyn_sync && (s + 1 < prog.nsteps || (multi && st.signal_mask))) {
+            small_row_barrier(P, S, g, s);
+            if (S.abort_flag) return;
+        }
+        if (multi && st.signal_mask && t < 32 && ((st.signal_mask >> t) & 1u) && (!P.dyn_sync || blockIdx.x == 0)) {
             __threadfence_system();
-            st_release_sys(&S.sym[t]->flags[g][blockIdx.x], (epoch << 8) | (uint64_t)(s + 1));
+            st_release_sys(&S.sym[t]->flags[g][fslot], (epoch << 8) | (uint64_t)(s + 1));
         }
         prev_wait = st.wait_mask;
     }
     if (multi && prev_wait) {
-        small_wait(P, S, prev_wait, &S.sym[g]->flags[0][blockIdx.x], kMaxCtas, (epoch << 8) | (uint64_t)prog.nsteps);
+        small_wait(P, S, prev_wait, &S.sym[g]->flags[0][P.dyn_sync ? 0 : (int)blockIdx.x], kMaxCtas,
+                   (epoch << 8) | (uint64_t)prog.nsteps);
         __syncthreads();
     }
-    if (multi && t == 0) {
+    if ((multi || P.dyn_sync) && t == 0) {
         __threadfence();
         if (atomicAdd(&P.dc->done_ctas, 1u) == gridDim.x * gridDim.y - 1) {
             P.dc->done_ctas = 0;
-            P.dc->epoch = epoch;
+            if (multi) P.dc->epoch = epoch;
+            if (P.dyn_sync)
+                for (int r = 0; r < (int)gridDim.y; r++) P.dc->dyn_bar[P.mode == 1 ? r : P.my_gpu] = 0;
             __threadfence();
         }
     }

@@ -496,3 +496,27 @@ def test_alltoallv_device_counts_pipeline():
         req.start(); req.wait()
         assert np.array_equal(host(d_recv).view(np.uint8), want), G
         req.free()
+
+
+@pytest.mark.parametrize("G", [0, 2])
+def test_small_sync_mode_multistep(G):
+    """Multi-step programs with short moves but more pieces than one CTA holds run the
+    small-message kernel on several CTAs with a barrier per step (allgather Bruck / ring,
+    hierarchical and Bruck alltoallv at mid sizes): exact vs the oracle."""
+    p = 8
+    c = comm(p, G, 2)
+    for b in (1024, 4096 + 8, 65536):
+        ag = np.random.default_rng(b).integers(0, 256, size=(p, b), dtype=np.uint8)
+        want = oracle.allgather_definition(ag)
+        for algo in ("bruck", "ring"):
+            d_r = torch.full((p, p * b), 0x5A, dtype=torch.uint8, device=DEV)
+            c.allgather(dev(ag), d_r, algo=algo)
+            assert np.array_equal(host(d_r), want), (b, algo, G)
+    c4 = synth.cfg4_counts(5, p, 16384)
+    send, sc, sd, rc, rd, S, Rcap = synth.alltoallv_buffers(5, c4, elem=8, packed=False)
+    recv0 = np.full((p, Rcap), 0xA5, dtype=np.uint8)
+    want = oracle.alltoallv_definition(send, sc, sd, rc, rd, 8, recv0)
+    for algo in ("hier", "bruck"):
+        d_recv = dev(recv0)
+        c.alltoallv(dev(send.view(np.int64)), sc, sd, d_recv.view(torch.int64), rc, rd, algo=algo)
+        assert np.array_equal(host(d_recv), want), (algo, G)
