@@ -1062,6 +1062,7 @@ constexpr int kRankTable = 256;   // small kernel: per-rank buffer bases kept in
 
 struct SmallShared {
     StepInfo steps[kMaxStepsSmem];   // step table, loaded in the prologue (before griddep wait)
+    uint32_t n_own;                  // owned-flow mode: moves of this step owned by this CTA
     char *rb[3][kRankTable];         // [kind][rank] buffer base (p <= kRankTable): no divisions
     char *recv_base[kMaxGpus];
     char *work_base[kMaxGpus];
@@ -1146,7 +1147,7 @@ __device__ __noinline__ void small_row_barrier(const ExecParams &P, SmallShared 
 // items = (move, 16-byte piece); thread takes items base0, base0 + TT, ... kBatch at a time
 template <bool A16>
 __device__ __forceinline__ void small_items(const ExecParams &P, const SmallShared &S, const Move *mv, uint32_t items,
-                                            uint32_t lg, uint32_t TT, uint32_t base0) {
+                                            uint32_t lg, uint32_t TT, uint32_t base0, const uint16_t *idx) {
     const uint32_t mask = (1u << lg) - 1u;   // pieces per move: a power of two (host-rounded)
     for (uint32_t base = base0; base < items; base += TT * kBatch) {
         PieceRegs<A16> R;
@@ -1156,7 +1157,7 @@ __device__ __forceinline__ void small_items(const ExecParams &P, const SmallShar
             sp[k] = nullptr;
             const uint32_t it = base + (uint32_t)k * TT;
             if (it >= items) continue;
-            const Move &m = mv[it >> lg];
+            const Move &m = mv[idx ? idx[it >> lg] : (it >> lg)];
             const uint32_t n = (uint32_t)((uint64_t)m.len * P.unit), o = (it & mask) * 16;
             if (o >= n) continue;
             sp[k] = sb(P, S, m.src_kind, m.src_rank) + (uint64_t)m.src_off * P.unit + o;
@@ -1167,7 +1168,7 @@ __device__ __forceinline__ void small_items(const ExecParams &P, const SmallShar
         for (int k = 0; k < kBatch; k++) {
             if (!sp[k]) continue;
             const uint32_t it = base + (uint32_t)k * TT;
-            const Move &m = mv[it >> lg];
+            const Move &m = mv[idx ? idx[it >> lg] : (it >> lg)];
             const uint32_t n = (uint32_t)((uint64_t)m.len * P.unit), o = (it & mask) * 16;
             const uint32_t len = min(16u, n - o);
             const uint64_t doff = (uint64_t)m.dst_off * P.unit + o;
@@ -1258,16 +1259,30 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
         }
         // items = (move, 16-byte piece); thread t takes items t, t+T, ... four at a time:
         // all four loads in flight before the stores
-        const uint32_t items = (uint32_t)st.nm * ppm;
-        const uint32_t TT = gridDim.x * kSmallThreads;   // several CTAs only for 1-step programs
+        uint32_t items = (uint32_t)st.nm * ppm;
+        uint32_t TT = gridDim.x * kSmallThreads;
+        uint32_t base0 = blockIdx.x * kSmallThreads + t;
+        const uint16_t *idx = nullptr;
+        if (P.small_own) {          // this CTA's flows only (compacted move list), all its threads
+            uint16_t *own = reinterpret_cast<uint16_t *>(small_dyn + (size_t)P.small_cache * sizeof(Move));
+            if (t == 0) S.n_own = 0;
+            __syncthreads();
+            for (int i = t; i < st.nm; i += kSmallThreads)
+                if ((int)(mvs[st.first + i].flow % (uint32_t)P.small_own) == (int)blockIdx.x)
+                    own[atomicAdd(&S.n_own, 1u)] = (uint16_t)i;
+            __syncthreads();
+            items = S.n_own * ppm;
+            TT = kSmallThreads;
+            base0 = t;
+            idx = own;
+        }
         // 16-B fast path: the host vouched for every local offset / length / base, and the
         // recv bases of the peers written in this step arrived with their CTS
         bool a16 = P.small_a16 != 0;
         for (int q = 0; q < P.G; q++)
             if (((st.signal_mask >> q) & 1u) && ((uintptr_t)S.recv_base[q] & 15)) a16 = false;
-        const uint32_t base0 = blockIdx.x * kSmallThreads + t;
-        if (a16) small_items<true>(P, S, mvs + st.first, items, lg, TT, base0);
-        else small_items<false>(P, S, mvs + st.first, items, lg, TT, base0);
+        if (a16) small_items<true>(P, S, mvs + st.first, items, lg, TT, base0, idx);
+        else small_items<false>(P, S, mvs + st.first, items, lg, TT, base0, idx);
         TRACE(2);
         __syncthreads();
         TRACE(3);
@@ -1323,9 +1338,10 @@ static cudaError_t launch_kernel(void (*kern)(ExecParams), const ExecParams &P, 
 
 cudaError_t launch_small(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream) {
     static cudaError_t attr = cudaFuncSetAttribute(mpxa_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)(kSmallMovesSmem * sizeof(Move)));
+                                                   (int)(kSmallMovesSmem * (sizeof(Move) + sizeof(uint16_t))));
     if (attr != cudaSuccess) return attr;
-    const size_t smem = P.small_cache ? (size_t)P.small_cache * sizeof(Move) : 0;
+    const size_t smem = (P.small_cache ? (size_t)P.small_cache * sizeof(Move) : 0) +
+                        (P.small_own ? (size_t)kSmallMovesSmem * sizeof(uint16_t) : 0);
     return launch_kernel(mpxa_small_kernel, P, dim3(nC, nG), dim3(kSmallThreads), smem, cooperative, pdl, stream);
 }
 

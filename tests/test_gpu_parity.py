@@ -520,3 +520,19 @@ def test_small_sync_mode_multistep(G):
         d_recv = dev(recv0)
         c.alltoallv(dev(send.view(np.int64)), sc, sd, d_recv.view(torch.int64), rc, rd, algo=algo)
         assert np.array_equal(host(d_recv), want), (algo, G)
+
+
+@pytest.mark.parametrize("G", [0, 2, 4])
+def test_small_owned_flow_mode_multistep(G):
+    """Uniform multi-step programs (Bruck, hierarchical, ring) with short moves on several
+    CTAs, each owning the same flows in every step (no barrier): exact vs the oracle, on one
+    device and across emulated GPUs (per-CTA flags)."""
+    p = 8
+    c = comm(p, G, 2)
+    for b in (1024, 4096 + 4, 16384):
+        send = np.random.default_rng(b).integers(0, 256, size=(p, p * b), dtype=np.uint8)
+        want = oracle.alltoall_definition(send)
+        for algo in ("bruck", "hier", "pairwise"):
+            d_r = torch.full((p, p * b), 0xA5, dtype=torch.uint8, device=DEV)
+            c.alltoall(dev(send), d_r, algo=algo)
+            assert np.array_equal(host(d_r), want), (b, algo, G)
