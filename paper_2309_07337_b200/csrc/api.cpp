@@ -68,7 +68,8 @@ constexpr uint64_t kSmallOneStepMove = 1u << 20;   // single-step programs: long
 constexpr uint64_t kSmallOneStepVol = 16u << 20;   // ... and source bytes per GPU for the small kernel
 constexpr uint64_t kSmallSyncMove = 256u << 10;    // multi-step small launches on several CTAs:
 constexpr uint64_t kSmallSyncVol = 8u << 20;       //   longest move, busiest step
-constexpr uint64_t kSmallOwnVol = 2u << 20;        // owned-flow mode: busiest step
+constexpr uint64_t kSmallOwnVol = 2u << 20;        // owned-flow mode: busiest step, and bytes per CTA
+constexpr uint64_t kSmallOwnPerCta = 64u << 10;    //   (few flows -> few CTAs: allgathers)
 constexpr uint64_t kSmallItemsOneCta = 2048;   // multi-step programs: largest step one CTA handles
 constexpr uint64_t kDynMinMove = 128u << 10;   // dynamic mode: smallest average move (bytes) when
 constexpr uint64_t kDynBigTotal = 128u << 20;  //   the busiest GPU moves this much, else ...
@@ -551,16 +552,19 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
     // (measured: it wins where the static executor is poorly balanced -- uneven moves, or few
     // flows to spread over CTAs as in the allgathers; uniform alltoalls keep the barrier-free
     // static executor)
+    const uint64_t n_own = std::max<uint64_t>(1, std::min<uint64_t>(std::min<uint64_t>(cdiv(items, kSmallItemsPerCta),
+                                                                                          (uint64_t)dp.host.nflows),
+                                                                     (uint64_t)c->cap_small));
+    const bool own_ok = dp.uniform_len && step_vol <= kSmallOwnVol && step_vol / n_own <= kSmallOwnPerCta;
     const bool small_sync = !one_step && items > kSmallItemsOneCta && maxmove <= kSmallSyncMove &&
-                            step_vol <= kSmallSyncVol && c->small_sync &&
+                            step_vol <= kSmallSyncVol && c->small_sync && !own_ok &&
                             (!dp.uniform_len || dp.host.nflows < 32);
     // uniform multi-step programs (flows of equal size, moved whole in every step): several
     // CTAs, each owning the flows f % nC == c through all steps -- no barrier needed
     // (measured, p=8: Bruck alltoall 4 KiB 13.9 -> 10.8 us, hier 9.8 -> 8.6 us at 16 KiB; from
     // 64 KiB blocks the TMA executor is faster again)
     const bool small_own = !one_step && !small_sync && items > kSmallItemsOneCta && maxmove <= kSmallSyncMove &&
-                           step_vol <= kSmallOwnVol && c->small_sync && dp.uniform_len &&
-                           dp.max_gpu_moves <= kSmallMovesSmem && dp.host.nflows >= 32;
+                           own_ok && c->small_sync && dp.max_gpu_moves <= kSmallMovesSmem;
     const bool small = !c->force_exec &&
                        (one_step ? (maxmove <= c->small_max1 && src_vol <= c->small_vol1)
                                  : ((maxmove <= kSmallKernelMax && items <= kSmallItemsOneCta) || small_sync ||
