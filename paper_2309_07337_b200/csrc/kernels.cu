@@ -472,9 +472,14 @@ __device__ __forceinline__ void store_piece(char *dp, uint4 v, uint32_t len) {
         return;
     }
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int b = 0; b < 16; b++)
-        if ((uint32_t)b < len) dp[b] = (char)(w[b >> 2] >> (8 * (b & 3)));
+    if ((len & 3) == 0 && (((uintptr_t)dp) & 3) == 0) {   // whole 4-byte words (e.g. 4-B elements)
+        uint32_t *d = (uint32_t *)dp;
+        d[0] = v.x;
+        if (len > 4) d[1] = v.y;
+        if (len > 8) d[2] = v.z;
+        return;
+    }
+    for (uint32_t b = 0; b < len; b++) dp[b] = (char)(w[b >> 2] >> (8 * (b & 3)));
 }
 
 // Batched copy of up to kBatch SMALL moves by one warp (n <= 512 B each): lane l moves bytes
