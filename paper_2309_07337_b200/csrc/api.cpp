@@ -96,6 +96,11 @@ struct DevProg {
     int64_t max_gpu_bytes_units = 0;  // single-step programs: most units any GPU moves (source side)
     int64_t dyn_tiles = 0;          // sum over steps of the most move tiles any GPU has in the step
     bool uniform_len = true;        // every move of the program has the same length
+    bool per_call = false;          // tables live in a ring slot (run_dynamic): no companions
+    // small-kernel variable-piece companion: the same program with long moves split
+    // (var_chop units each), built on first use for a unit, freed with its parent
+    mutable std::shared_ptr<DevProg> var;
+    mutable int64_t var_chop = 0;
 };
 
 // dynamic-mode eligibility facts of a program (DevProg::max_gpu_moves, max_gpu_bytes_units)
@@ -196,6 +201,8 @@ struct mpxa_comm_s {
     int sm_count = 148, cap_ctas = 296;   // cap_ctas: mid TMA config (2 CTAs / SM)
     int cap_big = 148;                     // big TMA config (1 CTA / SM)
     int cap_small = 148;                   // small-message kernel (1 CTA / SM)
+    int64_t var_chop = 32;                 // small kernel, variable pieces: longest move (bytes)
+    int var_tiles = 4;                     // ... and warp tiles (32 moves) per CTA
     int force_ns = 0, force_nf = 0;           // MPXA_NS / MPXA_NF overrides (tuning)
     int force_big = -1;                       // MPXA_TMA_BIG=0/1 override (tuning)
     bool force_exec = false;                  // MPXA_NO_SMALL=1: never use the small-message kernel
@@ -414,6 +421,66 @@ int upload_program(const Program &P, std::shared_ptr<DevProg> &out) {
     return MPXA_SUCCESS;
 }
 
+// The variable-piece companion of dp: moves longer than chop units become chop-unit moves
+// (same flow, order and kinds), so tiles of kSmallThreads moves carry comparable piece
+// counts and no CTA inherits a tile of whole long moves.  Small kernel only (no findex).
+int var_program(const DevProg &dp, int64_t chop, const DevProg *&out) {
+    if (!dp.var || dp.var_chop != chop) {
+        const Program &P = dp.host;
+        Program Q;
+        Q.p = P.p; Q.R = P.R; Q.G = P.G;
+        Q.nflows = P.nflows;
+        Q.work_units = P.work_units;
+        Q.max_step_units = P.max_step_units;
+        Q.signals = P.signals;
+        Q.max_move = std::min<int64_t>(P.max_move, chop);
+        Q.steps.resize(P.G);
+        Q.moves.resize(P.G);
+        Q.findex.assign(P.G, {});
+        for (int g = 0; g < P.G; g++)
+            for (const Step &st0 : P.steps[g]) {
+                Step st = st0;
+                st.move_begin = (int32_t)Q.moves[g].size();
+                for (int32_t i = st0.move_begin; i < st0.move_end; i++) {
+                    const Move &m = P.moves[g][i];
+                    int64_t o = 0;
+                    do {
+                        Move x = m;
+                        x.src_off += o;
+                        x.dst_off += o;
+                        x.len = std::min<int64_t>(chop, m.len - o);
+                        Q.moves[g].push_back(x);
+                        o += chop;
+                    } while (o < m.len);
+                }
+                st.move_end = (int32_t)Q.moves[g].size();
+                st.max_len = std::min<int64_t>(st.max_len, chop);
+                st.flow_index = 0;
+                st.dense_base = -1;
+                Q.max_step_moves = std::max<int64_t>(Q.max_step_moves, st.move_end - st.move_begin);
+                Q.steps[g].push_back(st);
+            }
+        auto v = std::shared_ptr<DevProg>(new DevProg, [](DevProg *d) {
+            if (d->dmem) cudaFree(d->dmem);
+            delete d;
+        });
+        size_t n = serialized_size(Q);
+        CK(cudaMalloc(&v->dmem, n ? n : 16));
+        std::vector<char> buf;
+        serialize(Q, buf, (uintptr_t)v->dmem);
+        CK(cudaMemcpy(v->dmem, buf.data(), n, cudaMemcpyHostToDevice));
+        v->gp.assign((const GpuProg *)buf.data(), (const GpuProg *)buf.data() + Q.G);
+        v->bytes = n;
+        v->host = std::move(Q);
+        v->nsteps = v->host.nsteps();
+        prog_facts(*v);
+        dp.var = v;
+        dp.var_chop = chop;
+    }
+    out = dp.var.get();
+    return MPXA_SUCCESS;
+}
+
 int cached_uniform(mpxa_comm_t c, int op, int algo, int stage, std::shared_ptr<DevProg> &out) {
     auto key = std::make_tuple(op, algo, stage, c->g);
     auto it = c->cache.find(key);
@@ -537,8 +604,13 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
     uint64_t ppm = 1;   // 16-B pieces per move, rounded up to a power of two (shift decode)
     while (ppm * 16 < maxmove) ppm <<= 1;
     // pieces per step, fan-out stores counted per destination (max_step_units counts them)
-    const uint64_t items = std::max<uint64_t>((uint64_t)dp.host.max_step_moves,
+    const uint64_t slots = std::max<uint64_t>((uint64_t)dp.host.max_step_moves,
                                               (uint64_t)dp.host.max_step_units / std::max<int64_t>(1, dp.host.max_move)) * ppm;
+    // moves of very different lengths (e.g. element runs next to whole blocks): max-move slots
+    // per move are mostly empty -- the small kernel then counts pieces exactly per tile of moves
+    const uint64_t exact = (uint64_t)dp.host.max_step_units * unit / 16 + (uint64_t)dp.host.max_step_moves;
+    const bool var = !dp.uniform_len && exact * 4 < slots;
+    const uint64_t items = var ? exact : slots;
     const bool one_step = dp.nsteps == 1;
     // Small-message kernel: multi-step programs with short moves and a step small enough for
     // one CTA; single-step programs (any number of CTAs) up to 1 MiB moves and 16 MiB of
@@ -557,8 +629,9 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
                                                                      (uint64_t)c->cap_small));
     const bool own_ok = dp.uniform_len && step_vol <= kSmallOwnVol && step_vol / n_own <= kSmallOwnPerCta;
     const bool small_sync = !one_step && items > kSmallItemsOneCta && maxmove <= kSmallSyncMove &&
-                            step_vol <= kSmallSyncVol && c->small_sync && !own_ok &&
-                            (!dp.uniform_len || dp.host.nflows < 32);
+                            step_vol <= kSmallSyncVol && c->small_sync &&
+                            (!own_ok || dp.max_gpu_moves > kSmallMovesSmem) &&
+                            (!dp.uniform_len || dp.host.nflows < 32 || dp.max_gpu_moves > kSmallMovesSmem);
     // uniform multi-step programs (flows of equal size, moved whole in every step): several
     // CTAs, each owning the flows f % nC == c through all steps -- no barrier needed
     // (measured, p=8: Bruck alltoall 4 KiB 13.9 -> 10.8 us, hier 9.8 -> 8.6 us at 16 KiB; from
@@ -574,14 +647,34 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
         E.small_a16 = unit % 16 == 0 && (uintptr_t)send % 16 == 0 && (uintptr_t)recv % 16 == 0 &&
                       send_stride % 16 == 0 && recv_stride % 16 == 0 && E.work_stride % 16 == 0;
         E.small_ppm = (int32_t)ppm;
+        const DevProg *sp = &dp;
+        // variable pieces: long moves split (companion program) unless the tables are per-call
+        // or the stream is being captured (the companion's upload is synchronous)
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        const int64_t chop = std::max<int64_t>(1, c->var_chop / (int64_t)unit);
+        if (var && !dp.per_call && c->var_chop > 0 && (uint64_t)dp.host.max_move * unit > (uint64_t)c->var_chop &&
+            ((dp.var && dp.var_chop == chop) ||
+             (cudaStreamIsCapturing(stream, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone))) {
+            rc = var_program(dp, chop, sp);
+            if (rc) return rc;
+            E.progs = (const GpuProg *)sp->dmem;
+            if (!c->emulated) E.prog = sp->gp[c->nprocs > 1 ? c->proc : 0];
+        }
         size_t nmoves_g = 0;
-        for (const auto &mv : dp.host.moves) nmoves_g = std::max(nmoves_g, mv.size());
+        for (const auto &mv : sp->host.moves) nmoves_g = std::max(nmoves_g, mv.size());
         E.small_cache = nmoves_g <= (size_t)kSmallMovesSmem ? (int32_t)nmoves_g : 0;
         int nC = (one_step || small_sync || small_own)
                      ? (int)std::min<uint64_t>(cdiv(items, kSmallItemsPerCta), (uint64_t)c->cap_small) : 1;
         if (small_own) nC = std::min<int>(nC, dp.host.nflows);
         E.dyn_sync = small_sync && nC > 1;
         E.small_own = small_own && nC > 1 ? nC : 0;
+        E.small_var = var && !E.small_own;
+        if (E.small_var) {   // warp tiles of 32 moves, about var_tiles per CTA
+            nC = (int)std::min<uint64_t>((uint64_t)c->cap_small,
+                                         std::max<uint64_t>(1, cdiv(cdiv((uint64_t)sp->host.max_step_moves, 32),
+                                                                    (uint64_t)c->var_tiles)));
+            E.dyn_sync = !one_step && nC > 1;
+        }
         e = launch_small(E, std::max(1, nC), c->emulated ? c->G : 1, c->emulated, pdl && c->pdl, stream);
     } else {
         int nC = gr.n();
@@ -667,6 +760,7 @@ int run_dynamic(mpxa_comm_t c, const Program &P, const char *send, char *recv, u
     memcpy(s.pinned, buf.data(), n);
     CK(cudaMemcpyAsync(s.dmem, s.pinned, n, cudaMemcpyHostToDevice, stream));
     DevProg dp;
+    dp.per_call = true;
     dp.dmem = s.dmem;
     dp.gp.assign((const GpuProg *)buf.data(), (const GpuProg *)buf.data() + P.G);
     dp.bytes = n;
@@ -1044,6 +1138,8 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     if (const char *e = getenv("MPXA_NO_SMALL_SYNC")) c->small_sync = atoi(e) == 0;
     if (const char *e = getenv("MPXA_SMALL_MAX")) c->small_max1 = strtoull(e, nullptr, 10);
     if (const char *e = getenv("MPXA_SMALL_VOL")) c->small_vol1 = strtoull(e, nullptr, 10);
+    if (const char *e = getenv("MPXA_VAR_CHOP")) c->var_chop = atoll(e);
+    if (const char *e = getenv("MPXA_VAR_TILES")) c->var_tiles = std::max(1, atoi(e));
     CK(cudaHostAlloc((void **)&c->err_host, sizeof(int32_t), cudaHostAllocMapped));
     *c->err_host = 0;
     CK(cudaHostGetDevicePointer((void **)&c->err_dev, c->err_host, 0));

@@ -1150,9 +1150,28 @@ __device__ __noinline__ void small_row_barrier(const ExecParams &P, SmallShared 
 }
 
 // items = (move, 16-byte piece); thread takes items base0, base0 + TT, ... kBatch at a time
-template <bool A16>
+// VAR: items are the exact pieces of a warp's tile of 32 moves mv[] (exclusive piece prefix
+// vpc[]): the move is the last j with vpc[j] <= it (moves past the tile's end carry the
+// tile total, zero-length ones share their successor's prefix and lose the search)
+template <bool VAR>
+__device__ __forceinline__ const Move &item_move(const Move *mv, const uint16_t *idx, const uint32_t *vpc, uint32_t it,
+                                                 uint32_t lg, uint32_t mask, uint32_t &o) {
+    if (VAR) {
+        int j = 0;
+#pragma unroll
+        for (int step = 16; step; step >>= 1)   // j + step <= 31 throughout
+            if (vpc[j + step] <= it) j += step;
+        o = (it - vpc[j]) * 16;
+        return mv[j];
+    }
+    o = (it & mask) * 16;
+    return mv[idx ? idx[it >> lg] : (it >> lg)];
+}
+
+template <bool A16, bool VAR = false>
 __device__ __forceinline__ void small_items(const ExecParams &P, const SmallShared &S, const Move *mv, uint32_t items,
-                                            uint32_t lg, uint32_t TT, uint32_t base0, const uint16_t *idx) {
+                                            uint32_t lg, uint32_t TT, uint32_t base0, const uint16_t *idx,
+                                            const uint32_t *vpc = nullptr) {
     const uint32_t mask = (1u << lg) - 1u;   // pieces per move: a power of two (host-rounded)
     for (uint32_t base = base0; base < items; base += TT * kBatch) {
         PieceRegs<A16> R;
@@ -1162,8 +1181,9 @@ __device__ __forceinline__ void small_items(const ExecParams &P, const SmallShar
             sp[k] = nullptr;
             const uint32_t it = base + (uint32_t)k * TT;
             if (it >= items) continue;
-            const Move &m = mv[idx ? idx[it >> lg] : (it >> lg)];
-            const uint32_t n = (uint32_t)((uint64_t)m.len * P.unit), o = (it & mask) * 16;
+            uint32_t o;
+            const Move &m = item_move<VAR>(mv, idx, vpc, it, lg, mask, o);
+            const uint32_t n = (uint32_t)((uint64_t)m.len * P.unit);
             if (o >= n) continue;
             sp[k] = sb(P, S, m.src_kind, m.src_rank) + (uint64_t)m.src_off * P.unit + o;
             R.issue(k, sp[k], min(16u, n - o));
@@ -1173,8 +1193,9 @@ __device__ __forceinline__ void small_items(const ExecParams &P, const SmallShar
         for (int k = 0; k < kBatch; k++) {
             if (!sp[k]) continue;
             const uint32_t it = base + (uint32_t)k * TT;
-            const Move &m = mv[idx ? idx[it >> lg] : (it >> lg)];
-            const uint32_t n = (uint32_t)((uint64_t)m.len * P.unit), o = (it & mask) * 16;
+            uint32_t o;
+            const Move &m = item_move<VAR>(mv, idx, vpc, it, lg, mask, o);
+            const uint32_t n = (uint32_t)((uint64_t)m.len * P.unit);
             const uint32_t len = min(16u, n - o);
             const uint64_t doff = (uint64_t)m.dst_off * P.unit + o;
             const uint4 val = R.value(k, sp[k]);
@@ -1187,6 +1208,45 @@ __device__ __forceinline__ void small_items(const ExecParams &P, const SmallShar
     }
 }
 
+// Variable-piece mode (P.small_var): one step of the small kernel.
+__device__ __forceinline__ void small_var_step(const ExecParams &P, const SmallShared &S, const Move *mvs, int first,
+                                            int nm, bool a16, char *small_dyn) {
+    const int t = threadIdx.x;
+    // warp tiles of 32 moves, round-robin over the grid's warps: one move per lane, a
+    // shuffle scan of their piece counts, then the lanes share the tile's pieces (no
+    // block barrier; the host split long moves so tiles carry comparable work).  The tile
+    // and its exclusive piece prefix live in dynamic shared memory after the cached moves.
+    const int lane = t & 31, warp = t >> 5;
+    Move *wm = reinterpret_cast<Move *>(small_dyn + (size_t)P.small_cache * sizeof(Move)) + warp * 32;
+    uint32_t *wp = reinterpret_cast<uint32_t *>(small_dyn + (size_t)(P.small_cache + kSmallThreads) * sizeof(Move)) +
+                   warp * 32;
+    const int nwt = (nm + 31) >> 5, W = kSmallThreads / 32;
+    for (int wt = (int)blockIdx.x * W + warp; wt < nwt; wt += (int)gridDim.x * W) {
+        __syncwarp();   // the previous tile is no longer read
+        const int i = wt * 32 + lane;
+        uint32_t pcs = 0;
+        if (i < nm) {
+            const Move m = mvs[first + i];
+            wm[lane] = m;
+            pcs = (uint32_t)(((uint64_t)m.len * P.unit + 15) / 16);
+        }
+        uint32_t inc = pcs;
+#pragma unroll
+        for (int o2 = 1; o2 < 32; o2 <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o2);
+            if (lane >= o2) inc += y;
+        }
+        wp[lane] = inc - pcs;
+        const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+        __syncwarp();
+        if (a16) small_items<true, true>(P, S, wm, tot, 0, 32, lane, nullptr, wp);
+        else small_items<false, true>(P, S, wm, tot, 0, 32, lane, nullptr, wp);
+    }
+}
+
+// VARK: the variable-piece instantiation (P.small_var), a kernel of its own -- compiled into
+// the common one its code cost every small launch ~8 % (registers / code layout, measured)
+template <bool VARK>
 __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __grid_constant__ ExecParams P) {
     __shared__ SmallShared S;
     extern __shared__ __align__(16) char small_dyn[];
@@ -1286,8 +1346,13 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
         bool a16 = P.small_a16 != 0;
         for (int q = 0; q < P.G; q++)
             if (((st.signal_mask >> q) & 1u) && ((uintptr_t)S.recv_base[q] & 15)) a16 = false;
-        if (a16) small_items<true>(P, S, mvs + st.first, items, lg, TT, base0, idx);
-        else small_items<false>(P, S, mvs + st.first, items, lg, TT, base0, idx);
+        if (VARK) {
+            small_var_step(P, S, mvs, st.first, st.nm, a16, small_dyn);
+        } else if (a16) {
+            small_items<true>(P, S, mvs + st.first, items, lg, TT, base0, idx);
+        } else {
+            small_items<false>(P, S, mvs + st.first, items, lg, TT, base0, idx);
+        }
         TRACE(2);
         __syncthreads();
         TRACE(3);
@@ -1342,12 +1407,18 @@ static cudaError_t launch_kernel(void (*kern)(ExecParams), const ExecParams &P, 
 }
 
 cudaError_t launch_small(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream) {
-    static cudaError_t attr = cudaFuncSetAttribute(mpxa_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    static cudaError_t attr = cudaFuncSetAttribute(mpxa_small_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)(kSmallMovesSmem * (sizeof(Move) + sizeof(uint16_t))));
+    static cudaError_t attr_v = cudaFuncSetAttribute(mpxa_small_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)(kSmallMovesSmem * sizeof(Move) +
+                                                           kSmallThreads * (sizeof(Move) + sizeof(uint32_t))));
     if (attr != cudaSuccess) return attr;
+    if (attr_v != cudaSuccess) return attr_v;
     const size_t smem = (P.small_cache ? (size_t)P.small_cache * sizeof(Move) : 0) +
-                        (P.small_own ? (size_t)kSmallMovesSmem * sizeof(uint16_t) : 0);
-    return launch_kernel(mpxa_small_kernel, P, dim3(nC, nG), dim3(kSmallThreads), smem, cooperative, pdl, stream);
+                        (P.small_own ? (size_t)kSmallMovesSmem * sizeof(uint16_t) : 0) +
+                        (P.small_var ? (size_t)kSmallThreads * (sizeof(Move) + sizeof(uint32_t)) : 0);
+    return launch_kernel(P.small_var ? mpxa_small_kernel<true> : mpxa_small_kernel<false>, P, dim3(nC, nG),
+                         dim3(kSmallThreads), smem, cooperative, pdl, stream);
 }
 
 static cudaError_t exec_attr_once() {

@@ -152,7 +152,8 @@ struct ExecParams {
     int32_t small_own;         // small kernel, multi-step on several CTAs without barriers: CTA c
                                // moves the flows f with f % small_own == c in every step (same
                                // owner across steps -> __syncthreads suffices); 0 = off
-    int32_t pad5;
+    int32_t small_var;         // small kernel: moves of very different lengths -- pieces counted
+                               // exactly per tile of moves (block scan) instead of max-move slots
     int32_t dyn_sync;          // multi-step dynamic mode: steps separated by a per-GPU-row CTA
                                // barrier and ONE flag per peer GPU (slot 0), so any CTA may move
                                // any piece (no flow ownership needed)

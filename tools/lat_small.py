@@ -1,0 +1,22 @@
+"""Small-message latency probe (device us per call, CUDA graphs): the small-kernel launches
+of the bench sweep at a few sizes.  One JSON line."""
+import json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2309_07337_b200 import Comm
+import tune_mid
+from tune_mid import t
+tune_mid.GS = GS = torch.cuda.Stream()
+res = {}
+for p in (4, 8):
+    c = Comm(ranks_per_proc=p, device=0)
+    for b in (16, 1024, 16384):
+        s = torch.randint(0, 255, (p, p * b), dtype=torch.uint8, device="cuda")
+        r = torch.empty_like(s)
+        for algo in ("pairwise", "bruck", "hier"):
+            res[f"a2a_p{p}_{algo}_{b}"] = round(t(lambda: c.alltoall(s, r, algo=algo, stream=GS), it=20), 2)
+        s2 = s[:, :b].contiguous()
+        for algo in ("pairwise", "bruck", "ring"):
+            res[f"ag_p{p}_{algo}_{b}"] = round(t(lambda: c.allgather(s2, r, algo=algo, stream=GS), it=20), 2)
+    c.finalize()
+print(json.dumps(res), flush=True)
