@@ -233,7 +233,9 @@ struct RingEntry {
 #ifdef MPXA_TRACE
 __device__ uint64_t g_cta_trace[2][kMaxCtas];   // per-CTA entry / exit %globaltimer (GPU 0)
 #define CTA_STAMP(w) do { if (threadIdx.x == 0 && blockIdx.y == 0) g_cta_trace[w][blockIdx.x] = globaltimer(); } while (0)
-#define TRACE(k) do { if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x == 0 || threadIdx.x == 32)) P.dc->trace[(k) + (threadIdx.x ? 16 : 0)] = globaltimer(); } while (0)
+// phase stamps of CTA 0 in SM cycles (clock64: one SM, so comparable; %globaltimer ticks only
+// every ~1 us outside a profiler)
+#define TRACE(k) do { if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x == 0 || threadIdx.x == 32)) P.dc->trace[(k) + (threadIdx.x ? 16 : 0)] = (uint64_t)clock64(); } while (0)
 #else
 #define TRACE(k) do { } while (0)
 #define CTA_STAMP(w) do { } while (0)
@@ -464,8 +466,10 @@ struct PieceRegs {
     }
 };
 
+// A16: the host vouched that every piece is a whole, 16-B aligned vector
+template <bool A16 = false>
 __device__ __forceinline__ void store_piece(char *dp, uint4 v, uint32_t len) {
-    if (len == 16 && (((uintptr_t)dp) & 15) == 0) { st16((uint4 *)dp, v); return; }
+    if (A16 || (len == 16 && (((uintptr_t)dp) & 15) == 0)) { st16((uint4 *)dp, v); return; }
     if (len == 16 && (((uintptr_t)dp) & 3) == 0) {
         uint32_t *d = (uint32_t *)dp;
         d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
@@ -1063,7 +1067,6 @@ __global__ void mpxa_scan_kernel(const int64_t *__restrict__ counts, int64_t *__
 // ------------------------------------------------------------------------------------
 constexpr int kSmallThreads = 512;
 
-constexpr int kRankTable = 256;   // small kernel: per-rank buffer bases kept in shared memory
 
 struct SmallShared {
     StepInfo steps[kMaxStepsSmem];   // step table, loaded in the prologue (before griddep wait)
@@ -1183,6 +1186,7 @@ __device__ __forceinline__ void small_items(const ExecParams &P, const SmallShar
             if (it >= items) continue;
             uint32_t o;
             const Move &m = item_move<VAR>(mv, idx, vpc, it, lg, mask, o);
+            if (k == 0) TRACE(13);
             const uint32_t n = (uint32_t)((uint64_t)m.len * P.unit);
             if (o >= n) continue;
             sp[k] = sb(P, S, m.src_kind, m.src_rank) + (uint64_t)m.src_off * P.unit + o;
@@ -1200,9 +1204,10 @@ __device__ __forceinline__ void small_items(const ExecParams &P, const SmallShar
             const uint64_t doff = (uint64_t)m.dst_off * P.unit + o;
             const uint4 val = R.value(k, sp[k]);
             if (!m.fanout) {
-                store_piece(sb(P, S, m.dst_kind, m.dst_rank) + doff, val, len);
+                store_piece<A16>(sb(P, S, m.dst_kind, m.dst_rank) + doff, val, len);
             } else {
-                for (int r = 0; r < P.p; r++) store_piece(sb(P, S, m.dst_kind, r) + doff, val, len);
+#pragma unroll 1
+                for (int r = 0; r < P.p; r++) store_piece<A16>(sb(P, S, m.dst_kind, r) + doff, val, len);
             }
         }
     }
@@ -1246,8 +1251,11 @@ __device__ __forceinline__ void small_var_step(const ExecParams &P, const SmallS
 
 // VARK: the variable-piece instantiation (P.small_var), a kernel of its own -- compiled into
 // the common one its code cost every small launch ~8 % (registers / code layout, measured)
-template <bool VARK>
+// KM: kSmallCommon or kSmallVar (variable pieces, P.small_var)
+// AK: 0 = the 16-B path decided per step at run time, 1 = always 16-B, 2 = never (host-known)
+template <int KM, int AK>
 __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __grid_constant__ ExecParams P) {
+    constexpr bool VARK = KM == kSmallVar;
     __shared__ SmallShared S;
     extern __shared__ __align__(16) char small_dyn[];
     CTA_STAMP(0);   // the program's moves, when they fit
@@ -1298,6 +1306,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
     const uint32_t lg = 31u - (uint32_t)__clz((int)ppm);
     uint32_t prev_wait = 0;
     for (int s = 0; s < prog.nsteps; s++) {
+        TRACE(11);
         StepInfo st;
         if (steps_smem) {
             st = S.steps[s];
@@ -1343,9 +1352,12 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
         }
         // 16-B fast path: the host vouched for every local offset / length / base, and the
         // recv bases of the peers written in this step arrived with their CTS
-        bool a16 = P.small_a16 != 0;
-        for (int q = 0; q < P.G; q++)
-            if (((st.signal_mask >> q) & 1u) && ((uintptr_t)S.recv_base[q] & 15)) a16 = false;
+        // (AK != 0: the host knows the answer for the whole launch -- one copy path compiled)
+        bool a16 = AK == 1 ? true : AK == 2 ? false : P.small_a16 != 0;
+        if (AK == 0)
+            for (int q = 0; q < P.G; q++)
+                if (((st.signal_mask >> q) & 1u) && ((uintptr_t)S.recv_base[q] & 15)) a16 = false;
+        TRACE(12);
         if (VARK) {
             small_var_step(P, S, mvs, st.first, st.nm, a16, small_dyn);
         } else if (a16) {
@@ -1355,7 +1367,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
         }
         TRACE(2);
         __syncthreads();
-        TRACE(3);
+        TRACE(3 + (s < 7 ? s : 7));   // stamps 3..10: end of steps 0..7
         if (P.dyn_sync && (s + 1 < prog.nsteps || (multi && st.signal_mask))) {
             small_row_barrier(P, S, g, s);
             if (S.abort_flag) return;
@@ -1406,19 +1418,43 @@ static cudaError_t launch_kernel(void (*kern)(ExecParams), const ExecParams &P, 
     return cudaLaunchKernelEx(&cfg, kern, P);
 }
 
+template <int KM, int AK>
+static cudaError_t small_attr(size_t max_dyn) {
+    static cudaError_t e = cudaFuncSetAttribute(mpxa_small_kernel<KM, AK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)max_dyn);
+    return e;
+}
+
+template <int KM, int AK>
+static cudaError_t launch_small_t(const ExecParams &P, size_t max_dyn, size_t smem, dim3 grid, bool cooperative,
+                                  bool pdl, cudaStream_t stream) {
+    const cudaError_t a = small_attr<KM, AK>(max_dyn);
+    if (a != cudaSuccess) return a;
+    return launch_kernel(mpxa_small_kernel<KM, AK>, P, grid, dim3(kSmallThreads), smem, cooperative, pdl, stream);
+}
+
+template <int KM>
+static cudaError_t launch_small_km(const ExecParams &P, size_t max_dyn, size_t smem, dim3 grid, bool cooperative,
+                                   bool pdl, cudaStream_t stream) {
+    // the 16-B decision is launch-wide unless peers' recv bases arrive at run time (mode 2)
+    const int ak = P.mode == 2 ? 0 : (P.small_a16 ? 1 : 2);
+    if (ak == 1) return launch_small_t<KM, 1>(P, max_dyn, smem, grid, cooperative, pdl, stream);
+    if (ak == 2) return launch_small_t<KM, 2>(P, max_dyn, smem, grid, cooperative, pdl, stream);
+    return launch_small_t<KM, 0>(P, max_dyn, smem, grid, cooperative, pdl, stream);
+}
+
 cudaError_t launch_small(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream) {
-    static cudaError_t attr = cudaFuncSetAttribute(mpxa_small_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)(kSmallMovesSmem * (sizeof(Move) + sizeof(uint16_t))));
-    static cudaError_t attr_v = cudaFuncSetAttribute(mpxa_small_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                     (int)(kSmallMovesSmem * sizeof(Move) +
-                                                           kSmallThreads * (sizeof(Move) + sizeof(uint32_t))));
-    if (attr != cudaSuccess) return attr;
-    if (attr_v != cudaSuccess) return attr_v;
-    const size_t smem = (P.small_cache ? (size_t)P.small_cache * sizeof(Move) : 0) +
-                        (P.small_own ? (size_t)kSmallMovesSmem * sizeof(uint16_t) : 0) +
-                        (P.small_var ? (size_t)kSmallThreads * (sizeof(Move) + sizeof(uint32_t)) : 0);
-    return launch_kernel(P.small_var ? mpxa_small_kernel<true> : mpxa_small_kernel<false>, P, dim3(nC, nG),
-                         dim3(kSmallThreads), smem, cooperative, pdl, stream);
+    const dim3 grid(nC, nG);
+    if (P.small_var)
+        return launch_small_km<kSmallVar>(P, kSmallMovesSmem * sizeof(Move) +
+                                                 kSmallThreads * (sizeof(Move) + sizeof(uint32_t)),
+                                          (size_t)P.small_cache * sizeof(Move) +
+                                              (size_t)kSmallThreads * (sizeof(Move) + sizeof(uint32_t)),
+                                          grid, cooperative, pdl, stream);
+    return launch_small_km<kSmallCommon>(P, kSmallMovesSmem * (sizeof(Move) + sizeof(uint16_t)),
+                                         (P.small_cache ? (size_t)P.small_cache * sizeof(Move) : 0) +
+                                             (P.small_own ? (size_t)kSmallMovesSmem * sizeof(uint16_t) : 0),
+                                         grid, cooperative, pdl, stream);
 }
 
 static cudaError_t exec_attr_once() {

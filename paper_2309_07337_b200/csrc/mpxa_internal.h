@@ -35,6 +35,8 @@ constexpr int kMoveTile = kThreads;   // moves staged in shared memory at a time
 constexpr int kMaxDynTiles = 64;      // dynamic mode: move tiles per step (queues per tile)
 constexpr uint64_t kSmallKernelMax = 8192;  // longest move (bytes) the small-message kernel takes
 constexpr int kSmallMovesSmem = 2048;       // program moves cached in shared memory by the small kernel
+enum { kSmallCommon = 0, kSmallVar = 1 };   // small-kernel instantiations
+constexpr int kRankTable = 256;   // small kernel: per-rank buffer bases kept in shared memory
 constexpr int kMaxWindows = 16;    // registered recv windows per process
 
 enum BufKind : uint8_t { BK_SEND = 0, BK_RECV = 1, BK_WORK = 2 };
@@ -154,6 +156,7 @@ struct ExecParams {
                                // owner across steps -> __syncthreads suffices); 0 = off
     int32_t small_var;         // small kernel: moves of very different lengths -- pieces counted
                                // exactly per tile of moves (block scan) instead of max-move slots
+    int32_t pad6[2];
     int32_t dyn_sync;          // multi-step dynamic mode: steps separated by a per-GPU-row CTA
                                // barrier and ONE flag per peer GPU (slot 0), so any CTA may move
                                // any piece (no flow ownership needed)

@@ -8,6 +8,6 @@ b = int(os.environ.get("B", str(16 << 20)))
 c = Comm(ranks_per_proc=p, device=0)
 s = torch.randint(0, 255, (p, p * b), dtype=torch.uint8, device="cuda"); r = torch.empty_like(s)
 for _ in range(5):
-    c.alltoall(s, r, algo="pairwise")
+    c.alltoall(s, r, algo=os.environ.get("ALGO", "pairwise"))
 torch.cuda.synchronize()
 print("ok")

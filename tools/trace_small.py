@@ -1,4 +1,4 @@
-"""Phase stamps (%globaltimer, ns) of CTA 0 (producer thread 0 / LSU thread 32) for one
+"""Phase stamps (SM cycles, clock64) of CTA 0 (producer thread 0 / LSU thread 32) for one
 launch (MPXA_TRACE build: MPXA_LIB=.../libmpxa_trace.so), next to the device time per call
 of the same launch in a CUDA graph.  CASES="op:bytes,..." """
 import ctypes, os, sys
@@ -14,10 +14,10 @@ for case in cases.split(","):
     op, b = case.split(":"); b = int(b)
     if op == "allgather":
         s = torch.zeros((p, b), dtype=torch.uint8, device="cuda"); r = torch.empty((p, p * b), dtype=torch.uint8, device="cuda")
-        fn = lambda: c.allgather(s, r, algo="pairwise", stream=GS)
+        fn = lambda: c.allgather(s, r, algo=os.environ.get("ALGO", "pairwise"), stream=GS)
     else:
         s = torch.zeros((p, p * b), dtype=torch.uint8, device="cuda"); r = torch.empty_like(s)
-        fn = lambda: c.alltoall(s, r, algo="pairwise", stream=GS)
+        fn = lambda: c.alltoall(s, r, algo=os.environ.get("ALGO", "pairwise"), stream=GS)
     for _ in range(5): fn()
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
@@ -31,7 +31,7 @@ for case in cases.split(","):
     buf = (ctypes.c_uint64 * 32)()
     f(c.handle, buf)
     t0 = buf[0]
-    print(op, b, f"graph us/call={us:.2f}", "producer:", [int(buf[i] - t0) if buf[i] else None for i in range(11)],
+    print(op, b, f"graph us/call={us:.2f}", "producer:", [int(buf[i] - t0) if buf[i] else None for i in range(16)],
           "lsu warp1:", [int(buf[16 + i] - t0) if buf[16 + i] else None for i in range(9)], flush=True)
 # per-CTA entry/exit of the last launch (exec kernel): spread of starts and ends
 if hasattr(L, "mpxa__cta_trace"):
@@ -40,10 +40,10 @@ if hasattr(L, "mpxa__cta_trace"):
         op, b = case.split(":"); b = int(b)
         if op == "allgather":
             s = torch.zeros((p, b), dtype=torch.uint8, device="cuda"); r = torch.empty((p, p * b), dtype=torch.uint8, device="cuda")
-            fn = lambda: c.allgather(s, r, algo="pairwise", stream=GS)
+            fn = lambda: c.allgather(s, r, algo=os.environ.get("ALGO", "pairwise"), stream=GS)
         else:
             s = torch.zeros((p, p * b), dtype=torch.uint8, device="cuda"); r = torch.empty_like(s)
-            fn = lambda: c.alltoall(s, r, algo="pairwise", stream=GS)
+            fn = lambda: c.alltoall(s, r, algo=os.environ.get("ALGO", "pairwise"), stream=GS)
         buf = (ctypes.c_uint64 * 2048)()
         for _ in range(4): fn()
         torch.cuda.synchronize()
