@@ -1251,6 +1251,61 @@ __device__ __forceinline__ void small_var_step(const ExecParams &P, const SmallS
 
 // VARK: the variable-piece instantiation (P.small_var), a kernel of its own -- compiled into
 // the common one its code cost every small launch ~8 % (registers / code layout, measured)
+// Cold per-step paths of the small kernel, kept out of line so the single-GPU step loop stays
+// compact in the instruction cache (measured: small launches are bound by per-step latency,
+// not by bytes).  Every thread of the CTA calls them.
+//
+// Step entry across GPUs: the peers' flags for the previous step and the CTS of the GPUs this
+// step writes to (their recv bases arrive with it).  Returns false after a watchdog abort.
+__device__ __noinline__ bool small_step_enter(const ExecParams &P, SmallShared &S, int g, int s, uint32_t prev_wait,
+                                              uint32_t signal_mask, uint64_t epoch, int fslot) {
+    const int t = threadIdx.x;
+    if (prev_wait) small_wait(P, S, prev_wait, &S.sym[g]->flags[0][fslot], kMaxCtas, (epoch << 8) | (uint64_t)s);
+    const uint32_t need = signal_mask & ~S.cts_ok;
+    if (need) {
+        small_wait(P, S, need, &S.sym[g]->cts[0].epoch, sizeof(CtsSlot) / 8, epoch);
+        if (t < 32 && ((need >> t) & 1u)) {
+            const CtsSlot *cs = &S.sym[g]->cts[t];
+            S.recv_base[t] = P.dc->win_table[t * kMaxWindows + cs->win] + cs->off;
+        }
+        __syncthreads();
+        fill_rank_bases(P, S, need, false);
+    }
+    __syncthreads();
+    if (t == 0) S.cts_ok |= need;
+    return !S.abort_flag;
+}
+
+// Owned-flow mode: compact the indexes of this CTA's moves of the step into own[]; returns
+// their number.
+__device__ __noinline__ uint32_t small_own_list(const ExecParams &P, SmallShared &S, const Move *mv, int nm,
+                                                uint16_t *own) {
+    const int t = threadIdx.x;
+    if (t == 0) S.n_own = 0;
+    __syncthreads();
+    for (int i = t; i < nm; i += kSmallThreads)
+        if ((int)(mv[i].flow % (uint32_t)P.small_own) == (int)blockIdx.x) own[atomicAdd(&S.n_own, 1u)] = (uint16_t)i;
+    __syncthreads();
+    return S.n_own;
+}
+
+// Step exit: the row barrier of sync mode, then the step's flags to the GPUs it wrote.
+// Returns false after a watchdog abort.
+__device__ __noinline__ bool small_step_exit(const ExecParams &P, SmallShared &S, int g, int s, int nsteps,
+                                             uint32_t signal_mask, uint64_t epoch, int fslot) {
+    const int t = threadIdx.x;
+    const bool multi = P.G > 1;
+    if (P.dyn_sync && (s + 1 < nsteps || (multi && signal_mask))) {
+        small_row_barrier(P, S, g, s);
+        if (S.abort_flag) return false;
+    }
+    if (multi && signal_mask && t < 32 && ((signal_mask >> t) & 1u) && (!P.dyn_sync || blockIdx.x == 0)) {
+        __threadfence_system();
+        st_release_sys(&S.sym[t]->flags[g][fslot], (epoch << 8) | (uint64_t)(s + 1));
+    }
+    return true;
+}
+
 // KM: kSmallCommon or kSmallVar (variable pieces, P.small_var)
 // AK: 0 = the 16-B path decided per step at run time, 1 = always 16-B, 2 = never (host-known)
 template <int KM, int AK>
@@ -1315,22 +1370,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
             st = StepInfo{g_st.move_begin, g_st.move_end - g_st.move_begin, g_st.signal_mask, g_st.wait_mask};
         }
         const int fslot = P.dyn_sync ? 0 : (int)blockIdx.x;   // the row's flag in sync mode
-        if (multi) {
-            if (prev_wait) small_wait(P, S, prev_wait, &S.sym[g]->flags[0][fslot], kMaxCtas, (epoch << 8) | (uint64_t)s);
-            const uint32_t need = st.signal_mask & ~S.cts_ok;
-            if (need) {
-                small_wait(P, S, need, &S.sym[g]->cts[0].epoch, sizeof(CtsSlot) / 8, epoch);
-                if (t < 32 && ((need >> t) & 1u)) {
-                    const CtsSlot *cs = &S.sym[g]->cts[t];
-                    S.recv_base[t] = P.dc->win_table[t * kMaxWindows + cs->win] + cs->off;
-                }
-                __syncthreads();
-                fill_rank_bases(P, S, need, false);
-            }
-            __syncthreads();
-            if (t == 0) S.cts_ok |= need;
-            if (S.abort_flag) return;
-        }
+        if (multi && !small_step_enter(P, S, g, s, prev_wait, st.signal_mask, epoch, fslot)) return;
         // items = (move, 16-byte piece); thread t takes items t, t+T, ... four at a time:
         // all four loads in flight before the stores
         uint32_t items = (uint32_t)st.nm * ppm;
@@ -1338,17 +1378,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
         uint32_t base0 = blockIdx.x * kSmallThreads + t;
         const uint16_t *idx = nullptr;
         if (P.small_own) {          // this CTA's flows only (compacted move list), all its threads
-            uint16_t *own = reinterpret_cast<uint16_t *>(small_dyn + (size_t)P.small_cache * sizeof(Move));
-            if (t == 0) S.n_own = 0;
-            __syncthreads();
-            for (int i = t; i < st.nm; i += kSmallThreads)
-                if ((int)(mvs[st.first + i].flow % (uint32_t)P.small_own) == (int)blockIdx.x)
-                    own[atomicAdd(&S.n_own, 1u)] = (uint16_t)i;
-            __syncthreads();
-            items = S.n_own * ppm;
+            idx = reinterpret_cast<uint16_t *>(small_dyn + (size_t)P.small_cache * sizeof(Move));
+            items = small_own_list(P, S, mvs + st.first, st.nm, reinterpret_cast<uint16_t *>(small_dyn + (size_t)P.small_cache * sizeof(Move))) * ppm;
             TT = kSmallThreads;
             base0 = t;
-            idx = own;
         }
         // 16-B fast path: the host vouched for every local offset / length / base, and the
         // recv bases of the peers written in this step arrived with their CTS
@@ -1368,14 +1401,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
         TRACE(2);
         __syncthreads();
         TRACE(3 + (s < 7 ? s : 7));   // stamps 3..10: end of steps 0..7
-        if (P.dyn_sync && (s + 1 < prog.nsteps || (multi && st.signal_mask))) {
-            small_row_barrier(P, S, g, s);
-            if (S.abort_flag) return;
-        }
-        if (multi && st.signal_mask && t < 32 && ((st.signal_mask >> t) & 1u) && (!P.dyn_sync || blockIdx.x == 0)) {
-            __threadfence_system();
-            st_release_sys(&S.sym[t]->flags[g][fslot], (epoch << 8) | (uint64_t)(s + 1));
-        }
+        if ((P.dyn_sync && (s + 1 < prog.nsteps || (multi && st.signal_mask))) || (multi && st.signal_mask))
+            if (!small_step_exit(P, S, g, s, prog.nsteps, st.signal_mask, epoch, fslot)) return;
         prev_wait = st.wait_mask;
     }
     if (multi && prev_wait) {
