@@ -1276,6 +1276,41 @@ __device__ __noinline__ bool small_step_enter(const ExecParams &P, SmallShared &
     return !S.abort_flag;
 }
 
+// Kernel start across GPUs: post this GPU's clear-to-send (epoch, and the recv window) into
+// every peer's symmetric region.
+__device__ __noinline__ void small_post_cts(const ExecParams &P, SmallShared &S, int g, uint64_t epoch) {
+    const int t = threadIdx.x;
+    if (t < P.G && t != g) {
+        CtsSlot *slot = &S.sym[t]->cts[g];
+        if (P.mode == 2) { slot->win = P.recv_win; slot->off = P.recv_off; }
+        else { slot->win = 0; slot->off = (uint64_t)(uintptr_t)(P.recv + (uint64_t)g * P.R * P.recv_stride); }
+        __threadfence_system();
+        st_release_sys(&slot->epoch, epoch);
+    }
+}
+
+// Kernel end: the peers' flags of the last step, then the last CTA of the launch publishes the
+// epoch and resets the sync-mode barrier counters (graph-replayable launches).
+__device__ __noinline__ void small_finish(const ExecParams &P, SmallShared &S, int g, int nsteps, uint32_t prev_wait,
+                                          uint64_t epoch) {
+    const bool multi = P.G > 1;
+    if (multi && prev_wait) {
+        small_wait(P, S, prev_wait, &S.sym[g]->flags[0][P.dyn_sync ? 0 : (int)blockIdx.x], kMaxCtas,
+                   (epoch << 8) | (uint64_t)nsteps);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&P.dc->done_ctas, 1u) == gridDim.x * gridDim.y - 1) {
+            P.dc->done_ctas = 0;
+            if (multi) P.dc->epoch = epoch;
+            if (P.dyn_sync)
+                for (int r = 0; r < (int)gridDim.y; r++) P.dc->dyn_bar[P.mode == 1 ? r : P.my_gpu] = 0;
+            __threadfence();
+        }
+    }
+}
+
 // Owned-flow mode: compact the indexes of this CTA's moves of the step into own[]; returns
 // their number.
 __device__ __noinline__ uint32_t small_own_list(const ExecParams &P, SmallShared &S, const Move *mv, int nm,
@@ -1349,13 +1384,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
     __syncthreads();
     TRACE(0);
     const uint64_t epoch = S.epoch;
-    if (multi && t < P.G && t != g) {
-        CtsSlot *slot = &S.sym[t]->cts[g];
-        if (P.mode == 2) { slot->win = P.recv_win; slot->off = P.recv_off; }
-        else { slot->win = 0; slot->off = (uint64_t)(uintptr_t)(P.recv + (uint64_t)g * P.R * P.recv_stride); }
-        __threadfence_system();
-        st_release_sys(&slot->epoch, epoch);
-    }
+    if (multi) small_post_cts(P, S, g, epoch);
     const Move *mvs = cached ? smoves : prog.moves;
     const uint32_t ppm = (uint32_t)P.small_ppm;        // 16-byte pieces per move: power-of-two bound
     const uint32_t lg = 31u - (uint32_t)__clz((int)ppm);
@@ -1405,21 +1434,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
             if (!small_step_exit(P, S, g, s, prog.nsteps, st.signal_mask, epoch, fslot)) return;
         prev_wait = st.wait_mask;
     }
-    if (multi && prev_wait) {
-        small_wait(P, S, prev_wait, &S.sym[g]->flags[0][P.dyn_sync ? 0 : (int)blockIdx.x], kMaxCtas,
-                   (epoch << 8) | (uint64_t)prog.nsteps);
-        __syncthreads();
-    }
-    if ((multi || P.dyn_sync) && t == 0) {
-        __threadfence();
-        if (atomicAdd(&P.dc->done_ctas, 1u) == gridDim.x * gridDim.y - 1) {
-            P.dc->done_ctas = 0;
-            if (multi) P.dc->epoch = epoch;
-            if (P.dyn_sync)
-                for (int r = 0; r < (int)gridDim.y; r++) P.dc->dyn_bar[P.mode == 1 ? r : P.my_gpu] = 0;
-            __threadfence();
-        }
-    }
+    if (multi || P.dyn_sync) small_finish(P, S, g, prog.nsteps, prev_wait, epoch);
     CTA_STAMP(1);
 }
 
