@@ -388,52 +388,15 @@ def configs_on_one_gpu(torch, reps=20):
         c.finalize()
 
     # ---- f1: persistent neighbor alltoallv, sparse-matrix halo: p=8 ranks,
-    #      each owning 1 Mi float64 boundary values, needing a 256 Ki window from each of 3
-    #      other ranks (overlapping windows within a group = duplicates); standard vs
-    #      locality-aware (groups of 2 ranks), all ranks on this GPU and as 4 emulated GPUs ----
-    p = 8
-    edges = synth.spmv_edges(0, p, 1 << 20, 1 << 18, 3, contiguous=True)
-    gr, si, ri = synth.graph_from_edges(p, edges)
-    ioff = np.concatenate([[0], np.cumsum(gr["indeg"])])
-    ooff = np.concatenate([[0], np.cumsum(gr["outdeg"])])
-    srcs = [list(map(int, gr["src"][ioff[r]:ioff[r + 1]])) for r in range(p)]
-    dsts = [list(map(int, gr["dst"][ooff[r]:ooff[r + 1]])) for r in range(p)]
-    S = int((gr["sd"] + gr["sc"]).max()) * 8
-    Rb = int((gr["rd"] + gr["rc"]).max()) * 8
-    d_send = torch.randint(0, 256, (p, S), dtype=torch.uint8, device=dev)
-    moved = int(gr["sc"].sum()) * 8
-    out = {"bytes_received": moved}
-    for G in (0, 4):
-        c = Comm(ranks_per_proc=p, device=torch.cuda.current_device(), group_size=2, emulate_gpus=G)
-        topo = c.dist_graph_create_adjacent(srcs, dsts)
-        for loc in (False, True):
-            d_recv = torch.zeros((p, Rb), dtype=torch.uint8, device=dev)
-            kw = dict(send_indices=si, recv_indices=ri) if loc else {}
-            # locality needs equal values for equal indices: fill by index (host, once)
-            if loc:
-                send_h, _ = synth.neighbor_buffers(1, p, gr, si, w=8)
-                d_send_l = torch.from_numpy(send_h).to(dev)
-            src_t = d_send_l if loc else d_send
-            req = c.neighbor_alltoallv_init(topo, src_t, gr["sc"], gr["sd"], d_recv, gr["rc"], gr["rd"],
-                                            dtype_size=8, **kw)
-            req.start(gstream); req.wait(gstream)
-            torch.cuda.synchronize()
-            want = oracle.neighbor_definition(src_t.cpu().numpy(), np.zeros((p, Rb), np.uint8), 8, gr)
-            ok = bool(np.array_equal(d_recv.cpu().numpy(), want))
-            us = 1e3 * time_graph(lambda: (req.start(gstream), req.wait(gstream)), 20, gstream)
-            key = ("locality_g2" if loc else "standard") + ("_1gpu" if G == 0 else "_4_emulated_gpus")
-            out[key] = {"us": round(us, 2), "verified": ok, "recv_GBps": round(moved / us / 1e3, 1)}
-            req.free()
-        topo.free()
-        c.finalize()
-    # values crossing group boundaries: standard = elements on crossing edges; locality =
-    # |{(index, src group, dst group)}| (the dedup count the oracle pins, by enumeration)
-    e_src = np.repeat(np.repeat(np.arange(p), gr["outdeg"]), gr["sc"]) // 2
-    e_dst = np.repeat(gr["dst"], gr["sc"]) // 2
-    cross = e_src != e_dst
-    trip = np.stack([si[cross], e_src[cross], e_dst[cross]], 1)
-    out["inter_group_values"] = {"standard": int(cross.sum()), "locality_g2": int(len(np.unique(trip, axis=0)))}
-    res["f1_neighbor_alltoallv_spmv_halo_p8"] = out
+    #      standard vs locality-aware (groups of 2 ranks), all ranks on this GPU and as 4
+    #      emulated GPUs.  Two index patterns: (a) each rank owns 1 Mi float64 boundary values
+    #      and needs a 256 Ki window from each of 3 other ranks (banded / reordered matrix:
+    #      overlapping windows within a group = duplicates, long runs); (b) each rank owns 64 Ki
+    #      values and needs a random 8 Ki subset from each of 3 others (unstructured matrix:
+    #      element-granular runs, the small kernel's variable-piece mode) ----
+    for key, (m_own, k_need, contiguous) in (("f1_neighbor_alltoallv_spmv_halo_p8", (1 << 20, 1 << 18, True)),
+                                             ("f1_neighbor_alltoallv_random_sparse_p8", (1 << 16, 1 << 13, False))):
+        res[key] = f1_neighbor(Comm, torch, dev, gstream, time_graph, m_own, k_need, contiguous)
 
     # ---- f3: partitioned channel rank 0 -> rank 1 on this GPU: a whole
     #      cycle (both starts, Pready of every partition, both waits), CUDA-graph timed ----
@@ -483,6 +446,56 @@ def configs_on_one_gpu(torch, reps=20):
     c.finalize()
     res["f2_allgather_p32_8_emulated_gpus"] = out
     return res
+
+
+def f1_neighbor(Comm, torch, dev, gstream, time_graph, m_own, k_need, contiguous):
+    """f1 neighbor alltoallv on one index pattern (see the caller): us per persistent
+    start/wait, verified against the oracle's definition."""
+    import oracle
+    import synth
+    p = 8
+    edges = synth.spmv_edges(0, p, m_own, k_need, 3, contiguous=contiguous)
+    gr, si, ri = synth.graph_from_edges(p, edges)
+    ioff = np.concatenate([[0], np.cumsum(gr["indeg"])])
+    ooff = np.concatenate([[0], np.cumsum(gr["outdeg"])])
+    srcs = [list(map(int, gr["src"][ioff[r]:ioff[r + 1]])) for r in range(p)]
+    dsts = [list(map(int, gr["dst"][ooff[r]:ooff[r + 1]])) for r in range(p)]
+    S = int((gr["sd"] + gr["sc"]).max()) * 8
+    Rb = int((gr["rd"] + gr["rc"]).max()) * 8
+    d_send = torch.randint(0, 256, (p, S), dtype=torch.uint8, device=dev)
+    moved = int(gr["sc"].sum()) * 8
+    out = {"bytes_received": moved}
+    for G in (0, 4):
+        c = Comm(ranks_per_proc=p, device=torch.cuda.current_device(), group_size=2, emulate_gpus=G)
+        topo = c.dist_graph_create_adjacent(srcs, dsts)
+        for loc in (False, True):
+            d_recv = torch.zeros((p, Rb), dtype=torch.uint8, device=dev)
+            kw = dict(send_indices=si, recv_indices=ri) if loc else {}
+            # locality needs equal values for equal indices: fill by index (host, once)
+            if loc:
+                send_h, _ = synth.neighbor_buffers(1, p, gr, si, w=8)
+                d_send_l = torch.from_numpy(send_h).to(dev)
+            src_t = d_send_l if loc else d_send
+            req = c.neighbor_alltoallv_init(topo, src_t, gr["sc"], gr["sd"], d_recv, gr["rc"], gr["rd"],
+                                            dtype_size=8, **kw)
+            req.start(gstream); req.wait(gstream)
+            torch.cuda.synchronize()
+            want = oracle.neighbor_definition(src_t.cpu().numpy(), np.zeros((p, Rb), np.uint8), 8, gr)
+            ok = bool(np.array_equal(d_recv.cpu().numpy(), want))
+            us = 1e3 * time_graph(lambda: (req.start(gstream), req.wait(gstream)), 20, gstream)
+            key = ("locality_g2" if loc else "standard") + ("_1gpu" if G == 0 else "_4_emulated_gpus")
+            out[key] = {"us": round(us, 2), "verified": ok, "recv_GBps": round(moved / us / 1e3, 1)}
+            req.free()
+        topo.free()
+        c.finalize()
+    # values crossing group boundaries: standard = elements on crossing edges; locality =
+    # |{(index, src group, dst group)}| (the dedup count the oracle pins, by enumeration)
+    e_src = np.repeat(np.repeat(np.arange(p), gr["outdeg"]), gr["sc"]) // 2
+    e_dst = np.repeat(gr["dst"], gr["sc"]) // 2
+    cross = e_src != e_dst
+    trip = np.stack([si[cross], e_src[cross], e_dst[cross]], 1)
+    out["inter_group_values"] = {"standard": int(cross.sum()), "locality_g2": int(len(np.unique(trip, axis=0)))}
+    return out
 
 
 def write_selector(sw, path, p, R):

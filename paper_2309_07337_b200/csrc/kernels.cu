@@ -725,6 +725,9 @@ __device__ __noinline__ void row_barrier(const ExecParams &P, ExecShared &S, int
 #ifndef MPXA_EXEC_MINB
 #define MPXA_EXEC_MINB 2
 #endif
+// DYN: dynamic (work-queue) mode, P.dyn_units != 0 -- its own instantiation, so the static
+// mode's code stays compact
+template <bool DYN>
 __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(const __grid_constant__ ExecParams Pk) {
     extern __shared__ __align__(128) char dyn_smem[];
     __shared__ ExecShared S;
@@ -765,7 +768,7 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
     if (pre) {
         const int a = clampi(x0 - P.d0_base, P.d0_n);
         const int nm = clampi(x1 - P.d0_base, P.d0_n) - a;
-        const int rot = (nm && !P.dyn_units) ? (int)(((int64_t)sl + (int64_t)g * nm / P.G) % nm) : 0;
+        const int rot = (nm && !DYN) ? (int)(((int64_t)sl + (int64_t)g * nm / P.G) % nm) : 0;
         pre_cnt = min(kMoveTile, nm);            // <= kThreads: one move per thread
         if (t < pre_cnt) {
             int q = t + rot;
@@ -866,9 +869,9 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
             if (S.abort_flag) return;
         }
         if (multi && t == 0) fence_proxy_async();   // acquired peer writes before TMA reads
-        const int nm = P.dyn_units ? 0 : st.nm;   // dynamic mode: the work queue below
+        const int nm = DYN ? 0 : st.nm;   // dynamic mode: the work queue below
         const int rot = nm ? (int)(((int64_t)sl + (int64_t)g * nm / P.G) % nm) : 0;
-        if (P.dyn_units) {
+        if (DYN) {
             wrote = dyn_step(P, S, prod, g, st.first, st.nm, pre && s == 0, tile_base);
             tile_base += (st.nm + kMoveTile - 1) / kMoveTile;
         }
@@ -980,13 +983,13 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
     }
     // the last CTA of the launch publishes the epoch and resets the work queues (the next
     // launch is stream-ordered after, and waits on griddepcontrol before reading either)
-    if ((multi || P.dyn_units) && t == 0) {
+    if ((multi || DYN) && t == 0) {
         __threadfence();
         const uint32_t total = gridDim.x * gridDim.y;
         if (atomicAdd(&P.dc->done_ctas, 1u) == total - 1) {
             P.dc->done_ctas = 0;
             if (multi) P.dc->epoch = epoch;
-            if (P.dyn_units)
+            if (DYN)
                 for (int r = 0; r < (int)gridDim.y; r++) {
                     const int row = P.my_gpu >= 0 ? P.my_gpu : r;
                     for (int ti = 0; ti < P.dyn_units; ti++) {
@@ -1500,16 +1503,19 @@ cudaError_t launch_small(const ExecParams &P, int nC, int nG, bool cooperative, 
 }
 
 static cudaError_t exec_attr_once() {
-    static cudaError_t e = cudaFuncSetAttribute(mpxa_exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                kMaxDynSmem);
-    return e;
+    static cudaError_t e0 = cudaFuncSetAttribute(mpxa_exec_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 kMaxDynSmem);
+    static cudaError_t e1 = cudaFuncSetAttribute(mpxa_exec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 kMaxDynSmem);
+    return e0 != cudaSuccess ? e0 : e1;
 }
 
 cudaError_t launch_exec(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream) {
     cudaError_t e = exec_attr_once();
     if (e != cudaSuccess) return e;
     const size_t smem = (size_t)P.stages * P.chunk;
-    return launch_kernel(mpxa_exec_kernel, P, dim3(nC, nG), dim3(kThreads), smem, cooperative, pdl, stream);
+    return launch_kernel(P.dyn_units ? mpxa_exec_kernel<true> : mpxa_exec_kernel<false>, P, dim3(nC, nG),
+                         dim3(kThreads), smem, cooperative, pdl, stream);
 }
 
 // ------------------------------------------------------------------------------------
@@ -1631,9 +1637,10 @@ cudaError_t launch_scan(const int64_t *counts, int64_t *rc, int64_t *rd, int p, 
 
 int exec_max_ctas_per_sm(size_t dyn_smem) {
     if (exec_attr_once() != cudaSuccess) return 1;
-    int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, mpxa_exec_kernel, kThreads, dyn_smem);
-    return n;
+    int n0 = 0, n1 = 0;   // both instantiations must fit the grids the host sizes
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n0, mpxa_exec_kernel<false>, kThreads, dyn_smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n1, mpxa_exec_kernel<true>, kThreads, dyn_smem);
+    return std::min(n0, n1);
 }
 
 }  // namespace mpxa

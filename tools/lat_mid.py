@@ -1,4 +1,4 @@
-"""Small-message latency probe (device us per call, CUDA graphs): the small-kernel launches
+"""Latency probe (device us per call, CUDA graphs): the small-kernel launches
 of the bench sweep at a few sizes.  One JSON line."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -8,9 +8,9 @@ import tune_mid
 from tune_mid import t
 tune_mid.GS = GS = torch.cuda.Stream()
 res = {}
-for p in (4, 8):
+for p in [int(x) for x in os.environ.get("PS", "8").split(",")]:
     c = Comm(ranks_per_proc=p, device=0)
-    for b in [int(x) for x in os.environ.get("SIZES", "16,1024,16384").split(",")]:
+    for b in [int(x) for x in os.environ.get("SIZES", "65536,262144,1048576,4194304").split(",")]:
         s = torch.randint(0, 255, (p, p * b), dtype=torch.uint8, device="cuda")
         r = torch.empty_like(s)
         for algo in ("pairwise", "bruck", "hier"):
