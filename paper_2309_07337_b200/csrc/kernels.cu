@@ -1216,6 +1216,63 @@ __device__ __forceinline__ void small_items(const ExecParams &P, const SmallShar
     }
 }
 
+// Single-GPU launches with every move cached (kSmallLocal): each move is resolved ONCE, in the
+// prologue, to absolute source / destination pointers and a byte count, in place of the cached
+// Move -- the per-item path is then one shared-memory record and no base-table lookups.
+struct RMove {
+    const char *src;
+    char *dst;         // non-fanout destination
+    uint64_t doff;     // fanout: byte offset inside every rank's dst_kind buffer
+    uint32_t n;        // bytes
+    uint32_t flow;
+    uint8_t fanout, dst_kind, pad[6];
+};
+static_assert(sizeof(RMove) == sizeof(Move), "resolved moves overwrite the cached moves 1:1");
+
+__device__ __forceinline__ char *local_base(const ExecParams &P, char *work0, int kind, int rank) {
+    if (kind == BK_SEND) return (char *)P.send + (uint64_t)rank * P.send_stride;
+    if (kind == BK_RECV) return P.recv + (uint64_t)rank * P.recv_stride;
+    return work0 + (uint64_t)rank * P.work_stride;
+}
+
+template <bool A16>
+__device__ __forceinline__ void small_items_loc(const ExecParams &P, const SmallShared &S, const RMove *mv,
+                                                uint32_t items, uint32_t lg, uint32_t TT, uint32_t base0,
+                                                const uint16_t *idx) {
+    const uint32_t mask = (1u << lg) - 1u;
+    for (uint32_t base = base0; base < items; base += TT * kBatch) {
+        PieceRegs<A16> R;
+        const char *sp[kBatch];
+#pragma unroll
+        for (int k = 0; k < kBatch; k++) {
+            sp[k] = nullptr;
+            const uint32_t it = base + (uint32_t)k * TT;
+            if (it >= items) continue;
+            const RMove &m = mv[idx ? idx[it >> lg] : (it >> lg)];
+            const uint32_t o = (it & mask) * 16;
+            if (o >= m.n) continue;
+            sp[k] = m.src + o;
+            R.issue(k, sp[k], min(16u, m.n - o));
+        }
+        TRACE(1);
+#pragma unroll
+        for (int k = 0; k < kBatch; k++) {
+            if (!sp[k]) continue;
+            const uint32_t it = base + (uint32_t)k * TT;
+            const RMove &m = mv[idx ? idx[it >> lg] : (it >> lg)];
+            const uint32_t o = (it & mask) * 16;
+            const uint32_t len = min(16u, m.n - o);
+            const uint4 val = R.value(k, sp[k]);
+            if (!m.fanout) {
+                store_piece<A16>(m.dst + o, val, len);
+            } else {
+#pragma unroll 1
+                for (int r = 0; r < P.p; r++) store_piece<A16>(S.rb[m.dst_kind][r] + m.doff + o, val, len);
+            }
+        }
+    }
+}
+
 // Variable-piece mode (P.small_var): one step of the small kernel.
 __device__ __forceinline__ void small_var_step(const ExecParams &P, const SmallShared &S, const Move *mvs, int first,
                                             int nm, bool a16, char *small_dyn) {
@@ -1317,12 +1374,14 @@ __device__ __noinline__ void small_finish(const ExecParams &P, SmallShared &S, i
 // Owned-flow mode: compact the indexes of this CTA's moves of the step into own[]; returns
 // their number.
 __device__ __noinline__ uint32_t small_own_list(const ExecParams &P, SmallShared &S, const Move *mv, int nm,
-                                                uint16_t *own) {
+                                                uint16_t *own, bool resolved) {
     const int t = threadIdx.x;
     if (t == 0) S.n_own = 0;
     __syncthreads();
-    for (int i = t; i < nm; i += kSmallThreads)
-        if ((int)(mv[i].flow % (uint32_t)P.small_own) == (int)blockIdx.x) own[atomicAdd(&S.n_own, 1u)] = (uint16_t)i;
+    for (int i = t; i < nm; i += kSmallThreads) {
+        const uint32_t flow = resolved ? reinterpret_cast<const RMove *>(mv)[i].flow : mv[i].flow;
+        if ((int)(flow % (uint32_t)P.small_own) == (int)blockIdx.x) own[atomicAdd(&S.n_own, 1u)] = (uint16_t)i;
+    }
     __syncthreads();
     return S.n_own;
 }
@@ -1348,7 +1407,7 @@ __device__ __noinline__ bool small_step_exit(const ExecParams &P, SmallShared &S
 // AK: 0 = the 16-B path decided per step at run time, 1 = always 16-B, 2 = never (host-known)
 template <int KM, int AK>
 __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __grid_constant__ ExecParams P) {
-    constexpr bool VARK = KM == kSmallVar;
+    constexpr bool VARK = KM == kSmallVar, LOC = KM == kSmallLocal;
     __shared__ SmallShared S;
     extern __shared__ __align__(16) char small_dyn[];
     CTA_STAMP(0);   // the program's moves, when they fit
@@ -1364,8 +1423,23 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
     const bool ld_step = steps_smem && t < prog.nsteps;
     Step st_r;
     if (ld_step) st_r = prog.steps[t];
-    if (cached)
+    if (LOC) {   // one GPU, every move cached: resolve the moves to pointers once, here
+        char *const work0 = P.dc->work_base[0];
+        for (int i = t; i < prog.nmoves; i += kSmallThreads) {
+            const Move m = prog.moves[i];
+            RMove r;
+            r.src = local_base(P, work0, m.src_kind, m.src_rank) + (uint64_t)m.src_off * P.unit;
+            r.doff = (uint64_t)m.dst_off * P.unit;
+            r.dst = m.fanout ? nullptr : local_base(P, work0, m.dst_kind, m.dst_rank) + r.doff;
+            r.n = (uint32_t)((uint64_t)m.len * P.unit);
+            r.flow = m.flow;
+            r.fanout = m.fanout;
+            r.dst_kind = m.dst_kind;
+            reinterpret_cast<RMove *>(smoves)[i] = r;
+        }
+    } else if (cached) {
         for (int i = t; i < prog.nmoves; i += kSmallThreads) smoves[i] = prog.moves[i];
+    }
     if (ld_step) S.steps[t] = StepInfo{st_r.move_begin, st_r.move_end - st_r.move_begin, st_r.signal_mask, st_r.wait_mask};
     if (t < P.G) {
         S.work_base[t] = P.dc->work_base[t];
@@ -1411,7 +1485,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
         const uint16_t *idx = nullptr;
         if (P.small_own) {          // this CTA's flows only (compacted move list), all its threads
             idx = reinterpret_cast<uint16_t *>(small_dyn + (size_t)P.small_cache * sizeof(Move));
-            items = small_own_list(P, S, mvs + st.first, st.nm, reinterpret_cast<uint16_t *>(small_dyn + (size_t)P.small_cache * sizeof(Move))) * ppm;
+            items = small_own_list(P, S, mvs + st.first, st.nm,
+                                   reinterpret_cast<uint16_t *>(small_dyn + (size_t)P.small_cache * sizeof(Move)), LOC) *
+                    ppm;
             TT = kSmallThreads;
             base0 = t;
         }
@@ -1423,7 +1499,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
             for (int q = 0; q < P.G; q++)
                 if (((st.signal_mask >> q) & 1u) && ((uintptr_t)S.recv_base[q] & 15)) a16 = false;
         TRACE(12);
-        if (VARK) {
+        if (LOC) {
+            const RMove *rm = reinterpret_cast<const RMove *>(smoves) + st.first;
+            if (a16) small_items_loc<true>(P, S, rm, items, lg, TT, base0, idx);
+            else small_items_loc<false>(P, S, rm, items, lg, TT, base0, idx);
+        } else if (VARK) {
             small_var_step(P, S, mvs, st.first, st.nm, a16, small_dyn);
         } else if (a16) {
             small_items<true>(P, S, mvs + st.first, items, lg, TT, base0, idx);
@@ -1490,6 +1570,11 @@ static cudaError_t launch_small_km(const ExecParams &P, size_t max_dyn, size_t s
 
 cudaError_t launch_small(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream) {
     const dim3 grid(nC, nG);
+    if (!P.small_var && P.mode == 0 && P.G == 1 && P.small_cache > 0 && P.p <= kRankTable)
+        return launch_small_km<kSmallLocal>(P, kSmallMovesSmem * (sizeof(Move) + sizeof(uint16_t)),
+                                            (size_t)P.small_cache * sizeof(Move) +
+                                                (P.small_own ? (size_t)kSmallMovesSmem * sizeof(uint16_t) : 0),
+                                            grid, cooperative, pdl, stream);
     if (P.small_var)
         return launch_small_km<kSmallVar>(P, kSmallMovesSmem * sizeof(Move) +
                                                  kSmallThreads * (sizeof(Move) + sizeof(uint32_t)),

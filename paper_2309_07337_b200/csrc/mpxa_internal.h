@@ -35,7 +35,7 @@ constexpr int kMoveTile = kThreads;   // moves staged in shared memory at a time
 constexpr int kMaxDynTiles = 64;      // dynamic mode: move tiles per step (queues per tile)
 constexpr uint64_t kSmallKernelMax = 8192;  // longest move (bytes) the small-message kernel takes
 constexpr int kSmallMovesSmem = 2048;       // program moves cached in shared memory by the small kernel
-enum { kSmallCommon = 0, kSmallVar = 1 };   // small-kernel instantiations
+enum { kSmallCommon = 0, kSmallVar = 1, kSmallLocal = 2 };   // small-kernel instantiations
 constexpr int kRankTable = 256;   // small kernel: per-rank buffer bases kept in shared memory
 constexpr int kMaxWindows = 16;    // registered recv windows per process
 
