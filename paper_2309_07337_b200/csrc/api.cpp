@@ -203,6 +203,8 @@ struct mpxa_comm_s {
     int cap_small = 148;                   // small-message kernel (1 CTA / SM)
     int64_t var_chop = 32;                 // small kernel, variable pieces: longest move (bytes)
     int var_tiles = 4;                     // ... and warp tiles (32 moves) per CTA
+    bool swork = true;                     // small kernel, one CTA on one GPU: WORK in shared memory
+    int small_nt = 64;                     // small kernel block size for launches with few pieces
     int force_ns = 0, force_nf = 0;           // MPXA_NS / MPXA_NF overrides (tuning)
     int force_big = -1;                       // MPXA_TMA_BIG=0/1 override (tuning)
     bool force_exec = false;                  // MPXA_NO_SMALL=1: never use the small-message kernel
@@ -675,6 +677,18 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
                                                                     (uint64_t)c->var_tiles)));
             E.dyn_sync = !one_step && nC > 1;
         }
+        // one CTA on one GPU, several steps, moves cached: the WORK rows live in the CTA's
+        // shared memory (the kernel resolves WORK pointers there)
+        const uint64_t wbytes = (uint64_t)dp.host.work_units * unit * (uint64_t)c->Rg;
+        if (c->swork && !E.small_var && !E.small_own && nC <= 1 && c->G == 1 && !c->emulated && c->nprocs == 1 &&
+            dp.nsteps > 1 && E.small_cache > 0 && c->p <= kRankTable && wbytes > 0 &&
+            wbytes <= (uint64_t)kSmallWorkSmem)
+            E.small_swork = 1;
+        // few pieces per CTA and step: a 64-thread block holds
+        // them in one batch, and fewer idle warps contend for issue slots at every step
+        if (!E.small_var && c->p <= c->small_nt && dp.nsteps <= c->small_nt &&
+            items <= (uint64_t)std::max(1, nC) * (uint64_t)c->small_nt * 4)
+            E.small_threads = c->small_nt;
         e = launch_small(E, std::max(1, nC), c->emulated ? c->G : 1, c->emulated, pdl && c->pdl, stream);
     } else {
         int nC = gr.n();
@@ -1140,6 +1154,8 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     if (const char *e = getenv("MPXA_SMALL_VOL")) c->small_vol1 = strtoull(e, nullptr, 10);
     if (const char *e = getenv("MPXA_VAR_CHOP")) c->var_chop = atoll(e);
     if (const char *e = getenv("MPXA_VAR_TILES")) c->var_tiles = std::max(1, atoi(e));
+    if (const char *e = getenv("MPXA_SWORK")) c->swork = atoi(e) != 0;
+    if (const char *e = getenv("MPXA_SMALL_NT")) c->small_nt = std::max(32, std::min(512, atoi(e)));
     CK(cudaHostAlloc((void **)&c->err_host, sizeof(int32_t), cudaHostAllocMapped));
     *c->err_host = 0;
     CK(cudaHostGetDevicePointer((void **)&c->err_dev, c->err_host, 0));

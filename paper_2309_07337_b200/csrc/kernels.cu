@@ -412,6 +412,18 @@ __device__ __noinline__ void lsu_copy(const ExecParams &P, const ExecShared &S, 
     }
 }
 
+// store_piece with generic stores only (the destination may be shared memory)
+__device__ __forceinline__ void store_piece_generic(char *dp, uint4 v, uint32_t len) {
+    if (len == 16 && (((uintptr_t)dp) & 15) == 0) { *(uint4 *)dp = v; return; }
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    if ((len & 3) == 0 && (((uintptr_t)dp) & 3) == 0) {
+        uint32_t *d = (uint32_t *)dp;
+        for (uint32_t b = 0; b < len / 4; b++) d[b] = w[b];
+        return;
+    }
+    for (uint32_t b = 0; b < len; b++) dp[b] = (char)(w[b >> 2] >> (8 * (b & 3)));
+}
+
 // Batched copy of up to kBatch SMALL moves by one warp (n <= 512 B each): every lane loads
 // its 16-byte piece of every move first (kBatch loads in flight), then stores them -- one
 // memory round trip per batch instead of one per move.  Byte-granular when a piece is not
@@ -457,6 +469,18 @@ struct PieceRegs {
             v[k].w = (a + 12 < end) ? __ldcg(wp + 3) : 0u;
             w4[k] = (a + 16 < end) ? __ldcg(wp + 4) : 0u;
         }
+    }
+    // the same with generic loads (the source may be shared memory)
+    __device__ __forceinline__ void issue_generic(int k, const char *sp, uint32_t len) {
+        if (A16) { v[k] = *(const uint4 *)sp; return; }
+        const uintptr_t a = (uintptr_t)sp & ~(uintptr_t)3;
+        const uint32_t *wp = (const uint32_t *)a;
+        const uintptr_t end = (uintptr_t)sp + len;
+        v[k].x = wp[0];
+        v[k].y = (a + 4 < end) ? wp[1] : 0u;
+        v[k].z = (a + 8 < end) ? wp[2] : 0u;
+        v[k].w = (a + 12 < end) ? wp[3] : 0u;
+        w4[k] = (a + 16 < end) ? wp[4] : 0u;
     }
     __device__ __forceinline__ uint4 value(int k, const char *sp) const {
         if (A16) return v[k];
@@ -1216,6 +1240,11 @@ __device__ __forceinline__ void small_items(const ExecParams &P, const SmallShar
     }
 }
 
+// kSmallLocal with P.small_swork: the WORK rows after the cached moves (16-B aligned)
+__host__ __device__ __forceinline__ size_t swork_offset(const ExecParams &P) {
+    return ((size_t)P.small_cache * sizeof(Move) + 15) / 16 * 16;
+}
+
 // Single-GPU launches with every move cached (kSmallLocal): each move is resolved ONCE, in the
 // prologue, to absolute source / destination pointers and a byte count, in place of the cached
 // Move -- the per-item path is then one shared-memory record and no base-table lookups.
@@ -1225,7 +1254,9 @@ struct RMove {
     uint64_t doff;     // fanout: byte offset inside every rank's dst_kind buffer
     uint32_t n;        // bytes
     uint32_t flow;
-    uint8_t fanout, dst_kind, pad[6];
+    uint8_t fanout, dst_kind;
+    uint8_t src_sm, dst_sm;   // source / destination in shared memory (P.small_swork)
+    uint8_t pad[4];
 };
 static_assert(sizeof(RMove) == sizeof(Move), "resolved moves overwrite the cached moves 1:1");
 
@@ -1252,7 +1283,8 @@ __device__ __forceinline__ void small_items_loc(const ExecParams &P, const Small
             const uint32_t o = (it & mask) * 16;
             if (o >= m.n) continue;
             sp[k] = m.src + o;
-            R.issue(k, sp[k], min(16u, m.n - o));
+            if (m.src_sm) R.issue_generic(k, sp[k], min(16u, m.n - o));
+            else R.issue(k, sp[k], min(16u, m.n - o));
         }
         TRACE(1);
 #pragma unroll
@@ -1263,11 +1295,13 @@ __device__ __forceinline__ void small_items_loc(const ExecParams &P, const Small
             const uint32_t o = (it & mask) * 16;
             const uint32_t len = min(16u, m.n - o);
             const uint4 val = R.value(k, sp[k]);
-            if (!m.fanout) {
+            if (m.dst_sm) {
+                store_piece_generic(m.dst + o, val, len);
+            } else if (!m.fanout) {
                 store_piece<A16>(m.dst + o, val, len);
             } else {
 #pragma unroll 1
-                for (int r = 0; r < P.p; r++) store_piece<A16>(S.rb[m.dst_kind][r] + m.doff + o, val, len);
+                for (int r = 0; r < P.p; r++) store_piece_generic(S.rb[m.dst_kind][r] + m.doff + o, val, len);
             }
         }
     }
@@ -1378,7 +1412,7 @@ __device__ __noinline__ uint32_t small_own_list(const ExecParams &P, SmallShared
     const int t = threadIdx.x;
     if (t == 0) S.n_own = 0;
     __syncthreads();
-    for (int i = t; i < nm; i += kSmallThreads) {
+    for (int i = t; i < nm; i += (int)blockDim.x) {
         const uint32_t flow = resolved ? reinterpret_cast<const RMove *>(mv)[i].flow : mv[i].flow;
         if ((int)(flow % (uint32_t)P.small_own) == (int)blockIdx.x) own[atomicAdd(&S.n_own, 1u)] = (uint16_t)i;
     }
@@ -1424,8 +1458,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
     Step st_r;
     if (ld_step) st_r = prog.steps[t];
     if (LOC) {   // one GPU, every move cached: resolve the moves to pointers once, here
-        char *const work0 = P.dc->work_base[0];
-        for (int i = t; i < prog.nmoves; i += kSmallThreads) {
+        char *const work0 = P.small_swork ? small_dyn + swork_offset(P) : P.dc->work_base[0];
+        for (int i = t; i < prog.nmoves; i += (int)blockDim.x) {
             const Move m = prog.moves[i];
             RMove r;
             r.src = local_base(P, work0, m.src_kind, m.src_rank) + (uint64_t)m.src_off * P.unit;
@@ -1435,14 +1469,16 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
             r.flow = m.flow;
             r.fanout = m.fanout;
             r.dst_kind = m.dst_kind;
+            r.src_sm = P.small_swork && m.src_kind == BK_WORK;
+            r.dst_sm = P.small_swork && m.dst_kind == BK_WORK && !m.fanout;
             reinterpret_cast<RMove *>(smoves)[i] = r;
         }
     } else if (cached) {
-        for (int i = t; i < prog.nmoves; i += kSmallThreads) smoves[i] = prog.moves[i];
+        for (int i = t; i < prog.nmoves; i += (int)blockDim.x) smoves[i] = prog.moves[i];
     }
     if (ld_step) S.steps[t] = StepInfo{st_r.move_begin, st_r.move_end - st_r.move_begin, st_r.signal_mask, st_r.wait_mask};
     if (t < P.G) {
-        S.work_base[t] = P.dc->work_base[t];
+        S.work_base[t] = (LOC && P.small_swork) ? small_dyn + swork_offset(P) : P.dc->work_base[t];
         S.sym[t] = P.dc->sym[t];
         S.recv_base[t] = P.mode == 0 ? P.recv
                          : P.mode == 1 ? (t == g ? P.recv + (uint64_t)t * P.R * P.recv_stride : nullptr)
@@ -1480,15 +1516,15 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
         // items = (move, 16-byte piece); thread t takes items t, t+T, ... four at a time:
         // all four loads in flight before the stores
         uint32_t items = (uint32_t)st.nm * ppm;
-        uint32_t TT = gridDim.x * kSmallThreads;
-        uint32_t base0 = blockIdx.x * kSmallThreads + t;
+        uint32_t TT = gridDim.x * blockDim.x;
+        uint32_t base0 = blockIdx.x * blockDim.x + t;
         const uint16_t *idx = nullptr;
         if (P.small_own) {          // this CTA's flows only (compacted move list), all its threads
             idx = reinterpret_cast<uint16_t *>(small_dyn + (size_t)P.small_cache * sizeof(Move));
             items = small_own_list(P, S, mvs + st.first, st.nm,
                                    reinterpret_cast<uint16_t *>(small_dyn + (size_t)P.small_cache * sizeof(Move)), LOC) *
                     ppm;
-            TT = kSmallThreads;
+            TT = blockDim.x;
             base0 = t;
         }
         // 16-B fast path: the host vouched for every local offset / length / base, and the
@@ -1555,7 +1591,10 @@ static cudaError_t launch_small_t(const ExecParams &P, size_t max_dyn, size_t sm
                                   bool pdl, cudaStream_t stream) {
     const cudaError_t a = small_attr<KM, AK>(max_dyn);
     if (a != cudaSuccess) return a;
-    return launch_kernel(mpxa_small_kernel<KM, AK>, P, grid, dim3(kSmallThreads), smem, cooperative, pdl, stream);
+    // P.small_threads: fewer threads for launches with few pieces per step -- the idle warps'
+    // step bookkeeping competes with the working warp for issue slots (measured)
+    const int nt = P.small_threads > 0 && !P.small_var ? P.small_threads : kSmallThreads;
+    return launch_kernel(mpxa_small_kernel<KM, AK>, P, grid, dim3(nt), smem, cooperative, pdl, stream);
 }
 
 template <int KM>
@@ -1571,9 +1610,11 @@ static cudaError_t launch_small_km(const ExecParams &P, size_t max_dyn, size_t s
 cudaError_t launch_small(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream) {
     const dim3 grid(nC, nG);
     if (!P.small_var && P.mode == 0 && P.G == 1 && P.small_cache > 0 && P.p <= kRankTable)
-        return launch_small_km<kSmallLocal>(P, kSmallMovesSmem * (sizeof(Move) + sizeof(uint16_t)),
-                                            (size_t)P.small_cache * sizeof(Move) +
-                                                (P.small_own ? (size_t)kSmallMovesSmem * sizeof(uint16_t) : 0),
+        return launch_small_km<kSmallLocal>(P, kSmallMovesSmem * sizeof(Move) + kSmallWorkSmem,
+                                            P.small_swork ? swork_offset(P) + (size_t)P.R * (size_t)P.work_stride
+                                                          : (size_t)P.small_cache * sizeof(Move) +
+                                                                (P.small_own ? (size_t)kSmallMovesSmem * sizeof(uint16_t)
+                                                                             : 0),
                                             grid, cooperative, pdl, stream);
     if (P.small_var)
         return launch_small_km<kSmallVar>(P, kSmallMovesSmem * sizeof(Move) +

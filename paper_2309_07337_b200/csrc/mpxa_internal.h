@@ -36,6 +36,7 @@ constexpr int kMaxDynTiles = 64;      // dynamic mode: move tiles per step (queu
 constexpr uint64_t kSmallKernelMax = 8192;  // longest move (bytes) the small-message kernel takes
 constexpr int kSmallMovesSmem = 2048;       // program moves cached in shared memory by the small kernel
 enum { kSmallCommon = 0, kSmallVar = 1, kSmallLocal = 2 };   // small-kernel instantiations
+constexpr int kSmallWorkSmem = 96 << 10;    // kSmallLocal: WORK rows in shared memory up to this size
 constexpr int kRankTable = 256;   // small kernel: per-rank buffer bases kept in shared memory
 constexpr int kMaxWindows = 16;    // registered recv windows per process
 
@@ -156,7 +157,10 @@ struct ExecParams {
                                // owner across steps -> __syncthreads suffices); 0 = off
     int32_t small_var;         // small kernel: moves of very different lengths -- pieces counted
                                // exactly per tile of moves (block scan) instead of max-move slots
-    int32_t pad6[2];
+    int32_t small_swork;       // small kernel, one CTA on one GPU, moves resolved (kSmallLocal): the
+                               // WORK rows live in this CTA's dynamic shared memory after the
+                               // cached moves, so steps chain through shared memory
+    int32_t small_threads;     // small kernel block size (0 = 512); >= p, >= nsteps
     int32_t dyn_sync;          // multi-step dynamic mode: steps separated by a per-GPU-row CTA
                                // barrier and ONE flag per peer GPU (slot 0), so any CTA may move
                                // any piece (no flow ownership needed)
