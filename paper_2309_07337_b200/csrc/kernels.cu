@@ -28,6 +28,12 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p) {
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+// Signalling pattern: every thread's data stores, __syncthreads, then one thread's release
+// store at system scope.  The release is cumulative over everything that happens-before it
+// (the CTA barrier orders the other threads' stores before it; the producer's bulk stores
+// are completed and proxy-fenced before the barrier), so no separate fence.sc.sys is issued:
+// it compiled to MEMBAR.SC.SYS + L1 invalidation and cost ~2-4 us per signal (clock64
+// stamps, 4 emulated GPUs).
 __device__ __forceinline__ void st_release_sys(uint64_t *p, uint64_t v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -855,7 +861,6 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
         CtsSlot *slot = &S.sym[t]->cts[g];
         if (P.mode == 2) { slot->win = P.recv_win; slot->off = P.recv_off; }
         else { slot->win = 0; slot->off = (uint64_t)(uintptr_t)(P.recv + (uint64_t)g * P.R * P.recv_stride); }
-        __threadfence_system();
         st_release_sys(&slot->epoch, epoch);
     }
 
@@ -986,14 +991,12 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
             if (s + 1 < nsteps || (multi && st.signal_mask)) row_barrier(P, S, g, s);
             if (S.abort_flag) return;
             if (multi && c == 0 && st.signal_mask && t < 32 && ((st.signal_mask >> t) & 1u)) {
-                __threadfence_system();
                 st_release_sys(&S.sym[t]->flags[g][0], (epoch << 8) | (uint64_t)(s + 1));
             }
             continue;
         }
         // ---- signal the peers written in this step (this CTA's share) ----
         if (multi && st.signal_mask && t < 32 && ((st.signal_mask >> t) & 1u)) {
-            __threadfence_system();
             st_release_sys(&S.sym[t]->flags[g][c], (epoch << 8) | (uint64_t)(s + 1));
         }
     }
@@ -1256,14 +1259,20 @@ struct RMove {
     uint32_t flow;
     uint8_t fanout, dst_kind;
     uint8_t src_sm, dst_sm;   // source / destination in shared memory (P.small_swork)
-    uint8_t pad[4];
+    uint8_t dst_remote;       // destination on a peer GPU: base from the CTS-filled table at store
+    uint8_t pad;
+    uint16_t dst_rank;
 };
 static_assert(sizeof(RMove) == sizeof(Move), "resolved moves overwrite the cached moves 1:1");
 
-__device__ __forceinline__ char *local_base(const ExecParams &P, char *work0, int kind, int rank) {
-    if (kind == BK_SEND) return (char *)P.send + (uint64_t)rank * P.send_stride;
-    if (kind == BK_RECV) return P.recv + (uint64_t)rank * P.recv_stride;
-    return work0 + (uint64_t)rank * P.work_stride;
+// buffer base of `rank`, a rank of this CTA's GPU g (every move reads there; destinations on
+// g too), from the launch parameters alone
+__device__ __forceinline__ char *local_base(const ExecParams &P, int g, char *work_g, int kind, int rank) {
+    const uint64_t local = (uint64_t)(rank - g * P.R);
+    if (kind == BK_SEND)
+        return (char *)P.send + (P.mode == 2 ? 0 : (uint64_t)g * P.R * P.send_stride) + local * P.send_stride;
+    if (kind == BK_RECV) return P.recv + (P.mode == 1 ? (uint64_t)g * P.R * P.recv_stride : 0) + local * P.recv_stride;
+    return work_g + local * P.work_stride;
 }
 
 template <bool A16>
@@ -1298,7 +1307,7 @@ __device__ __forceinline__ void small_items_loc(const ExecParams &P, const Small
             if (m.dst_sm) {
                 store_piece_generic(m.dst + o, val, len);
             } else if (!m.fanout) {
-                store_piece<A16>(m.dst + o, val, len);
+                store_piece<A16>((m.dst_remote ? S.rb[m.dst_kind][m.dst_rank] + m.doff : m.dst) + o, val, len);
             } else {
 #pragma unroll 1
                 for (int r = 0; r < P.p; r++) store_piece_generic(S.rb[m.dst_kind][r] + m.doff + o, val, len);
@@ -1378,7 +1387,6 @@ __device__ __noinline__ void small_post_cts(const ExecParams &P, SmallShared &S,
         CtsSlot *slot = &S.sym[t]->cts[g];
         if (P.mode == 2) { slot->win = P.recv_win; slot->off = P.recv_off; }
         else { slot->win = 0; slot->off = (uint64_t)(uintptr_t)(P.recv + (uint64_t)g * P.R * P.recv_stride); }
-        __threadfence_system();
         st_release_sys(&slot->epoch, epoch);
     }
 }
@@ -1431,7 +1439,6 @@ __device__ __noinline__ bool small_step_exit(const ExecParams &P, SmallShared &S
         if (S.abort_flag) return false;
     }
     if (multi && signal_mask && t < 32 && ((signal_mask >> t) & 1u) && (!P.dyn_sync || blockIdx.x == 0)) {
-        __threadfence_system();
         st_release_sys(&S.sym[t]->flags[g][fslot], (epoch << 8) | (uint64_t)(s + 1));
     }
     return true;
@@ -1457,14 +1464,17 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
     const bool ld_step = steps_smem && t < prog.nsteps;
     Step st_r;
     if (ld_step) st_r = prog.steps[t];
-    if (LOC) {   // one GPU, every move cached: resolve the moves to pointers once, here
-        char *const work0 = P.small_swork ? small_dyn + swork_offset(P) : P.dc->work_base[0];
+    if (LOC) {   // every move cached: resolve the moves to pointers once, here (destinations on
+                 // peer GPUs keep their kind / rank: those bases arrive with the CTS)
+        char *const work_g = P.small_swork ? small_dyn + swork_offset(P) : P.dc->work_base[g];
         for (int i = t; i < prog.nmoves; i += (int)blockDim.x) {
             const Move m = prog.moves[i];
             RMove r;
-            r.src = local_base(P, work0, m.src_kind, m.src_rank) + (uint64_t)m.src_off * P.unit;
+            r.src = local_base(P, g, work_g, m.src_kind, m.src_rank) + (uint64_t)m.src_off * P.unit;
             r.doff = (uint64_t)m.dst_off * P.unit;
-            r.dst = m.fanout ? nullptr : local_base(P, work0, m.dst_kind, m.dst_rank) + r.doff;
+            r.dst_remote = !m.fanout && (int)m.dst_rank / P.R != g;
+            r.dst_rank = m.dst_rank;
+            r.dst = (m.fanout || r.dst_remote) ? nullptr : local_base(P, g, work_g, m.dst_kind, m.dst_rank) + r.doff;
             r.n = (uint32_t)((uint64_t)m.len * P.unit);
             r.flow = m.flow;
             r.fanout = m.fanout;
@@ -1513,6 +1523,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
         }
         const int fslot = P.dyn_sync ? 0 : (int)blockIdx.x;   // the row's flag in sync mode
         if (multi && !small_step_enter(P, S, g, s, prev_wait, st.signal_mask, epoch, fslot)) return;
+        TRACE(13);
         // items = (move, 16-byte piece); thread t takes items t, t+T, ... four at a time:
         // all four loads in flight before the stores
         uint32_t items = (uint32_t)st.nm * ppm;
@@ -1551,9 +1562,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
         TRACE(3 + (s < 7 ? s : 7));   // stamps 3..10: end of steps 0..7
         if ((P.dyn_sync && (s + 1 < prog.nsteps || (multi && st.signal_mask))) || (multi && st.signal_mask))
             if (!small_step_exit(P, S, g, s, prog.nsteps, st.signal_mask, epoch, fslot)) return;
+        TRACE(14);
         prev_wait = st.wait_mask;
     }
     if (multi || P.dyn_sync) small_finish(P, S, g, prog.nsteps, prev_wait, epoch);
+    TRACE(15);
     CTA_STAMP(1);
 }
 
@@ -1609,7 +1622,7 @@ static cudaError_t launch_small_km(const ExecParams &P, size_t max_dyn, size_t s
 
 cudaError_t launch_small(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream) {
     const dim3 grid(nC, nG);
-    if (!P.small_var && P.mode == 0 && P.G == 1 && P.small_cache > 0 && P.p <= kRankTable)
+    if (!P.small_var && P.small_cache > 0 && P.p <= kRankTable)
         return launch_small_km<kSmallLocal>(P, kSmallMovesSmem * sizeof(Move) + kSmallWorkSmem,
                                             P.small_swork ? swork_offset(P) + (size_t)P.R * (size_t)P.work_stride
                                                           : (size_t)P.small_cache * sizeof(Move) +
@@ -1667,7 +1680,6 @@ __global__ void part_start_recv(unsigned long long *rcycle, unsigned long long *
     if (threadIdx.x == 0) {
         const unsigned long long c = *rcycle + 1ull;
         *rcycle = c;
-        __threadfence_system();
         asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(cts_remote), "l"(c) : "memory");
     }
 }
