@@ -42,6 +42,15 @@
  *    MPXA_ERR_TIMEOUT from the device watchdog, not as a hang.
  *  - Multi-process mode (nprocs > 1): one process per GPU; recvbufs written by peers
  *    must lie in buffers registered with mpxa_register (or bound by a persistent *_init).
+ *  - Completion across GPUs: large launches write peers' recvbufs
+ *    directly after a clear-to-send from each receiver and release a flag per step; small
+ *    launches (<= 32 KiB per GPU pair) run EAGER: the payload travels as 8-byte words that
+ *    each carry the launch's sequence number into the receiver's staging (two parities,
+ *    alternating per eager launch), the receiver copies it out -- no clear-to-send, no
+ *    fence.  MPXA_NO_LL=1 disables eager mode.  The eager form of a schedule is built on its
+ *    first launch for a dtype size; if that first launch is inside a CUDA-graph capture the
+ *    launch uses the direct protocol instead, so in multi-process mode either every process
+ *    or none captures the first call of a schedule.
  */
 #ifndef MPXA_H
 #define MPXA_H

@@ -27,8 +27,10 @@ typedef struct {
     int64_t src_off, dst_off, len;   /* units                                   */
     uint32_t flow;                   /* identity of the data moved (origin block / segment) */
     uint16_t src_rank, dst_rank;
-    uint8_t src_kind, dst_kind;      /* 0 send buffer, 1 recv buffer, 2 library workspace */
-    uint8_t fanout;                  /* 1: to every rank's dst_kind buffer at dst_off */
+    uint8_t src_kind, dst_kind;      /* 0 send buffer, 1 recv buffer, 2 library workspace,
+                                        3 eager staging (mpxa_plan_eager) */
+    uint8_t fanout;                  /* 1: to every rank's dst_kind buffer at dst_off;
+                                        2: to every rank of the executing GPU (eager plans) */
     uint8_t pad[5];
 } mpxa_plan_move;
 
@@ -54,6 +56,16 @@ int mpxa_plan_build_neighbor(int p, int R, int G, int g, int locality, const int
                              const int64_t *rc, const int64_t *rd, const int *outdeg, const int *dst,
                              const int64_t *sc, const int64_t *sd, const int64_t *send_idx,
                              const int64_t *recv_idx, void **plan);
+/* The eager (LL) form of a multi-GPU plan for `unit` bytes per unit -- what small launches
+ * run (SURVEY.md §8 A9 "epoch-parity staging for eager mode"): a move whose destination is on
+ * peer GPU d becomes a SEND move with dst_kind 3 (staging), dst_rank = d, dst_off = word
+ * offset (4 payload bytes per 8-byte word, each word carrying the launch's flag) on the
+ * source GPU, and a RECEIVE move with src_kind 3, src_rank = source GPU, src_off = word
+ * offset on GPU d.  Fan-out moves keep fanout = 2 (this GPU's ranks only) plus one stream per
+ * peer GPU.  In each step the receive moves come last; wait_mask = their number.  Pairs
+ * without data exchange one flag word (len 0).  MPXA_ERR_ALGO when G < 2 or a GPU pair needs
+ * more than 8192 words.  Released with mpxa_plan_free. */
+int mpxa_plan_eager(const void *plan, size_t unit, void **eager);
 int mpxa_plan_info(const void *plan, mpxa_plan_info_t *info);
 /* copies GPU `gpu`'s steps / moves; *n in: capacity, out: count */
 int mpxa_plan_steps(const void *plan, int gpu, mpxa_plan_step *out, int *n);

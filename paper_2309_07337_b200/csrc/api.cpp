@@ -101,6 +101,10 @@ struct DevProg {
     // (var_chop units each), built on first use for a unit, freed with its parent
     mutable std::shared_ptr<DevProg> var;
     mutable int64_t var_chop = 0;
+    // eager (LL) companion for one unit (ll_unit); ll_ok < 0: this program/unit is ineligible
+    mutable std::shared_ptr<DevProg> ll;
+    mutable uint64_t ll_unit = 0;
+    mutable int ll_ok = 0;
 };
 
 // dynamic-mode eligibility facts of a program (DevProg::max_gpu_moves, max_gpu_bytes_units)
@@ -205,6 +209,7 @@ struct mpxa_comm_s {
     int var_tiles = 4;                     // ... and warp tiles (32 moves) per CTA
     bool swork = true;                     // small kernel, one CTA on one GPU: WORK in shared memory
     int small_nt = 64;                     // small kernel block size for launches with few pieces
+    bool ll = true;                        // eager (LL) mode for small multi-GPU launches
     int force_ns = 0, force_nf = 0;           // MPXA_NS / MPXA_NF overrides (tuning)
     int force_big = -1;                       // MPXA_TMA_BIG=0/1 override (tuning)
     bool force_exec = false;                  // MPXA_NO_SMALL=1: never use the small-message kernel
@@ -483,6 +488,148 @@ int var_program(const DevProg &dp, int64_t chop, const DevProg *&out) {
     return MPXA_SUCCESS;
 }
 
+// Upload a companion program (small kernel only: no flow index) as a self-freeing DevProg.
+static int upload_companion(Program &&Q, std::shared_ptr<DevProg> &out) {
+    auto v = std::shared_ptr<DevProg>(new DevProg, [](DevProg *d) {
+        if (d->dmem) cudaFree(d->dmem);
+        delete d;
+    });
+    size_t n = serialized_size(Q);
+    CK(cudaMalloc(&v->dmem, n ? n : 16));
+    std::vector<char> buf;
+    serialize(Q, buf, (uintptr_t)v->dmem);
+    CK(cudaMemcpy(v->dmem, buf.data(), n, cudaMemcpyHostToDevice));
+    v->gp.assign((const GpuProg *)buf.data(), (const GpuProg *)buf.data() + Q.G);
+    v->bytes = n;
+    v->host = std::move(Q);
+    v->nsteps = v->host.nsteps();
+    prog_facts(*v);
+    out = v;
+    return MPXA_SUCCESS;
+}
+
+// Eager (LL) companion of a program for one unit ("epoch-parity staging for
+// eager mode"): every move whose destination is on a peer GPU d becomes
+//   on its GPU g:  a SEND move to (BK_LL, d, word offset w) -- the payload as 4-byte words,
+//                  each stored with the launch's flag in one 8-byte word into d's staging;
+//   on GPU d:      a RECEIVE move (BK_LL, g, w) -> the original destination, which polls
+//                  the words until they carry the flag.
+// Fan-out moves (allgather direct) keep a local fan-out (fanout = 2: this GPU's ranks) and
+// send one stream per peer GPU, which the peer fans out to its own ranks.  Word offsets run
+// per (g, d) pair across all steps of the launch; a pair without data still exchanges one
+// flag word, so every GPU hears from every peer in every eager launch -- which is what makes
+// the two staging parities safe to alternate.  In each step the receive moves come last
+// (Step::wait_mask = their number): a CTA issues all its sends before it polls.
+// Returns false when a pair needs more than kLLWords words or a GPU more moves than the
+// small kernel caches.
+static bool build_ll(const Program &P, uint64_t unit, int R, Program &Q) {
+    const int G = P.G, ns = P.nsteps();
+    Q = Program();
+    Q.p = P.p; Q.R = P.R; Q.G = G;
+    Q.nflows = P.nflows;
+    Q.work_units = P.work_units;
+    Q.max_step_units = P.max_step_units;
+    Q.max_move = P.max_move;
+    Q.signals = 0;
+    Q.steps.assign(G, {});
+    Q.moves.assign(G, {});
+    Q.findex.assign(G, {});
+    std::vector<int64_t> wc((size_t)G * G, 0);
+    auto words = [&](const Move &m) { return std::max<int64_t>(1, (int64_t)((m.len * unit + 3) / 4)); };
+    for (int s = 0; s < ns; s++) {
+        std::vector<std::vector<Move>> out(G), in(G);
+        for (int g = 0; g < G; g++) {
+            const Step &st = P.steps[g][s];
+            for (int32_t i = st.move_begin; i < st.move_end; i++) {
+                const Move &m = P.moves[g][i];
+                if (m.fanout) {
+                    Move x = m;
+                    x.fanout = 2;
+                    out[g].push_back(x);
+                }
+                for (int d = 0; d < G; d++) {
+                    if (d == g) continue;
+                    if (!m.fanout && (int)m.dst_rank / R != d) continue;
+                    Move snd = m, rcv = m;
+                    snd.fanout = 0;
+                    snd.dst_kind = BK_LL;
+                    snd.dst_rank = (uint16_t)d;
+                    snd.dst_off = wc[(size_t)g * G + d];
+                    rcv.fanout = m.fanout ? 2 : 0;
+                    rcv.src_kind = BK_LL;
+                    rcv.src_rank = (uint16_t)g;
+                    rcv.src_off = wc[(size_t)g * G + d];
+                    wc[(size_t)g * G + d] += words(m);
+                    out[g].push_back(snd);
+                    in[d].push_back(rcv);
+                }
+                if (!m.fanout && (int)m.dst_rank / R == g) out[g].push_back(m);
+            }
+        }
+        if (s == 0)   // flag-only words for pairs without data in the whole launch
+            for (int g = 0; g < G; g++)
+                for (int d = 0; d < G; d++) {
+                    if (d == g) continue;
+                    bool any = false;
+                    for (int s2 = 0; s2 < ns && !any; s2++) {
+                        const Step &st = P.steps[g][s2];
+                        for (int32_t i = st.move_begin; i < st.move_end && !any; i++) {
+                            const Move &m = P.moves[g][i];
+                            any = m.fanout || (int)m.dst_rank / R == d;
+                        }
+                    }
+                    if (any) continue;
+                    Move snd{}, rcv{};
+                    snd.src_kind = BK_SEND;
+                    snd.src_rank = (uint16_t)(g * R);
+                    snd.dst_kind = BK_LL;
+                    snd.dst_rank = (uint16_t)d;
+                    rcv.src_kind = BK_LL;
+                    rcv.src_rank = (uint16_t)g;
+                    rcv.dst_kind = BK_RECV;
+                    rcv.dst_rank = (uint16_t)(d * R);
+                    wc[(size_t)g * G + d] = 1;
+                    out[g].push_back(snd);
+                    in[d].push_back(rcv);
+                }
+        for (int g = 0; g < G; g++) {
+            Step st = P.steps[g][s];
+            st.move_begin = (int32_t)Q.moves[g].size();
+            for (const Move &m : out[g]) Q.moves[g].push_back(m);
+            for (const Move &m : in[g]) Q.moves[g].push_back(m);
+            st.move_end = (int32_t)Q.moves[g].size();
+            st.signal_mask = 0;
+            st.wait_mask = (uint32_t)in[g].size();
+            st.flow_index = 0;
+            st.dense_base = -1;
+            Q.max_step_moves = std::max<int64_t>(Q.max_step_moves, st.move_end - st.move_begin);
+            Q.steps[g].push_back(st);
+        }
+    }
+    for (int64_t w : wc)
+        if (w > kLLWords) return false;
+    for (int g = 0; g < G; g++)
+        if (Q.moves[g].size() > (size_t)kSmallMovesSmem) return false;
+    return true;
+}
+
+// The eager companion of dp for `unit`, built on first use (never inside a stream capture:
+// the upload is synchronous).  nullptr when ineligible or not available.
+static const DevProg *ll_program(mpxa_comm_t c, const DevProg &dp, uint64_t unit, cudaStream_t stream) {
+    if (dp.ll_unit == unit && dp.ll_ok != 0) return dp.ll_ok > 0 ? dp.ll.get() : nullptr;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (dp.per_call || cudaStreamIsCapturing(stream, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
+        return nullptr;
+    dp.ll.reset();
+    dp.ll_unit = unit;
+    dp.ll_ok = -1;
+    Program Q;
+    if (!build_ll(dp.host, unit, c->Rg, Q)) return nullptr;
+    if (upload_companion(std::move(Q), dp.ll) != MPXA_SUCCESS) return nullptr;
+    dp.ll_ok = 1;
+    return dp.ll.get();
+}
+
 int cached_uniform(mpxa_comm_t c, int op, int algo, int stage, std::shared_ptr<DevProg> &out) {
     auto key = std::make_tuple(op, algo, stage, c->g);
     auto it = c->cache.find(key);
@@ -662,6 +809,16 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
             E.progs = (const GpuProg *)sp->dmem;
             if (!c->emulated) E.prog = sp->gp[c->nprocs > 1 ? c->proc : 0];
         }
+        // eager (LL) mode: several GPUs, small launches -- the payload travels with its flags,
+        // no CTS, no system-scope release (build_ll)
+        if (c->ll && c->G > 1 && !var && c->p <= kRankTable) {
+            if (const DevProg *lp = ll_program(c, dp, unit, stream)) {
+                sp = lp;
+                E.small_ll = 1;
+                E.progs = (const GpuProg *)sp->dmem;
+                if (!c->emulated) E.prog = sp->gp[c->nprocs > 1 ? c->proc : 0];
+            }
+        }
         size_t nmoves_g = 0;
         for (const auto &mv : sp->host.moves) nmoves_g = std::max(nmoves_g, mv.size());
         E.small_cache = nmoves_g <= (size_t)kSmallMovesSmem ? (int32_t)nmoves_g : 0;
@@ -670,6 +827,10 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
         if (small_own) nC = std::min<int>(nC, dp.host.nflows);
         E.dyn_sync = small_sync && nC > 1;
         E.small_own = small_own && nC > 1 ? nC : 0;
+        if (E.small_ll && E.small_own) {   // eager steps take every piece of the step (no flow
+            E.small_own = 0;               // ownership): CTAs meet at the row barrier instead
+            E.dyn_sync = 1;
+        }
         E.small_var = var && !E.small_own;
         if (E.small_var) {   // warp tiles of 32 moves, about var_tiles per CTA
             nC = (int)std::min<uint64_t>((uint64_t)c->cap_small,
@@ -1160,6 +1321,7 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     if (const char *e = getenv("MPXA_VAR_TILES")) c->var_tiles = std::max(1, atoi(e));
     if (const char *e = getenv("MPXA_SWORK")) c->swork = atoi(e) != 0;
     if (const char *e = getenv("MPXA_SMALL_NT")) c->small_nt = std::max(32, std::min(512, atoi(e)));
+    if (const char *e = getenv("MPXA_NO_LL")) c->ll = atoi(e) == 0;
     CK(cudaHostAlloc((void **)&c->err_host, sizeof(int32_t), cudaHostAllocMapped));
     *c->err_host = 0;
     CK(cudaHostGetDevicePointer((void **)&c->err_dev, c->err_host, 0));
@@ -1871,6 +2033,17 @@ int mpxa_plan_build_neighbor(int p, int R, int G, int g, int locality, const int
     int r = build_neighbor(*P, locality != 0, p, R, G, g, indeg, src, rc, rd, outdeg, dst, sc, sd, send_idx, recv_idx);
     if (r) { delete P; return r; }
     *plan = P;
+    return MPXA_SUCCESS;
+}
+
+int mpxa_plan_eager(const void *plan, size_t unit, void **eager) {
+    if (!plan || !eager || unit == 0) return MPXA_ERR_ARG;
+    *eager = nullptr;
+    const Program *P = (const Program *)plan;
+    if (P->G < 2) return MPXA_ERR_ALGO;
+    auto Q = new Program();
+    if (!build_ll(*P, unit, P->p / P->G, *Q)) { delete Q; return MPXA_ERR_ALGO; }
+    *eager = Q;
     return MPXA_SUCCESS;
 }
 

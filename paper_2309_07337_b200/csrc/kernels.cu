@@ -1108,6 +1108,8 @@ struct SmallShared {
     uint64_t epoch;
     uint32_t cts_ok;
     int abort_flag;
+    uint64_t ll_seq;                 // eager mode: this launch's sequence number (the flag) ...
+    uint64_t ll_par;                 // ... and the byte offset of its staging parity
 };
 
 __device__ __forceinline__ char *sbase(const ExecParams &P, const SmallShared &S, int kind, int rank) {
@@ -1260,7 +1262,8 @@ struct RMove {
     uint8_t fanout, dst_kind;
     uint8_t src_sm, dst_sm;   // source / destination in shared memory (P.small_swork)
     uint8_t dst_remote;       // destination on a peer GPU: base from the CTS-filled table at store
-    uint8_t pad;
+    uint8_t ll;               // eager mode: 1 = send words to dst (peer staging, parity 0 address),
+                              // 2 = receive words from src (own staging); fanout 2 = own ranks only
     uint16_t dst_rank;
 };
 static_assert(sizeof(RMove) == sizeof(Move), "resolved moves overwrite the cached moves 1:1");
@@ -1311,6 +1314,100 @@ __device__ __forceinline__ void small_items_loc(const ExecParams &P, const Small
             } else {
 #pragma unroll 1
                 for (int r = 0; r < P.p; r++) store_piece_generic(S.rb[m.dst_kind][r] + m.doff + o, val, len);
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_sys(uint64_t *p, uint64_t v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Eager (LL) mode, one phase of a step (P.small_ll).  RECV = false: local moves
+// and sends -- a send piece stores its (up to) four payload words, each with the launch's flag
+// in the high half, into the peer's staging (no fence: every 8-byte word is its own signal).
+// RECV = true: receive pieces poll their words in this GPU's staging until all carry the flag,
+// then store the payload to the destination (fan-out 2: every rank of this GPU).  Flag-only
+// moves (n = 0) send / await one word.
+template <bool A16, bool RECV>
+__device__ __forceinline__ void small_items_ll(const ExecParams &P, SmallShared &S, const RMove *mv, uint32_t items,
+                                               uint32_t lg, uint32_t TT, uint32_t base0, int g) {
+    const uint32_t mask = (1u << lg) - 1u;
+    const uint64_t flag = S.ll_seq << 32, par = S.ll_par;
+    for (uint32_t base = base0; base < items; base += TT * kBatch) {
+        PieceRegs<A16> R;
+        uint4 lv[kBatch];
+        bool on[kBatch];
+#pragma unroll
+        for (int k = 0; k < kBatch; k++) {
+            on[k] = false;
+            const uint32_t it = base + (uint32_t)k * TT;
+            if (it >= items) continue;
+            const RMove &m = mv[it >> lg];
+            const uint32_t o = (it & mask) * 16;
+            if (o >= m.n && !(m.ll && o == 0)) continue;
+            on[k] = true;
+            if (RECV) continue;
+            if (o < m.n) R.issue(k, m.src + o, min(16u, m.n - o));
+        }
+        if (RECV) {   // poll: all words of the piece carry this launch's flag
+#pragma unroll
+            for (int k = 0; k < kBatch; k++) {
+                if (!on[k]) continue;
+                const uint32_t it = base + (uint32_t)k * TT;
+                const RMove &m = mv[it >> lg];
+                const uint32_t o = (it & mask) * 16;
+                const uint32_t nw = m.n > o ? (min(16u, m.n - o) + 3) / 4 : 1;
+                const uint64_t *w = reinterpret_cast<const uint64_t *>(m.src + par) + o / 4;
+                uint32_t d[4] = {0, 0, 0, 0};
+                uint64_t t0 = 0;
+                for (uint32_t j = 0; j < nw; j++) {
+                    uint64_t v = ld_relaxed_sys(w + j);
+                    int spins = 0;
+                    while ((v & 0xffffffff00000000ull) != flag) {
+                        if (++spins > 64) {
+                            __nanosleep(64);
+                            if (!t0) t0 = globaltimer();
+                            else if ((int64_t)(globaltimer() - t0) > P.timeout_ns) {
+                                atomicExch(P.err, 1);
+                                S.abort_flag = 1;
+                                return;
+                            }
+                        }
+                        v = ld_relaxed_sys(w + j);
+                    }
+                    d[j] = (uint32_t)v;
+                }
+                lv[k] = make_uint4(d[0], d[1], d[2], d[3]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kBatch; k++) {
+            if (!on[k]) continue;
+            const uint32_t it = base + (uint32_t)k * TT;
+            const RMove &m = mv[it >> lg];
+            const uint32_t o = (it & mask) * 16;
+            const uint32_t len = m.n > o ? min(16u, m.n - o) : 0u;
+            if (!RECV && m.ll == 1) {   // send: payload words + flag into the peer's staging
+                const uint4 val = len ? R.value(k, m.src + o) : make_uint4(0, 0, 0, 0);
+                uint64_t *w = reinterpret_cast<uint64_t *>(m.dst + par) + o / 4;
+                const uint32_t d[4] = {val.x, val.y, val.z, val.w};
+                const uint32_t nw = len ? (len + 3) / 4 : 1;
+                for (uint32_t j = 0; j < nw; j++) st_relaxed_sys(w + j, flag | d[j]);
+                continue;
+            }
+            if (!len) continue;
+            const uint4 val = RECV ? lv[k] : R.value(k, m.src + o);
+            if (m.fanout == 2) {
+#pragma unroll 1
+                for (int r = g * P.R; r < (g + 1) * P.R; r++) store_piece<A16>(S.rb[m.dst_kind][r] + m.doff + o, val, len);
+            } else {
+                store_piece<A16>(m.dst + o, val, len);
             }
         }
     }
@@ -1406,6 +1503,7 @@ __device__ __noinline__ void small_finish(const ExecParams &P, SmallShared &S, i
         if (atomicAdd(&P.dc->done_ctas, 1u) == gridDim.x * gridDim.y - 1) {
             P.dc->done_ctas = 0;
             if (multi) P.dc->epoch = epoch;
+            if (P.small_ll) P.dc->ll_seq = S.ll_seq;
             if (P.dyn_sync)
                 for (int r = 0; r < (int)gridDim.y; r++) P.dc->dyn_bar[P.mode == 1 ? r : P.my_gpu] = 0;
             __threadfence();
@@ -1448,7 +1546,7 @@ __device__ __noinline__ bool small_step_exit(const ExecParams &P, SmallShared &S
 // AK: 0 = the 16-B path decided per step at run time, 1 = always 16-B, 2 = never (host-known)
 template <int KM, int AK>
 __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __grid_constant__ ExecParams P) {
-    constexpr bool VARK = KM == kSmallVar, LOC = KM == kSmallLocal;
+    constexpr bool VARK = KM == kSmallVar, LLK = KM == kSmallLL, LOC = KM == kSmallLocal || LLK;
     __shared__ SmallShared S;
     extern __shared__ __align__(16) char small_dyn[];
     CTA_STAMP(0);   // the program's moves, when they fit
@@ -1472,9 +1570,13 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
             RMove r;
             r.src = local_base(P, g, work_g, m.src_kind, m.src_rank) + (uint64_t)m.src_off * P.unit;
             r.doff = (uint64_t)m.dst_off * P.unit;
-            r.dst_remote = !m.fanout && (int)m.dst_rank / P.R != g;
+            r.ll = m.dst_kind == BK_LL ? 1 : m.src_kind == BK_LL ? 2 : 0;
+            r.dst_remote = !m.fanout && m.dst_kind != BK_LL && (int)m.dst_rank / P.R != g;
             r.dst_rank = m.dst_rank;
-            r.dst = (m.fanout || r.dst_remote) ? nullptr : local_base(P, g, work_g, m.dst_kind, m.dst_rank) + r.doff;
+            r.dst = (m.fanout || r.dst_remote) ? nullptr
+                    : r.ll == 1 ? reinterpret_cast<char *>(&P.dc->sym[m.dst_rank]->ll[0][g][m.dst_off])
+                                : local_base(P, g, work_g, m.dst_kind, m.dst_rank) + r.doff;
+            if (r.ll == 2) r.src = reinterpret_cast<const char *>(&P.dc->sym[g]->ll[0][m.src_rank][m.src_off]);
             r.n = (uint32_t)((uint64_t)m.len * P.unit);
             r.flow = m.flow;
             r.fanout = m.fanout;
@@ -1501,13 +1603,17 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
         S.cts_ok = 0;
         S.abort_flag = 0;
         S.epoch = multi ? *(volatile uint64_t *)&P.dc->epoch + 1 : 0;
+        if (P.small_ll) {
+            S.ll_seq = *(volatile uint64_t *)&P.dc->ll_seq + 1;
+            S.ll_par = (S.ll_seq & 1) * sizeof(((SymRegion *)nullptr)->ll[0]);
+        }
     }
     // rank bases known now: every rank's SEND / WORK row and the RECV rows of resolved GPUs
     fill_rank_bases(P, S, 0xffffffffu, true);
     __syncthreads();
     TRACE(0);
     const uint64_t epoch = S.epoch;
-    if (multi) small_post_cts(P, S, g, epoch);
+    if (multi && !P.small_ll) small_post_cts(P, S, g, epoch);
     const Move *mvs = cached ? smoves : prog.moves;
     const uint32_t ppm = (uint32_t)P.small_ppm;        // 16-byte pieces per move: power-of-two bound
     const uint32_t lg = 31u - (uint32_t)__clz((int)ppm);
@@ -1522,7 +1628,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
             st = StepInfo{g_st.move_begin, g_st.move_end - g_st.move_begin, g_st.signal_mask, g_st.wait_mask};
         }
         const int fslot = P.dyn_sync ? 0 : (int)blockIdx.x;   // the row's flag in sync mode
-        if (multi && !small_step_enter(P, S, g, s, prev_wait, st.signal_mask, epoch, fslot)) return;
+        if (multi && !P.small_ll && !small_step_enter(P, S, g, s, prev_wait, st.signal_mask, epoch, fslot)) return;
         TRACE(13);
         // items = (move, 16-byte piece); thread t takes items t, t+T, ... four at a time:
         // all four loads in flight before the stores
@@ -1546,7 +1652,18 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
             for (int q = 0; q < P.G; q++)
                 if (((st.signal_mask >> q) & 1u) && ((uintptr_t)S.recv_base[q] & 15)) a16 = false;
         TRACE(12);
-        if (LOC) {
+        if (LLK) {   // sends (and local moves) first, then the receives
+            const RMove *rm = reinterpret_cast<const RMove *>(smoves) + st.first;
+            const int nrecv = (int)st.wait_mask, nsend = st.nm - nrecv;
+            const uint32_t is = (uint32_t)nsend * ppm, ir = (uint32_t)nrecv * ppm;
+            if (a16) {
+                small_items_ll<true, false>(P, S, rm, is, lg, TT, base0, g);
+                small_items_ll<true, true>(P, S, rm + nsend, ir, lg, TT, base0, g);
+            } else {
+                small_items_ll<false, false>(P, S, rm, is, lg, TT, base0, g);
+                small_items_ll<false, true>(P, S, rm + nsend, ir, lg, TT, base0, g);
+            }
+        } else if (LOC) {
             const RMove *rm = reinterpret_cast<const RMove *>(smoves) + st.first;
             if (a16) small_items_loc<true>(P, S, rm, items, lg, TT, base0, idx);
             else small_items_loc<false>(P, S, rm, items, lg, TT, base0, idx);
@@ -1560,10 +1677,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
         TRACE(2);
         __syncthreads();
         TRACE(3 + (s < 7 ? s : 7));   // stamps 3..10: end of steps 0..7
+        if (P.small_ll && S.abort_flag) return;   // a receive timed out (watchdog)
         if ((P.dyn_sync && (s + 1 < prog.nsteps || (multi && st.signal_mask))) || (multi && st.signal_mask))
             if (!small_step_exit(P, S, g, s, prog.nsteps, st.signal_mask, epoch, fslot)) return;
         TRACE(14);
-        prev_wait = st.wait_mask;
+        prev_wait = P.small_ll ? 0u : st.wait_mask;
     }
     if (multi || P.dyn_sync) small_finish(P, S, g, prog.nsteps, prev_wait, epoch);
     TRACE(15);
@@ -1622,6 +1740,9 @@ static cudaError_t launch_small_km(const ExecParams &P, size_t max_dyn, size_t s
 
 cudaError_t launch_small(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream) {
     const dim3 grid(nC, nG);
+    if (P.small_ll)
+        return launch_small_km<kSmallLL>(P, kSmallMovesSmem * (sizeof(Move) + sizeof(uint16_t)),
+                                         (size_t)P.small_cache * sizeof(Move), grid, cooperative, pdl, stream);
     if (!P.small_var && P.small_cache > 0 && P.p <= kRankTable)
         return launch_small_km<kSmallLocal>(P, kSmallMovesSmem * sizeof(Move) + kSmallWorkSmem,
                                             P.small_swork ? swork_offset(P) + (size_t)P.R * (size_t)P.work_stride

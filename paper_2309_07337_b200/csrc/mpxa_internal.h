@@ -35,12 +35,13 @@ constexpr int kMoveTile = kThreads;   // moves staged in shared memory at a time
 constexpr int kMaxDynTiles = 64;      // dynamic mode: move tiles per step (queues per tile)
 constexpr uint64_t kSmallKernelMax = 8192;  // longest move (bytes) the small-message kernel takes
 constexpr int kSmallMovesSmem = 2048;       // program moves cached in shared memory by the small kernel
-enum { kSmallCommon = 0, kSmallVar = 1, kSmallLocal = 2 };   // small-kernel instantiations
+enum { kSmallCommon = 0, kSmallVar = 1, kSmallLocal = 2, kSmallLL = 3 };   // small-kernel instantiations
 constexpr int kSmallWorkSmem = 96 << 10;    // kSmallLocal: WORK rows in shared memory up to this size
 constexpr int kRankTable = 256;   // small kernel: per-rank buffer bases kept in shared memory
 constexpr int kMaxWindows = 16;    // registered recv windows per process
 
-enum BufKind : uint8_t { BK_SEND = 0, BK_RECV = 1, BK_WORK = 2 };
+enum BufKind : uint8_t { BK_SEND = 0, BK_RECV = 1, BK_WORK = 2,
+                         BK_LL = 3 };   // eager (LL) staging word stream: rank = peer GPU, offset in words
 
 // One copy of `len` units from (src_kind, src_rank, src_off) to (dst_kind, dst_rank, dst_off).
 // Offsets and lengths are in UNITS of ExecParams::unit bytes.  fanout = 1: copy to the
@@ -93,9 +94,14 @@ struct CtsSlot {
 };
 
 // Per-GPU symmetric region (device memory, IPC-exported in multi-process mode).
+constexpr int kLLWords = 8192;      // eager staging words per (parity, source GPU): 32 KiB payload
 struct SymRegion {
     CtsSlot cts[kMaxGpus];                    // cts[d]: receiver d cleared this GPU to send
     uint64_t flags[kMaxGpus][kMaxCtas];       // flags[s][c]: src GPU s, CTA c, (epoch<<8)|(step+1)
+    // eager (LL) mode: ll[seq & 1][s][w] = (seq << 32) | 4 payload bytes from source GPU s --
+    // the flag travels in every 8-byte word, so no fence or separate signal is needed; the
+    // parity alternates per eager launch (SURVEY §8 A9 "epoch-parity staging")
+    uint64_t ll[2][kMaxGpus][kLLWords];
 };
 
 // Per-communicator device-resident state (rewritten by the host only between launches:
@@ -112,6 +118,7 @@ struct DevComm {
     uint32_t dyn_next2[kMaxGpus * kMaxDynTiles];  // row, move tile): TMA pieces / LSU pieces;
                                                   // reset by the launch's last CTA
     uint32_t dyn_bar[kMaxGpus];                   // multi-step dynamic mode: per-row step barrier
+    uint64_t ll_seq;                        // eager (LL) launches completed (flag of the next + 1)
     uint64_t trace[32];                     // MPXA_TRACE builds: %globaltimer phase stamps
 };
 
@@ -164,6 +171,10 @@ struct ExecParams {
     int32_t dyn_sync;          // multi-step dynamic mode: steps separated by a per-GPU-row CTA
                                // barrier and ONE flag per peer GPU (slot 0), so any CTA may move
                                // any piece (no flow ownership needed)
+    int32_t small_ll;          // small kernel, eager (LL) companion program: moves to peer GPUs
+                               // are word streams into their staging (BK_LL); each step lists
+                               // its receive moves last (Step::wait_mask = their number)
+    int32_t pad7;
 };
 
 }  // namespace mpxa

@@ -112,6 +112,7 @@ SIGNATURES = {
     "mpxa_parrived_wait": ([_P, _I, _I, _P], _I),
     "mpxa_psend_device": ([_P, _P, _Z], _I),
     "mpxa_plan_build_neighbor": ([_I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.POINTER(_P)], _I),
+    "mpxa_plan_eager": ([_P, _Z, ctypes.POINTER(_P)], _I),
     "mpxa_plan_info": ([_P, ctypes.POINTER(PlanInfo)], _I),
     "mpxa_plan_steps": ([_P, _I, _P, ctypes.POINTER(_I)], _I),
     "mpxa_plan_moves": ([_P, _I, _P, ctypes.POINTER(_I)], _I),
@@ -548,6 +549,20 @@ class Plan:
         _ck(_lib().mpxa_plan_info(h, ctypes.byref(info)), "plan_info")
         self.info = {n: int(getattr(info, n)) for n, _ in PlanInfo._fields_}
         return self
+
+    def eager(self, unit: int) -> "Plan":
+        """The eager (LL) form of this multi-GPU plan for `unit` bytes per unit
+        (mpxa_plan_eager): raises MpxaError(ERR_ALGO) when ineligible."""
+        h = ctypes.c_void_p()
+        _ck(_lib().mpxa_plan_eager(self.h, unit, ctypes.byref(h)), "plan_eager")
+        q = Plan.__new__(Plan)
+        q.h = h
+        q.p, q.R, q.G = self.p, self.R, self.G
+        q._keep = []
+        info = PlanInfo()
+        _ck(_lib().mpxa_plan_info(h, ctypes.byref(info)), "plan_info")
+        q.info = {n: int(getattr(info, n)) for n, _ in PlanInfo._fields_}
+        return q
 
     def steps(self, gpu: int):
         n = ctypes.c_int(0)

@@ -83,3 +83,79 @@ def simulate(plan, send, recv, unit, work_units=None):
             bufs[dk][dr, do:do + dn] = val
             written.setdefault((dk, dr), {})[do] = dn
     return recv
+
+
+LL = 3            # eager staging (mpxa_plan_eager)
+LL_WORDS = 8192   # kLLWords (mpxa_internal.h): staging words per (parity, source GPU)
+
+
+def simulate_eager(plan, send, recv, unit, work_units=None):
+    """Execute an eager (LL) plan (Plan.eager) with the kernel's semantics: per step, every
+    GPU first runs its local moves and SEND moves (payload -> 4-byte words of the (src, dst)
+    stream), then its RECEIVE moves (words -> destination).  Checks: receives are the last
+    moves of each step and their number is the step's wait_mask; a GPU reads only its own
+    sources and writes only its own ranks; every staging word is written once per launch and
+    read only after it was written (same or earlier step); streams fit LL_WORDS; every
+    ordered GPU pair exchanges at least one word (the parity invariant).  Returns recv."""
+    p, R, G = plan.p, plan.R, plan.G
+    wu = plan.info["work_units"] if work_units is None else work_units
+    work = np.zeros((p, max(1, wu * unit)), dtype=np.uint8)
+    recv = recv.copy()
+    bufs = {SEND: send, RECV: recv, WORK: work}
+    staging = {}      # (src gpu, dst gpu) -> bytearray of payload (4 bytes per word)
+    wrote = {}        # (src gpu, dst gpu) -> set of word indexes written
+    steps = [plan.steps(g) for g in range(G)]
+    moves = [plan.moves(g) for g in range(G)]
+    nsteps = len(steps[0])
+
+    def words(m):
+        return max(1, (m.len * unit + 3) // 4)
+
+    def own_ranks(g):
+        return range(g * R, (g + 1) * R)
+
+    for s in range(nsteps):
+        phase_b = []
+        for g in range(G):
+            st = steps[g][s]
+            mv = moves[g][st.move_begin:st.move_end]
+            nrecv = st.wait_mask
+            assert st.signal_mask == 0
+            assert all(m.src_kind == LL for m in mv[len(mv) - nrecv:]), "receives last"
+            assert not any(m.src_kind == LL for m in mv[:len(mv) - nrecv])
+            for m in mv[:len(mv) - nrecv]:
+                assert m.src_rank // R == g, "a GPU reads only its own ranks"
+                data = bufs[m.src_kind][m.src_rank, m.src_off * unit:(m.src_off + m.len) * unit].copy()
+                if m.dst_kind == LL:
+                    d = m.dst_rank
+                    assert d != g and m.fanout == 0
+                    buf = staging.setdefault((g, d), bytearray(4 * LL_WORDS))
+                    ws = wrote.setdefault((g, d), set())
+                    for w in range(m.dst_off, m.dst_off + words(m)):
+                        assert w < LL_WORDS and w not in ws, "staging word written twice"
+                        ws.add(w)
+                    buf[4 * m.dst_off:4 * m.dst_off + len(data)] = data.tobytes()
+                else:
+                    targets = own_ranks(g) if m.fanout == 2 else [m.dst_rank]
+                    assert m.fanout in (0, 2)
+                    for r in targets:
+                        assert r // R == g, "a local move writes only this GPU's ranks"
+                        bufs[m.dst_kind][r, m.dst_off * unit:(m.dst_off + m.len) * unit] = data
+            phase_b.append((g, mv[len(mv) - nrecv:]))
+        for g, mv in phase_b:
+            for m in mv:
+                src = m.src_rank
+                ws = wrote.get((src, g), set())
+                for w in range(m.src_off, m.src_off + words(m)):
+                    assert w in ws, "word received before it was sent"
+                n = m.len * unit
+                data = np.frombuffer(bytes(staging[(src, g)][4 * m.src_off:4 * m.src_off + n]), np.uint8)
+                targets = own_ranks(g) if m.fanout == 2 else [m.dst_rank]
+                for r in targets:
+                    assert r // R == g
+                    bufs[m.dst_kind][r, m.dst_off * unit:m.dst_off * unit + n] = data
+    for a in range(G):
+        for b in range(G):
+            if a != b:
+                assert wrote.get((a, b)), f"GPU pair {a}->{b} exchanges no word"
+    return recv

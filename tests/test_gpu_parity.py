@@ -583,3 +583,53 @@ def test_small_variable_piece_mode(p, G):
     del g
     req.free()
     assert c.check() == 0
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_eager_ll_mode_interleaved(G):
+    """Eager (LL) launches -- payload words carry the launch's flag in the receiver's staging,
+    two parities alternating per eager launch -- interleaved with CTS-mode launches (large
+    blocks) and with pairs that exchange nothing (flag-only words): every result exact, many
+    launches in a row so both parities are reused."""
+    p = 8
+    c = comm(p, G, 2)
+    rng = np.random.default_rng(G)
+    for it in range(12):
+        b = int(rng.choice([16, 100, 4096 + 4, 300_000]))     # 300 KB: CTS mode, not eager
+        send = synth.alltoall_sendbuf(it * 7 + G, p, b)
+        algo = ("pairwise", "bruck", "hier")[it % 3]
+        got = run_alltoall(c, send, algo)
+        assert np.array_equal(got, oracle.alltoall_definition(send)), (it, b, algo)
+        ag = rng.integers(0, 256, size=(p, 24 + it), dtype=np.uint8)
+        d_r = torch.full((p, p * ag.shape[1]), 0x5A, dtype=torch.uint8, device=DEV)
+        c.allgather(dev(ag), d_r, algo=("pairwise", "bruck", "ring")[it % 3])
+        assert np.array_equal(host(d_r), oracle.allgather_definition(ag)), it
+    # sparse alltoallv: most GPU pairs exchange nothing (flag-only words), byte-granular
+    counts = np.zeros((p, p), np.int64)
+    counts[0, 5] = 37
+    counts[3, 3] = 11
+    counts[6, 1] = 4
+    sc, rc = counts, counts.T.copy()
+    sd = np.zeros_like(sc); sd[:, 1:] = np.cumsum(sc, 1)[:, :-1]
+    rd = np.zeros_like(rc); rd[:, 1:] = np.cumsum(rc, 1)[:, :-1]
+    S, R = int((sd + sc).max()) + 8, int((rd + rc).max()) + 8
+    send = rng.integers(0, 256, size=(p, S), dtype=np.uint8)
+    recv0 = np.full((p, R), 0xA5, dtype=np.uint8)
+    want = oracle.alltoallv_definition(send, sc, sd, rc, rd, 1, recv0)
+    for rep in range(3):
+        d_recv = dev(recv0)
+        c.alltoallv(dev(send), sc, sd, d_recv, rc, rd, algo="pairwise")
+        assert np.array_equal(host(d_recv), want), rep
+    assert c.check() == 0
+
+
+def test_eager_ll_matches_cts_mode(monkeypatch):
+    """MPXA_NO_LL=1 (every small multi-GPU launch through CTS + flags) gives the same bytes."""
+    p, G, b = 8, 4, 260
+    send = synth.alltoall_sendbuf(5, p, b)
+    want = oracle.alltoall_definition(send)
+    monkeypatch.setenv("MPXA_NO_LL", "1")
+    c = Comm(ranks_per_proc=p, device=0, emulate_gpus=G, group_size=2, timeout_s=20.0)
+    for algo in ("pairwise", "bruck", "hier"):
+        assert np.array_equal(run_alltoall(c, send, algo), want), algo
+    c.finalize()
