@@ -210,6 +210,8 @@ struct mpxa_comm_s {
     bool swork = true;                     // small kernel, one CTA on one GPU: WORK in shared memory
     int small_nt = 64;                     // small kernel block size for launches with few pieces
     bool ll = true;                        // eager (LL) mode for small multi-GPU launches
+    int64_t ll_max = 4 * kLLWords;         // eager: payload bytes per GPU pair, single-step launches
+    int64_t ll_max_ms = 16384;             // ... multi-step launches
     int force_ns = 0, force_nf = 0;           // MPXA_NS / MPXA_NF overrides (tuning)
     int force_big = -1;                       // MPXA_TMA_BIG=0/1 override (tuning)
     bool force_exec = false;                  // MPXA_NO_SMALL=1: never use the small-message kernel
@@ -522,7 +524,7 @@ static int upload_companion(Program &&Q, std::shared_ptr<DevProg> &out) {
 // (Step::wait_mask = their number): a CTA issues all its sends before it polls.
 // Returns false when a pair needs more than kLLWords words or a GPU more moves than the
 // small kernel caches.
-static bool build_ll(const Program &P, uint64_t unit, int R, Program &Q) {
+static bool build_ll(const Program &P, uint64_t unit, int R, Program &Q, int64_t max_words = kLLWords) {
     const int G = P.G, ns = P.nsteps();
     Q = Program();
     Q.p = P.p; Q.R = P.R; Q.G = G;
@@ -607,7 +609,7 @@ static bool build_ll(const Program &P, uint64_t unit, int R, Program &Q) {
         }
     }
     for (int64_t w : wc)
-        if (w > kLLWords) return false;
+        if (w > std::min<int64_t>(max_words, kLLWords)) return false;
     for (int g = 0; g < G; g++)
         if (Q.moves[g].size() > (size_t)kSmallMovesSmem) return false;
     return true;
@@ -624,7 +626,11 @@ static const DevProg *ll_program(mpxa_comm_t c, const DevProg &dp, uint64_t unit
     dp.ll_unit = unit;
     dp.ll_ok = -1;
     Program Q;
-    if (!build_ll(dp.host, unit, c->Rg, Q)) return nullptr;
+    // measured (4 emulated GPUs, p = 4 / 8): eager wins up to the full 32 KiB staging per GPU
+    // pair for single-step launches; multi-step ones pay its 2x bytes and word stores in
+    // every step and break even at 16-32 KiB per pair
+    const int64_t max_words = (dp.nsteps > 1 ? c->ll_max_ms : c->ll_max) / 4;
+    if (!build_ll(dp.host, unit, c->Rg, Q, max_words)) return nullptr;
     if (upload_companion(std::move(Q), dp.ll) != MPXA_SUCCESS) return nullptr;
     dp.ll_ok = 1;
     return dp.ll.get();
@@ -1322,6 +1328,8 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     if (const char *e = getenv("MPXA_SWORK")) c->swork = atoi(e) != 0;
     if (const char *e = getenv("MPXA_SMALL_NT")) c->small_nt = std::max(32, std::min(512, atoi(e)));
     if (const char *e = getenv("MPXA_NO_LL")) c->ll = atoi(e) == 0;
+    if (const char *e = getenv("MPXA_LL_MAX")) c->ll_max = atoll(e);
+    if (const char *e = getenv("MPXA_LL_MAX_MS")) c->ll_max_ms = atoll(e);
     CK(cudaHostAlloc((void **)&c->err_host, sizeof(int32_t), cudaHostAllocMapped));
     *c->err_host = 0;
     CK(cudaHostGetDevicePointer((void **)&c->err_dev, c->err_host, 0));
