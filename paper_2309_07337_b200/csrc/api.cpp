@@ -552,6 +552,8 @@ static bool build_ll(const Program &P, uint64_t unit, int R, Program &Q, int64_t
                 for (int d = 0; d < G; d++) {
                     if (d == g) continue;
                     if (!m.fanout && (int)m.dst_rank / R != d) continue;
+                    int64_t &w0 = wc[(size_t)g * G + d];
+                    w0 += w0 & 1;   // even word offsets: 16-byte aligned pairs of words
                     Move snd = m, rcv = m;
                     snd.fanout = 0;
                     snd.dst_kind = BK_LL;

@@ -1327,6 +1327,18 @@ __device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t *p) {
 __device__ __forceinline__ void st_relaxed_sys(uint64_t *p, uint64_t v) {
     asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// two eager words {data0, flag, data1, flag} in one 16-byte store; each 8-byte half is written
+// atomically, so the receiver checks both flags (the 16 bytes as a whole are not atomic)
+__device__ __forceinline__ void st_ll_pair(uint64_t *p, uint32_t d0, uint32_t d1, uint32_t flag) {
+    asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(d0), "r"(flag), "r"(d1), "r"(flag)
+                 : "memory");
+}
+__device__ __forceinline__ uint4 ld_ll_pair(const uint64_t *p) {
+    uint4 v;
+    asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+    return v;
+}
 
 // Eager (LL) mode, one phase of a step (P.small_ll).  RECV = false: local moves
 // and sends -- a send piece stores its (up to) four payload words, each with the launch's flag
@@ -1363,13 +1375,14 @@ __device__ __forceinline__ void small_items_ll(const ExecParams &P, SmallShared 
                 const RMove &m = mv[it >> lg];
                 const uint32_t o = (it & mask) * 16;
                 const uint32_t nw = m.n > o ? (min(16u, m.n - o) + 3) / 4 : 1;
-                const uint64_t *w = reinterpret_cast<const uint64_t *>(m.src + par) + o / 4;
+                const uint64_t *w = reinterpret_cast<const uint64_t *>(m.src + par) + o / 4;   // 16-B aligned
+                const uint32_t f32 = (uint32_t)(flag >> 32);
                 uint32_t d[4] = {0, 0, 0, 0};
                 uint64_t t0 = 0;
-                for (uint32_t j = 0; j < nw; j++) {
-                    uint64_t v = ld_relaxed_sys(w + j);
+                for (uint32_t j = 0; j < nw; j += 2) {   // word pairs: one 16-byte load each
+                    uint4 v = ld_ll_pair(w + j);
                     int spins = 0;
-                    while ((v & 0xffffffff00000000ull) != flag) {
+                    while (v.y != f32 || (j + 1 < nw && v.w != f32)) {
                         if (++spins > 64) {
                             __nanosleep(64);
                             if (!t0) t0 = globaltimer();
@@ -1379,9 +1392,10 @@ __device__ __forceinline__ void small_items_ll(const ExecParams &P, SmallShared 
                                 return;
                             }
                         }
-                        v = ld_relaxed_sys(w + j);
+                        v = ld_ll_pair(w + j);
                     }
-                    d[j] = (uint32_t)v;
+                    d[j] = v.x;
+                    if (j + 1 < 4) d[j + 1] = v.z;
                 }
                 lv[k] = make_uint4(d[0], d[1], d[2], d[3]);
             }
@@ -1395,10 +1409,13 @@ __device__ __forceinline__ void small_items_ll(const ExecParams &P, SmallShared 
             const uint32_t len = m.n > o ? min(16u, m.n - o) : 0u;
             if (!RECV && m.ll == 1) {   // send: payload words + flag into the peer's staging
                 const uint4 val = len ? R.value(k, m.src + o) : make_uint4(0, 0, 0, 0);
-                uint64_t *w = reinterpret_cast<uint64_t *>(m.dst + par) + o / 4;
+                uint64_t *w = reinterpret_cast<uint64_t *>(m.dst + par) + o / 4;   // 16-B aligned
                 const uint32_t d[4] = {val.x, val.y, val.z, val.w};
-                const uint32_t nw = len ? (len + 3) / 4 : 1;
-                for (uint32_t j = 0; j < nw; j++) st_relaxed_sys(w + j, flag | d[j]);
+                const uint32_t nw = len ? (len + 3) / 4 : 1, f32 = (uint32_t)(flag >> 32);
+                for (uint32_t j = 0; j < nw; j += 2) {
+                    if (j + 1 < nw) st_ll_pair(w + j, d[j], d[j + 1], f32);
+                    else st_relaxed_sys(w + j, flag | d[j]);
+                }
                 continue;
             }
             if (!len) continue;
