@@ -130,6 +130,8 @@ def _lib():
                               "(build()) -- there is no fallback implementation")
         lib = ctypes.CDLL(LIB_PATH)
         for name, (args, res) in SIGNATURES.items():
+            if os.environ.get("MPXA_LIB") and not hasattr(lib, name):
+                continue   # an older tuning build (MPXA_LIB) may predate a symbol
             f = getattr(lib, name)
             f.argtypes = args
             f.restype = res
