@@ -64,7 +64,7 @@ int mpxa_plan_build_neighbor(int p, int R, int G, int g, int locality, const int
  * offset on GPU d.  Fan-out moves keep fanout = 2 (this GPU's ranks only) plus one stream per
  * peer GPU.  In each step the receive moves come last; wait_mask = their number.  Pairs
  * without data exchange one flag word (len 0).  MPXA_ERR_ALGO when G < 2 or a GPU pair needs
- * more than 8192 words.  Released with mpxa_plan_free. */
+ * more than 32768 words.  Released with mpxa_plan_free. */
 int mpxa_plan_eager(const void *plan, size_t unit, void **eager);
 int mpxa_plan_info(const void *plan, mpxa_plan_info_t *info);
 /* copies GPU `gpu`'s steps / moves; *n in: capacity, out: count */

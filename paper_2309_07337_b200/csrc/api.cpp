@@ -628,9 +628,11 @@ static const DevProg *ll_program(mpxa_comm_t c, const DevProg &dp, uint64_t unit
     dp.ll_unit = unit;
     dp.ll_ok = -1;
     Program Q;
-    // measured (4 emulated GPUs, p = 4 / 8): eager wins up to the full 32 KiB staging per GPU
-    // pair for single-step launches; multi-step ones pay its 2x bytes and word stores in
-    // every step and break even at 16-32 KiB per pair
+    // measured (4 emulated GPUs, p = 4 / 8): eager wins up to the full 128 KiB staging per
+    // GPU pair for single-step launches (pairwise alltoall 64 KiB pairs 16.0 -> 10.2 us; the
+    // direct protocol's CTS + two system-scope releases cost more than eager's 2x bytes);
+    // multi-step ones pay the 2x bytes and word stores in every step and break even at
+    // 16-32 KiB per pair
     const int64_t max_words = (dp.nsteps > 1 ? c->ll_max_ms : c->ll_max) / 4;
     if (!build_ll(dp.host, unit, c->Rg, Q, max_words)) return nullptr;
     if (upload_companion(std::move(Q), dp.ll) != MPXA_SUCCESS) return nullptr;

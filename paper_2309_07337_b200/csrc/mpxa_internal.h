@@ -94,7 +94,7 @@ struct CtsSlot {
 };
 
 // Per-GPU symmetric region (device memory, IPC-exported in multi-process mode).
-constexpr int kLLWords = 8192;      // eager staging words per (parity, source GPU): 32 KiB payload
+constexpr int kLLWords = 32768;     // eager staging words per (parity, source GPU): 128 KiB payload
 struct SymRegion {
     CtsSlot cts[kMaxGpus];                    // cts[d]: receiver d cleared this GPU to send
     uint64_t flags[kMaxGpus][kMaxCtas];       // flags[s][c]: src GPU s, CTA c, (epoch<<8)|(step+1)

@@ -86,7 +86,7 @@ def simulate(plan, send, recv, unit, work_units=None):
 
 
 LL = 3            # eager staging (mpxa_plan_eager)
-LL_WORDS = 8192   # kLLWords (mpxa_internal.h): staging words per (parity, source GPU)
+LL_WORDS = 32768  # kLLWords (mpxa_internal.h): staging words per (parity, source GPU)
 
 
 def simulate_eager(plan, send, recv, unit, work_units=None):
