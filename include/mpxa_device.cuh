@@ -108,10 +108,18 @@ __device__ __forceinline__ void mpxa_dev_pready_part(const mpxa_psend_dev_t *ch,
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence_system();   /* this CTA's stores, before its completion is counted */
-        if (atomicAdd(&ch->done[i], 1u) + 1u == nct) {
-            ch->done[i] = 0;      /* every CTA of partition i has counted: reset for next cycle */
-            __threadfence_system();
+        /* Count this CTA's completion with an acq_rel RMW at system scope: the release half
+         * publishes the CTA's stores (ordered before it by the barrier), the acquire half lets
+         * the last CTA's release below cover every other CTA's stores too (cumulativity) --
+         * no separate fence.sc.sys, which costs microseconds. */
+        unsigned int prev;
+        if (nct == 1u) {
+            prev = 0u;
+        } else {
+            asm volatile("atom.acq_rel.sys.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&ch->done[i]) : "memory");
+        }
+        if (prev + 1u == nct) {
+            if (nct > 1u) ch->done[i] = 0;   /* every CTA of partition i has counted: reset */
             asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&ch->arr[i]), "l"(s_cycle) : "memory");
         }
     }
