@@ -986,10 +986,22 @@ int check_uniform(mpxa_comm_t c, const void *send, size_t count, size_t w, void 
 // counts / displacements may live in device memory (SURVEY.md §8(b) ownership): such arrays
 // are copied to the host first (a synchronous copy -- the persistent forms pay it once)
 int host_view(const int64_t *&a, size_t n, std::vector<int64_t> &store) {
+    // recently seen HOST arrays skip the driver query (~1 us each): a host address never
+    // becomes a device address (the driver's device VA range is reserved apart from the heap)
+    static thread_local const void *known_host[8] = {};
+    static thread_local int known_next = 0;
+    for (const void *k : known_host)
+        if (k == (const void *)a) return MPXA_SUCCESS;
     cudaPointerAttributes at{};
     if (cudaPointerGetAttributes(&at, a) != cudaSuccess) {
         cudaGetLastError();   // unregistered host memory on older drivers: treat as host
+        known_host[known_next] = a;
+        known_next = (known_next + 1) & 7;
         return MPXA_SUCCESS;
+    }
+    if (at.type != cudaMemoryTypeDevice) {
+        known_host[known_next] = a;
+        known_next = (known_next + 1) & 7;
     }
     if (at.type == cudaMemoryTypeDevice) {
         store.resize(n);
@@ -1049,9 +1061,15 @@ int gather_v(mpxa_comm_t c, const int64_t *sc, const int64_t *sd, const int64_t 
 
 constexpr size_t kVCacheMax = 32;
 
-uint64_t fnv(uint64_t h, const void *p, size_t n) {
+uint64_t fnv(uint64_t h, const void *p, size_t n) {   // FNV-1a over 8-byte words
     const unsigned char *b = (const unsigned char *)p;
-    for (size_t i = 0; i < n; i++) h = (h ^ b[i]) * 1099511628211ull;
+    size_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+        uint64_t w;
+        memcpy(&w, b + i, 8);
+        h = (h ^ w) * 1099511628211ull;
+    }
+    for (; i < n; i++) h = (h ^ b[i]) * 1099511628211ull;
     return h;
 }
 
@@ -1077,7 +1095,10 @@ int vprogram(mpxa_comm_t c, int algo, const std::vector<int64_t> &C, const std::
             for (size_t i = 0; i < kv.second.size(); i++)
                 if (kv.second[i].used < best) { best = kv.second[i].used; bh = kv.first; bi = i; }
         auto &vb = c->vcache[bh];
-        if (vb[bi].last) { CK(cudaEventSynchronize(vb[bi].last)); cudaEventDestroy(vb[bi].last); }
+        // the evicted program may still be in flight on any stream (launches record no event:
+        // eviction is rare, a device-wide sync there is cheaper than an event per call)
+        CK(cudaDeviceSynchronize());
+        if (vb[bi].last) cudaEventDestroy(vb[bi].last);
         if (vb[bi].prog) cudaFree(vb[bi].prog->dmem);
         vb.erase(vb.begin() + (long)bi);
         if (vb.empty()) c->vcache.erase(bh);
@@ -1116,10 +1137,7 @@ int alltoallv_impl(const void *sendbuf, const int64_t *sc, const int64_t *sd, si
         mpxa_comm_s::VEntry *e = nullptr;
         r = vprogram(c, algo, C, SD, RD, e);
         if (r) return r;
-        r = run_program(c, *e->prog, (const char *)sendbuf, (char *)recvbuf, w, send_bpr, recv_bpr, stream);
-        if (r) return r;
-        CK(cudaEventRecord(e->last, stream));
-        return MPXA_SUCCESS;
+        return run_program(c, *e->prog, (const char *)sendbuf, (char *)recvbuf, w, send_bpr, recv_bpr, stream);
     }
     Program P;
     if (!build_alltoallv(P, algo, c->p, c->Rg, c->G, c->g, C.data(), SD.data(), RD.data())) return MPXA_ERR_ALGO;

@@ -8,6 +8,7 @@ PyTorch fallback: if libmpxa.so is missing the import fails loudly.
 from __future__ import annotations
 
 import ctypes
+import weakref
 import os
 from typing import Optional, Sequence
 
@@ -169,7 +170,19 @@ def _ptr(t) -> Optional[int]:
     return t.data_ptr()
 
 
+_PTRS = {}   # id(ndarray) -> (weakref, address): repeated calls with the same arrays
+
+
 def _host_i64(a):
+    if type(a) is np.ndarray and a.dtype == np.int64 and a.flags.c_contiguous:   # fast path
+        e = _PTRS.get(id(a))
+        if e is not None and e[0]() is a:
+            return a, e[1]
+        addr = a.__array_interface__["data"][0]
+        if len(_PTRS) > 256:
+            _PTRS.clear()
+        _PTRS[id(a)] = (weakref.ref(a), addr)
+        return a, addr
     a = np.ascontiguousarray(np.asarray(a, dtype=np.int64))
     return a, a.ctypes.data_as(ctypes.c_void_p)
 
