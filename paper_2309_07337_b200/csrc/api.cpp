@@ -64,8 +64,11 @@ constexpr uint64_t kMovesPerCta = 1;       // moves per CTA (latency-bound regim
 constexpr uint64_t kMinSlice = 2048;       // smallest slice worth a CTA when filling the GPU (= TMA min)
 constexpr uint64_t kBigPerCta = 1u << 20;  // bytes per CTA per step above which the big TMA config wins
 constexpr uint64_t kSmallItemsPerCta = 2048;   // small kernel: 16-B pieces per CTA per step (one batch)
-constexpr uint64_t kSmallOneStepMove = 1u << 20;   // single-step programs: longest move ...
-constexpr uint64_t kSmallOneStepVol = 16u << 20;   // ... and source bytes per GPU for the small kernel
+constexpr uint64_t kSmallOneStepMove = 2u << 20;   // single-step programs: longest move ...
+constexpr uint64_t kSmallOneStepVol = 32u << 20;   // ... and source bytes per GPU for the small kernel
+                                                    // (re-measured after the small-kernel work:
+                                                    // a2a p=8 512 KiB 13.5 -> 10.5 us, allgather
+                                                    // p=4 2 MiB 11.4 -> 7.2 us; 64 MiB loses)
 constexpr uint64_t kSmallSyncMove = 256u << 10;    // multi-step small launches on several CTAs:
 constexpr uint64_t kSmallSyncVol = 8u << 20;       //   longest move, busiest step
 constexpr uint64_t kSmallOwnVol = 2u << 20;        // owned-flow mode: busiest step, and bytes per CTA
@@ -772,7 +775,7 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
     const uint64_t items = var ? exact : slots;
     const bool one_step = dp.nsteps == 1;
     // Small-message kernel: multi-step programs with short moves and a step small enough for
-    // one CTA; single-step programs (any number of CTAs) up to 1 MiB moves and 16 MiB of
+    // one CTA; single-step programs (any number of CTAs) up to 2 MiB moves and 32 MiB of
     // source data per GPU -- measured on one B200: its LSU pieces beat the TMA executor's
     // fixed costs there (alltoall 64 KiB blocks 5.3 -> 3.8 us, allgather 1 MiB 17.9 -> 13.8 us,
     // alltoallv cfg4 64 KiB mean 9.2 -> 5.2 us); beyond, the executor streams better.
