@@ -213,6 +213,7 @@ struct mpxa_comm_s {
     bool swork = true;                     // small kernel, one CTA on one GPU: WORK in shared memory
     int small_nt = 64;                     // small kernel block size for launches with few pieces
     bool ll = true;                        // eager (LL) mode for small multi-GPU launches
+    uint32_t last_path = 0;                // bits of the last launch's path (mpxa__last_launch)
     int64_t ll_max = 4 * kLLWords;         // eager: payload bytes per GPU pair, single-step launches
     int64_t ll_max_ms = 16384;             // ... multi-step launches
     int force_ns = 0, force_nf = 0;           // MPXA_NS / MPXA_NF overrides (tuning)
@@ -924,6 +925,10 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
         return MPXA_ERR_CUDA;
     }
     c->launches++;
+    // execution path of this launch (tests assert the intended path ran: mpxa__last_launch)
+    c->last_path = (small ? 1u : 0u) | (E.small_ll ? 2u : 0u) | (E.small_var ? 4u : 0u) |
+                   (E.dyn_units ? 8u : 0u) | (E.dyn_sync ? 16u : 0u) | (E.small_own ? 32u : 0u) |
+                   (E.small_swork ? 64u : 0u);
     return MPXA_SUCCESS;
 }
 
@@ -2121,6 +2126,15 @@ int mpxa_plan_moves(const void *plan, int gpu, mpxa_plan_move *out, int *n) {
         memcpy(out, v.data(), sizeof(Move) * v.size());
     }
     *n = (int)v.size();
+    return MPXA_SUCCESS;
+}
+
+// undocumented test hook: the execution path of the comm's last collective launch, as bits
+// 1 small kernel, 2 eager (LL), 4 variable pieces, 8 dynamic work queues, 16 row-barrier
+// sync, 32 owned flows, 64 WORK in shared memory
+int mpxa__last_launch(mpxa_comm_t c, uint32_t *bits) {
+    if (!c || !bits) return MPXA_ERR_ARG;
+    *bits = c->last_path;
     return MPXA_SUCCESS;
 }
 

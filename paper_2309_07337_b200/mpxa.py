@@ -275,6 +275,18 @@ class Comm:
         _ck(_lib().mpxa_launch_count(self.handle, ctypes.byref(n)), "launch_count")
         return n.value
 
+    # bits of mpxa__last_launch (test hook, not part of the C ABI headers)
+    PATH_BITS = {"small": 1, "eager": 2, "var": 4, "dyn": 8, "sync": 16, "own": 32, "swork": 64}
+
+    def last_launch_path(self) -> set:
+        """Execution path of this comm's last collective launch (test hook)."""
+        f = _lib().mpxa__last_launch
+        f.argtypes = [_P, ctypes.POINTER(ctypes.c_uint32)]
+        f.restype = _I
+        b = ctypes.c_uint32()
+        _ck(f(self.handle, ctypes.byref(b)), "last_launch")
+        return {k for k, v in self.PATH_BITS.items() if b.value & v}
+
     def check(self) -> int:
         return _lib().mpxa_comm_check(self.handle)
 

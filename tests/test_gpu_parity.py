@@ -633,3 +633,41 @@ def test_eager_ll_matches_cts_mode(monkeypatch):
     for algo in ("pairwise", "bruck", "hier"):
         assert np.array_equal(run_alltoall(c, send, algo), want), algo
     c.finalize()
+
+
+def test_execution_paths_are_the_intended_ones(monkeypatch):
+    """The launches these parity tests rely on take the paths they are meant to exercise
+    (mpxa__last_launch): eager on emulated GPUs for small messages, direct otherwise; the
+    variable-piece mode for mixed move lengths; dynamic queues for a large allgather; the
+    small kernel's owned-flow / sync modes for multi-step mid sizes; shared-memory WORK for a
+    one-CTA single-GPU Bruck."""
+    p = 8
+    c1 = comm(p, 0, 2)
+    send = synth.alltoall_sendbuf(1, p, 16)
+    run_alltoall(c1, send, "bruck")
+    assert {"small", "swork"} <= c1.last_launch_path() and "eager" not in c1.last_launch_path()
+    c4 = comm(p, 4, 2)
+    run_alltoall(c4, send, "pairwise")
+    assert {"small", "eager"} <= c4.last_launch_path()
+    big = synth.alltoall_sendbuf(2, p, 300_000)
+    run_alltoall(c4, big, "pairwise")
+    assert "eager" not in c4.last_launch_path()
+    # mixed lengths: variable pieces
+    counts = np.ones((p, p), np.int64)
+    counts[0, 1] = 60 << 10
+    counts[2, 3] = 50 << 10
+    sc, rc = counts, counts.T.copy()
+    sd = np.zeros_like(sc); sd[:, 1:] = np.cumsum(sc, 1)[:, :-1]
+    rd = np.zeros_like(rc); rd[:, 1:] = np.cumsum(rc, 1)[:, :-1]
+    S, R = int((sd + sc).max()), int((rd + rc).max())
+    sendv = np.random.default_rng(0).integers(0, 256, size=(p, S), dtype=np.uint8)
+    d_r = torch.zeros((p, R), dtype=torch.uint8, device=DEV)
+    c1.alltoallv(dev(sendv), sc, sd, d_r, rc, rd, algo="pairwise")
+    assert {"small", "var"} <= c1.last_launch_path()
+    assert np.array_equal(host(d_r), oracle.alltoallv_definition(sendv, sc, sd, rc, rd, 1, np.zeros((p, R), np.uint8)))
+    # large allgather: dynamic work queues in the executor
+    ag = torch.randint(0, 256, (p, 8 << 20), dtype=torch.uint8, device=DEV)
+    out = torch.empty((p, p * (8 << 20)), dtype=torch.uint8, device=DEV)
+    c1.allgather(ag, out, algo="pairwise")
+    assert c1.last_launch_path() == {"dyn"}
+    del ag, out
