@@ -623,15 +623,25 @@ def test_eager_ll_mode_interleaved(G):
     assert c.check() == 0
 
 
-def test_eager_ll_matches_cts_mode(monkeypatch):
-    """MPXA_NO_LL=1 (every small multi-GPU launch through CTS + flags) gives the same bytes."""
-    p, G, b = 8, 4, 260
-    send = synth.alltoall_sendbuf(5, p, b)
-    want = oracle.alltoall_definition(send)
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_direct_protocol_small_sizes(G, monkeypatch):
+    """MPXA_NO_LL=1: small multi-GPU launches through the direct protocol (CTS + per-step
+    flags, small kernel) -- the path eager mode replaced for these sizes stays exact."""
+    p = 8
     monkeypatch.setenv("MPXA_NO_LL", "1")
     c = Comm(ranks_per_proc=p, device=0, emulate_gpus=G, group_size=2, timeout_s=20.0)
-    for algo in ("pairwise", "bruck", "hier"):
-        assert np.array_equal(run_alltoall(c, send, algo), want), algo
+    for b in (1, 16, 260, 4096 + 12):
+        send = synth.alltoall_sendbuf(b + G, p, b)
+        want = oracle.alltoall_definition(send)
+        for algo in ("pairwise", "bruck", "hier"):
+            assert np.array_equal(run_alltoall(c, send, algo), want), (b, algo)
+            assert "eager" not in c.last_launch_path()
+        ag = np.random.default_rng(b).integers(0, 256, size=(p, b), dtype=np.uint8)
+        for algo in ("pairwise", "bruck", "ring"):
+            d_r = torch.full((p, p * b), 0x5A, dtype=torch.uint8, device=DEV)
+            c.allgather(dev(ag), d_r, algo=algo)
+            assert np.array_equal(host(d_r), oracle.allgather_definition(ag)), (b, algo)
+    assert c.check() == 0
     c.finalize()
 
 
