@@ -146,30 +146,37 @@ bool build_alltoall(Program &P, int algo, int p, int R, int G, int g, int stop_s
     if (algo == A_BRUCK) {
         // A4-A6: T_r[i] = send_r[(r+i) mod p]; round k: the blocks with bit k of i set go, in
         // increasing i, to (r+2^k) mod p, which keeps them as its new T[i]; finally
-        // recv_r[j] = T_r[(r-j) mod p].  Zero-copy receive: round k lands in the receiver's
-        // round-k area S_k and T[i] is thereafter READ from there (loc[i]) instead of being
-        // unpacked over the old T[i].  Every workspace byte is written once per launch, so no
-        // CTA ever overwrites data another CTA has still to read.
+        // recv_r[j] = T_r[(r-j) mod p].  The rotation is virtual: a block that has not moved
+        // yet is READ from send_r[(r+i) mod p] where round k (or the inverse rotation) needs
+        // it -- no HBM pass for A4.  Zero-copy receive: round k lands in the receiver's round-k
+        // area S_k and T[i] is thereafter read from there (loc[i]) instead of being unpacked
+        // over the old T[i].  Every workspace byte is written once per launch, so no CTA ever
+        // overwrites data another CTA has still to read.
         const int K = ceil_log2(p);
-        std::vector<int64_t> soff(K + 1, p);
+        std::vector<int64_t> soff(K + 1, 0);
         for (int k = 0; k < K; k++) {
             int64_t mk = 0;
             for (int i = 0; i < p; i++) mk += (i >> k) & 1;
             soff[k + 1] = soff[k] + mk;
         }
         P.work_units = soff[K];
-        std::vector<int64_t> loc(p);                         // current WORK offset of T[i]
-        for (int i = 0; i < p; i++) loc[i] = i;
+        std::vector<int64_t> loc(p, -1);                     // WORK offset of T[i]; -1: still in send
+        // T_r[i] read where it currently is (rank r's send buffer, rotated, or its WORK row)
+        auto read_T = [&](int r, int i, int dk, int dr, int64_t dof) {
+            if (loc[i] < 0) {
+                const int b = imod(r + i, p);
+                B.move(BK_SEND, r, b, dk, dr, dof, 1, (int64_t)r * p + b);
+            } else {
+                B.move(BK_WORK, r, loc[i], dk, dr, dof, 1);
+            }
+        };
         const int rounds = stop_stage < 0 ? K : std::min(stop_stage, K);
-        for (int r = 0; r < p; r++)                          // A4 local rotation
-            for (int i = 0; i < p; i++) B.move(BK_SEND, r, imod(r + i, p), BK_WORK, r, i, 1, (int64_t)r * p + imod(r + i, p));
-        B.end_step();
         for (int k = 0; k < rounds; k++) {                   // A5 bit-indexed rounds
             const int d = 1 << k;
             for (int r = 0; r < p; r++) {
                 int64_t pos = 0;
                 for (int i = 0; i < p; i++)
-                    if ((i >> k) & 1) B.move(BK_WORK, r, loc[i], BK_WORK, imod(r + d, p), soff[k] + pos++, 1);
+                    if ((i >> k) & 1) read_T(r, i, BK_WORK, imod(r + d, p), soff[k] + pos++);
             }
             B.end_step();
             int64_t pos = 0;
@@ -178,10 +185,10 @@ bool build_alltoall(Program &P, int algo, int p, int R, int G, int g, int stop_s
         }
         if (stop_stage < 0) {                                // A6 inverse rotation
             for (int r = 0; r < p; r++)
-                for (int j = 0; j < p; j++) B.move(BK_WORK, r, loc[imod(r - j, p)], BK_RECV, r, j, 1);
+                for (int j = 0; j < p; j++) read_T(r, imod(r - j, p), BK_RECV, r, j);
         } else {                                             // dump T for stage tests
             for (int r = 0; r < p; r++)
-                for (int i = 0; i < p; i++) B.move(BK_WORK, r, loc[i], BK_RECV, r, i, 1);
+                for (int i = 0; i < p; i++) read_T(r, i, BK_RECV, r, i);
         }
         B.end_step();
         return true;
@@ -256,25 +263,28 @@ bool build_allgather(Program &P, int algo, int p, int R, int G, int stop_stage, 
     }
     if (algo == A_BRUCK) {
         // T_r[0] = send_r; round k sends T_r[0..n_k) to (r-2^k) mod p,
-        // stored at T[2^k..2^k+n_k); recv_r[j] = T_r[(j-r) mod p].
+        // stored at T[2^k..2^k+n_k); recv_r[j] = T_r[(j-r) mod p].  T_r[0] is never copied:
+        // it is read from send_r wherever it is needed (WORK row 0 stays unused).
         const int K = ceil_log2(p);
         P.work_units = p;
+        auto read_T = [&](int r, int i, int dk, int dr, int64_t dof) {
+            if (i == 0) B.move(BK_SEND, r, 0, dk, dr, dof, 1, r);
+            else B.move(BK_WORK, r, i, dk, dr, dof, 1);
+        };
         const int rounds = stop_stage < 0 ? K : std::min(stop_stage, K);
-        for (int r = 0; r < p; r++) B.move(BK_SEND, r, 0, BK_WORK, r, 0, 1, r);
-        B.end_step();
         for (int k = 0; k < rounds; k++) {
             const int d = 1 << k, nk = std::min(d, p - d);
             for (int r = 0; r < p; r++)
-                for (int i = 0; i < nk; i++) B.move(BK_WORK, r, i, BK_WORK, imod(r - d, p), d + i, 1);
+                for (int i = 0; i < nk; i++) read_T(r, i, BK_WORK, imod(r - d, p), d + i);
             B.end_step();
         }
         if (stop_stage < 0) {
             for (int r = 0; r < p; r++)
-                for (int j = 0; j < p; j++) B.move(BK_WORK, r, imod(j - r, p), BK_RECV, r, j, 1);
+                for (int j = 0; j < p; j++) read_T(r, imod(j - r, p), BK_RECV, r, j);
         } else {
             int filled = std::min(1 << rounds, p);
             for (int r = 0; r < p; r++)
-                for (int i = 0; i < filled; i++) B.move(BK_WORK, r, i, BK_RECV, r, i, 1);
+                for (int i = 0; i < filled; i++) read_T(r, i, BK_RECV, r, i);
         }
         B.end_step();
         return true;
@@ -310,17 +320,20 @@ bool build_alltoallv(Program &P, int algo, int p, int R, int G, int g, const int
         // finally recv_r[rd_r[j]] = T_r[(r-j) mod p].  Areas are sized per rank.
         Builder B(P, p, R, G, p * p);
         const int K = ceil_log2(p);
-        std::vector<std::vector<int64_t>> loc(p, std::vector<int64_t>(p)), len(p, std::vector<int64_t>(p));
+        // loc[r][i] < 0: T_r[i] has not moved and is read from rank r's send buffer (the
+        // rotation is virtual, as for alltoall); else its offset in rank r's WORK row
+        std::vector<std::vector<int64_t>> loc(p, std::vector<int64_t>(p, -1)), len(p, std::vector<int64_t>(p));
         std::vector<int64_t> cur(p, 0);
-        for (int r = 0; r < p; r++)                          // A4 rotation into the rank's T area
-            for (int i = 0; i < p; i++) {
+        for (int r = 0; r < p; r++)
+            for (int i = 0; i < p; i++) len[r][i] = C(r, imod(r + i, p));
+        auto read_T = [&](int r, int i, int dk, int dr, int64_t dof) {
+            if (loc[r][i] < 0) {
                 const int j = imod(r + i, p);
-                loc[r][i] = cur[r];
-                len[r][i] = C(r, j);
-                B.move(BK_SEND, r, SD(r, j), BK_WORK, r, cur[r], C(r, j), (int64_t)r * p + j);
-                cur[r] += C(r, j);
+                B.move(BK_SEND, r, SD(r, j), dk, dr, dof, len[r][i], (int64_t)r * p + j);
+            } else {
+                B.move(BK_WORK, r, loc[r][i], dk, dr, dof, len[r][i]);
             }
-        B.end_step();
+        };
         for (int k = 0; k < K; k++) {                        // A5 rounds
             const int d = 1 << k;
             std::vector<std::vector<int64_t>> nloc = loc, nlen = len;
@@ -328,7 +341,7 @@ bool build_alltoallv(Program &P, int algo, int p, int R, int G, int g, const int
                 const int to = imod(r + d, p);
                 for (int i = 0; i < p; i++)
                     if ((i >> k) & 1) {
-                        B.move(BK_WORK, r, loc[r][i], BK_WORK, to, cur[to], len[r][i]);
+                        read_T(r, i, BK_WORK, to, cur[to]);
                         nloc[to][i] = cur[to];
                         nlen[to][i] = len[r][i];
                         cur[to] += len[r][i];
@@ -342,7 +355,7 @@ bool build_alltoallv(Program &P, int algo, int p, int R, int G, int g, const int
             for (int j = 0; j < p; j++) {
                 const int i = imod(r - j, p);
                 if (len[r][i] != C(j, r)) return false;      // (counts consistent by construction)
-                B.move(BK_WORK, r, loc[r][i], BK_RECV, r, RD(r, j), len[r][i]);
+                read_T(r, i, BK_RECV, r, RD(r, j));
             }
         B.end_step();
         int64_t work = 0;
