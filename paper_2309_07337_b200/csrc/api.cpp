@@ -406,8 +406,15 @@ int default_algo(mpxa_comm_t c, int op, size_t bytes) {
     if (c->user_algo[op]) return c->user_algo[op];
     for (const SelEntry &e : c->selector)
         if (e.op == op && e.p == c->p && e.R == c->R && bytes <= e.max_bytes) return e.algo;
-    // SPEC.md:256 defaults when nothing was measured: pairwise (alltoall/v); for allgather
-    // the direct (pairwise) exchange, which the measured tables confirm on NVSwitch.
+    // SPEC.md:256 defaults when nothing was measured: pairwise (alltoall/v: its flags are
+    // already one per GPU pair and CTA, so the hierarchical variant's fewer messages buy
+    // nothing here).  Allgather: the direct (pairwise) exchange -- except across GPUs with
+    // several ranks per GPU beyond the eager range, where direct fan-out sends every block to
+    // each of a peer GPU's R ranks over NVLink and the hierarchical variant (groups = GPUs,
+    // SURVEY §8 A10 "hier when R > 1") sends it once per GPU: R x fewer NVLink bytes.
+    if (op == MPXA_OP_ALLGATHER && c->G > 1 && c->Rg > 1 && c->g == c->Rg &&
+        (int64_t)bytes * c->Rg > c->ll_max)
+        return A_HIER;
     return A_PAIRWISE;
 }
 

@@ -354,6 +354,12 @@ def test_selector_and_registry():
     c.set_algorithm("alltoallv", "default")
     with pytest.raises(MpxaError):
         c.set_algorithm("alltoallv", "ring")          # ring is allgather-only
+    # several ranks per GPU across GPUs: allgather beyond the eager range defaults to the
+    # hierarchical variant (one NVLink copy per GPU instead of one per rank)
+    ce = comm(32, 8, 4)
+    assert ce.get_algorithm("allgather", 64) == "pairwise"
+    assert ce.get_algorithm("allgather", 1 << 20) == "hier"
+    assert ce.get_algorithm("alltoall", 1 << 20) == "pairwise"
 
 
 # ------------------------------------------------------------------ full-size (bench launch config)
