@@ -47,10 +47,11 @@
  *    launches (<= 128 KiB per GPU pair) run EAGER: the payload travels as 8-byte words that
  *    each carry the launch's sequence number into the receiver's staging (two parities,
  *    alternating per eager launch), the receiver copies it out -- no clear-to-send, no
- *    fence.  MPXA_NO_LL=1 disables eager mode.  The eager form of a schedule is built on its
- *    first launch for a dtype size; if that first launch is inside a CUDA-graph capture the
- *    launch uses the direct protocol instead, so in multi-process mode either every process
- *    or none captures the first call of a schedule.
+ *    fence.  MPXA_NO_LL=1 disables eager mode.  Persistent requests build their eager form
+ *    at *_init; one-shot calls build it on the first launch of a schedule for a dtype size,
+ *    and if that first launch is inside a CUDA-graph capture it uses the direct protocol
+ *    instead -- so in multi-process mode either every process or none captures the first
+ *    one-shot call of a schedule (persistent requests have no such constraint).
  */
 #ifndef MPXA_H
 #define MPXA_H

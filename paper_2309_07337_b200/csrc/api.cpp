@@ -651,6 +651,12 @@ static const DevProg *ll_program(mpxa_comm_t c, const DevProg &dp, uint64_t unit
     return dp.ll.get();
 }
 
+// Persistent *_init: build the eager companion now (collective, outside any stream capture),
+// so a first start() inside a CUDA-graph capture already runs eager, the same in every process.
+static void prebuild_companions(mpxa_comm_t c, const DevProg &dp, uint64_t unit) {
+    if (c->ll && c->G > 1 && c->p <= kRankTable) (void)ll_program(c, dp, unit, (cudaStream_t)0);
+}
+
 int cached_uniform(mpxa_comm_t c, int op, int algo, int stage, std::shared_ptr<DevProg> &out) {
     auto key = std::make_tuple(op, algo, stage, c->g);
     auto it = c->cache.find(key);
@@ -1170,6 +1176,7 @@ int alltoallv_impl(const void *sendbuf, const int64_t *sc, const int64_t *sd, si
         }
         rc2 = ensure_work(c, (size_t)P.work_units * w * c->Rg);
         if (rc2) { delete q; return rc2; }
+        prebuild_companions(c, *q->prog, w);
         *req = q;
         return MPXA_SUCCESS;
     }
@@ -1203,6 +1210,7 @@ int uniform_impl(int op, const void *sendbuf, size_t count, size_t w, void *recv
         }
         rc = ensure_work(c, (size_t)dp->host.work_units * unit * c->Rg);
         if (rc) { delete q; return rc; }
+        if (unit) prebuild_companions(c, *dp, unit);
         *req = q;
         return MPXA_SUCCESS;
     }
@@ -1261,6 +1269,7 @@ int neighbor_impl(bool locality, const void *sendbuf, const int64_t *sc, const i
         }
         rc2 = ensure_work(c, (size_t)P.work_units * w * c->Rg);
         if (rc2) { delete q; return rc2; }
+        prebuild_companions(c, *q->prog, w);
         *req = q;
         return MPXA_SUCCESS;
     }

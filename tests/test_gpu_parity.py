@@ -687,3 +687,28 @@ def test_execution_paths_are_the_intended_ones(monkeypatch):
     c1.allgather(ag, out, algo="pairwise")
     assert c1.last_launch_path() == {"dyn"}
     del ag, out
+
+
+def test_eager_persistent_first_start_captured():
+    """A persistent request's eager companion is built at *_init, so even a first start()
+    inside a CUDA-graph capture runs eager (the same in every process); replays exact."""
+    p, G, b = 8, 4, 1000
+    c = Comm(ranks_per_proc=p, device=0, emulate_gpus=G, group_size=2, timeout_s=20.0)
+    send = synth.alltoall_sendbuf(9, p, b)
+    d_s, d_r = dev(send), torch.zeros((p, p * b), dtype=torch.uint8, device=DEV)
+    req = c.alltoall_init(d_s, d_r, algo="pairwise")
+    s = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        req.start(s); req.wait(s)
+    assert "eager" in c.last_launch_path()
+    for rep in range(3):
+        fresh = synth.alltoall_sendbuf(20 + rep, p, b)
+        d_s.copy_(dev(fresh)); d_r.zero_(); torch.cuda.synchronize()
+        g.replay(); torch.cuda.synchronize()
+        assert np.array_equal(host(d_r), oracle.alltoall_definition(fresh)), rep
+    del g
+    req.free()
+    assert c.check() == 0
+    c.finalize()
