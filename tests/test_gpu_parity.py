@@ -712,3 +712,23 @@ def test_eager_persistent_first_start_captured():
     req.free()
     assert c.check() == 0
     c.finalize()
+
+
+@pytest.mark.parametrize("G", [0, 4])
+def test_many_ranks_beyond_rank_table(G):
+    """p = 300 ranks (beyond the small kernel's 256-entry rank-base table: bases computed per
+    piece, no resolved moves / eager companion): pairwise, Bruck and hier alltoall and the
+    allgathers stay exact, on one device and over 4 emulated GPUs."""
+    p = 300
+    c = comm(p, G, 4)
+    for b in (4, 36):
+        send = synth.alltoall_sendbuf(b, p, b)
+        want = oracle.alltoall_definition(send)
+        for algo in ("pairwise", "bruck", "hier"):
+            assert np.array_equal(run_alltoall(c, send, algo), want), (b, algo)
+        ag = np.random.default_rng(b).integers(0, 256, size=(p, b), dtype=np.uint8)
+        for algo in ("pairwise", "bruck", "ring"):
+            d_r = torch.full((p, p * b), 0x5A, dtype=torch.uint8, device=DEV)
+            c.allgather(dev(ag), d_r, algo=algo)
+            assert np.array_equal(host(d_r), oracle.allgather_definition(ag)), (b, algo)
+    assert c.check() == 0
