@@ -1,5 +1,5 @@
-"""Latency probe (device us per call, CUDA graphs): the small-kernel launches
-of the bench sweep at a few sizes.  One JSON line."""
+"""Mid-size latency probe (device us per call, CUDA graphs; SIZES / PS / EMU env): alltoall
+and allgather variants.  One JSON line."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
