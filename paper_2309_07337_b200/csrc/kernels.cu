@@ -37,6 +37,16 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p) {
 __device__ __forceinline__ void st_release_sys(uint64_t *p, uint64_t v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// GPU-scope counters (row barriers, launch completion): release / acq_rel RMWs instead of
+// __threadfence() (fence.sc.gpu) + a relaxed atomic -- the same cumulative ordering
+__device__ __forceinline__ void red_release_gpu_add(uint32_t *p, uint32_t v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t atom_acq_rel_gpu_add(uint32_t *p, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
 // Programmatic dependent launch (launches carry programmaticStreamSerialization): the
 // prologue (program tables: library-owned, immutable while launches are in flight) overlaps
 // the previous kernel's tail; everything that kernel may have written or still reads (user
@@ -732,8 +742,7 @@ __device__ __noinline__ bool dyn_step(const ExecParams &P, ExecShared &S, Produc
 __device__ __noinline__ void row_barrier(const ExecParams &P, ExecShared &S, int g, int s) {
     if (threadIdx.x == 0) {
         uint32_t *bar = &P.dc->dyn_bar[g];
-        __threadfence();
-        atomicAdd(bar, 1u);
+        red_release_gpu_add(bar, 1u);
         const uint32_t want = (uint32_t)(s + 1) * gridDim.x;
         uint64_t t0 = 0;
         int it = 0;
@@ -1011,9 +1020,8 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
     // the last CTA of the launch publishes the epoch and resets the work queues (the next
     // launch is stream-ordered after, and waits on griddepcontrol before reading either)
     if ((multi || DYN) && t == 0) {
-        __threadfence();
         const uint32_t total = gridDim.x * gridDim.y;
-        if (atomicAdd(&P.dc->done_ctas, 1u) == total - 1) {
+        if (atom_acq_rel_gpu_add(&P.dc->done_ctas, 1u) == total - 1) {
             P.dc->done_ctas = 0;
             if (multi) P.dc->epoch = epoch;
             if (DYN)
@@ -1025,7 +1033,7 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
                     }
                     P.dc->dyn_bar[row] = 0;
                 }
-            __threadfence();
+            // (no fence: the next launch reads these after griddepcontrol.wait / grid completion)
         }
     }
     CTA_STAMP(1);
@@ -1165,8 +1173,7 @@ __device__ __forceinline__ void small_wait(const ExecParams &P, SmallShared &S, 
 __device__ __noinline__ void small_row_barrier(const ExecParams &P, SmallShared &S, int g, int s) {
     if (threadIdx.x == 0) {
         uint32_t *bar = &P.dc->dyn_bar[g];
-        __threadfence();
-        atomicAdd(bar, 1u);
+        red_release_gpu_add(bar, 1u);
         const uint32_t want = (uint32_t)(s + 1) * gridDim.x;
         uint64_t t0 = 0;
         int it = 0;
@@ -1516,14 +1523,12 @@ __device__ __noinline__ void small_finish(const ExecParams &P, SmallShared &S, i
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        __threadfence();
-        if (atomicAdd(&P.dc->done_ctas, 1u) == gridDim.x * gridDim.y - 1) {
+        if (atom_acq_rel_gpu_add(&P.dc->done_ctas, 1u) == gridDim.x * gridDim.y - 1) {
             P.dc->done_ctas = 0;
             if (multi) P.dc->epoch = epoch;
             if (P.small_ll) P.dc->ll_seq = S.ll_seq;
             if (P.dyn_sync)
                 for (int r = 0; r < (int)gridDim.y; r++) P.dc->dyn_bar[P.mode == 1 ? r : P.my_gpu] = 0;
-            __threadfence();
         }
     }
 }
