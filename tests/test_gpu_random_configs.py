@@ -110,3 +110,37 @@ def test_random_alltoallv(seed):
     torch.cuda.synchronize()
     assert np.array_equal(d_r.cpu().numpy(), want), (p, G, g, w, shape, algo)
     assert c.check() == 0
+
+
+KNOBS = [{"MPXA_NO_LL": "1"}, {"MPXA_NO_SMALL": "1"}, {"MPXA_NO_DYN": "1"}, {"MPXA_SWORK": "0"},
+         {"MPXA_SMALL_NT": "512"}, {"MPXA_NO_PDL": "1"}, {"MPXA_NO_SMALL_SYNC": "1"}]
+
+
+@pytest.mark.parametrize("knob", range(len(KNOBS)), ids=[",".join(k) for k in KNOBS])
+def test_random_under_path_knobs(knob, monkeypatch):
+    """The same random draws with a launch-path knob forcing the alternative path (direct
+    instead of eager, executor instead of small kernel, static slices instead of queues, ...):
+    every path stays exact."""
+    for k, v in KNOBS[knob].items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(3000 + knob)
+    for it in range(6):
+        p = int(rng.choice([3, 4, 8]))
+        G = int(rng.choice(splits(p)))
+        g = int(rng.choice([x for x in (1, 2, 4) if p % x == 0]))
+        b = int(rng.choice([1, 16, 100, 4096, 70000]))
+        c = Comm(ranks_per_proc=p, device=0, emulate_gpus=G, group_size=g, timeout_s=20.0)
+        send = rng.integers(0, 256, size=(p, p * b), dtype=np.uint8)
+        d_r = torch.zeros((p, p * b), dtype=torch.uint8, device=DEV)
+        algo = str(rng.choice(["pairwise", "bruck", "hier"]))
+        c.alltoall(torch.from_numpy(send).to(DEV), d_r, algo=algo)
+        torch.cuda.synchronize()
+        assert np.array_equal(d_r.cpu().numpy(), oracle.alltoall_definition(send)), (knob, p, G, b, algo)
+        ag = rng.integers(0, 256, size=(p, b), dtype=np.uint8)
+        d_o = torch.zeros((p, p * b), dtype=torch.uint8, device=DEV)
+        algo = str(rng.choice(["pairwise", "bruck", "ring"]))
+        c.allgather(torch.from_numpy(ag).to(DEV), d_o, algo=algo)
+        torch.cuda.synchronize()
+        assert np.array_equal(d_o.cpu().numpy(), oracle.allgather_definition(ag)), (knob, p, G, b, algo)
+        assert c.check() == 0
+        c.finalize()
