@@ -249,8 +249,7 @@ struct RingEntry {
 #ifdef MPXA_TRACE
 __device__ uint64_t g_cta_trace[2][kMaxCtas];   // per-CTA entry / exit %globaltimer (GPU 0)
 #define CTA_STAMP(w) do { if (threadIdx.x == 0 && blockIdx.y == 0) g_cta_trace[w][blockIdx.x] = globaltimer(); } while (0)
-// phase stamps of CTA 0 in SM cycles (clock64: one SM, so comparable; %globaltimer ticks only
-// every ~1 us outside a profiler)
+// phase stamps of CTA 0 in SM cycles (clock64: one SM, so comparable and cycle-accurate)
 #define TRACE(k) do { if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x == 0 || threadIdx.x == 32)) P.dc->trace[(k) + (threadIdx.x ? 16 : 0)] = (uint64_t)clock64(); } while (0)
 #else
 #define TRACE(k) do { } while (0)
