@@ -365,27 +365,39 @@ def configs_on_one_gpu(torch, reps=20):
 
     # ---- cfg5: p=32 ranks, bf16, block 16 B .. 1 MiB x4: all 32 ranks on this GPU, and the
     #      same ranks as 8 emulated GPUs x 4 ranks (multi-GPU flag/CTS protocol) ----
+    #      On the emulated GPUs (group = GPU) "hier" is the fused form and "hier_staged" the
+    #      literal gather / exchange / redistribute (MPXA_HIER_STAGED=1) --
     p = 32
     for G in (0, 8):
         c = Comm(ranks_per_proc=p, device=torch.cuda.current_device(), group_size=4, emulate_gpus=G)
+        cs = None
+        if G:
+            os.environ["MPXA_HIER_STAGED"] = "1"
+            cs = Comm(ranks_per_proc=p, device=torch.cuda.current_device(), group_size=4, emulate_gpus=G)
+            del os.environ["MPXA_HIER_STAGED"]
         big = torch.randint(0, 256, (p * p * (1 << 20),), dtype=torch.uint8, device=dev)
         out = {}
-        for algo in ("hier", "bruck", "pairwise"):
+        for name in ("hier", "hier_staged", "bruck", "pairwise"):
+            if name == "hier_staged" and cs is None:
+                continue
+            cc, algo = (cs, "hier") if name == "hier_staged" else (c, name)
             rows = []
             b = 16
             while b <= (1 << 20):
                 s_ = big[: p * p * b].view(p, p * b).view(torch.bfloat16)
                 r_ = torch.empty_like(s_)
                 it = max(3, min(reps, int(2e9 // max(1, p * p * b))))
-                us = 1e3 * time_graph(lambda: c.alltoall(s_, r_, algo=algo, stream=gstream), it, gstream)
+                us = 1e3 * time_graph(lambda: cc.alltoall(s_, r_, algo=algo, stream=gstream), it, gstream)
                 rows.append([b, round(us, 3), round(p * p * b / us / 1e3, 2)])
                 b *= 4
             want = oracle.alltoall_definition(s_.view(torch.uint8).cpu().numpy())
             rows.append({"verified_1MiB": bool(np.array_equal(r_.view(torch.uint8).cpu().numpy(), want))})
-            out[algo] = rows
+            out[name] = rows
         res["cfg5_alltoall_p32_" + ("1gpu" if G == 0 else "8_emulated_gpus")] = out
         del big
         c.finalize()
+        if cs is not None:
+            cs.finalize()
 
     # ---- f1: persistent neighbor alltoallv, sparse-matrix halo: p=8 ranks,
     #      standard vs locality-aware (groups of 2 ranks), all ranks on this GPU and as 4

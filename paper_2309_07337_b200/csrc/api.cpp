@@ -213,6 +213,8 @@ struct mpxa_comm_s {
     bool swork = true;                     // small kernel, one CTA on one GPU: WORK in shared memory
     int small_nt = 64;                     // small kernel block size for launches with few pieces
     bool ll = true;                        // eager (LL) mode for small multi-GPU launches
+    bool hier_staged = false;              // MPXA_HIER_STAGED=1: hierarchical with group = GPU in its
+                                           // literal three-step form instead of the fused one
     uint32_t last_path = 0;                // bits of the last launch's path (mpxa__last_launch)
     int64_t ll_max = 4 * kLLWords;         // eager: payload bytes per GPU pair, single-step launches
     int64_t ll_max_ms = 16384;             // ... multi-step launches
@@ -662,7 +664,7 @@ int cached_uniform(mpxa_comm_t c, int op, int algo, int stage, std::shared_ptr<D
     auto it = c->cache.find(key);
     if (it != c->cache.end()) { out = it->second; return MPXA_SUCCESS; }
     Program P;
-    bool ok = op == MPXA_OP_ALLTOALL ? build_alltoall(P, algo, c->p, c->Rg, c->G, c->g, stage)
+    bool ok = op == MPXA_OP_ALLTOALL ? build_alltoall(P, algo, c->p, c->Rg, c->G, c->g, stage, c->hier_staged)
                                      : build_allgather(P, algo, c->p, c->Rg, c->G, stage, c->g);
     if (!ok) return MPXA_ERR_ALGO;
     int rc = upload_program(P, out);
@@ -1126,7 +1128,8 @@ int vprogram(mpxa_comm_t c, int algo, const std::vector<int64_t> &C, const std::
         c->vcache_n--;
     }
     Program P;
-    if (!build_alltoallv(P, algo, c->p, c->Rg, c->G, c->g, C.data(), SD.data(), RD.data())) return MPXA_ERR_ALGO;
+    if (!build_alltoallv(P, algo, c->p, c->Rg, c->G, c->g, C.data(), SD.data(), RD.data(), c->hier_staged))
+        return MPXA_ERR_ALGO;
     mpxa_comm_s::VEntry e;
     e.algo = algo;
     e.C = C; e.SD = SD; e.RD = RD;
@@ -1161,7 +1164,8 @@ int alltoallv_impl(const void *sendbuf, const int64_t *sc, const int64_t *sd, si
         return run_program(c, *e->prog, (const char *)sendbuf, (char *)recvbuf, w, send_bpr, recv_bpr, stream);
     }
     Program P;
-    if (!build_alltoallv(P, algo, c->p, c->Rg, c->G, c->g, C.data(), SD.data(), RD.data())) return MPXA_ERR_ALGO;
+    if (!build_alltoallv(P, algo, c->p, c->Rg, c->G, c->g, C.data(), SD.data(), RD.data(), c->hier_staged))
+        return MPXA_ERR_ALGO;
     if (req) {
         auto q = new mpxa_request_s();
         q->comm = c; q->op = MPXA_OP_ALLTOALLV; q->algo = algo;
@@ -1374,6 +1378,7 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     if (const char *e = getenv("MPXA_SWORK")) c->swork = atoi(e) != 0;
     if (const char *e = getenv("MPXA_SMALL_NT")) c->small_nt = std::max(32, std::min(512, atoi(e)));
     if (const char *e = getenv("MPXA_NO_LL")) c->ll = atoi(e) == 0;
+    if (const char *e = getenv("MPXA_HIER_STAGED")) c->hier_staged = atoi(e) != 0;
     if (const char *e = getenv("MPXA_LL_MAX")) c->ll_max = atoll(e);
     if (const char *e = getenv("MPXA_LL_MAX_MS")) c->ll_max_ms = atoll(e);
     CK(cudaHostAlloc((void **)&c->err_host, sizeof(int32_t), cudaHostAllocMapped));
@@ -2069,9 +2074,11 @@ int mpxa_plan_build(int op, int algo, int p, int R, int G, int g, int stop_stage
     *plan = nullptr;
     auto P = new Program();
     bool ok = false;
-    if (op == MPXA_OP_ALLTOALL) ok = build_alltoall(*P, algo, p, R, G, g, stop_stage);
+    const char *hs = getenv("MPXA_HIER_STAGED");   // same knob as the comms (tests of both forms)
+    const bool staged = hs && atoi(hs) != 0;
+    if (op == MPXA_OP_ALLTOALL) ok = build_alltoall(*P, algo, p, R, G, g, stop_stage, staged);
     else if (op == MPXA_OP_ALLGATHER) ok = build_allgather(*P, algo, p, R, G, stop_stage, g);
-    else if (op == MPXA_OP_ALLTOALLV && cnt && sd && rd) ok = build_alltoallv(*P, algo, p, R, G, g, cnt, sd, rd);
+    else if (op == MPXA_OP_ALLTOALLV && cnt && sd && rd) ok = build_alltoallv(*P, algo, p, R, G, g, cnt, sd, rd, staged);
     if (!ok) { delete P; return MPXA_ERR_ALGO; }
     *plan = P;
     return MPXA_SUCCESS;

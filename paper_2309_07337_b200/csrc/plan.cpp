@@ -129,7 +129,7 @@ bool topo_ok(int p, int R, int G) {
 // ---------------------------------------------------------------------------------------
 // alltoall
 // ---------------------------------------------------------------------------------------
-bool build_alltoall(Program &P, int algo, int p, int R, int G, int g, int stop_stage) {
+bool build_alltoall(Program &P, int algo, int p, int R, int G, int g, int stop_stage, bool hier_staged) {
     if (!topo_ok(p, R, G)) return false;
     Builder B(P, p, R, G, p * p);
     if (algo == A_PAIRWISE) {
@@ -198,7 +198,7 @@ bool build_alltoall(Program &P, int algo, int p, int R, int G, int g, int stop_s
         std::vector<int64_t> c((size_t)p * p, 1), sd((size_t)p * p), rd((size_t)p * p);
         for (int s = 0; s < p; s++)
             for (int j = 0; j < p; j++) { sd[(size_t)s * p + j] = j; rd[(size_t)j * p + s] = s; }
-        return build_alltoallv(P, A_HIER, p, R, G, g, c.data(), sd.data(), rd.data());
+        return build_alltoallv(P, A_HIER, p, R, G, g, c.data(), sd.data(), rd.data(), hier_staged);
     }
     return false;
 }
@@ -296,7 +296,7 @@ bool build_allgather(Program &P, int algo, int p, int R, int G, int stop_stage, 
 // alltoallv
 // ---------------------------------------------------------------------------------------
 bool build_alltoallv(Program &P, int algo, int p, int R, int G, int g, const int64_t *c,
-                     const int64_t *sd, const int64_t *rd) {
+                     const int64_t *sd, const int64_t *rd, bool hier_staged) {
     if (!topo_ok(p, R, G)) return false;
     auto C = [&](int s, int j) { return c[(size_t)s * p + j]; };
     auto SD = [&](int s, int j) { return sd[(size_t)s * p + j]; };
@@ -365,6 +365,22 @@ bool build_alltoallv(Program &P, int algo, int p, int R, int G, int g, const int
     }
     if (algo != A_HIER) return false;
     if (g < 1 || p % g) return false;
+    if (g == R && !hier_staged) {
+        // A8 with group = GPU, fused ("steps 1 and 3 are HBM-local and can be
+        // fused into K1's addressing"): the GPU of group A reads every local rank's segments
+        // for group B and stores them straight into B's ranks' recvbufs -- one aggregated
+        // transfer per GPU pair carrying one flag per CTA, i.e. the G(G-1) inter-group
+        // messages of the staged form without its two HBM-local passes.
+        Builder B(P, p, R, G, p * p);
+        for (int s = 0; s < p; s++)
+            for (int t = 0; t < p; t++) {
+                int j = imod(s + t, p);
+                B.move(BK_SEND, s, SD(s, j), BK_RECV, j, RD(j, s), C(s, j), (int64_t)s * p + j);
+            }
+        B.end_step();
+        P.work_units = 0;
+        return true;
+    }
     // A8: groups of g consecutive ranks, leader
     // L(A,B) = A*g + (B mod g); aggregated message segments ordered (s,t) row-major.
     const int NG = p / g;

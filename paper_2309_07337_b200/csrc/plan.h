@@ -29,13 +29,15 @@ enum Algo { A_DEFAULT = 0, A_PAIRWISE = 1, A_BRUCK = 2, A_HIER = 3, A_RING = 4, 
 
 // Uniform ops: units are blocks (count * dtype_size bytes).
 //   stop_stage: -1 complete; >= 0 truncated Bruck ending with a T dump into RECV.
-bool build_alltoall(Program &P, int algo, int p, int R, int G, int g, int stop_stage);
+// hier_staged: A_HIER with group = GPU (g == R) in its literal three-step form (gather to
+// the leader, exchange, redistribute); by default that case compiles to the fused form.
+bool build_alltoall(Program &P, int algo, int p, int R, int G, int g, int stop_stage, bool hier_staged = false);
 bool build_allgather(Program &P, int algo, int p, int R, int G, int stop_stage, int g = 1);
 // v-op: units are elements.  c, sd, rd are FULL p x p matrices:
 //   c[s*p+j]  = elements rank s sends to j, sd[s*p+j] its displacement in s's sendbuf,
 //   rd[j*p+s] = displacement in j's recvbuf of the segment from s.
 bool build_alltoallv(Program &P, int algo, int p, int R, int G, int g, const int64_t *c,
-                     const int64_t *sd, const int64_t *rd);
+                     const int64_t *sd, const int64_t *rd, bool hier_staged = false);
 
 // f1 neighbor alltoallv.  Global graph, rank-major edge lists: indeg[p],
 // src/rc/rd per in-edge; outdeg[p], dst/sc/sd per out-edge (elements).  Edges pair like MPI

@@ -61,8 +61,12 @@ def _topologies(p):
     return out
 
 
+@pytest.mark.parametrize("staged", [0, 1])
 @pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 8, 12])
-def test_alltoall_plans_simulate_to_oracle(p):
+def test_alltoall_plans_simulate_to_oracle(p, staged, monkeypatch):
+    """Every variant and GPU split; hierarchical with group = GPU in the fused form (default)
+    and the literal three-step form (MPXA_HIER_STAGED=1)."""
+    monkeypatch.setenv("MPXA_HIER_STAGED", str(staged))
     b = 3
     send = synth.alltoall_sendbuf(p, p, b)
     want = oracle.alltoall_definition(send)
@@ -89,8 +93,10 @@ def test_allgather_plans_simulate_to_oracle(p):
             assert np.array_equal(got, want), (algo, G)
 
 
+@pytest.mark.parametrize("staged", [0, 1])
 @pytest.mark.parametrize("p,g", [(4, 2), (8, 2), (8, 4), (6, 3), (8, 8), (5, 1)])
-def test_alltoallv_plans_simulate_to_oracle(p, g):
+def test_alltoallv_plans_simulate_to_oracle(p, g, staged, monkeypatch):
+    monkeypatch.setenv("MPXA_HIER_STAGED", str(staged))
     for seed in range(4):
         c = synth.cfg4_counts(seed, p, 24)
         send, sc, sd, rc, rd, S, Rcap = synth.alltoallv_buffers(seed, c, elem=8, packed=bool(seed % 2))
@@ -136,3 +142,14 @@ def test_message_counts_of_plans():
     # single GPU: no signals at all
     for algo in ("pairwise", "bruck", "hier"):
         assert Plan("alltoall", algo, 8, G=1, g=2).info["signals"] == 0
+
+
+def test_hier_group_gpu_fused_vs_staged(monkeypatch):
+    """Hierarchical with group = GPU: fused = one step, no workspace, the same G(G-1)
+    inter-group messages as the staged three-step form."""
+    fused = Plan("alltoall", "hier", 32, R=4, G=8, g=4)
+    monkeypatch.setenv("MPXA_HIER_STAGED", "1")
+    staged = Plan("alltoall", "hier", 32, R=4, G=8, g=4)
+    assert fused.info["nsteps"] == 1 and fused.info["work_units"] == 0
+    assert staged.info["nsteps"] == 3 and staged.info["work_units"] > 0
+    assert fused.info["signals"] == staged.info["signals"] == 8 * 7
