@@ -816,8 +816,13 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
     // 64 KiB blocks the TMA executor is faster again)
     const bool small_own = !one_step && !small_sync && items > kSmallItemsOneCta && maxmove <= kSmallSyncMove &&
                            own_ok && c->small_sync && dp.max_gpu_moves <= kSmallMovesSmem;
+    // (emulated GPUs share the SMs: a virtual GPU's small-kernel row has 1/G of them, and its
+    // LSU pieces lose to the executor's TMA on long moves sooner -- measured: f1 halo, 2 MiB
+    // moves on 4 emulated GPUs, 47 -> 32 us with the executor; cfg5's 64-256 KiB moves stay
+    // 3x faster in the small kernel)
+    const uint64_t max1 = c->emulated ? std::min<uint64_t>(c->small_max1, 1u << 20) : c->small_max1;
     const bool small = !c->force_exec &&
-                       (one_step ? (maxmove <= c->small_max1 && src_vol <= c->small_vol1)
+                       (one_step ? (maxmove <= max1 && src_vol <= c->small_vol1)
                                  : ((maxmove <= kSmallKernelMax && items <= kSmallItemsOneCta) || small_sync ||
                                     small_own));
     if (small) {
@@ -1257,7 +1262,7 @@ int neighbor_impl(bool locality, const void *sendbuf, const int64_t *sc, const i
     Program P;
     r = build_neighbor(P, locality, c->p, c->Rg, c->G, c->g, topo->indeg.data(), topo->src.data(), RC.data(),
                        RD.data(), topo->outdeg.data(), topo->dst.data(), SC.data(), SD.data(),
-                       locality ? SI.data() : nullptr, locality ? RI.data() : nullptr);
+                       locality ? SI.data() : nullptr, locality ? RI.data() : nullptr, c->hier_staged);
     if (r) return r;
     if (req) {
         auto q = new mpxa_request_s();
@@ -2091,7 +2096,9 @@ int mpxa_plan_build_neighbor(int p, int R, int G, int g, int locality, const int
     if (!plan || !indeg || !outdeg) return MPXA_ERR_ARG;
     *plan = nullptr;
     auto P = new Program();
-    int r = build_neighbor(*P, locality != 0, p, R, G, g, indeg, src, rc, rd, outdeg, dst, sc, sd, send_idx, recv_idx);
+    const char *hs = getenv("MPXA_HIER_STAGED");   // same knob as the comms
+    int r = build_neighbor(*P, locality != 0, p, R, G, g, indeg, src, rc, rd, outdeg, dst, sc, sd, send_idx, recv_idx,
+                           hs && atoi(hs) != 0);
     if (r) { delete P; return r; }
     *plan = P;
     return MPXA_SUCCESS;

@@ -519,7 +519,7 @@ int nb_prepare(NbGraph &N, int p, const int *indeg, const int *src, const int64_
 
 int build_neighbor(Program &P, bool locality, int p, int R, int G, int g, const int *indeg, const int *src,
                    const int64_t *rc, const int64_t *rd, const int *outdeg, const int *dst, const int64_t *sc,
-                   const int64_t *sd, const int64_t *send_idx, const int64_t *recv_idx) {
+                   const int64_t *sd, const int64_t *send_idx, const int64_t *recv_idx, bool staged) {
     if (!topo_ok(p, R, G)) return MPXA_ERR_TOPOLOGY;
     NbGraph N;
     int rcode = nb_prepare(N, p, indeg, src, rc, rd, outdeg, dst, sc, sd);
@@ -617,9 +617,13 @@ int build_neighbor(Program &P, bool locality, int p, int R, int G, int g, const 
                 if (!cont) { runs.push_back(Run{A, Bg, s0, s2 - s0}); s0 = s2; }
             }
         }
+    // fused (group = GPU, g == R): the gather to the leader is GPU-local, so the exchange reads
+    // each run straight from its holder's sendbuf (same GPU as the leader) -- two steps, no
+    // out-aggregates (as for the hierarchical alltoall)
+    const bool fused = g == R && !staged;
     // workspace of each rank: out-aggregates it leads, then in-aggregates it receives
     std::vector<int64_t> out_base((size_t)NG * NG, 0), in_base((size_t)NG * NG, 0), cur(p, 0);
-    for (int A = 0; A < NG; A++)
+    for (int A = 0; A < NG && !fused; A++)
         for (int Bg = 0; Bg < NG; Bg++) {
             const size_t k = (size_t)A * NG + Bg;
             if (ps[k].ids.empty()) continue;
@@ -649,17 +653,22 @@ int build_neighbor(Program &P, bool locality, int p, int R, int G, int g, const 
     for (size_t k = 0; k < runs.size(); k++) {
         const Run &u = runs[k];
         const size_t pk = (size_t)u.A * NG + u.Bg;
-        B.move(BK_SEND, ps[pk].holder[u.s0], ps[pk].hoff[u.s0], BK_WORK, L(u.A, u.Bg), out_base[pk] + (int64_t)u.s0,
-               (int64_t)u.n, nintra + (int64_t)k);
+        if (fused)   // holder's sendbuf -> L(B,A), each unique id once
+            B.move(BK_SEND, ps[pk].holder[u.s0], ps[pk].hoff[u.s0], BK_WORK, L(u.Bg, u.A), in_base[pk] + (int64_t)u.s0,
+                   (int64_t)u.n, nintra + (int64_t)k);
+        else
+            B.move(BK_SEND, ps[pk].holder[u.s0], ps[pk].hoff[u.s0], BK_WORK, L(u.A, u.Bg), out_base[pk] + (int64_t)u.s0,
+                   (int64_t)u.n, nintra + (int64_t)k);
     }
     B.end_step();
     // step 2: L(A,B) -> L(B,A), each unique id once (one signal per GPU pair per CTA)
     for (const Run &u : runs) {
+        if (fused) break;
         const size_t pk = (size_t)u.A * NG + u.Bg;
         B.move(BK_WORK, L(u.A, u.Bg), out_base[pk] + (int64_t)u.s0, BK_WORK, L(u.Bg, u.A), in_base[pk] + (int64_t)u.s0,
                (int64_t)u.n);
     }
-    B.end_step();
+    B.end_step();   // (an empty step is dropped)
     // step 3: fan out to every final (rank, offset)
     for (const Run &u : runs) {
         const size_t pk = (size_t)u.A * NG + u.Bg;

@@ -46,7 +46,7 @@ bool build_alltoallv(Program &P, int algo, int p, int R, int G, int g, const int
 // Returns 0, or an mpxa status (MPXA_ERR_ARG / _MISMATCH / _TOPOLOGY) without building.
 int build_neighbor(Program &P, bool locality, int p, int R, int G, int g, const int *indeg, const int *src,
                    const int64_t *rc, const int64_t *rd, const int *outdeg, const int *dst, const int64_t *sc,
-                   const int64_t *sd, const int64_t *send_idx, const int64_t *recv_idx);
+                   const int64_t *sd, const int64_t *send_idx, const int64_t *recv_idx, bool staged = false);
 
 int ceil_log2(int p);
 

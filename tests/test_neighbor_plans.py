@@ -33,8 +33,10 @@ def instances():
     yield "empty", 4, []
 
 
+@pytest.mark.parametrize("staged", [0, 1])
 @pytest.mark.parametrize("name,p,edges", list(instances()), ids=[x[0] for x in instances()])
-def test_neighbor_plans_simulate_to_oracle(name, p, edges):
+def test_neighbor_plans_simulate_to_oracle(name, p, edges, staged, monkeypatch):
+    monkeypatch.setenv("MPXA_HIER_STAGED", str(staged))   # group = GPU: fused or three steps
     gr, si, ri = synth.graph_from_edges(p, edges)
     send, recv0 = synth.neighbor_buffers(1, p, gr, si, w=8)
     want = oracle.neighbor_definition(send, recv0, 8, gr)
@@ -57,10 +59,11 @@ def test_locality_crossing_values_match_oracle(name, p, edges):
     send, recv0 = synth.neighbor_buffers(2, p, gr, si, w=8)
     for g in [x for x in (1, 2, 4) if p % x == 0]:
         _, st = oracle.neighbor(send, recv0, 8, gr, "locality", g=g, send_idx=si, recv_idx=ri)
-        pl = Plan.neighbor(gr, R=p, G=1, g=g, locality=True, send_idx=si, recv_idx=ri)
-        mv = pl.moves(0)                  # the only group-crossing moves are WORK -> WORK
-        crossing = sum(m.len for m in mv if m.src_kind == WORK and m.dst_kind == WORK and m.src_rank // g != m.dst_rank // g)
-        assert crossing == st["inter_values"], g
+        for G in (1, p // g):             # staged (groups inside one GPU) and fused (group = GPU)
+            pl = Plan.neighbor(gr, R=p // G, G=G, g=g, locality=True, send_idx=si, recv_idx=ri)
+            mv = [m for x in range(G) for m in pl.moves(x)]
+            crossing = sum(m.len for m in mv if m.src_rank // g != m.dst_rank // g)
+            assert crossing == st["inter_values"], (g, G)
 
 
 def test_stencil_runs_coalesce():
@@ -106,3 +109,14 @@ def test_neighbor_plan_errors():
 def test_neighbor_registry():
     assert M.list_algorithms("neighbor_alltoallv") == ["pairwise", "locality"]
     assert M.lib().mpxa_algo_name(5) == b"locality"
+
+
+def test_locality_fused_has_two_steps(monkeypatch):
+    """Group = GPU: the gather to the leader is GPU-local and fused into the exchange (two
+    steps, no out-aggregates); MPXA_HIER_STAGED=1 keeps the literal three steps."""
+    gr, si, ri = synth.graph_from_edges(8, synth.stencil_edges(4, 2, 16, 8, corners=True))
+    fused = Plan.neighbor(gr, R=2, G=4, g=2, locality=True, send_idx=si, recv_idx=ri)
+    monkeypatch.setenv("MPXA_HIER_STAGED", "1")
+    staged = Plan.neighbor(gr, R=2, G=4, g=2, locality=True, send_idx=si, recv_idx=ri)
+    assert fused.info["nsteps"] == 2 and staged.info["nsteps"] == 3
+    assert fused.info["work_units"] < staged.info["work_units"]
