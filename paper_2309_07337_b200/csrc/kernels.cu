@@ -1023,14 +1023,14 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
         if (atom_acq_rel_gpu_add(&P.dc->done_ctas, 1u) == total - 1) {
             P.dc->done_ctas = 0;
             if (multi) P.dc->epoch = epoch;
-            if (DYN)
+            if (DYN || P.dyn_sync)
                 for (int r = 0; r < (int)gridDim.y; r++) {
                     const int row = P.my_gpu >= 0 ? P.my_gpu : r;
-                    for (int ti = 0; ti < P.dyn_units; ti++) {
+                    for (int ti = 0; DYN && ti < P.dyn_units; ti++) {
                         P.dc->dyn_next[row * kMaxDynTiles + ti] = 0;
                         P.dc->dyn_next2[row * kMaxDynTiles + ti] = 0;
                     }
-                    P.dc->dyn_bar[row] = 0;
+                    P.dc->dyn_bar[row] = 0;   // row barriers (dynamic or per-GPU-signalled steps)
                 }
             // (no fence: the next launch reads these after griddepcontrol.wait / grid completion)
         }
