@@ -291,6 +291,9 @@ __device__ __forceinline__ char *base_of(const ExecParams &P, const ExecShared &
 }
 
 // Spin (threads < 32, one per bit of mask) until *slot(bit) >= want; sets abort on timeout.
+#ifndef MPXA_POLL_NS
+#define MPXA_POLL_NS 128   // executor flag polls: back-off between system-scope loads
+#endif
 __device__ __noinline__ void wait_mask_ge(const ExecParams &P, ExecShared &S, uint32_t mask,
                                              const uint64_t *slot0, uint64_t stride_elems,
                                              uint64_t want) {
@@ -301,7 +304,7 @@ __device__ __noinline__ void wait_mask_ge(const ExecParams &P, ExecShared &S, ui
         int it = 0;
         while (ld_acquire_sys(slot) < want) {
             if (++it > 32) {
-                __nanosleep(128);
+                __nanosleep(MPXA_POLL_NS);
                 if (start == 0) start = globaltimer();
                 else if ((int64_t)(globaltimer() - start) > P.timeout_ns) {
                     atomicExch(P.err, 1);

@@ -6,7 +6,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2309_07337_b200 import Comm, lib
 L = lib(); f = L.mpxa__trace; f.argtypes = [ctypes.c_void_p, ctypes.c_void_p]; f.restype = ctypes.c_int
-p = 8
+p = int(os.environ.get("P", "8"))
 c = Comm(ranks_per_proc=p, device=0, emulate_gpus=int(os.environ.get("EMU", "0")))
 GS = torch.cuda.Stream()
 cases = os.environ.get("CASES", "allgather:4,alltoall:4,allgather:1024,alltoall:16384,allgather:16384,alltoall:65536,alltoall:1048576")
