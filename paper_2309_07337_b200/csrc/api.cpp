@@ -944,7 +944,12 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
         // x (G-1) peers of microsecond releases per step otherwise (measured, 8 emulated GPUs:
         // ring allgather 16 KiB 341 -> 285 us, Bruck allgather 64 KiB 125 -> 102 us; single-step
         // launches unchanged)
-        if (c->G > 1 && c->row_signal) E.dyn_sync = 1;
+        if (c->G > 1 && c->row_signal) {
+            // (and the CTAs split the GPU's own moves evenly: the kernel's flow-group ranges
+            // become move-index ranges, so step 0's flow-range prefetch does not apply)
+            if (!E.dyn_units) E.d0_base = -1;
+            E.dyn_sync = 1;
+        }
         e = launch_exec(E, nC, c->emulated ? c->G : 1, c->emulated, pdl && c->pdl, stream);
     }
     if (e != cudaSuccess) {

@@ -831,6 +831,12 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
     if (ld_step) {
         if (P.nF == 1) {            // one flow group: the whole step, no flow-index lookup
             S.steps[t] = StepInfo{st_r.move_begin, st_r.move_end - st_r.move_begin, st_r.signal_mask, st_r.wait_mask};
+        } else if (P.dyn_sync) {    // steps end at a row barrier: no cross-step ownership, so the
+                                    // GPU's own moves split evenly (global flow ranges would leave
+                                    // all but 1/G of the flow groups idle on each GPU)
+            const int n = st_r.move_end - st_r.move_begin;
+            const int a = (int)((int64_t)n * f / P.nF), b = (int)((int64_t)n * (f + 1) / P.nF);
+            S.steps[t] = StepInfo{st_r.move_begin + a, b - a, st_r.signal_mask, st_r.wait_mask};
         } else if (st_r.dense_base >= 0) {   // move k carries flow dense_base + k: arithmetic range
             const int n = st_r.move_end - st_r.move_begin;
             const int a = clampi(x0 - st_r.dense_base, n);
@@ -884,9 +890,15 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
             st = S.steps[s];
         } else {
             const Step g_st = prog.steps[s];
-            const int32_t *fx = prog.findex + g_st.flow_index;
-            const int m0 = fx[x0];
-            st = StepInfo{g_st.move_begin + m0, fx[x1] - m0, g_st.signal_mask, g_st.wait_mask};
+            if (P.dyn_sync) {
+                const int n = g_st.move_end - g_st.move_begin;
+                const int a = (int)((int64_t)n * f / P.nF), b = (int)((int64_t)n * (f + 1) / P.nF);
+                st = StepInfo{g_st.move_begin + a, b - a, g_st.signal_mask, g_st.wait_mask};
+            } else {
+                const int32_t *fx = prog.findex + g_st.flow_index;
+                const int m0 = fx[x0];
+                st = StepInfo{g_st.move_begin + m0, fx[x1] - m0, g_st.signal_mask, g_st.wait_mask};
+            }
         }
         const uint32_t prev_wait = s == 0 ? 0u : (steps_in_smem ? S.steps[s - 1].wait_mask : prog.steps[s - 1].wait_mask);
         bool wrote = false;   // this thread issued generic global stores in this step
