@@ -34,9 +34,10 @@ constexpr int kMaxDynSmem = 6 * 32768;
 constexpr int kMoveTile = kThreads;   // moves staged in shared memory at a time (one per thread)
 constexpr int kMaxDynTiles = 64;      // dynamic mode: move tiles per step (queues per tile)
 constexpr uint64_t kSmallKernelMax = 8192;  // longest move (bytes) the small-message kernel takes
-constexpr int kSmallMovesSmem = 2048;       // program moves cached in shared memory by the small kernel
+constexpr int kSmallMovesSmem = 4096;       // program moves cached in shared memory by the small kernel
 enum { kSmallCommon = 0, kSmallVar = 1, kSmallLocal = 2, kSmallLL = 3 };   // small-kernel instantiations
-constexpr int kSmallWorkSmem = 96 << 10;    // kSmallLocal: WORK rows in shared memory up to this size
+constexpr int kSmallWorkSmem = 48 << 10;    // kSmallLocal: WORK rows in shared memory up to this size
+                                            // (+ 4096 cached moves + static smem <= 227 KiB)
 constexpr int kRankTable = 256;   // small kernel: per-rank buffer bases kept in shared memory
 constexpr int kMaxWindows = 16;    // registered recv windows per process
 

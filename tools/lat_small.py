@@ -8,8 +8,9 @@ import tune_mid
 from tune_mid import t
 tune_mid.GS = GS = torch.cuda.Stream()
 res = {}
-for p in (4, 8):
-    c = Comm(ranks_per_proc=p, device=0, emulate_gpus=int(os.environ.get("EMU", "0")))
+for p in [int(x) for x in os.environ.get("PS", "4,8").split(",")]:
+    c = Comm(ranks_per_proc=p, device=0, emulate_gpus=int(os.environ.get("EMU", "0")),
+             group_size=int(os.environ.get("GRP", "0")))
     for b in [int(x) for x in os.environ.get("SIZES", "16,1024,16384").split(",")]:
         s = torch.randint(0, 255, (p, p * b), dtype=torch.uint8, device="cuda")
         r = torch.empty_like(s)
