@@ -213,6 +213,7 @@ struct mpxa_comm_s {
     bool swork = true;                     // small kernel, one CTA on one GPU: WORK in shared memory
     int small_nt = 64;                     // small kernel block size for launches with few pieces
     bool ll = true;                        // eager (LL) mode for small multi-GPU launches
+    uint64_t one_cta_items = kSmallItemsOneCta;  // MPXA_ONE_CTA_ITEMS (tuning)
     bool row_signal = true;                // MPXA_ROW_SIGNAL=0: executor steps signalled per (CTA, peer)
     bool hier_staged = false;              // MPXA_HIER_STAGED=1: hierarchical with group = GPU in its
                                            // literal three-step form instead of the fused one
@@ -807,7 +808,7 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
                                                                                           (uint64_t)dp.host.nflows),
                                                                      (uint64_t)c->cap_small));
     const bool own_ok = dp.uniform_len && step_vol <= kSmallOwnVol && step_vol / n_own <= kSmallOwnPerCta;
-    const bool small_sync = !one_step && items > kSmallItemsOneCta && maxmove <= kSmallSyncMove &&
+    const bool small_sync = !one_step && items > c->one_cta_items && maxmove <= kSmallSyncMove &&
                             step_vol <= kSmallSyncVol && c->small_sync &&
                             (!own_ok || dp.max_gpu_moves > kSmallMovesSmem) &&
                             (!dp.uniform_len || dp.host.nflows < 32 || dp.max_gpu_moves > kSmallMovesSmem);
@@ -815,7 +816,7 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
     // CTAs, each owning the flows f % nC == c through all steps -- no barrier needed
     // (measured, p=8: Bruck alltoall 4 KiB 13.9 -> 10.8 us, hier 9.8 -> 8.6 us at 16 KiB; from
     // 64 KiB blocks the TMA executor is faster again)
-    const bool small_own = !one_step && !small_sync && items > kSmallItemsOneCta && maxmove <= kSmallSyncMove &&
+    const bool small_own = !one_step && !small_sync && items > c->one_cta_items && maxmove <= kSmallSyncMove &&
                            own_ok && c->small_sync && dp.max_gpu_moves <= kSmallMovesSmem;
     // (emulated GPUs share the SMs: a virtual GPU's small-kernel row has 1/G of them, and its
     // LSU pieces lose to the executor's TMA on long moves sooner -- measured: f1 halo, 2 MiB
@@ -824,7 +825,7 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
     const uint64_t max1 = c->emulated ? std::min<uint64_t>(c->small_max1, 1u << 20) : c->small_max1;
     const bool small = !c->force_exec &&
                        (one_step ? (maxmove <= max1 && src_vol <= c->small_vol1)
-                                 : ((maxmove <= kSmallKernelMax && items <= kSmallItemsOneCta) || small_sync ||
+                                 : ((maxmove <= kSmallKernelMax && items <= c->one_cta_items) || small_sync ||
                                     small_own));
     if (small) {
         E.nS = E.nF = 1;
@@ -1395,6 +1396,7 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     if (const char *e = getenv("MPXA_SWORK")) c->swork = atoi(e) != 0;
     if (const char *e = getenv("MPXA_SMALL_NT")) c->small_nt = std::max(32, std::min(512, atoi(e)));
     if (const char *e = getenv("MPXA_NO_LL")) c->ll = atoi(e) == 0;
+    if (const char *e = getenv("MPXA_ONE_CTA_ITEMS")) c->one_cta_items = strtoull(e, nullptr, 10);
     if (const char *e = getenv("MPXA_HIER_STAGED")) c->hier_staged = atoi(e) != 0;
     if (const char *e = getenv("MPXA_ROW_SIGNAL")) c->row_signal = atoi(e) != 0;
     if (const char *e = getenv("MPXA_LL_MAX")) c->ll_max = atoll(e);
