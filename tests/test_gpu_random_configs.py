@@ -3,6 +3,8 @@ count, emulated GPU split, block / count sizes, dtype size, buffer misalignment,
 or one-shot -- each checked bit-exactly against the oracle with canaries around the results.
 Covers the launch-path combinations the directed tests reach one at a time (small kernel
 modes, eager staging, variable pieces, shared-memory WORK, block sizing, executor)."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -34,13 +36,15 @@ def to_dev(a, off):
     return flat, flat[off:off + a.size].view(a.shape)
 
 
-@pytest.mark.parametrize("seed", range(96))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("MPXA_RANDOM_SEEDS", "96"))))
 def test_random_alltoall_allgather(seed):
     rng = np.random.default_rng(1000 + seed)
     p = int(rng.choice([2, 3, 4, 6, 8, 12, 16]))
     G = int(rng.choice(splits(p)))
     g = int(rng.choice([x for x in (1, 2, 3, 4) if p % x == 0]))
-    b = int(rng.choice([1, 3, 8, 16, 44, 256, 1000, 4096, 4100, 65536, 70000]))
+    b = int(rng.choice([1, 3, 8, 16, 44, 256, 1000, 4096, 4100, 65536, 70000, 300_000, 1 << 20]))
+    if p * p * b > (48 << 20):   # keep the executor-sized draws to small p
+        b = 70000
     off = int(rng.choice([0, 0, 1, 4, 8]))
     c = comm(p, G, g)
     send = rng.integers(0, 256, size=(p, p * b), dtype=np.uint8)
@@ -69,7 +73,7 @@ def test_random_alltoall_allgather(seed):
     assert c.check() == 0
 
 
-@pytest.mark.parametrize("seed", range(64))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("MPXA_RANDOM_SEEDS", "96")) * 2 // 3))
 def test_random_alltoallv(seed):
     rng = np.random.default_rng(2000 + seed)
     p = int(rng.choice([2, 4, 5, 8, 16]))
