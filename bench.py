@@ -595,9 +595,11 @@ def gpu_arm(args):
     total_recv = p * p * b                      # all ranks, bytes received (incl. own block)
     value = total_recv / (ms * 1e-3) / 1e9
     # algorithmic bytes of the kernel on this GPU.  1 GPU: HBM read R*b + write R*p*b.
-    # N GPUs: NVLink ingress per GPU (p-R)*b*R (every hosted rank receives p-R remote blocks)
+    # N GPUs: the operation's minimum NVLink ingress per GPU: each of the
+    # p-R remote blocks arrives once, (p-R)*b -- the direct fan-out moves it R times (once per
+    # hosted rank), the hierarchical variant once and replicates it in HBM
     hbm_bytes = R * b + R * p * b
-    nvl_bytes = R * (p - R) * b
+    nvl_bytes = (p - R) * b
     if ws == 1:
         bound, alg_bytes, peak_use, peak_note = "hbm", hbm_bytes, peak, peak_src
     else:
