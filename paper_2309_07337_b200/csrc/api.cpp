@@ -219,7 +219,7 @@ struct mpxa_comm_s {
                                            // literal three-step form instead of the fused one
     uint32_t last_path = 0;                // bits of the last launch's path (mpxa__last_launch)
     int64_t ll_max = 4 * kLLWords;         // eager: payload bytes per GPU pair, single-step launches
-    int64_t ll_max_ms = 16384;             // ... multi-step launches
+    int64_t ll_max_ms = 65536;             // ... multi-step launches
     int force_ns = 0, force_nf = 0;           // MPXA_NS / MPXA_NF overrides (tuning)
     int force_big = -1;                       // MPXA_TMA_BIG=0/1 override (tuning)
     bool force_exec = false;                  // MPXA_NO_SMALL=1: never use the small-message kernel
@@ -646,8 +646,9 @@ static const DevProg *ll_program(mpxa_comm_t c, const DevProg &dp, uint64_t unit
     // measured (4 emulated GPUs, p = 4 / 8): eager wins up to the full 128 KiB staging per
     // GPU pair for single-step launches (pairwise alltoall 64 KiB pairs 16.0 -> 10.2 us; the
     // direct protocol's CTS + two system-scope releases cost more than eager's 2x bytes);
-    // multi-step ones pay the 2x bytes and word stores in every step and break even at
-    // 16-32 KiB per pair
+    // multi-step ones pay the 2x bytes and word stores in every step; re-measured after the
+    // executor's per-GPU signalling: eager still wins at 64 KiB per pair (ring allgather 4 KiB
+    // blocks 37.5 -> 19.7 us, Bruck alltoall 2 KiB 24.5 -> 16.2 us on 4 emulated GPUs)
     const int64_t max_words = (dp.nsteps > 1 ? c->ll_max_ms : c->ll_max) / 4;
     if (!build_ll(dp.host, unit, c->Rg, Q, max_words)) return nullptr;
     if (upload_companion(std::move(Q), dp.ll) != MPXA_SUCCESS) return nullptr;
