@@ -1026,7 +1026,9 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
     // completion: everything peers write into this GPU in the last step has landed
     const uint32_t last_wait = nsteps == 0 ? 0u : (steps_in_smem ? S.steps[nsteps - 1].wait_mask
                                                                   : prog.steps[nsteps - 1].wait_mask);
-    if (multi && last_wait) {
+    // (per-GPU signals: the peers' last-step data is complete when their one flag is; one
+    // CTA waiting keeps the grid alive until then, the others retire and free their SMs)
+    if (multi && last_wait && (!P.dyn_sync || c == 0)) {
         wait_mask_ge(P, S, last_wait, &S.sym[g]->flags[0][P.dyn_sync ? 0 : c], kMaxCtas,
                      (epoch << 8) | (uint64_t)nsteps);
         __syncthreads();
