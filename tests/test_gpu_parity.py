@@ -5,6 +5,8 @@ bytes, so the bar is bit-exactness for every op, variant, size and topology, inc
 ragged / misaligned sizes, zero counts, canaries outside received ranges, emulated
 multi-GPU protocol runs, Bruck intermediate states and persistent start/wait cycles.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -651,6 +653,7 @@ def test_direct_protocol_small_sizes(G, monkeypatch):
     c.finalize()
 
 
+@pytest.mark.skipif(os.environ.get("MPXA_NO_LL", "0") != "0", reason="asserts the eager path")
 def test_execution_paths_are_the_intended_ones(monkeypatch):
     """The launches these parity tests rely on take the paths they are meant to exercise
     (mpxa__last_launch): eager on emulated GPUs for small messages, direct otherwise; the
@@ -689,6 +692,7 @@ def test_execution_paths_are_the_intended_ones(monkeypatch):
     del ag, out
 
 
+@pytest.mark.skipif(os.environ.get("MPXA_NO_LL", "0") != "0", reason="asserts the eager path")
 def test_eager_persistent_first_start_captured():
     """A persistent request's eager companion is built at *_init, so even a first start()
     inside a CUDA-graph capture runs eager (the same in every process); replays exact."""
