@@ -38,3 +38,10 @@ req = c.alltoallv_init(d_s, sc, sd, d_r, rc, rd, dtype_size=8)
 res["python_persistent_us"] = wall(lambda: (req.start(st), req.wait(st)))
 rh = ctypes.c_void_p(req.h) if hasattr(req, "h") else None
 print(json.dumps(res), flush=True)
+
+# uniform one-shot alltoall (p = 8, 64 B blocks)
+s8 = torch.randint(0, 255, (p, p * 64), dtype=torch.uint8, device="cuda"); r8 = torch.empty_like(s8)
+res["python_alltoall_us"] = wall(lambda: c.alltoall(s8, r8, stream=st))
+sp8, rp8 = ctypes.c_void_p(s8.data_ptr()), ctypes.c_void_p(r8.data_ptr())
+res["c_alltoall_us"] = wall(lambda: L.mpxa_alltoall_algo(sp8, 64, 1, rp8, 0, h, s_))
+print(json.dumps(res), flush=True)
