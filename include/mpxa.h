@@ -301,6 +301,14 @@ int mpxa_list_algorithms(mpxa_op_t op, mpxa_algo_t *out, int *n);  /* *n in: cap
 /* Load a selector table: lines "op p ranks_per_proc max_bytes algo" (text, '#' comments);
  * for each (op, p, R) the first line with bytes <= max_bytes wins. */
 int mpxa_load_selector(mpxa_comm_t comm, const char *path);
+/* 64-bit digest of everything that chooses a launch's protocol, path or grid on the host:
+ * every tuning knob, the selector table, forced variants (MPXA_ALGO) and the
+ * initial heap size.  mpxa_init compares it across processes before any CUDA call and fails
+ * with MPXA_ERR_MISMATCH on a difference (a process running the eager protocol against one
+ * running the direct protocol would otherwise stall until the watchdog fires).  Local call.
+ * Note: mpxa_load_selector / mpxa_set_algorithm after init change it; they must be called
+ * identically on every process. */
+int mpxa_config_digest(mpxa_comm_t comm, uint64_t *digest);
 
 const char *mpxa_error_string(int status);
 const char *mpxa_algo_name(mpxa_algo_t algo);

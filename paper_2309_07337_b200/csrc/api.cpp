@@ -209,6 +209,7 @@ struct mpxa_comm_s {
     mpxa_allgather_fn boot = nullptr;
     void *ctx = nullptr;
     double timeout_s = 60.0;
+    size_t heap0 = 0;                      // initial workspace heap per GPU (mpxa_init_args)
     int sm_count = 148, cap_ctas = 296;   // cap_ctas: mid TMA config (2 CTAs / SM)
     int cap_big = 148;                     // big TMA config (1 CTA / SM)
     int cap_small = 148;                   // small-message kernel (1 CTA / SM)
@@ -1217,12 +1218,22 @@ int alltoallv_impl(const void *sendbuf, const int64_t *sc, const int64_t *sd, si
     if (!dtype_ok(w)) return MPXA_ERR_ARG;
     if (!sendbuf || !recvbuf) return MPXA_ERR_ARG;
     if (overlap(sendbuf, send_bpr * c->R, recvbuf, recv_bpr * c->R)) return MPXA_ERR_ARG;
-    if (algo == A_DEFAULT) algo = default_algo(c, MPXA_OP_ALLTOALLV, recv_bpr);
-    if (!algo_valid(MPXA_OP_ALLTOALLV, algo)) return MPXA_ERR_ALGO;
+    if (algo != A_DEFAULT && !algo_valid(MPXA_OP_ALLTOALLV, algo)) return MPXA_ERR_ALGO;
     if (algo == A_HIER && c->p % c->g) return MPXA_ERR_TOPOLOGY;
     std::vector<int64_t> C, SD, RD;
     int r = gather_v(c, sc, sd, rc, rd, w, send_bpr, recv_bpr, C, SD, RD, stream);
     if (r) return r;
+    if (algo == A_DEFAULT) {
+        // the selector's size for a v-collective is the mean pair segment of the GLOBAL count
+        // matrix (the same on every process; a local size such as this rank's recv capacity
+        // could pick different variants on different processes)
+        int64_t tot = 0;
+        for (int64_t x : C) tot += x;
+        const uint64_t mean = ((uint64_t)tot * w + (uint64_t)c->p * c->p - 1) / ((uint64_t)c->p * c->p);
+        algo = default_algo(c, MPXA_OP_ALLTOALLV, mean);
+        if (!algo_valid(MPXA_OP_ALLTOALLV, algo)) return MPXA_ERR_ALGO;
+        if (algo == A_HIER && c->p % c->g) return MPXA_ERR_TOPOLOGY;
+    }
     if (!req) {                                  // one-shot: cached program, PDL launch
         mpxa_comm_s::VEntry *e = nullptr;
         r = vprogram(c, algo, C, SD, RD, e);
@@ -1348,6 +1359,77 @@ int neighbor_impl(bool locality, const void *sendbuf, const int64_t *sc, const i
 
 cudaStream_t S(mpxa_stream_t s) { return (cudaStream_t)s; }
 
+int load_selector_file(mpxa_comm_t c, const char *path);
+
+// Tuning knobs, the selector table and forced variants, read once per comm.
+void read_knobs(mpxa_comm_t c) {
+    if (const char *e = getenv("MPXA_NS")) c->force_ns = atoi(e);
+    if (const char *e = getenv("MPXA_NF")) c->force_nf = atoi(e);
+    if (const char *e = getenv("MPXA_TMA_BIG")) c->force_big = atoi(e);
+    if (const char *e = getenv("MPXA_NO_SMALL")) c->force_exec = atoi(e) != 0;
+    if (const char *e = getenv("MPXA_NO_PDL")) c->pdl = atoi(e) == 0;
+    if (const char *e = getenv("MPXA_NO_DYN")) c->dyn = atoi(e) == 0;
+    if (const char *e = getenv("MPXA_DYN_PIECES")) c->dyn_pieces = std::max(1, atoi(e));
+    if (const char *e = getenv("MPXA_DYN_MIN")) c->dyn_min_total = strtoull(e, nullptr, 10);
+    if (const char *e = getenv("MPXA_DYN_SYNC")) c->force_sync = atoi(e);
+    if (const char *e = getenv("MPXA_NO_SMALL_SYNC")) c->small_sync = atoi(e) == 0;
+    if (const char *e = getenv("MPXA_SMALL_MAX")) c->small_max1 = strtoull(e, nullptr, 10);
+    if (const char *e = getenv("MPXA_SMALL_VOL")) c->small_vol1 = strtoull(e, nullptr, 10);
+    if (const char *e = getenv("MPXA_VAR_CHOP")) c->var_chop = atoll(e);
+    if (const char *e = getenv("MPXA_VAR_TILES")) c->var_tiles = std::max(1, atoi(e));
+    if (const char *e = getenv("MPXA_SWORK")) c->swork = atoi(e) != 0;
+    if (const char *e = getenv("MPXA_SMALL_NT")) c->small_nt = std::max(32, std::min(512, atoi(e)));
+    if (const char *e = getenv("MPXA_NO_LL")) c->ll = atoi(e) == 0;
+    if (const char *e = getenv("MPXA_ONE_CTA_ITEMS")) c->one_cta_items = strtoull(e, nullptr, 10);
+    if (const char *e = getenv("MPXA_HIER_STAGED")) c->hier_staged = atoi(e) != 0;
+    if (const char *e = getenv("MPXA_ROW_SIGNAL")) c->row_signal = atoi(e) != 0;
+    if (const char *e = getenv("MPXA_LL_MAX")) c->ll_max = atoll(e);
+    if (const char *e = getenv("MPXA_LL_MAX_MS")) c->ll_max_ms = atoll(e);
+    // measured selector table: $MPXA_SELECTOR, else selector_b200.txt next to libmpxa.so
+    // (an absent or unreadable file leaves the built-in rules)
+    if (const char *sel = getenv("MPXA_SELECTOR")) {
+        load_selector_file(c, sel);
+    } else {
+        Dl_info info;
+        if (dladdr((void *)&read_knobs, &info) && info.dli_fname) {
+            std::string path(info.dli_fname);
+            auto slash = path.rfind('/');
+            path = (slash == std::string::npos ? std::string(".") : path.substr(0, slash)) + "/selector_b200.txt";
+            load_selector_file(c, path.c_str());
+        }
+    }
+    if (const char *al = getenv("MPXA_ALGO")) {   // e.g. "alltoall:bruck,allgather:ring"
+        std::stringstream ss{std::string(al)};
+        std::string item;
+        while (std::getline(ss, item, ',')) {
+            auto k = item.find(':');
+            if (k == std::string::npos) continue;
+            std::string o = item.substr(0, k), v = item.substr(k + 1);
+            int op = o == "alltoall" ? 0 : o == "alltoallv" ? 1 : o == "allgather" ? 2 : -1;
+            int av = v == "pairwise" ? 1 : v == "bruck" ? 2 : v == "hier" ? 3 : v == "ring" ? 4 : 0;
+            if (op >= 0 && algo_valid(op, av)) c->user_algo[op] = av;
+        }
+    }
+}
+
+// Digest of everything that chooses a launch's protocol, path or grid on the host: every
+// knob, the selector table, the forced variants and the initial heap size (heap growth is
+// a collective IPC exchange: the sizes must evolve identically on every process).
+uint64_t knob_digest(mpxa_comm_t c, size_t heap) {
+    const int64_t v[] = {c->force_ns, c->force_nf, c->force_big, c->force_exec, c->pdl, c->dyn, c->dyn_pieces,
+                         (int64_t)c->dyn_min_total, c->force_sync, c->small_sync, (int64_t)c->small_max1,
+                         (int64_t)c->small_vol1, c->var_chop, c->var_tiles, c->swork, c->small_nt, c->ll,
+                         (int64_t)c->one_cta_items, c->hier_staged, c->row_signal, c->ll_max, c->ll_max_ms,
+                         c->user_algo[0], c->user_algo[1], c->user_algo[2], (int64_t)heap,
+                         (int64_t)c->selector.size()};
+    uint64_t h = fnv(1469598103934665603ull, v, sizeof v);
+    for (const SelEntry &e : c->selector) {
+        const int64_t r[] = {e.op, e.p, e.R, (int64_t)e.max_bytes, e.algo};
+        h = fnv(h, r, sizeof r);
+    }
+    return h;
+}
+
 }  // namespace
 
 // =========================================================================================
@@ -1412,6 +1494,22 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     c->g = a->group_size > 0 ? a->group_size : c->Rg;
     if (c->p % c->g) return MPXA_ERR_TOPOLOGY;
     if (c->G > kMaxGpus || c->p > 65535) return MPXA_ERR_TOPOLOGY;
+    read_knobs(c.get());
+    size_t heap = a->heap_bytes ? a->heap_bytes : (size_t)64 << 20;
+    c->heap0 = heap;
+    if (c->nprocs > 1) {
+        // Every process must run the same protocol: the topology, every effective tuning knob,
+        // the selector table and the forced variants are compared BEFORE any CUDA call (all
+        // processes see all digests, so all return the same verdict -- no one is left waiting
+        // in a later collective step).  A difference is MPXA_ERR_MISMATCH.
+        uint64_t mine[5] = {(uint64_t)c->R, (uint64_t)c->g, (uint64_t)c->nprocs, knob_digest(c.get(), heap),
+                            (uint64_t)(a->emulate_gpus > 1 ? a->emulate_gpus : 0)};
+        std::vector<uint64_t> all(5 * (size_t)c->nprocs);
+        int rc = bootstrap(c.get(), mine, all.data(), sizeof mine);
+        if (rc) return rc;
+        for (int q = 0; q < c->nprocs; q++)
+            if (memcmp(mine, &all[5 * (size_t)q], sizeof mine)) return MPXA_ERR_MISMATCH;
+    }
     CK(cudaSetDevice(c->device));
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, c->device));
@@ -1427,28 +1525,6 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     if (getenv("MPXA_DEBUG"))
         fprintf(stderr, "mpxa: %d SMs, executor CTAs/SM mid %d big %d -> caps %d / %d\n", c->sm_count, occ, occ_big,
                 c->cap_ctas, c->cap_big);
-    if (const char *e = getenv("MPXA_NS")) c->force_ns = atoi(e);
-    if (const char *e = getenv("MPXA_NF")) c->force_nf = atoi(e);
-    if (const char *e = getenv("MPXA_TMA_BIG")) c->force_big = atoi(e);
-    if (const char *e = getenv("MPXA_NO_SMALL")) c->force_exec = atoi(e) != 0;
-    if (const char *e = getenv("MPXA_NO_PDL")) c->pdl = atoi(e) == 0;
-    if (const char *e = getenv("MPXA_NO_DYN")) c->dyn = atoi(e) == 0;
-    if (const char *e = getenv("MPXA_DYN_PIECES")) c->dyn_pieces = std::max(1, atoi(e));
-    if (const char *e = getenv("MPXA_DYN_MIN")) c->dyn_min_total = strtoull(e, nullptr, 10);
-    if (const char *e = getenv("MPXA_DYN_SYNC")) c->force_sync = atoi(e);
-    if (const char *e = getenv("MPXA_NO_SMALL_SYNC")) c->small_sync = atoi(e) == 0;
-    if (const char *e = getenv("MPXA_SMALL_MAX")) c->small_max1 = strtoull(e, nullptr, 10);
-    if (const char *e = getenv("MPXA_SMALL_VOL")) c->small_vol1 = strtoull(e, nullptr, 10);
-    if (const char *e = getenv("MPXA_VAR_CHOP")) c->var_chop = atoll(e);
-    if (const char *e = getenv("MPXA_VAR_TILES")) c->var_tiles = std::max(1, atoi(e));
-    if (const char *e = getenv("MPXA_SWORK")) c->swork = atoi(e) != 0;
-    if (const char *e = getenv("MPXA_SMALL_NT")) c->small_nt = std::max(32, std::min(512, atoi(e)));
-    if (const char *e = getenv("MPXA_NO_LL")) c->ll = atoi(e) == 0;
-    if (const char *e = getenv("MPXA_ONE_CTA_ITEMS")) c->one_cta_items = strtoull(e, nullptr, 10);
-    if (const char *e = getenv("MPXA_HIER_STAGED")) c->hier_staged = atoi(e) != 0;
-    if (const char *e = getenv("MPXA_ROW_SIGNAL")) c->row_signal = atoi(e) != 0;
-    if (const char *e = getenv("MPXA_LL_MAX")) c->ll_max = atoll(e);
-    if (const char *e = getenv("MPXA_LL_MAX_MS")) c->ll_max_ms = atoll(e);
     CK(cudaHostAlloc((void **)&c->err_host, sizeof(int32_t), cudaHostAllocMapped));
     *c->err_host = 0;
     CK(cudaHostGetDevicePointer((void **)&c->err_dev, c->err_host, 0));
@@ -1459,49 +1535,21 @@ int mpxa_init(mpxa_comm_t *out, const mpxa_init_args *a) {
     CK(cudaMemset(c->dc, 0, sizeof(DevComm)));
     memset(&c->dc_host, 0, sizeof(DevComm));
     if (c->nprocs > 1) {
-        // consistency of the topology across processes (MPXA_ERR_MISMATCH)
-        int mine[3] = {c->R, c->g, c->nprocs};
-        std::vector<int> all(3 * c->nprocs);
+        // the grid of a launch is computed from the CTA caps, and processes pair CTA flag
+        // slots 1:1 -- the devices must agree on them (SM count, occupancy)
+        uint64_t mine[3] = {(uint64_t)c->cap_ctas, (uint64_t)c->cap_big, (uint64_t)c->cap_small};
+        std::vector<uint64_t> all(3 * (size_t)c->nprocs);
         int rc = bootstrap(c.get(), mine, all.data(), sizeof mine);
         if (rc) return rc;
         for (int q = 0; q < c->nprocs; q++)
-            if (memcmp(mine, &all[3 * q], sizeof mine)) return MPXA_ERR_MISMATCH;
+            if (memcmp(mine, &all[3 * (size_t)q], sizeof mine)) return MPXA_ERR_MISMATCH;
         rc = ipc_exchange(c.get(), c->sym_local, (char **)c->sym_map);
         if (rc) return rc;
     } else {
         for (int g = 0; g < c->G; g++) c->sym_map[g] = c->sym_local + g;
     }
-    size_t heap = a->heap_bytes ? a->heap_bytes : (size_t)64 << 20;
     int rc = ensure_work(c.get(), heap);
     if (rc) return rc;
-    // built-in selector table shipped next to the library (optional)
-    // measured selector table: $MPXA_SELECTOR, else selector_b200.txt next to libmpxa.so
-    const char *sel = getenv("MPXA_SELECTOR");
-    if (sel) {
-        mpxa_load_selector(c.get(), sel);
-    } else {
-        Dl_info info;
-        if (dladdr((void *)&mpxa_init, &info) && info.dli_fname) {
-            std::string path(info.dli_fname);
-            auto slash = path.rfind('/');
-            path = (slash == std::string::npos ? std::string(".") : path.substr(0, slash)) + "/selector_b200.txt";
-            mpxa_load_selector(c.get(), path.c_str());   // absent file: built-in defaults
-        }
-    }
-    const char *al = getenv("MPXA_ALGO");   // e.g. "alltoall:bruck,allgather:ring"
-    if (al) {
-        std::string s(al);
-        std::stringstream ss(s);
-        std::string item;
-        while (std::getline(ss, item, ',')) {
-            auto k = item.find(':');
-            if (k == std::string::npos) continue;
-            std::string o = item.substr(0, k), v = item.substr(k + 1);
-            int op = o == "alltoall" ? 0 : o == "alltoallv" ? 1 : o == "allgather" ? 2 : -1;
-            int av = v == "pairwise" ? 1 : v == "bruck" ? 2 : v == "hier" ? 3 : v == "ring" ? 4 : 0;
-            if (op >= 0 && algo_valid(op, av)) c->user_algo[op] = av;
-        }
-    }
     CK(cudaDeviceSynchronize());
     *out = c.release();
     return MPXA_SUCCESS;
@@ -2113,6 +2161,19 @@ int mpxa_list_algorithms(mpxa_op_t op, mpxa_algo_t *out, int *n) {
 
 int mpxa_load_selector(mpxa_comm_t c, const char *path) {
     if (!c || !path) return MPXA_ERR_ARG;
+    return load_selector_file(c, path);
+}
+
+int mpxa_config_digest(mpxa_comm_t c, uint64_t *digest) {
+    if (!c || !digest) return MPXA_ERR_ARG;
+    *digest = knob_digest(c, c->heap0);
+    return MPXA_SUCCESS;
+}
+
+}  // extern "C"
+
+namespace {
+int load_selector_file(mpxa_comm_t c, const char *path) {
     std::ifstream f(path);
     if (!f) return MPXA_ERR_ARG;
     std::vector<SelEntry> t;
@@ -2134,6 +2195,9 @@ int mpxa_load_selector(mpxa_comm_t c, const char *path) {
     c->selector = t;
     return MPXA_SUCCESS;
 }
+}  // namespace
+
+extern "C" {
 
 // ---- host-only plan introspection (include/mpxa_plan.h) ---------------------------------
 int mpxa_plan_build(int op, int algo, int p, int R, int G, int g, int stop_stage, const int64_t *cnt,

@@ -95,6 +95,7 @@ SIGNATURES = {
     "mpxa_get_algorithm": ([_P, _I, _Z, ctypes.POINTER(_I)], _I),
     "mpxa_list_algorithms": ([_I, ctypes.POINTER(_I), ctypes.POINTER(_I)], _I),
     "mpxa_load_selector": ([_P, ctypes.c_char_p], _I),
+    "mpxa_config_digest": ([_P, _U64P], _I),
     "mpxa_error_string": ([_I], ctypes.c_char_p),
     "mpxa_algo_name": ([_I], ctypes.c_char_p),
     "mpxa_plan_build": ([_I, _I, _I, _I, _I, _I, _I, _P, _P, _P, ctypes.POINTER(_P)], _I),
@@ -297,6 +298,12 @@ class Comm:
         a = ctypes.c_int()
         _ck(_lib().mpxa_get_algorithm(self.handle, OPS[op], nbytes, ctypes.byref(a)), "get_algorithm")
         return ALGO_NAME[a.value]
+
+    def config_digest(self) -> int:
+        """Digest of the knobs / selector / forced variants compared across processes at init."""
+        d = ctypes.c_uint64()
+        _ck(_lib().mpxa_config_digest(self.handle, ctypes.byref(d)), "config_digest")
+        return d.value
 
     def load_selector(self, path: str):
         _ck(_lib().mpxa_load_selector(self.handle, path.encode()), "load_selector")

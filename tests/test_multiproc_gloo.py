@@ -28,7 +28,7 @@ def _free_port():
     return port
 
 
-def _run(rank, port, fn, q):
+def _run(rank, port, fn, q):  # noqa: C901
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=WS)
@@ -150,3 +150,54 @@ def _sim_body(rank):
 
 def test_two_process_schedule_composition():
     spawn(_sim_body)
+
+
+# --------------------------------------------------------------------------------------
+# cross-process configuration consistency (mpxa_init, before any CUDA call)
+
+def _knob_body(rank, cases):
+    """Each case: (env of rank 0, env of rank 1, expected); all cases run in order on both
+    processes (mpxa_init is collective)."""
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    from paper_2309_07337_b200 import Comm, MpxaError
+    from paper_2309_07337_b200 import mpxa as M
+    for env_by_rank, expect in cases:
+        env = env_by_rank[rank]
+        for k, v in env.items():
+            os.environ[k] = v
+        try:
+            c = Comm(ranks_per_proc=2, device=0, pg=dist.group.WORLD, timeout_s=5.0)
+            status = M.SUCCESS
+            c.finalize()
+        except MpxaError as e:
+            status = e.status
+        for k in env:
+            del os.environ[k]
+        # equal configurations pass the check and init proceeds to the device (no GPU here:
+        # MPXA_ERR_CUDA; on a GPU box it may succeed); unequal ones stop at the check
+        if expect == "mismatch":
+            assert status == M.ERR_MISMATCH, (env_by_rank, status)
+        else:
+            assert status in (M.SUCCESS, M.ERR_CUDA), (env_by_rank, status)
+
+
+def test_init_knob_consistency(tmp_path):
+    """processes that disagree on a protocol knob, the selector table or a forced
+    variant must fail mpxa_init with MPXA_ERR_MISMATCH (on every process), not desynchronize
+    the eager / direct protocols at the first launch."""
+    import functools
+    sel = tmp_path / "sel.txt"
+    sel.write_text("alltoall 4 2 1024 bruck\n")
+    cases = [([{}, {k: v}], "mismatch") for k, v in (
+        ("MPXA_NO_LL", "1"),                  # eager protocol on one process only
+        ("MPXA_LL_MAX", "4096"),
+        ("MPXA_ROW_SIGNAL", "0"),
+        ("MPXA_HIER_STAGED", "1"),
+        ("MPXA_ALGO", "alltoall:bruck"),
+        ("MPXA_NO_SMALL", "1"),
+        ("MPXA_SELECTOR", str(sel)))]
+    same = {"MPXA_NO_LL": "1", "MPXA_SELECTOR": str(sel)}
+    cases += [([same, dict(same)], "ok"), ([{}, {}], "ok")]
+    spawn(functools.partial(_knob_body, cases=cases))
