@@ -38,6 +38,8 @@ BASELINE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
 METRIC = BASELINE["metric"]
 P_RANKS = 8
 DEFAULT_BYTES = 64 << 20
+NVL_NOMINAL = 900.0     # GB/s per direction per GPU, NVLink 5 through NVSwitch (north_star roofline)
+NVL_MEASURED = 770.0    # GB/s measured peer copy per direction (B200_PROFILING.md), reported beside it
 
 
 def load_peaks():
@@ -330,7 +332,7 @@ def _configs_on_one_gpu(torch, gstream, reps):
         Rc = int(max(1, (rd + rc).max())) * 8
         d_s = torch.randint(0, 256, (p, S), dtype=torch.uint8, device=dev)
         d_r = torch.full((p, Rc), 0xA5, dtype=torch.uint8, device=dev)
-        req = c.alltoallv_init(d_s, sc, sd, d_r, rc, rd, dtype_size=8)
+        req = c.alltoallv_init(d_s, sc, sd, d_r, rc, rd, dtype_size=8, algo="pairwise")
         req.start(gstream); req.wait(gstream)
         torch.cuda.synchronize()
         want = oracle.alltoallv_definition(d_s.cpu().numpy(), sc, sd, rc, rd, 8,
@@ -362,18 +364,19 @@ def _configs_on_one_gpu(torch, gstream, reps):
         torch.cuda.synchronize()
         us_o = e0.elapsed_time(e1) * 1e3 / 20
         req.free()
-        # the other alltoallv variants (persistent, graph-timed, verified): hierarchical with
-        # groups of 2 ranks and Bruck-v
+        # the other alltoallv variants (persistent, graph-timed, verified): Bruck-v and the
+        # hierarchical variant on this comm (group = the GPU), and hierarchical with groups of
+        # 2 ranks
         others = {}
         cg = Comm(ranks_per_proc=p, device=torch.cuda.current_device(), group_size=2)
-        for algo in ("hier", "bruck"):
+        for name, cc, algo in (("bruck", c, "bruck"), ("hier", c, "hier"), ("hier_g2", cg, "hier")):
             d_r.fill_(0xA5)
-            rq = cg.alltoallv_init(d_s, sc, sd, d_r, rc, rd, dtype_size=8, algo=algo)
+            rq = cc.alltoallv_init(d_s, sc, sd, d_r, rc, rd, dtype_size=8, algo=algo)
             rq.start(gstream); rq.wait(gstream)
             torch.cuda.synchronize()
             ok_a = bool(np.array_equal(d_r.cpu().numpy(), want))
             us_a = 1e3 * time_graph(lambda: (rq.start(gstream), rq.wait(gstream)), 20, gstream)
-            others[algo] = {"persistent_graph_us": round(us_a, 3), "verified": ok_a}
+            others[name] = {"persistent_graph_us": round(us_a, 3), "verified": ok_a}
             rq.free()
         cg.finalize()
         out[f"mean_{mean}B"] = {"bytes_moved": moved, "verified": ok,
@@ -382,7 +385,12 @@ def _configs_on_one_gpu(torch, gstream, reps):
                                 "one_shot_us": round(us_o, 3),
                                 "GBps_persistent": round(moved / us_p / 1e3, 2),
                                 "hbm_TBps_persistent_graph": round(2 * moved / us_g / 1e6, 3),
-                                "other_variants": others}
+                                "roofline_frac_hbm": round(2 * moved / us_g / 1e6 / (load_peaks()[0] / 1e3), 4),
+                                "other_variants": others,
+                                # the selector's inputs: same comm (group = GPU), graph-timed
+                                "variants_graph_us": {"pairwise": round(us_g, 3),
+                                                      "bruck": others["bruck"]["persistent_graph_us"],
+                                                      "hier": others["hier"]["persistent_graph_us"]}}
         del d_s, d_r
     res["cfg4_alltoallv_p8_persistent_100x"] = out
     c.finalize()
@@ -534,41 +542,336 @@ def f1_neighbor(Comm, torch, dev, gstream, time_graph, m_own, k_need, contiguous
     return out
 
 
-def write_selector(sw, path, p, R):
-    """Measured selector table: for each op and size, the fastest variant (ties -> SPEC default)."""
-    lines = ["# op p ranks_per_proc max_bytes algo  (generated by bench.py --write-selector)"]
-    for op in ("allgather", "alltoall"):
-        variants = {k: v for k, v in sw[op].items() if not k.startswith("torch")}
-        sizes = [row[0] for row in next(iter(variants.values()))]
-        best_prev = None
-        for i, b in enumerate(sizes):
-            # a non-default variant must beat pairwise by > 3 % (measurement noise), else the
-            # SPEC default stays (SURVEY.md Q18)
-            best = min(variants, key=lambda a: variants[a][i][1])
-            if best != "pairwise" and variants[best][i][1] > 0.97 * variants["pairwise"][i][1]:
-                best = "pairwise"
-            if best_prev is not None and best != best_prev[0]:
-                lines.append(f"{op} {p} {R} {best_prev[1]} {best_prev[0]}")
-            best_prev = (best, b)
-        lines.append(f"{op} {p} {R} 18446744073709551615 {best_prev[0]}")
-    open(path, "w").write("\n".join(lines) + "\n")
+def selector_rows(op, p, R, G, g, variants, default="pairwise"):
+    """Selector lines for one measured (op, p, R, G, g): variants = {algo: [(bytes, us), ...]}
+    over the same sizes.  Per size the fastest variant wins; a non-default one must beat the
+    SPEC default by > 3 % (measurement noise; ties -> default).  Consecutive
+    sizes with the same winner merge; a row covers sizes up to its last measured size, the
+    last row everything above."""
+    if not variants or default not in variants:
+        return []
+    sizes = [b for b, _ in variants[default]]
+    best_of = []
+    for i, b in enumerate(sizes):
+        t = {a: rows[i][1] for a, rows in variants.items() if i < len(rows) and rows[i][0] == b}
+        best = min(t, key=t.get)
+        if best != default and t[best] > 0.97 * t[default]:
+            best = default
+        best_of.append(best)
+    lines = []
+    for i, b in enumerate(sizes):
+        if i + 1 < len(sizes) and best_of[i + 1] == best_of[i]:
+            continue
+        mb = b if i + 1 < len(sizes) else 18446744073709551615
+        lines.append(f"{op} {p} {R} {G} {g} {mb} {best_of[i]}")
+    return lines
+
+
+def measured_selector(sw, cfgs, p, R, g, nccl_sweep=None, N=1):
+    """Every (op, p, R, G, g) this bench run measured -> selector lines."""
+    def rows(v):
+        return [(r[0], r[1]) for r in v if isinstance(r, list)]
+    out = []
+    if sw:
+        for op in ("allgather", "alltoall"):
+            out += selector_rows(op, p, R, 1, g, {a: rows(v) for a, v in sw[op].items() if not a.startswith("torch")})
+    if cfgs:
+        for pp in (2, 4):
+            k = f"cfg3_alltoall_p{pp}"
+            if k in cfgs:
+                out += selector_rows("alltoall", pp, pp, 1, 2, {a: rows(v) for a, v in cfgs[k].items()})
+        for k, G in (("cfg5_alltoall_p32_1gpu", 1), ("cfg5_alltoall_p32_8_emulated_gpus", 8)):
+            if k in cfgs:   # (emulated: one process hosts all 32 ranks, R = 32)
+                out += selector_rows("alltoall", 32, 32, G, 4,
+                                     {a: rows(v) for a, v in cfgs[k].items() if a != "hier_staged"})
+        c4 = cfgs.get("cfg4_alltoallv_p8_persistent_100x")
+        if c4:
+            var = {}
+            for key, d in sorted(c4.items(), key=lambda kv: int(kv[0].split("_")[1][:-1])):
+                mean = int(key.split("_")[1][:-1])
+                for a, us in d.get("variants_graph_us", {}).items():
+                    var.setdefault(a, []).append((mean, us))
+            out += selector_rows("alltoallv", 8, 8, 1, 8, var)
+    if nccl_sweep:
+        for op in ("alltoall", "allgather"):
+            var = {}
+            for r in nccl_sweep[op]:
+                for a, us in r[7].items():
+                    var.setdefault(a, []).append((r[0], us))
+            out += selector_rows(op, N, 1, N, 1, var)
+    return out
+
+
+def write_selector(lines, path):
+    """Merge measured lines into the table at path: rows of every (op, p, R, G, g) measured
+    now replace that key's old rows; other keys' rows are kept."""
+    keys = {tuple(ln.split()[:5]) for ln in lines}
+    old = []
+    if os.path.exists(path):
+        for ln in open(path):
+            s = ln.split("#")[0].split()
+            if len(s) == 7 and tuple(s[:5]) not in keys:
+                old.append(" ".join(s))
+    hdr = ["# op p ranks_per_proc gpus group_size max_bytes algo",
+           "# measured on B200 by bench.py --write-selector (device us per call; ties -> pairwise, SURVEY Q18)"]
+    def key(ln):        # first matching line wins: rows of a key in increasing max_bytes
+        s = ln.split()
+        return (s[0], int(s[1]), int(s[2]), int(s[3]), int(s[4]), int(s[5]))
+    open(path, "w").write("\n".join(hdr + sorted(old + lines, key=key)) + "\n")
+
+
+def host_info():
+    """CPU model and core counts of the host the oracle runs on."""
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        aff = os.cpu_count()
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(), "affinity_cores": aff}
 
 
 def cpu_oracle_sample(send_host: np.ndarray, budget_s: float):
-    """Time the oracle's allgather (direct variant, as the GPU's selector chose) on host cores."""
+    """The oracle on the host cores, on the full workload: (1) its direct-variant simulation
+    (transport envelopes, single thread) and (2) its allgather definition with the receiving
+    ranks split over min(p, affinity cores) threads.  value / cores = the threaded run."""
     import oracle
     p, b = send_host.shape
-    t0 = time.perf_counter()
-    oracle.allgather(send_host, "direct")
-    dt = time.perf_counter() - t0
-    reps = 1
-    while time.perf_counter() - t0 + dt < budget_s and reps < 50:
-        oracle.allgather(send_host, "direct")
-        reps += 1
-    total = time.perf_counter() - t0
-    return {"value": round(p * p * b * reps / total / 1e9, 3), "unit": "GB/s", "cores": 1, "kind": "oracle",
-            "sample": f"{reps} full step(s) of the workload (allgather p={p}, {b} B per rank, direct variant, "
-                      f"single-threaded C simulation incl. transport envelopes), {total:.1f} s"}
+    info = host_info()
+    T = max(1, min(p, info["affinity_cores"] or 1))
+
+    def timed(fn, budget):
+        t0 = time.perf_counter()
+        fn()
+        dt = time.perf_counter() - t0
+        reps = 1
+        while time.perf_counter() - t0 + dt < budget and reps < 50:
+            fn()
+            reps += 1
+        return reps, time.perf_counter() - t0
+
+    reps1, tot1 = timed(lambda: oracle.allgather(send_host, "direct"), budget_s / 2)
+    recv = np.empty((p, p * b), dtype=np.uint8)
+    repsT, totT = timed(lambda: oracle.allgather_definition_threaded(send_host, T, recv), budget_s / 2)
+    single = round(p * p * b * reps1 / tot1 / 1e9, 3)
+    threaded = round(p * p * b * repsT / totT / 1e9, 3)
+    return {"value": threaded, "unit": "GB/s", "cores": T, "kind": "oracle",
+            "sample": f"{repsT} full step(s) of the workload (allgather p={p}, {b} B per rank): the oracle's "
+                      f"definition, receiving ranks split over {T} host threads, {totT:.1f} s",
+            "single_thread": {"value": single, "unit": "GB/s", "cores": 1,
+                              "sample": f"{reps1} full step(s), direct-variant transport simulation, {tot1:.1f} s"},
+            **info}
+
+
+# ---------------------------------------------------------------------------------------
+# N > 1: NCCL init evidence, sampled oracle checks, NCCL (B1) baseline and per-size sweep
+# ---------------------------------------------------------------------------------------
+def nccl_debug_to_file():
+    """NCCL init lines (NCCL_DEBUG=INFO, INIT + NVLS subsystems) go to a per-process file, not
+    stdout (rank 0's stdout carries exactly one JSON line); nccl_init_lines() reads them back.
+    Called first thing in main(), before torch (and with it NCCL) is loaded."""
+    os.environ["NCCL_DEBUG"] = "INFO"
+    os.environ["NCCL_DEBUG_SUBSYS"] = "INIT,NVLS"
+    os.environ["NCCL_DEBUG_FILE"] = f"/tmp/mpxa_bench_nccl.{os.getpid()}.log"
+
+
+def nccl_init_lines(ws):
+    """Every rank's NCCL 'Init COMPLETE' / NVLS lines, gathered to every rank (evidence of N ranks)."""
+    import torch.distributed as dist
+    lines = []
+    path = os.environ.get("NCCL_DEBUG_FILE", "").replace("%p", str(os.getpid()))
+    try:
+        for ln in open(path, errors="replace"):
+            if "Init COMPLETE" in ln or "NVLS" in ln or "nRanks" in ln:
+                lines.append(ln.strip()[:240])
+    except OSError:
+        pass
+    allv = [None] * ws
+    dist.all_gather_object(allv, lines[:4])
+    for r, lst in enumerate(allv):
+        for ln in lst or []:
+            print(f"[rank {r}] {ln}", file=sys.stderr)
+    return {"ranks_reporting": sum(1 for x in allv if x), "lines": [x for lst in allv for x in (lst or [])][:64]}
+
+
+def _sample_cols(n, k=1024, seed=0):
+    return np.unique(np.random.default_rng(seed).integers(0, max(1, n), min(k, max(1, n))))
+
+
+def check_allgather_sampled(send, recv, R, p, b, recv_rows=None):
+    """Every rank: sampled columns of the allgather result vs the oracle's definition over the
+    sampled columns of ALL ranks' contributions (gathered with a plain NCCL all_gather).
+    recv holds recv_rows (default R) rank rows of p*b bytes.  Returns the AND over ranks."""
+    import torch
+    import torch.distributed as dist
+    import oracle
+    cols = torch.from_numpy(_sample_cols(b)).cuda()
+    mine = send[:, cols].contiguous()                       # [R, nc]
+    allc = torch.empty((dist.get_world_size(), R, cols.numel()), dtype=torch.uint8, device="cuda")
+    dist.all_gather_into_tensor(allc, mine)
+    s = allc.view(p, -1).cpu().numpy()
+    want = oracle.allgather_definition(s)                   # [p, p * nc]
+    r0 = dist.get_rank() * R
+    rr = R if recv_rows is None else recv_rows
+    got = recv.view(rr, p, b)[:, :, cols].cpu().numpy().reshape(rr, -1)
+    ok = torch.tensor([int(np.array_equal(got, want[r0:r0 + rr]))], device="cuda")
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    return bool(ok.item())
+
+
+def check_alltoall_sampled(send, recv, R, p, b):
+    """alltoall recv_r[j] = send_j[r] on sampled byte columns of every block, all ranks."""
+    import torch
+    import torch.distributed as dist
+    import oracle
+    c = _sample_cols(b, 256)
+    idx = torch.from_numpy((np.arange(p)[:, None] * b + c[None, :]).reshape(-1)).cuda()
+    mine = send.view(R, p * b)[:, idx].contiguous()         # [R, p * nc]
+    allc = torch.empty((dist.get_world_size(), R, idx.numel()), dtype=torch.uint8, device="cuda")
+    dist.all_gather_into_tensor(allc, mine)
+    want = oracle.alltoall_definition(allc.view(p, -1).cpu().numpy())
+    r0 = dist.get_rank() * R
+    got = recv.view(R, p * b)[:, idx].cpu().numpy()
+    ok = torch.tensor([int(np.array_equal(got, want[r0:r0 + R]))], device="cuda")
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    return bool(ok.item())
+
+
+def _max_ranks(x):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _mpxa_us(fn, stream, small, iters):
+    """device us per call of an mpxa call: CUDA graph of `iters` calls (median of 5 replays)
+    at <= 4 KiB, else an eager loop between events; max over ranks."""
+    import torch
+    import torch.distributed as dist
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    dist.barrier()
+    if small:
+        us = 1e3 * time_graph(fn, iters, stream)
+    else:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(iters):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        us = 1e3 * e0.elapsed_time(e1) / iters
+    return _max_ranks(us)
+
+
+def multi_gpu_nccl(args, comm, send, recv, R, p, b, ms, total_recv, stream, local):
+    """(1) the headline config through NCCL B1 (ncclAllGather of this GPU's R*b bytes: the
+    on-GPU replication to R hosted ranks that mpxa performs is EXCLUDED from NCCL's time, in
+    NCCL's favour); (2) per-size sweep at p = N ranks, one per GPU: alltoall 4 B..16 MiB (x4)
+    and allgather 4 B..64 MiB (x2), every mpxa variant vs NCCL, with the roofline fraction
+    at 900 GB/s; outputs of the largest points checked against the oracle (sampled)."""
+    import torch
+    import torch.distributed as dist
+    from baseline import b1 as B1
+    from paper_2309_07337_b200 import Comm
+    B1.build()
+    N = dist.get_world_size()
+    nc = B1.NcclB1(dist.group.WORLD, local)
+    # everything below runs on one non-default stream (CUDA graphs cannot capture the legacy
+    # default stream), ordered after the headline's work
+    ss = torch.cuda.Stream()
+    ss.wait_stream(stream)
+    with torch.cuda.stream(ss):
+        res = _multi_gpu_nccl(args, comm, send, recv, R, p, b, ms, total_recv, ss, nc, B1, N)
+    stream.wait_stream(ss)
+    nc.finalize()
+    return res
+
+
+def _multi_gpu_nccl(args, comm, send, recv, R, p, b, ms, total_recv, stream, nc, B1, N):
+    import torch
+    import torch.distributed as dist
+    from paper_2309_07337_b200 import Comm
+    gathered = torch.empty((N, R * b), dtype=torch.uint8, device="cuda")
+    dist.barrier()
+    n_us = _max_ranks(nc.time("allgather", send, gathered, R * b, stream=stream, warmup=3,
+                              iters=max(3, min(args.steps, 20))))
+    # NCCL output == oracle (bit-exact, sampled columns of every rank's contribution)
+    nc.call("allgather", send, gathered, R * b, stream=stream)
+    torch.cuda.synchronize()
+    ok_n = check_allgather_sampled(send, gathered, R, p, b, recv_rows=1)
+    nccl = {"impl": f"B1: ncclAllGather from C++ (NCCL {B1.version()}), on-GPU replication to the "
+                    f"{R} hosted ranks excluded", "us_per_call": round(n_us, 2),
+            "value": round(total_recv / (n_us * 1e-6) / 1e9, 3), "unit": "GB/s",
+            "mpxa_us_per_call": round(ms * 1e3, 2), "verified_sampled_vs_oracle": ok_n}
+    if not args.sweep:
+        return nccl, None
+    # ---- sweep at p = N, R = 1 ----
+    c1 = Comm(ranks_per_proc=1, device=torch.cuda.current_device(), pg=dist.group.WORLD)
+    out = {"p": N, "ranks_per_gpu": 1,
+           "timing": "device us per call, max over ranks; CUDA graph of back-to-back calls (median of 5 "
+                     "replays) at <= 4 KiB, eager loop between events above; NCCL B1 from C++ the same way",
+           "roofline": "t_roof = max(NVLink (p-1)*b per GPU per direction / 900 GB/s, HBM / measured peak); "
+                       "frac = t_roof / t of the best variant",
+           "columns": ["bytes_per_block", "t_roof_us", "nccl_us", "best_mpxa_us", "best_variant", "frac_900",
+                       "speedup_vs_nccl", "us_by_variant"],
+           "alltoall": [], "allgather": []}
+    peak, _ = load_peaks()
+    bmax_a, bmax_g = 16 << 20, 64 << 20
+    a_send = torch.randint(0, 256, (1, N * bmax_a), dtype=torch.uint8, device="cuda")
+    a_recv = torch.empty_like(a_send)
+    g_send = torch.randint(0, 256, (1, bmax_g), dtype=torch.uint8, device="cuda")
+    g_recv = torch.empty((1, N * bmax_g), dtype=torch.uint8, device="cuda")
+    c1.register(a_recv)
+    c1.register(g_recv)
+    for op, sizes, variants in (("alltoall", [4 ** k for k in range(1, 13)], ("pairwise", "bruck")),
+                                ("allgather", [2 ** k for k in range(2, 27)], ("pairwise", "bruck", "ring"))):
+        for bb in sizes:
+            small = bb <= 4096
+            iters = 100 if small else (20 if bb < (4 << 20) else 5)
+            if op == "alltoall":
+                s_ = a_send.view(-1)[: N * bb].view(1, N * bb)
+                r_ = a_recv.view(-1)[: N * bb].view(1, N * bb)
+                hbm = 2 * N * bb
+            else:
+                s_ = g_send.view(-1)[:bb].view(1, bb)
+                r_ = g_recv.view(-1)[: N * bb].view(1, N * bb)
+                hbm = bb + N * bb
+            t_roof = 1e6 * max((N - 1) * bb / (NVL_NOMINAL * 1e9), hbm / (peak * 1e9))
+            byv = {}
+            for v in variants:
+                fn = (lambda v=v: comm_call(c1, op, s_, r_, v, stream))
+                byv[v] = round(_mpxa_us(fn, stream, small, iters), 3)
+            dist.barrier()
+            n_us = _max_ranks(nc.time(op, s_, r_, bb, stream=stream, warmup=5, iters=iters, graph=small))
+            best = min(byv, key=byv.get)
+            out[op].append([bb, round(t_roof, 3), round(n_us, 3), byv[best], best, round(t_roof / byv[best], 4),
+                            round(n_us / byv[best], 3), byv])
+        # oracle check of the largest point, default variant
+        comm_call(c1, op, s_, r_, None, stream)
+        torch.cuda.synchronize()
+        chk = check_alltoall_sampled if op == "alltoall" else check_allgather_sampled
+        out[f"{op}_largest_verified_sampled_vs_oracle"] = chk(s_, r_, 1, N, bb)
+    del a_send, a_recv, g_send, g_recv
+    c1.finalize()
+    return nccl, out
+
+
+def comm_call(c, op, s_, r_, algo, stream):
+    if op == "alltoall":
+        c.alltoall(s_, r_, algo=algo, stream=stream)
+    else:
+        c.allgather(s_, r_, algo=algo, stream=stream)
+
 
 
 def gpu_arm(args):
@@ -580,10 +883,21 @@ def gpu_arm(args):
     assert ws == N or (ws == 1 and N == 1), f"--gpus {N} but WORLD_SIZE={ws}"
     torch.cuda.set_device(local)
     pg = None
-    if ws > 1:
+    nccl_init = None
+    # --force-multi (testing aid): run the N > 1 code paths -- process group, NCCL B1, the
+    # p = N sweep, the sampled checks -- in a world of one process on one GPU
+    multi = ws > 1 or args.force_multi
+    if multi and ws == 1:
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(sk.getsockname()[1]), RANK="0", WORLD_SIZE="1")
+        sk.close()
+    if multi:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         pg = dist.group.WORLD
+        dist.barrier()
     p = P_RANKS
     if p % N:
         raise SystemExit(f"--gpus {N} must divide p={p}")
@@ -595,7 +909,7 @@ def gpu_arm(args):
     gen.manual_seed(1000 + rank)
     send = torch.randint(0, 256, (R, b), dtype=torch.uint8, device="cuda", generator=gen)
     recv = torch.empty((R, p * b), dtype=torch.uint8, device="cuda")
-    if ws > 1:
+    if multi:
         comm.register(recv)
     algo = comm.get_algorithm("allgather", b)
 
@@ -609,7 +923,7 @@ def gpu_arm(args):
     launches = comm.launch_count() - l0 - args.warmup
     # ---- parity spot check of the timed configuration (sampled columns, oracle) ----
     verified = None
-    if rank == 0 and ws == 1:
+    if rank == 0 and not multi:
         import oracle
         cols = torch.from_numpy(np.unique(np.random.default_rng(0).integers(0, b, 2048))).cuda()
         s = send[:, cols].cpu().numpy()
@@ -624,11 +938,22 @@ def gpu_arm(args):
     # hosted rank), the hierarchical variant once and replicates it in HBM
     hbm_bytes = R * b + R * p * b
     nvl_bytes = (p - R) * b
-    if ws == 1:
+    roof_extra = {}
+    if not multi:
         bound, alg_bytes, peak_use, peak_note = "hbm", hbm_bytes, peak, peak_src
     else:
-        bound, alg_bytes, peak_use, peak_note = ("nvlink", nvl_bytes, 770.0,
-                                                 "measured peer copy 770 GB/s/direction (B200_PROFILING.md); 900 nominal")
+        # north_star: t_roof = the slower of (NVLink bytes per GPU per direction / 900 GB/s) and
+        # (local HBM bytes / HBM peak); the measured 770 GB/s peer copy is reported beside it
+        t_nvl, t_hbm = nvl_bytes / (NVL_NOMINAL * 1e9), hbm_bytes / (peak * 1e9)
+        if t_nvl >= t_hbm:
+            bound, alg_bytes, peak_use, peak_note = ("nvlink", nvl_bytes, NVL_NOMINAL,
+                                                     "NVLink 5 nominal 900 GB/s per direction per GPU (north_star)")
+        else:
+            bound, alg_bytes, peak_use, peak_note = "hbm", hbm_bytes, peak, peak_src
+        roof_extra = {"nvlink_bytes_per_gpu": nvl_bytes, "hbm_bytes_per_gpu": hbm_bytes,
+                      "t_roof_us": round(1e6 * max(t_nvl, t_hbm), 3),
+                      "nvlink_GBps_achieved": round(nvl_bytes / (ms * 1e-3) / 1e9, 1),
+                      "frac_vs_measured_peer_copy_770": round(nvl_bytes / (ms * 1e-3) / 1e9 / NVL_MEASURED, 4)}
     achieved = alg_bytes / (ms * 1e-3) / 1e9
     # ---- e2e through host buffers (pinned), same metric ----
     e2e = None
@@ -642,7 +967,7 @@ def gpu_arm(args):
         streams = [stream, torch.cuda.Stream()]
         sends = [send, torch.empty_like(send)]
         recvs = [recv, torch.empty_like(recv)]
-        if ws > 1:
+        if multi:
             comm.register(recvs[1])      # peers write into it directly (multi-process mode)
         h_recvs = [torch.empty((R, p * b), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
         kev = [torch.cuda.Event(), torch.cuda.Event()]
@@ -679,60 +1004,21 @@ def gpu_arm(args):
                "h2d_bytes_per_step": R * b, "d2h_bytes_per_step": R * p * b, "ms_per_step": round(e_ms, 4),
                "pipelining": "two buffer sets / streams: step i+1's H2D + collective overlap step i's D2H"}
         del sends[1], recvs[1], h_recvs
-    # ---- NCCL baseline on the same buffers (N > 1 only; NCCL needs one rank per GPU) ----
-    nccl = None
-    if ws > 1:
-        import torch.distributed as dist
-        gathered = torch.empty((N, R * b), dtype=torch.uint8, device="cuda")
-
-        def nccl_step():
-            dist.all_gather_into_tensor(gathered, send.view(-1))
-            if R > 1:   # every hosted rank needs the full concatenation (rank-major layout)
-                recv.view(R, p * b).copy_(gathered.view(1, p * b).expand(R, p * b))
-            else:
-                recv.view(-1).copy_(gathered.view(-1))
-
-        n_ms = time_loop(nccl_step, max(3, min(args.steps, 20)), 3, stream, ws)
-        nccl = {"impl": "torch.distributed all_gather_into_tensor (NCCL %s) + local replication" %
-                        ".".join(map(str, torch.cuda.nccl.version())),
-                "ms_per_step": round(n_ms, 5), "value": round(total_recv / (n_ms * 1e-3) / 1e9, 3), "unit": "GB/s"}
-    # ---- multi-GPU sweep vs NCCL (N > 1): alltoall (one rank per GPU: NCCL all_to_all_single
-    #      has the same semantics) and allgather (process-level all_gather + replication) ----
-    nccl_sweep = None
-    if ws > 1 and args.sweep:
-        import torch.distributed as dist
-        nccl_sweep = {"timing": "eager loops, CUDA events, max over ranks; us per call",
-                      "columns": ["bytes_per_block", "mpxa_us", "nccl_us"], "alltoall": [], "allgather": []}
-        bmax = 16 << 20
-        a_send = torch.randint(0, 256, (R, p * bmax), dtype=torch.uint8, device="cuda")
-        a_recv = torch.empty_like(a_send)
-        comm.register(a_recv)
-        for bb in (4096, 65536, 1 << 20, 16 << 20):
-            it = 20 if bb < (1 << 20) else 5
-            if R == 1:
-                s_ = a_send.view(-1)[: p * bb].view(1, p * bb)
-                r_ = a_recv.view(-1)[: p * bb].view(1, p * bb)
-                m_ms = time_loop(lambda: comm.alltoall(s_, r_, algo="pairwise", stream=stream), it, 3, stream, ws)
-                n_ms = time_loop(lambda: dist.all_to_all_single(r_.view(-1), s_.view(-1)), it, 3, stream, ws)
-                nccl_sweep["alltoall"].append([bb, round(m_ms * 1e3, 2), round(n_ms * 1e3, 2)])
-            s2 = a_send.view(-1)[: R * bb].view(R, bb)
-            r2 = a_recv.view(-1)[: R * p * bb].view(R, p * bb)
-            g2 = torch.empty((N, R * bb), dtype=torch.uint8, device="cuda")
-
-            def ag_nccl():
-                dist.all_gather_into_tensor(g2, s2.view(-1))
-                r2.copy_(g2.view(1, p * bb).expand(R, p * bb))
-            m_ms = time_loop(lambda: comm.allgather(s2, r2, algo="pairwise", stream=stream), it, 3, stream, ws)
-            n_ms = time_loop(ag_nccl, it, 3, stream, ws)
-            nccl_sweep["allgather"].append([bb, round(m_ms * 1e3, 2), round(n_ms * 1e3, 2)])
-        del a_send, a_recv
+    # ---- N > 1: the same config through NCCL (B1, C++), a per-size sweep at p = N, R = 1
+    #      (mpxa vs NCCL), and a sampled oracle check of the headline on every rank ----
+    nccl = nccl_sweep = None
+    if multi:
+        verified = check_allgather_sampled(send, recv, R, p, b)
+        nccl, nccl_sweep = multi_gpu_nccl(args, comm, send, recv, R, p, b, ms, total_recv, stream, local)
     sw = None
     cfgs = None
-    if args.sweep and ws == 1:
+    if args.sweep and not multi:
         sw = sweep(comm, torch, stream)
-        if args.write_selector:
-            write_selector(sw, args.write_selector, p, R)
         cfgs = configs_on_one_gpu(torch)
+    if args.write_selector and rank == 0:
+        write_selector(measured_selector(sw, cfgs, p, R, comm.g, nccl_sweep, N), args.write_selector)
+    if multi:
+        nccl_init = nccl_init_lines(max(ws, 1))
     cpu = None
     if rank == 0 and not args.no_cpu:
         cpu = cpu_oracle_sample(send.cpu().numpy(), args.cpu_budget) if ws == 1 else None
@@ -754,8 +1040,9 @@ def gpu_arm(args):
                          "frac": round(achieved / peak_use, 4), "traffic": None,
                          "peak_source": peak_note,
                          "algorithmic_bytes_per_launch": alg_bytes,
-                         "kernel": "mpxa_exec_kernel (one launch per step; CUDA events on its stream)"},
+                         "kernel": "mpxa_exec_kernel (one launch per step; CUDA events on its stream)", **roof_extra},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "nccl": nccl, "nccl_sweep": nccl_sweep,
+            "nccl_init": nccl_init,
             "clocks": clk.report(), "sweep": sw, "configs": cfgs,
         }
         if args.traffic is not None:
@@ -769,7 +1056,7 @@ def gpu_arm(args):
                     line["roofline"]["traffic"] = t["bytes"]
                     line["roofline"]["traffic_source"] = t["source"]
         print(json.dumps(line))
-    if ws > 1:
+    if multi:
         import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()
@@ -817,6 +1104,46 @@ def reference_arm(args):
     }))
 
 
+def self_launch(args):
+    """`python bench.py --gpus N` without a torchrun environment: launch N ranks on this node
+    (torch.distributed.run, rendezvous on 127.0.0.1) running this same command line; rank 0's
+    JSON line is this process's output."""
+    import socket
+    import subprocess
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "4")
+    sys.exit(subprocess.call(cmd, env=env))
+
+
+def dry_run(args):
+    """Launcher / plumbing check without a GPU (CPU tests): N ranks over gloo, the same
+    barrier + max-over-ranks + rank-0-prints-one-line path as the GPU arm, no kernels."""
+    import torch
+    import torch.distributed as dist
+    ws, rank, _ = dist_env()
+    if ws > 1:
+        dist.init_process_group("gloo")
+    t = torch.tensor([1.0 + rank], dtype=torch.float64)
+    seen = torch.tensor([1], dtype=torch.int64)
+    if ws > 1:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(seen)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "metric": METRIC, "value": None, "unit": "GB/s", "n_gpus": args.gpus,
+                          "world_size": ws, "ranks_seen": int(seen.item()), "max_over_ranks": float(t.item()),
+                          "steps": args.steps, "warmup": args.warmup}))
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -830,10 +1157,19 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--write-selector", default=None)
     ap.add_argument("--traffic", type=float, default=None, help="ncu dram bytes per launch, if captured")
+    ap.add_argument("--dry-run", action="store_true", help="launcher / rank plumbing only (no GPU)")
+    ap.add_argument("--force-multi", action="store_true",
+                    help="testing aid: exercise the N > 1 code paths in a world of one process")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        self_launch(args)
+    if (args.gpus > 1 or args.force_multi) and not args.dry_run and args.impl != "reference":
+        nccl_debug_to_file()
+    if args.dry_run:
+        dry_run(args)
+    elif args.impl == "reference":
         reference_arm(args)
     else:
         gpu_arm(args)

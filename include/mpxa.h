@@ -298,8 +298,17 @@ int mpxa_psend_device(mpxa_request_t req, void *handle_out, size_t handle_bytes)
 int mpxa_set_algorithm(mpxa_comm_t comm, mpxa_op_t op, mpxa_algo_t algo); /* DEFAULT = selector */
 int mpxa_get_algorithm(mpxa_comm_t comm, mpxa_op_t op, size_t bytes, mpxa_algo_t *chosen);
 int mpxa_list_algorithms(mpxa_op_t op, mpxa_algo_t *out, int *n);  /* *n in: capacity; out: count */
-/* Load a selector table: lines "op p ranks_per_proc max_bytes algo" (text, '#' comments);
- * for each (op, p, R) the first line with bytes <= max_bytes wins. */
+/* Load a selector table (text, '#' comments), lines
+ *     "op p ranks_per_proc gpus group_size max_bytes algo"   (or "op p ranks_per_proc max_bytes
+ *     algo": any GPU count and group size),
+ * op in {alltoall, alltoallv, allgather}, algo in {pairwise, bruck, hier, ring}.  For a call
+ * the first line matching (op, p, R, G, g) with bytes <= max_bytes wins; bytes is the block /
+ * contribution size, for alltoallv the mean pair segment of the global count matrix.  The
+ * default algorithm is: mpxa_set_algorithm override > table > built-in fallback rules
+ * (pairwise; hierarchical allgather across GPUs with several ranks per GPU beyond the eager
+ * range).  Replaces the comm's table; MPXA_ERR_ARG on an unreadable file or a bad line.
+ * Tables shipped: selector_b200.txt next to libmpxa.so (measured by bench.py --write-selector),
+ * loaded at mpxa_init unless $MPXA_SELECTOR names another. */
 int mpxa_load_selector(mpxa_comm_t comm, const char *path);
 /* 64-bit digest of everything that chooses a launch's protocol, path or grid on the host:
  * every tuning knob, the selector table, forced variants (MPXA_ALGO) and the

@@ -49,6 +49,7 @@ def lib():
         sig = {
             "orc_alltoall_definition": [I, Z, P, P],
             "orc_allgather_definition": [I, Z, P, P],
+            "orc_allgather_definition_rows": [I, Z, P, P, I, I],
             "orc_alltoallv_definition": [I, Z, P, Z, P, P, P, Z, P, P],
             "orc_alltoallv_pairwise": [I, Z, P, Z, P, P, P, Z, P, P, S],
             "orc_alltoall_pairwise": [I, Z, P, P, S],
@@ -105,6 +106,26 @@ def allgather_definition(send: np.ndarray) -> np.ndarray:
     p, blk = send.shape
     recv = np.zeros((p, p * blk), dtype=np.uint8)
     _check(lib().orc_allgather_definition(p, blk, _ptr(send), _ptr(recv)), "allgather_definition")
+    return recv
+
+
+def allgather_definition_threaded(send: np.ndarray, nthreads: int, recv: np.ndarray = None) -> np.ndarray:
+    """allgather_definition with the receiving ranks split over `nthreads` host threads, each
+    calling orc_allgather_definition_rows on its own rows (ctypes releases the GIL during
+    the call, so the threads run concurrently).  Timing aid for the host baseline."""
+    from concurrent.futures import ThreadPoolExecutor
+    send = _u8(send)
+    p, blk = send.shape
+    if recv is None:
+        recv = np.zeros((p, p * blk), dtype=np.uint8)
+    T = max(1, min(int(nthreads), p))
+    bounds = [(p * t // T, p * (t + 1) // T) for t in range(T)]
+    L = lib()
+    with ThreadPoolExecutor(T) as ex:
+        rcs = list(ex.map(lambda b: L.orc_allgather_definition_rows(p, blk, _ptr(send), _ptr(recv), b[0], b[1]),
+                          bounds))
+    for rc in rcs:
+        _check(rc, "allgather_definition_rows")
     return recv
 
 

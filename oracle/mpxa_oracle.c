@@ -167,6 +167,18 @@ int orc_allgather_definition(int p, size_t blk, const unsigned char *send, unsig
     return 0;
 }
 
+/* The same definition restricted to receiving ranks [r0, r1) -- so several host threads can
+ * each fill their own receivers ("one thread per simulated rank");
+ * the per-block copies are exactly orc_allgather_definition's. */
+int orc_allgather_definition_rows(int p, size_t blk, const unsigned char *send, unsigned char *recv, int r0,
+                                  int r1) {
+    if (p < 1 || r0 < 0 || r1 > p || r0 > r1) return -1;
+    for (int r = r0; r < r1; r++)
+        for (int j = 0; j < p; j++)
+            if (blk) memcpy(recv + ((size_t)r * p + j) * blk, send + (size_t)j * blk, blk);
+    return 0;
+}
+
 /* Checks of the MPI alltoallv argument contract: non-negative counts,
  * in-bounds regions, sendcounts_j[r] == recvcounts_r[j]. */
 static int v_args_ok(int p, size_t w, size_t sstride, const int64_t *sc, const int64_t *sd,

@@ -176,6 +176,7 @@ struct Window {
 
 struct SelEntry {
     int op, p, R;
+    int G, g;            // GPUs of the comm and its group size (-1: any -- 5-field lines)
     uint64_t max_bytes;
     int algo;
 };
@@ -230,6 +231,8 @@ struct mpxa_comm_s {
     bool force_exec = false;                  // MPXA_NO_SMALL=1: never use the small-message kernel
     bool pdl = true;                          // MPXA_NO_PDL=1: launches without programmatic serialization
     bool dyn = true;                          // MPXA_NO_DYN=1: static slices only (no work queue)
+    int wring = 1;                            // warp-ring dynamic mode: 1 when moves may be misaligned,
+                                              // MPXA_NO_WRING=1: never (LSU-register path), MPXA_WRING=2: always
     int dyn_pieces = (int)kDynPiecesPerCta;   // MPXA_DYN_PIECES: queue pieces per CTA (tuning)
     uint64_t dyn_min_total = kDynMinTotal;    // MPXA_DYN_MIN: smallest busiest-GPU volume (tuning)
     int force_sync = -1;                      // MPXA_DYN_SYNC=0/1: force multi-step dynamic mode (tuning)
@@ -437,8 +440,12 @@ int ensure_work(mpxa_comm_t c, size_t need_per_gpu) {
 // ---- selector -------------------------------------------------------------------------
 int default_algo(mpxa_comm_t c, int op, size_t bytes) {
     if (c->user_algo[op]) return c->user_algo[op];
+    // the measured table first (bench.py --write-selector); the rules below are fallbacks for
+    // configurations no table row covers -- they were NOT measured on NVLink
     for (const SelEntry &e : c->selector)
-        if (e.op == op && e.p == c->p && e.R == c->R && bytes <= e.max_bytes) return e.algo;
+        if (e.op == op && e.p == c->p && e.R == c->R && (e.G < 0 || e.G == c->G) && (e.g < 0 || e.g == c->g) &&
+            bytes <= e.max_bytes)
+            return e.algo;
     // SPEC.md:256 defaults when nothing was measured: pairwise (alltoall/v: its flags are
     // already one per GPU pair and CTA, so the hierarchical variant's fewer messages buy
     // nothing here).  Allgather: the direct (pairwise) exchange -- except across GPUs with
@@ -992,6 +999,18 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
             if (!E.dyn_units) E.d0_base = -1;
             E.dyn_sync = 1;
         }
+        // warp-ring dynamic mode: when some moves may not be 16-B congruent, every warp streams
+        // its own pieces through a TMA ring -- congruent ones with bulk stores, the others with
+        // 16-B stores the warp shifts out of shared memory (kernels.cu dyn_tile_w; measured,
+        // cfg4 mean 4 MiB int64: 96.9 / 103.1 / 106.6 -> 92.3 / 87.2 / 100.6 us, seeds 0-2)
+        if (E.dyn_units && c->wring &&
+            (c->wring == 2 || unit % 16 ||
+             ((uintptr_t)send | (uintptr_t)recv | send_stride | recv_stride | E.work_stride) % 16)) {
+            E.wring = 1;
+            E.chunk = kWChunk;
+            E.stages = kWarpsExec * kWStages;   // dynamic smem = stages x chunk (every warp's ring)
+            E.ahead = 0;
+        }
         e = launch_exec(E, nC, c->emulated ? c->G : 1, c->emulated, pdl && c->pdl, stream);
     }
     if (e != cudaSuccess) {
@@ -1002,7 +1021,7 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
     // execution path of this launch (tests assert the intended path ran: mpxa__last_launch)
     c->last_path = (small ? 1u : 0u) | (E.small_ll ? 2u : 0u) | (E.small_var ? 4u : 0u) |
                    (E.dyn_units ? 8u : 0u) | (E.dyn_sync ? 16u : 0u) | (E.small_own ? 32u : 0u) |
-                   (E.small_swork ? 64u : 0u);
+                   (E.small_swork ? 64u : 0u) | (E.wring ? 128u : 0u);
     return MPXA_SUCCESS;
 }
 
@@ -1369,6 +1388,8 @@ void read_knobs(mpxa_comm_t c) {
     if (const char *e = getenv("MPXA_NO_SMALL")) c->force_exec = atoi(e) != 0;
     if (const char *e = getenv("MPXA_NO_PDL")) c->pdl = atoi(e) == 0;
     if (const char *e = getenv("MPXA_NO_DYN")) c->dyn = atoi(e) == 0;
+    if (const char *e = getenv("MPXA_NO_WRING")) c->wring = atoi(e) == 0 ? 1 : 0;
+    if (const char *e = getenv("MPXA_WRING")) c->wring = atoi(e);
     if (const char *e = getenv("MPXA_DYN_PIECES")) c->dyn_pieces = std::max(1, atoi(e));
     if (const char *e = getenv("MPXA_DYN_MIN")) c->dyn_min_total = strtoull(e, nullptr, 10);
     if (const char *e = getenv("MPXA_DYN_SYNC")) c->force_sync = atoi(e);
@@ -1416,7 +1437,7 @@ void read_knobs(mpxa_comm_t c) {
 // knob, the selector table, the forced variants and the initial heap size (heap growth is
 // a collective IPC exchange: the sizes must evolve identically on every process).
 uint64_t knob_digest(mpxa_comm_t c, size_t heap) {
-    const int64_t v[] = {c->force_ns, c->force_nf, c->force_big, c->force_exec, c->pdl, c->dyn, c->dyn_pieces,
+    const int64_t v[] = {c->force_ns, c->force_nf, c->force_big, c->force_exec, c->pdl, c->dyn, c->wring, c->dyn_pieces,
                          (int64_t)c->dyn_min_total, c->force_sync, c->small_sync, (int64_t)c->small_max1,
                          (int64_t)c->small_vol1, c->var_chop, c->var_tiles, c->swork, c->small_nt, c->ll,
                          (int64_t)c->one_cta_items, c->hier_staged, c->row_signal, c->ll_max, c->ll_max_ms,
@@ -1424,7 +1445,7 @@ uint64_t knob_digest(mpxa_comm_t c, size_t heap) {
                          (int64_t)c->selector.size()};
     uint64_t h = fnv(1469598103934665603ull, v, sizeof v);
     for (const SelEntry &e : c->selector) {
-        const int64_t r[] = {e.op, e.p, e.R, (int64_t)e.max_bytes, e.algo};
+        const int64_t r[] = {e.op, e.p, e.R, e.G, e.g, (int64_t)e.max_bytes, e.algo};
         h = fnv(h, r, sizeof r);
     }
     return h;
@@ -2182,10 +2203,20 @@ int load_selector_file(mpxa_comm_t c, const char *path) {
         auto h = line.find('#');
         if (h != std::string::npos) line = line.substr(0, h);
         std::stringstream ss(line);
-        std::string op, algo;
+        std::vector<std::string> tok;
+        for (std::string x; ss >> x;) tok.push_back(x);
+        if (tok.empty()) continue;
+        // "op p R max_bytes algo" (any GPU count / group) or "op p R G g max_bytes algo"
+        if (tok.size() != 5 && tok.size() != 7) return MPXA_ERR_ARG;
+        const bool full = tok.size() == 7;
+        const std::string &op = tok[0], &algo = tok.back();
         SelEntry e{};
-        unsigned long long mb = 0;
-        if (!(ss >> op >> e.p >> e.R >> mb >> algo)) continue;
+        char *endp = nullptr;
+        e.p = (int)strtol(tok[1].c_str(), &endp, 10);
+        e.R = (int)strtol(tok[2].c_str(), &endp, 10);
+        e.G = full ? (int)strtol(tok[3].c_str(), &endp, 10) : -1;
+        e.g = full ? (int)strtol(tok[4].c_str(), &endp, 10) : -1;
+        const unsigned long long mb = strtoull(tok[full ? 5 : 3].c_str(), &endp, 10);
         e.op = op == "alltoall" ? 0 : op == "alltoallv" ? 1 : op == "allgather" ? 2 : -1;
         e.algo = algo == "pairwise" ? 1 : algo == "bruck" ? 2 : algo == "hier" ? 3 : algo == "ring" ? 4 : 0;
         e.max_bytes = mb;
@@ -2288,7 +2319,7 @@ int mpxa_plan_moves(const void *plan, int gpu, mpxa_plan_move *out, int *n) {
 
 // undocumented test hook: the execution path of the comm's last collective launch, as bits
 // 1 small kernel, 2 eager (LL), 4 variable pieces, 8 dynamic work queues, 16 row-barrier
-// sync, 32 owned flows, 64 WORK in shared memory
+// sync, 32 owned flows, 64 WORK in shared memory, 128 warp-ring dynamic mode
 int mpxa__last_launch(mpxa_comm_t c, uint32_t *bits) {
     if (!c || !bits) return MPXA_ERR_ARG;
     *bits = c->last_path;

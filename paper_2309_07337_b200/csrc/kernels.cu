@@ -279,6 +279,20 @@ struct ExecShared {
     const char *msrc[kMoveTile];  //               resolved source of each move
     uint64_t mdst[kMoveTile];     //               destination address (fan-out: offset)
     uint64_t wsum[kThreads / 32];
+    // warp-ring mode: per-warp stage barriers and the descriptor of each stage's contents
+    uint64_t wmbar[kWarpsExec][kWStages];
+    struct WEntry {
+        const char *src;    // kind 0: 16-B aligned body source; kind 1: payload source
+        char *dst;          // kind 0 non-fanout / kind 1: destination
+        uint64_t doff;      // kind 0 fan-out: offset inside every rank's dst_kind buffer
+        uint32_t n;         // payload bytes
+        uint32_t lbytes;    // bytes loaded into the stage (16-B multiple)
+        uint16_t sh;        // kind 1: payload byte 0 sits at stage + sh
+        uint8_t kind;       // 0: bulk-store stage; 1: warp stores shifted out of the stage
+        uint8_t fanout, dst_kind;
+    } went[kWarpsExec][kWStages];
+    uint32_t wseq[kWarpsExec];   // loads issued on each warp's ring so far in this launch (stage
+                                 // index and mbarrier phase continue across tiles and steps)
 };
 
 __device__ __forceinline__ char *base_of(const ExecParams &P, const ExecShared &S, int kind, int rank) {
@@ -638,11 +652,12 @@ __device__ __forceinline__ MovePlan piece_plan(const ExecParams &P, const ExecSh
     return mp;
 }
 
-// One tile of at most kMoveTile moves (queues of tile ti).
-__device__ __noinline__ bool dyn_tile(const ExecParams &P, ExecShared &S, Producer &prod, int g, int first, int nm,
-                                      bool loaded, int ti) {
+// Load (unless prefetched) and classify one tile of moves: S.msrc / S.mdst resolved, and the
+// exclusive piece prefixes S.pcA (16-B congruent moves of >= kTmaMin bytes: the TMA queue)
+// and S.pcB (the rest), totals at index nm.
+__device__ __noinline__ void dyn_classify(const ExecParams &P, ExecShared &S, int g, int first, int nm, bool loaded) {
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const uint64_t U = (uint64_t)P.dyn_u, chunk = (uint64_t)P.chunk;
+    const uint64_t U = (uint64_t)P.dyn_u;
     if (!loaded) {   // moves not prefetched by the prologue (later tiles, or step 0 not dense)
         __syncthreads();   // everyone is done with the previous tile's moves
         if (t < nm) S.moves[t] = P.mode == 1 ? P.progs[g].moves[first + t] : P.prog.moves[first + t];
@@ -682,6 +697,14 @@ __device__ __noinline__ bool dyn_tile(const ExecParams &P, ExecShared &S, Produc
         S.pcB[kThreads] = (uint32_t)((wo + inc) >> 32);
     }
     __syncthreads();
+}
+
+// One tile of at most kMoveTile moves (queues of tile ti).
+__device__ __noinline__ bool dyn_tile(const ExecParams &P, ExecShared &S, Producer &prod, int g, int first, int nm,
+                                      bool loaded, int ti) {
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint64_t U = (uint64_t)P.dyn_u, chunk = (uint64_t)P.chunk;
+    dyn_classify(P, S, g, first, nm, loaded);
     const uint32_t totA = S.pcA[nm], totB = S.pcB[nm];
     bool wrote = false;
     if (t == 0) {
@@ -729,13 +752,201 @@ __device__ __noinline__ bool dyn_tile(const ExecParams &P, ExecShared &S, Produc
     return wrote;
 }
 
+// 16 bytes starting at byte d (0..15) of the 32-byte pair (a, b)
+__device__ __forceinline__ uint4 shift16(const uint4 &a, const uint4 &b, uint32_t d) {
+    uint32_t x0, x1, x2, x3, x4;
+    switch (d >> 2) {
+        case 0: x0 = a.x; x1 = a.y; x2 = a.z; x3 = a.w; x4 = b.x; break;
+        case 1: x0 = a.y; x1 = a.z; x2 = a.w; x3 = b.x; x4 = b.y; break;
+        case 2: x0 = a.z; x1 = a.w; x2 = b.x; x3 = b.y; x4 = b.z; break;
+        default: x0 = a.w; x1 = b.x; x2 = b.y; x3 = b.z; x4 = b.w; break;
+    }
+    const uint32_t r = 8u * (d & 3u);
+    if (!r) return make_uint4(x0, x1, x2, x3);
+    return make_uint4(__funnelshift_r(x0, x1, r), __funnelshift_r(x1, x2, r), __funnelshift_r(x2, x3, r),
+                      __funnelshift_r(x3, x4, r));
+}
+
+// The warp stores n payload bytes that sit at stage byte sh to dst: 16-B stores at the
+// destination's alignment, each assembled from two aligned 16-B shared-memory loads.
+__device__ __forceinline__ void wring_shift_store(const char *stage, uint32_t sh, char *dst, uint32_t n, int lane) {
+    uint32_t hd = (uint32_t)((16 - ((uintptr_t)dst & 15)) & 15);
+    if (hd > n) hd = n;
+    for (uint32_t i = lane; i < hd; i += 32) dst[i] = stage[sh + i];
+    const uint32_t nv = (n - hd) >> 4;
+    const uint32_t o0 = sh + hd, d = o0 & 15;
+    const uint4 *s4 = (const uint4 *)(stage + (o0 & ~15u));
+    uint4 *d4 = (uint4 *)(dst + hd);
+    if (d == 0) {
+        for (uint32_t v = lane; v < nv; v += 32) st16(d4 + v, s4[v]);
+    } else {
+        for (uint32_t v = lane; v < nv; v += 32) st16(d4 + v, shift16(s4[v], s4[v + 1], d));
+    }
+    for (uint32_t i = hd + nv * 16 + lane; i < n; i += 32) dst[i] = stage[sh + i];
+}
+
+// Warp-ring dynamic mode, one tile: the tile's pieces (TMA queue first, then the rest) are
+// taken from ONE work queue by the CTA's warps, each running its own pipeline: lane 0 keeps
+// up to kWStages - 2 TMA bulk loads in flight (16-B aligned spans) into the warp's ring; the
+// warp then drains the oldest stage -- a bulk store for a congruent piece, or 16-B stores
+// shifted out of shared memory by the whole warp for a piece whose source and destination
+// are not 16-B congruent (the LSU path's register-bound loads become TMA loads).  Pieces
+// shorter than kTmaMin, and shifted fan-out pieces, go through lsu_copy.
+__device__ __noinline__ bool dyn_tile_w(const ExecParams &P, ExecShared &S, int g, int first, int nm, bool loaded,
+                                        int ti) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint64_t U = (uint64_t)P.dyn_u;
+    dyn_classify(P, S, g, first, nm, loaded);
+    const uint32_t totA = S.pcA[nm], tot = totA + S.pcB[nm];
+    if (tot == 0) return false;
+    extern __shared__ __align__(128) char dyn_smem[];
+    char *ring = dyn_smem + (size_t)w * kWStages * kWChunk;
+    uint32_t *q = &P.dc->dyn_next[g * kMaxDynTiles + ti];
+    bool wrote = false;
+    const uint32_t base = S.wseq[w];   // ring position where this tile starts (all lanes)
+    // lane 0's producer state; the next piece index is requested while the current streams
+    uint32_t issued = 0, consumed = 0;
+    bool have = false, exhausted = false;
+    uint32_t nextu = lane == 0 ? atomicAdd(q, 1u) : 0u;
+    int mi = 0;
+    bool isA = false;
+    MovePlan mp;
+    uint64_t off = 0, end = 0;
+    int lsu_mi = -1;             // a piece for lsu_copy by the whole warp (broadcast)
+    uint64_t lsu_lo = 0;
+    for (;;) {
+        if (lane == 0) {
+            // at most kWStages - 2 loads in flight: the two stages behind them are draining
+            // their bulk stores, so re-arming a stage rarely waits for one
+            while (!exhausted && lsu_mi < 0 && issued - consumed < (uint32_t)(kWStages - 2)) {
+                if (!have) {
+                    const uint32_t u = nextu;
+                    if (u >= tot) { exhausted = true; break; }
+                    nextu = atomicAdd(q, 1u);
+                    isA = u < totA;
+                    const uint32_t *pc = isA ? S.pcA : S.pcB;
+                    const uint32_t uu = isA ? u : u - totA;
+                    mi = find_move(pc, nm, uu);
+                    const uint64_t lo = (uint64_t)(uu - pc[mi]) * U;
+                    mp = piece_plan(P, S, mi, lo, U);
+                    const Move &m = S.moves[mi];
+                    if (!isA && (mp.n < kTmaMin || m.fanout)) {   // warp lsu_copy, outside the ring
+                        lsu_mi = mi;
+                        lsu_lo = lo;
+                        break;
+                    }
+                    if (isA) {
+                        uint64_t head = (16 - ((uintptr_t)mp.src & 15)) & 15;
+                        if (head > mp.n) head = mp.n;
+                        const uint64_t body = (mp.n - head) & ~(uint64_t)15;
+                        if (head) { copy_edge(P, S, m, mp, 0, (uint32_t)head); wrote = true; }
+                        if (mp.n > head + body) {
+                            copy_edge(P, S, m, mp, head + body, (uint32_t)(mp.n - head - body));
+                            wrote = true;
+                        }
+                        off = head;
+                        end = head + body;
+                    } else {
+                        off = 0;
+                        end = mp.n;
+                    }
+                    have = off < end;
+                    if (!have) continue;
+                }
+                const uint32_t s = (base + issued) % (uint32_t)kWStages;
+                ExecShared::WEntry &e = S.went[w][s];
+                const Move &m = S.moves[mi];
+                uint64_t len;
+                const char *lsrc;
+                if (isA) {
+                    len = end - off < (uint64_t)kWChunk ? end - off : (uint64_t)kWChunk;
+                    lsrc = mp.src + off;
+                    e.kind = 0;
+                    e.src = lsrc;
+                    e.lbytes = (uint32_t)len;
+                    e.sh = 0;
+                    e.fanout = m.fanout;
+                    e.dst_kind = m.dst_kind;
+                    e.doff = mp.doff + off;
+                    e.dst = m.fanout ? nullptr : mp.dst + off;
+                } else {
+                    // chunks end at 16-B boundaries of the destination (except the piece's last)
+                    len = end - off < (uint64_t)(kWChunk - 32) ? end - off : (uint64_t)(kWChunk - 32);
+                    if (off + len < end) len -= ((uintptr_t)(mp.dst + off + len)) & 15;
+                    const uintptr_t s0 = (uintptr_t)(mp.src + off), a0 = s0 & ~(uintptr_t)15;
+                    lsrc = (const char *)a0;
+                    e.kind = 1;
+                    e.src = mp.src + off;
+                    e.lbytes = (uint32_t)(((s0 + len + 15) & ~(uintptr_t)15) - a0);
+                    e.sh = (uint16_t)(s0 - a0);
+                    e.fanout = 0;
+                    e.dst_kind = m.dst_kind;
+                    e.doff = 0;
+                    e.dst = mp.dst + off;
+                }
+                e.n = (uint32_t)len;
+                // the stage's previous contents: consumed, and its bulk store (if any) has
+                // read shared memory -- one bulk group was committed per consumed entry
+                if (issued >= (uint32_t)kWStages) bulk_wait_read((int)(consumed - 1 - (issued - kWStages)));
+                tma_load_1d(smem_u32(ring + (size_t)s * kWChunk), lsrc, e.lbytes, smem_u32(&S.wmbar[w][s]));
+                issued++;
+                off += len;
+                if (off >= end) have = false;
+            }
+        }
+        issued = __shfl_sync(0xffffffffu, issued, 0);
+        exhausted = __shfl_sync(0xffffffffu, exhausted, 0);
+        lsu_mi = __shfl_sync(0xffffffffu, lsu_mi, 0);
+        if (consumed == issued) {
+            if (lsu_mi >= 0) {           // ring drained: the pending lsu_copy piece, whole warp
+                lsu_lo = __shfl_sync(0xffffffffu, lsu_lo, 0);
+                const MovePlan lp = piece_plan(P, S, lsu_mi, lsu_lo, U);
+                lsu_copy(P, S, S.moves[lsu_mi], lp, 0, lp.n, lane, 32);
+                wrote = true;
+                lsu_mi = -1;
+                __syncwarp();
+                continue;
+            }
+            if (exhausted) break;
+            continue;
+        }
+        __syncwarp();   // lane 0's stage descriptor before every lane reads it
+        const uint32_t s = (base + consumed) % (uint32_t)kWStages;
+        mbar_wait(smem_u32(&S.wmbar[w][s]), ((base + consumed) / (uint32_t)kWStages) & 1u);
+        const ExecShared::WEntry &e = S.went[w][s];
+        const char *stage = ring + (size_t)s * kWChunk;
+        if (e.kind == 0) {
+            if (lane == 0) {
+                if (!e.fanout) {
+                    tma_store_1d(e.dst, smem_u32(stage), e.n);
+                } else {
+                    for (int j = 0; j < P.p; j++) tma_store_1d(base_of(P, S, e.dst_kind, j) + e.doff, smem_u32(stage), e.n);
+                }
+            }
+        } else {
+            wring_shift_store(stage, e.sh, e.dst, e.n, lane);
+            wrote = true;
+        }
+        __syncwarp();   // every lane's shared-memory reads of the stage are done
+        if (lane == 0) bulk_commit();
+        consumed++;
+    }
+    if (lane == 0) {
+        bulk_wait_all();   // this warp's bulk stores complete (the step end fences)
+        S.wseq[w] = base + issued;
+    }
+    __syncwarp();
+    return wrote;
+}
+
 // Dynamic mode over the whole step: move tiles in order, each with its own pair of queues; a
 // CTA moves on to the next tile as soon as the current tile's queues are dry (no barrier).
 __device__ __noinline__ bool dyn_step(const ExecParams &P, ExecShared &S, Producer &prod, int g, int first, int nm,
                                       bool loaded, int tile0) {
     bool wrote = false;
     for (int tile = 0, ti = tile0; tile < nm; tile += kMoveTile, ti++)
-        wrote |= dyn_tile(P, S, prod, g, first + tile, min(kMoveTile, nm - tile), loaded && tile == 0, ti);
+        wrote |= P.wring ? dyn_tile_w(P, S, g, first + tile, min(kMoveTile, nm - tile), loaded && tile == 0, ti)
+                         : dyn_tile(P, S, prod, g, first + tile, min(kMoveTile, nm - tile), loaded && tile == 0, ti);
     return wrote;
 }
 
@@ -824,7 +1035,12 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
         sym_r = P.dc->sym[t];
     }
     if (t == kThreads - 1) {    // a thread with no load outstanding (the fence is a release)
-        for (int s = 0; s < P.stages; s++) mbar_init(smem_u32(&S.mbar[s]), 1);
+        if (P.wring) {
+            for (int w = 0; w < kWarpsExec; w++)
+                for (int s = 0; s < kWStages; s++) mbar_init(smem_u32(&S.wmbar[w][s]), 1);
+        } else {
+            for (int s = 0; s < P.stages; s++) mbar_init(smem_u32(&S.mbar[s]), 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     TRACE(9);
@@ -861,6 +1077,7 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
         S.cts_ok = 0;
         S.abort_flag = 0;
     }
+    if (t < kWarpsExec) S.wseq[t] = 0;
     TRACE(10);
     __syncthreads();
     griddep_wait();

@@ -33,6 +33,13 @@ constexpr TmaConfig kTmaBig = {6, 32768, 4};
 constexpr int kMaxDynSmem = 6 * 32768;
 constexpr int kMoveTile = kThreads;   // moves staged in shared memory at a time (one per thread)
 constexpr int kMaxDynTiles = 64;      // dynamic mode: move tiles per step (queues per tile)
+// warp-ring dynamic mode (ExecParams::wring): every warp of the CTA is its own TMA pipeline
+// over a ring of kWStages stages of kWChunk bytes (same 96 KiB of dynamic shared memory as
+// the mid ring, so 2 CTAs / SM); moves that are not 16-B congruent are stored by the warp
+// with 16-B stores shifted out of shared memory instead of through LSU registers
+constexpr int kWarpsExec = kThreads / 32;
+constexpr int kWStages = 6;
+constexpr int kWChunk = 4096;
 constexpr uint64_t kSmallKernelMax = 8192;  // longest move (bytes) the small-message kernel takes
 constexpr int kSmallMovesSmem = 4096;       // program moves cached in shared memory by the small kernel
 enum { kSmallCommon = 0, kSmallVar = 1, kSmallLocal = 2, kSmallLL = 3 };   // small-kernel instantiations
@@ -175,7 +182,8 @@ struct ExecParams {
     int32_t small_ll;          // small kernel, eager (LL) companion program: moves to peer GPUs
                                // are word streams into their staging (BK_LL); each step lists
                                // its receive moves last (Step::wait_mask = their number)
-    int32_t pad7;
+    int32_t wring;             // dynamic mode with per-warp TMA rings (kWStages x kWChunk each);
+                               // stages / chunk then describe the whole dynamic smem
 };
 
 }  // namespace mpxa

@@ -263,6 +263,9 @@ class Comm:
                         ctx=None, heap_bytes=heap_bytes, timeout_s=timeout_s)
         _ck(_lib().mpxa_init(ctypes.byref(self.handle), ctypes.byref(args)), "init")
         self.R = ranks_per_proc
+        # group size g of the hierarchical variants (default: the ranks of one (virtual) GPU)
+        self.g = group_size if group_size > 0 else (ranks_per_proc // emulate_gpus if emulate_gpus > 1
+                                                    else ranks_per_proc)
         self.nprocs = nprocs
         self.proc = proc
         p = ctypes.c_int()
@@ -277,7 +280,7 @@ class Comm:
         return n.value
 
     # bits of mpxa__last_launch (test hook, not part of the C ABI headers)
-    PATH_BITS = {"small": 1, "eager": 2, "var": 4, "dyn": 8, "sync": 16, "own": 32, "swork": 64}
+    PATH_BITS = {"small": 1, "eager": 2, "var": 4, "dyn": 8, "sync": 16, "own": 32, "swork": 64, "wring": 128}
 
     def last_launch_path(self) -> set:
         """Execution path of this comm's last collective launch (test hook)."""

@@ -222,6 +222,37 @@ def test_cfg4_alltoallv(mean, packed):
                 assert np.array_equal(host(d_recv).view(np.uint8), want), (seed, G, algo, g)
 
 
+@pytest.mark.parametrize("elem", [8, 4])
+@pytest.mark.parametrize("packed", [True, False])
+def test_cfg4_alltoallv_mean_4MiB(elem, packed, monkeypatch):
+    """cfg4 at its real mean (4 MiB per pair, p = 8, 10 % zero pairs): the dynamic work-queue
+    executor in warp-ring mode: every warp streams its pieces through its own TMA ring, and
+    segments that are only 8-B (int64) or 4-B (int32) congruent are stored 16 B at a time,
+    shifted out of shared memory.  Bit-exact with the oracle's slice identity, canaries
+    outside the segments untouched; also with MPXA_NO_WRING=1 (the LSU-register queue) and
+    over 2 emulated GPUs."""
+    p = 8
+    for seed in (0, 1):
+        c4 = synth.cfg4_counts(seed, p, 4 << 20, elem=elem)
+        send, sc, sd, rc, rd, S, Rcap = synth.alltoallv_buffers(seed, c4, elem=elem, packed=packed)
+        recv0 = np.full((p, Rcap), 0xA5, dtype=np.uint8)
+        want = oracle.alltoallv_definition(send, sc, sd, rc, rd, elem, recv0)
+        d_send = dev(send)
+        for G, wring in ((0, True), (0, False), (2, True)):
+            if wring:
+                monkeypatch.delenv("MPXA_NO_WRING", raising=False)
+            else:
+                monkeypatch.setenv("MPXA_NO_WRING", "1")
+            c = Comm(ranks_per_proc=p, device=0, emulate_gpus=G, timeout_s=20.0)
+            d_recv = dev(recv0)
+            c.alltoallv(d_send, sc, sd, d_recv, rc, rd, algo="pairwise", dtype_size=elem)
+            path = c.last_launch_path()
+            assert np.array_equal(host(d_recv), want), (seed, G, wring)
+            if G == 0:
+                assert "dyn" in path and (("wring" in path) == wring), path
+            c.finalize()
+
+
 @pytest.mark.parametrize("dyn", [True, False])
 def test_alltoallv_large_misaligned(dyn, monkeypatch):
     """Large byte-granular alltoallv (dtype 1, 0.5-1.5 MiB per pair, 0-15 byte gaps between

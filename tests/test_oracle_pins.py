@@ -59,6 +59,8 @@ def test_allgather_definition_is_concatenation(p, b):
     send = synth.allgather_sendbuf(7, p, b)
     cat = np.concatenate(list(send))
     assert np.array_equal(oracle.allgather_definition(send), np.tile(cat, (p, 1)))
+    for T in (1, 2, 3, 8):       # the row-split (host-threaded) form: the same concatenation
+        assert np.array_equal(oracle.allgather_definition_threaded(send, T), np.tile(cat, (p, 1))), T
 
 
 # ---------------------------------------------------------------- brute force, labels
