@@ -7,9 +7,9 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import torch
 import synth
 from paper_2309_07337_b200 import Comm
-import tune_mid
-from tune_mid import t
-tune_mid.GS = GS = torch.cuda.Stream()
+import timing
+from timing import t
+GS = timing.GS
 p = 8
 res = {}
 for name, elem, env in (("int64_wring", 8, {}), ("int64_lsu", 8, {"MPXA_NO_WRING": "1"}), ("int32_wring", 4, {}),
