@@ -52,7 +52,8 @@ def _collectives(rank, world, R):
     c = Comm(ranks_per_proc=R, device=rank, pg=dist.group.WORLD, group_size=R, timeout_s=30.0)
     cg = Comm(ranks_per_proc=R, device=rank, pg=dist.group.WORLD, group_size=max(1, (p // 2)), timeout_s=30.0) \
         if p >= 4 else None
-    for b in (16, 1000, 300_000, 4 << 20):
+    # (host memory: every process builds the global p x p*b input and the oracle's result)
+    for b in (16, 1000, 300_000, (4 << 20) if p <= 8 else (1 << 20)):
         send_all = synth.alltoall_sendbuf(b % 97, p, b)
         want = oracle.alltoall_definition(send_all)
         d_s = torch.from_numpy(send_all[rows].copy()).to(dev)
@@ -81,7 +82,7 @@ def _collectives(rank, world, R):
             assert np.array_equal(g_r.cpu().numpy(), agw[rows]), ("allgather", b, algo)
         del d_s, d_r, g_s, g_r
     # alltoallv (cfg4 counts, gapped displacements, canaries) -- three means
-    for mean in (64, 64 << 10, 1 << 20):
+    for mean in (64, 64 << 10, (1 << 20) if p <= 8 else (256 << 10)):
         counts = synth.cfg4_counts(1, p, mean)
         send_all, sc, sd, rc, rd, S, Rcap = synth.alltoallv_buffers(1, counts, elem=8, packed=False)
         recv0 = np.full((p, Rcap), 0xA5, dtype=np.uint8)

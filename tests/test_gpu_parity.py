@@ -719,7 +719,7 @@ def test_execution_paths_are_the_intended_ones(monkeypatch):
     ag = torch.randint(0, 256, (p, 8 << 20), dtype=torch.uint8, device=DEV)
     out = torch.empty((p, p * (8 << 20)), dtype=torch.uint8, device=DEV)
     c1.allgather(ag, out, algo="pairwise")
-    assert c1.last_launch_path() == {"dyn"}
+    assert "dyn" in c1.last_launch_path() and c1.last_launch_path() <= {"dyn", "wring"}   # (wring: MPXA_WRING=2)
     del ag, out
 
 
