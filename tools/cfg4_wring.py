@@ -12,7 +12,7 @@ from timing import t
 GS = timing.GS
 p = 8
 res = {}
-for name, elem, env in (("int64_wring", 8, {}), ("int64_lsu", 8, {"MPXA_NO_WRING": "1"}), ("int32_wring", 4, {}),
+for name, elem, env in (("int64_wring", 8, {}), ("int64_wring_slack1", 8, {"MPXA_WSLACK": "1"}), ("int64_lsu", 8, {"MPXA_NO_WRING": "1"}), ("int32_wring", 4, {}),
                         ("16B_elements", 16, {}), ("16B_elements_wring", 16, {"MPXA_WRING": "2"})):
     for k, v in env.items():
         os.environ[k] = v
