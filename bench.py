@@ -191,7 +191,11 @@ def _sweep(comm, torch, gstream, reps):
     p = comm.p
     R = comm.R
     out = {"timing": "CUDA graph of back-to-back calls (device us per call, median of 5 replays)",
-           "columns": ["bytes_per_block", "us", "aggregate_GBps"], "allgather": {}, "alltoall": {}}
+           "columns": ["bytes_per_block", "us", "aggregate_GBps", "hbm_roofline_frac"],
+           "roofline": "one GPU: t_roof = algorithmic HBM bytes (allgather R*b read + R*p*b write; alltoall "
+                       "2*R*p*b) / measured copy peak; frac = t_roof / t (small sizes are latency-bound)",
+           "allgather": {}, "alltoall": {}}
+    peak, _ = load_peaks()
     dev = "cuda"
     big = torch.empty(2 << 30, dtype=torch.uint8, device=dev)
     # allgather, cfg2 sizes 4 B .. 64 MiB (x2)
@@ -204,7 +208,9 @@ def _sweep(comm, torch, gstream, reps):
             it = max(3, min(reps, int(2e9 // max(1, p * p * b))))
             fn = lambda: comm.allgather(send, recv, algo=algo, stream=gstream)
             us = 1e3 * time_graph(fn, it, gstream)
-            rows.append([b, round(us, 3), round(p * p * b / us / 1e3, 2)])
+            # HBM roofline of the operation on one GPU: read R*b, write R*p*b
+            t_roof = (R * b + R * p * b) / (peak * 1e3)
+            rows.append([b, round(us, 3), round(p * p * b / us / 1e3, 2), round(t_roof / us, 4)])
             del recv
             b *= 2
         out["allgather"][algo] = rows
@@ -218,7 +224,8 @@ def _sweep(comm, torch, gstream, reps):
             it = max(3, min(reps, int(2e9 // max(1, p * p * b))))
             fn = lambda: comm.alltoall(send, recv, algo=algo, stream=gstream)
             us = 1e3 * time_graph(fn, it, gstream)
-            rows.append([b, round(us, 3), round(p * p * b / us / 1e3, 2)])
+            t_roof = 2 * R * p * b / (peak * 1e3)      # read + write every block once
+            rows.append([b, round(us, 3), round(p * p * b / us / 1e3, 2), round(t_roof / us, 4)])
             del recv
             b *= 4
         out["alltoall"][algo] = rows
