@@ -235,8 +235,6 @@ struct mpxa_comm_s {
                                               // MPXA_NO_WRING=1: never (LSU-register path), MPXA_WRING=2: always
     int dyn_pieces = (int)kDynPiecesPerCta;   // MPXA_DYN_PIECES: queue pieces per CTA (tuning)
     int wslack = 2;                           // MPXA_WSLACK: warp-ring stages kept out of the load window
-    int dyn_tail = 0;                         // MPXA_DYN_TAIL: last pieces per CTA split in four (fine tail;
-                                              // measured: ends CTAs within ~3 us, total unchanged)
     uint64_t dyn_min_total = kDynMinTotal;    // MPXA_DYN_MIN: smallest busiest-GPU volume (tuning)
     int force_sync = -1;                      // MPXA_DYN_SYNC=0/1: force multi-step dynamic mode (tuning)
     bool small_sync = true;                   // MPXA_NO_SMALL_SYNC=1: multi-step small launches in one CTA
@@ -968,7 +966,6 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
                 E.nF = 1;
                 E.dyn_units = (int32_t)std::max<int64_t>(1, ntiles);
                 E.dyn_u = (int32_t)U;
-                E.dyn_tail = c->dyn_tail;
             }
         } else if (c->dyn && dp.nsteps > 1 && dp.dyn_tiles <= kMaxDynTiles &&
                    (c->force_sync > 0 || (dp.host.max_step_moves >= kDynSyncMoves && (uint64_t)dp.host.max_step_units * unit >= kDynSyncMin) ||
@@ -990,7 +987,6 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
             E.nF = 1;
             E.dyn_units = (int32_t)dp.dyn_tiles;
             E.dyn_u = (int32_t)U;
-            E.dyn_tail = c->dyn_tail;
             E.dyn_sync = 1;
         }
         // several GPUs: CTAs of a GPU meet at a GPU-scope counter barrier after each step and ONE
@@ -1397,7 +1393,6 @@ void read_knobs(mpxa_comm_t c) {
     if (const char *e = getenv("MPXA_NO_WRING")) c->wring = atoi(e) == 0 ? 1 : 0;
     if (const char *e = getenv("MPXA_WRING")) c->wring = atoi(e);
     if (const char *e = getenv("MPXA_DYN_PIECES")) c->dyn_pieces = std::max(1, atoi(e));
-    if (const char *e = getenv("MPXA_DYN_TAIL")) c->dyn_tail = std::max(0, atoi(e));
     if (const char *e = getenv("MPXA_WSLACK")) c->wslack = std::max(1, std::min(kWStages - 1, atoi(e)));
     if (const char *e = getenv("MPXA_DYN_MIN")) c->dyn_min_total = strtoull(e, nullptr, 10);
     if (const char *e = getenv("MPXA_DYN_SYNC")) c->force_sync = atoi(e);
@@ -1445,7 +1440,7 @@ void read_knobs(mpxa_comm_t c) {
 // knob, the selector table, the forced variants and the initial heap size (heap growth is
 // a collective IPC exchange: the sizes must evolve identically on every process).
 uint64_t knob_digest(mpxa_comm_t c, size_t heap) {
-    const int64_t v[] = {c->force_ns, c->force_nf, c->force_big, c->force_exec, c->pdl, c->dyn, c->wring, c->wslack, c->dyn_pieces, c->dyn_tail,
+    const int64_t v[] = {c->force_ns, c->force_nf, c->force_big, c->force_exec, c->pdl, c->dyn, c->wring, c->wslack, c->dyn_pieces,
                          (int64_t)c->dyn_min_total, c->force_sync, c->small_sync, (int64_t)c->small_max1,
                          (int64_t)c->small_vol1, c->var_chop, c->var_tiles, c->swork, c->small_nt, c->ll,
                          (int64_t)c->one_cta_items, c->hier_staged, c->row_signal, c->ll_max, c->ll_max_ms,

@@ -710,23 +710,12 @@ __device__ __noinline__ bool dyn_tile(const ExecParams &P, ExecShared &S, Produc
     if (t == 0) {
         if (totA == 0) return false;
         uint32_t *q = &P.dc->dyn_next[g * kMaxDynTiles + ti];
-        // fine tail: the last dyn_tail x gridDim.x pieces of the queue are split in four (each
-        // CTA's last pieces are short, so the launch does not wait on a slow SM's full piece)
-        const uint32_t F = min(totA, (uint32_t)gridDim.x * (uint32_t)P.dyn_tail);
-        const uint32_t c0 = totA - F, totQ = c0 + 4 * F;
         uint32_t u = atomicAdd(q, 1u);
-        while (u < totQ) {
+        while (u < totA) {
             const uint32_t un = atomicAdd(q, 1u);   // next piece requested while this one streams
-            const uint32_t cu = u < c0 ? u : c0 + (u - c0) / 4;
-            const int mi = find_move(S.pcA, nm, cu);
+            const int mi = find_move(S.pcA, nm, u);
             const Move &m = S.moves[mi];
-            uint64_t lo = (uint64_t)(cu - S.pcA[mi]) * U, len = U;
-            if (u >= c0) {
-                lo += (uint64_t)((u - c0) % 4) * (U / 4);
-                len = U / 4;
-                if (lo >= (uint64_t)m.len * P.unit) { u = un; continue; }   // past a short last piece
-            }
-            const MovePlan mp = piece_plan(P, S, mi, lo, len);
+            const MovePlan mp = piece_plan(P, S, mi, (uint64_t)(u - S.pcA[mi]) * U, U);
             const uint64_t nb = mp.n;
             uint64_t head = (16 - ((uintptr_t)mp.src & 15)) & 15;
             if (head > nb) head = nb;

@@ -184,8 +184,7 @@ struct ExecParams {
                                // its receive moves last (Step::wait_mask = their number)
     int32_t wring;             // dynamic mode with per-warp TMA rings (kWStages x kWChunk each);
                                // stages / chunk then describe the whole dynamic smem
-    int32_t dyn_tail;          // dynamic mode: the last dyn_tail x gridDim.x pieces of the TMA
-                               // queue are split in four (fine tail)
+    int32_t pad8;
     int32_t wslack;            // warp-ring mode: stages kept out of the load window (1 or 2)
 };
 
