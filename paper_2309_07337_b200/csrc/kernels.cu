@@ -304,6 +304,17 @@ __device__ __forceinline__ char *base_of(const ExecParams &P, const ExecShared &
     return S.work_base[g] + local * P.work_stride;
 }
 
+// Fan-out bulk store of one staged chunk to offset doff of the dst_kind buffer of every rank:
+// the ranks' bases walked GPU by GPU (no per-rank division, unlike base_of).
+__device__ __forceinline__ void fan_store(const ExecParams &P, const ExecShared &S, int kind, uint64_t doff,
+                                          uint32_t src, uint32_t len) {
+    const uint64_t stride = kind == BK_RECV ? P.recv_stride : P.work_stride;
+    for (int g = 0; g < P.G; g++) {
+        char *b = (kind == BK_RECV ? S.recv_base[g] : S.work_base[g]) + doff;
+        for (int l = 0; l < P.R; l++, b += stride) tma_store_1d(b, src, len);
+    }
+}
+
 // Spin (threads < 32, one per bit of mask) until *slot(bit) >= want; sets abort on timeout.
 #ifndef MPXA_POLL_NS
 #define MPXA_POLL_NS 128   // executor flag polls: back-off between system-scope loads
@@ -331,28 +342,29 @@ __device__ __noinline__ void wait_mask_ge(const ExecParams &P, ExecShared &S, ui
     }
 }
 
-// The single-thread TMA producer: a ring of P.stages smem stages; loads run P.ahead chunks
+// The single-thread TMA producer: a ring of kRingStages smem stages (= P.stages, a compile-time
+// constant so the ring index is a multiply, not a division); loads run P.ahead chunks
 // ahead of the oldest pending store; each chunk's stores form one bulk group.
 struct Producer {
     uint32_t issued = 0, stored = 0;
     char *stages;
 
     __device__ __forceinline__ void store_one(const ExecParams &P, ExecShared &S) {
-        const uint32_t s = stored % (uint32_t)P.stages;
-        mbar_wait(smem_u32(&S.mbar[s]), (stored / (uint32_t)P.stages) & 1u);
+        const uint32_t s = stored % kRingStages;
+        mbar_wait(smem_u32(&S.mbar[s]), (stored / kRingStages) & 1u);
         const RingEntry e = S.ring[s];
         const uint32_t src = smem_u32(stages + (size_t)s * P.chunk);
         if (!e.fanout) {
             tma_store_1d(e.dst, src, e.len);
         } else {
-            for (int j = 0; j < P.p; j++) tma_store_1d(base_of(P, S, e.dst_kind, j) + e.doff, src, e.len);
+            fan_store(P, S, e.dst_kind, e.doff, src, e.len);
         }
         bulk_commit();
         stored++;
     }
     __device__ __forceinline__ void push(const ExecParams &P, ExecShared &S, const char *src, const RingEntry &e) {
         if (issued - stored == (uint32_t)P.ahead) store_one(P, S);
-        const uint32_t ns = (uint32_t)P.stages;
+        const uint32_t ns = kRingStages;
         const uint32_t s = issued % ns;
         if (issued >= ns) bulk_wait_read((int)(stored - 1 - (issued - ns)));
         S.ring[s] = e;
@@ -655,7 +667,11 @@ __device__ __forceinline__ MovePlan piece_plan(const ExecParams &P, const ExecSh
 // Load (unless prefetched) and classify one tile of moves: S.msrc / S.mdst resolved, and the
 // exclusive piece prefixes S.pcA (16-B congruent moves of >= kTmaMin bytes: the TMA queue)
 // and S.pcB (the rest), totals at index nm.
-__device__ __noinline__ void dyn_classify(const ExecParams &P, ExecShared &S, int g, int first, int nm, bool loaded) {
+// Returns k > 0 when every move of the tile is in the TMA queue with the same number k of
+// pieces (uniform alltoall / allgather blocks): piece u is then piece u % k of move u / k, no
+// search of the prefix array.
+__device__ __noinline__ uint32_t dyn_classify(const ExecParams &P, ExecShared &S, int g, int first, int nm,
+                                              bool loaded) {
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const uint64_t U = (uint64_t)P.dyn_u;
     if (!loaded) {   // moves not prefetched by the prologue (later tiles, or step 0 not dense)
@@ -697,6 +713,9 @@ __device__ __noinline__ void dyn_classify(const ExecParams &P, ExecShared &S, in
         S.pcB[kThreads] = (uint32_t)((wo + inc) >> 32);
     }
     __syncthreads();
+    const uint32_t k0 = S.pcA[1];
+    const int uni = __syncthreads_and(t >= nm || (kt == (uint64_t)k0 && k0 > 0));
+    return uni ? k0 : 0u;
 }
 
 // One tile of at most kMoveTile moves (queues of tile ti).
@@ -704,7 +723,7 @@ __device__ __noinline__ bool dyn_tile(const ExecParams &P, ExecShared &S, Produc
                                       bool loaded, int ti) {
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const uint64_t U = (uint64_t)P.dyn_u, chunk = (uint64_t)P.chunk;
-    dyn_classify(P, S, g, first, nm, loaded);
+    const uint32_t kuni = dyn_classify(P, S, g, first, nm, loaded);
     const uint32_t totA = S.pcA[nm], totB = S.pcB[nm];
     bool wrote = false;
     if (t == 0) {
@@ -713,7 +732,7 @@ __device__ __noinline__ bool dyn_tile(const ExecParams &P, ExecShared &S, Produc
         uint32_t u = atomicAdd(q, 1u);
         while (u < totA) {
             const uint32_t un = atomicAdd(q, 1u);   // next piece requested while this one streams
-            const int mi = find_move(S.pcA, nm, u);
+            const int mi = kuni ? (int)(u / kuni) : find_move(S.pcA, nm, u);
             const Move &m = S.moves[mi];
             const MovePlan mp = piece_plan(P, S, mi, (uint64_t)(u - S.pcA[mi]) * U, U);
             const uint64_t nb = mp.n;
@@ -921,7 +940,7 @@ __device__ __noinline__ bool dyn_tile_w(const ExecParams &P, ExecShared &S, int 
                 if (!e.fanout) {
                     tma_store_1d(e.dst, smem_u32(stage), e.n);
                 } else {
-                    for (int j = 0; j < P.p; j++) tma_store_1d(base_of(P, S, e.dst_kind, j) + e.doff, smem_u32(stage), e.n);
+                    fan_store(P, S, e.dst_kind, e.doff, smem_u32(stage), e.n);
                 }
             }
         } else {

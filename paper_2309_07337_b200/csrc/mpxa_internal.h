@@ -28,8 +28,9 @@ constexpr int kMaxStages = 8;
 struct TmaConfig {
     int stages, chunk, ahead;
 };
-constexpr TmaConfig kTmaMid = {6, 16384, 4};
-constexpr TmaConfig kTmaBig = {6, 32768, 4};
+constexpr int kRingStages = 6;   // both configurations' stage count (the producer's ring index)
+constexpr TmaConfig kTmaMid = {kRingStages, 16384, 4};
+constexpr TmaConfig kTmaBig = {kRingStages, 32768, 4};
 constexpr int kMaxDynSmem = 6 * 32768;
 constexpr int kMoveTile = kThreads;   // moves staged in shared memory at a time (one per thread)
 constexpr int kMaxDynTiles = 64;      // dynamic mode: move tiles per step (queues per tile)
