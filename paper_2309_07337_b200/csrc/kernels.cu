@@ -890,9 +890,10 @@ __device__ __noinline__ bool dyn_tile_w(const ExecParams &P, ExecShared &S, int 
                     e.doff = mp.doff + off;
                     e.dst = m.fanout ? nullptr : mp.dst + off;
                 } else {
-                    // chunks end at 16-B boundaries of the destination (except the piece's last)
+                    // chunks end at 128-B (line) boundaries of the destination (except the
+                    // piece's last), so no line is written half by one stage, half by the next
                     len = end - off < (uint64_t)(kWChunk - 32) ? end - off : (uint64_t)(kWChunk - 32);
-                    if (off + len < end) len -= ((uintptr_t)(mp.dst + off + len)) & 15;
+                    if (off + len < end) len -= ((uintptr_t)(mp.dst + off + len)) & 127;
                     const uintptr_t s0 = (uintptr_t)(mp.src + off), a0 = s0 & ~(uintptr_t)15;
                     lsrc = (const char *)a0;
                     e.kind = 1;
