@@ -961,6 +961,11 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
                 nC = c->force_big > 0 ? c->cap_big : c->cap_ctas;
                 uint64_t U = total / ((uint64_t)nC * (uint64_t)c->dyn_pieces);
                 U = std::max<uint64_t>((uint64_t)E.chunk, std::min<uint64_t>(U, kDynMaxPiece));
+                // many move tiles (p >= 23 ranks on one GPU): each tile is classified by the whole
+                // CTA while the producer stops issuing, so fewer, longer pieces pay (measured,
+                // p = 32, 256 KiB blocks: 16 -> 48 KiB pieces, 93.2 -> 85.7 us; one or two
+                // tiles: unchanged or slower)
+                if (ntiles >= 4) U = std::max<uint64_t>(U, 3 * (uint64_t)E.chunk);
                 U = U / (uint64_t)E.chunk * (uint64_t)E.chunk;
                 E.nS = nC;
                 E.nF = 1;
