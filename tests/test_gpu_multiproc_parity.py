@@ -58,7 +58,9 @@ def _collectives(rank, world, R):
         want = oracle.alltoall_definition(send_all)
         d_s = torch.from_numpy(send_all[rows].copy()).to(dev)
         d_r = torch.empty_like(d_s)
-        c.register(d_r)
+        c.register(d_r)                 # (windows are per comm: register with each)
+        if cg:
+            cg.register(d_r)
         for cc, algo in ((c, "pairwise"), (c, "bruck"), (c, "hier")) + (((cg, "hier"),) if cg else ()):
             d_r.fill_(0xA5)
             torch.cuda.synchronize()
@@ -90,6 +92,8 @@ def _collectives(rank, world, R):
         d_s = torch.from_numpy(send_all[rows].copy()).to(dev)
         d_r = torch.from_numpy(recv0[rows].copy()).to(dev)
         c.register(d_r)
+        if cg:
+            cg.register(d_r)
         for cc, algo in ((c, "pairwise"), (c, "hier"), (c, "bruck")) + (((cg, "hier"),) if cg else ()):
             d_r.copy_(torch.from_numpy(recv0[rows].copy()).to(dev))
             torch.cuda.synchronize()
