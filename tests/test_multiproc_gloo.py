@@ -197,6 +197,7 @@ def test_init_knob_consistency(tmp_path):
         ("MPXA_HIER_STAGED", "1"),
         ("MPXA_ALGO", "alltoall:bruck"),
         ("MPXA_NO_SMALL", "1"),
+        ("MPXA_NO_WRING", "1"),                # warp-ring dynamic mode on one process only
         ("MPXA_SELECTOR", str(sel)))]
     same = {"MPXA_NO_LL": "1", "MPXA_SELECTOR": str(sel)}
     cases += [([same, dict(same)], "ok"), ([{}, {}], "ok")]
