@@ -496,13 +496,20 @@ struct PieceRef {
     const char *src;
     uint32_t len;     // 0: no piece
 };
-template <bool A16>
+// AW: 16 -- the host vouched that every piece is a whole, 16-B aligned vector; 8 -- every
+// offset, length, base and stride is a multiple of 8 (int64 / double payloads): pieces move as
+// 8-byte words; 0 -- any alignment: aligned 4-byte words and funnel shifts
+template <int AW>
 struct PieceRegs {
     uint4 v[kBatch];
     uint32_t w4[kBatch];
     __device__ __forceinline__ void issue(int k, const char *sp, uint32_t len) {
-        if (A16) {
+        if (AW == 16) {
             v[k] = ld16<false>((const uint4 *)sp);
+        } else if (AW == 8) {
+            const uint2 lo = __ldcg((const uint2 *)sp);
+            const uint2 hi = len > 8 ? __ldcg((const uint2 *)sp + 1) : make_uint2(0u, 0u);
+            v[k] = make_uint4(lo.x, lo.y, hi.x, hi.y);
         } else {
             const uintptr_t a = (uintptr_t)sp & ~(uintptr_t)3;
             const uint32_t *wp = (const uint32_t *)a;
@@ -516,7 +523,13 @@ struct PieceRegs {
     }
     // the same with generic loads (the source may be shared memory)
     __device__ __forceinline__ void issue_generic(int k, const char *sp, uint32_t len) {
-        if (A16) { v[k] = *(const uint4 *)sp; return; }
+        if (AW == 16) { v[k] = *(const uint4 *)sp; return; }
+        if (AW == 8) {
+            const uint2 lo = *(const uint2 *)sp;
+            const uint2 hi = len > 8 ? *((const uint2 *)sp + 1) : make_uint2(0u, 0u);
+            v[k] = make_uint4(lo.x, lo.y, hi.x, hi.y);
+            return;
+        }
         const uintptr_t a = (uintptr_t)sp & ~(uintptr_t)3;
         const uint32_t *wp = (const uint32_t *)a;
         const uintptr_t end = (uintptr_t)sp + len;
@@ -527,17 +540,22 @@ struct PieceRegs {
         w4[k] = (a + 16 < end) ? wp[4] : 0u;
     }
     __device__ __forceinline__ uint4 value(int k, const char *sp) const {
-        if (A16) return v[k];
+        if (AW != 0) return v[k];
         const uint32_t sh = 8u * (uint32_t)((uintptr_t)sp & 3);
         return make_uint4(__funnelshift_r(v[k].x, v[k].y, sh), __funnelshift_r(v[k].y, v[k].z, sh),
                           __funnelshift_r(v[k].z, v[k].w, sh), __funnelshift_r(v[k].w, w4[k], sh));
     }
 };
 
-// A16: the host vouched that every piece is a whole, 16-B aligned vector
-template <bool A16 = false>
+// AW as in PieceRegs
+template <int AW = 0>
 __device__ __forceinline__ void store_piece(char *dp, uint4 v, uint32_t len) {
-    if (A16 || (len == 16 && (((uintptr_t)dp) & 15) == 0)) { st16((uint4 *)dp, v); return; }
+    if (AW == 16 || (len == 16 && (((uintptr_t)dp) & 15) == 0)) { st16((uint4 *)dp, v); return; }
+    if (AW == 8) {                                      // 8-B aligned, len 8 or 16
+        *(uint2 *)dp = make_uint2(v.x, v.y);
+        if (len > 8) *((uint2 *)dp + 1) = make_uint2(v.z, v.w);
+        return;
+    }
     if (len == 16 && (((uintptr_t)dp) & 3) == 0) {
         uint32_t *d = (uint32_t *)dp;
         d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
@@ -559,7 +577,7 @@ __device__ __forceinline__ void store_piece(char *dp, uint4 v, uint32_t len) {
 template <bool A16>
 __device__ __forceinline__ void small_batch_t(const ExecParams &P, const ExecShared &S, const SmallJob *jobs, int nj,
                                               int lane) {
-    PieceRegs<A16> R;
+    PieceRegs<A16 ? 16 : 0> R;
     const uint32_t o = (uint32_t)lane * 16;
 #pragma unroll
     for (int k = 0; k < kBatch; k++)
@@ -1464,13 +1482,13 @@ __device__ __forceinline__ const Move &item_move(const Move *mv, const uint16_t 
     return mv[idx ? idx[it >> lg] : (it >> lg)];
 }
 
-template <bool A16, bool VAR = false>
+template <int AW, bool VAR = false>
 __device__ __forceinline__ void small_items(const ExecParams &P, const SmallShared &S, const Move *mv, uint32_t items,
                                             uint32_t lg, uint32_t TT, uint32_t base0, const uint16_t *idx,
                                             const uint32_t *vpc = nullptr) {
     const uint32_t mask = (1u << lg) - 1u;   // pieces per move: a power of two (host-rounded)
     for (uint32_t base = base0; base < items; base += TT * kBatch) {
-        PieceRegs<A16> R;
+        PieceRegs<AW> R;
         const char *sp[kBatch];
 #pragma unroll
         for (int k = 0; k < kBatch; k++) {
@@ -1497,10 +1515,10 @@ __device__ __forceinline__ void small_items(const ExecParams &P, const SmallShar
             const uint64_t doff = (uint64_t)m.dst_off * P.unit + o;
             const uint4 val = R.value(k, sp[k]);
             if (!m.fanout) {
-                store_piece<A16>(sb(P, S, m.dst_kind, m.dst_rank) + doff, val, len);
+                store_piece<AW>(sb(P, S, m.dst_kind, m.dst_rank) + doff, val, len);
             } else {
 #pragma unroll 1
-                for (int r = 0; r < P.p; r++) store_piece<A16>(sb(P, S, m.dst_kind, r) + doff, val, len);
+                for (int r = 0; r < P.p; r++) store_piece<AW>(sb(P, S, m.dst_kind, r) + doff, val, len);
             }
         }
     }
@@ -1539,13 +1557,13 @@ __device__ __forceinline__ char *local_base(const ExecParams &P, int g, char *wo
     return work_g + local * P.work_stride;
 }
 
-template <bool A16>
+template <int AW>
 __device__ __forceinline__ void small_items_loc(const ExecParams &P, const SmallShared &S, const RMove *mv,
                                                 uint32_t items, uint32_t lg, uint32_t TT, uint32_t base0,
                                                 const uint16_t *idx) {
     const uint32_t mask = (1u << lg) - 1u;
     for (uint32_t base = base0; base < items; base += TT * kBatch) {
-        PieceRegs<A16> R;
+        PieceRegs<AW> R;
         const char *sp[kBatch];
 #pragma unroll
         for (int k = 0; k < kBatch; k++) {
@@ -1571,7 +1589,7 @@ __device__ __forceinline__ void small_items_loc(const ExecParams &P, const Small
             if (m.dst_sm) {
                 store_piece_generic(m.dst + o, val, len);
             } else if (!m.fanout) {
-                store_piece<A16>((m.dst_remote ? S.rb[m.dst_kind][m.dst_rank] + m.doff : m.dst) + o, val, len);
+                store_piece<AW>((m.dst_remote ? S.rb[m.dst_kind][m.dst_rank] + m.doff : m.dst) + o, val, len);
             } else {
 #pragma unroll 1
                 for (int r = 0; r < P.p; r++) store_piece_generic(S.rb[m.dst_kind][r] + m.doff + o, val, len);
@@ -1613,7 +1631,7 @@ __device__ __forceinline__ void small_items_ll(const ExecParams &P, SmallShared 
     const uint32_t mask = (1u << lg) - 1u;
     const uint64_t flag = S.ll_seq << 32, par = S.ll_par;
     for (uint32_t base = base0; base < items; base += TT * kBatch) {
-        PieceRegs<A16> R;
+        PieceRegs<A16 ? 16 : 0> R;
         uint4 lv[kBatch];
         bool on[kBatch];
 #pragma unroll
@@ -1683,9 +1701,9 @@ __device__ __forceinline__ void small_items_ll(const ExecParams &P, SmallShared 
             const uint4 val = RECV ? lv[k] : R.value(k, m.src + o);
             if (m.fanout == 2) {
 #pragma unroll 1
-                for (int r = g * P.R; r < (g + 1) * P.R; r++) store_piece<A16>(S.rb[m.dst_kind][r] + m.doff + o, val, len);
+                for (int r = g * P.R; r < (g + 1) * P.R; r++) store_piece<A16 ? 16 : 0>(S.rb[m.dst_kind][r] + m.doff + o, val, len);
             } else {
-                store_piece<A16>(m.dst + o, val, len);
+                store_piece<A16 ? 16 : 0>(m.dst + o, val, len);
             }
         }
     }
@@ -1722,8 +1740,8 @@ __device__ __forceinline__ void small_var_step(const ExecParams &P, const SmallS
         wp[lane] = inc - pcs;
         const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
         __syncwarp();
-        if (a16) small_items<true, true>(P, S, wm, tot, 0, 32, lane, nullptr, wp);
-        else small_items<false, true>(P, S, wm, tot, 0, 32, lane, nullptr, wp);
+        if (a16) small_items<16, true>(P, S, wm, tot, 0, 32, lane, nullptr, wp);
+        else small_items<0, true>(P, S, wm, tot, 0, 32, lane, nullptr, wp);
     }
 }
 
@@ -1923,7 +1941,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
         // 16-B fast path: the host vouched for every local offset / length / base, and the
         // recv bases of the peers written in this step arrived with their CTS
         // (AK != 0: the host knows the answer for the whole launch -- one copy path compiled)
-        bool a16 = AK == 1 ? true : AK == 2 ? false : P.small_a16 != 0;
+        bool a16 = AK == 1 ? true : (AK == 2 || AK == 3) ? false : P.small_a16 != 0;
+        const bool a8 = AK == 3;   // the host vouched for 8-B alignment of everything (not 16)
         if (AK == 0)
             for (int q = 0; q < P.G; q++)
                 if (((st.signal_mask >> q) & 1u) && ((uintptr_t)S.recv_base[q] & 15)) a16 = false;
@@ -1941,14 +1960,16 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
             }
         } else if (LOC) {
             const RMove *rm = reinterpret_cast<const RMove *>(smoves) + st.first;
-            if (a16) small_items_loc<true>(P, S, rm, items, lg, TT, base0, idx);
-            else small_items_loc<false>(P, S, rm, items, lg, TT, base0, idx);
+            if (a16) small_items_loc<16>(P, S, rm, items, lg, TT, base0, idx);
+            else if (a8) small_items_loc<8>(P, S, rm, items, lg, TT, base0, idx);
+            else small_items_loc<0>(P, S, rm, items, lg, TT, base0, idx);
         } else if (VARK) {
             small_var_step(P, S, mvs, st.first, st.nm, a16, small_dyn);
         } else if (a16) {
-            small_items<true>(P, S, mvs + st.first, items, lg, TT, base0, idx);
+            small_items<16>(P, S, mvs + st.first, items, lg, TT, base0, idx);
         } else {
-            small_items<false>(P, S, mvs + st.first, items, lg, TT, base0, idx);
+            if (a8) small_items<8>(P, S, mvs + st.first, items, lg, TT, base0, idx);
+            else small_items<0>(P, S, mvs + st.first, items, lg, TT, base0, idx);
         }
         TRACE(2);
         __syncthreads();
@@ -2008,8 +2029,9 @@ template <int KM>
 static cudaError_t launch_small_km(const ExecParams &P, size_t max_dyn, size_t smem, dim3 grid, bool cooperative,
                                    bool pdl, cudaStream_t stream) {
     // the 16-B decision is launch-wide unless peers' recv bases arrive at run time (mode 2)
-    const int ak = P.mode == 2 ? 0 : (P.small_a16 ? 1 : 2);
+    const int ak = P.mode == 2 ? 0 : (P.small_a16 ? 1 : (P.small_a8 ? 3 : 2));
     if (ak == 1) return launch_small_t<KM, 1>(P, max_dyn, smem, grid, cooperative, pdl, stream);
+    if (ak == 3) return launch_small_t<KM, 3>(P, max_dyn, smem, grid, cooperative, pdl, stream);
     if (ak == 2) return launch_small_t<KM, 2>(P, max_dyn, smem, grid, cooperative, pdl, stream);
     return launch_small_t<KM, 0>(P, max_dyn, smem, grid, cooperative, pdl, stream);
 }

@@ -185,7 +185,8 @@ struct ExecParams {
                                // its receive moves last (Step::wait_mask = their number)
     int32_t wring;             // dynamic mode with per-warp TMA rings (kWStages x kWChunk each);
                                // stages / chunk then describe the whole dynamic smem
-    int32_t pad8;
+    int32_t small_a8;          // small kernel: every local offset, length, base and stride is an
+                               // 8-B multiple (not all 16): pieces move as 8-byte words
     int32_t wslack;            // warp-ring mode: stages kept out of the load window (1 or 2)
 };
 
