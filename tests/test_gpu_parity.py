@@ -253,12 +253,13 @@ def test_cfg4_alltoallv_mean_4MiB(elem, packed, monkeypatch):
             c.finalize()
 
 
-@pytest.mark.parametrize("dyn", [True, False])
+@pytest.mark.parametrize("dyn", [True, False, "wring"])
 def test_alltoallv_large_misaligned(dyn, monkeypatch):
     """Large byte-granular alltoallv (dtype 1, 0.5-1.5 MiB per pair, 0-15 byte gaps between
     segments): every source/destination misalignment class, through the dynamic work-queue
     executor (TMA queue for 16-B congruent segments, LSU queue with shifted 16-B stores
-    otherwise) and the static slices; canary bytes outside the segments must survive."""
+    otherwise), the warp rings forced on (shifted stores out of shared memory for every byte
+    offset) and the static slices; canary bytes outside the segments must survive."""
     p = 8
     rng = np.random.default_rng(7)
     counts = rng.integers(512 << 10, 3 << 19, size=(p, p)).astype(np.int64)
@@ -275,6 +276,8 @@ def test_alltoallv_large_misaligned(dyn, monkeypatch):
     want = oracle.alltoallv_definition(send, sc, sd, rc, rd, 1, recv0)
     if not dyn:
         monkeypatch.setenv("MPXA_NO_DYN", "1")
+    if dyn == "wring":      # every byte offset class through the warp rings' shifted stores
+        monkeypatch.setenv("MPXA_WRING", "2")
     for G in (0, 8):
         c = Comm(ranks_per_proc=p, device=0, emulate_gpus=G, timeout_s=20.0)
         for off in (0, 1, 8):           # shift the whole send buffer: more alignment classes
