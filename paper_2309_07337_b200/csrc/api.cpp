@@ -1818,8 +1818,9 @@ int mpxa_start(mpxa_request_t q, mpxa_stream_t st) {
         int rc = run_program(c, *q->prog, q->send, q->recv, q->unit, q->send_stride, q->recv_stride, S(st), &q->grid);
         if (rc) return rc;
     }
-    if (!q->done) CK(cudaEventCreateWithFlags(&q->done, cudaEventDisableTiming));
-    CK(cudaEventRecord(q->done, S(st)));
+    // (no event here: mpxa_wait on the start stream -- the common case -- needs none; a wait on
+    // another stream records one on the start stream then, which also covers any work queued
+    // there after the start: conservative, never too early)
     q->start_stream = S(st);
     q->active = true;
     c->active = q;
@@ -1839,7 +1840,11 @@ int mpxa_wait(mpxa_request_t q, mpxa_stream_t st) {
         q->active = false;
         return MPXA_SUCCESS;
     }
-    if (S(st) != q->start_stream) CK(cudaStreamWaitEvent(S(st), q->done, 0));
+    if (S(st) != q->start_stream) {
+        if (!q->done) CK(cudaEventCreateWithFlags(&q->done, cudaEventDisableTiming));
+        CK(cudaEventRecord(q->done, q->start_stream));
+        CK(cudaStreamWaitEvent(S(st), q->done, 0));
+    }
     q->active = false;
     if (q->comm->active == q) q->comm->active = nullptr;
     return MPXA_SUCCESS;

@@ -805,3 +805,29 @@ def test_many_ranks_beyond_rank_table(G):
             c.allgather(dev(ag), d_r, algo=algo)
             assert np.array_equal(host(d_r), oracle.allgather_definition(ag)), (b, algo)
     assert c.check() == 0
+
+
+def test_persistent_wait_on_another_stream():
+    """mpxa_wait on a stream other than the start stream orders that stream after the
+    collective (the start stream is delayed by a long device sleep before the start): a copy
+    of recvbuf queued on the wait stream right after the wait sees the whole result."""
+    p, b = 8, 4096
+    c = comm(p)
+    send = synth.alltoall_sendbuf(77, p, b)
+    d_s, d_r = dev(send), torch.zeros((p, p * b), dtype=torch.uint8, device=DEV)
+    req = c.alltoall_init(d_s, d_r, algo="pairwise")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    out = torch.zeros_like(d_r)
+    for rep in range(3):
+        d_r.zero_()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s1):
+            torch.cuda._sleep(50_000_000)             # the collective starts late on s1
+        req.start(s1)
+        req.wait(s2)
+        with torch.cuda.stream(s2):
+            out.copy_(d_r)
+        torch.cuda.synchronize()
+        assert np.array_equal(host(out), oracle.alltoall_definition(send)), rep
+    req.free()
+    assert c.check() == 0

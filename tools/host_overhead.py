@@ -36,7 +36,7 @@ h, s_ = c.handle, ctypes.c_void_p(st.cuda_stream)
 res["c_one_shot_us"] = wall(lambda: L.mpxa_alltoallv_algo(sp, ptrs[0], ptrs[1], sb, rp, ptrs[2], ptrs[3], rb, 8, 0, h, s_))
 req = c.alltoallv_init(d_s, sc, sd, d_r, rc, rd, dtype_size=8)
 res["python_persistent_us"] = wall(lambda: (req.start(st), req.wait(st)))
-rh = ctypes.c_void_p(req.h) if hasattr(req, "h") else None
+res["c_persistent_us"] = wall(lambda: (L.mpxa_start(req.handle, s_), L.mpxa_wait(req.handle, s_)))
 print(json.dumps(res), flush=True)
 
 # uniform one-shot alltoall (p = 8, 64 B blocks)
