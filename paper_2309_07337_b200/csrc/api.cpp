@@ -877,8 +877,9 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
         E.nS = E.nF = 1;
         E.small_a16 = unit % 16 == 0 && (uintptr_t)send % 16 == 0 && (uintptr_t)recv % 16 == 0 &&
                       send_stride % 16 == 0 && recv_stride % 16 == 0 && E.work_stride % 16 == 0;
-        // int64 / double payloads: 8-byte words instead of 4-byte words and funnel shifts
-        // (the eager companion's word streams are 4-byte: not for eager launches)
+        // int64 / double payloads: 8-byte words instead of 4-byte words and funnel shifts (eager
+        // launches keep their own 4-byte word streams; a per-process choice -- no protocol
+        // consequence across processes)
         E.small_a8 = !E.small_a16 && unit % 8 == 0 && (uintptr_t)send % 8 == 0 && (uintptr_t)recv % 8 == 0 &&
                      send_stride % 8 == 0 && recv_stride % 8 == 0 && E.work_stride % 8 == 0;
         E.small_ppm = (int32_t)ppm;
