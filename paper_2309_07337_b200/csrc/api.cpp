@@ -32,6 +32,7 @@
 namespace mpxa {
 cudaError_t launch_exec(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream);
 cudaError_t launch_small(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream);
+cudaError_t launch_tiny(const ExecParams &P, int nC, bool pdl, cudaStream_t stream);
 cudaError_t launch_counts(const int64_t *sc, int64_t *rc, int64_t *rd, int p, int r0, int nr,
                           cudaStream_t stream);
 cudaError_t launch_scan(const int64_t *counts, int64_t *rc, int64_t *rd, int p, int nr,
@@ -236,6 +237,7 @@ struct mpxa_comm_s {
                                               // MPXA_NO_WRING=1: never (LSU-register path), MPXA_WRING=2: always
     int dyn_pieces = (int)kDynPiecesPerCta;   // MPXA_DYN_PIECES: queue pieces per CTA (tuning)
     int wslack = 2;                           // MPXA_WSLACK: warp-ring stages kept out of the load window
+    bool tiny = true;                         // MPXA_NO_TINY=1: small one-GPU launches in the general kernel
     uint64_t dyn_min_total = kDynMinTotal;    // MPXA_DYN_MIN: smallest busiest-GPU volume (tuning)
     int force_sync = -1;                      // MPXA_DYN_SYNC=0/1: force multi-step dynamic mode (tuning)
     bool small_sync = true;                   // MPXA_NO_SMALL_SYNC=1: multi-step small launches in one CTA
@@ -826,6 +828,7 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
     E.ahead = tc.ahead;
     ++c->epoch;   // host mirror only; the kernels keep the authoritative epoch in DevComm
     cudaError_t e;
+    bool tiny = false;
     const uint64_t maxmove = (uint64_t)dp.host.max_move * unit;
     uint64_t ppm = 1;   // 16-B pieces per move, rounded up to a power of two (shift decode)
     while (ppm * 16 < maxmove) ppm <<= 1;
@@ -945,7 +948,13 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
             while (nt < 512 && (nt < per_cta || nt < (uint64_t)c->p || nt < (uint64_t)dp.nsteps)) nt *= 2;
             if (nt < 512) E.small_threads = (int32_t)nt;
         }
-        e = launch_small(E, std::max(1, nC), c->emulated ? c->G : 1, c->emulated, pdl && c->pdl, stream);
+        // one step on one GPU, every move cached, 16- or 8-B aligned: the tiny kernel (no flags,
+        // steps or rank tables -- the shortest instruction stream for a cold SM)
+        tiny = c->tiny && one_step && c->G == 1 && !c->emulated && c->nprocs == 1 && !E.small_var &&
+               !E.small_own && !E.small_ll && E.small_cache > 0 && (E.small_a16 || E.small_a8) &&
+               sp == &dp;
+        if (tiny) e = launch_tiny(E, std::max(1, nC), pdl && c->pdl, stream);
+        else e = launch_small(E, std::max(1, nC), c->emulated ? c->G : 1, c->emulated, pdl && c->pdl, stream);
     } else {
         int nC = gr.n();
         // dynamic mode: one step whose moves all fit the CTA's shared-memory move tile and
@@ -1038,7 +1047,7 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
     // execution path of this launch (tests assert the intended path ran: mpxa__last_launch)
     c->last_path = (small ? 1u : 0u) | (E.small_ll ? 2u : 0u) | (E.small_var ? 4u : 0u) |
                    (E.dyn_units ? 8u : 0u) | (E.dyn_sync ? 16u : 0u) | (E.small_own ? 32u : 0u) |
-                   (E.small_swork ? 64u : 0u) | (E.wring ? 128u : 0u);
+                   (E.small_swork ? 64u : 0u) | (E.wring ? 128u : 0u) | (tiny ? 256u : 0u);
     return MPXA_SUCCESS;
 }
 
@@ -1408,6 +1417,7 @@ void read_knobs(mpxa_comm_t c) {
     if (const char *e = getenv("MPXA_NO_WRING")) c->wring = atoi(e) == 0 ? 1 : 0;
     if (const char *e = getenv("MPXA_WRING")) c->wring = atoi(e);
     if (const char *e = getenv("MPXA_DYN_PIECES")) c->dyn_pieces = std::max(1, atoi(e));
+    if (const char *e = getenv("MPXA_NO_TINY")) c->tiny = atoi(e) == 0;
     if (const char *e = getenv("MPXA_WSLACK")) c->wslack = std::max(1, std::min(kWStages - 1, atoi(e)));
     if (const char *e = getenv("MPXA_DYN_MIN")) c->dyn_min_total = strtoull(e, nullptr, 10);
     if (const char *e = getenv("MPXA_DYN_SYNC")) c->force_sync = atoi(e);
@@ -1455,7 +1465,7 @@ void read_knobs(mpxa_comm_t c) {
 // knob, the selector table, the forced variants and the initial heap size (heap growth is
 // a collective IPC exchange: the sizes must evolve identically on every process).
 uint64_t knob_digest(mpxa_comm_t c, size_t heap) {
-    const int64_t v[] = {c->force_ns, c->force_nf, c->force_big, c->force_exec, c->pdl, c->dyn, c->wring, c->wslack, c->dyn_pieces,
+    const int64_t v[] = {c->force_ns, c->force_nf, c->force_big, c->force_exec, c->pdl, c->dyn, c->wring, c->wslack, c->tiny, c->dyn_pieces,
                          (int64_t)c->dyn_min_total, c->force_sync, c->small_sync, (int64_t)c->small_max1,
                          (int64_t)c->small_vol1, c->var_chop, c->var_tiles, c->swork, c->small_nt, c->ll,
                          (int64_t)c->one_cta_items, c->hier_staged, c->row_signal, c->ll_max, c->ll_max_ms,
@@ -2342,7 +2352,7 @@ int mpxa_plan_moves(const void *plan, int gpu, mpxa_plan_move *out, int *n) {
 
 // undocumented test hook: the execution path of the comm's last collective launch, as bits
 // 1 small kernel, 2 eager (LL), 4 variable pieces, 8 dynamic work queues, 16 row-barrier
-// sync, 32 owned flows, 64 WORK in shared memory, 128 warp-ring dynamic mode
+// sync, 32 owned flows, 64 WORK in shared memory, 128 warp-ring dynamic mode, 256 tiny kernel
 int mpxa__last_launch(mpxa_comm_t c, uint32_t *bits) {
     if (!c || !bits) return MPXA_ERR_ARG;
     *bits = c->last_path;

@@ -1985,6 +1985,90 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
     CTA_STAMP(1);
 }
 
+// ------------------------------------------------------------------------------------
+// Tiny launches: ONE step on ONE GPU (every rank local), every move cached, 16-B or 8-B
+// aligned throughout -- the small single-GPU collectives (cfg1, small alltoall / allgather /
+// alltoallv) -- as a kernel of its own.  The launch-latency floor of such calls is the
+// instruction stream a cold SM runs (each launch lands on other SMs): no flags, CTS, step
+// loop, rank table or path switches here, just resolve -> wait -> load -> store.
+// ------------------------------------------------------------------------------------
+struct TMove {
+    const char *src;
+    char *dst;          // non-fanout destination; fanout: offset inside every rank's buffer
+    uint32_t n;         // bytes
+    uint32_t fanout;    // 0, or 1 + the destination kind of a fan-out move
+};
+static_assert(sizeof(TMove) == 24, "TMove layout");
+
+__device__ __forceinline__ char *tiny_base(const ExecParams &P, char *work, int kind, int rank) {
+    return kind == BK_SEND ? (char *)P.send + (uint64_t)rank * P.send_stride
+           : kind == BK_RECV ? P.recv + (uint64_t)rank * P.recv_stride
+                             : work + (uint64_t)rank * P.work_stride;
+}
+
+template <int AW>
+__global__ void __launch_bounds__(kSmallThreads, 1) mpxa_tiny_kernel(const __grid_constant__ ExecParams P) {
+    extern __shared__ __align__(16) char tiny_dyn[];
+    TMove *tm = reinterpret_cast<TMove *>(tiny_dyn);
+    const int t = threadIdx.x;
+    const int nm = P.prog.nmoves;
+    // prologue (overlaps the previous kernel under PDL): resolve every move to pointers
+    char *const work = P.dc->work_base[0];
+    for (int i = t; i < nm; i += (int)blockDim.x) {
+        const Move m = P.prog.moves[i];
+        TMove r;
+        r.src = tiny_base(P, work, m.src_kind, m.src_rank) + (uint64_t)m.src_off * P.unit;
+        r.dst = m.fanout ? reinterpret_cast<char *>((uint64_t)m.dst_off * P.unit)
+                         : tiny_base(P, work, m.dst_kind, m.dst_rank) + (uint64_t)m.dst_off * P.unit;
+        r.n = (uint32_t)((uint64_t)m.len * P.unit);
+        r.fanout = m.fanout ? 1u + m.dst_kind : 0u;
+        tm[i] = r;
+    }
+    __syncthreads();
+    griddep_wait();
+    griddep_launch_dependents();
+    const uint32_t ppm = (uint32_t)P.small_ppm, lg = 31u - (uint32_t)__clz((int)ppm), mask = ppm - 1u;
+    const uint32_t items = (uint32_t)nm * ppm, TT = gridDim.x * blockDim.x;
+    for (uint32_t base = blockIdx.x * blockDim.x + t; base < items; base += TT * kBatch) {
+        PieceRegs<AW> R;
+        const char *sp[kBatch];
+#pragma unroll
+        for (int k = 0; k < kBatch; k++) {
+            sp[k] = nullptr;
+            const uint32_t it = base + (uint32_t)k * TT;
+            if (it >= items) continue;
+            const TMove &m = tm[it >> lg];
+            const uint32_t o = (it & mask) * 16;
+            if (o >= m.n) continue;
+            sp[k] = m.src + o;
+            R.issue(k, sp[k], min(16u, m.n - o));
+        }
+#pragma unroll
+        for (int k = 0; k < kBatch; k++) {
+            if (!sp[k]) continue;
+            const uint32_t it = base + (uint32_t)k * TT;
+            const TMove &m = tm[it >> lg];
+            const uint32_t o = (it & mask) * 16;
+            const uint32_t len = min(16u, m.n - o);
+            const uint4 val = R.value(k, sp[k]);
+            if (!m.fanout) {
+                store_piece<AW>(m.dst + o, val, len);
+            } else {
+                const uint64_t off = (uint64_t)(uintptr_t)m.dst + o;
+#pragma unroll 1
+                for (int r = 0; r < P.p; r++) store_piece<AW>(tiny_base(P, work, (int)m.fanout - 1, r) + off, val, len);
+            }
+        }
+    }
+}
+
+template <int AW>
+static cudaError_t tiny_attr() {
+    static cudaError_t e = cudaFuncSetAttribute(mpxa_tiny_kernel<AW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)(kSmallMovesSmem * sizeof(TMove)));
+    return e;
+}
+
 // Launch with the PDL attribute (pdl) or cooperatively (emulated GPUs: co-residency of the
 // virtual GPUs' CTA rows is required by the flag protocol).
 static cudaError_t launch_kernel(void (*kern)(ExecParams), const ExecParams &P, dim3 grid, dim3 block, size_t smem,
@@ -2034,6 +2118,19 @@ static cudaError_t launch_small_km(const ExecParams &P, size_t max_dyn, size_t s
     if (ak == 3) return launch_small_t<KM, 3>(P, max_dyn, smem, grid, cooperative, pdl, stream);
     if (ak == 2) return launch_small_t<KM, 2>(P, max_dyn, smem, grid, cooperative, pdl, stream);
     return launch_small_t<KM, 0>(P, max_dyn, smem, grid, cooperative, pdl, stream);
+}
+
+cudaError_t launch_tiny(const ExecParams &P, int nC, bool pdl, cudaStream_t stream) {
+    const size_t smem = (size_t)P.prog.nmoves * sizeof(TMove);
+    const int nt = P.small_threads > 0 ? P.small_threads : kSmallThreads;
+    if (P.small_a16) {
+        const cudaError_t a = tiny_attr<16>();
+        if (a != cudaSuccess) return a;
+        return launch_kernel(mpxa_tiny_kernel<16>, P, dim3(nC), dim3(nt), smem, false, pdl, stream);
+    }
+    const cudaError_t a = tiny_attr<8>();
+    if (a != cudaSuccess) return a;
+    return launch_kernel(mpxa_tiny_kernel<8>, P, dim3(nC), dim3(nt), smem, false, pdl, stream);
 }
 
 cudaError_t launch_small(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream) {
