@@ -2062,6 +2062,130 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_tiny_kernel(const __gri
     }
 }
 
+// Tiny EAGER launches: one-step eager (LL) companion programs across GPUs (modes 1 and 2):
+// every move resolved in the prologue; after the dependency wait this GPU's sends (payload
+// words, each with the launch's flag, into the peers' staging) and local copies, then its
+// receives (poll the words, copy the payload out).  The same word protocol as the general
+// kernel's eager mode (small_items_ll), in a fraction of its code.
+struct TLMove {
+    const char *src;    // local source; receive: this GPU's staging (parity 0)
+    char *dst;          // local destination; send: the peer's staging (parity 0); fan-out: offset
+    uint32_t n;         // payload bytes (0: flag-only word)
+    uint8_t ll;         // 0 local copy, 1 send, 2 receive
+    uint8_t fan;        // 0, or 1 + destination kind: the payload goes to every rank of this GPU
+    uint16_t pad;
+};
+static_assert(sizeof(TLMove) == 24, "TLMove layout");
+
+__device__ __forceinline__ char *tl_base(const ExecParams &P, int g, char *work, int kind, int rank) {
+    const uint64_t local = (uint64_t)(rank - g * P.R);
+    if (kind == BK_SEND)
+        return (char *)P.send + (P.mode == 2 ? 0 : (uint64_t)g * P.R * P.send_stride) + local * P.send_stride;
+    if (kind == BK_RECV) return P.recv + (P.mode == 1 ? (uint64_t)g * P.R * P.recv_stride : 0) + local * P.recv_stride;
+    return work + local * P.work_stride;
+}
+
+__global__ void __launch_bounds__(kSmallThreads, 1) mpxa_tiny_ll_kernel(const __grid_constant__ ExecParams P) {
+    extern __shared__ __align__(16) char tiny_dyn[];
+    TLMove *tm = reinterpret_cast<TLMove *>(tiny_dyn);
+    const int t = threadIdx.x;
+    const int g = P.mode == 1 ? (int)blockIdx.y : P.my_gpu;
+    const GpuProg prog = P.mode == 1 ? P.progs[g] : P.prog;
+    const int nm = prog.nmoves;
+    char *const work = P.dc->work_base[g];
+    for (int i = t; i < nm; i += (int)blockDim.x) {
+        const Move m = prog.moves[i];
+        TLMove r;
+        r.ll = m.dst_kind == BK_LL ? 1 : m.src_kind == BK_LL ? 2 : 0;
+        r.src = r.ll == 2 ? reinterpret_cast<const char *>(&P.dc->sym[g]->ll[0][m.src_rank][m.src_off])
+                          : tl_base(P, g, work, m.src_kind, m.src_rank) + (uint64_t)m.src_off * P.unit;
+        r.fan = m.fanout ? (uint8_t)(1 + m.dst_kind) : 0;
+        r.dst = r.ll == 1 ? reinterpret_cast<char *>(&P.dc->sym[m.dst_rank]->ll[0][g][m.dst_off])
+                : m.fanout ? reinterpret_cast<char *>((uint64_t)m.dst_off * P.unit)
+                           : tl_base(P, g, work, m.dst_kind, m.dst_rank) + (uint64_t)m.dst_off * P.unit;
+        r.n = (uint32_t)((uint64_t)m.len * P.unit);
+        r.pad = 0;
+        tm[i] = r;
+    }
+    const int nrecv = (int)prog.steps[0].wait_mask;   // receives are listed last
+    __syncthreads();
+    griddep_wait();
+    griddep_launch_dependents();
+    const uint64_t seq = *(volatile const uint64_t *)&P.dc->ll_seq + 1;
+    const uint32_t f32 = (uint32_t)seq;                // (the flag word: low 32 bits of seq)
+    const uint64_t par = (seq & 1) * sizeof(((SymRegion *)nullptr)->ll[0]);
+    const uint32_t ppm = (uint32_t)P.small_ppm, lg = 31u - (uint32_t)__clz((int)ppm), mask = ppm - 1u;
+    const uint32_t TT = gridDim.x * blockDim.x, b0 = blockIdx.x * blockDim.x + t;
+    // phase 0: local copies and sends (no waiting); phase 1: receives
+    for (int ph = 0; ph < 2; ph++) {
+        const TLMove *mv = tm + (ph ? nm - nrecv : 0);
+        const uint32_t items = (uint32_t)(ph ? nrecv : nm - nrecv) * ppm;
+        for (uint32_t it = b0; it < items; it += TT) {
+            const TLMove &m = mv[it >> lg];
+            const uint32_t o = (it & mask) * 16;
+            if (o >= m.n && !(m.ll && o == 0)) continue;
+            const uint32_t len = m.n > o ? min(16u, m.n - o) : 0u;
+            uint32_t d[4] = {0, 0, 0, 0};
+            if (m.ll == 2) {                                // poll this piece's words
+                const uint64_t *w = reinterpret_cast<const uint64_t *>(m.src + par) + o / 4;
+                const uint32_t nw = len ? (len + 3) / 4 : 1;
+                uint64_t t0 = 0;
+                for (uint32_t j = 0; j < nw; j += 2) {
+                    uint4 v = ld_ll_pair(w + j);
+                    int spins = 0;
+                    while (v.y != f32 || (j + 1 < nw && v.w != f32)) {
+                        if (++spins > 64) {
+                            __nanosleep(64);
+                            if (!t0) t0 = globaltimer();
+                            else if ((int64_t)(globaltimer() - t0) > P.timeout_ns) { atomicExch(P.err, 1); return; }
+                        }
+                        v = ld_ll_pair(w + j);
+                    }
+                    d[j] = v.x;
+                    if (j + 1 < 4) d[j + 1] = v.z;
+                }
+            } else if (len) {                               // 4-byte words of the source piece
+                const uintptr_t a = (uintptr_t)(m.src + o) & ~(uintptr_t)3;
+                const uint32_t sh = 8u * (uint32_t)((uintptr_t)(m.src + o) & 3);
+                const uint32_t *wp = (const uint32_t *)a;
+                const uintptr_t end = (uintptr_t)(m.src + o) + len;
+                uint32_t x[5];
+#pragma unroll
+                for (int q = 0; q < 5; q++) x[q] = (a + 4u * q < end) ? __ldcg(wp + q) : 0u;
+#pragma unroll
+                for (int q = 0; q < 4; q++) d[q] = __funnelshift_r(x[q], x[q + 1], sh);
+            }
+            if (m.ll == 1) {                                // send: words + flag to the peer
+                uint64_t *w = reinterpret_cast<uint64_t *>(m.dst + par) + o / 4;
+                const uint32_t nw = len ? (len + 3) / 4 : 1;
+                for (uint32_t j = 0; j < nw; j += 2) {
+                    if (j + 1 < nw) st_ll_pair(w + j, d[j], d[j + 1], f32);
+                    else st_relaxed_sys(w + j, ((uint64_t)f32 << 32) | d[j]);
+                }
+                continue;
+            }
+            if (!len) continue;
+            const uint4 val = make_uint4(d[0], d[1], d[2], d[3]);
+            if (m.fan) {
+                const uint64_t off = (uint64_t)(uintptr_t)m.dst + o;
+#pragma unroll 1
+                for (int r = g * P.R; r < (g + 1) * P.R; r++)
+                    store_piece<0>(tl_base(P, g, work, m.fan - 1, r) + off, val, len);
+            } else {
+                store_piece<0>(m.dst + o, val, len);
+            }
+        }
+    }
+    // the launch's last CTA publishes the sequence number and the epoch (the general kernel's
+    // eager launches advance both)
+    __syncthreads();
+    if (t == 0 && atom_acq_rel_gpu_add(&P.dc->done_ctas, 1u) == gridDim.x * gridDim.y - 1) {
+        P.dc->done_ctas = 0;
+        P.dc->epoch = *(volatile uint64_t *)&P.dc->epoch + 1;
+        P.dc->ll_seq = seq;
+    }
+}
+
 template <int AW>
 static cudaError_t tiny_attr() {
     static cudaError_t e = cudaFuncSetAttribute(mpxa_tiny_kernel<AW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2131,6 +2255,21 @@ cudaError_t launch_tiny(const ExecParams &P, int nC, bool pdl, cudaStream_t stre
     const cudaError_t a = tiny_attr<8>();
     if (a != cudaSuccess) return a;
     return launch_kernel(mpxa_tiny_kernel<8>, P, dim3(nC), dim3(nt), smem, false, pdl, stream);
+}
+
+cudaError_t launch_tiny_ll(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream) {
+    static cudaError_t a = cudaFuncSetAttribute(mpxa_tiny_ll_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)(kSmallMovesSmem * sizeof(TLMove)));
+    if (a != cudaSuccess) return a;
+    int nmax = 0;   // the largest program of any GPU (emulated rows share the launch)
+    if (P.mode == 1) {
+        nmax = P.small_cache;
+    } else {
+        nmax = P.prog.nmoves;
+    }
+    const int nt = P.small_threads > 0 ? P.small_threads : kSmallThreads;
+    return launch_kernel(mpxa_tiny_ll_kernel, P, dim3(nC, nG), dim3(nt), (size_t)nmax * sizeof(TLMove), cooperative,
+                         pdl, stream);
 }
 
 cudaError_t launch_small(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream) {

@@ -1,5 +1,6 @@
-"""Small-message latency, single GPU p = P ranks (default 8): alltoall and allgather device us
-per call (CUDA graph of 200 calls) at SIZES bytes, under KNOBS="A=1;B=2" ('' = defaults)."""
+"""Small-message latency, single GPU p = P ranks (default 8; EMU = G emulated GPUs): alltoall and
+allgather device us per call (CUDA graph of 200 calls) at SIZES bytes, under KNOBS="A=1;B=2"
+('' = defaults)."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
@@ -12,7 +13,7 @@ for cfg in os.environ.get("KNOBS", "").split(";"):
     env = dict(kv.split("=") for kv in cfg.split(",") if kv)
     for k, v in env.items():
         os.environ[k] = v
-    c = Comm(ranks_per_proc=p, device=0)
+    c = Comm(ranks_per_proc=p, device=0, emulate_gpus=int(os.environ.get("EMU", "0")))
     for k in env:
         del os.environ[k]
     row = {}
@@ -20,6 +21,7 @@ for cfg in os.environ.get("KNOBS", "").split(";"):
         s = torch.randint(0, 255, (p, p * b), dtype=torch.uint8, device="cuda")
         r = torch.empty_like(s)
         row[f"a2a_{b}"] = round(t(lambda: c.alltoall(s, r, algo="pairwise"), it=200), 3)
+        row[f"a2a_{b}_path"] = sorted(c.last_launch_path())
         s2 = s[:, :b].contiguous()
         row[f"ag_{b}"] = round(t(lambda: c.allgather(s2, r[:, : p * b], algo="pairwise"), it=200), 3)
     # the launch floor: a trivial torch copy of the same bytes
