@@ -949,11 +949,10 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
             while (nt < 512 && (nt < per_cta || nt < (uint64_t)c->p || nt < (uint64_t)dp.nsteps)) nt *= 2;
             if (nt < 512) E.small_threads = (int32_t)nt;
         }
-        // one step on one GPU, every move cached, 16- or 8-B aligned: the tiny kernel (no flags,
+        // one step on one GPU, every move cached: the tiny kernel (no flags,
         // steps or rank tables -- the shortest instruction stream for a cold SM)
         tiny = c->tiny && one_step && c->G == 1 && !c->emulated && c->nprocs == 1 && !E.small_var &&
-               !E.small_own && !E.small_ll && E.small_cache > 0 && (E.small_a16 || E.small_a8) &&
-               sp == &dp;
+               !E.small_own && !E.small_ll && E.small_cache > 0 && sp == &dp;
         // one-step eager launches across GPUs: the tiny eager kernel (same word protocol)
         const bool tiny_ll = c->tiny && one_step && E.small_ll && !E.small_var && !E.small_own && E.small_cache > 0;
         if (tiny) e = launch_tiny(E, std::max(1, nC), pdl && c->pdl, stream);

@@ -1986,8 +1986,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_small_kernel(const __gr
 }
 
 // ------------------------------------------------------------------------------------
-// Tiny launches: ONE step on ONE GPU (every rank local), every move cached, 16-B or 8-B
-// aligned throughout -- the small single-GPU collectives (cfg1, small alltoall / allgather /
+// Tiny launches: ONE step on ONE GPU (every rank local), every move cached -- the small
+// single-GPU collectives (cfg1, small alltoall / allgather /
 // alltoallv) -- as a kernel of its own.  The launch-latency floor of such calls is the
 // instruction stream a cold SM runs (each launch lands on other SMs): no flags, CTS, step
 // loop, rank table or path switches here, just resolve -> wait -> load -> store.
@@ -2252,9 +2252,14 @@ cudaError_t launch_tiny(const ExecParams &P, int nC, bool pdl, cudaStream_t stre
         if (a != cudaSuccess) return a;
         return launch_kernel(mpxa_tiny_kernel<16>, P, dim3(nC), dim3(nt), smem, false, pdl, stream);
     }
-    const cudaError_t a = tiny_attr<8>();
+    if (P.small_a8) {
+        const cudaError_t a = tiny_attr<8>();
+        if (a != cudaSuccess) return a;
+        return launch_kernel(mpxa_tiny_kernel<8>, P, dim3(nC), dim3(nt), smem, false, pdl, stream);
+    }
+    const cudaError_t a = tiny_attr<0>();   // any alignment: 4-byte words and funnel shifts
     if (a != cudaSuccess) return a;
-    return launch_kernel(mpxa_tiny_kernel<8>, P, dim3(nC), dim3(nt), smem, false, pdl, stream);
+    return launch_kernel(mpxa_tiny_kernel<0>, P, dim3(nC), dim3(nt), smem, false, pdl, stream);
 }
 
 cudaError_t launch_tiny_ll(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream) {

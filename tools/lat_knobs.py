@@ -24,6 +24,7 @@ for cfg in os.environ.get("KNOBS", "").split(";"):
         row[f"a2a_{b}_path"] = sorted(c.last_launch_path())
         s2 = s[:, :b].contiguous()
         row[f"ag_{b}"] = round(t(lambda: c.allgather(s2, r[:, : p * b], algo="pairwise"), it=200), 3)
+        row[f"ag_{b}_path"] = sorted(c.last_launch_path())
     # the launch floor: a trivial torch copy of the same bytes
     x = torch.empty(16, dtype=torch.uint8, device="cuda")
     y = torch.empty_like(x)
