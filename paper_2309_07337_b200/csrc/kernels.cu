@@ -255,7 +255,6 @@ __device__ uint64_t g_cta_trace[2][kMaxCtas];   // per-CTA entry / exit %globalt
 #define TRACE(k) do { } while (0)
 #define CTA_STAMP(w) do { } while (0)
 #endif
-constexpr int kMaxStepsSmem = 64;
 static_assert(kMoveTile <= kThreads, "prologue prefetch: one move per thread");
 struct StepInfo {
     int32_t first;          // index of this CTA's first move (flow group range start)
@@ -2186,6 +2185,82 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_tiny_ll_kernel(const __
     }
 }
 
+// Tiny MULTI-STEP launches: several steps on one GPU in ONE CTA (Bruck, ring, hierarchical at
+// small sizes), every move cached -- steps separated by __syncthreads only (a step reads what
+// earlier steps of this CTA wrote).
+template <int AW>
+__global__ void __launch_bounds__(kSmallThreads, 1) mpxa_tiny_ms_kernel(const __grid_constant__ ExecParams P) {
+    extern __shared__ __align__(16) char tiny_dyn[];
+    __shared__ int2 st[kMaxStepsSmem];
+    TMove *tm = reinterpret_cast<TMove *>(tiny_dyn);
+    const int t = threadIdx.x;
+    const int nm = P.prog.nmoves, ns = P.prog.nsteps;
+    char *const work = P.dc->work_base[0];
+    if (t < ns) {
+        const Step s = P.prog.steps[t];
+        st[t] = make_int2(s.move_begin, s.move_end);
+    }
+    for (int i = t; i < nm; i += (int)blockDim.x) {
+        const Move m = P.prog.moves[i];
+        TMove r;
+        r.src = tiny_base(P, work, m.src_kind, m.src_rank) + (uint64_t)m.src_off * P.unit;
+        r.dst = m.fanout ? reinterpret_cast<char *>((uint64_t)m.dst_off * P.unit)
+                         : tiny_base(P, work, m.dst_kind, m.dst_rank) + (uint64_t)m.dst_off * P.unit;
+        r.n = (uint32_t)((uint64_t)m.len * P.unit);
+        r.fanout = m.fanout ? 1u + m.dst_kind : 0u;
+        tm[i] = r;
+    }
+    __syncthreads();
+    griddep_wait();
+    griddep_launch_dependents();
+    const uint32_t ppm = (uint32_t)P.small_ppm, lg = 31u - (uint32_t)__clz((int)ppm), mask = ppm - 1u;
+    const uint32_t TT = blockDim.x;
+    for (int s = 0; s < ns; s++) {
+        const TMove *mv = tm + st[s].x;
+        const uint32_t items = (uint32_t)(st[s].y - st[s].x) * ppm;
+        for (uint32_t base = t; base < items; base += TT * kBatch) {
+            PieceRegs<AW> R;
+            const char *sp[kBatch];
+#pragma unroll
+            for (int k = 0; k < kBatch; k++) {
+                sp[k] = nullptr;
+                const uint32_t it = base + (uint32_t)k * TT;
+                if (it >= items) continue;
+                const TMove &m = mv[it >> lg];
+                const uint32_t o = (it & mask) * 16;
+                if (o >= m.n) continue;
+                sp[k] = m.src + o;
+                R.issue(k, sp[k], min(16u, m.n - o));
+            }
+#pragma unroll
+            for (int k = 0; k < kBatch; k++) {
+                if (!sp[k]) continue;
+                const uint32_t it = base + (uint32_t)k * TT;
+                const TMove &m = mv[it >> lg];
+                const uint32_t o = (it & mask) * 16;
+                const uint32_t len = min(16u, m.n - o);
+                const uint4 val = R.value(k, sp[k]);
+                if (!m.fanout) {
+                    store_piece<AW>(m.dst + o, val, len);
+                } else {
+                    const uint64_t off = (uint64_t)(uintptr_t)m.dst + o;
+#pragma unroll 1
+                    for (int r = 0; r < P.p; r++) store_piece<AW>(tiny_base(P, work, (int)m.fanout - 1, r) + off, val, len);
+                }
+            }
+        }
+        __syncthreads();   // this step's writes before the next step's reads
+    }
+}
+
+template <int AW>
+static cudaError_t tiny_ms_attr() {
+    static cudaError_t e = cudaFuncSetAttribute(mpxa_tiny_ms_kernel<AW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)(kSmallMovesSmem * sizeof(TMove)));
+    return e;
+}
+
+
 template <int AW>
 static cudaError_t tiny_attr() {
     static cudaError_t e = cudaFuncSetAttribute(mpxa_tiny_kernel<AW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2242,6 +2317,22 @@ static cudaError_t launch_small_km(const ExecParams &P, size_t max_dyn, size_t s
     if (ak == 3) return launch_small_t<KM, 3>(P, max_dyn, smem, grid, cooperative, pdl, stream);
     if (ak == 2) return launch_small_t<KM, 2>(P, max_dyn, smem, grid, cooperative, pdl, stream);
     return launch_small_t<KM, 0>(P, max_dyn, smem, grid, cooperative, pdl, stream);
+}
+
+cudaError_t launch_tiny_ms(const ExecParams &P, bool pdl, cudaStream_t stream) {
+    const size_t smem = (size_t)P.prog.nmoves * sizeof(TMove);
+    const int nt = P.small_threads > 0 ? P.small_threads : kSmallThreads;
+    cudaError_t a;
+    if (P.small_a16) {
+        if ((a = tiny_ms_attr<16>()) != cudaSuccess) return a;
+        return launch_kernel(mpxa_tiny_ms_kernel<16>, P, dim3(1), dim3(nt), smem, false, pdl, stream);
+    }
+    if (P.small_a8) {
+        if ((a = tiny_ms_attr<8>()) != cudaSuccess) return a;
+        return launch_kernel(mpxa_tiny_ms_kernel<8>, P, dim3(1), dim3(nt), smem, false, pdl, stream);
+    }
+    if ((a = tiny_ms_attr<0>()) != cudaSuccess) return a;
+    return launch_kernel(mpxa_tiny_ms_kernel<0>, P, dim3(1), dim3(nt), smem, false, pdl, stream);
 }
 
 cudaError_t launch_tiny(const ExecParams &P, int nC, bool pdl, cudaStream_t stream) {

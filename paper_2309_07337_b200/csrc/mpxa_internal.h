@@ -34,6 +34,7 @@ constexpr TmaConfig kTmaBig = {kRingStages, 32768, 4};
 constexpr int kMaxDynSmem = 6 * 32768;
 constexpr int kMoveTile = kThreads;   // moves staged in shared memory at a time (one per thread)
 constexpr int kMaxDynTiles = 64;      // dynamic mode: move tiles per step (queues per tile)
+constexpr int kMaxStepsSmem = 64;     // step tables kept in shared memory by the kernels
 // warp-ring dynamic mode (ExecParams::wring): every warp of the CTA is its own TMA pipeline
 // over a ring of kWStages stages of kWChunk bytes (same 96 KiB of dynamic shared memory as
 // the mid ring, so 2 CTAs / SM); moves that are not 16-B congruent are stored by the warp

@@ -697,8 +697,14 @@ def test_execution_paths_are_the_intended_ones(monkeypatch):
     p = 8
     c1 = comm(p, 0, 2)
     send = synth.alltoall_sendbuf(1, p, 16)
-    run_alltoall(c1, send, "bruck")
-    assert {"small", "swork"} <= c1.last_launch_path() and "eager" not in c1.last_launch_path()
+    run_alltoall(c1, send, "bruck")          # one CTA, several steps, one GPU: the tiny kernel
+    assert {"small", "tiny"} <= c1.last_launch_path() and "eager" not in c1.last_launch_path()
+    monkeypatch.setenv("MPXA_NO_TINY", "1")   # the general kernel: WORK rows in shared memory
+    cg = Comm(ranks_per_proc=p, device=0, group_size=2, timeout_s=20.0)
+    assert np.array_equal(run_alltoall(cg, send, "bruck"), oracle.alltoall_definition(send))
+    assert {"small", "swork"} <= cg.last_launch_path() and "tiny" not in cg.last_launch_path()
+    cg.finalize()
+    monkeypatch.delenv("MPXA_NO_TINY")
     c4 = comm(p, 4, 2)
     run_alltoall(c4, send, "pairwise")
     assert {"small", "eager"} <= c4.last_launch_path()

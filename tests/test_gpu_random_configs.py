@@ -120,7 +120,9 @@ KNOBS = [{"MPXA_NO_LL": "1"}, {"MPXA_NO_SMALL": "1"}, {"MPXA_NO_DYN": "1"}, {"MP
          {"MPXA_SMALL_NT": "512"}, {"MPXA_NO_PDL": "1"}, {"MPXA_NO_SMALL_SYNC": "1"},
          {"MPXA_HIER_STAGED": "1"}, {"MPXA_ROW_SIGNAL": "0", "MPXA_NO_SMALL": "1"},
          # every dynamic launch through the per-warp TMA rings, multi-step programs included
-         {"MPXA_WRING": "2", "MPXA_DYN_SYNC": "1", "MPXA_NO_SMALL": "1"}]
+         {"MPXA_WRING": "2", "MPXA_DYN_SYNC": "1", "MPXA_NO_SMALL": "1"},
+         # the general small kernel for launches the tiny kernels would take
+         {"MPXA_NO_TINY": "1"}]
 
 
 @pytest.mark.parametrize("knob", range(len(KNOBS)), ids=[",".join(k) for k in KNOBS])
