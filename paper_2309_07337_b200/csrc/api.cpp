@@ -33,7 +33,7 @@ namespace mpxa {
 cudaError_t launch_exec(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream);
 cudaError_t launch_small(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream);
 cudaError_t launch_tiny(const ExecParams &P, int nC, bool pdl, cudaStream_t stream);
-cudaError_t launch_tiny_ms(const ExecParams &P, bool pdl, cudaStream_t stream);
+cudaError_t launch_tiny_ms(const ExecParams &P, int nC, bool pdl, cudaStream_t stream);
 cudaError_t launch_tiny_ll(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream);
 cudaError_t launch_counts(const int64_t *sc, int64_t *rc, int64_t *rd, int p, int r0, int nr,
                           cudaStream_t stream);
@@ -955,15 +955,15 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
         tiny = c->tiny && one_step && c->G == 1 && !c->emulated && c->nprocs == 1 && !E.small_var &&
                !E.small_own && !E.small_ll && E.small_cache > 0 && sp == &dp;
         // several steps, one CTA, one GPU, every move cached: the tiny multi-step kernel
-        const bool tiny_ms = c->tiny && !one_step && c->G == 1 && !c->emulated && c->nprocs == 1 && nC <= 1 &&
-                             !E.small_var && !E.small_own && !E.dyn_sync && !E.small_ll && E.small_cache > 0 &&
-                             dp.nsteps <= kMaxStepsSmem && sp == &dp;
+        const bool tiny_ms = c->tiny && !one_step && c->G == 1 && !c->emulated && c->nprocs == 1 &&
+                             (nC <= 1 || E.small_own > 1) && !E.small_var && !E.dyn_sync && !E.small_ll &&
+                             E.small_cache > 0 && dp.nsteps <= kMaxStepsSmem && sp == &dp;
         // one-step eager launches across GPUs: the tiny eager kernel (same word protocol)
         const bool tiny_ll = c->tiny && one_step && E.small_ll && !E.small_var && !E.small_own && E.small_cache > 0;
         if (tiny) e = launch_tiny(E, std::max(1, nC), pdl && c->pdl, stream);
         else if (tiny_ms) {
             E.small_swork = 0;   // (the tiny multi-step kernel keeps WORK in global memory / L2)
-            e = launch_tiny_ms(E, pdl && c->pdl, stream);
+            e = launch_tiny_ms(E, std::max(1, nC), pdl && c->pdl, stream);
         }
         else if (tiny_ll)
             e = launch_tiny_ll(E, std::max(1, nC), c->emulated ? c->G : 1, c->emulated, pdl && c->pdl, stream);

@@ -2185,9 +2185,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_tiny_ll_kernel(const __
     }
 }
 
-// Tiny MULTI-STEP launches: several steps on one GPU in ONE CTA (Bruck, ring, hierarchical at
-// small sizes), every move cached -- steps separated by __syncthreads only (a step reads what
-// earlier steps of this CTA wrote).
+// Tiny MULTI-STEP launches: several steps on one GPU (Bruck, ring, hierarchical at small
+// sizes), every move cached, in one CTA or in several CTAs that each own a set of flows --
+// steps separated by __syncthreads only (a step reads what earlier steps of this CTA wrote).
 template <int AW>
 __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_tiny_ms_kernel(const __grid_constant__ ExecParams P) {
     extern __shared__ __align__(16) char tiny_dyn[];
@@ -2196,19 +2196,39 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_tiny_ms_kernel(const __
     const int t = threadIdx.x;
     const int nm = P.prog.nmoves, ns = P.prog.nsteps;
     char *const work = P.dc->work_base[0];
-    if (t < ns) {
-        const Step s = P.prog.steps[t];
-        st[t] = make_int2(s.move_begin, s.move_end);
-    }
-    for (int i = t; i < nm; i += (int)blockDim.x) {
-        const Move m = P.prog.moves[i];
+    auto resolve = [&](const Move &m) {
         TMove r;
         r.src = tiny_base(P, work, m.src_kind, m.src_rank) + (uint64_t)m.src_off * P.unit;
         r.dst = m.fanout ? reinterpret_cast<char *>((uint64_t)m.dst_off * P.unit)
                          : tiny_base(P, work, m.dst_kind, m.dst_rank) + (uint64_t)m.dst_off * P.unit;
         r.n = (uint32_t)((uint64_t)m.len * P.unit);
         r.fanout = m.fanout ? 1u + m.dst_kind : 0u;
-        tm[i] = r;
+        return r;
+    };
+    if (P.small_own > 1) {
+        // owned flows (several CTAs): this CTA keeps, step by step, only the moves of the flows
+        // f with f % small_own == its index -- the same CTA moves a flow through every step,
+        // so the steps still need no barrier but __syncthreads
+        __shared__ uint32_t cnt;
+        if (t == 0) cnt = 0;
+        __syncthreads();
+        for (int s = 0; s < ns; s++) {
+            const Step sp = P.prog.steps[s];
+            const uint32_t b = cnt;
+            __syncthreads();
+            for (int i = sp.move_begin + t; i < sp.move_end; i += (int)blockDim.x) {
+                const Move m = P.prog.moves[i];
+                if ((int)(m.flow % (uint32_t)P.small_own) == (int)blockIdx.x) tm[atomicAdd(&cnt, 1u)] = resolve(m);
+            }
+            __syncthreads();
+            if (t == 0) st[s] = make_int2((int)b, (int)cnt);
+        }
+    } else {
+        if (t < ns) {
+            const Step s = P.prog.steps[t];
+            st[t] = make_int2(s.move_begin, s.move_end);
+        }
+        for (int i = t; i < nm; i += (int)blockDim.x) tm[i] = resolve(P.prog.moves[i]);
     }
     __syncthreads();
     griddep_wait();
@@ -2319,20 +2339,20 @@ static cudaError_t launch_small_km(const ExecParams &P, size_t max_dyn, size_t s
     return launch_small_t<KM, 0>(P, max_dyn, smem, grid, cooperative, pdl, stream);
 }
 
-cudaError_t launch_tiny_ms(const ExecParams &P, bool pdl, cudaStream_t stream) {
+cudaError_t launch_tiny_ms(const ExecParams &P, int nC, bool pdl, cudaStream_t stream) {
     const size_t smem = (size_t)P.prog.nmoves * sizeof(TMove);
     const int nt = P.small_threads > 0 ? P.small_threads : kSmallThreads;
     cudaError_t a;
     if (P.small_a16) {
         if ((a = tiny_ms_attr<16>()) != cudaSuccess) return a;
-        return launch_kernel(mpxa_tiny_ms_kernel<16>, P, dim3(1), dim3(nt), smem, false, pdl, stream);
+        return launch_kernel(mpxa_tiny_ms_kernel<16>, P, dim3(nC), dim3(nt), smem, false, pdl, stream);
     }
     if (P.small_a8) {
         if ((a = tiny_ms_attr<8>()) != cudaSuccess) return a;
-        return launch_kernel(mpxa_tiny_ms_kernel<8>, P, dim3(1), dim3(nt), smem, false, pdl, stream);
+        return launch_kernel(mpxa_tiny_ms_kernel<8>, P, dim3(nC), dim3(nt), smem, false, pdl, stream);
     }
     if ((a = tiny_ms_attr<0>()) != cudaSuccess) return a;
-    return launch_kernel(mpxa_tiny_ms_kernel<0>, P, dim3(1), dim3(nt), smem, false, pdl, stream);
+    return launch_kernel(mpxa_tiny_ms_kernel<0>, P, dim3(nC), dim3(nt), smem, false, pdl, stream);
 }
 
 cudaError_t launch_tiny(const ExecParams &P, int nC, bool pdl, cudaStream_t stream) {
