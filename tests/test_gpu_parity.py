@@ -705,6 +705,13 @@ def test_execution_paths_are_the_intended_ones(monkeypatch):
     assert {"small", "swork"} <= cg.last_launch_path() and "tiny" not in cg.last_launch_path()
     cg.finalize()
     monkeypatch.delenv("MPXA_NO_TINY")
+    # mid-size multi-step on one GPU: the tiny kernel over several CTAs owning flows
+    ag4 = np.random.default_rng(4).integers(0, 256, size=(p, 4096 + 8), dtype=np.uint8)
+    d_r4 = torch.full((p, p * ag4.shape[1]), 0x5A, dtype=torch.uint8, device=DEV)
+    for algo in ("ring", "bruck"):
+        c1.allgather(dev(ag4), d_r4, algo=algo)
+        assert {"small", "tiny", "own"} <= c1.last_launch_path(), algo
+        assert np.array_equal(host(d_r4), oracle.allgather_definition(ag4)), algo
     c4 = comm(p, 4, 2)
     run_alltoall(c4, send, "pairwise")
     assert {"small", "eager"} <= c4.last_launch_path()
