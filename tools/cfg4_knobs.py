@@ -1,6 +1,7 @@
-"""cfg4 alltoallv (p = 8) device time per persistent start+wait (CUDA graph) with the warp
-rings filled by TMA loads (default) vs per-lane cp.async (MPXA_WLOAD=1, two load windows),
-int64 and int32 segments, means 1-8 MiB; every variant's output compared with the default's."""
+"""cfg4 alltoallv (p = 8) device time per persistent start+wait (CUDA graph) under knob sets
+(VARIANTS='{"name": {"ENV": "val"}, ...}', first = reference), int64 and int32 segments
+(ELEMS), means in MiB (MEANS); every variant's output compared with the first's.  (Used for
+the round-2 cp.async warp-ring experiment, MPXA_WLOAD, since removed: profiles/r02/shift_probe.txt.)"""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
@@ -11,8 +12,7 @@ import timing
 from timing import t
 GS = timing.GS
 p = 8
-VARIANTS = (("tma", {}), ("ldg_s2", {"MPXA_WLOAD": "1"}), ("ldg_s1", {"MPXA_WLOAD": "1", "MPXA_WSLACK": "1"}),
-            ("tma_s1", {"MPXA_WSLACK": "1"}))
+VARIANTS = tuple(json.loads(os.environ.get("VARIANTS", '{"default": {}}')).items())
 comms = {}
 for name, env in VARIANTS:
     for k, v in env.items():
@@ -21,7 +21,7 @@ for name, env in VARIANTS:
     for k in env:
         del os.environ[k]
 res = {}
-for elem in (8, 4):
+for elem in (int(x) for x in os.environ.get("ELEMS", "8,4").split(",")):
     for mean in (int(x) for x in os.environ.get("MEANS", "1,2,4,8").split(",")):
         for seed in (0, 1):
             c4 = synth.cfg4_counts(seed, p, mean << 20, elem=8) * 8 // elem
@@ -40,7 +40,7 @@ for elem in (8, 4):
                 else:
                     ok = bool(torch.equal(ref, d_r))
                 moved = int(sc.sum()) * elem
-                res[f"e{elem}_m{mean}_s{seed}_{name}"] = [round(us, 1), round(2 * moved / us / 1e6 / 6543.7, 4),
+                res[f"e{elem}_m{mean}_s{seed}_{name}"] = [round(us, 1), round(2 * moved / us / 1e3 / 6543.7, 4),
                                                          ok, sorted(c.last_launch_path())]
                 q.free()
                 del d_r
