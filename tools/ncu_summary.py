@@ -6,7 +6,11 @@ KEYS = [r"^gpu__time_duration.sum$", r"^dram__bytes_(read|write)\.sum$", r"^dram
         r"^sm__warps_active.avg.pct_of_peak_sustained_active$", r"^lts__throughput.avg.pct_of_peak_sustained_elapsed$",
         r"^l1tex__throughput.avg.pct_of_peak_sustained_elapsed$", r"^sm__throughput.avg.pct_of_peak_sustained_elapsed$",
         r"^launch__shared_mem_per_block_(dynamic|static)$", r"^smsp__inst_executed.sum$",
-        r"^nvlrx__bytes.sum$", r"^nvltx__bytes.sum$"]
+        r"^nvlrx__bytes.sum$", r"^nvltx__bytes.sum$",
+        r"^smsp__sass_inst_executed_op_(global|shared)_(ld|st)\.sum$",
+        r"^l1tex__t_(sectors|requests)_pipe_lsu_mem_global_op_(ld|st)\.sum$",
+        r"^sm__ctas_launched\.sum$", r"^launch__occupancy_per_block_size$",
+        r"^sm__maximum_warps_per_active_cycle_pct$", r"^launch__waves_per_multiprocessor$"]
 
 
 def report(path):
