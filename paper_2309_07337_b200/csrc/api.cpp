@@ -67,7 +67,11 @@ constexpr uint64_t kSliceBytes = 16384;    // target column-slice length of the 
 constexpr uint64_t kMovesPerCta = 1;       // moves per CTA (latency-bound regime: one each)
 constexpr uint64_t kMinSlice = 2048;       // smallest slice worth a CTA when filling the GPU (= TMA min)
 constexpr uint64_t kBigPerCta = 1u << 20;  // bytes per CTA per step above which the big TMA config wins
-constexpr uint64_t kSmallItemsPerCta = 2048;   // small kernel: 16-B pieces per CTA per step (one batch)
+// small kernel: 16-B pieces per CTA per step -- about one per thread, so more CTAs share the
+// bytes of a launch (measured, p = 8 one GPU: alltoall 1 / 4 / 16 KiB blocks 1.75 / 1.74 / 1.74
+// -> 1.14 / 1.17 / 1.53 us going from 2048 to 256 pieces per CTA); fan-out pieces (allgather
+// direct: one load, R stores) half of it (allgather 1 / 4 KiB 2.06 / 2.09 -> 1.48 / 1.51 us)
+constexpr uint64_t kSmallItemsPerCta = 256;
 constexpr uint64_t kSmallOneStepMove = 2u << 20;   // single-step programs: longest move ...
 constexpr uint64_t kSmallOneStepVol = 32u << 20;   // ... and source bytes per GPU for the small kernel
                                                     // (re-measured after the small-kernel work:
@@ -104,6 +108,7 @@ struct DevProg {
     int64_t max_gpu_bytes_units = 0;  // single-step programs: most units any GPU moves (source side)
     int64_t dyn_tiles = 0;          // sum over steps of the most move tiles any GPU has in the step
     bool uniform_len = true;        // every move of the program has the same length
+    bool fanout = false;            // some move writes every rank of a GPU (allgather direct)
     bool per_call = false;          // tables live in a ring slot (run_dynamic): no companions
     // Companion programs, built on first use and kept until the parent is freed: a CUDA graph
     // or a persistent request may hold device pointers into any of them, so a companion is
@@ -130,9 +135,12 @@ void prog_facts(DevProg &dp) {
         dp.dyn_tiles += std::max<int64_t>(1, (mx + kMoveTile - 1) / kMoveTile);
     }
     dp.uniform_len = true;
+    dp.fanout = false;
     for (const auto &mv : P.moves)
-        for (const Move &m : mv)
-            if (m.len != P.max_move) { dp.uniform_len = false; break; }
+        for (const Move &m : mv) {
+            if (m.len != P.max_move) dp.uniform_len = false;
+            if (m.fanout) dp.fanout = true;
+        }
     for (const auto &mv : P.moves) {
         dp.max_gpu_moves = std::max<int64_t>(dp.max_gpu_moves, (int64_t)mv.size());
         int64_t u = 0;
@@ -224,6 +232,7 @@ struct mpxa_comm_s {
     int small_nt = 64;                     // small kernel block size for launches with few pieces
     bool ll = true;                        // eager (LL) mode for small multi-GPU launches
     uint64_t one_cta_items = kSmallItemsOneCta;  // MPXA_ONE_CTA_ITEMS (tuning)
+    uint64_t small_items = kSmallItemsPerCta;    // MPXA_SMALL_ITEMS: 16-B pieces per small-kernel CTA
     bool row_signal = true;                // MPXA_ROW_SIGNAL=0: executor steps signalled per (CTA, peer)
     bool hier_staged = false;              // MPXA_HIER_STAGED=1: hierarchical with group = GPU in its
                                            // literal three-step form instead of the fused one
@@ -855,7 +864,8 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
     // (measured: it wins where the static executor is poorly balanced -- uneven moves, or few
     // flows to spread over CTAs as in the allgathers; uniform alltoalls keep the barrier-free
     // static executor)
-    const uint64_t n_own = std::max<uint64_t>(1, std::min<uint64_t>(std::min<uint64_t>(cdiv(items, kSmallItemsPerCta),
+    const uint64_t per_cta = dp.fanout ? std::max<uint64_t>(32, c->small_items / 2) : c->small_items;
+    const uint64_t n_own = std::max<uint64_t>(1, std::min<uint64_t>(std::min<uint64_t>(cdiv(items, per_cta),
                                                                                           (uint64_t)dp.host.nflows),
                                                                      (uint64_t)c->cap_small));
     const bool own_ok = dp.uniform_len && step_vol <= kSmallOwnVol && step_vol / n_own <= kSmallOwnPerCta;
@@ -919,7 +929,7 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
         for (const auto &mv : sp->host.moves) nmoves_g = std::max(nmoves_g, mv.size());
         E.small_cache = nmoves_g <= (size_t)kSmallMovesSmem ? (int32_t)nmoves_g : 0;
         int nC = (one_step || small_sync || small_own)
-                     ? (int)std::min<uint64_t>(cdiv(items, kSmallItemsPerCta), (uint64_t)c->cap_small) : 1;
+                     ? (int)std::min<uint64_t>(cdiv(items, per_cta), (uint64_t)c->cap_small) : 1;
         if (small_own) nC = std::min<int>(nC, dp.host.nflows);
         E.dyn_sync = small_sync && nC > 1;
         E.small_own = small_own && nC > 1 ? nC : 0;
@@ -1444,6 +1454,7 @@ void read_knobs(mpxa_comm_t c) {
     if (const char *e = getenv("MPXA_SMALL_NT")) c->small_nt = std::max(32, std::min(512, atoi(e)));
     if (const char *e = getenv("MPXA_NO_LL")) c->ll = atoi(e) == 0;
     if (const char *e = getenv("MPXA_ONE_CTA_ITEMS")) c->one_cta_items = strtoull(e, nullptr, 10);
+    if (const char *e = getenv("MPXA_SMALL_ITEMS")) c->small_items = std::max<uint64_t>(64, strtoull(e, nullptr, 10));
     if (const char *e = getenv("MPXA_HIER_STAGED")) c->hier_staged = atoi(e) != 0;
     if (const char *e = getenv("MPXA_ROW_SIGNAL")) c->row_signal = atoi(e) != 0;
     if (const char *e = getenv("MPXA_LL_MAX")) c->ll_max = atoll(e);
@@ -1482,7 +1493,7 @@ uint64_t knob_digest(mpxa_comm_t c, size_t heap) {
     const int64_t v[] = {c->force_ns, c->force_nf, c->force_big, c->force_exec, c->pdl, c->dyn, c->wring, c->wslack, c->tiny, c->dyn_pieces,
                          (int64_t)c->dyn_min_total, c->force_sync, c->small_sync, (int64_t)c->small_max1,
                          (int64_t)c->small_vol1, c->var_chop, c->var_tiles, c->swork, c->small_nt, c->ll,
-                         (int64_t)c->one_cta_items, c->hier_staged, c->row_signal, c->ll_max, c->ll_max_ms,
+                         (int64_t)c->one_cta_items, (int64_t)c->small_items, c->hier_staged, c->row_signal, c->ll_max, c->ll_max_ms,
                          c->user_algo[0], c->user_algo[1], c->user_algo[2], (int64_t)heap,
                          (int64_t)c->selector.size()};
     uint64_t h = fnv(1469598103934665603ull, v, sizeof v);

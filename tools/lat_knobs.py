@@ -1,6 +1,6 @@
 """Small-message latency, single GPU p = P ranks (default 8; EMU = G emulated GPUs): alltoall and
 allgather device us per call (CUDA graph of 200 calls) at SIZES bytes, under KNOBS="A=1;B=2"
-('' = defaults)."""
+('' = defaults), for the variants in ALGOS (default pairwise; allgather maps hier -> ring)."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
@@ -17,14 +17,17 @@ for cfg in os.environ.get("KNOBS", "").split(";"):
     for k in env:
         del os.environ[k]
     row = {}
-    for b in sizes:
-        s = torch.randint(0, 255, (p, p * b), dtype=torch.uint8, device="cuda")
-        r = torch.empty_like(s)
-        row[f"a2a_{b}"] = round(t(lambda: c.alltoall(s, r, algo="pairwise"), it=200), 3)
-        row[f"a2a_{b}_path"] = sorted(c.last_launch_path())
-        s2 = s[:, :b].contiguous()
-        row[f"ag_{b}"] = round(t(lambda: c.allgather(s2, r[:, : p * b], algo="pairwise"), it=200), 3)
-        row[f"ag_{b}_path"] = sorted(c.last_launch_path())
+    for algo in os.environ.get("ALGOS", "pairwise").split(","):
+        sfx = "" if algo == "pairwise" else "_" + algo
+        for b in sizes:
+            s = torch.randint(0, 255, (p, p * b), dtype=torch.uint8, device="cuda")
+            r = torch.empty_like(s)
+            row[f"a2a{sfx}_{b}"] = round(t(lambda: c.alltoall(s, r, algo=algo), it=200), 3)
+            row[f"a2a{sfx}_{b}_path"] = sorted(c.last_launch_path())
+            s2 = s[:, :b].contiguous()
+            ag = "ring" if algo == "hier" else algo
+            row[f"ag{sfx}_{b}"] = round(t(lambda: c.allgather(s2, r[:, : p * b], algo=ag), it=200), 3)
+            row[f"ag{sfx}_{b}_path"] = sorted(c.last_launch_path())
     # the launch floor: a trivial torch copy of the same bytes
     x = torch.empty(16, dtype=torch.uint8, device="cuda")
     y = torch.empty_like(x)
