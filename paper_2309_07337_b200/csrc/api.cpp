@@ -79,8 +79,16 @@ constexpr uint64_t kSmallOneStepVol = 32u << 20;   // ... and source bytes per G
                                                     // p=4 2 MiB 11.4 -> 7.2 us; 64 MiB loses)
 constexpr uint64_t kSmallSyncMove = 256u << 10;    // multi-step small launches on several CTAs:
 constexpr uint64_t kSmallSyncVol = 8u << 20;       //   longest move, busiest step
-constexpr uint64_t kSmallOwnVol = 2u << 20;        // owned-flow mode: busiest step, and bytes per CTA
-constexpr uint64_t kSmallOwnPerCta = 64u << 10;    //   (few flows -> few CTAs: allgathers)
+// owned-flow mode: busiest step, and bytes per CTA (few flows -> few CTAs: allgathers).
+// Measured on one B200: 8 MiB / 128 KiB (up from 2 MiB / 64 KiB) take p = 8 Bruck alltoall at
+// 64 KiB blocks 12.1 -> 8.4 us, Bruck allgather 16 KiB 10.9 -> 7.9, ring allgather 64 KiB 17.8
+// -> 15.8, p = 32 Bruck alltoall / allgather 4 KiB 29.0 / 68.8 -> 7.7 / 8.9 us; emulated GPUs
+// (a row of CTAs per virtual GPU) keep the smaller limits -- there the larger ones lose up to 2x
+// at 64-256 KiB
+constexpr uint64_t kSmallOwnVol = 8u << 20;
+constexpr uint64_t kSmallOwnPerCta = 128u << 10;
+constexpr uint64_t kSmallOwnVolEmu = 2u << 20;
+constexpr uint64_t kSmallOwnPerCtaEmu = 64u << 10;
 constexpr uint64_t kSmallItemsOneCta = 2048;   // multi-step programs: largest step one CTA handles
 constexpr uint64_t kDynMinMove = 128u << 10;   // dynamic mode: smallest average move (bytes) when
 constexpr uint64_t kDynBigTotal = 128u << 20;  //   the busiest GPU moves this much, else ...
@@ -233,6 +241,8 @@ struct mpxa_comm_s {
     bool ll = true;                        // eager (LL) mode for small multi-GPU launches
     uint64_t one_cta_items = kSmallItemsOneCta;  // MPXA_ONE_CTA_ITEMS (tuning)
     uint64_t small_items = kSmallItemsPerCta;    // MPXA_SMALL_ITEMS: 16-B pieces per small-kernel CTA
+    uint64_t own_vol = 0;                        // MPXA_OWN_VOL / MPXA_OWN_PER_CTA: owned-flow mode
+    uint64_t own_per_cta = 0;                    //   limits (busiest step; bytes per CTA); 0: default
     bool row_signal = true;                // MPXA_ROW_SIGNAL=0: executor steps signalled per (CTA, peer)
     bool hier_staged = false;              // MPXA_HIER_STAGED=1: hierarchical with group = GPU in its
                                            // literal three-step form instead of the fused one
@@ -868,7 +878,9 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
     const uint64_t n_own = std::max<uint64_t>(1, std::min<uint64_t>(std::min<uint64_t>(cdiv(items, per_cta),
                                                                                           (uint64_t)dp.host.nflows),
                                                                      (uint64_t)c->cap_small));
-    const bool own_ok = dp.uniform_len && step_vol <= kSmallOwnVol && step_vol / n_own <= kSmallOwnPerCta;
+    const uint64_t own_vol = c->own_vol ? c->own_vol : c->emulated ? kSmallOwnVolEmu : kSmallOwnVol;
+    const uint64_t own_per_cta = c->own_per_cta ? c->own_per_cta : c->emulated ? kSmallOwnPerCtaEmu : kSmallOwnPerCta;
+    const bool own_ok = dp.uniform_len && step_vol <= own_vol && step_vol / n_own <= own_per_cta;
     const bool small_sync = !one_step && items > c->one_cta_items && maxmove <= kSmallSyncMove &&
                             step_vol <= kSmallSyncVol && c->small_sync &&
                             (!own_ok || dp.max_gpu_moves > kSmallMovesSmem) &&
@@ -1454,6 +1466,8 @@ void read_knobs(mpxa_comm_t c) {
     if (const char *e = getenv("MPXA_SMALL_NT")) c->small_nt = std::max(32, std::min(512, atoi(e)));
     if (const char *e = getenv("MPXA_NO_LL")) c->ll = atoi(e) == 0;
     if (const char *e = getenv("MPXA_ONE_CTA_ITEMS")) c->one_cta_items = strtoull(e, nullptr, 10);
+    if (const char *e = getenv("MPXA_OWN_VOL")) c->own_vol = strtoull(e, nullptr, 10);
+    if (const char *e = getenv("MPXA_OWN_PER_CTA")) c->own_per_cta = strtoull(e, nullptr, 10);
     if (const char *e = getenv("MPXA_SMALL_ITEMS")) c->small_items = std::max<uint64_t>(64, strtoull(e, nullptr, 10));
     if (const char *e = getenv("MPXA_HIER_STAGED")) c->hier_staged = atoi(e) != 0;
     if (const char *e = getenv("MPXA_ROW_SIGNAL")) c->row_signal = atoi(e) != 0;
@@ -1493,7 +1507,8 @@ uint64_t knob_digest(mpxa_comm_t c, size_t heap) {
     const int64_t v[] = {c->force_ns, c->force_nf, c->force_big, c->force_exec, c->pdl, c->dyn, c->wring, c->wslack, c->tiny, c->dyn_pieces,
                          (int64_t)c->dyn_min_total, c->force_sync, c->small_sync, (int64_t)c->small_max1,
                          (int64_t)c->small_vol1, c->var_chop, c->var_tiles, c->swork, c->small_nt, c->ll,
-                         (int64_t)c->one_cta_items, (int64_t)c->small_items, c->hier_staged, c->row_signal, c->ll_max, c->ll_max_ms,
+                         (int64_t)c->one_cta_items, (int64_t)c->small_items, (int64_t)c->own_vol,
+                         (int64_t)c->own_per_cta, c->hier_staged, c->row_signal, c->ll_max, c->ll_max_ms,
                          c->user_algo[0], c->user_algo[1], c->user_algo[2], (int64_t)heap,
                          (int64_t)c->selector.size()};
     uint64_t h = fnv(1469598103934665603ull, v, sizeof v);

@@ -199,6 +199,7 @@ def test_init_knob_consistency(tmp_path):
         ("MPXA_NO_SMALL", "1"),
         ("MPXA_NO_WRING", "1"),                # warp-ring dynamic mode on one process only
         ("MPXA_SMALL_ITEMS", "2048"),          # small-kernel grid (CTA flag slots pair 1:1)
+        ("MPXA_OWN_VOL", "1048576"),            # owned-flow vs row-barrier mode
         ("MPXA_SELECTOR", str(sel)))]
     same = {"MPXA_NO_LL": "1", "MPXA_SELECTOR": str(sel)}
     cases += [([same, dict(same)], "ok"), ([{}, {}], "ok")]
