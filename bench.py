@@ -175,7 +175,7 @@ def time_graph(fn, calls, stream):
     return statistics.median(times)
 
 
-def sweep(comm, torch, stream, reps=20):
+def sweep(comm, torch, stream, reps=200):
     """Per-size / per-variant us and GB/s on this device (BASELINE metric: vs block size).
     Every input is allocated and filled on the stream the collectives run on (the current
     stream inside this function), so no fill can race a collective."""
