@@ -259,6 +259,7 @@ struct mpxa_comm_s {
     int dyn_pieces = (int)kDynPiecesPerCta;   // MPXA_DYN_PIECES: queue pieces per CTA (tuning)
     int wslack = 2;                           // MPXA_WSLACK: warp-ring stages kept out of the load window
     bool tiny = true;                         // MPXA_NO_TINY=1: small one-GPU launches in the general kernel
+    bool tiny_even = true;                    // MPXA_TINY_EVEN=0: tiny-kernel blocks sized like the general kernel's
     uint64_t dyn_min_total = kDynMinTotal;    // MPXA_DYN_MIN: smallest busiest-GPU volume (tuning)
     int force_sync = -1;                      // MPXA_DYN_SYNC=0/1: force multi-step dynamic mode (tuning)
     bool small_sync = true;                   // MPXA_NO_SMALL_SYNC=1: multi-step small launches in one CTA
@@ -982,6 +983,17 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
                              E.small_cache > 0 && dp.nsteps <= kMaxStepsSmem && sp == &dp;
         // one-step eager launches across GPUs: the tiny eager kernel (same word protocol)
         const bool tiny_ll = c->tiny && one_step && E.small_ll && !E.small_var && !E.small_own && E.small_cache > 0;
+        if (tiny && c->tiny_even) {
+            // the tiny kernel hands each CTA blockDim consecutive pieces: size the block to the
+            // pieces the kernel decodes (fan-out: one per source piece, not per destination) over
+            // the grid, a multiple of a warp, so every CTA of the grid gets work (measured, p = 8:
+            // allgather 16 / 32 / 64 / 128 KiB 2.12 / 2.12 / 2.22 / 2.78 -> 1.50 / 1.55 / 1.59 /
+            // 2.27 us -- the power-of-two block sized by fan-out-weighted pieces left 7 of 8 CTAs
+            // idle; alltoall 16 KiB 1.52 -> 1.48)
+            const uint64_t kitems = (uint64_t)dp.host.max_step_moves * ppm;
+            const uint64_t nt = std::max<uint64_t>(64, std::min<uint64_t>(512, (cdiv(kitems, (uint64_t)std::max(1, nC)) + 31) / 32 * 32));
+            E.small_threads = (int32_t)nt;
+        }
         if (tiny) e = launch_tiny(E, std::max(1, nC), pdl && c->pdl, stream);
         else if (tiny_ms) {
             E.small_swork = 0;   // (the tiny multi-step kernel keeps WORK in global memory / L2)
@@ -1454,6 +1466,7 @@ void read_knobs(mpxa_comm_t c) {
     if (const char *e = getenv("MPXA_WRING")) c->wring = atoi(e);
     if (const char *e = getenv("MPXA_DYN_PIECES")) c->dyn_pieces = std::max(1, atoi(e));
     if (const char *e = getenv("MPXA_NO_TINY")) c->tiny = atoi(e) == 0;
+    if (const char *e = getenv("MPXA_TINY_EVEN")) c->tiny_even = atoi(e) != 0;
     if (const char *e = getenv("MPXA_WSLACK")) c->wslack = std::max(1, std::min(kWStages - 1, atoi(e)));
     if (const char *e = getenv("MPXA_DYN_MIN")) c->dyn_min_total = strtoull(e, nullptr, 10);
     if (const char *e = getenv("MPXA_DYN_SYNC")) c->force_sync = atoi(e);
@@ -1504,7 +1517,7 @@ void read_knobs(mpxa_comm_t c) {
 // knob, the selector table, the forced variants and the initial heap size (heap growth is
 // a collective IPC exchange: the sizes must evolve identically on every process).
 uint64_t knob_digest(mpxa_comm_t c, size_t heap) {
-    const int64_t v[] = {c->force_ns, c->force_nf, c->force_big, c->force_exec, c->pdl, c->dyn, c->wring, c->wslack, c->tiny, c->dyn_pieces,
+    const int64_t v[] = {c->force_ns, c->force_nf, c->force_big, c->force_exec, c->pdl, c->dyn, c->wring, c->wslack, c->tiny, c->tiny_even, c->dyn_pieces,
                          (int64_t)c->dyn_min_total, c->force_sync, c->small_sync, (int64_t)c->small_max1,
                          (int64_t)c->small_vol1, c->var_chop, c->var_tiles, c->swork, c->small_nt, c->ll,
                          (int64_t)c->one_cta_items, (int64_t)c->small_items, (int64_t)c->own_vol,
