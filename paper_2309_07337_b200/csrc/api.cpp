@@ -999,9 +999,14 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
             E.small_swork = 0;   // (the tiny multi-step kernel keeps WORK in global memory / L2)
             e = launch_tiny_ms(E, std::max(1, nC), pdl && c->pdl, stream);
         }
-        else if (tiny_ll)
+        else if (tiny_ll) {
+            if (c->tiny_even) {   // (the same sizing: the pieces of the busiest GPU's eager program)
+                const uint64_t kitems = (uint64_t)nmoves_g * ppm;
+                E.small_threads = (int32_t)std::max<uint64_t>(
+                    64, std::min<uint64_t>(512, (cdiv(kitems, (uint64_t)std::max(1, nC)) + 31) / 32 * 32));
+            }
             e = launch_tiny_ll(E, std::max(1, nC), c->emulated ? c->G : 1, c->emulated, pdl && c->pdl, stream);
-        else e = launch_small(E, std::max(1, nC), c->emulated ? c->G : 1, c->emulated, pdl && c->pdl, stream);
+        } else e = launch_small(E, std::max(1, nC), c->emulated ? c->G : 1, c->emulated, pdl && c->pdl, stream);
         tiny = tiny || tiny_ll || tiny_ms;
     } else {
         int nC = gr.n();
