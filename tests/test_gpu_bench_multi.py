@@ -33,3 +33,24 @@ def test_force_multi_line():
     assert any("Init COMPLETE" in ln for ln in d["nccl_init"]["lines"])
     assert d["roofline"]["bound"] in ("hbm", "nvlink") and 0 < d["roofline"]["frac"] <= 1.1
     assert d["gpu_launches"] == 3
+
+
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a GPU")
+def test_force_multi_sweep():
+    """The p = N per-size sweep (every mpxa variant vs NCCL B1, largest points checked against
+    the oracle) at N = 1."""
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--force-multi",
+                          "--steps", "3", "--warmup", "3", "--no-e2e", "--no-cpu"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    ns = d["nccl_sweep"]
+    assert ns["p"] == 1
+    for op, n in (("alltoall", 12), ("allgather", 25)):
+        rows = ns[op]
+        assert len(rows) == n
+        for r in rows:                      # [bytes, t_roof, nccl_us, best_us, best, frac, speedup, by_variant]
+            assert r[2] > 0 and r[3] > 0 and r[4] in r[7]
+        assert ns[f"{op}_largest_verified_sampled_vs_oracle"] is True
