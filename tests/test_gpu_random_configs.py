@@ -122,7 +122,11 @@ KNOBS = [{"MPXA_NO_LL": "1"}, {"MPXA_NO_SMALL": "1"}, {"MPXA_NO_DYN": "1"}, {"MP
          # every dynamic launch through the per-warp TMA rings, multi-step programs included
          {"MPXA_WRING": "2", "MPXA_DYN_SYNC": "1", "MPXA_NO_SMALL": "1"},
          # the general small kernel for launches the tiny kernels would take
-         {"MPXA_NO_TINY": "1"}]
+         {"MPXA_NO_TINY": "1"},
+         # the round-2 grid sizing choices, reverted: power-of-two tiny blocks, 2048 pieces per
+         # small-kernel CTA, the smaller owned-flow limits
+         {"MPXA_TINY_EVEN": "0"}, {"MPXA_SMALL_ITEMS": "2048"},
+         {"MPXA_OWN_VOL": "2097152", "MPXA_OWN_PER_CTA": "65536"}]
 
 
 @pytest.mark.parametrize("knob", range(len(KNOBS)), ids=[",".join(k) for k in KNOBS])
