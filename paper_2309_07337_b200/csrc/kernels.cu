@@ -471,7 +471,10 @@ __device__ __forceinline__ void store_piece_generic(char *dp, uint4 v, uint32_t 
 // its 16-byte piece of every move first (kBatch loads in flight), then stores them -- one
 // memory round trip per batch instead of one per move.  Byte-granular when a piece is not
 // 16-B aligned on both sides.
-constexpr int kBatch = 4;
+#ifndef MPXA_KBATCH
+#define MPXA_KBATCH 4
+#endif
+constexpr int kBatch = MPXA_KBATCH;
 constexpr uint64_t kSmallMax = 512;
 
 struct SmallJob {
