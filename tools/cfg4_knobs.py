@@ -1,6 +1,7 @@
 """cfg4 alltoallv (p = 8) device time per persistent start+wait (CUDA graph) under knob sets
 (VARIANTS='{"name": {"ENV": "val"}, ...}', first = reference), int64 and int32 segments
-(ELEMS), means in MiB (MEANS); every variant's output compared with the first's.  (Used for
+(ELEMS), means in MiB (MEANS), ODD=1 for counts that leave segments at every alignment; every
+variant's output compared with the first's.  (Used for
 the round-2 cp.async warp-ring experiment, MPXA_WLOAD, since removed: profiles/r02/shift_probe.txt.)"""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -25,6 +26,8 @@ for elem in (int(x) for x in os.environ.get("ELEMS", "8,4").split(",")):
     for mean in (int(x) for x in os.environ.get("MEANS", "1,2,4,8").split(",")):
         for seed in (0, 1):
             c4 = synth.cfg4_counts(seed, p, mean << 20, elem=8) * 8 // elem
+            if os.environ.get("ODD"):   # one more element per nonzero pair: offsets of every alignment
+                c4 = c4 + (c4 > 0)
             send, sc, sd, rc, rd, S, Rcap = synth.alltoallv_buffers(seed, c4, elem=elem)
             d_s = torch.from_numpy(send).cuda()
             ref = None
