@@ -101,7 +101,10 @@ constexpr uint64_t kDynMinTotal = 8u << 20;    // smallest per-GPU step volume
 constexpr uint64_t kDynSyncMin = 128u << 20;
 constexpr int64_t kDynSyncMoves = 32;
 constexpr uint64_t kDynSyncMinUneven = 16u << 20;
-constexpr uint64_t kWringMinVol = 96u << 20;   // warp-ring mode: smallest busiest-GPU volume
+constexpr uint64_t kWringMinVol = 48u << 20;   // warp-ring mode: smallest busiest-GPU volume (96 MiB
+                                               // before the constant-shift stores; measured since, cfg4:
+                                               // mean 1 MiB (58 MiB) 25.9 / 29.5 -> 25.2 / 28.3 us with
+                                               // the rings, mean 0.75 MiB (44 MiB) still LSU: 21.3 vs 22.9)
 constexpr uint64_t kDynPiecesPerCta = 64;      // target queue pieces per CTA (measured: 16 -> 64 closes the tail)
 constexpr uint64_t kDynMaxPiece = 512u << 10;  // largest piece (bytes)
 
@@ -1077,8 +1080,9 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
         // its own pieces through a TMA ring -- congruent ones with bulk stores, the others with
         // 16-B stores the warp shifts out of shared memory (kernels.cu dyn_tile_w; measured,
         // cfg4 mean 4 MiB int64: 96.9 / 103.1 / 106.6 -> 92.3 / 87.2 / 100.6 us, seeds 0-2)
-        // (measured, cfg4 int64: the LSU path wins below ~100 MiB per GPU -- mean 1 MiB 24.3 vs
-        // 25.7 us -- and the warp rings above: mean 2 MiB 55.5 -> 51.9, 4 MiB 96.9 -> 92.3)
+        // (measured, cfg4 int64, first version: the LSU path won below ~100 MiB per GPU -- mean
+        // 1 MiB 24.3 vs 25.7 us -- and the warp rings above: mean 2 MiB 55.5 -> 51.9, 4 MiB 96.9
+        // -> 92.3; with constant-shift stores the rings win from 1 MiB: kWringMinVol)
         const uint64_t wr_vol = dp.nsteps == 1 ? src_vol : step_vol;
         if (E.dyn_units && c->wring &&
             (c->wring == 2 ||

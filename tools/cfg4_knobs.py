@@ -23,9 +23,9 @@ for name, env in VARIANTS:
         del os.environ[k]
 res = {}
 for elem in (int(x) for x in os.environ.get("ELEMS", "8,4").split(",")):
-    for mean in (int(x) for x in os.environ.get("MEANS", "1,2,4,8").split(",")):
+    for mean in (float(x) for x in os.environ.get("MEANS", "1,2,4,8").split(",")):
         for seed in (0, 1):
-            c4 = synth.cfg4_counts(seed, p, mean << 20, elem=8) * 8 // elem
+            c4 = synth.cfg4_counts(seed, p, int(mean * (1 << 20)), elem=8) * 8 // elem
             if os.environ.get("ODD"):   # one more element per nonzero pair: offsets of every alignment
                 c4 = c4 + (c4 > 0)
             send, sc, sd, rc, rd, S, Rcap = synth.alltoallv_buffers(seed, c4, elem=elem)
