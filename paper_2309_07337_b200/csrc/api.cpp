@@ -913,6 +913,9 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
         // consequence across processes)
         E.small_a8 = !E.small_a16 && unit % 8 == 0 && (uintptr_t)send % 8 == 0 && (uintptr_t)recv % 8 == 0 &&
                      send_stride % 8 == 0 && recv_stride % 8 == 0 && E.work_stride % 8 == 0;
+        E.small_a4 = !E.small_a16 && !E.small_a8 && unit % 4 == 0 && (uintptr_t)send % 4 == 0 &&
+                     (uintptr_t)recv % 4 == 0 && send_stride % 4 == 0 && recv_stride % 4 == 0 &&
+                     E.work_stride % 4 == 0;
         E.small_ppm = (int32_t)ppm;
         const DevProg *sp = &dp;
         // variable pieces: long moves split (companion program) unless the tables are per-call

@@ -512,6 +512,12 @@ struct PieceRegs {
             const uint2 lo = __ldcg((const uint2 *)sp);
             const uint2 hi = len > 8 ? __ldcg((const uint2 *)sp + 1) : make_uint2(0u, 0u);
             v[k] = make_uint4(lo.x, lo.y, hi.x, hi.y);
+        } else if (AW == 4) {   // 4-B aligned, len a multiple of 4: whole words, no shifts
+            const uint32_t *wp = (const uint32_t *)sp;
+            v[k].x = __ldcg(wp);
+            v[k].y = len > 4 ? __ldcg(wp + 1) : 0u;
+            v[k].z = len > 8 ? __ldcg(wp + 2) : 0u;
+            v[k].w = len > 12 ? __ldcg(wp + 3) : 0u;
         } else {
             const uintptr_t a = (uintptr_t)sp & ~(uintptr_t)3;
             const uint32_t *wp = (const uint32_t *)a;
@@ -556,6 +562,14 @@ __device__ __forceinline__ void store_piece(char *dp, uint4 v, uint32_t len) {
     if (AW == 8) {                                      // 8-B aligned, len 8 or 16
         *(uint2 *)dp = make_uint2(v.x, v.y);
         if (len > 8) *((uint2 *)dp + 1) = make_uint2(v.z, v.w);
+        return;
+    }
+    if (AW == 4) {                                      // 4-B aligned, len 4, 8, 12 or 16
+        uint32_t *d = (uint32_t *)dp;
+        d[0] = v.x;
+        if (len > 4) d[1] = v.y;
+        if (len > 8) d[2] = v.z;
+        if (len > 12) d[3] = v.w;
         return;
     }
     if (len == 16 && (((uintptr_t)dp) & 3) == 0) {
@@ -2394,6 +2408,11 @@ cudaError_t launch_tiny(const ExecParams &P, int nC, bool pdl, cudaStream_t stre
         const cudaError_t a = tiny_attr<16>();
         if (a != cudaSuccess) return a;
         return launch_kernel(mpxa_tiny_kernel<16>, P, dim3(nC), dim3(nt), smem, false, pdl, stream);
+    }
+    if (P.small_a4) {   // 4-byte words (e.g. 4-B allgather contributions): no funnel shifts
+        const cudaError_t a = tiny_attr<4>();
+        if (a != cudaSuccess) return a;
+        return launch_kernel(mpxa_tiny_kernel<4>, P, dim3(nC), dim3(nt), smem, false, pdl, stream);
     }
     if (P.small_a8) {
         const cudaError_t a = tiny_attr<8>();
