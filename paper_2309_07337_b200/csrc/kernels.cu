@@ -2051,7 +2051,7 @@ __device__ __forceinline__ char *tiny_base(const ExecParams &P, char *work, int 
                              : work + (uint64_t)rank * P.work_stride;
 }
 
-template <int AW>
+template <int AW, int TB>
 __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_tiny_kernel(const __grid_constant__ ExecParams P) {
     extern __shared__ __align__(16) char tiny_dyn[];
     TMove *tm = reinterpret_cast<TMove *>(tiny_dyn);
@@ -2074,11 +2074,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_tiny_kernel(const __gri
     griddep_launch_dependents();
     const uint32_t ppm = (uint32_t)P.small_ppm, lg = 31u - (uint32_t)__clz((int)ppm), mask = ppm - 1u;
     const uint32_t items = (uint32_t)nm * ppm, TT = gridDim.x * blockDim.x;
-    for (uint32_t base = blockIdx.x * blockDim.x + t; base < items; base += TT * kBatch) {
+    for (uint32_t base = blockIdx.x * blockDim.x + t; base < items; base += TT * TB) {
         PieceRegs<AW> R;
-        const char *sp[kBatch];
+        const char *sp[TB];
 #pragma unroll
-        for (int k = 0; k < kBatch; k++) {
+        for (int k = 0; k < TB; k++) {
             sp[k] = nullptr;
             const uint32_t it = base + (uint32_t)k * TT;
             if (it >= items) continue;
@@ -2089,7 +2089,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_tiny_kernel(const __gri
             R.issue(k, sp[k], min(16u, m.n - o));
         }
 #pragma unroll
-        for (int k = 0; k < kBatch; k++) {
+        for (int k = 0; k < TB; k++) {
             if (!sp[k]) continue;
             const uint32_t it = base + (uint32_t)k * TT;
             const TMove &m = tm[it >> lg];
@@ -2329,9 +2329,22 @@ static cudaError_t tiny_ms_attr() {
 
 template <int AW>
 static cudaError_t tiny_attr() {
-    static cudaError_t e = cudaFuncSetAttribute(mpxa_tiny_kernel<AW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    static cudaError_t e = cudaFuncSetAttribute(mpxa_tiny_kernel<AW, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 (int)(kSmallMovesSmem * sizeof(TMove)));
-    return e;
+    static cudaError_t f = cudaFuncSetAttribute(mpxa_tiny_kernel<AW, kBatch>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)(kSmallMovesSmem * sizeof(TMove)));
+    return e != cudaSuccess ? e : f;
+}
+// one pass of the grid covers every piece: the one-piece-per-thread build (the shortest
+// instruction stream -- tiny launches are instruction-fetch bound on cold SMs)
+template <int AW>
+static cudaError_t launch_tiny_aw(const ExecParams &P, int nC, int nt, size_t smem, bool pdl, cudaStream_t stream) {
+    const cudaError_t a = tiny_attr<AW>();
+    if (a != cudaSuccess) return a;
+    const bool one = (uint64_t)P.prog.nmoves * (uint64_t)P.small_ppm <= (uint64_t)nC * (uint64_t)nt;
+    return launch_kernel(one ? mpxa_tiny_kernel<AW, 1> : mpxa_tiny_kernel<AW, kBatch>, P, dim3(nC), dim3(nt), smem,
+                         false, pdl, stream);
 }
 
 // Launch with the PDL attribute (pdl) or cooperatively (emulated GPUs: co-residency of the
@@ -2404,24 +2417,10 @@ cudaError_t launch_tiny_ms(const ExecParams &P, int nC, bool pdl, cudaStream_t s
 cudaError_t launch_tiny(const ExecParams &P, int nC, bool pdl, cudaStream_t stream) {
     const size_t smem = (size_t)P.prog.nmoves * sizeof(TMove);
     const int nt = P.small_threads > 0 ? P.small_threads : kSmallThreads;
-    if (P.small_a16) {
-        const cudaError_t a = tiny_attr<16>();
-        if (a != cudaSuccess) return a;
-        return launch_kernel(mpxa_tiny_kernel<16>, P, dim3(nC), dim3(nt), smem, false, pdl, stream);
-    }
-    if (P.small_a4) {   // 4-byte words (e.g. 4-B allgather contributions): no funnel shifts
-        const cudaError_t a = tiny_attr<4>();
-        if (a != cudaSuccess) return a;
-        return launch_kernel(mpxa_tiny_kernel<4>, P, dim3(nC), dim3(nt), smem, false, pdl, stream);
-    }
-    if (P.small_a8) {
-        const cudaError_t a = tiny_attr<8>();
-        if (a != cudaSuccess) return a;
-        return launch_kernel(mpxa_tiny_kernel<8>, P, dim3(nC), dim3(nt), smem, false, pdl, stream);
-    }
-    const cudaError_t a = tiny_attr<0>();   // any alignment: 4-byte words and funnel shifts
-    if (a != cudaSuccess) return a;
-    return launch_kernel(mpxa_tiny_kernel<0>, P, dim3(nC), dim3(nt), smem, false, pdl, stream);
+    if (P.small_a16) return launch_tiny_aw<16>(P, nC, nt, smem, pdl, stream);
+    if (P.small_a4) return launch_tiny_aw<4>(P, nC, nt, smem, pdl, stream);   // 4-byte words: no shifts
+    if (P.small_a8) return launch_tiny_aw<8>(P, nC, nt, smem, pdl, stream);
+    return launch_tiny_aw<0>(P, nC, nt, smem, pdl, stream);   // any alignment: words and funnel shifts
 }
 
 cudaError_t launch_tiny_ll(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream) {
