@@ -1003,6 +1003,7 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
         if (tiny) e = launch_tiny(E, std::max(1, nC), pdl && c->pdl, stream);
         else if (tiny_ms) {
             E.small_swork = 0;   // (the tiny multi-step kernel keeps WORK in global memory / L2)
+            E.tiny_step_items = (int32_t)std::min<uint64_t>(INT32_MAX, (uint64_t)dp.host.max_step_moves * ppm);
             e = launch_tiny_ms(E, std::max(1, nC), pdl && c->pdl, stream);
         }
         else if (tiny_ll) {

@@ -2234,7 +2234,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_tiny_ll_kernel(const __
 // Tiny MULTI-STEP launches: several steps on one GPU (Bruck, ring, hierarchical at small
 // sizes), every move cached, in one CTA or in several CTAs that each own a set of flows --
 // steps separated by __syncthreads only (a step reads what earlier steps of this CTA wrote).
-template <int AW>
+template <int AW, int TB>
 __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_tiny_ms_kernel(const __grid_constant__ ExecParams P) {
     extern __shared__ __align__(16) char tiny_dyn[];
     __shared__ int2 st[kMaxStepsSmem];
@@ -2284,11 +2284,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_tiny_ms_kernel(const __
     for (int s = 0; s < ns; s++) {
         const TMove *mv = tm + st[s].x;
         const uint32_t items = (uint32_t)(st[s].y - st[s].x) * ppm;
-        for (uint32_t base = t; base < items; base += TT * kBatch) {
+        for (uint32_t base = t; base < items; base += TT * TB) {
             PieceRegs<AW> R;
-            const char *sp[kBatch];
+            const char *sp[TB];
 #pragma unroll
-            for (int k = 0; k < kBatch; k++) {
+            for (int k = 0; k < TB; k++) {
                 sp[k] = nullptr;
                 const uint32_t it = base + (uint32_t)k * TT;
                 if (it >= items) continue;
@@ -2299,7 +2299,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_tiny_ms_kernel(const __
                 R.issue(k, sp[k], min(16u, m.n - o));
             }
 #pragma unroll
-            for (int k = 0; k < kBatch; k++) {
+            for (int k = 0; k < TB; k++) {
                 if (!sp[k]) continue;
                 const uint32_t it = base + (uint32_t)k * TT;
                 const TMove &m = mv[it >> lg];
@@ -2321,9 +2321,24 @@ __global__ void __launch_bounds__(kSmallThreads, 1) mpxa_tiny_ms_kernel(const __
 
 template <int AW>
 static cudaError_t tiny_ms_attr() {
-    static cudaError_t e = cudaFuncSetAttribute(mpxa_tiny_ms_kernel<AW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    static cudaError_t e = cudaFuncSetAttribute(mpxa_tiny_ms_kernel<AW, 1>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 (int)(kSmallMovesSmem * sizeof(TMove)));
-    return e;
+    static cudaError_t f = cudaFuncSetAttribute(mpxa_tiny_ms_kernel<AW, kBatch>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)(kSmallMovesSmem * sizeof(TMove)));
+    return e != cudaSuccess ? e : f;
+}
+// every step's pieces (a CTA's share in the owned-flow mode) fit one pass of the block: the
+// one-piece-per-thread build
+template <int AW>
+static cudaError_t launch_tiny_ms_aw(const ExecParams &P, int nC, int nt, size_t smem, bool pdl, cudaStream_t stream) {
+    const cudaError_t a = tiny_ms_attr<AW>();
+    if (a != cudaSuccess) return a;
+    const uint64_t per = P.small_own > 1 ? (uint64_t)P.tiny_step_items * 2 / (uint64_t)nC : (uint64_t)P.tiny_step_items;
+    const bool one = per <= (uint64_t)nt;
+    return launch_kernel(one ? mpxa_tiny_ms_kernel<AW, 1> : mpxa_tiny_ms_kernel<AW, kBatch>, P, dim3(nC), dim3(nt),
+                         smem, false, pdl, stream);
 }
 
 
@@ -2401,17 +2416,9 @@ static cudaError_t launch_small_km(const ExecParams &P, size_t max_dyn, size_t s
 cudaError_t launch_tiny_ms(const ExecParams &P, int nC, bool pdl, cudaStream_t stream) {
     const size_t smem = (size_t)P.prog.nmoves * sizeof(TMove);
     const int nt = P.small_threads > 0 ? P.small_threads : kSmallThreads;
-    cudaError_t a;
-    if (P.small_a16) {
-        if ((a = tiny_ms_attr<16>()) != cudaSuccess) return a;
-        return launch_kernel(mpxa_tiny_ms_kernel<16>, P, dim3(nC), dim3(nt), smem, false, pdl, stream);
-    }
-    if (P.small_a8) {
-        if ((a = tiny_ms_attr<8>()) != cudaSuccess) return a;
-        return launch_kernel(mpxa_tiny_ms_kernel<8>, P, dim3(nC), dim3(nt), smem, false, pdl, stream);
-    }
-    if ((a = tiny_ms_attr<0>()) != cudaSuccess) return a;
-    return launch_kernel(mpxa_tiny_ms_kernel<0>, P, dim3(nC), dim3(nt), smem, false, pdl, stream);
+    if (P.small_a16) return launch_tiny_ms_aw<16>(P, nC, nt, smem, pdl, stream);
+    if (P.small_a8) return launch_tiny_ms_aw<8>(P, nC, nt, smem, pdl, stream);
+    return launch_tiny_ms_aw<0>(P, nC, nt, smem, pdl, stream);
 }
 
 cudaError_t launch_tiny(const ExecParams &P, int nC, bool pdl, cudaStream_t stream) {

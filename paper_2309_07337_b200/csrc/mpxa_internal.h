@@ -191,6 +191,8 @@ struct ExecParams {
     int32_t wslack;            // warp-ring mode: stages kept out of the load window (1 or 2)
     int32_t small_a4;          // tiny kernel: every offset, length, base and stride a 4-B multiple
                                // (not all 8): pieces move as 4-byte words, no funnel shifts
+    int32_t tiny_step_items;   // tiny multi-step kernel: 16-B pieces of the busiest step (launch
+                               // choice of the one-piece-per-thread build)
 };
 
 }  // namespace mpxa
