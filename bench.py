@@ -131,11 +131,24 @@ def barrier(ws):
 # ---------------------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------------------
-def time_loop(fn, steps, warmup, stream, ws):
+class BenchAbort(RuntimeError):
+    """The library's device watchdog fired on some rank (MPXA_ERR_TIMEOUT): every rank stops
+    measuring and rank 0 reports the error instead of timing a poisoned communicator."""
+
+
+def any_rank_error(comm, ws):
+    """comm.check() != 0 on any rank (all ranks take the same branch)."""
+    err = comm.check()
+    return max_over_ranks(float(err != 0), ws) > 0 if ws > 1 else err != 0
+
+
+def time_loop(fn, steps, warmup, stream, ws, comm=None):
     import torch
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
+    if comm is not None and any_rank_error(comm, ws):
+        raise BenchAbort("device watchdog timeout during warm-up (MPXA_ERR_TIMEOUT)")
     barrier(ws)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -823,7 +836,8 @@ def _multi_gpu_nccl(args, comm, send, recv, R, p, b, ms, total_recv, stream, nc,
     if not args.sweep:
         return nccl, None
     # ---- sweep at p = N, R = 1 ----
-    c1 = Comm(ranks_per_proc=1, device=torch.cuda.current_device(), pg=dist.group.WORLD)
+    c1 = Comm(ranks_per_proc=1, device=torch.cuda.current_device(), pg=dist.group.WORLD, timeout_s=10.0)
+    broken = None      # first point where the device watchdog fired: mpxa skipped from there on
     out = {"p": N, "ranks_per_gpu": 1,
            "timing": "device us per call, max over ranks; CUDA graph of back-to-back calls (median of 5 "
                      "replays) at <= 4 KiB, eager loop between events above; NCCL B1 from C++ the same way",
@@ -856,14 +870,27 @@ def _multi_gpu_nccl(args, comm, send, recv, R, p, b, ms, total_recv, stream, nc,
             t_roof = 1e6 * max((N - 1) * bb / (NVL_NOMINAL * 1e9), hbm / (peak * 1e9))
             byv = {}
             for v in variants:
+                if broken:
+                    break
                 fn = (lambda v=v: comm_call(c1, op, s_, r_, v, stream))
-                byv[v] = round(_mpxa_us(fn, stream, small, iters), 3)
+                us = _mpxa_us(fn, stream, small, iters)
+                if any_rank_error(c1, N):
+                    broken = f"{op} {v} {bb} B: device watchdog timeout (MPXA_ERR_TIMEOUT)"
+                    out["error"] = broken
+                    break
+                byv[v] = round(us, 3)
             dist.barrier()
             n_us = _max_ranks(nc.time(op, s_, r_, bb, stream=stream, warmup=5, iters=iters, graph=small))
+            if not byv:
+                out[op].append([bb, round(t_roof, 3), round(n_us, 3), None, None, None, None, {}])
+                continue
             best = min(byv, key=byv.get)
             out[op].append([bb, round(t_roof, 3), round(n_us, 3), byv[best], best, round(t_roof / byv[best], 4),
                             round(n_us / byv[best], 3), byv])
         # oracle check of the largest point, default variant
+        if broken:
+            out[f"{op}_largest_verified_sampled_vs_oracle"] = None
+            continue
         comm_call(c1, op, s_, r_, None, stream)
         torch.cuda.synchronize()
         chk = check_alltoall_sampled if op == "alltoall" else check_allgather_sampled
@@ -910,7 +937,9 @@ def gpu_arm(args):
         raise SystemExit(f"--gpus {N} must divide p={p}")
     R = p // N
     b = args.bytes
-    comm = Comm(ranks_per_proc=R, device=local, pg=pg)
+    # (several GPUs: a 10 s device watchdog -- every collective here ends in milliseconds --
+    # so a protocol failure ends the run with an error line, not hours of timed-out calls)
+    comm = Comm(ranks_per_proc=R, device=local, pg=pg, timeout_s=10.0 if multi else 0.0)
     stream = torch.cuda.current_stream()
     gen = torch.Generator(device="cuda")
     gen.manual_seed(1000 + rank)
@@ -925,8 +954,22 @@ def gpu_arm(args):
 
     peak, peak_src = load_peaks()
     l0 = comm.launch_count()
-    with ClockSampler(local) as clk:
-        ms = time_loop(step, args.steps, args.warmup, stream, ws)
+    try:
+        with ClockSampler(local) as clk:
+            ms = time_loop(step, args.steps, args.warmup, stream, ws, comm)
+        if any_rank_error(comm, ws):
+            raise BenchAbort("device watchdog timeout in the timed region (MPXA_ERR_TIMEOUT)")
+    except BenchAbort as e:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": None, "unit": "GB/s", "n_gpus": N, "steps": args.steps,
+                              "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
+                              "error": str(e), "config": {"workload": "BASELINE configs[1]: allgather p=8, "
+                                                                     "64 MiB per rank", "ranks_per_gpu": R}}))
+        if multi:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     launches = comm.launch_count() - l0 - args.warmup
     # ---- parity spot check of the timed configuration (sampled columns, oracle) ----
     verified = None
