@@ -30,11 +30,11 @@
 #include "plan.h"
 
 namespace mpxa {
-cudaError_t launch_exec(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream);
-cudaError_t launch_small(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream);
+cudaError_t launch_exec(const ExecParams &P, int nC, int nG, int cooperative, bool pdl, cudaStream_t stream);
+cudaError_t launch_small(const ExecParams &P, int nC, int nG, int cooperative, bool pdl, cudaStream_t stream);
 cudaError_t launch_tiny(const ExecParams &P, int nC, bool pdl, cudaStream_t stream);
 cudaError_t launch_tiny_ms(const ExecParams &P, int nC, bool pdl, cudaStream_t stream);
-cudaError_t launch_tiny_ll(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream);
+cudaError_t launch_tiny_ll(const ExecParams &P, int nC, int nG, int cooperative, bool pdl, cudaStream_t stream);
 cudaError_t launch_counts(const int64_t *sc, int64_t *rc, int64_t *rd, int p, int r0, int nr,
                           cudaStream_t stream);
 cudaError_t launch_scan(const int64_t *counts, int64_t *rc, int64_t *rd, int p, int nr,
@@ -830,6 +830,17 @@ int make_params(mpxa_comm_t c, ExecParams &E, const DevProg &dp, const char *sen
     return MPXA_SUCCESS;
 }
 
+// Cooperative level of a launch (kernels.cu launch_kernel): CTAs that wait on one another must
+// be co-resident.  Emulated GPUs: cooperative (their CTA rows exchange flags; launches as in
+// round 1, no PDL).  Across processes every CTA may wait on a peer GPU's CTAs, which wait on
+// this grid's: cooperative + PDL, so no CTA spins while another of its grid is not scheduled
+// (another stream's kernel holding SMs).  One GPU: only launches with per-step row barriers
+// (barriers: several steps over several CTAs, not owned-flow).
+static int coop_level(mpxa_comm_t c, bool barriers) {
+    if (c->emulated) return 1;
+    return (c->nprocs > 1 || barriers) ? 2 : 0;
+}
+
 // pdl: the launch may overlap the previous kernel's tail (the kernel waits on
 // griddepcontrol before touching anything that kernel wrote).  Off for per-call programs,
 // whose tables arrive by a cudaMemcpyAsync right before the launch.
@@ -853,6 +864,7 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
     E.ahead = tc.ahead;
     ++c->epoch;   // host mirror only; the kernels keep the authoritative epoch in DevComm
     cudaError_t e;
+    int coop = 0;   // cooperative level of the launch (coop_level)
     bool tiny = false;
     const uint64_t maxmove = (uint64_t)dp.host.max_move * unit;
     uint64_t ppm = 1;   // 16-B pieces per move, rounded up to a power of two (shift decode)
@@ -1012,8 +1024,12 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
                 E.small_threads = (int32_t)std::max<uint64_t>(
                     64, std::min<uint64_t>(512, (cdiv(kitems, (uint64_t)std::max(1, nC)) + 31) / 32 * 32));
             }
-            e = launch_tiny_ll(E, std::max(1, nC), c->emulated ? c->G : 1, c->emulated, pdl && c->pdl, stream);
-        } else e = launch_small(E, std::max(1, nC), c->emulated ? c->G : 1, c->emulated, pdl && c->pdl, stream);
+            coop = coop_level(c, !one_step && nC > 1 && !E.small_own);
+            e = launch_tiny_ll(E, std::max(1, nC), c->emulated ? c->G : 1, coop, pdl && c->pdl, stream);
+        } else {
+            coop = coop_level(c, !one_step && nC > 1 && !E.small_own);
+            e = launch_small(E, std::max(1, nC), c->emulated ? c->G : 1, coop, pdl && c->pdl, stream);
+        }
         tiny = tiny || tiny_ll || tiny_ms;
     } else {
         int nC = gr.n();
@@ -1098,7 +1114,8 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
             E.stages = kWarpsExec * kWStages;   // dynamic smem = stages x chunk (every warp's ring)
             E.ahead = 0;
         }
-        e = launch_exec(E, nC, c->emulated ? c->G : 1, c->emulated, pdl && c->pdl, stream);
+        coop = coop_level(c, dp.nsteps > 1 && nC > 1);
+        e = launch_exec(E, nC, c->emulated ? c->G : 1, coop, pdl && c->pdl, stream);
     }
     if (e != cudaSuccess) {
         if (getenv("MPXA_DEBUG")) fprintf(stderr, "mpxa: launch failed: %s\n", cudaGetErrorString(e));
@@ -1108,7 +1125,8 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
     // execution path of this launch (tests assert the intended path ran: mpxa__last_launch)
     c->last_path = (small ? 1u : 0u) | (E.small_ll ? 2u : 0u) | (E.small_var ? 4u : 0u) |
                    (E.dyn_units ? 8u : 0u) | (E.dyn_sync ? 16u : 0u) | (E.small_own ? 32u : 0u) |
-                   (E.small_swork ? 64u : 0u) | (E.wring ? 128u : 0u) | (tiny ? 256u : 0u);
+                   (E.small_swork ? 64u : 0u) | (E.wring ? 128u : 0u) | (tiny ? 256u : 0u) |
+                   (coop ? 512u : 0u);
     return MPXA_SUCCESS;
 }
 

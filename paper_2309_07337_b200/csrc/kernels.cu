@@ -2362,26 +2362,42 @@ static cudaError_t launch_tiny_aw(const ExecParams &P, int nC, int nt, size_t sm
                          false, pdl, stream);
 }
 
-// Launch with the PDL attribute (pdl) or cooperatively (emulated GPUs: co-residency of the
-// virtual GPUs' CTA rows is required by the flag protocol).
+// Launch with the PDL attribute (pdl) and/or cooperatively.  cooperative = 1: the grid's CTAs
+// wait on one another (emulated GPUs' CTA rows, per-step row barriers, peers across processes)
+// and must be co-resident -- a cooperative launch guarantees it; 2: the same with PDL as well
+// (accepted on sm_100a: tools/probes/coop_probe.cu, +0.1-0.25 us per launch over PDL alone).
+// A cooperative launch the device cannot make co-resident falls back to the plain launch
+// (grids are sized to the co-resident count, so this is a guard, not a path).
 static cudaError_t launch_kernel(void (*kern)(ExecParams), const ExecParams &P, dim3 grid, dim3 block, size_t smem,
-                                 bool cooperative, bool pdl, cudaStream_t stream) {
+                                 int cooperative, bool pdl, cudaStream_t stream) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
+    int na = 0;
     if (cooperative) {
-        at[0].id = cudaLaunchAttributeCooperative;
-        at[0].val.cooperative = 1;
-    } else {
-        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+        at[na].id = cudaLaunchAttributeCooperative;
+        at[na].val.cooperative = 1;
+        na++;
+    }
+    if (!cooperative || cooperative == 2) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+        na++;
     }
     cfg.attrs = at;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, P);
+    cfg.numAttrs = na;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, P);
+    if (e == cudaErrorCooperativeLaunchTooLarge && cooperative == 2) {
+        (void)cudaGetLastError();
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, kern, P);
+    }
+    return e;
 }
 
 template <int KM, int AK>
@@ -2392,7 +2408,7 @@ static cudaError_t small_attr(size_t max_dyn) {
 }
 
 template <int KM, int AK>
-static cudaError_t launch_small_t(const ExecParams &P, size_t max_dyn, size_t smem, dim3 grid, bool cooperative,
+static cudaError_t launch_small_t(const ExecParams &P, size_t max_dyn, size_t smem, dim3 grid, int cooperative,
                                   bool pdl, cudaStream_t stream) {
     const cudaError_t a = small_attr<KM, AK>(max_dyn);
     if (a != cudaSuccess) return a;
@@ -2403,7 +2419,7 @@ static cudaError_t launch_small_t(const ExecParams &P, size_t max_dyn, size_t sm
 }
 
 template <int KM>
-static cudaError_t launch_small_km(const ExecParams &P, size_t max_dyn, size_t smem, dim3 grid, bool cooperative,
+static cudaError_t launch_small_km(const ExecParams &P, size_t max_dyn, size_t smem, dim3 grid, int cooperative,
                                    bool pdl, cudaStream_t stream) {
     // the 16-B decision is launch-wide unless peers' recv bases arrive at run time (mode 2)
     const int ak = P.mode == 2 ? 0 : (P.small_a16 ? 1 : (P.small_a8 ? 3 : 2));
@@ -2430,7 +2446,7 @@ cudaError_t launch_tiny(const ExecParams &P, int nC, bool pdl, cudaStream_t stre
     return launch_tiny_aw<0>(P, nC, nt, smem, pdl, stream);   // any alignment: words and funnel shifts
 }
 
-cudaError_t launch_tiny_ll(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream) {
+cudaError_t launch_tiny_ll(const ExecParams &P, int nC, int nG, int cooperative, bool pdl, cudaStream_t stream) {
     static cudaError_t a = cudaFuncSetAttribute(mpxa_tiny_ll_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 (int)(kSmallMovesSmem * sizeof(TLMove)));
     if (a != cudaSuccess) return a;
@@ -2445,7 +2461,7 @@ cudaError_t launch_tiny_ll(const ExecParams &P, int nC, int nG, bool cooperative
                          pdl, stream);
 }
 
-cudaError_t launch_small(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream) {
+cudaError_t launch_small(const ExecParams &P, int nC, int nG, int cooperative, bool pdl, cudaStream_t stream) {
     const dim3 grid(nC, nG);
     if (P.small_ll)
         return launch_small_km<kSmallLL>(P, kSmallMovesSmem * (sizeof(Move) + sizeof(uint16_t)),
@@ -2477,7 +2493,7 @@ static cudaError_t exec_attr_once() {
     return e0 != cudaSuccess ? e0 : e1;
 }
 
-cudaError_t launch_exec(const ExecParams &P, int nC, int nG, bool cooperative, bool pdl, cudaStream_t stream) {
+cudaError_t launch_exec(const ExecParams &P, int nC, int nG, int cooperative, bool pdl, cudaStream_t stream) {
     cudaError_t e = exec_attr_once();
     if (e != cudaSuccess) return e;
     const size_t smem = (size_t)P.stages * P.chunk;

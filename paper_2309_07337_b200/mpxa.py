@@ -280,7 +280,7 @@ class Comm:
         return n.value
 
     # bits of mpxa__last_launch (test hook, not part of the C ABI headers)
-    PATH_BITS = {"small": 1, "eager": 2, "var": 4, "dyn": 8, "sync": 16, "own": 32, "swork": 64, "wring": 128, "tiny": 256}
+    PATH_BITS = {"small": 1, "eager": 2, "var": 4, "dyn": 8, "sync": 16, "own": 32, "swork": 64, "wring": 128, "tiny": 256, "coop": 512}
 
     def last_launch_path(self) -> set:
         """Execution path of this comm's last collective launch (test hook)."""

@@ -739,6 +739,32 @@ def test_execution_paths_are_the_intended_ones(monkeypatch):
     del ag, out
 
 
+def test_cooperative_launches_where_ctas_wait_on_each_other():
+    """Launches whose CTAs wait on one another are cooperative (co-residency guaranteed, with
+    PDL): several steps over several CTAs on one GPU (per-step row barriers) and emulated GPUs;
+    one-step and owned-flow launches are not (mpxa__last_launch bit "coop")."""
+    p = 8
+    c1 = comm(p, 0, 2)
+    small = synth.alltoall_sendbuf(1, p, 16)
+    run_alltoall(c1, small, "pairwise")
+    assert "coop" not in c1.last_launch_path()
+    big = synth.alltoall_sendbuf(3, p, 1 << 20)            # Bruck, 1 MiB blocks: multi-step executor
+    assert np.array_equal(run_alltoall(c1, big, "bruck"), oracle.alltoall_definition(big))
+    path = c1.last_launch_path()
+    assert "coop" in path and "tiny" not in path and "own" not in path, sorted(path)
+    c4 = synth.cfg4_counts(5, p, 64 << 10, elem=8)          # hierarchical alltoallv: sync mode
+    send, sc, sd, rc, rd, S, Rcap = synth.alltoallv_buffers(5, c4, elem=8, packed=True)
+    recv0 = np.full((p, Rcap), 0xA5, dtype=np.uint8)
+    d_r = dev(recv0)
+    c1.alltoallv(dev(send), sc, sd, d_r, rc, rd, algo="hier", dtype_size=8)
+    path = c1.last_launch_path()
+    assert np.array_equal(host(d_r), oracle.alltoallv_definition(send, sc, sd, rc, rd, 8, recv0))
+    assert ("sync" in path) <= ("coop" in path), sorted(path)
+    ce = comm(p, 4, 2)
+    run_alltoall(ce, small, "pairwise")
+    assert "coop" in ce.last_launch_path()
+
+
 @pytest.mark.skipif(os.environ.get("MPXA_NO_LL", "0") != "0", reason="asserts the eager path")
 def test_eager_persistent_first_start_captured():
     """A persistent request's eager companion is built at *_init, so even a first start()
