@@ -188,6 +188,20 @@ def time_graph(fn, calls, stream):
     return statistics.median(times)
 
 
+def schedule_units(op, algo, p, R, g=0):
+    """HBM units (blocks) one call of (op, algo) reads + writes on ONE GPU, from the schedule
+    the library compiles (include/mpxa_plan.h): every move reads its source once and writes
+    each destination (a fan-out move: every rank).  For pairwise it equals the operation's
+    algorithmic bytes; Bruck / ring / hierarchical move more (their rounds and rotations),
+    so frac against it says whether a variant runs at the roofline of its OWN traffic."""
+    from paper_2309_07337_b200.mpxa import Plan
+    pl = Plan(op, algo, p, R=R, G=1, g=g or R)
+    total = 0
+    for m in pl.moves(0):
+        total += int(m.len) * (1 + (p if m.fanout else 1))
+    return total
+
+
 def sweep(comm, torch, stream, reps=200):
     """Per-size / per-variant us and GB/s on this device (BASELINE metric: vs block size).
     Every input is allocated and filled on the stream the collectives run on (the current
@@ -204,9 +218,11 @@ def _sweep(comm, torch, gstream, reps):
     p = comm.p
     R = comm.R
     out = {"timing": "CUDA graph of back-to-back calls (device us per call, median of 5 replays)",
-           "columns": ["bytes_per_block", "us", "aggregate_GBps", "hbm_roofline_frac"],
+           "columns": ["bytes_per_block", "us", "aggregate_GBps", "hbm_roofline_frac", "schedule_roofline_frac"],
            "roofline": "one GPU: t_roof = algorithmic HBM bytes (allgather R*b read + R*p*b write; alltoall "
-                       "2*R*p*b) / measured copy peak; frac = t_roof / t (small sizes are latency-bound)",
+                       "2*R*p*b) / measured copy peak; frac = t_roof / t (small sizes are latency-bound); "
+                       "schedule_roofline_frac: the same against the bytes the variant's compiled schedule "
+                       "reads + writes (Bruck rounds, ring steps, hierarchical gathers: bench.schedule_units)",
            "allgather": {}, "alltoall": {}}
     peak, _ = load_peaks()
     dev = "cuda"
@@ -214,6 +230,7 @@ def _sweep(comm, torch, gstream, reps):
     # allgather, cfg2 sizes 4 B .. 64 MiB (x2)
     for algo in ("pairwise", "bruck", "ring"):
         rows = []
+        sched = schedule_units("allgather", algo, p, R, comm.g)
         b = 4
         while b <= (64 << 20):
             send = big[: R * b].view(R, b)
@@ -223,13 +240,15 @@ def _sweep(comm, torch, gstream, reps):
             us = 1e3 * time_graph(fn, it, gstream)
             # HBM roofline of the operation on one GPU: read R*b, write R*p*b
             t_roof = (R * b + R * p * b) / (peak * 1e3)
-            rows.append([b, round(us, 3), round(p * p * b / us / 1e3, 2), round(t_roof / us, 4)])
+            rows.append([b, round(us, 3), round(p * p * b / us / 1e3, 2), round(t_roof / us, 4),
+                         round(sched * b / (peak * 1e3) / us, 4)])
             del recv
             b *= 2
         out["allgather"][algo] = rows
     # alltoall, cfg3 sizes 4 B .. 16 MiB (x4)
     for algo in ("pairwise", "bruck", "hier"):
         rows = []
+        sched = schedule_units("alltoall", algo, p, R, comm.g)
         b = 4
         while b <= (16 << 20):
             send = big[: R * p * b].view(R, p * b)
@@ -238,7 +257,8 @@ def _sweep(comm, torch, gstream, reps):
             fn = lambda: comm.alltoall(send, recv, algo=algo, stream=gstream)
             us = 1e3 * time_graph(fn, it, gstream)
             t_roof = 2 * R * p * b / (peak * 1e3)      # read + write every block once
-            rows.append([b, round(us, 3), round(p * p * b / us / 1e3, 2), round(t_roof / us, 4)])
+            rows.append([b, round(us, 3), round(p * p * b / us / 1e3, 2), round(t_roof / us, 4),
+                         round(sched * b / (peak * 1e3) / us, 4)])
             del recv
             b *= 4
         out["alltoall"][algo] = rows

@@ -54,3 +54,22 @@ def test_cpu_baseline_record():
     assert d["kind"] == "oracle" and d["unit"] == "GB/s" and d["value"] > 0
     assert 1 <= d["cores"] <= 4 and d["single_thread"]["cores"] == 1
     assert d["os_cpu_count"] >= 1 and d["affinity_cores"] >= 1
+
+
+def test_schedule_units_closed_forms():
+    """The sweep's per-variant HBM units (bench.schedule_units, read from the compiled
+    schedule) match the closed forms for p ranks on one GPU: pairwise allgather p + p^2
+    (one read, p writes per rank), pairwise alltoall 2p^2, ring allgather 2p(p-1) + 2p (p-1
+    forwarding steps plus the self copy), Bruck allgather 2p(p-1) + 2p^2 (rounds of 1, 2, 4 ..
+    blocks, then the final rotation), Bruck alltoall 2p*sum(m_k) + 2p^2 (the first rotation
+    is virtual; m_k = blocks with bit k set), hierarchical with one
+    group = pairwise."""
+    for p in (2, 5, 8):
+        K = (p - 1).bit_length()
+        m = sum(sum(1 for i in range(p) if i >> k & 1) for k in range(K))
+        assert bench.schedule_units("allgather", "pairwise", p, p, p) == p + p * p
+        assert bench.schedule_units("alltoall", "pairwise", p, p, p) == 2 * p * p
+        assert bench.schedule_units("allgather", "ring", p, p, p) == 2 * p * (p - 1) + 2 * p
+        assert bench.schedule_units("allgather", "bruck", p, p, p) == 2 * p * (p - 1) + 2 * p * p
+        assert bench.schedule_units("alltoall", "bruck", p, p, p) == 2 * p * m + 2 * p * p
+        assert bench.schedule_units("alltoall", "hier", p, p, p) == 2 * p * p
