@@ -247,7 +247,7 @@ struct RingEntry {
 };
 
 #ifdef MPXA_TRACE
-__device__ uint64_t g_cta_trace[2][kMaxCtas];   // per-CTA entry / exit %globaltimer (GPU 0)
+__device__ uint64_t g_cta_trace[6][kMaxCtas];   // per-CTA entry / exit / after the dependency wait / first piece / classified / first store (GPU 0)
 #define CTA_STAMP(w) do { if (threadIdx.x == 0 && blockIdx.y == 0) g_cta_trace[w][blockIdx.x] = globaltimer(); } while (0)
 // phase stamps of CTA 0 in SM cycles (clock64: one SM, so comparable and cycle-accurate)
 #define TRACE(k) do { if (blockIdx.x == 0 && blockIdx.y == 0 && (threadIdx.x == 0 || threadIdx.x == 32)) P.dc->trace[(k) + (threadIdx.x ? 16 : 0)] = (uint64_t)clock64(); } while (0)
@@ -272,6 +272,8 @@ struct ExecShared {
     StepInfo steps[kMaxStepsSmem];   // this CTA's view of every step, loaded once
     uint64_t epoch;      // this launch's epoch (device-side sequence number)
     uint32_t cts_ok;     // remote GPUs whose CTS for this epoch was observed
+    uint32_t kuni0;      // dynamic mode: dyn_classify's result for step 0's first tile when classified
+                         // in the prologue (before the dependency wait)
     int abort_flag;
     uint32_t pcA[kMoveTile + 1];  // dynamic mode: exclusive prefix of TMA pieces per move
     uint32_t pcB[kMoveTile + 1];  //               and of LSU pieces per move
@@ -352,6 +354,9 @@ struct Producer {
         const uint32_t s = stored % kRingStages;
         mbar_wait(smem_u32(&S.mbar[s]), (stored / kRingStages) & 1u);
         const RingEntry e = S.ring[s];
+#ifdef MPXA_TRACE
+        if (stored == 0) CTA_STAMP(5);
+#endif
         const uint32_t src = smem_u32(stages + (size_t)s * P.chunk);
         if (!e.fanout) {
             tma_store_1d(e.dst, src, e.len);
@@ -754,16 +759,18 @@ __device__ __noinline__ uint32_t dyn_classify(const ExecParams &P, ExecShared &S
 
 // One tile of at most kMoveTile moves (queues of tile ti).
 __device__ __noinline__ bool dyn_tile(const ExecParams &P, ExecShared &S, Producer &prod, int g, int first, int nm,
-                                      bool loaded, int ti) {
+                                      bool loaded, bool classified, int ti) {
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const uint64_t U = (uint64_t)P.dyn_u, chunk = (uint64_t)P.chunk;
-    const uint32_t kuni = dyn_classify(P, S, g, first, nm, loaded);
+    const uint32_t kuni = classified ? S.kuni0 : dyn_classify(P, S, g, first, nm, loaded);
+    CTA_STAMP(4);
     const uint32_t totA = S.pcA[nm], totB = S.pcB[nm];
     bool wrote = false;
     if (t == 0) {
         if (totA == 0) return false;
         uint32_t *q = &P.dc->dyn_next[g * kMaxDynTiles + ti];
         uint32_t u = atomicAdd(q, 1u);
+        CTA_STAMP(3);
         while (u < totA) {
             const uint32_t un = atomicAdd(q, 1u);   // next piece requested while this one streams
             const int mi = kuni ? (int)(u / kuni) : find_move(S.pcA, nm, u);
@@ -876,10 +883,10 @@ __device__ __forceinline__ void wring_shift_store(const char *stage, uint32_t sh
 // are not 16-B congruent (the LSU path's register-bound loads become TMA loads).  Pieces
 // shorter than kTmaMin, and shifted fan-out pieces, go through lsu_copy.
 __device__ __noinline__ bool dyn_tile_w(const ExecParams &P, ExecShared &S, int g, int first, int nm, bool loaded,
-                                        int ti) {
+                                        bool classified, int ti) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint64_t U = (uint64_t)P.dyn_u;
-    dyn_classify(P, S, g, first, nm, loaded);
+    if (!classified) dyn_classify(P, S, g, first, nm, loaded);
     const uint32_t totA = S.pcA[nm], tot = totA + S.pcB[nm];
     if (tot == 0) return false;
     extern __shared__ __align__(128) char dyn_smem[];
@@ -1026,11 +1033,14 @@ __device__ __noinline__ bool dyn_tile_w(const ExecParams &P, ExecShared &S, int 
 // Dynamic mode over the whole step: move tiles in order, each with its own pair of queues; a
 // CTA moves on to the next tile as soon as the current tile's queues are dry (no barrier).
 __device__ __noinline__ bool dyn_step(const ExecParams &P, ExecShared &S, Producer &prod, int g, int first, int nm,
-                                      bool loaded, int tile0) {
+                                      bool loaded, bool classified, int tile0) {
     bool wrote = false;
-    for (int tile = 0, ti = tile0; tile < nm; tile += kMoveTile, ti++)
-        wrote |= P.wring ? dyn_tile_w(P, S, g, first + tile, min(kMoveTile, nm - tile), loaded && tile == 0, ti)
-                         : dyn_tile(P, S, prod, g, first + tile, min(kMoveTile, nm - tile), loaded && tile == 0, ti);
+    for (int tile = 0, ti = tile0; tile < nm; tile += kMoveTile, ti++) {
+        const int cnt = min(kMoveTile, nm - tile);
+        const bool l0 = loaded && tile == 0, c0 = classified && tile == 0;
+        wrote |= P.wring ? dyn_tile_w(P, S, g, first + tile, cnt, l0, c0, ti)
+                         : dyn_tile(P, S, prod, g, first + tile, cnt, l0, c0, ti);
+    }
     return wrote;
 }
 
@@ -1164,8 +1174,20 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
     if (t < kWarpsExec) S.wseq[t] = 0;
     TRACE(10);
     __syncthreads();
+    // Dynamic mode on one GPU: step 0's first move tile (prefetched above) is classified and
+    // its piece prefixes scanned BEFORE the dependency wait -- it reads only this launch's
+    // moves, parameters and buffer bases, nothing a previous kernel writes -- so the ~2 us
+    // of cold-instruction classification overlaps the previous kernel's tail (measured, p = 8
+    // allgather 4 MiB: wait -> first piece 2.4 us, MPXA_TRACE build, tools/ag_trace2.py).
+    // Peers' bases (several GPUs) arrive with the CTS after the wait: classified there.
+    const bool pre_cls = DYN && pre && !multi && nsteps > 0;
+    if (pre_cls) {
+        const uint32_t k0 = dyn_classify(P, S, g, S.steps[0].first, min(kMoveTile, S.steps[0].nm), true);
+        if (t == 0) S.kuni0 = k0;
+    }
     griddep_wait();
     griddep_launch_dependents();
+    CTA_STAMP(2);
     if (multi) {
         if (t == 0) S.epoch = *(volatile uint64_t *)&P.dc->epoch + 1;
         __syncthreads();
@@ -1225,7 +1247,7 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
         const int nm = DYN ? 0 : st.nm;   // dynamic mode: the work queue below
         const int rot = nm ? (int)(((int64_t)sl + (int64_t)g * nm / P.G) % nm) : 0;
         if (DYN) {
-            wrote = dyn_step(P, S, prod, g, st.first, st.nm, pre && s == 0, tile_base);
+            wrote = dyn_step(P, S, prod, g, st.first, st.nm, pre && s == 0, pre_cls && s == 0, tile_base);
             tile_base += (st.nm + kMoveTile - 1) / kMoveTile;
         }
         for (int tile = 0; tile < nm; tile += kMoveTile) {
@@ -2630,7 +2652,7 @@ int exec_max_ctas_per_sm(size_t dyn_smem) {
 #ifdef MPXA_TRACE
 extern "C" int mpxa__cta_trace(uint64_t *out) {   // debug hook: [2][kMaxCtas] stamps; NULL resets
     if (!out) {
-        static uint64_t zero[2][mpxa::kMaxCtas];
+        static uint64_t zero[6][mpxa::kMaxCtas];
         return cudaMemcpyToSymbol(mpxa::g_cta_trace, zero, sizeof zero) == cudaSuccess ? 0 : 6;
     }
     return cudaMemcpyFromSymbol(out, mpxa::g_cta_trace, sizeof(mpxa::g_cta_trace)) == cudaSuccess ? 0 : 6;
