@@ -1179,10 +1179,17 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
     // moves, parameters and buffer bases, nothing a previous kernel writes -- so the ~2 us
     // of cold-instruction classification overlaps the previous kernel's tail (measured, p = 8
     // allgather 4 MiB: wait -> first piece 2.4 us, MPXA_TRACE build, tools/ag_trace2.py).
-    // Peers' bases (several GPUs) arrive with the CTS after the wait: classified there.
-    const bool pre_cls = DYN && pre && !multi && nsteps > 0;
+    // Peers' bases (several GPUs) arrive with the CTS after the wait: classified there.  A
+    // step 0 that is not dense (alltoallv) has its first tile loaded here first (program
+    // tables are this launch's: persistent, or uploaded before a launch without PDL).
+    const bool pre_cls = DYN && steps_in_smem && !multi && nsteps > 0;
     if (pre_cls) {
-        const uint32_t k0 = dyn_classify(P, S, g, S.steps[0].first, min(kMoveTile, S.steps[0].nm), true);
+        const int nm0 = min(kMoveTile, S.steps[0].nm);
+        if (!pre) {
+            if (t < nm0) S.moves[t] = prog.moves[S.steps[0].first + t];
+            __syncthreads();
+        }
+        const uint32_t k0 = dyn_classify(P, S, g, S.steps[0].first, nm0, true);
         if (t == 0) S.kuni0 = k0;
     }
     griddep_wait();
@@ -1247,7 +1254,7 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
         const int nm = DYN ? 0 : st.nm;   // dynamic mode: the work queue below
         const int rot = nm ? (int)(((int64_t)sl + (int64_t)g * nm / P.G) % nm) : 0;
         if (DYN) {
-            wrote = dyn_step(P, S, prod, g, st.first, st.nm, pre && s == 0, pre_cls && s == 0, tile_base);
+            wrote = dyn_step(P, S, prod, g, st.first, st.nm, (pre || pre_cls) && s == 0, pre_cls && s == 0, tile_base);
             tile_base += (st.nm + kMoveTile - 1) / kMoveTile;
         }
         for (int tile = 0; tile < nm; tile += kMoveTile) {
