@@ -887,6 +887,7 @@ __device__ __noinline__ bool dyn_tile_w(const ExecParams &P, ExecShared &S, int 
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint64_t U = (uint64_t)P.dyn_u;
     if (!classified) dyn_classify(P, S, g, first, nm, loaded);
+    CTA_STAMP(4);
     const uint32_t totA = S.pcA[nm], tot = totA + S.pcB[nm];
     if (tot == 0) return false;
     extern __shared__ __align__(128) char dyn_smem[];
@@ -1004,6 +1005,9 @@ __device__ __noinline__ bool dyn_tile_w(const ExecParams &P, ExecShared &S, int 
         __syncwarp();   // lane 0's stage descriptor before every lane reads it
         const uint32_t s = (base + consumed) % (uint32_t)kWStages;
         mbar_wait(smem_u32(&S.wmbar[w][s]), ((base + consumed) / (uint32_t)kWStages) & 1u);
+#ifdef MPXA_TRACE
+        if (consumed == 0 && w == 0) CTA_STAMP(5);
+#endif
         const ExecShared::WEntry &e = S.went[w][s];
         const char *stage = ring + (size_t)s * kWChunk;
         if (e.kind == 0) {
