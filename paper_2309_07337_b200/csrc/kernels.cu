@@ -2572,6 +2572,63 @@ __global__ void __launch_bounds__(256) part_pready(mpxa_psend_dev_t ch, int p0, 
     mpxa_dev_pready_part(&ch, i, lo, hi, nct);
 }
 
+// Host-enqueued Pready of large 16-B aligned partitions: the same (partition, slice) CTAs, each
+// slice streamed by ONE thread through a TMA ring (kPartStages x kPartChunk of shared memory,
+// loads kept kPartAhead chunks ahead of the oldest store) instead of the CTA's LSU loop (4 x 16 B
+// in flight per thread): f3 256 MiB in 16 partitions, see DESIGN §8 f3.  The slice's bulk
+// writes complete (wait_group 0) and are fenced to the generic proxy before the CTA counts
+// itself (acq_rel) and the last CTA of the partition releases its arrival flag.
+constexpr int kPartStages = 4, kPartAhead = 3;
+constexpr unsigned long long kPartTmaMin = 64ull << 20;   // calls from 64 MiB take the TMA slices (measured:
+                                                         // the LSU loop is as fast or faster below)
+constexpr unsigned long long kPartSliceMax = 256ull << 10;
+constexpr uint32_t kPartChunk = 16384;
+__global__ void __launch_bounds__(32) part_pready_tma(mpxa_psend_dev_t ch, int p0, unsigned long long chunk,
+                                                      unsigned int nct) {
+    extern __shared__ __align__(128) char pbuf[];
+    __shared__ __align__(8) uint64_t mbar[kPartStages];
+    part_enter();
+    if (threadIdx.x != 0) return;
+    const int i = p0 + (int)(blockIdx.x / nct);
+    const unsigned long long k = blockIdx.x % nct;
+    const unsigned long long lo = k * chunk;
+    const unsigned long long hi = lo + chunk < ch.part_bytes ? lo + chunk : ch.part_bytes;
+    const unsigned long long cyc = *(volatile const unsigned long long *)ch.scycle;
+    if (mpxa_dev_wait_ge(ch.cts, cyc, ch.err, ch.timeout_ns)) return;   // clear to send
+    for (int s = 0; s < kPartStages; s++) mbar_init(smem_u32(&mbar[s]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const char *src = (const char *)ch.src + (unsigned long long)i * ch.part_bytes;
+    char *dst = (char *)ch.dst + (unsigned long long)i * ch.part_bytes;
+    uint32_t issued = 0, stored = 0;
+    __shared__ unsigned long long ooff[kPartStages];   // each stage's offset / length
+    __shared__ uint32_t olen[kPartStages];
+    auto store_one = [&]() {
+        const uint32_t st = stored % kPartStages;
+        mbar_wait(smem_u32(&mbar[st]), (stored / kPartStages) & 1u);
+        tma_store_1d(dst + ooff[st], smem_u32(pbuf + (size_t)st * kPartChunk), olen[st]);
+        bulk_commit();
+        stored++;
+    };
+    for (unsigned long long o = lo; o < hi; o += kPartChunk) {
+        if (issued - stored == (uint32_t)kPartAhead) store_one();
+        const uint32_t st = issued % kPartStages;
+        if (issued >= (uint32_t)kPartStages) bulk_wait_read((int)(stored - 1 - (issued - kPartStages)));
+        ooff[st] = o;
+        olen[st] = (uint32_t)(hi - o < kPartChunk ? hi - o : kPartChunk);
+        tma_load_1d(smem_u32(pbuf + (size_t)st * kPartChunk), src + o, olen[st], smem_u32(&mbar[st]));
+        issued++;
+    }
+    while (stored < issued) store_one();
+    bulk_wait_all();
+    fence_proxy_async();   // the bulk writes before the generic-proxy release below
+    unsigned int prev = 0u;
+    if (nct > 1u) asm volatile("atom.acq_rel.sys.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&ch.done[i]) : "memory");
+    if (prev + 1u == nct) {
+        if (nct > 1u) ch.done[i] = 0;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&ch.arr[i]), "l"(cyc) : "memory");
+    }
+}
+
 // stream-ordered Parrived / completion: block until flags[lo, hi) >= *cycle (one CTA)
 __global__ void part_wait_flags(const unsigned long long *flags, int lo, int hi, const unsigned long long *cycle,
                                 int *err, long long timeout_ns) {
@@ -2613,6 +2670,38 @@ cudaError_t launch_part_start(bool sender, unsigned long long *cycle, unsigned l
 }
 
 cudaError_t launch_part_pready(const mpxa_psend_dev_t &ch, int p0, int np, cudaStream_t stream) {
+    // large 16-B aligned calls: TMA slices, 3 CTAs per SM (64 KiB of shared memory each),
+    // slices a multiple of 16 B
+    if (np > 0 && ch.part_bytes * (unsigned long long)np >= kPartTmaMin &&
+        !(((uintptr_t)ch.src | (uintptr_t)ch.dst | ch.part_bytes) & 15)) {
+        static cudaError_t a = cudaFuncSetAttribute(part_pready_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    (int)(kPartStages * kPartChunk));
+        if (a != cudaSuccess) return a;
+        // slices: the call's bytes over one wave of 3 CTAs / SM, at most kPartSliceMax -- large
+        // calls run several waves of short slices, so SMs that stream faster take more of them
+        // (the block scheduler balances; one wave of long slices waits for the slowest SMs:
+        // measured, 256 MiB in 16 partitions 107 -> 99.7 us per cycle, 128-256 KiB slices best)
+        int dev = 0, sms = 148;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            sms = 148;
+        unsigned long long nct = 3ull * (unsigned long long)sms / (unsigned long long)np;   // one wave
+        if (nct < 1) nct = 1;
+        unsigned long long per = ((ch.part_bytes + nct - 1) / nct + 15) & ~15ull;
+        if (per > kPartSliceMax) per = kPartSliceMax;   // large calls: several waves of short slices
+        if (per < kPartChunk) per = kPartChunk;
+        nct = (ch.part_bytes + per - 1) / per;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(np * nct));
+        cfg.blockDim = dim3(32);
+        cfg.dynamicSmemBytes = kPartStages * kPartChunk;
+        cfg.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, part_pready_tma, ch, p0, per, (unsigned)nct);
+    }
     // CTAs per partition: 32 KiB pieces, up to ~4 waves of the machine over the whole call
     const unsigned long long chunk = 32ull << 10;
     unsigned long long nct = (ch.part_bytes + chunk - 1) / chunk;

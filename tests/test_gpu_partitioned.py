@@ -140,6 +140,39 @@ def test_256MiB_channel_producer_on_other_stream(n_s, n_r):
     c.finalize()
 
 
+def test_large_pready_ranges_out_of_order():
+    """Host Pready calls of >= 64 MiB take the TMA slice kernel (several waves of short
+    slices); ranges readied out of order and one partition at a time (p0 > 0) deliver the
+    same bytes, and Parrived follows the coverage oracle after each call."""
+    c = Comm(ranks_per_proc=2, device=0, timeout_s=20.0)
+    nbytes, n_s, n_r = 256 << 20, 4, 8
+    s = torch.empty(nbytes, dtype=torch.uint8, device=DEV)
+    r = torch.empty(nbytes, dtype=torch.uint8, device=DEV)
+    ps = c.psend_init(s, n_s, 0, 1)
+    pr = c.precv_init(r, n_r, 1, 0)
+    c.pmatch()
+    gen = torch.Generator(device=DEV)
+    for cyc, order in enumerate(([(2, 4), (0, 2)], [(3, 4), (1, 2), (0, 1), (2, 3)])):
+        gen.manual_seed(5 + cyc)
+        s.random_(0, 256, generator=gen)
+        r.zero_()
+        torch.cuda.synchronize()
+        pr.start(); ps.start()
+        ready = np.zeros(n_s, np.uint8)
+        for lo, hi in order:
+            ps.pready(lo, hi)
+            torch.cuda.synchronize()
+            ready[lo:hi] = 1
+            want = oracle.part_arrived(n_s, nbytes // n_s, n_r, nbytes // n_r, ready)
+            assert [pr.parrived(j) for j in range(n_r)] == list(want), (cyc, lo, hi)
+        ps.wait(); pr.wait()
+        torch.cuda.synchronize()
+        assert torch.equal(r, s), cyc
+    assert c.check() == 0
+    ps.free(); pr.free()
+    c.finalize()
+
+
 def test_device_parrived_orders_consumer_after_arrival():
     """mpxa_parrived_wait on the consumer stream: the copy behind it sees partition 0 even
     though the sender readies it only after a long device delay on another stream."""
