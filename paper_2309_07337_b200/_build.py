@@ -8,8 +8,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmpxa.so")
-SOURCES = ["kernels.cu", "api.cpp", "plan.cpp"]
-HEADERS = ["mpxa_internal.h", "plan.h"]
+SOURCES = ["exec_kernel.cu", "small_kernels.cu", "aux_kernels.cu", "api.cpp", "plan.cpp"]
+HEADERS = ["mpxa_internal.h", "plan.h", "kern_common.cuh"]
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

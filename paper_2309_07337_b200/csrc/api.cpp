@@ -830,7 +830,7 @@ int make_params(mpxa_comm_t c, ExecParams &E, const DevProg &dp, const char *sen
     return MPXA_SUCCESS;
 }
 
-// Cooperative level of a launch (kernels.cu launch_kernel): CTAs that wait on one another must
+// Cooperative level of a launch (kern_common.cuh launch_kernel): CTAs that wait on one another must
 // be co-resident.  Emulated GPUs: cooperative (their CTA rows exchange flags; launches as in
 // round 1, no PDL).  Across processes every CTA may wait on a peer GPU's CTAs, which wait on
 // this grid's: cooperative + PDL, so no CTA spins while another of its grid is not scheduled
@@ -1098,7 +1098,7 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
         }
         // warp-ring dynamic mode: when some moves may not be 16-B congruent, every warp streams
         // its own pieces through a TMA ring -- congruent ones with bulk stores, the others with
-        // 16-B stores the warp shifts out of shared memory (kernels.cu dyn_tile_w; measured,
+        // 16-B stores the warp shifts out of shared memory (exec_kernel.cu dyn_tile_w; measured,
         // cfg4 mean 4 MiB int64: 96.9 / 103.1 / 106.6 -> 92.3 / 87.2 / 100.6 us, seeds 0-2)
         // (measured, cfg4 int64, first version: the LSU path won below ~100 MiB per GPU -- mean
         // 1 MiB 24.3 vs 25.7 us -- and the warp rings above: mean 2 MiB 55.5 -> 51.9, 4 MiB 96.9

@@ -1,5 +1,5 @@
 // Internal types shared by the host runtime (comm.cpp, plan.cpp, api.cpp) and the sm_100a
-// kernels (kernels.cu).  Not part of the C ABI (include/mpxa.h).
+// kernels (exec_kernel.cu, small_kernels.cu, aux_kernels.cu).  Not part of the C ABI (include/mpxa.h).
 //
 // Execution model: every collective call is compiled, on the host, into a
 // PROGRAM per GPU: a list of STEPS, each a list of MOVES (byte copies between rank
