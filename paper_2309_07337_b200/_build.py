@@ -8,8 +8,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmpxa.so")
-SOURCES = ["exec_kernel.cu", "small_kernels.cu", "aux_kernels.cu", "api.cpp", "plan.cpp"]
-HEADERS = ["mpxa_internal.h", "plan.h", "kern_common.cuh"]
+SOURCES = ["exec_kernel.cu", "small_kernels.cu", "aux_kernels.cu", "comm.cpp", "launch.cpp", "collectives.cpp",
+           "partitioned.cpp", "selector.cpp", "plan_api.cpp", "plan.cpp"]
+HEADERS = ["mpxa_internal.h", "plan.h", "kern_common.cuh", "runtime.h"]
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

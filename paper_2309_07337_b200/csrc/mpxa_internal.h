@@ -1,4 +1,4 @@
-// Internal types shared by the host runtime (comm.cpp, plan.cpp, api.cpp) and the sm_100a
+// Internal types shared by the host runtime (comm.cpp, launch.cpp, collectives.cpp, partitioned.cpp, plan.cpp, ...) and the sm_100a
 // kernels (exec_kernel.cu, small_kernels.cu, aux_kernels.cu).  Not part of the C ABI (include/mpxa.h).
 //
 // Execution model: every collective call is compiled, on the host, into a

@@ -1,6 +1,6 @@
 // Schedule builders: compile one collective call into a per-GPU program of steps and moves
 // (mpxa_internal.h).  Pure host logic, no CUDA calls -- exported for CPU tests through
-// mpxa_plan_* in api.cpp.
+// mpxa_plan_* in plan_api.cpp.
 #pragma once
 #include <stdint.h>
 
