@@ -131,10 +131,18 @@ int mpxa_comm_check(mpxa_comm_t comm);
 int mpxa_launch_count(mpxa_comm_t comm, uint64_t *count);
 
 /* Collective registration of a device buffer for direct peer writes (multi-process mode;
- * a no-op in single-process mode).  The whole [ptr, ptr+bytes) range must lie in one
- * cudaMalloc allocation. */
+ * a no-op in single-process mode): every process calls it with a buffer of its own; the
+ * cudaMalloc allocation holding ptr becomes a window (its CUDA IPC handle is exchanged through
+ * the bootstrap and opened by every peer), so later collectives into any buffer inside it
+ * resolve peers' destinations on the device (window id + offset in the clear-to-send message).
+ * The whole [ptr, ptr+bytes) range must lie in one cudaMalloc allocation, and that allocation
+ * must stay allocated until mpxa_finalize: windows are never unmapped (mpxa_deregister is a
+ * no-op), so an allocation freed and re-made at the same address (e.g. after
+ * torch.cuda.empty_cache()) would still resolve to the peers' old mapping.  Persistent *_init
+ * calls register their recvbuf implicitly.  Errors: MPXA_ERR_ARG (NULL, or ptr not inside a
+ * device allocation), MPXA_ERR_NOMEM (more than 16 windows), MPXA_ERR_CUDA (IPC failure). */
 int mpxa_register(mpxa_comm_t comm, void *ptr, size_t bytes);
-int mpxa_deregister(mpxa_comm_t comm, void *ptr);
+int mpxa_deregister(mpxa_comm_t comm, void *ptr);   /* no-op (see mpxa_register) */
 
 /* ---- one-shot collectives (MPI semantics) ---------------------------- */
 /* count elements of dtype_size bytes per destination block. */
