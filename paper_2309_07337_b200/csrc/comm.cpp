@@ -122,6 +122,7 @@ void read_knobs(mpxa_comm_t c) {
     if (const char *e = getenv("MPXA_NO_WRING")) c->wring = atoi(e) == 0 ? 1 : 0;
     if (const char *e = getenv("MPXA_WRING")) c->wring = atoi(e);
     if (const char *e = getenv("MPXA_DYN_PIECES")) c->dyn_pieces = std::max(1, atoi(e));
+    if (const char *e = getenv("MPXA_NO_PREFETCH")) c->prefetch = atoi(e) ? 0 : 1;
     if (const char *e = getenv("MPXA_NO_TINY")) c->tiny = atoi(e) == 0;
     if (const char *e = getenv("MPXA_TINY_EVEN")) c->tiny_even = atoi(e) != 0;
     if (const char *e = getenv("MPXA_WSLACK")) c->wslack = std::max(1, std::min(kWStages - 1, atoi(e)));
@@ -174,7 +175,7 @@ void read_knobs(mpxa_comm_t c) {
 // knob, the selector table, the forced variants and the initial heap size (heap growth is
 // a collective IPC exchange: the sizes must evolve identically on every process).
 uint64_t knob_digest(mpxa_comm_t c, size_t heap) {
-    const int64_t v[] = {c->force_ns, c->force_nf, c->force_big, c->force_exec, c->pdl, c->dyn, c->wring, c->wslack, c->tiny, c->tiny_even, c->dyn_pieces,
+    const int64_t v[] = {c->force_ns, c->force_nf, c->force_big, c->force_exec, c->pdl, c->dyn, c->wring, c->wslack, c->tiny, c->tiny_even, c->dyn_pieces, c->prefetch,
                          (int64_t)c->dyn_min_total, c->force_sync, c->small_sync, (int64_t)c->small_max1,
                          (int64_t)c->small_vol1, c->var_chop, c->var_tiles, c->swork, c->small_nt, c->ll,
                          (int64_t)c->one_cta_items, (int64_t)c->small_items, (int64_t)c->own_vol,

@@ -679,6 +679,28 @@ __device__ __noinline__ bool dyn_step(const ExecParams &P, ExecShared &S, Produc
     return wrote;
 }
 
+// Pre-wait L2 prefetch of the source of the pieces the grid takes first -- pieces c + k *
+// gridDim.x, k < P.dyn_prefetch -- while the previous kernel finishes: a cache fill only (L2 is
+// the device's point of coherence; the data is read after the wait), so the first loads after
+// the wait hit L2 instead of queueing behind the whole grid's initial DRAM burst (measured,
+// DESIGN §4 launch timeline).
+__device__ __noinline__ void dyn_prefetch_first(const ExecParams &P, const ExecShared &S, int nm0) {
+    const int t = threadIdx.x;
+    if (t >= P.dyn_prefetch) return;
+    const uint64_t U = (uint64_t)P.dyn_u;
+    const uint32_t totA = S.pcA[nm0], tot = totA + S.pcB[nm0];
+    const uint32_t u = blockIdx.x + (uint32_t)t * gridDim.x;
+    if (u >= tot) return;
+    const bool isA = u < totA;
+    const uint32_t *pc = isA ? S.pcA : S.pcB;
+    const uint32_t uu = isA ? u : u - totA;
+    const int mi = find_move(pc, nm0, uu);
+    const MovePlan mp = piece_plan(P, S, mi, (uint64_t)(uu - pc[mi]) * U, U);
+    const uintptr_t a0 = (uintptr_t)mp.src & ~(uintptr_t)15;
+    const uintptr_t a1 = ((uintptr_t)mp.src + mp.n + 15) & ~(uintptr_t)15;
+    if (a1 > a0) prefetch_l2(a0, (uint32_t)(a1 - a0));
+}
+
 // Multi-step dynamic mode: every CTA of this GPU row has finished step s (its writes complete
 // and fenced) -- a counter barrier; the grid never exceeds the co-resident CTA count.
 __device__ __noinline__ void row_barrier(const ExecParams &P, ExecShared &S, int g, int s) {
@@ -826,6 +848,9 @@ __global__ void __launch_bounds__(kThreads, MPXA_EXEC_MINB) mpxa_exec_kernel(con
         }
         const uint32_t k0 = dyn_classify(P, S, g, S.steps[0].first, nm0, true);
         if (t == 0) S.kuni0 = k0;
+        // L2 prefetch of the source of the grid's first pieces (out of line: its code is only
+        // fetched by launches that use it)
+        if (P.dyn_prefetch) dyn_prefetch_first(P, S, nm0);
     }
     griddep_wait();
     griddep_launch_dependents();

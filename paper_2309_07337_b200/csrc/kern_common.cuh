@@ -219,6 +219,10 @@ __device__ __forceinline__ void bulk_wait_read(int n) {
         default: asm volatile("cp.async.bulk.wait_group.read 8;" ::: "memory"); break;
     }
 }
+// bulk prefetch of [a, a + bytes) into L2 (16-B aligned, a 16-B multiple)
+__device__ __forceinline__ void prefetch_l2(uintptr_t a, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
 
 __device__ __forceinline__ int clampi(int64_t v, int n) { return v < 0 ? 0 : v > n ? n : (int)v; }

@@ -193,6 +193,8 @@ struct ExecParams {
                                // (not all 8): pieces move as 4-byte words, no funnel shifts
     int32_t tiny_step_items;   // tiny multi-step kernel: 16-B pieces of the busiest step (launch
                                // choice of the one-piece-per-thread build)
+    int32_t dyn_prefetch;      // dynamic mode, one GPU: the grid's first pieces (this many per CTA)
+                               // prefetched into L2 before the dependency wait
 };
 
 }  // namespace mpxa

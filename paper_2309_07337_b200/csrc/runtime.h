@@ -104,6 +104,7 @@ constexpr uint64_t kDynMinTotal = 8u << 20;    // smallest per-GPU step volume
 constexpr uint64_t kDynSyncMin = 128u << 20;
 constexpr int64_t kDynSyncMoves = 32;
 constexpr uint64_t kDynSyncMinUneven = 16u << 20;
+constexpr uint64_t kWringPrefetchVol = 128u << 20;   // warp rings: pre-wait L2 prefetch from this volume
 constexpr uint64_t kWringMinVol = 48u << 20;   // warp-ring mode: smallest busiest-GPU volume (96 MiB
                                                // before the constant-shift stores; measured since, cfg4:
                                                // mean 1 MiB (58 MiB) 25.9 / 29.5 -> 25.2 / 28.3 us with
@@ -208,6 +209,7 @@ struct mpxa_comm_s {
     int wring = 1;                            // warp-ring dynamic mode: 1 when moves may be misaligned,
                                               // MPXA_NO_WRING=1: never (LSU-register path), MPXA_WRING=2: always
     int dyn_pieces = (int)kDynPiecesPerCta;   // MPXA_DYN_PIECES: queue pieces per CTA (tuning)
+    int prefetch = 1;                         // MPXA_NO_PREFETCH=1: no pre-wait L2 prefetch (dynamic mode)
     int wslack = 2;                           // MPXA_WSLACK: warp-ring stages kept out of the load window
     bool tiny = true;                         // MPXA_NO_TINY=1: small one-GPU launches in the general kernel
     bool tiny_even = true;                    // MPXA_TINY_EVEN=0: tiny-kernel blocks sized like the general kernel's

@@ -126,7 +126,9 @@ KNOBS = [{"MPXA_NO_LL": "1"}, {"MPXA_NO_SMALL": "1"}, {"MPXA_NO_DYN": "1"}, {"MP
          # the round-2 grid sizing choices, reverted: power-of-two tiny blocks, 2048 pieces per
          # small-kernel CTA, the smaller owned-flow limits
          {"MPXA_TINY_EVEN": "0"}, {"MPXA_SMALL_ITEMS": "2048"},
-         {"MPXA_OWN_VOL": "2097152", "MPXA_OWN_PER_CTA": "65536"}]
+         {"MPXA_OWN_VOL": "2097152", "MPXA_OWN_PER_CTA": "65536"},
+         # no pre-wait L2 prefetch of the dynamic mode's first pieces
+         {"MPXA_NO_PREFETCH": "1", "MPXA_NO_SMALL": "1"}]
 
 
 @pytest.mark.parametrize("knob", range(len(KNOBS)), ids=[",".join(k) for k in KNOBS])
