@@ -684,11 +684,11 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
         }
         // pre-wait L2 prefetch of the grid's first pieces (one GPU; kernel prologue): one piece
         // per CTA for the producer ring (allgather 4 / 64 MiB 56.1 / 746.4 -> 54.0 / 744.6 us,
-        // alltoall 4 MiB blocks 83.0 -> 82.5); for the warp rings one per warp from 128 MiB per
-        // launch (cfg4 mean 4 MiB 88.2 -> 87.4 us; at mean 1 MiB any prefetch cost 1-2 %)
+        // alltoall 4 MiB blocks 83.0 -> 82.5), one per warp for the warp rings (cfg4 mean 2 / 4
+        // MiB 48.6 / 88.2 -> 47.0 / 87.2 us; two per warp or one per CTA: no better)
         // (profiles/r02/prewait_l2_ab.txt)
         if (E.dyn_units && c->G == 1 && c->nprocs == 1 && c->prefetch)
-            E.dyn_prefetch = !E.wring ? 1 : (wr_vol >= kWringPrefetchVol ? kWarpsExec : 0);
+            E.dyn_prefetch = E.wring ? kWarpsExec : 1;
         coop = coop_level(c, dp.nsteps > 1 && nC > 1);
         e = launch_exec(E, nC, c->emulated ? c->G : 1, coop, pdl && c->pdl, stream);
     }
