@@ -111,12 +111,17 @@ __global__ void __launch_bounds__(32) part_pready_tma(mpxa_psend_dev_t ch, int p
                                                       unsigned int nct) {
     extern __shared__ __align__(128) char pbuf[];
     __shared__ __align__(8) uint64_t mbar[kPartStages];
-    part_enter();
-    if (threadIdx.x != 0) return;
     const int i = p0 + (int)(blockIdx.x / nct);
     const unsigned long long k = blockIdx.x % nct;
     const unsigned long long lo = k * chunk;
     const unsigned long long hi = lo + chunk < ch.part_bytes ? lo + chunk : ch.part_bytes;
+    // the slice's first chunks into L2 before the dependency wait -- a cache fill only, read
+    // after the wait (measured, 256 MiB cycle 98.6-100.1 -> 97.3-98.8 us)
+    if (threadIdx.x == 0 && hi > lo)
+        prefetch_l2((uintptr_t)(ch.src + (unsigned long long)i * ch.part_bytes + lo),
+                    (uint32_t)min(hi - lo, (unsigned long long)kPartAhead * kPartChunk));
+    part_enter();
+    if (threadIdx.x != 0) return;
     const unsigned long long cyc = *(volatile const unsigned long long *)ch.scycle;
     if (mpxa_dev_wait_ge(ch.cts, cyc, ch.err, ch.timeout_ns)) return;   // clear to send
     for (int s = 0; s < kPartStages; s++) mbar_init(smem_u32(&mbar[s]), 1);
