@@ -681,6 +681,16 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
             E.chunk = kWChunk;
             E.stages = kWarpsExec * kWStages;   // dynamic smem = stages x chunk (every warp's ring)
             E.ahead = 0;
+            if (dp.nsteps == 1) {
+                // queue pieces: the same share per CTA as above, but rounded to the nearest warp
+                // chunk (4 KiB) instead of down to a 16 KiB ring chunk -- e.g. 28 instead of 16
+                // KiB at cfg4 mean 8 MiB (measured: mean 6 / 8 MiB 124.7 / 165.6 -> 123.3 / 162.3
+                // us, seed 1 162.3 -> 156.9; 2 / 4 MiB unchanged; 4 / 8 KiB pieces much slower)
+                uint64_t U = src_vol / ((uint64_t)nC * (uint64_t)c->dyn_pieces);
+                U = std::max<uint64_t>(kWringMinPiece, std::min<uint64_t>(U, kDynMaxPiece));
+                if (ntiles >= 4) U = std::max<uint64_t>(U, 3 * (uint64_t)kTmaMid.chunk);   // (as above)
+                E.dyn_u = (int32_t)((U + kWChunk / 2) / kWChunk * kWChunk);
+            }
         }
         // pre-wait L2 prefetch of the grid's first pieces (one GPU; kernel prologue): one piece
         // per CTA for the producer ring (allgather 4 / 64 MiB 56.1 / 746.4 -> 54.0 / 744.6 us,

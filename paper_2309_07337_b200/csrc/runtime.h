@@ -104,6 +104,7 @@ constexpr uint64_t kDynMinTotal = 8u << 20;    // smallest per-GPU step volume
 constexpr uint64_t kDynSyncMin = 128u << 20;
 constexpr int64_t kDynSyncMoves = 32;
 constexpr uint64_t kDynSyncMinUneven = 16u << 20;
+constexpr uint64_t kWringMinPiece = 16u << 10;  // warp rings: smallest queue piece (4 / 8 KiB: slower)
 constexpr uint64_t kWringMinVol = 48u << 20;   // warp-ring mode: smallest busiest-GPU volume (96 MiB
                                                // before the constant-shift stores; measured since, cfg4:
                                                // mean 1 MiB (58 MiB) 25.9 / 29.5 -> 25.2 / 28.3 us with
