@@ -248,7 +248,7 @@ def test_cfg4_alltoallv_mean_4MiB(elem, packed, monkeypatch):
             c.alltoallv(d_send, sc, sd, d_recv, rc, rd, algo="pairwise", dtype_size=elem)
             path = c.last_launch_path()
             assert np.array_equal(host(d_recv), want), (seed, G, wring)
-            if G == 0:
+            if G == 0 and os.environ.get("MPXA_NO_DYN", "0") == "0":   # (path knobs off)
                 assert "dyn" in path and (("wring" in path) == wring), path
             c.finalize()
 
@@ -687,7 +687,8 @@ def test_direct_protocol_small_sizes(G, monkeypatch):
     c.finalize()
 
 
-@pytest.mark.skipif(os.environ.get("MPXA_NO_LL", "0") != "0", reason="asserts the eager path")
+@pytest.mark.skipif(any(os.environ.get(k, "0") != "0" for k in ("MPXA_NO_LL", "MPXA_NO_DYN", "MPXA_NO_TINY")),
+                    reason="asserts the default execution paths")
 def test_execution_paths_are_the_intended_ones(monkeypatch):
     """The launches these parity tests rely on take the paths they are meant to exercise
     (mpxa__last_launch): eager on emulated GPUs for small messages, direct otherwise; the
