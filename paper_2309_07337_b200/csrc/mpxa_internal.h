@@ -188,7 +188,7 @@ struct ExecParams {
                                // stages / chunk then describe the whole dynamic smem
     int32_t small_a8;          // small kernel: every local offset, length, base and stride is an
                                // 8-B multiple (not all 16): pieces move as 8-byte words
-    int32_t wslack;            // warp-ring mode: stages kept out of the load window (1 or 2)
+    int32_t wslack;            // warp-ring mode: stages kept out of the load window (1..kWStages-1; 3)
     int32_t small_a4;          // tiny kernel: every offset, length, base and stride a 4-B multiple
                                // (not all 8): pieces move as 4-byte words, no funnel shifts
     int32_t tiny_step_items;   // tiny multi-step kernel: 16-B pieces of the busiest step (launch

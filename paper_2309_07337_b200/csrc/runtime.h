@@ -210,7 +210,10 @@ struct mpxa_comm_s {
                                               // MPXA_NO_WRING=1: never (LSU-register path), MPXA_WRING=2: always
     int dyn_pieces = (int)kDynPiecesPerCta;   // MPXA_DYN_PIECES: queue pieces per CTA (tuning)
     int prefetch = 1;                         // MPXA_NO_PREFETCH=1: no pre-wait L2 prefetch (dynamic mode)
-    int wslack = 2;                           // MPXA_WSLACK: warp-ring stages kept out of the load window
+    int wslack = 3;                           // MPXA_WSLACK: warp-ring stages kept out of the load window
+                                              // (measured, cfg4 p = 8 int64 / int32, means 1-8 MiB, seeds 0-1:
+                                              // 3 loads in flight at or below 4 (wslack 2) in all 16 cases, 0.1-1 us;
+                                              // 2 loads slower from 2 MiB, 1 load +25 %: profiles/r02/cfg4_wslack_s18.txt)
     bool tiny = true;                         // MPXA_NO_TINY=1: small one-GPU launches in the general kernel
     bool tiny_even = true;                    // MPXA_TINY_EVEN=0: tiny-kernel blocks sized like the general kernel's
     uint64_t dyn_min_total = kDynMinTotal;    // MPXA_DYN_MIN: smallest busiest-GPU volume (tuning)
