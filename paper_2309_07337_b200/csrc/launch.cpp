@@ -692,6 +692,14 @@ int run_program(mpxa_comm_t c, const DevProg &dp, const char *send, char *recv, 
                 // us, seed 1 162.3 -> 156.9; 2 / 4 MiB unchanged; 4 / 8 KiB pieces much slower)
                 uint64_t U = src_vol / ((uint64_t)nC * (uint64_t)c->dyn_pieces);
                 U = std::max<uint64_t>(kWringMinPiece, std::min<uint64_t>(U, kDynMaxPiece));
+                // larger piece floors from 192 / 256 MiB per GPU: 20 / 24 KiB instead of the 16 /
+                // 17 KiB shares of cfg4 means 4 / 5 MiB (the mean-4 MiB matrices total 250-256 MiB,
+                // so they take the 20 KiB floor) -- measured, int64 seeds 0 / 1: 86.7 / 83.5 -> 85.4
+                // / 82.0 us at 4 MiB, 100.7 / 100.6 -> 99.7 / 99.2 at 5 MiB; int32 the same; 3 / 6
+                // MiB neutral, 8 MiB shares 28 KiB (profiles/r02/cfg4_pieces_s19.txt; the s21 build
+                // with the 24 KiB floor alone left mean 4 MiB at 16 KiB pieces: 85.8 us in bench)
+                if (src_vol >= kWringFloorVol24) U = std::max<uint64_t>(U, 24u << 10);
+                else if (src_vol >= kWringFloorVol20) U = std::max<uint64_t>(U, 20u << 10);
                 if (ntiles >= 4) U = std::max<uint64_t>(U, 3 * (uint64_t)kTmaMid.chunk);   // (as above)
                 E.dyn_u = (int32_t)((U + kWChunk / 2) / kWChunk * kWChunk);
             }

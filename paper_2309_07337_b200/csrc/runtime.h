@@ -105,6 +105,8 @@ constexpr uint64_t kDynSyncMin = 128u << 20;
 constexpr int64_t kDynSyncMoves = 32;
 constexpr uint64_t kDynSyncMinUneven = 16u << 20;
 constexpr uint64_t kWringMinPiece = 16u << 10;  // warp rings: smallest queue piece (4 / 8 KiB: slower)
+constexpr uint64_t kWringFloorVol20 = 192ull << 20, kWringFloorVol24 = 256ull << 20;   // warp rings: larger
+                                                 // piece floors (20 / 24 KiB) from these busiest-GPU volumes
 constexpr uint64_t kWringMinVol = 48u << 20;   // warp-ring mode: smallest busiest-GPU volume (96 MiB
                                                // before the constant-shift stores; measured since, cfg4:
                                                // mean 1 MiB (58 MiB) 25.9 / 29.5 -> 25.2 / 28.3 us with
